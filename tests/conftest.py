@@ -1,0 +1,27 @@
+"""Shared pytest setup.
+
+``-m gpu`` tests need a B200 and the built libpsd.so; ``-m "not gpu"`` tests
+run anywhere (oracle vs golden vectors, scheduler parity, host logic, C-ABI
+symbol checks, gloo multi-process tests).
+"""
+
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+
+
+@pytest.fixture(scope="session")
+def cuda_device():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.device("cuda:0")
