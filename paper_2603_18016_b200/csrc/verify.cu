@@ -1,0 +1,511 @@
+// verify.cu -- K1: fused speculative verification on sm_100a.
+//
+// Replaces the reference's coin-flip acceptance (pkg/src/specsim/
+// acceptance_model.py:82-97, called from engine.py:245-256) with the real
+// token-level rule over target / draft logits.  Bit-exact with the CPU oracle
+// (oracle/verify_oracle.c) because both evaluate include/psd_canon.h in the
+// canonical order documented there.
+//
+// Two kernels, HBM-bound by design:
+//   verify_stats<SAMPLE>  grid (slice, request*row): every active (row, slice)
+//       streams 8192 fp32 logits once with 128-bit L1-bypassing loads and
+//       produces (max, sum-exp) [sampling] or (max, argmax) [greedy] partials;
+//       the last CTA of each request (atomic ticket) folds the slices, runs the
+//       accept test of all k drafts at once (one lane per draft, __ballot_sync
+//       finds the first rejection) and writes the accepted prefix.  Greedy is
+//       done after this kernel.
+//   verify_sample         grid (1024-block, request): block sums of the
+//       residual max(0, p - q) (or p for the bonus), the last CTA per request
+//       does the normalised prefix search and writes the final token.
+// Algorithmic bytes: greedy 4V*sum(k_b+1); sampling
+// 4V*sum(2k_b+1) (+ small terms).  The sampling pass re-reads one (t, d) row
+// pair per request (mostly from L2).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/psd.h"
+#include "../../include/psd_canon.h"
+
+namespace {
+
+constexpr int kThreads = 256;
+
+struct Plan {
+  int mode;     // 1 = residual at row `row`, 2 = bonus from p at row `row`
+  int row;      // position index a
+  float Mt, St, Md, Sd;
+  int pad[2];
+};
+
+struct Params {
+  const float* t; int64_t tsb, tsi; int V;
+  const float* d; int64_t dsb, dsi; int Vd;
+  const int32_t* ids; const int32_t* len; const float* u;
+  float inv_temp; int B, K;
+  int32_t* acc; int32_t* out;
+  int* cnt_a; int* cnt_b;
+  float2* part; Plan* plan; float* wblk;
+  int NS, NB, R;
+};
+
+__device__ __forceinline__ float4 ld_stream(const float* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ psd_ms shfl_ms(psd_ms v, int off) {
+  psd_ms o;
+  o.m = __shfl_down_sync(0xffffffffu, v.m, off);
+  o.s = __shfl_down_sync(0xffffffffu, v.s, off);
+  return o;
+}
+
+__device__ __forceinline__ psd_vi shfl_vi(psd_vi v, int off) {
+  psd_vi o;
+  o.v = __shfl_down_sync(0xffffffffu, v.v, off);
+  o.i = __shfl_down_sync(0xffffffffu, v.i, off);
+  return o;
+}
+
+__device__ __forceinline__ float shfl_add_tree(float v) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) v = psd_add(v, __shfl_down_sync(0xffffffffu, v, off));
+  return v;
+}
+
+// number of stats CTAs request b launches work in
+__device__ __forceinline__ int expected_stats(const Params& p, int kb, bool sample) {
+  const int nst = (p.V + PSD_SLICE - 1) / PSD_SLICE;
+  const int nsd = (p.Vd + PSD_SLICE - 1) / PSD_SLICE;
+  return nst * (kb + 1) + (sample ? nsd * kb : 0);
+}
+
+template <bool SAMPLE>
+__global__ void __launch_bounds__(kThreads)
+verify_stats(const Params p) {
+  const int slice = blockIdx.x;
+  const int b = blockIdx.y / p.R;
+  const int r = blockIdx.y % p.R;
+  const int kb = p.len[b];
+  const bool is_draft = r > p.K;
+  const int i = is_draft ? r - (p.K + 1) : r;
+  const int n = is_draft ? p.Vd : p.V;
+  const bool active = (is_draft ? i < kb : i <= kb) && slice * PSD_SLICE < n;
+  if (!active) return;
+  const float* row = is_draft ? p.d + b * p.dsb + i * p.dsi : p.t + b * p.tsb + i * p.tsi;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int base = slice * PSD_SLICE;
+
+  float4 v[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int e = base + 4 * (tid + kThreads * j);
+    v[j] = e < n ? ld_stream(row + e) : make_float4(PSD_NEG_INF, PSD_NEG_INF, PSD_NEG_INF,
+                                                    PSD_NEG_INF);
+  }
+
+  __shared__ float2 red[kThreads / 32];
+  __shared__ int s_last;
+  if constexpr (SAMPLE) {
+    float m = PSD_NEG_INF;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      v[j].x = psd_mul(v[j].x, p.inv_temp); v[j].y = psd_mul(v[j].y, p.inv_temp);
+      v[j].z = psd_mul(v[j].z, p.inv_temp); v[j].w = psd_mul(v[j].w, p.inv_temp);
+      m = psd_max(m, psd_max(psd_max(v[j].x, v[j].y), psd_max(v[j].z, v[j].w)));
+    }
+    float s = 0.0f;
+    if (m != PSD_NEG_INF) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        // invalid elements are -inf -> E() == 0, adding 0.0f is exact
+        s = psd_add(s, psd_exp(psd_sub(v[j].x, m)));
+        s = psd_add(s, psd_exp(psd_sub(v[j].y, m)));
+        s = psd_add(s, psd_exp(psd_sub(v[j].z, m)));
+        s = psd_add(s, psd_exp(psd_sub(v[j].w, m)));
+      }
+    }
+    psd_ms acc = {m, s};
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) acc = psd_combine(acc, shfl_ms(acc, off));
+    if (lane == 0) red[warp] = make_float2(acc.m, acc.s);
+    __syncthreads();
+    if (tid == 0) {
+      psd_ms w[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) { w[q].m = red[q].x; w[q].s = red[q].y; }
+#pragma unroll
+      for (int off = 4; off >= 1; off >>= 1)
+#pragma unroll
+        for (int q = 0; q < off; ++q) w[q] = psd_combine(w[q], w[q + off]);
+      p.part[(b * p.R + r) * p.NS + slice] = make_float2(w[0].m, w[0].s);
+    }
+  } else {
+    psd_vi best = {PSD_NEG_INF, 0x7fffffff};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int e = base + 4 * (tid + kThreads * j);
+      best = psd_argmax2(best, psd_vi{v[j].x, e});
+      best = psd_argmax2(best, psd_vi{v[j].y, e + 1});
+      best = psd_argmax2(best, psd_vi{v[j].z, e + 2});
+      best = psd_argmax2(best, psd_vi{v[j].w, e + 3});
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) best = psd_argmax2(best, shfl_vi(best, off));
+    if (lane == 0) red[warp] = make_float2(best.v, __int_as_float(best.i));
+    __syncthreads();
+    if (tid == 0) {
+      psd_vi w = {red[0].x, __float_as_int(red[0].y)};
+#pragma unroll
+      for (int q = 1; q < 8; ++q) w = psd_argmax2(w, psd_vi{red[q].x, __float_as_int(red[q].y)});
+      p.part[(b * p.R + r) * p.NS + slice] = make_float2(w.v, __int_as_float(w.i));
+    }
+  }
+
+  // ---- last CTA of request b: fold slices, decide --------------------------
+  if (tid == 0) {
+    __threadfence();
+    const int ticket = atomicAdd(p.cnt_a + b, 1);
+    s_last = ticket == expected_stats(p, kb, SAMPLE) - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+
+  __shared__ float sMt[PSD_MAX_K + 1], sSt[PSD_MAX_K + 1], sMd[PSD_MAX_K], sSd[PSD_MAX_K];
+  __shared__ int sG[PSD_MAX_K + 1];
+  const int nst = (p.V + PSD_SLICE - 1) / PSD_SLICE;
+  const int nsd = (p.Vd + PSD_SLICE - 1) / PSD_SLICE;
+  const int nrows = SAMPLE ? 2 * kb + 1 : kb + 1;
+  if (tid < nrows) {
+    const bool dr = tid > kb;
+    const int ri = dr ? tid - (kb + 1) : tid;
+    const int rr = dr ? p.K + 1 + ri : ri;
+    const float2* pp = p.part + (b * p.R + rr) * p.NS;
+    const int ns = dr ? nsd : nst;
+    if constexpr (SAMPLE) {
+      float2 f = __ldcg(pp);
+      psd_ms a = {f.x, f.y};
+      for (int s = 1; s < ns; ++s) {
+        f = __ldcg(pp + s);
+        a = psd_combine(a, psd_ms{f.x, f.y});
+      }
+      if (dr) { sMd[ri] = a.m; sSd[ri] = a.s; } else { sMt[ri] = a.m; sSt[ri] = a.s; }
+    } else {
+      float2 f = __ldcg(pp);
+      psd_vi a = {f.x, __float_as_int(f.y)};
+      for (int s = 1; s < ns; ++s) {
+        f = __ldcg(pp + s);
+        a = psd_argmax2(a, psd_vi{f.x, __float_as_int(f.y)});
+      }
+      sG[ri] = a.i;
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    // lane i tests draft i; first rejection = first zero bit of the ballot
+    bool ok = false;
+    const int x = lane < kb ? p.ids[b * p.K + lane] : -1;
+    if (lane < kb) {
+      if constexpr (SAMPLE) {
+        if (x >= 0 && x < p.V) {
+          const float* tr = p.t + b * p.tsb + lane * p.tsi;
+          const float* drw = p.d + b * p.dsb + lane * p.dsi;
+          const float et = psd_exp(psd_sub(psd_mul(__ldg(tr + x), p.inv_temp), sMt[lane]));
+          const float ed = x < p.Vd
+                               ? psd_exp(psd_sub(psd_mul(__ldg(drw + x), p.inv_temp), sMd[lane]))
+                               : 0.0f;
+          ok = psd_accept(p.u[b * (p.K + 1) + lane], et, ed, sSt[lane], sSd[lane]);
+        }
+      } else {
+        ok = x == sG[lane];
+      }
+    }
+    const unsigned rej = __ballot_sync(0xffffffffu, !ok);
+    const unsigned rej_in = rej & ((kb >= 32) ? 0xffffffffu : ((1u << kb) - 1u));
+    const int a = rej_in ? __ffs(rej_in) - 1 : kb;
+    int32_t* o = p.out + b * (p.K + 1);
+    if (lane <= p.K) o[lane] = lane < a ? x : -1;
+    if (lane == 0) {
+      p.acc[b] = a;
+      if constexpr (SAMPLE) {
+        Plan pl;
+        pl.row = a;
+        pl.Mt = sMt[a]; pl.St = sSt[a];
+        pl.mode = a < kb ? 1 : 2;
+        pl.Md = a < kb ? sMd[a] : 0.0f;
+        pl.Sd = a < kb ? sSd[a] : 0.0f;
+        pl.pad[0] = pl.pad[1] = 0;
+        p.plan[b] = pl;
+      }
+      p.cnt_a[b] = 0;  // self-cleaning ticket for the next launch
+    }
+    __syncwarp();
+    if constexpr (!SAMPLE) {
+      if (lane == 0) o[a] = sG[a];
+    }
+  }
+}
+
+// ---- sampling pass ---------------------------------------------------------
+struct WeightCtx {
+  const float* t; const float* d; int V, Vd; float inv_temp, Mt, St, Md, Sd; int residual;
+};
+
+__device__ __forceinline__ float weight_of(const WeightCtx& w, float tv, float dv, int x) {
+  if (x >= w.V) return 0.0f;
+  const float et = psd_exp(psd_sub(psd_mul(tv, w.inv_temp), w.Mt));
+  if (!w.residual) return et;
+  const float ed = x < w.Vd ? psd_exp(psd_sub(psd_mul(dv, w.inv_temp), w.Md)) : 0.0f;
+  return psd_residual(et, ed, w.St, w.Sd);
+}
+
+// weights of the 4 elements lane `tid` owns in block `blk`
+__device__ __forceinline__ void lane_weights(const WeightCtx& w, int blk, int tid, float out[4]) {
+  const int x0 = blk * PSD_SBLK + 4 * tid;
+  float4 tv = make_float4(0.f, 0.f, 0.f, 0.f), dv = tv;
+  if (x0 < w.V) tv = __ldg(reinterpret_cast<const float4*>(w.t + x0));
+  if (w.residual && x0 < w.Vd) dv = __ldg(reinterpret_cast<const float4*>(w.d + x0));
+  out[0] = weight_of(w, tv.x, dv.x, x0);
+  out[1] = weight_of(w, tv.y, dv.y, x0 + 1);
+  out[2] = weight_of(w, tv.z, dv.z, x0 + 2);
+  out[3] = weight_of(w, tv.w, dv.w, x0 + 3);
+}
+
+__device__ float block_weight_sum(const WeightCtx& w, int blk, float* s_lane, float* s_red) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float wv[4];
+  lane_weights(w, blk, tid, wv);
+  const float ls = psd_add(psd_add(psd_add(wv[0], wv[1]), wv[2]), wv[3]);
+  if (s_lane) s_lane[tid] = ls;
+  const float ws = shfl_add_tree(ls);
+  if (lane == 0) s_red[warp] = ws;
+  __syncthreads();
+  float tot = 0.0f;
+  if (tid == 0) {
+    float q[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) q[k] = s_red[k];
+#pragma unroll
+    for (int off = 4; off >= 1; off >>= 1)
+#pragma unroll
+      for (int k = 0; k < off; ++k) q[k] = psd_add(q[k], q[k + off]);
+    tot = q[0];
+  }
+  __syncthreads();
+  return tot;  // valid in thread 0
+}
+
+// last element with positive weight in block blk (all threads return it)
+__device__ int last_positive(const WeightCtx& w, int blk, int* s_int) {
+  float wv[4];
+  lane_weights(w, blk, threadIdx.x, wv);
+  int best = -1;
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    if (wv[c] > 0.0f) best = blk * PSD_SBLK + 4 * threadIdx.x + c;
+  if (threadIdx.x == 0) *s_int = -1;
+  __syncthreads();
+  if (best >= 0) atomicMax(s_int, best);
+  __syncthreads();
+  const int r = *s_int;
+  __syncthreads();
+  return r < 0 ? blk * PSD_SBLK : r;
+}
+
+__global__ void __launch_bounds__(kThreads)
+verify_sample(const Params p) {
+  const int blk = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+  const Plan pl = p.plan[b];
+  WeightCtx w;
+  w.V = p.V; w.Vd = p.Vd; w.inv_temp = p.inv_temp;
+  w.t = p.t + b * p.tsb + pl.row * p.tsi;
+  w.d = p.d + b * p.dsb + pl.row * p.dsi;
+  w.Mt = pl.Mt; w.St = pl.St; w.Md = pl.Md; w.Sd = pl.Sd;
+  w.residual = pl.mode == 1;
+
+  __shared__ float s_red[8];
+  __shared__ float s_lane[kThreads];
+  __shared__ int s_last, s_int;
+  __shared__ float s_T, s_Pprev;
+  __shared__ int s_chosen;
+
+  const float W = block_weight_sum(w, blk, nullptr, s_red);
+  if (tid == 0) {
+    p.wblk[b * p.NB + blk] = W;
+    __threadfence();
+    s_last = atomicAdd(p.cnt_b + b, 1) == p.NB - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  float* wb = p.wblk + b * p.NB;
+
+  // degenerate residual (sums to 0 in fp32): fall back to sampling from p
+  if (tid == 0) {
+    float R = 0.0f;
+    for (int k = 0; k < p.NB; ++k) R = psd_add(R, __ldcg(wb + k));
+    s_int = (w.residual && !(R > 0.0f)) ? 1 : 0;
+  }
+  __syncthreads();
+  if (s_int) {
+    w.residual = 0;
+    __syncthreads();
+    for (int k = 0; k < p.NB; ++k) {
+      const float Wk = block_weight_sum(w, k, nullptr, s_red);
+      if (tid == 0) wb[k] = Wk;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    float R = 0.0f;
+    for (int k = 0; k < p.NB; ++k) R = psd_add(R, __ldcg(wb + k));
+    const float T = psd_mul(p.u[b * (p.K + 1) + p.K], R);
+    float P = 0.0f;
+    int chosen = -1;
+    float Pprev = 0.0f;
+    for (int k = 0; k < p.NB; ++k) {
+      const float Pn = psd_add(P, __ldcg(wb + k));
+      if (Pn > T) { chosen = k; Pprev = P; break; }
+      P = Pn;
+    }
+    if (chosen < 0) {
+      chosen = -2 - (p.NB - 1);
+      for (int k = p.NB - 1; k >= 0; --k)
+        if (__ldcg(wb + k) > 0.0f) { chosen = -2 - k; break; }
+    }
+    s_chosen = chosen; s_T = T; s_Pprev = Pprev;
+  }
+  __syncthreads();
+  int tok;
+  if (s_chosen <= -2) {
+    tok = last_positive(w, -2 - s_chosen, &s_int);
+  } else {
+    const int cb = s_chosen;
+    float wv[4];
+    lane_weights(w, cb, tid, wv);
+    s_lane[tid] = psd_add(psd_add(psd_add(wv[0], wv[1]), wv[2]), wv[3]);
+    __syncthreads();
+    if (tid == 0) {  // exclusive sequential prefix of lane sums, in place
+      float C = 0.0f;
+      for (int l = 0; l < kThreads; ++l) { const float s = s_lane[l]; s_lane[l] = C; C = psd_add(C, s); }
+      s_int = 0x7fffffff;
+    }
+    __syncthreads();
+    float acc = s_lane[tid];
+    int hit = 0x7fffffff;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      acc = psd_add(acc, wv[c]);
+      if (hit == 0x7fffffff && psd_add(s_Pprev, acc) > s_T) hit = cb * PSD_SBLK + 4 * tid + c;
+    }
+    if (hit != 0x7fffffff) atomicMin(&s_int, hit);
+    __syncthreads();
+    tok = s_int;
+    __syncthreads();
+    if (tok == 0x7fffffff) tok = last_positive(w, cb, &s_int);
+  }
+  if (tid == 0) {
+    p.out[b * (p.K + 1) + pl.row] = tok;
+    p.cnt_b[b] = 0;
+  }
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct WsLayout {
+  size_t cnt_a, cnt_b, part, plan, wblk, total;
+};
+
+WsLayout layout(int B, int K, int V, int Vd, int sampling) {
+  const int nmax = V > Vd ? V : Vd;
+  const int NS = (nmax + PSD_SLICE - 1) / PSD_SLICE;
+  const int NB = (V + PSD_SBLK - 1) / PSD_SBLK;
+  const int R = (K + 1) + (sampling ? K : 0);
+  WsLayout L;
+  size_t off = 0;
+  L.cnt_a = off; off = align_up(off + sizeof(int) * B);
+  L.cnt_b = off; off = align_up(off + sizeof(int) * B);
+  L.part = off; off = align_up(off + sizeof(float2) * (size_t)B * R * NS);
+  L.plan = off; off = align_up(off + sizeof(Plan) * (size_t)B);
+  L.wblk = off; off = align_up(off + sizeof(float) * (size_t)B * NB);
+  L.total = off;
+  return L;
+}
+
+int check_common(const float* t, int64_t tsb, int64_t tsi, int V, int B, int K,
+                 const void* ws, size_t ws_bytes, size_t need) {
+  if (!t || V <= 0 || B <= 0 || K < 0 || K > PSD_MAX_K) return (int)cudaErrorInvalidValue;
+  if ((V & 3) || (tsb & 3) || (tsi & 3) || (reinterpret_cast<uintptr_t>(t) & 15))
+    return (int)cudaErrorMisalignedAddress;
+  if (!ws || ws_bytes < need) return (int)cudaErrorInvalidValue;
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t psd_verify_workspace_bytes(int B, int K, int V, int Vd, int sampling) {
+  return layout(B, K, V, sampling ? Vd : 0, sampling).total;
+}
+
+int psd_verify_workspace_init(void* ws, size_t ws_bytes, void* stream) {
+  return (int)cudaMemsetAsync(ws, 0, ws_bytes, (cudaStream_t)stream);
+}
+
+int psd_verify_greedy(const float* target_logits, int64_t t_stride_b, int64_t t_stride_i, int V,
+                      const int32_t* draft_ids, const int32_t* draft_len, int B, int K,
+                      int32_t* accepted_len, int32_t* out_tokens, void* ws, size_t ws_bytes,
+                      void* stream) {
+  const WsLayout L = layout(B, K, V, 0, 0);
+  int rc = check_common(target_logits, t_stride_b, t_stride_i, V, B, K, ws, ws_bytes, L.total);
+  if (rc) return rc;
+  Params p{};
+  char* w = static_cast<char*>(ws);
+  p.t = target_logits; p.tsb = t_stride_b; p.tsi = t_stride_i; p.V = V;
+  p.d = nullptr; p.Vd = 0; p.ids = draft_ids; p.len = draft_len; p.u = nullptr;
+  p.inv_temp = 1.0f; p.B = B; p.K = K; p.acc = accepted_len; p.out = out_tokens;
+  p.cnt_a = reinterpret_cast<int*>(w + L.cnt_a); p.cnt_b = reinterpret_cast<int*>(w + L.cnt_b);
+  p.part = reinterpret_cast<float2*>(w + L.part); p.plan = reinterpret_cast<Plan*>(w + L.plan);
+  p.wblk = reinterpret_cast<float*>(w + L.wblk);
+  p.NS = (V + PSD_SLICE - 1) / PSD_SLICE; p.NB = (V + PSD_SBLK - 1) / PSD_SBLK; p.R = K + 1;
+  dim3 grid(p.NS, B * p.R);
+  verify_stats<false><<<grid, kThreads, 0, (cudaStream_t)stream>>>(p);
+  return (int)cudaGetLastError();
+}
+
+int psd_verify_sample(const float* target_logits, int64_t t_stride_b, int64_t t_stride_i, int V,
+                      const float* draft_logits, int64_t d_stride_b, int64_t d_stride_i, int Vd,
+                      const int32_t* draft_ids, const int32_t* draft_len, const float* uniforms,
+                      float temperature, int B, int K, int32_t* accepted_len,
+                      int32_t* out_tokens, void* ws, size_t ws_bytes, void* stream) {
+  const WsLayout L = layout(B, K, V, Vd, 1);
+  int rc = check_common(target_logits, t_stride_b, t_stride_i, V, B, K, ws, ws_bytes, L.total);
+  if (rc) return rc;
+  if (!draft_logits || Vd <= 0 || Vd > V || !uniforms || !(temperature > 0.0f))
+    return (int)cudaErrorInvalidValue;
+  if ((Vd & 3) || (d_stride_b & 3) || (d_stride_i & 3) ||
+      (reinterpret_cast<uintptr_t>(draft_logits) & 15))
+    return (int)cudaErrorMisalignedAddress;
+  Params p{};
+  char* w = static_cast<char*>(ws);
+  p.t = target_logits; p.tsb = t_stride_b; p.tsi = t_stride_i; p.V = V;
+  p.d = draft_logits; p.dsb = d_stride_b; p.dsi = d_stride_i; p.Vd = Vd;
+  p.ids = draft_ids; p.len = draft_len; p.u = uniforms;
+  p.inv_temp = 1.0f / temperature; p.B = B; p.K = K; p.acc = accepted_len; p.out = out_tokens;
+  p.cnt_a = reinterpret_cast<int*>(w + L.cnt_a); p.cnt_b = reinterpret_cast<int*>(w + L.cnt_b);
+  p.part = reinterpret_cast<float2*>(w + L.part); p.plan = reinterpret_cast<Plan*>(w + L.plan);
+  p.wblk = reinterpret_cast<float*>(w + L.wblk);
+  p.NS = (V + PSD_SLICE - 1) / PSD_SLICE; p.NB = (V + PSD_SBLK - 1) / PSD_SBLK;
+  p.R = 2 * K + 1;
+  dim3 grid(p.NS, B * p.R);
+  verify_stats<true><<<grid, kThreads, 0, (cudaStream_t)stream>>>(p);
+  dim3 grid2(p.NB, B);
+  verify_sample<<<grid2, kThreads, 0, (cudaStream_t)stream>>>(p);
+  return (int)cudaGetLastError();
+}
+
+}  // extern "C"

@@ -1,0 +1,68 @@
+"""ctypes binding of libpsd.so -- the C ABI declared in include/psd.h.
+
+The product path has no CPU fallback: if the library is missing, every entry
+point raises ``NativeError`` (on a GPU host this is loud by design).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+from .errors import NativeError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpsd.so")
+HEADER = os.path.join(_HERE, "..", "include", "psd.h")
+
+_c = ctypes
+_p = _c.c_void_p
+_i = _c.c_int
+_i64 = _c.c_int64
+_sz = _c.c_size_t
+_f = _c.c_float
+
+# name -> (restype, argtypes); must match include/psd.h exactly
+SIGNATURES: dict[str, tuple] = {
+    "psd_verify_workspace_bytes": (_sz, [_i, _i, _i, _i, _i]),
+    "psd_verify_workspace_init": (_i, [_p, _sz, _p]),
+    "psd_verify_greedy": (_i, [_p, _i64, _i64, _i, _p, _p, _i, _i, _p, _p, _p, _sz, _p]),
+    "psd_verify_sample": (_i, [_p, _i64, _i64, _i, _p, _i64, _i64, _i, _p, _p, _p, _f, _i, _i,
+                               _p, _p, _p, _sz, _p]),
+}
+
+_lib = None
+
+
+def header_symbols() -> list[str]:
+    """Every function declared in include/psd.h."""
+    with open(HEADER) as fh:
+        text = fh.read()
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|void|float)\s+\**(psd_\w+)\s*\(", text,
+                                 re.M)))
+
+
+def load():
+    """Load libpsd.so once and attach the signatures."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NativeError(f"{LIB_PATH} is missing: run `python -m "
+                          "paper_2603_18016_b200.build_native` (there is no CPU fallback)")
+    try:
+        lib = ctypes.CDLL(LIB_PATH)
+    except OSError as exc:
+        raise NativeError(f"cannot load {LIB_PATH}: {exc}") from exc
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        raise NativeError(f"{what} failed: cudaError {rc}")
