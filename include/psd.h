@@ -30,6 +30,8 @@ extern "C" {
 #endif
 
 #define PSD_MAX_K 16 /* largest draft depth a verification row may carry */
+#define PSD_MAX_SLICES 32 /* vocab <= 32 * 8192 = 262144 */
+#define PSD_MAX_SBLKS 256 /* vocab / 1024 */
 
 /* ---- K1: fused speculative verification --------------------------------
  * Layouts (elements, fp32 logits):
@@ -56,6 +58,72 @@ int psd_verify_sample(const float* target_logits, int64_t t_stride_b, int64_t t_
                       const float* uniforms, float temperature, int B, int K,
                       int32_t* accepted_len, int32_t* out_tokens, void* workspace,
                       size_t workspace_bytes, void* stream);
+
+/* ---- K2: bf16 GEMM on tcgen05 (TMEM accumulators, TMA, mbarrier ring) -----
+ *   Y[m, n] = epi( sum_k X[m*ldx + k] * W[n*ldw + k] )   X [M,K], W [N,K] bf16
+ * Replaces the virtual pass durations verify_latency / draft_latency
+ * .duration(...) (pkg/src/specsim/engine.py:338, 359-360, 378, 402, 429;
+ * request_model.py:112-117) with the real contractions of the forwards.
+ * epi: PSD_EPI_BF16 (Y bf16), PSD_EPI_F32 (Y fp32), PSD_EPI_RESID (Y bf16 =
+ * acc + R, Y may alias R), PSD_EPI_SILU (W rows packed per 128-row tile as 64
+ * gate rows then the 64 matching up rows; Y [M, N/2] bf16 = silu(g) * u).
+ * N must be a multiple of 128, K and the leading dims multiples of 8.
+ * splits_hint 0 = automatic split-K (fp32 partials in `workspace`, sized by
+ * psd_gemm_plan; with too little workspace fewer splits are used). */
+#define PSD_EPI_BF16 0
+#define PSD_EPI_F32 1
+#define PSD_EPI_RESID 2
+#define PSD_EPI_SILU 3
+#define PSD_EPI_PARTIAL 4 /* internal: split-K partials */
+int psd_gemm_plan(int M, int N, int K, int epi, int splits_hint, int* splits_out,
+                  size_t* workspace_bytes);
+int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, int N, void* Y,
+                  int ldy, int epi, const void* R, int ldr, int splits_hint, void* workspace,
+                  size_t workspace_bytes, void* stream);
+
+/* ---- K3/K3'/K4: forward-pass building blocks (bf16 storage, fp32 math) ----
+ * Same seam as K2 (the virtual pass durations).  Row-major activations. */
+int psd_embed(const int32_t* tokens, int M, const void* table, int H, void* out, void* stream);
+/* y[m] = x[rows ? rows[m] : m] * rsqrt(mean(x^2) + eps) * w */
+int psd_rmsnorm(const void* x, int ldx, const int32_t* rows, const void* w, void* y, int ldy,
+                int M, int H, float eps, void* stream);
+/* qkv [M, (Hq+2Hkv) D] (+ optional bias) -> rotate-half RoPE on q, k;
+ * q -> q_out [M, Hq, D]; k, v -> caches [blocks*block_size, Hkv, D] at slot
+ * slots[m] (negative: not written). */
+int psd_rope_kv(const void* qkv, int M, int Hq, int Hkv, int D, const int32_t* positions,
+                const int32_t* slots, const float* inv_freq, const void* qkv_bias, void* q_out,
+                void* k_cache, void* v_cache, void* stream);
+/* Paged multi-query attention, GQA.  Sequence s: query tokens q_start[s] ..
+ * +q_len[s]-1 at positions q_pos0[s] + t; token t attends keys
+ * 0 .. min(q_pos0[s] + t, kv_len[s] - 1) read through
+ * block_table[seq_slot[s] * max_blocks + key / block_size]. */
+int psd_attention(const void* q, const void* k_cache, const void* v_cache,
+                  const int32_t* block_table, int max_blocks, const int32_t* seq_slot,
+                  const int32_t* q_start, const int32_t* q_len, const int32_t* q_pos0,
+                  const int32_t* kv_len, int num_seqs, int max_q_len, int Hq, int Hkv, int D,
+                  int block_size, float scale, void* out, void* stream);
+/* synthetic-language logit bias: logits[m, successor[prev_tokens[m]]] += beta */
+int psd_bigram_bias(float* logits, int64_t ld, const int32_t* prev_tokens, int M,
+                    const int32_t* successor, int V, float beta, void* stream);
+/* out[b*n + i] = Philox4x32-10((seed), counter (request_ids[b], verify_index[b], i, 0)) in [0,1) */
+int psd_philox_uniforms(uint64_t seed, const int32_t* request_ids, const int32_t* verify_index,
+                        int B, int n, float* out, void* stream);
+
+/* ---- K5 / glue: KV commit of accepted tokens, token routing ---------------
+ * psd_commit replaces the commit rule + KV write accounting of a verified row
+ * (pkg/src/specsim/engine.py:257-262; kv_manager.py:130-144): per row b
+ * (slot row_slot[b]), append out_tokens[b, 0..a_b] to outputs[slot], advance
+ * generated[slot] by a_b + 1 and the slot's last two tokens.  The rejected
+ * tail needs no device work: KV validity is positional, so rolling back is the
+ * host shrinking the sequence length / block list (KVBlockTable.trim_to_written). */
+int psd_commit(const int32_t* accepted_len, const int32_t* out_tokens, int K,
+               const int32_t* row_slot, int n, int32_t* generated, int32_t* slot_tokens,
+               int slot_tokens_ld, int32_t* outputs, int outputs_ld, void* stream);
+/* dst[dst_idx ? dst_idx[i] : i] = src[src_idx ? src_idx[i] : i], negative dst skipped */
+int psd_index_copy_i32(int32_t* dst, const int32_t* dst_idx, const int32_t* src,
+                       const int32_t* src_idx, int n, void* stream);
+/* deterministic random init: (u - 1/2) * span, u = splitmix64(seed, i) >> 40 / 2^24 */
+int psd_fill_uniform_bf16(void* out, size_t n, uint64_t seed, float span, void* stream);
 
 #ifdef __cplusplus
 }

@@ -10,16 +10,23 @@
  * -ffp-contract=off; device code uses the explicit __f*_rn intrinsics below,
  * which nvcc never fuses.
  *
+ * Probabilities.  With c = fl(fl(1/T) * log2 e) (psd_scale) and a reference
+ * maximum M of the raw logits, the unnormalised weight of logit x is
+ *     e(x; M) = E2(fma(x, c, -fl(M * c)))        (= exp((x - M) / T))
+ * where E2 is the canonical 2^t below.  p(x) = e(x; M_row) / S_row.
+ *
  * Reduction structure ("canonical order"):
- *   softmax statistics (max M, sum S = sum_x E(z_x - M)) of a row of n logits:
- *     - the row is cut into slices of PSD_SLICE = 8192 elements;
+ *   softmax statistics (row max M, S = sum_x e(x; M)) of a row of n logits:
+ *     - the row is cut into slices of PSD_SLICE = 8192 elements; slice max
+ *       M_s is exact;
  *     - inside a slice, lane l (0..255) owns the float4 vectors l + 256 j
- *       (j = 0..7); lane max m_l is exact; lane sum s_l = sequential sum over
- *       j, then x,y,z,w, of E(z - m_l);
- *     - lanes combine pairwise with psd_combine: first inside each warp of 32
- *       (offsets 16,8,4,2,1: v[l] = combine(v[l], v[l+off])), then the 8 warp
- *       results (offsets 4,2,1);
- *     - slices fold left to right: acc = combine(acc, slice[s]).
+ *       (j = 0..7); lane sum s_l = sequential sum over j, then x,y,z,w, of
+ *       e(x; M_s);
+ *     - slice sum: each warp of 32 lanes adds pairwise with offsets
+ *       16,8,4,2,1 (v[l] = v[l] + v[l+off]), then the 8 warp results with
+ *       offsets 4,2,1;
+ *     - slices fold left to right with psd_combine.
+ *   greedy: argmax over the row, ties -> lowest index (order free).
  *   sampling by prefix search over non-negative weights w_x:
  *     - the row is cut into blocks of PSD_SBLK = 1024 elements; lane l owns
  *       elements 4l..4l+3; lane sum = ((w0 + w1) + w2) + w3; block sum W_b is
@@ -33,8 +40,8 @@
  *       (or, with no block hit, of the last positive-weight block).
  * Acceptance (speculative sampling, Leviathan et al. / Chen et al.):
  *     accept draft x at position i  iff  (u_i * e_d(x)) * S_t < e_t(x) * S_d
- *     with e_t(x) = E(z_t(x) - M_t), e_d(x) = E(z_d(x) - M_d); this is
- *     u_i < p(x) / q(x) without a division.
+ *     with e_t(x) = e(x; M_t), e_d(x) = e(x; M_d) over the target / draft
+ *     rows; this is u_i < p(x) / q(x) without a division.
  * Residual weight: r(x) = max(0, e_t(x) * S_d - e_d(x) * S_t), proportional to
  *     max(0, p(x) - q(x)); e_d(x) = 0 beyond the draft vocabulary.
  */
@@ -77,13 +84,13 @@ PSD_HD float psd_max(float a, float b) { return a > b ? a : b; }
 
 #define PSD_NEG_INF (-__builtin_inff())
 
-/* E(x) = exp(x) for x <= 0, canonical: 2^n * P(f), t = x*log2(e), n = rint(t),
- * f = t - n in [-1/2, 1/2], P = degree-6 Taylor polynomial of 2^f (Horner,
- * fused multiply-adds).  E(0) == 1 exactly; E(x) = 0 for x < -87 (and -inf). */
-PSD_HD float psd_exp(float x) {
-  if (!(x >= -87.0f)) return 0.0f;           /* also catches NaN and -inf */
-  const float t = psd_mul(x, 1.44269504088896341f);
-  const float r = psd_add(t, 12582912.0f);   /* 1.5 * 2^23: round to nearest */
+/* E2(t) = 2^t for t <= ~0, canonical: t clamped to >= -125 (so results stay
+ * normal; -inf and NaN map to 2^-125), n = rint(t) by the 1.5*2^23 trick,
+ * f = t - n in [-1/2, 1/2], 2^f by a degree-6 Taylor polynomial (Horner with
+ * fused multiply-adds), exponent added as an integer.  E2(0) == 1 exactly. */
+PSD_HD float psd_exp2(float t) {
+  t = t > -125.0f ? t : -125.0f;
+  const float r = psd_add(t, 12582912.0f); /* 1.5 * 2^23 */
   const float n = psd_sub(r, 12582912.0f);
   const float f = psd_sub(t, n);
   float p = 1.54035304e-4f;
@@ -93,20 +100,27 @@ PSD_HD float psd_exp(float x) {
   p = psd_fma(p, f, 2.40226507e-1f);
   p = psd_fma(p, f, 6.93147181e-1f);
   p = psd_fma(p, f, 1.0f);
-  const int32_t ni = (int32_t)n;               /* exact: n is integral */
-  return psd_from_bits(psd_bits(p) + (uint32_t)(ni * (1 << 23)));
+  /* bits(r) = 0x4B400000 + n for |n| < 2^22: no float->int conversion */
+  return psd_from_bits(psd_bits(p) + ((psd_bits(r) - 0x4B400000u) << 23));
 }
 
-/* (m, s) pair: running max and sum of E(z - m). */
+/* c = fl(fl(1/T) * log2(e)) */
+PSD_HD float psd_scale(float inv_temp) { return psd_mul(inv_temp, 1.44269504088896341f); }
+/* exponent bias for reference max M: -fl(M * c) */
+PSD_HD float psd_bias(float M, float c) { return -psd_mul(M, c); }
+/* e(x; M) = E2(fma(x, c, bias)) */
+PSD_HD float psd_weight(float x, float c, float bias) { return psd_exp2(psd_fma(x, c, bias)); }
+
+/* (m, s) pair: max of the raw logits and sum of e(x; m). */
 typedef struct { float m; float s; } psd_ms;
 
-PSD_HD psd_ms psd_combine(psd_ms a, psd_ms b) {
+PSD_HD psd_ms psd_combine(psd_ms a, psd_ms b, float c) {
   if (a.m == PSD_NEG_INF) return b;
   if (b.m == PSD_NEG_INF) return a;
   psd_ms o;
   o.m = psd_max(a.m, b.m);
-  o.s = psd_add(psd_mul(a.s, psd_exp(psd_sub(a.m, o.m))),
-                psd_mul(b.s, psd_exp(psd_sub(b.m, o.m))));
+  const float bias = psd_bias(o.m, c);
+  o.s = psd_add(psd_mul(a.s, psd_weight(a.m, c, bias)), psd_mul(b.s, psd_weight(b.m, c, bias)));
   return o;
 }
 

@@ -30,8 +30,8 @@ def lib():
         if not os.path.exists(_LIB_PATH):
             build()
         L = ctypes.CDLL(_LIB_PATH)
-        L.oracle_exp.restype = ctypes.c_float
-        L.oracle_exp.argtypes = [ctypes.c_float]
+        L.oracle_exp2.restype = ctypes.c_float
+        L.oracle_exp2.argtypes = [ctypes.c_float]
         L.oracle_row_stats.restype = None
         L.oracle_row_stats.argtypes = [_f32p, ctypes.c_int, ctypes.c_float, _f32p, _f32p]
         L.oracle_row_argmax.restype = ctypes.c_int32
@@ -56,8 +56,8 @@ def _ip(a):
     return a.ctypes.data_as(_i32p)
 
 
-def exp(x: float) -> float:
-    return lib().oracle_exp(float(x))
+def exp2(x: float) -> float:
+    return lib().oracle_exp2(float(x))
 
 
 def row_stats(row: np.ndarray, temperature: float = 1.0) -> tuple[float, float]:

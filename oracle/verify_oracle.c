@@ -19,7 +19,7 @@
  * It is pinned instead (tests/test_verify_oracle.py) against an independent
  * float64 numpy evaluation of the same rule (decisions must agree wherever
  * the exact-math margin exceeds fp32 rounding) and against committed golden
- * vectors tests/golden/verify_golden.npz.
+ * vectors tests/golden/verify_golden.json.
  *
  * Arithmetic: every float op goes through include/psd_canon.h, evaluated in the
  * canonical order documented there, written here as plain sequential loops.
@@ -32,54 +32,47 @@
 #include "../include/psd_canon.h"
 
 /* ---- softmax statistics in canonical order ------------------------------ */
-static psd_ms slice_stats(const float* row, int begin, int n, float inv_temp) {
-  psd_ms lane[PSD_SLICE_LANES];
+static psd_ms slice_stats(const float* row, int begin, int n, float c) {
+  /* exact slice max */
+  float M = PSD_NEG_INF;
+  const int end = begin + PSD_SLICE < n ? begin + PSD_SLICE : n;
+  for (int e = begin; e < end; ++e) M = psd_max(M, row[e]);
+  const float bias = psd_bias(M, c);
+  float lane[PSD_SLICE_LANES];
   for (int l = 0; l < PSD_SLICE_LANES; ++l) {
-    float z[32];
-    int valid[32];
-    float m = PSD_NEG_INF;
-    for (int j = 0; j < 8; ++j) {
-      for (int c = 0; c < 4; ++c) {
-        const int e = begin + 4 * (l + PSD_SLICE_LANES * j) + c;
-        const int idx = 4 * j + c;
-        valid[idx] = e < n;
-        z[idx] = valid[idx] ? psd_mul(row[e], inv_temp) : PSD_NEG_INF;
-        if (valid[idx]) m = psd_max(m, z[idx]);
-      }
-    }
     float s = 0.0f;
-    if (m != PSD_NEG_INF)
-      for (int idx = 0; idx < 32; ++idx)
-        if (valid[idx]) s = psd_add(s, psd_exp(psd_sub(z[idx], m)));
-    lane[l].m = m;
-    lane[l].s = s;
+    for (int j = 0; j < 8; ++j)
+      for (int q = 0; q < 4; ++q) {
+        const int e = begin + 4 * (l + PSD_SLICE_LANES * j) + q;
+        if (e < n) s = psd_add(s, psd_weight(row[e], c, bias));
+      }
+    lane[l] = s;
   }
-  /* warp trees (32 lanes each) */
   for (int w = 0; w < PSD_SLICE_LANES / 32; ++w)
     for (int off = 16; off >= 1; off >>= 1)
-      for (int l = 0; l < off; ++l)
-        lane[32 * w + l] = psd_combine(lane[32 * w + l], lane[32 * w + l + off]);
-  /* 8 warp results */
-  psd_ms wr[8];
+      for (int l = 0; l < off; ++l) lane[32 * w + l] = psd_add(lane[32 * w + l], lane[32 * w + l + off]);
+  float wr[8];
   for (int w = 0; w < 8; ++w) wr[w] = lane[32 * w];
   for (int off = 4; off >= 1; off >>= 1)
-    for (int w = 0; w < off; ++w) wr[w] = psd_combine(wr[w], wr[w + off]);
-  return wr[0];
+    for (int w = 0; w < off; ++w) wr[w] = psd_add(wr[w], wr[w + off]);
+  psd_ms out = {M, wr[0]};
+  return out;
 }
 
 void oracle_row_stats(const float* row, int n, float inv_temp, float* M, float* S) {
+  const float c = psd_scale(inv_temp);
   psd_ms acc = {PSD_NEG_INF, 0.0f};
   int first = 1;
   for (int begin = 0; begin < n; begin += PSD_SLICE) {
-    psd_ms sl = slice_stats(row, begin, n, inv_temp);
-    acc = first ? sl : psd_combine(acc, sl);
+    psd_ms sl = slice_stats(row, begin, n, c);
+    acc = first ? sl : psd_combine(acc, sl, c);
     first = 0;
   }
   *M = acc.m;
   *S = acc.s;
 }
 
-float oracle_exp(float x) { return psd_exp(x); }
+float oracle_exp2(float t) { return psd_exp2(t); }
 
 int32_t oracle_row_argmax(const float* row, int n) {
   psd_vi best = {PSD_NEG_INF, 0x7fffffff};
@@ -92,19 +85,18 @@ int32_t oracle_row_argmax(const float* row, int n) {
 
 /* ---- prefix-search sampling in canonical order -------------------------- */
 typedef struct {
-  const float* t; /* target row (scaled by inv_temp on load) */
+  const float* t; /* target row */
   const float* d; /* draft row or NULL (bonus mode) */
   int V, Vd;
-  float inv_temp, Mt, St, Md, Sd;
+  float c, Mt, St, Md, Sd;
   int residual; /* 1: r = max(0, p - q); 0: w = p */
 } weight_src;
 
 static float weight_at(const weight_src* w, int x) {
   if (x >= w->V) return 0.0f;
-  const float et = psd_exp(psd_sub(psd_mul(w->t[x], w->inv_temp), w->Mt));
+  const float et = psd_weight(w->t[x], w->c, psd_bias(w->Mt, w->c));
   if (!w->residual) return et;
-  const float ed = (x < w->Vd) ? psd_exp(psd_sub(psd_mul(w->d[x], w->inv_temp), w->Md))
-                               : 0.0f;
+  const float ed = (x < w->Vd) ? psd_weight(w->d[x], w->c, psd_bias(w->Md, w->c)) : 0.0f;
   return psd_residual(et, ed, w->St, w->Sd);
 }
 
@@ -209,6 +201,7 @@ int oracle_verify_sample(const float* t, int64_t tsb, int64_t tsi, int V, const 
                          const int32_t* draft_len, const float* uniforms, float temperature,
                          int B, int K, int32_t* accepted_len, int32_t* out_tokens) {
   const float inv_temp = 1.0f / temperature;
+  const float c = psd_scale(inv_temp);
   for (int b = 0; b < B; ++b) {
     const int kb = draft_len[b];
     if (kb < 0 || kb > K) return 1;
@@ -221,14 +214,14 @@ int oracle_verify_sample(const float* t, int64_t tsb, int64_t tsi, int V, const 
       oracle_row_stats(dr, Vd, inv_temp, &Md, &Sd);
       const int32_t x = draft_ids[b * K + a];
       if (x < 0 || x >= V) break;
-      const float et = psd_exp(psd_sub(psd_mul(tr[x], inv_temp), Mt));
-      const float ed = x < Vd ? psd_exp(psd_sub(psd_mul(dr[x], inv_temp), Md)) : 0.0f;
+      const float et = psd_weight(tr[x], c, psd_bias(Mt, c));
+      const float ed = x < Vd ? psd_weight(dr[x], c, psd_bias(Md, c)) : 0.0f;
       if (!psd_accept(uniforms[b * (K + 1) + a], et, ed, St, Sd)) break;
     }
     weight_src w;
     w.V = V;
     w.Vd = Vd;
-    w.inv_temp = inv_temp;
+    w.c = c;
     w.t = t + b * tsb + a * tsi;
     if (a < kb) { /* rejected at a: stats of rows a already computed */
       w.d = d + b * dsb + a * dsi;

@@ -1,0 +1,381 @@
+// gemm.cu -- K2: bf16 GEMM on tcgen05 tensor cores (TMEM accumulators, TMA
+// operand staging, mbarrier pipeline), swap-AB for skinny token counts.
+//
+//   Y[m, n] = sum_k X[m, k] * W[n, k]          X: [M, K] bf16, W: [N, K] bf16
+//
+// Replaces the reference's virtual pass durations
+// (verify_latency / draft_latency .duration, pkg/src/specsim/engine.py:338,
+// 359-360, 378, 402, 429) with the real dense contractions of the target
+// verify forward (M = B (k+1) tokens) and the draft decode (M = B tokens).
+//
+// Design (B200-first):
+//   * swap-AB: the weight tile is the UMMA "A" operand (M = 128 weight rows),
+//     the token tile is "B" (N = 32..256 tokens).  Decode / verify token counts
+//     are 32..320, so one UMMA N covers the whole batch and every weight byte
+//     is read from HBM exactly once per GEMM (weights are the HBM roofline).
+//   * warp specialisation, 6 warps: warp 0 = TMA producer (one elected lane),
+//     warp 1 = MMA issuer (one lane issues tcgen05.mma, commits release smem
+//     stages), warps 2-5 = epilogue (tcgen05.ld TMEM -> registers -> global).
+//   * multi-stage smem ring (4-8 stages of 16 KB weights + BN*128 B tokens),
+//     128-byte swizzle matching the UMMA descriptors; weights are loaded with an
+//     L2 evict-first policy (streamed once), tokens evict-last (re-read by
+//     every weight tile).
+//   * split-K over blockIdx.z when the weight-tile count cannot fill 148 SMs;
+//     fp32 partials are reduced by psd_gemm_reduce with the same epilogue.
+// Epilogues: bf16 store, fp32 store (LM-head logits), residual add (x += W o),
+// fused SiLU(gate) * up (weights packed gate/up per 64-row half tile).
+#include <algorithm>
+#include <mutex>
+
+#include "../../include/psd.h"
+#include "sm100.cuh"
+
+namespace {
+using namespace psd;
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kThreads = 192;
+
+struct GemmArgs {
+  int M, N, K;
+  int kb_total, kb_per_split;
+  void* Y;
+  int ldy;
+  const __nv_bfloat16* R;
+  int ldr;
+};
+
+template <int BN>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int MAXS = (200 * 1024) / STAGE;
+  static constexpr int STAGES = MAXS > 8 ? 8 : MAXS;
+  static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  static constexpr int XCHG_BYTES = 64 * 17 * 4;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + 256 + XCHG_BYTES;
+};
+
+__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+            const GemmArgs g) {
+  using C = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* accum = empty + C::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+  float* xchg = reinterpret_cast<float*>(full + 32);  // after the 256 B barrier area
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * BM, m0 = blockIdx.y * BN, z = blockIdx.z;
+  const int kb0 = z * g.kb_per_split;
+  const int nkb = min(g.kb_total, kb0 + g.kb_per_split) - kb0;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmW);
+    tma_prefetch(&tmX);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    mbar_init(accum, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_w = policy_evict_first();
+      const uint64_t pol_x = policy_evict_last();
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % C::STAGES;
+        const uint32_t ph = (i / C::STAGES) & 1;
+        mbar_wait(empty + s, ph ^ 1);
+        mbar_arrive_expect_tx(full + s, C::STAGE);
+        const int kc = (kb0 + i) * BK;
+        tma_load_2d(sA + s * C::A_BYTES, &tmW, full + s, kc, n0, pol_w);
+        tma_load_2d(sB + s * C::B_BYTES, &tmX, full + s, kc, m0, pol_x);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % C::STAGES;
+        const uint32_t ph = (i / C::STAGES) & 1;
+        mbar_wait(full + s, ph);
+        tc_fence_after();
+        const uint32_t a = smem_u32(sA + s * C::A_BYTES);
+        const uint32_t b = smem_u32(sB + s * C::B_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < BK / 16; ++kk)
+          mma_bf16(tmem, umma_desc_sw128(a + kk * 32), umma_desc_sw128(b + kk * 32), idesc,
+                   (i | kk) != 0);
+        mma_commit(empty + s);
+      }
+      mma_commit(accum);
+    }
+    __syncwarp();
+  } else {
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    mbar_wait(accum, 0);
+    tc_fence_after();
+    const int n = n0 + 32 * q + lane;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 16) {
+      uint32_t r[16];
+      tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c, r);
+      tmem_ld_wait();
+      if constexpr (EPI == PSD_EPI_SILU) {
+        // rows 0-63 of the tile: gate j, rows 64-127: up j (j = tile*64 + row%64)
+        if (q >= 2) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) xchg[((q - 2) * 32 + lane) * 17 + j] = __uint_as_float(r[j]);
+        }
+        named_bar_sync(1, 128);
+        if (q < 2) {
+          const int jo = blockIdx.x * 64 + 32 * q + lane;
+          __nv_bfloat16* Y = static_cast<__nv_bfloat16*>(g.Y);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int m = m0 + c + j;
+            if (m < g.M) {
+              const float gt = __uint_as_float(r[j]);
+              const float up = xchg[(q * 32 + lane) * 17 + j];
+              Y[(size_t)m * g.ldy + jo] = __float2bfloat16(silu(gt) * up);
+            }
+          }
+        }
+        named_bar_sync(1, 128);
+      } else {
+        if (n < g.N) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int m = m0 + c + j;
+            if (m >= g.M) break;
+            const float v = __uint_as_float(r[j]);
+            if constexpr (EPI == PSD_EPI_PARTIAL) {
+              float* P = static_cast<float*>(g.Y) + (size_t)z * g.M * g.N;
+              P[(size_t)m * g.N + n] = v;
+            } else if constexpr (EPI == PSD_EPI_F32) {
+              static_cast<float*>(g.Y)[(size_t)m * g.ldy + n] = v;
+            } else if constexpr (EPI == PSD_EPI_RESID) {
+              __nv_bfloat16* Y = static_cast<__nv_bfloat16*>(g.Y);
+              const float rv = __bfloat162float(g.R[(size_t)m * g.ldr + n]);
+              Y[(size_t)m * g.ldy + n] = __float2bfloat16(v + rv);
+            } else {
+              static_cast<__nv_bfloat16*>(g.Y)[(size_t)m * g.ldy + n] = __float2bfloat16(v);
+            }
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
+}
+
+// ---- split-K reduction with the same epilogues ------------------------------
+__global__ void gemm_reduce_kernel(const float* __restrict__ P, int splits, int M, int N, int epi,
+                                   void* Y, int ldy, const __nv_bfloat16* R, int ldr) {
+  const int Nout = epi == PSD_EPI_SILU ? N / 2 : N;
+  const size_t total = (size_t)M * Nout;
+  const size_t slice = (size_t)M * N;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const int m = idx / Nout, n = idx % Nout;
+    if (epi == PSD_EPI_SILU) {
+      const int t = n / 64, jl = n % 64;
+      const size_t ig = (size_t)m * N + t * 128 + jl, iu = ig + 64;
+      float gs = 0.f, us = 0.f;
+      for (int s = 0; s < splits; ++s) {
+        gs += P[s * slice + ig];
+        us += P[s * slice + iu];
+      }
+      static_cast<__nv_bfloat16*>(Y)[(size_t)m * ldy + n] = __float2bfloat16(silu(gs) * us);
+      continue;
+    }
+    float acc = 0.f;
+    for (int s = 0; s < splits; ++s) acc += P[s * slice + (size_t)m * N + n];
+    if (epi == PSD_EPI_F32) {
+      static_cast<float*>(Y)[(size_t)m * ldy + n] = acc;
+    } else if (epi == PSD_EPI_RESID) {
+      const float rv = __bfloat162float(R[(size_t)m * ldr + n]);
+      static_cast<__nv_bfloat16*>(Y)[(size_t)m * ldy + n] = __float2bfloat16(acc + rv);
+    } else {
+      static_cast<__nv_bfloat16*>(Y)[(size_t)m * ldy + n] = __float2bfloat16(acc);
+    }
+  }
+}
+
+// ---- host side -----------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 tensor [rows, K] (row pitch ld elements), box = 64 x box_rows, SW128
+int make_map(CUtensorMap* map, const void* base, int rows, int K, int ld, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return (int)cudaErrorNotSupported;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
+}
+
+template <int BN, int EPI>
+int launch_bn(const CUtensorMap& mw, const CUtensorMap& mx, const GemmArgs& g, dim3 grid,
+              cudaStream_t st) {
+  using C = Cfg<BN>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN, EPI>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return (int)e;
+    attr_done = true;
+  }
+  gemm_kernel<BN, EPI><<<grid, kThreads, C::SMEM, st>>>(mw, mx, g);
+  return (int)cudaGetLastError();
+}
+
+template <int EPI>
+int launch_epi(int bn, const CUtensorMap& mw, const CUtensorMap& mx, const GemmArgs& g, dim3 grid,
+               cudaStream_t st) {
+  switch (bn) {
+    case 32: return launch_bn<32, EPI>(mw, mx, g, grid, st);
+    case 64: return launch_bn<64, EPI>(mw, mx, g, grid, st);
+    case 96: return launch_bn<96, EPI>(mw, mx, g, grid, st);
+    case 128: return launch_bn<128, EPI>(mw, mx, g, grid, st);
+    case 160: return launch_bn<160, EPI>(mw, mx, g, grid, st);
+    case 192: return launch_bn<192, EPI>(mw, mx, g, grid, st);
+    case 224: return launch_bn<224, EPI>(mw, mx, g, grid, st);
+    case 256: return launch_bn<256, EPI>(mw, mx, g, grid, st);
+  }
+  return (int)cudaErrorInvalidValue;
+}
+
+int token_tile(int M) {
+  if (M > 256) {
+    // fewest tiles, then least padding
+    int best = 256, best_pad = 1 << 30;
+    for (int bn = 256; bn >= 128; bn -= 32) {
+      const int tiles = (M + bn - 1) / bn;
+      const int pad = tiles * bn - M + tiles * 8;  // mild preference for fewer tiles
+      if (pad < best_pad) { best_pad = pad; best = bn; }
+    }
+    return best;
+  }
+  return std::max(32, (M + 31) / 32 * 32);
+}
+
+}  // namespace
+
+extern "C" {
+
+int psd_gemm_plan(int M, int N, int K, int epi, int splits_hint, int* splits_out,
+                  size_t* workspace_bytes) {
+  if (M <= 0 || N <= 0 || K <= 0 || (K % 8) || (N % BM)) return (int)cudaErrorInvalidValue;
+  const int bn = token_tile(M);
+  const int tiles = (N / BM) * ((M + bn - 1) / bn);
+  const int kb_total = (K + BK - 1) / BK;
+  int splits = splits_hint;
+  if (splits <= 0) {
+    splits = 1;
+    if (tiles < 120) splits = std::max(1, std::min(148 / tiles, kb_total / 4));
+  }
+  splits = std::max(1, std::min(splits, kb_total));
+  const int per = (kb_total + splits - 1) / splits;
+  splits = (kb_total + per - 1) / per;
+  if (splits_out) *splits_out = splits;
+  if (workspace_bytes) *workspace_bytes = splits > 1 ? (size_t)splits * M * N * sizeof(float) : 0;
+  (void)epi;
+  return 0;
+}
+
+int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, int N, void* Y,
+                  int ldy, int epi, const void* R, int ldr, int splits_hint, void* workspace,
+                  size_t workspace_bytes, void* stream) {
+  if (!X || !W || !Y || epi < 0 || epi > PSD_EPI_SILU) return (int)cudaErrorInvalidValue;
+  if (epi == PSD_EPI_RESID && !R) return (int)cudaErrorInvalidValue;
+  if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(W)) & 15)
+    return (int)cudaErrorMisalignedAddress;
+  if ((ldx % 8) || (ldw % 8)) return (int)cudaErrorMisalignedAddress;
+  int splits = 1;
+  size_t need = 0;
+  int rc = psd_gemm_plan(M, N, K, epi, splits_hint, &splits, &need);
+  if (rc) return rc;
+  if (splits > 1 && (!workspace || workspace_bytes < need)) {
+    // not enough workspace: fall back to fewer splits that fit (or none)
+    while (splits > 1 && (size_t)splits * M * N * sizeof(float) > workspace_bytes) --splits;
+    rc = psd_gemm_plan(M, N, K, epi, splits, &splits, &need);
+    if (rc) return rc;
+    if (splits > 1 && (!workspace || workspace_bytes < need)) splits = 1;
+  }
+  const int bn = token_tile(M);
+  CUtensorMap mw, mx;
+  if ((rc = make_map(&mw, W, N, K, ldw, BM))) return rc;
+  if ((rc = make_map(&mx, X, M, K, ldx, bn))) return rc;
+  GemmArgs g;
+  g.M = M; g.N = N; g.K = K;
+  g.kb_total = (K + BK - 1) / BK;
+  g.kb_per_split = (g.kb_total + splits - 1) / splits;
+  splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
+  g.Y = splits > 1 ? workspace : Y;
+  g.ldy = ldy; g.R = static_cast<const __nv_bfloat16*>(R); g.ldr = ldr;
+  dim3 grid(N / BM, (M + bn - 1) / bn, splits);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (splits > 1) {
+    rc = launch_epi<PSD_EPI_PARTIAL>(bn, mw, mx, g, grid, st);
+    if (rc) return rc;
+    const int Nout = epi == PSD_EPI_SILU ? N / 2 : N;
+    const size_t total = (size_t)M * Nout;
+    const int blocks = (int)std::min<size_t>((total + 255) / 256, 148 * 8);
+    gemm_reduce_kernel<<<blocks, 256, 0, st>>>(static_cast<const float*>(workspace), splits, M, N,
+                                               epi, Y, ldy, static_cast<const __nv_bfloat16*>(R),
+                                               ldr);
+    return (int)cudaGetLastError();
+  }
+  switch (epi) {
+    case PSD_EPI_BF16: return launch_epi<PSD_EPI_BF16>(bn, mw, mx, g, grid, st);
+    case PSD_EPI_F32: return launch_epi<PSD_EPI_F32>(bn, mw, mx, g, grid, st);
+    case PSD_EPI_RESID: return launch_epi<PSD_EPI_RESID>(bn, mw, mx, g, grid, st);
+    case PSD_EPI_SILU: return launch_epi<PSD_EPI_SILU>(bn, mw, mx, g, grid, st);
+  }
+  return (int)cudaErrorInvalidValue;
+}
+
+}  // extern "C"

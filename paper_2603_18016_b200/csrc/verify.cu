@@ -41,7 +41,7 @@ struct Params {
   const float* t; int64_t tsb, tsi; int V;
   const float* d; int64_t dsb, dsi; int Vd;
   const int32_t* ids; const int32_t* len; const float* u;
-  float inv_temp; int B, K;
+  float c; int B, K;  // c = psd_scale(1/T)
   int32_t* acc; int32_t* out;
   int* cnt_a; int* cnt_b;
   float2* part; Plan* plan; float* wblk;
@@ -102,65 +102,76 @@ verify_stats(const Params p) {
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const int e = base + 4 * (tid + kThreads * j);
-    v[j] = e < n ? ld_stream(row + e) : make_float4(PSD_NEG_INF, PSD_NEG_INF, PSD_NEG_INF,
-                                                    PSD_NEG_INF);
+    v[j] = e < n ? ld_stream(row + e)
+                 : make_float4(PSD_NEG_INF, PSD_NEG_INF, PSD_NEG_INF, PSD_NEG_INF);
   }
-
-  __shared__ float2 red[kThreads / 32];
+  // exact slice max: lane -> warp (xor tree) -> block
+  float lm = PSD_NEG_INF;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    lm = psd_max(lm, psd_max(psd_max(v[j].x, v[j].y), psd_max(v[j].z, v[j].w)));
+  float wm = lm;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) wm = psd_max(wm, __shfl_xor_sync(0xffffffffu, wm, off));
+  __shared__ float s_max[kThreads / 32];
+  __shared__ float s_sum[kThreads / 32];
+  __shared__ int s_idx[kThreads / 32];
   __shared__ int s_last;
+  if (lane == 0) s_max[warp] = wm;
+  __syncthreads();
+  float M = s_max[0];
+#pragma unroll
+  for (int q = 1; q < kThreads / 32; ++q) M = psd_max(M, s_max[q]);
+
   if constexpr (SAMPLE) {
-    float m = PSD_NEG_INF;
+    const float bias = psd_bias(M, p.c);
+    float s = 0.0f;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      v[j].x = psd_mul(v[j].x, p.inv_temp); v[j].y = psd_mul(v[j].y, p.inv_temp);
-      v[j].z = psd_mul(v[j].z, p.inv_temp); v[j].w = psd_mul(v[j].w, p.inv_temp);
-      m = psd_max(m, psd_max(psd_max(v[j].x, v[j].y), psd_max(v[j].z, v[j].w)));
-    }
-    float s = 0.0f;
-    if (m != PSD_NEG_INF) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        // invalid elements are -inf -> E() == 0, adding 0.0f is exact
-        s = psd_add(s, psd_exp(psd_sub(v[j].x, m)));
-        s = psd_add(s, psd_exp(psd_sub(v[j].y, m)));
-        s = psd_add(s, psd_exp(psd_sub(v[j].z, m)));
-        s = psd_add(s, psd_exp(psd_sub(v[j].w, m)));
+      // invalid elements (-inf) are not part of the row: skip them
+      const int e = base + 4 * (tid + kThreads * j);
+      if (e < n) {
+        s = psd_add(s, psd_weight(v[j].x, p.c, bias));
+        s = psd_add(s, psd_weight(v[j].y, p.c, bias));
+        s = psd_add(s, psd_weight(v[j].z, p.c, bias));
+        s = psd_add(s, psd_weight(v[j].w, p.c, bias));
       }
     }
-    psd_ms acc = {m, s};
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) acc = psd_combine(acc, shfl_ms(acc, off));
-    if (lane == 0) red[warp] = make_float2(acc.m, acc.s);
+    s = shfl_add_tree(s);
+    if (lane == 0) s_sum[warp] = s;
     __syncthreads();
     if (tid == 0) {
-      psd_ms w[8];
+      float w[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) { w[q].m = red[q].x; w[q].s = red[q].y; }
+      for (int q = 0; q < 8; ++q) w[q] = s_sum[q];
 #pragma unroll
       for (int off = 4; off >= 1; off >>= 1)
 #pragma unroll
-        for (int q = 0; q < off; ++q) w[q] = psd_combine(w[q], w[q + off]);
-      p.part[(b * p.R + r) * p.NS + slice] = make_float2(w[0].m, w[0].s);
+        for (int q = 0; q < off; ++q) w[q] = psd_add(w[q], w[q + off]);
+      p.part[(b * p.R + r) * p.NS + slice] = make_float2(M, w[0]);
     }
   } else {
-    psd_vi best = {PSD_NEG_INF, 0x7fffffff};
+    // first (lowest) index attaining M
+    int idx = 0x7fffffff;
+    if (lm == M) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int e = base + 4 * (tid + kThreads * j);
-      best = psd_argmax2(best, psd_vi{v[j].x, e});
-      best = psd_argmax2(best, psd_vi{v[j].y, e + 1});
-      best = psd_argmax2(best, psd_vi{v[j].z, e + 2});
-      best = psd_argmax2(best, psd_vi{v[j].w, e + 3});
+      for (int j = 7; j >= 0; --j) {
+        const int e = base + 4 * (tid + kThreads * j);
+        if (v[j].w == M) idx = e + 3;
+        if (v[j].z == M) idx = e + 2;
+        if (v[j].y == M) idx = e + 1;
+        if (v[j].x == M) idx = e;
+      }
     }
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) best = psd_argmax2(best, shfl_vi(best, off));
-    if (lane == 0) red[warp] = make_float2(best.v, __int_as_float(best.i));
+    for (int off = 16; off >= 1; off >>= 1) idx = min(idx, __shfl_xor_sync(0xffffffffu, idx, off));
+    if (lane == 0) s_idx[warp] = idx;
     __syncthreads();
     if (tid == 0) {
-      psd_vi w = {red[0].x, __float_as_int(red[0].y)};
+      int w = s_idx[0];
 #pragma unroll
-      for (int q = 1; q < 8; ++q) w = psd_argmax2(w, psd_vi{red[q].x, __float_as_int(red[q].y)});
-      p.part[(b * p.R + r) * p.NS + slice] = make_float2(w.v, __int_as_float(w.i));
+      for (int q = 1; q < 8; ++q) w = min(w, s_idx[q]);
+      p.part[(b * p.R + r) * p.NS + slice] = make_float2(M, __int_as_float(w));
     }
   }
 
@@ -174,32 +185,31 @@ verify_stats(const Params p) {
   if (!s_last) return;
   __threadfence();
 
+  __shared__ float2 s_part[(2 * PSD_MAX_K + 1) * PSD_MAX_SLICES];
   __shared__ float sMt[PSD_MAX_K + 1], sSt[PSD_MAX_K + 1], sMd[PSD_MAX_K], sSd[PSD_MAX_K];
   __shared__ int sG[PSD_MAX_K + 1];
   const int nst = (p.V + PSD_SLICE - 1) / PSD_SLICE;
   const int nsd = (p.Vd + PSD_SLICE - 1) / PSD_SLICE;
   const int nrows = SAMPLE ? 2 * kb + 1 : kb + 1;
+  // stage every partial of request b in shared memory (parallel loads)
+  for (int q = tid; q < nrows * p.NS; q += kThreads) {
+    const int rowi = q / p.NS, sl = q % p.NS;
+    const int rr = rowi > kb ? p.K + 1 + (rowi - (kb + 1)) : rowi;
+    s_part[q] = __ldcg(p.part + (b * p.R + rr) * p.NS + sl);
+  }
+  __syncthreads();
   if (tid < nrows) {
     const bool dr = tid > kb;
     const int ri = dr ? tid - (kb + 1) : tid;
-    const int rr = dr ? p.K + 1 + ri : ri;
-    const float2* pp = p.part + (b * p.R + rr) * p.NS;
+    const float2* pp = s_part + tid * p.NS;
     const int ns = dr ? nsd : nst;
     if constexpr (SAMPLE) {
-      float2 f = __ldcg(pp);
-      psd_ms a = {f.x, f.y};
-      for (int s = 1; s < ns; ++s) {
-        f = __ldcg(pp + s);
-        a = psd_combine(a, psd_ms{f.x, f.y});
-      }
+      psd_ms a = {pp[0].x, pp[0].y};
+      for (int q = 1; q < ns; ++q) a = psd_combine(a, psd_ms{pp[q].x, pp[q].y}, p.c);
       if (dr) { sMd[ri] = a.m; sSd[ri] = a.s; } else { sMt[ri] = a.m; sSt[ri] = a.s; }
     } else {
-      float2 f = __ldcg(pp);
-      psd_vi a = {f.x, __float_as_int(f.y)};
-      for (int s = 1; s < ns; ++s) {
-        f = __ldcg(pp + s);
-        a = psd_argmax2(a, psd_vi{f.x, __float_as_int(f.y)});
-      }
+      psd_vi a = {pp[0].x, __float_as_int(pp[0].y)};
+      for (int q = 1; q < ns; ++q) a = psd_argmax2(a, psd_vi{pp[q].x, __float_as_int(pp[q].y)});
       sG[ri] = a.i;
     }
   }
@@ -213,21 +223,19 @@ verify_stats(const Params p) {
         if (x >= 0 && x < p.V) {
           const float* tr = p.t + b * p.tsb + lane * p.tsi;
           const float* drw = p.d + b * p.dsb + lane * p.dsi;
-          const float et = psd_exp(psd_sub(psd_mul(__ldg(tr + x), p.inv_temp), sMt[lane]));
-          const float ed = x < p.Vd
-                               ? psd_exp(psd_sub(psd_mul(__ldg(drw + x), p.inv_temp), sMd[lane]))
-                               : 0.0f;
+          const float et = psd_weight(__ldg(tr + x), p.c, psd_bias(sMt[lane], p.c));
+          const float ed =
+              x < p.Vd ? psd_weight(__ldg(drw + x), p.c, psd_bias(sMd[lane], p.c)) : 0.0f;
           ok = psd_accept(p.u[b * (p.K + 1) + lane], et, ed, sSt[lane], sSd[lane]);
         }
       } else {
         ok = x == sG[lane];
       }
     }
-    const unsigned rej = __ballot_sync(0xffffffffu, !ok);
-    const unsigned rej_in = rej & ((kb >= 32) ? 0xffffffffu : ((1u << kb) - 1u));
-    const int a = rej_in ? __ffs(rej_in) - 1 : kb;
+    const unsigned rej = __ballot_sync(0xffffffffu, !ok) & ((1u << kb) - 1u);
+    const int a = rej ? __ffs(rej) - 1 : kb;
     int32_t* o = p.out + b * (p.K + 1);
-    if (lane <= p.K) o[lane] = lane < a ? x : -1;
+    if (lane <= p.K) o[lane] = lane < a ? x : (!SAMPLE && lane == a ? sG[a] : -1);
     if (lane == 0) {
       p.acc[b] = a;
       if constexpr (SAMPLE) {
@@ -242,23 +250,19 @@ verify_stats(const Params p) {
       }
       p.cnt_a[b] = 0;  // self-cleaning ticket for the next launch
     }
-    __syncwarp();
-    if constexpr (!SAMPLE) {
-      if (lane == 0) o[a] = sG[a];
-    }
   }
 }
 
 // ---- sampling pass ---------------------------------------------------------
 struct WeightCtx {
-  const float* t; const float* d; int V, Vd; float inv_temp, Mt, St, Md, Sd; int residual;
+  const float* t; const float* d; int V, Vd; float c, bt, bd, St, Sd; int residual;
 };
 
 __device__ __forceinline__ float weight_of(const WeightCtx& w, float tv, float dv, int x) {
   if (x >= w.V) return 0.0f;
-  const float et = psd_exp(psd_sub(psd_mul(tv, w.inv_temp), w.Mt));
+  const float et = psd_weight(tv, w.c, w.bt);
   if (!w.residual) return et;
-  const float ed = x < w.Vd ? psd_exp(psd_sub(psd_mul(dv, w.inv_temp), w.Md)) : 0.0f;
+  const float ed = x < w.Vd ? psd_weight(dv, w.c, w.bd) : 0.0f;
   return psd_residual(et, ed, w.St, w.Sd);
 }
 
@@ -320,10 +324,10 @@ verify_sample(const Params p) {
   const int blk = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
   const Plan pl = p.plan[b];
   WeightCtx w;
-  w.V = p.V; w.Vd = p.Vd; w.inv_temp = p.inv_temp;
+  w.V = p.V; w.Vd = p.Vd; w.c = p.c;
   w.t = p.t + b * p.tsb + pl.row * p.tsi;
   w.d = p.d + b * p.dsb + pl.row * p.dsi;
-  w.Mt = pl.Mt; w.St = pl.St; w.Md = pl.Md; w.Sd = pl.Sd;
+  w.bt = psd_bias(pl.Mt, p.c); w.bd = psd_bias(pl.Md, p.c); w.St = pl.St; w.Sd = pl.Sd;
   w.residual = pl.mode == 1;
 
   __shared__ float s_red[8];
@@ -341,12 +345,14 @@ verify_sample(const Params p) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  float* wb = p.wblk + b * p.NB;
+  __shared__ float wb[PSD_MAX_SBLKS];
+  for (int k = tid; k < p.NB; k += kThreads) wb[k] = __ldcg(p.wblk + b * p.NB + k);
+  __syncthreads();
 
   // degenerate residual (sums to 0 in fp32): fall back to sampling from p
   if (tid == 0) {
     float R = 0.0f;
-    for (int k = 0; k < p.NB; ++k) R = psd_add(R, __ldcg(wb + k));
+    for (int k = 0; k < p.NB; ++k) R = psd_add(R, wb[k]);
     s_int = (w.residual && !(R > 0.0f)) ? 1 : 0;
   }
   __syncthreads();
@@ -361,20 +367,20 @@ verify_sample(const Params p) {
   }
   if (tid == 0) {
     float R = 0.0f;
-    for (int k = 0; k < p.NB; ++k) R = psd_add(R, __ldcg(wb + k));
+    for (int k = 0; k < p.NB; ++k) R = psd_add(R, wb[k]);
     const float T = psd_mul(p.u[b * (p.K + 1) + p.K], R);
     float P = 0.0f;
     int chosen = -1;
     float Pprev = 0.0f;
     for (int k = 0; k < p.NB; ++k) {
-      const float Pn = psd_add(P, __ldcg(wb + k));
+      const float Pn = psd_add(P, wb[k]);
       if (Pn > T) { chosen = k; Pprev = P; break; }
       P = Pn;
     }
     if (chosen < 0) {
       chosen = -2 - (p.NB - 1);
       for (int k = p.NB - 1; k >= 0; --k)
-        if (__ldcg(wb + k) > 0.0f) { chosen = -2 - k; break; }
+        if (wb[k] > 0.0f) { chosen = -2 - k; break; }
     }
     s_chosen = chosen; s_T = T; s_Pprev = Pprev;
   }
@@ -438,6 +444,7 @@ WsLayout layout(int B, int K, int V, int Vd, int sampling) {
 int check_common(const float* t, int64_t tsb, int64_t tsi, int V, int B, int K,
                  const void* ws, size_t ws_bytes, size_t need) {
   if (!t || V <= 0 || B <= 0 || K < 0 || K > PSD_MAX_K) return (int)cudaErrorInvalidValue;
+  if (V > PSD_MAX_SLICES * PSD_SLICE) return (int)cudaErrorInvalidValue;
   if ((V & 3) || (tsb & 3) || (tsi & 3) || (reinterpret_cast<uintptr_t>(t) & 15))
     return (int)cudaErrorMisalignedAddress;
   if (!ws || ws_bytes < need) return (int)cudaErrorInvalidValue;
@@ -467,7 +474,7 @@ int psd_verify_greedy(const float* target_logits, int64_t t_stride_b, int64_t t_
   char* w = static_cast<char*>(ws);
   p.t = target_logits; p.tsb = t_stride_b; p.tsi = t_stride_i; p.V = V;
   p.d = nullptr; p.Vd = 0; p.ids = draft_ids; p.len = draft_len; p.u = nullptr;
-  p.inv_temp = 1.0f; p.B = B; p.K = K; p.acc = accepted_len; p.out = out_tokens;
+  p.c = psd_scale(1.0f); p.B = B; p.K = K; p.acc = accepted_len; p.out = out_tokens;
   p.cnt_a = reinterpret_cast<int*>(w + L.cnt_a); p.cnt_b = reinterpret_cast<int*>(w + L.cnt_b);
   p.part = reinterpret_cast<float2*>(w + L.part); p.plan = reinterpret_cast<Plan*>(w + L.plan);
   p.wblk = reinterpret_cast<float*>(w + L.wblk);
@@ -495,7 +502,7 @@ int psd_verify_sample(const float* target_logits, int64_t t_stride_b, int64_t t_
   p.t = target_logits; p.tsb = t_stride_b; p.tsi = t_stride_i; p.V = V;
   p.d = draft_logits; p.dsb = d_stride_b; p.dsi = d_stride_i; p.Vd = Vd;
   p.ids = draft_ids; p.len = draft_len; p.u = uniforms;
-  p.inv_temp = 1.0f / temperature; p.B = B; p.K = K; p.acc = accepted_len; p.out = out_tokens;
+  p.c = psd_scale(1.0f / temperature); p.B = B; p.K = K; p.acc = accepted_len; p.out = out_tokens;
   p.cnt_a = reinterpret_cast<int*>(w + L.cnt_a); p.cnt_b = reinterpret_cast<int*>(w + L.cnt_b);
   p.part = reinterpret_cast<float2*>(w + L.part); p.plan = reinterpret_cast<Plan*>(w + L.plan);
   p.wblk = reinterpret_cast<float*>(w + L.wblk);

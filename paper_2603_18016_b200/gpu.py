@@ -1,0 +1,476 @@
+"""GpuBackend: the scheduler's passes as real sm_100a work.
+
+Replaces the reference's two abstractions:
+  * pass durations ``draft_latency`` / ``verify_latency .duration`` (engine.py:
+    338, 359-360, 378, 402, 429) -> the draft model's k-step decode loop and the
+    target model's verify forward over k+1 tokens per request (model.py),
+    timed with CUDA events;
+  * ``accepted_count(acceptance_stream(seed, rid, j))`` (engine.py:245-256)
+    -> the fused verification kernel K1 (ops.verify_greedy / verify_sample)
+    over the real logits.
+
+Batch parallelism: the skip batch's draft loop runs on the *draft stream*
+while the target batch is verified on the *target stream* (one GPU; or the
+draft model on its own device, see ``draft_device``).  The only host sync per
+step is the D2H of the verified rows' accepted lengths.
+
+Per-request device state lives in "slots" (one per running request):
+  slot_tok[s, 0..1]   last two committed tokens (inputs of the next draft)
+  slot_tok[s, 2+i]    draft i of the pending draft
+  generated[s], outputs[s, :]   committed output tokens
+  block_table[s, :]   physical KV blocks (shared by target and draft caches)
+KV sizing: a GPU cannot peek the next acceptance (the reference does,
+engine.py:162-175), so grants reserve k_i + 1 positions and the rejected
+tail is given back after the commit (KVBlockTable.trim_to_written).
+"""
+
+from __future__ import annotations
+
+import time
+
+import numpy as np
+import torch
+
+from . import native, ops
+from .errors import ConfigError, KVError, ProtocolError
+from .kvtable import BlockPool
+from .model import PRESETS, Forward, ModelShape, Transformer, successor_table
+from .scheduler import EngineState, StepPlan, StepResult, VerifyRow
+from .workload import attach_prompt_ids
+
+__all__ = ["GpuBackend"]
+
+
+def _shape(x) -> ModelShape:
+    if isinstance(x, ModelShape):
+        return x
+    if x not in PRESETS:
+        raise ConfigError(f"unknown model preset {x!r}; known: {sorted(PRESETS)}")
+    return PRESETS[x]
+
+
+class GpuBackend:
+    """Real draft / verify passes on a B200 (sm_100a)."""
+
+    def __init__(self, target="llama-3.1-8b", draft="llama-3.2-1b", *, max_requests: int = 64,
+                 max_batch: int = 64, k_max: int = 8, max_seq_len: int = 1024,
+                 mode: str = "greedy", temperature: float = 1.0, seed: int = 0,
+                 beta_target: float = 6.0, beta_draft: float = 12.0,
+                 device: str | torch.device = "cuda:0", dual_stream: bool = True,
+                 block_size: int = 16, num_blocks: int | None = None,
+                 prefill_chunk_tokens: int = 4096) -> None:
+        if not torch.cuda.is_available():
+            raise native.NativeError("GpuBackend needs a CUDA device (no CPU fallback)")
+        native.load()
+        if mode not in ("greedy", "sample"):
+            raise ConfigError(f"mode must be greedy or sample, got {mode!r}")
+        if k_max > 16:
+            raise ConfigError("k_max must be <= 16 (PSD_MAX_K)")
+        self.tshape, self.dshape = _shape(target), _shape(draft)
+        if self.dshape.vocab > self.tshape.vocab:
+            raise ConfigError("draft vocabulary must not exceed the target vocabulary")
+        self.device = torch.device(device)
+        self.mode = mode
+        self.temperature = float(temperature)
+        self.seed = seed
+        self.k_max = k_max
+        self.max_requests = max_requests
+        self.max_batch = max_batch
+        self.block_size = block_size
+        self.max_blocks = (max_seq_len + block_size - 1) // block_size + 1
+        if num_blocks is None:
+            num_blocks = max_requests * self.max_blocks + 1
+        # block 0 is a reserved scratch block: unused slots point at it
+        self.block_pool = BlockPool(num_blocks)
+        self.block_pool.take(1)
+        self.prefill_chunk = prefill_chunk_tokens
+        self.beta_target, self.beta_draft = beta_target, beta_draft
+        dev = self.device
+        with torch.cuda.device(dev):
+            self.target = Transformer(self.tshape, dev, seed * 2 + 1, num_blocks, block_size,
+                                      self.max_blocks)
+            self.draft = Transformer(self.dshape, dev, seed * 2 + 2, num_blocks, block_size,
+                                     self.max_blocks)
+            i32 = torch.int32
+            self.block_table = torch.zeros(max_requests, self.max_blocks, dtype=i32, device=dev)
+            self.block_table_host = torch.zeros(max_requests, self.max_blocks,
+                                                dtype=i32).pin_memory()
+            self.ldt = k_max + 2
+            self.slot_tok = torch.zeros(max_requests, self.ldt, dtype=i32, device=dev)
+            self.generated = torch.zeros(max_requests, dtype=i32, device=dev)
+            self.max_out = max_seq_len
+            self.outputs = torch.full((max_requests, self.max_out), -1, dtype=i32, device=dev)
+            succ = successor_table(self.tshape.vocab, self.dshape.vocab, seed)
+            self.succ_t = torch.from_numpy(succ).to(dev)
+            self.succ_d = torch.from_numpy(succ[:self.dshape.vocab].copy()).to(dev)
+            B, K = max_batch, k_max
+            vt_tokens = max(B * (K + 1), prefill_chunk_tokens)
+            vd_tokens = max(2 * B, prefill_chunk_tokens)
+            self.tfwd = Forward(self.target, vt_tokens, max(B, 256), B * (K + 1), self.block_table,
+                                sets=1)
+            self.dfwd = Forward(self.draft, vd_tokens, max(B, 256), B, self.block_table,
+                                sets=K + 1)
+            self.tlogits = torch.empty(B * (K + 1), self.tshape.vocab, dtype=torch.float32,
+                                       device=dev)
+            self.dlogits = torch.empty(B, self.dshape.vocab, dtype=torch.float32, device=dev)
+            if mode == "sample":
+                self.qbuf = torch.empty(max_requests, K, self.dshape.vocab, dtype=torch.float32,
+                                        device=dev)
+            self.v_ids = torch.empty(B, K, dtype=i32, device=dev)
+            self.v_len = torch.empty(B, dtype=i32, device=dev)
+            self.v_slot = torch.empty(B, dtype=i32, device=dev)
+            self.v_meta_host = torch.zeros(3 * B + B * K, dtype=i32).pin_memory()
+            self.v_meta = torch.zeros(3 * B + B * K, dtype=i32, device=dev)
+            self.acc_host = torch.zeros(B, dtype=i32).pin_memory()
+            self.d_out = torch.empty(B, 1, dtype=i32, device=dev)
+            self.d_acc = torch.empty(B, dtype=i32, device=dev)
+            self.d_len0 = torch.zeros(B, dtype=i32, device=dev)
+            self.d_ids0 = torch.zeros(B, 0, dtype=i32, device=dev)
+            self.s_target = torch.cuda.Stream(dev)
+            self.s_draft = torch.cuda.Stream(dev) if dual_stream else self.s_target
+            torch.cuda.synchronize(dev)
+        self.slots: dict[int, int] = {}
+        self.free_slots = list(range(max_requests - 1, -1, -1))
+        self.pending_k: dict[int, int] = {}
+        self.stats = {"draft_ms": 0.0, "verify_ms": 0.0, "prefill_ms": 0.0, "steps": 0}
+        self._state: EngineState | None = None
+
+    # ------------------------------------------------------------------
+    # Backend protocol
+    # ------------------------------------------------------------------
+    def bind(self, state: EngineState) -> None:
+        if state.config.block_size != self.block_size:
+            raise ConfigError(f"SimConfig.block_size {state.config.block_size} != KV cache "
+                              f"block size {self.block_size}")
+        if state.config.k > self.k_max or any(k > self.k_max for k in state.config.k_overrides):
+            raise ConfigError(f"draft depth exceeds k_max={self.k_max}")
+        need = [r for r in state.requests.values() if r.prompt_ids is None]
+        if need:
+            attach_prompt_ids(need, self.dshape.vocab, self.seed)
+        for r in state.requests.values():
+            if r.prompt_len < 2:
+                raise ConfigError(f"request {r.id}: GPU backend needs prompt_len >= 2")
+            if len(r.prompt_ids) != r.prompt_len:
+                raise ConfigError(f"request {r.id}: prompt_ids length != prompt_len")
+            if r.prompt_len + r.target_output_len + self.k_max + 1 > self.max_out:
+                raise ConfigError(f"request {r.id} exceeds max_seq_len={self.max_out}")
+        self._state = state
+
+    def estimate(self, state, plan):
+        return 0.0, 0.0, 0.0
+
+    def planned_commit(self, state, rid, k_i, draft_time):
+        return min(k_i + 1, state.requests[rid].remaining)
+
+    def commit(self, state, rid, tokens):
+        # roll back the reserved-but-rejected tail: keep blocks for the
+        # committed tokens only (the reference's exact-size invariant)
+        state.kv.trim_to_written(rid)
+
+    def retire(self, state, rid):
+        s = self.slots.pop(rid, None)
+        if s is None:
+            return
+        req = state.requests[rid]
+        n = req.generated
+        req.output_ids = self.outputs[s, :n].cpu().tolist()
+        self.free_slots.append(s)
+        self.pending_k.pop(rid, None)
+
+    # ------------------------------------------------------------------
+    # helpers
+    # ------------------------------------------------------------------
+    def _kv_slot(self, state, rid: int, pos: int) -> int:
+        blocks = state.kv.blocks_of(rid)
+        bi = pos // self.block_size
+        if bi >= len(blocks):
+            raise KVError(f"request {rid}: KV position {pos} beyond its {len(blocks)} blocks")
+        return blocks[bi] * self.block_size + pos % self.block_size
+
+    def _upload_block_table(self, state) -> None:
+        bt = self.block_table_host.numpy()
+        bt[:] = 0
+        for rid, s in self.slots.items():
+            blocks = state.kv.blocks_of(rid)
+            if len(blocks) > self.max_blocks:
+                raise KVError(f"request {rid}: {len(blocks)} blocks > max {self.max_blocks}")
+            bt[s, :len(blocks)] = blocks
+        self.block_table.copy_(self.block_table_host, non_blocking=True)
+
+    def _admit(self, state, ids) -> None:
+        """Assign slots and initialise slot tokens for new requests."""
+        n = len(ids)
+        idx = np.empty(3 * n, dtype=np.int32)
+        val = np.empty(3 * n, dtype=np.int32)
+        for i, rid in enumerate(ids):
+            if not self.free_slots:
+                raise ProtocolError("GpuBackend: out of request slots")
+            s = self.free_slots.pop()
+            self.slots[rid] = s
+            p = state.requests[rid].prompt_ids
+            idx[3 * i:3 * i + 3] = (s * self.ldt, s * self.ldt + 1, -1)
+            val[3 * i:3 * i + 3] = (p[-2], p[-1], 0)
+        dev = self.device
+        stage = torch.from_numpy(np.concatenate([idx, val])).pin_memory().to(dev,
+                                                                            non_blocking=True)
+        st = torch.cuda.current_stream(dev).cuda_stream
+        lib = native.load()
+        native.check(lib.psd_index_copy_i32(self.slot_tok.data_ptr(), stage.data_ptr(),
+                                            stage[3 * n:].data_ptr(), None, 3 * n, st),
+                     "slot init")
+        sl = torch.tensor([self.slots[r] for r in ids], dtype=torch.int64)
+        self.generated[sl.to(dev)] = 0
+
+    def _prefill(self, state, ids, fwd: Forward, logits_model: str) -> None:
+        """Prompt tokens 0..p-2 of each new request through one model."""
+        chunks, cur, cur_tok = [], [], 0
+        for rid in ids:
+            n = state.requests[rid].prompt_len - 1
+            if cur and cur_tok + n > self.prefill_chunk:
+                chunks.append(cur)
+                cur, cur_tok = [], 0
+            cur.append(rid)
+            cur_tok += n
+        if cur:
+            chunks.append(cur)
+        for chunk in chunks:
+            toks, pos, slots = [], [], []
+            seq_slot, q_start, q_len, q_pos0, kv_len = [], [], [], [], []
+            for rid in chunk:
+                req = state.requests[rid]
+                n = req.prompt_len - 1
+                q_start.append(len(toks))
+                toks.extend(req.prompt_ids[:n])
+                pos.extend(range(n))
+                slots.extend(self._kv_slot(state, rid, p) for p in range(n))
+                seq_slot.append(self.slots[rid])
+                q_len.append(n)
+                q_pos0.append(0)
+                kv_len.append(n)
+            if len(toks) > fwd.max_tokens:
+                raise ConfigError("prompt longer than the prefill chunk")
+            fwd.begin()
+            fwd.stage(0, {"tokens": np.asarray(toks, np.int32),
+                          "positions": np.asarray(pos, np.int32),
+                          "slots": np.asarray(slots, np.int32),
+                          "seq_slot": np.asarray(seq_slot, np.int32),
+                          "q_start": np.asarray(q_start, np.int32),
+                          "q_len": np.asarray(q_len, np.int32),
+                          "q_pos0": np.asarray(q_pos0, np.int32),
+                          "kv_len": np.asarray(kv_len, np.int32)})
+            fwd.upload(1)
+            fwd.run(len(toks), len(chunk), max(q_len), 0, None)
+
+    def _draft_loop(self, state, ids, quotas) -> None:
+        """k-step draft decode for the rows in ``ids`` (k_i = quotas[rid])."""
+        rows = [(rid, self.slots[rid], state.requests[rid].prompt_len +
+                 state.requests[rid].generated, quotas[rid]) for rid in ids if quotas[rid] > 0]
+        for rid in ids:
+            self.pending_k[rid] = quotas[rid]
+        if not rows:
+            return
+        n = len(rows)
+        kmax = max(r[3] for r in rows)
+        fwd = self.dfwd
+        ldt = self.ldt
+        fwd.begin()
+        for i in range(kmax):
+            if i == 0:
+                gather = np.empty(2 * n, np.int32)
+                pos = np.empty(2 * n, np.int32)
+                slots = np.empty(2 * n, np.int32)
+                for r, (rid, s, L, k) in enumerate(rows):
+                    gather[2 * r:2 * r + 2] = (s * ldt, s * ldt + 1)
+                    pos[2 * r:2 * r + 2] = (L - 2, L - 1)
+                    slots[2 * r] = self._kv_slot(state, rid, L - 2)
+                    slots[2 * r + 1] = self._kv_slot(state, rid, L - 1)
+                arrays = {
+                    "gather_src": gather, "positions": pos, "slots": slots,
+                    "seq_slot": np.asarray([s for _, s, _, _ in rows], np.int32),
+                    "q_start": np.arange(0, 2 * n, 2, dtype=np.int32),
+                    "q_len": np.full(n, 2, np.int32),
+                    "q_pos0": np.asarray([L - 2 for _, _, L, _ in rows], np.int32),
+                    "kv_len": np.asarray([L for _, _, L, _ in rows], np.int32),
+                    "logit_rows": np.arange(1, 2 * n, 2, dtype=np.int32),
+                    "scatter_dst": np.asarray([s * ldt + 2 for _, s, _, _ in rows], np.int32),
+                }
+            else:
+                act = [i < k for _, _, _, k in rows]
+                arrays = {
+                    "gather_src": np.asarray([s * ldt + 2 + i - 1 for _, s, _, _ in rows],
+                                             np.int32),
+                    "positions": np.asarray([L - 1 + i for _, _, L, _ in rows], np.int32),
+                    "slots": np.asarray([self._kv_slot(state, rid, L - 1 + i) if a else -1
+                                         for (rid, _, L, _), a in zip(rows, act)], np.int32),
+                    "seq_slot": np.asarray([s for _, s, _, _ in rows], np.int32),
+                    "q_start": np.arange(n, dtype=np.int32),
+                    "q_len": np.ones(n, np.int32),
+                    "q_pos0": np.asarray([L - 1 + i if a else 0
+                                          for (_, _, L, _), a in zip(rows, act)], np.int32),
+                    "kv_len": np.asarray([L + i if a else 1
+                                          for (_, _, L, _), a in zip(rows, act)], np.int32),
+                    "logit_rows": np.arange(n, dtype=np.int32),
+                    "scatter_dst": np.asarray([s * ldt + 2 + i if a else -1
+                                               for (_, s, _, _), a in zip(rows, act)], np.int32),
+                }
+            fwd.stage(i, arrays)
+        fwd.upload(kmax)
+        lib = native.load()
+        st = torch.cuda.current_stream(self.device).cuda_stream
+        for i in range(kmax):
+            M = 2 * n if i == 0 else n
+            tok = fwd.view("tokens", i)
+            native.check(lib.psd_index_copy_i32(tok.data_ptr(), None, self.slot_tok.data_ptr(),
+                                                fwd.view("gather_src", i).data_ptr(), M, st),
+                         "draft gather")
+            fwd.run(M, n, 2 if i == 0 else 1, n, self.dlogits, self.dshape.vocab,
+                    bigram=(self.succ_d, self.beta_draft), set_index=i)
+            if self.mode == "greedy":
+                ops.verify_greedy(self.dlogits[:n].view(n, 1, -1), self.d_ids0[:n],
+                                  self.d_len0[:n], self.d_acc[:n], self.d_out[:n])
+            else:
+                raise ConfigError("sampling-mode draft loop not implemented yet")
+            native.check(lib.psd_index_copy_i32(self.slot_tok.data_ptr(),
+                                                fwd.view("scatter_dst", i).data_ptr(),
+                                                self.d_out.data_ptr(), None, n, st),
+                         "draft scatter")
+
+    def _verify(self, state, rows: list[VerifyRow]):
+        """Target forward over [last, d_1..d_k] per row + K1 + commit kernel.
+        Returns the device accepted-length tensor (n,) and kmax."""
+        n = len(rows)
+        kmax = max((r.k for r in rows), default=0)
+        K1 = kmax + 1
+        ldt = self.ldt
+        gather = np.empty(n * K1, np.int32)
+        pos = np.empty(n * K1, np.int32)
+        slots = np.empty(n * K1, np.int32)
+        seq_slot = np.empty(n, np.int32)
+        kv_len = np.empty(n, np.int32)
+        q_pos0 = np.empty(n, np.int32)
+        ids_src = np.empty(n * max(kmax, 1), np.int32)
+        for r, row in enumerate(rows):
+            rid = row.request_id
+            s = self.slots[rid]
+            req = state.requests[rid]
+            L = req.prompt_len + req.generated
+            k = row.k
+            if k != self.pending_k.get(rid, 0):
+                raise ProtocolError(f"request {rid}: verifying {k} drafts, device holds "
+                                    f"{self.pending_k.get(rid, 0)}")
+            for j in range(K1):
+                gather[r * K1 + j] = s * ldt + (1 if j == 0 or j > k else 1 + j)
+                pos[r * K1 + j] = L - 1 + j
+                slots[r * K1 + j] = self._kv_slot(state, rid, L - 1 + j) if j <= k else -1
+            for j in range(kmax):
+                ids_src[r * kmax + j] = s * ldt + 2 + j
+            seq_slot[r] = s
+            kv_len[r] = L + k
+            q_pos0[r] = L - 1
+        fwd = self.tfwd
+        fwd.begin()
+        fwd.stage(0, {"gather_src": gather, "positions": pos, "slots": slots,
+                      "seq_slot": seq_slot, "q_start": np.arange(0, n * K1, K1, dtype=np.int32),
+                      "q_len": np.full(n, K1, np.int32), "q_pos0": q_pos0, "kv_len": kv_len,
+                      "logit_rows": np.arange(n * K1, dtype=np.int32)})
+        fwd.upload(1)
+        vm = self.v_meta_host.numpy()
+        B = self.max_batch
+        vm[:n] = [r.k for r in rows]
+        vm[B:B + n] = seq_slot
+        vm[3 * B:3 * B + n * kmax] = ids_src[:n * kmax]
+        self.v_meta.copy_(self.v_meta_host, non_blocking=True)
+        lib = native.load()
+        st = torch.cuda.current_stream(self.device).cuda_stream
+        M = n * K1
+        native.check(lib.psd_index_copy_i32(fwd.view("tokens").data_ptr(), None,
+                                            self.slot_tok.data_ptr(),
+                                            fwd.view("gather_src").data_ptr(), M, st),
+                     "verify gather")
+        fwd.run(M, n, K1, M, self.tlogits, self.tshape.vocab,
+                bigram=(self.succ_t, self.beta_target))
+        v_len = self.v_meta[:n]
+        v_slot = self.v_meta[B:B + n]
+        v_ids = self.v_ids[:n, :kmax]
+        if kmax:
+            native.check(lib.psd_index_copy_i32(self.v_ids.data_ptr(), None,
+                                                self.slot_tok.data_ptr(),
+                                                self.v_meta[3 * B:].data_ptr(), n * kmax, st),
+                         "verify ids")
+            v_ids = self.v_ids.view(-1)[:n * kmax].view(n, kmax)
+        logits = self.tlogits[:M].view(n, K1, -1)
+        if self.mode == "greedy":
+            acc, out = ops.verify_greedy(logits, v_ids, v_len, self.d_acc[:n],
+                                         self._out_buf(n, K1))
+        else:
+            raise ConfigError("sampling-mode verify not implemented yet")
+        native.check(lib.psd_commit(acc.data_ptr(), out.data_ptr(), kmax, v_slot.data_ptr(), n,
+                                    self.generated.data_ptr(), self.slot_tok.data_ptr(), ldt,
+                                    self.outputs.data_ptr(), self.max_out, st), "commit")
+        return acc, kmax
+
+    def _out_buf(self, n, K1):
+        if not hasattr(self, "_vout") or self._vout.numel() < n * K1:
+            self._vout = torch.empty(self.max_batch * (self.k_max + 1), dtype=torch.int32,
+                                     device=self.device)
+        return self._vout[:n * K1].view(n, K1)
+
+    # ------------------------------------------------------------------
+    def execute(self, state: EngineState, plan: StepPlan, rows: list[VerifyRow]) -> StepResult:
+        dev = self.device
+        ts, ds = self.s_target, self.s_draft
+        ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+        e_start, e_pf_t, e_pf_d, e_sd, e_ov, e_v0, e_v1 = (ev() for _ in range(7))
+        t_host = time.perf_counter()
+        cur = torch.cuda.current_stream(dev)
+        cur.synchronize()
+        with torch.cuda.stream(ts):
+            e_start.record(ts)
+            if plan.prefill_ids:
+                self._admit(state, plan.prefill_ids)
+            self._upload_block_table(state)
+        ds.wait_stream(ts)
+        # prefill: target model on the target stream, draft model on the draft stream
+        with torch.cuda.stream(ts):
+            if plan.prefill_ids:
+                self._prefill(state, plan.prefill_ids, self.tfwd, "target")
+            e_pf_t.record(ts)
+        with torch.cuda.stream(ds):
+            if plan.prefill_ids:
+                self._prefill(state, plan.prefill_ids, self.dfwd, "draft")
+            e_pf_d.record(ds)
+            # serial drafts (startup target batch / fallback / SD batch)
+            self._draft_loop(state, plan.serial_draft_ids, plan.quotas)
+            e_sd.record(ds)
+        ts.wait_event(e_sd)
+        with torch.cuda.stream(ds):
+            # overlapped drafts of the skip batch
+            self._draft_loop(state, plan.overlap_draft_ids, plan.quotas)
+            e_ov.record(ds)
+        with torch.cuda.stream(ts):
+            e_v0.record(ts)
+            if rows:
+                acc, _ = self._verify(state, rows)
+                self.acc_host[:len(rows)].copy_(acc, non_blocking=True)
+            e_v1.record(ts)
+        e_v1.synchronize()
+        e_ov.synchronize()
+        accepted = {}
+        if rows:
+            a = self.acc_host.numpy()[:len(rows)]
+            for r, row in enumerate(rows):
+                if row.k > 0:
+                    accepted[row.request_id] = int(a[r])
+        for row in rows:
+            self.pending_k.pop(row.request_id, None)
+        prefill_ms = max(e_start.elapsed_time(e_pf_t), e_start.elapsed_time(e_pf_d))
+        serial_ms = e_pf_d.elapsed_time(e_sd)
+        overlap_ms = e_sd.elapsed_time(e_ov)
+        verify_ms = e_v0.elapsed_time(e_v1)
+        step_ms = max(e_start.elapsed_time(e_v1), e_start.elapsed_time(e_ov))
+        self.stats["steps"] += 1
+        self.stats["draft_ms"] += serial_ms + overlap_ms
+        self.stats["verify_ms"] += verify_ms
+        self.stats["prefill_ms"] += prefill_ms
+        self.stats["host_s"] = self.stats.get("host_s", 0.0) + (time.perf_counter() - t_host)
+        return StepResult(prefill_ms, serial_ms, overlap_ms, verify_ms, step_ms, accepted)

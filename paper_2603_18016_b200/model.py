@@ -1,0 +1,357 @@
+"""Llama / Qwen2-shaped decoder-only transformers on the C ABI (target verify
+forward and draft decode forward).
+
+The reference simulates these passes as virtual durations
+(``LatencyModel.duration``, pkg/src/specsim/request_model.py:92-117, charged
+at engine.py:338, 359-360, 378, 402, 429).  Here they are real: embedding ->
+L x [RMSNorm -> QKV GEMM -> RoPE + paged-KV write -> paged attention ->
+O GEMM (+residual) -> RMSNorm -> gate/up GEMM (+SiLU*up) -> down GEMM
+(+residual)] -> final RMSNorm on the logit rows -> LM-head GEMM (fp32 logits)
+-> synthetic-language bias.  Every step is one of our sm_100a kernels
+(include/psd.h); torch only allocates memory.
+
+Weights are random-init (no checkpoints offline): every matrix is
+``(u - 1/2) * span`` with u from splitmix64(seed_t, i) (uniform, std 0.02),
+norms are 1.  ``oracle/model.py`` regenerates the identical bf16 weights in
+numpy for the CPU reference forward.
+
+Synthetic language: random-init models agree on the next token with
+probability ~1/V, which would make speculative decoding degenerate.  Both
+models therefore add ``beta * onehot(successor[prev_token])`` to their logits
+(SURVEY.md §7 hard part 4, option (a)); ``beta_target`` sets how often the
+target's argmax follows the shared successor table, i.e. the acceptance rate.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import native
+from .errors import ConfigError
+
+__all__ = ["ModelShape", "PRESETS", "Transformer", "Forward", "successor_table",
+           "tensor_seed", "rope_inv_freq"]
+
+INIT_STD = 0.02
+INIT_SPAN = INIT_STD * math.sqrt(12.0)  # uniform(-span/2, span/2) has std 0.02
+
+
+@dataclass(frozen=True)
+class ModelShape:
+    name: str
+    vocab: int
+    hidden: int
+    layers: int
+    heads: int
+    kv_heads: int
+    head_dim: int
+    ffn: int
+    rope_theta: float
+    rope_scaling: tuple | None = None  # llama3: (factor, low, high, original_max)
+    tie_embeddings: bool = False
+    qkv_bias: bool = False
+    rms_eps: float = 1e-5
+
+    @property
+    def ffn_padded(self) -> int:
+        """FFN width padded to 64 (gate/up are packed per 64-row half tiles);
+        padded features have zero weights and contribute exactly 0."""
+        return (self.ffn + 63) // 64 * 64
+
+    @property
+    def qkv_out(self) -> int:
+        return (self.heads + 2 * self.kv_heads) * self.head_dim
+
+    def param_count(self) -> int:
+        h = self.hidden
+        per = h * self.qkv_out + self.heads * self.head_dim * h + 3 * h * self.ffn + 2 * h
+        emb = self.vocab * h * (1 if self.tie_embeddings else 2)
+        return self.layers * per + emb + h
+
+
+_L31 = (8.0, 1.0, 4.0, 8192)
+_L32 = (32.0, 1.0, 4.0, 8192)
+PRESETS: dict[str, ModelShape] = {
+    "llama-3.1-8b": ModelShape("llama-3.1-8b", 128256, 4096, 32, 32, 8, 128, 14336, 500000.0,
+                               _L31),
+    "llama-3.2-1b": ModelShape("llama-3.2-1b", 128256, 2048, 16, 32, 8, 64, 8192, 500000.0,
+                               _L32, tie_embeddings=True),
+    "llama-3.1-70b": ModelShape("llama-3.1-70b", 128256, 8192, 80, 64, 8, 128, 28672, 500000.0,
+                                _L31),
+    "qwen2.5-7b": ModelShape("qwen2.5-7b", 152064, 3584, 28, 28, 4, 128, 18944, 1000000.0,
+                             None, qkv_bias=True, rms_eps=1e-6),
+    "qwen2.5-0.5b": ModelShape("qwen2.5-0.5b", 151936, 896, 24, 14, 2, 64, 4864, 1000000.0,
+                               None, tie_embeddings=True, qkv_bias=True, rms_eps=1e-6),
+    # BASELINE config 1: tiny random-init pair
+    "tiny-target": ModelShape("tiny-target", 1024, 256, 4, 8, 2, 32, 688, 10000.0),
+    "tiny-draft": ModelShape("tiny-draft", 1024, 128, 2, 4, 2, 32, 344, 10000.0),
+}
+
+
+def rope_inv_freq(shape: ModelShape) -> np.ndarray:
+    """Rotary inverse frequencies (Llama-3 scaled where configured), float32."""
+    d = shape.head_dim
+    inv = 1.0 / (shape.rope_theta ** (np.arange(0, d, 2, dtype=np.float64) / d))
+    if shape.rope_scaling is not None:
+        factor, low, high, orig = shape.rope_scaling
+        wavelen = 2.0 * math.pi / inv
+        low_wl, high_wl = orig / low, orig / high
+        scaled = np.where(wavelen > low_wl, inv / factor, inv)
+        smooth = (orig / wavelen - low) / (high - low)
+        smoothed = (1.0 - smooth) * scaled / factor + smooth * scaled
+        medium = (wavelen >= high_wl) & (wavelen <= low_wl)
+        inv = np.where(medium, smoothed, scaled)
+    return inv.astype(np.float32)
+
+
+def tensor_seed(model_seed: int, layer: int, which: int) -> int:
+    """Per-tensor init seed (also used by oracle/model.py)."""
+    return (model_seed * 1_000_003 + (layer + 1) * 101 + which) & 0x7FFFFFFF
+
+
+def successor_table(vocab: int, draft_vocab: int, seed: int) -> np.ndarray:
+    """The synthetic language: next token = successor[prev] (a permutation of
+    the shared vocabulary; ids past it wrap)."""
+    v = min(vocab, draft_vocab)
+    perm = np.random.Generator(np.random.Philox(key=[seed, 0x5EC])).permutation(v)
+    succ = np.empty(vocab, dtype=np.int32)
+    succ[:v] = perm
+    succ[v:] = perm[np.arange(v, vocab) % v]
+    return succ
+
+
+def _stream_ptr(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _chk(rc: int, what: str) -> None:
+    if rc != 0:
+        native.check(rc, what)
+
+
+class Transformer:
+    """Device weights + paged KV cache of one model."""
+
+    # which-ids for tensor_seed
+    W_QKV, W_O, W_GATE, W_UP, W_DOWN, W_EMB, W_LM, B_QKV = range(8)
+
+    def __init__(self, shape: ModelShape, device: torch.device, seed: int, num_blocks: int,
+                 block_size: int = 16, max_blocks_per_seq: int = 64) -> None:
+        if shape.qkv_out % 128 or shape.hidden % 128 or shape.vocab % 128:
+            raise ConfigError(f"{shape.name}: GEMM output dims must be multiples of 128")
+        self.shape = shape
+        self.device = device
+        self.seed = seed
+        self.block_size = block_size
+        self.num_blocks = num_blocks
+        self.max_blocks = max_blocks_per_seq
+        lib = native.load()
+        self._lib = lib
+        s = shape
+        H, F, Fp = s.hidden, s.ffn, s.ffn_padded
+        bf = torch.bfloat16
+        dev = device
+
+        def fill(t: torch.Tensor, tseed: int) -> torch.Tensor:
+            _chk(lib.psd_fill_uniform_bf16(t.data_ptr(), t.numel(), tseed, INIT_SPAN,
+                                           _stream_ptr(dev)), "psd_fill_uniform_bf16")
+            return t
+
+        self.layers = []
+        for li in range(s.layers):
+            wqkv = fill(torch.empty(s.qkv_out, H, dtype=bf, device=dev),
+                        tensor_seed(seed, li, self.W_QKV))
+            wo = fill(torch.empty(H, s.heads * s.head_dim, dtype=bf, device=dev),
+                      tensor_seed(seed, li, self.W_O))
+            gate = torch.zeros(Fp, H, dtype=bf, device=dev)
+            up = torch.zeros(Fp, H, dtype=bf, device=dev)
+            fill(gate[:F], tensor_seed(seed, li, self.W_GATE))
+            fill(up[:F], tensor_seed(seed, li, self.W_UP))
+            # pack per 128-row tile: 64 gate rows then the matching 64 up rows
+            wgu = torch.cat([gate.view(Fp // 64, 64, H), up.view(Fp // 64, 64, H)], dim=1)
+            wgu = wgu.reshape(2 * Fp, H).contiguous()
+            del gate, up
+            down = torch.zeros(H, Fp, dtype=bf, device=dev)
+            dtmp = fill(torch.empty(H, F, dtype=bf, device=dev), tensor_seed(seed, li, self.W_DOWN))
+            down[:, :F] = dtmp
+            del dtmp
+            bias = None
+            if s.qkv_bias:
+                bias = fill(torch.empty(s.qkv_out, dtype=bf, device=dev),
+                            tensor_seed(seed, li, self.B_QKV))
+            self.layers.append({
+                "attn_norm": torch.ones(H, dtype=bf, device=dev),
+                "wqkv": wqkv, "wo": wo,
+                "mlp_norm": torch.ones(H, dtype=bf, device=dev),
+                "wgu": wgu, "wdown": down, "bqkv": bias,
+            })
+        self.embed = fill(torch.empty(s.vocab, H, dtype=bf, device=dev),
+                          tensor_seed(seed, -1, self.W_EMB))
+        self.lm_head = self.embed if s.tie_embeddings else fill(
+            torch.empty(s.vocab, H, dtype=bf, device=dev), tensor_seed(seed, -1, self.W_LM))
+        self.final_norm = torch.ones(H, dtype=bf, device=dev)
+        self.inv_freq = torch.from_numpy(rope_inv_freq(s)).to(dev)
+        # paged KV cache: [layers, 2, blocks * block_size, Hkv, D]
+        self.kv = torch.zeros(s.layers, 2, num_blocks * block_size, s.kv_heads, s.head_dim,
+                              dtype=bf, device=dev)
+        self.block_table = torch.zeros(0, dtype=torch.int32, device=dev)
+
+    def kv_bytes_per_block(self) -> int:
+        s = self.shape
+        return s.layers * 2 * self.block_size * s.kv_heads * s.head_dim * 2
+
+
+META_FIELDS = ("tokens", "positions", "slots", "seq_slot", "q_start", "q_len", "q_pos0",
+               "kv_len", "logit_rows", "gather_src", "scatter_dst")
+
+
+class Forward:
+    """One model's forward over a batch described by device metadata.
+
+    Per token: tokens, positions, slots (KV write slot, -1 = none).  Per
+    sequence: seq_slot (block-table row), q_start, q_len, q_pos0, kv_len.
+    logit_rows: hidden-state rows that get logits.  gather_src / scatter_dst:
+    device token routing for the draft loop (see GpuBackend).  ``sets``
+    independent metadata sets live in one packed int32 buffer, uploaded with a
+    single copy, so a k-step draft loop needs one host->device transfer.
+    """
+
+    def __init__(self, model: Transformer, max_tokens: int, max_seqs: int,
+                 max_logit_rows: int, block_table: torch.Tensor, sets: int = 1,
+                 workspace_bytes: int = 64 << 20) -> None:
+        s = model.shape
+        dev = model.device
+        self.model = model
+        self.block_table = block_table  # [slots, max_blocks] int32, shared with the backend
+        self.max_tokens, self.max_seqs, self.max_logit_rows = max_tokens, max_seqs, max_logit_rows
+        bf = torch.bfloat16
+        T = max_tokens
+        self.x = torch.empty(T, s.hidden, dtype=bf, device=dev)
+        self.xn = torch.empty(T, s.hidden, dtype=bf, device=dev)
+        self.qkv = torch.empty(T, s.qkv_out, dtype=bf, device=dev)
+        self.q = torch.empty(T, s.heads * s.head_dim, dtype=bf, device=dev)
+        self.attn = torch.empty(T, s.heads * s.head_dim, dtype=bf, device=dev)
+        self.act = torch.empty(T, s.ffn_padded, dtype=bf, device=dev)
+        self.xf = torch.empty(max_logit_rows, s.hidden, dtype=bf, device=dev)
+        self.prev = torch.empty(max_logit_rows, dtype=torch.int32, device=dev)
+        self.ws = torch.empty(workspace_bytes, dtype=torch.uint8, device=dev)
+        sizes = {"tokens": T, "positions": T, "slots": T, "seq_slot": max_seqs,
+                 "q_start": max_seqs, "q_len": max_seqs, "q_pos0": max_seqs, "kv_len": max_seqs,
+                 "logit_rows": max_logit_rows, "gather_src": T, "scatter_dst": max_logit_rows}
+        self._offsets = {}
+        o = 0
+        for name in META_FIELDS:
+            self._offsets[name] = (o, sizes[name])
+            o += sizes[name]
+        self.set_size = o
+        self.sets = sets
+        self.meta = torch.zeros(sets, o, dtype=torch.int32, device=dev)
+        # ring of pinned staging buffers: an async H2D copy reads its buffer
+        # when it executes, so a buffer is rewritten only after its copy ran
+        self.ring = 4
+        self.meta_host = torch.zeros(self.ring, sets, o, dtype=torch.int32).pin_memory()
+        self._host_np = self.meta_host.numpy()
+        self._events = [None] * self.ring
+        self._cur = 0
+
+    def view(self, name: str, set_index: int = 0) -> torch.Tensor:
+        o, n = self._offsets[name]
+        return self.meta[set_index, o:o + n]
+
+    def begin(self) -> None:
+        """Start staging a new upload (advances the staging ring)."""
+        self._cur = (self._cur + 1) % self.ring
+        ev = self._events[self._cur]
+        if ev is not None:
+            ev.synchronize()
+
+    def stage(self, set_index: int, arrays: dict[str, np.ndarray]) -> None:
+        """Write host metadata (int32) for one set into pinned staging."""
+        host = self._host_np[self._cur, set_index]
+        for name, arr in arrays.items():
+            o, n = self._offsets[name]
+            if len(arr) > n:
+                raise ConfigError(f"forward metadata {name}: {len(arr)} > capacity {n}")
+            host[o:o + len(arr)] = arr
+
+    def upload(self, n_sets: int = 1) -> None:
+        """Copy staged sets 0..n_sets-1 to the device on the current stream."""
+        self.meta[:n_sets].copy_(self.meta_host[self._cur, :n_sets], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._events[self._cur] = ev
+
+    def run(self, n_tokens: int, n_seqs: int, max_q_len: int, n_logit_rows: int,
+            logits: torch.Tensor | None, logits_ld: int = 0, bigram=None,
+            set_index: int = 0) -> None:
+        """Enqueue the forward on the current stream.  ``tokens`` may be
+        filled on device beforehand (draft loop); ``logits`` (fp32, row pitch
+        ``logits_ld``) receives the LM-head output of ``logit_rows``."""
+        m = self.model
+        s = m.shape
+        lib = m._lib
+        dev = m.device
+        st = _stream_ptr(dev)
+        M = n_tokens
+        v = {name: self.view(name, set_index) for name in META_FIELDS}
+        H = s.hidden
+        _chk(lib.psd_embed(v["tokens"].data_ptr(), M, m.embed.data_ptr(), H, self.x.data_ptr(),
+                           st), "psd_embed")
+        kv_stride = m.kv.stride(1) * m.kv.element_size()
+        scale = 1.0 / math.sqrt(s.head_dim)
+        ws, wsn = self.ws.data_ptr(), self.ws.numel()
+        for li, L in enumerate(m.layers):
+            kc = m.kv[li, 0]
+            vc = m.kv[li, 1]
+            _chk(lib.psd_rmsnorm(self.x.data_ptr(), H, None, L["attn_norm"].data_ptr(),
+                                 self.xn.data_ptr(), H, M, H, s.rms_eps, st), "psd_rmsnorm")
+            _chk(lib.psd_gemm_bf16(self.xn.data_ptr(), H, M, H, L["wqkv"].data_ptr(), H,
+                                   s.qkv_out, self.qkv.data_ptr(), s.qkv_out, native.EPI_BF16,
+                                   None, 0, 0, ws, wsn, st), "gemm qkv")
+            _chk(lib.psd_rope_kv(self.qkv.data_ptr(), M, s.heads, s.kv_heads, s.head_dim,
+                                 v["positions"].data_ptr(), v["slots"].data_ptr(),
+                                 m.inv_freq.data_ptr(),
+                                 L["bqkv"].data_ptr() if L["bqkv"] is not None else None,
+                                 self.q.data_ptr(), kc.data_ptr(), vc.data_ptr(), st), "rope_kv")
+            _chk(lib.psd_attention(self.q.data_ptr(), kc.data_ptr(), vc.data_ptr(),
+                                   self.block_table.data_ptr(), self.block_table.shape[1],
+                                   v["seq_slot"].data_ptr(), v["q_start"].data_ptr(),
+                                   v["q_len"].data_ptr(), v["q_pos0"].data_ptr(),
+                                   v["kv_len"].data_ptr(), n_seqs, max_q_len, s.heads,
+                                   s.kv_heads, s.head_dim, m.block_size, scale,
+                                   self.attn.data_ptr(), st), "attention")
+            _chk(lib.psd_gemm_bf16(self.attn.data_ptr(), s.heads * s.head_dim, M,
+                                   s.heads * s.head_dim, L["wo"].data_ptr(), s.heads * s.head_dim,
+                                   H, self.x.data_ptr(), H, native.EPI_RESID, self.x.data_ptr(),
+                                   H, 0, ws, wsn, st), "gemm o")
+            _chk(lib.psd_rmsnorm(self.x.data_ptr(), H, None, L["mlp_norm"].data_ptr(),
+                                 self.xn.data_ptr(), H, M, H, s.rms_eps, st), "psd_rmsnorm")
+            _chk(lib.psd_gemm_bf16(self.xn.data_ptr(), H, M, H, L["wgu"].data_ptr(), H,
+                                   2 * s.ffn_padded, self.act.data_ptr(), s.ffn_padded,
+                                   native.EPI_SILU, None, 0, 0, ws, wsn, st), "gemm gate/up")
+            _chk(lib.psd_gemm_bf16(self.act.data_ptr(), s.ffn_padded, M, s.ffn_padded,
+                                   L["wdown"].data_ptr(), s.ffn_padded, H, self.x.data_ptr(), H,
+                                   native.EPI_RESID, self.x.data_ptr(), H, 0, ws, wsn, st),
+                 "gemm down")
+        if n_logit_rows == 0 or logits is None:
+            return
+        R = n_logit_rows
+        _chk(lib.psd_rmsnorm(self.x.data_ptr(), H, v["logit_rows"].data_ptr(),
+                             m.final_norm.data_ptr(), self.xf.data_ptr(), H, R, H, s.rms_eps, st),
+             "final norm")
+        ld = logits_ld or s.vocab
+        _chk(lib.psd_gemm_bf16(self.xf.data_ptr(), H, R, H, m.lm_head.data_ptr(), H, s.vocab,
+                               logits.data_ptr(), ld, native.EPI_F32, None, 0, 0, ws, wsn, st),
+             "gemm lm_head")
+        if bigram is not None:
+            succ, beta = bigram
+            if beta != 0.0:
+                # the token that produced each logit row is its predecessor
+                _chk(lib.psd_index_copy_i32(self.prev.data_ptr(), None, v["tokens"].data_ptr(),
+                                            v["logit_rows"].data_ptr(), R, st), "prev tokens")
+                _chk(lib.psd_bigram_bias(logits.data_ptr(), ld, self.prev.data_ptr(), R,
+                                         succ.data_ptr(), s.vocab, float(beta), st), "bigram")

@@ -30,7 +30,21 @@ SIGNATURES: dict[str, tuple] = {
     "psd_verify_greedy": (_i, [_p, _i64, _i64, _i, _p, _p, _i, _i, _p, _p, _p, _sz, _p]),
     "psd_verify_sample": (_i, [_p, _i64, _i64, _i, _p, _i64, _i64, _i, _p, _p, _p, _f, _i, _i,
                                _p, _p, _p, _sz, _p]),
+    "psd_gemm_plan": (_i, [_i, _i, _i, _i, _i, _c.POINTER(_i), _c.POINTER(_sz)]),
+    "psd_gemm_bf16": (_i, [_p, _i, _i, _i, _p, _i, _i, _p, _i, _i, _p, _i, _i, _p, _sz, _p]),
+    "psd_embed": (_i, [_p, _i, _p, _i, _p, _p]),
+    "psd_rmsnorm": (_i, [_p, _i, _p, _p, _p, _i, _i, _i, _f, _p]),
+    "psd_rope_kv": (_i, [_p, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "psd_attention": (_i, [_p, _p, _p, _p, _i, _p, _p, _p, _p, _p, _i, _i, _i, _i, _i, _i, _f,
+                           _p, _p]),
+    "psd_bigram_bias": (_i, [_p, _i64, _p, _i, _p, _i, _f, _p]),
+    "psd_philox_uniforms": (_i, [_c.c_uint64, _p, _p, _i, _i, _p, _p]),
+    "psd_commit": (_i, [_p, _p, _i, _p, _i, _p, _p, _i, _p, _i, _p]),
+    "psd_index_copy_i32": (_i, [_p, _p, _p, _p, _i, _p]),
+    "psd_fill_uniform_bf16": (_i, [_p, _sz, _c.c_uint64, _f, _p]),
 }
+
+EPI_BF16, EPI_F32, EPI_RESID, EPI_SILU = 0, 1, 2, 3
 
 _lib = None
 

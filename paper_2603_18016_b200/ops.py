@@ -12,7 +12,7 @@ import torch
 from . import native
 from .errors import ConfigError
 
-__all__ = ["verify_greedy", "verify_sample"]
+__all__ = ["gemm", "gemm_plan", "verify_greedy", "verify_sample"]
 
 _workspaces: dict[tuple, torch.Tensor] = {}
 
@@ -121,3 +121,54 @@ def verify_sample(target_logits: torch.Tensor, draft_logits: torch.Tensor,
         out_tokens.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(dev)),
         "psd_verify_sample")
     return accepted_len, out_tokens
+
+
+# ---------------------------------------------------------------------------
+# K2: tcgen05 GEMM
+# ---------------------------------------------------------------------------
+def gemm_plan(M: int, N: int, K: int, epi: int = 0, splits: int = 0) -> tuple[int, int]:
+    """(splits, workspace bytes) the GEMM will use for this shape."""
+    import ctypes
+    lib = native.load()
+    s = ctypes.c_int()
+    w = ctypes.c_size_t()
+    native.check(lib.psd_gemm_plan(M, N, K, epi, splits, ctypes.byref(s), ctypes.byref(w)),
+                 "psd_gemm_plan")
+    return s.value, w.value
+
+
+def gemm(x: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None,
+         epi: int = 0, residual: torch.Tensor | None = None, splits: int = 0,
+         workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """out = epi(x @ w.T) on tcgen05.  x [M, K] bf16, w [N, K] bf16 (row-major).
+
+    epi: native.EPI_BF16 / EPI_F32 / EPI_RESID (out = acc + residual) /
+    EPI_SILU (w packed gate/up per 128-row tile, out [M, N/2]).
+    """
+    _check(x, "x", torch.bfloat16, 2)
+    _check(w, "w", torch.bfloat16, 2)
+    M, K = x.shape
+    N = w.shape[0]
+    if w.shape[1] != K or x.stride(1) != 1 or w.stride(1) != 1:
+        raise ConfigError("gemm: x [M, K], w [N, K] with unit inner stride")
+    n_out = N // 2 if epi == native.EPI_SILU else N
+    odt = torch.float32 if epi == native.EPI_F32 else torch.bfloat16
+    if out is None:
+        out = torch.empty(M, n_out, dtype=odt, device=x.device)
+    if out.dtype != odt or out.shape[0] != M or out.shape[1] != n_out or out.stride(1) != 1:
+        raise ConfigError(f"gemm: out must be [{M}, {n_out}] {odt}")
+    if epi == native.EPI_RESID:
+        if residual is None or residual.dtype != torch.bfloat16 or residual.stride(1) != 1:
+            raise ConfigError("gemm: EPI_RESID needs a bf16 residual [M, N]")
+    nsplit, need = gemm_plan(M, N, K, epi, splits)
+    if need and (workspace is None or workspace.numel() * workspace.element_size() < need):
+        workspace = torch.empty(need, dtype=torch.uint8, device=x.device)
+    lib = native.load()
+    native.check(lib.psd_gemm_bf16(
+        x.data_ptr(), x.stride(0), M, K, w.data_ptr(), w.stride(0), N, out.data_ptr(),
+        out.stride(0), epi, residual.data_ptr() if residual is not None else None,
+        residual.stride(0) if residual is not None else 0, splits,
+        workspace.data_ptr() if workspace is not None else None,
+        (workspace.numel() * workspace.element_size()) if workspace is not None else 0,
+        _stream_ptr(x.device)), "psd_gemm_bf16")
+    return out

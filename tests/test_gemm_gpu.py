@@ -1,0 +1,68 @@
+"""K2 (tcgen05 GEMM) vs a torch fp32 reference of the same op.
+
+Shapes cover the verify (M = B(k+1)) and draft (M = B) token counts of the
+BASELINE configs, split-K and no split, every epilogue.  Tolerance: bf16
+output rounding + fp32 accumulation-order differences (rtol 1e-2 on values
+of O(1), atol scaled by sqrt(K)).
+"""
+
+import pytest
+import torch
+
+from paper_2603_18016_b200 import native, ops
+
+pytestmark = pytest.mark.gpu
+
+
+def _ref(x, w):
+    return x.float() @ w.float().T
+
+
+def _close(got, ref, K):
+    err = (got.float() - ref).abs().max().item()
+    scale = ref.abs().max().item()
+    assert err <= 1e-2 * scale + 1e-3, (err, scale)
+
+
+@pytest.mark.parametrize("M,N,K", [(32, 3072, 2048), (192, 6144, 4096), (160, 4608, 3584),
+                                   (1, 128, 64), (37, 256, 192), (320, 2560, 8192),
+                                   (64, 1024, 1000), (700, 512, 512), (192, 8192, 4096), (32, 128256, 2048)])
+@pytest.mark.parametrize("splits", [0, 1])
+def test_gemm_bf16(cuda_device, M, N, K, splits):
+    g = torch.Generator(device=cuda_device).manual_seed(M * 7 + N + K)
+    x = torch.randn(M, K, device=cuda_device, generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device=cuda_device, generator=g) * 0.05).to(torch.bfloat16)
+    y = ops.gemm(x, w, splits=splits)
+    torch.cuda.synchronize()
+    _close(y, _ref(x, w), K)
+
+
+@pytest.mark.parametrize("splits", [0, 1])
+def test_gemm_f32_and_resid(cuda_device, splits):
+    g = torch.Generator(device=cuda_device).manual_seed(5)
+    M, N, K = 96, 2048, 2048
+    x = torch.randn(M, K, device=cuda_device, generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device=cuda_device, generator=g) * 0.05).to(torch.bfloat16)
+    y = ops.gemm(x, w, epi=native.EPI_F32, splits=splits)
+    torch.cuda.synchronize()
+    _close(y, _ref(x, w), K)
+    r = torch.randn(M, N, device=cuda_device, generator=g).to(torch.bfloat16)
+    r0 = r.clone()
+    ops.gemm(x, w, out=r, epi=native.EPI_RESID, residual=r, splits=splits)  # in place
+    torch.cuda.synchronize()
+    _close(r, _ref(x, w) + r0.float(), K)
+
+
+@pytest.mark.parametrize("M,splits", [(32, 0), (192, 1), (192, 0)])
+def test_gemm_silu_mul(cuda_device, M, splits):
+    g = torch.Generator(device=cuda_device).manual_seed(9)
+    F, K = 1024, 2048
+    x = torch.randn(M, K, device=cuda_device, generator=g).to(torch.bfloat16)
+    wg = (torch.randn(F, K, device=cuda_device, generator=g) * 0.05).to(torch.bfloat16)
+    wu = (torch.randn(F, K, device=cuda_device, generator=g) * 0.05).to(torch.bfloat16)
+    packed = torch.cat([wg.view(F // 64, 64, K), wu.view(F // 64, 64, K)], dim=1).reshape(2 * F, K)
+    y = ops.gemm(x, packed.contiguous(), epi=native.EPI_SILU, splits=splits)
+    torch.cuda.synchronize()
+    gt = _ref(x, wg)
+    ref = torch.nn.functional.silu(gt) * _ref(x, wu)
+    _close(y, ref, K)

@@ -20,15 +20,14 @@ from tests import _gen
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "verify_golden.json")
 
 
-def test_canonical_exp_accuracy_and_edges():
-    assert ov.exp(0.0) == 1.0
-    assert ov.exp(-87.5) == 0.0
-    assert ov.exp(float("-inf")) == 0.0
-    xs = np.linspace(-87.0, 0.0, 20001, dtype=np.float32)
-    got = np.array([ov.exp(float(x)) for x in xs], dtype=np.float64)
-    ref = np.exp(xs.astype(np.float64))
-    rel = np.abs(got - ref) / ref
-    assert rel.max() < 2e-5  # |x| * 2^-24 argument rounding dominates at x=-87
+def test_canonical_exp2_accuracy_and_edges():
+    assert ov.exp2(0.0) == 1.0
+    assert ov.exp2(-1.0) == 0.5
+    assert ov.exp2(float("-inf")) == ov.exp2(-125.0) == 2.0 ** -125
+    ts = np.linspace(-125.0, 0.0, 20001, dtype=np.float32)
+    got = np.array([ov.exp2(float(t)) for t in ts], dtype=np.float64)
+    ref = np.exp2(ts.astype(np.float64))
+    assert (np.abs(got - ref) / ref).max() < 5e-7
 
 
 @pytest.mark.parametrize("n", [1, 4, 1000, 8192, 8196, 128256])
