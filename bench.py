@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""PSD output tokens/s vs sequential SD on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Workload (BASELINE config 2): Llama-3.2-1B draft / Llama-3.1-8B target shapes,
+random-init bf16 weights (no checkpoints offline), synthetic prompts, two
+batches of 32 requests (m=32), k=5, prompt 128, output 256, greedy, one GPU
+per replica with draft and verify on separate CUDA streams.  One bench *step*
+is one complete pass of the hot path over the workload: all 64 requests from
+admission to their last token through the public API ``run(config,
+workload, backend=GpuBackend)``.
+
+Multi-GPU: one process per GPU, each an independent PSD replica on its own
+64 requests (requests shard with no data-path collective) -> "scaling":
+"weak"; time is the max over ranks.
+
+Keys beyond the base contract: ``sd`` (same workload, mode standard-sd with
+sd_batch_factor 2 = one batch of 64), ``psd_vs_sd``, ``mean_accepted_len``,
+``draft_hidden_frac``, ``verify_kernel`` (K1 at the workload shape),
+``roofline`` (dominant kernel: the verify gate/up GEMM), ``cpu_baseline``
+(CPU oracle PSD on a bounded sample, rank 0, N=1).
+``--impl reference`` times the CPU oracle (the reference has no CPU
+implementation of token-level PSD; oracle/ is its restatement) on the same
+workload shapes, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG = dict(target="llama-3.1-8b", draft="llama-3.2-1b", m=32, n_requests=64, k=5,
+           prompt=128, output=256)
+BETA_TARGET = 7.0
+BETA_DRAFT = 16.0
+METRIC = "PSD output tok/s vs sequential SD, mean accepted len; verify-kernel HBM GB/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return p["hbm_gbs"], p.get("bf16_tflops", 1682.3), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, 1590.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region."""
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _workload(seed: int):
+    from paper_2603_18016_b200 import make_requests
+    return make_requests([CFG["output"]] * CFG["n_requests"], prompt_len=CFG["prompt"])
+
+
+def _config(mode: str):
+    from paper_2603_18016_b200 import SimConfig
+    return SimConfig(mode=mode, m=CFG["m"], k=CFG["k"],
+                     sd_batch_factor=2 if mode == "standard-sd" else 1)
+
+
+def _time_kernel(fn, iters: int = 20) -> float:
+    """Average device time (ms) of fn() on the current stream, CUDA events."""
+    import torch
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / iters
+
+
+def kernel_rooflines(backend, hbm_peak: float) -> tuple[dict, dict]:
+    """Dominant kernel (verify-forward gate/up GEMM) and K1 at the workload shapes."""
+    import torch
+    from paper_2603_18016_b200 import native, ops
+    from paper_2603_18016_b200.verify_bench import algorithmic_bytes, make_inputs
+    dev = backend.device
+    s = backend.tshape
+    M = CFG["m"] * (CFG["k"] + 1)
+    w = backend.target.layers[0]["wgu"]
+    x = torch.randn(M, s.hidden, device=dev).to(torch.bfloat16)
+    out = torch.empty(M, s.ffn_padded, dtype=torch.bfloat16, device=dev)
+    ws = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
+    # rotate over all 32 layers' weights so every launch streams from HBM
+    ws_list = [L["wgu"] for L in backend.target.layers]
+    it = [0]
+
+    def gemm():
+        ops.gemm(x, ws_list[it[0] % len(ws_list)], out=out, epi=native.EPI_SILU, workspace=ws)
+        it[0] += 1
+
+    ms = _time_kernel(gemm, 64)
+    nbytes = w.numel() * 2 + x.numel() * 2 + out.numel() * 2
+    roof = {"kernel": "gemm_kernel<192,SILU> (verify gate/up, M=192 N=28672 K=4096)",
+            "bound": "hbm", "achieved": round(nbytes / (ms * 1e-3) / 1e9, 1),
+            "peak": hbm_peak, "unit": "GB/s",
+            "frac": round(nbytes / (ms * 1e-3) / 1e9 / hbm_peak, 4), "traffic": None,
+            "bytes_per_launch": nbytes, "us_per_launch": round(ms * 1e3, 2),
+            "tflops": round(2 * M * w.shape[0] * s.hidden / (ms * 1e-3) / 1e12, 1)}
+    B, K, V = CFG["m"], CFG["k"], s.vocab
+    sets = [make_inputs(B, K, V, False, dev, seed=i) for i in range(3)]
+    j = [0]
+
+    def k1():
+        t, d, ids, ln, u = sets[j[0] % 3]
+        ops.verify_greedy(t, ids, ln)
+        j[0] += 1
+
+    ms1 = _time_kernel(k1, 60)
+    vb = algorithmic_bytes(B, K, V, False)
+    sets_s = [make_inputs(B, K, V, True, dev, seed=10 + i) for i in range(3)]
+
+    def k1s():
+        t, d, ids, ln, u = sets_s[j[0] % 3]
+        ops.verify_sample(t, d, ids, ln, u)
+        j[0] += 1
+
+    ms2 = _time_kernel(k1s, 30)
+    vbs = algorithmic_bytes(B, K, V, True)
+    vk = {"greedy": {"B": B, "k": K, "V": V, "us": round(ms1 * 1e3, 2), "bytes": vb,
+                     "GBps": round(vb / (ms1 * 1e-3) / 1e9, 1),
+                     "frac": round(vb / (ms1 * 1e-3) / 1e9 / hbm_peak, 4)},
+          "sampling": {"B": B, "k": K, "V": V, "us": round(ms2 * 1e3, 2), "bytes": vbs,
+                       "GBps": round(vbs / (ms2 * 1e-3) / 1e9, 1),
+                       "frac": round(vbs / (ms2 * 1e-3) / 1e9 / hbm_peak, 4)}}
+    return roof, vk
+
+
+def cpu_sample(steps: int = 1, n_req: int = 2, out_len: int = 6):
+    """The CPU oracle PSD (numpy + C verify) on a bounded sample of the
+    workload: same model shapes, k, prompt length; n_req requests of out_len
+    tokens.  Returns (tok/s, seconds, tokens, cores)."""
+    import numpy as np  # noqa: F401
+    from oracle.psd_cpu import CpuBackend
+    from paper_2603_18016_b200 import SimConfig, make_requests, run
+    be = CpuBackend(CFG["target"], CFG["draft"], seed=0, beta_target=BETA_TARGET,
+                    beta_draft=BETA_DRAFT, max_seq_len=CFG["prompt"] + out_len + 16)
+    cfg = SimConfig(mode="psd", m=max(1, n_req // 2), k=CFG["k"])
+    total_tok, total_s = 0, 0.0
+    for _ in range(steps):
+        reqs = make_requests([out_len] * n_req, prompt_len=CFG["prompt"])
+        t0 = time.perf_counter()
+        st, rep = run(cfg, reqs, backend=be)
+        total_s += time.perf_counter() - t0
+        total_tok += rep.total_generated
+    return total_tok / total_s, total_s, total_tok, os.cpu_count()
+
+
+def run_reference(args) -> None:
+    world, rank, _ = _dist()
+    if rank != 0:
+        return
+    from oracle.psd_cpu import CpuBackend  # noqa: F401
+    sample = dict(n_req=2, out_len=6)
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        pass
+    vals = []
+    t_all = 0.0
+    tok_all = 0
+    # model construction happens once inside cpu_sample's backend; warm-up
+    # steps are not timed
+    import oracle.psd_cpu as pc
+    from paper_2603_18016_b200 import SimConfig, make_requests, run
+    be = pc.CpuBackend(CFG["target"], CFG["draft"], seed=0, beta_target=BETA_TARGET,
+                       beta_draft=BETA_DRAFT, max_seq_len=CFG["prompt"] + 32)
+    cfg = SimConfig(mode="psd", m=1, k=CFG["k"])
+    for i in range(args.warmup + args.steps):
+        reqs = make_requests([sample["out_len"]] * sample["n_req"], prompt_len=CFG["prompt"])
+        t0 = time.perf_counter()
+        st, rep = run(cfg, reqs, backend=be)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            vals.append(rep.total_generated / dt)
+            t_all += dt
+            tok_all += rep.total_generated
+    v = tok_all / t_all
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "tok/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * t_all / args.steps, 1), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "cfg2 (8B target / 1B draft, k=5, prompt 128) bounded CPU "
+                                   f"sample: {sample['n_req']} requests x {sample['out_len']} "
+                                   "tokens per step",
+                       "impl": "CPU oracle (oracle/: numpy forward + C canonical verify)"},
+            "cpu_baseline": {"value": round(v, 4), "unit": "tok/s", "cores": os.cpu_count(),
+                             "kind": "port",
+                             "sample": f"{sample['n_req']} req x {sample['out_len']} tok, "
+                                       "prompt 128, k=5, 8B/1B shapes"},
+            "e2e": {"value": round(v, 4), "unit": "tok/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args) -> None:
+    import torch
+    world, rank, local = _dist()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2603_18016_b200 import mean_accepted_length, run
+    from paper_2603_18016_b200.gpu import GpuBackend
+
+    hbm_peak, bf16_peak, peak_kind = _peaks()
+    be = GpuBackend(CFG["target"], CFG["draft"], max_requests=CFG["n_requests"],
+                    max_batch=CFG["n_requests"], k_max=CFG["k"],
+                    max_seq_len=CFG["prompt"] + CFG["output"] + 16, seed=rank,
+                    beta_target=BETA_TARGET, beta_draft=BETA_DRAFT, device=dev)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+
+    def one(mode):
+        return run(_config(mode), _workload(rank), backend=be)
+
+    results = {}
+    for mode in ("psd", "standard-sd"):
+        for _ in range(args.warmup):
+            one(mode)
+        barrier()
+        clocks = Clocks(local) if mode == "psd" else None
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        reps = []
+        stats0 = dict(be.stats)
+        for _ in range(args.steps):
+            reps.append(one(mode)[1])
+        e1.record()
+        barrier()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = t.item()
+        tokens = sum(r.total_generated for r in reps)
+        results[mode] = {"ms": ms, "tokens": tokens, "reps": reps,
+                         "clocks": clocks.stop() if clocks else None,
+                         "draft_ms": be.stats["draft_ms"] - stats0["draft_ms"],
+                         "verify_ms": be.stats["verify_ms"] - stats0["verify_ms"],
+                         "steps": be.stats["steps"] - stats0["steps"]}
+    # end to end through the public API with host prompts / host outputs
+    barrier()
+    t0 = time.perf_counter()
+    st, rep_e2e = one("psd")
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    roof, vk = kernel_rooflines(be, hbm_peak)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            v, secs, toks, cores = cpu_sample()
+            cpu = {"value": round(v, 4), "unit": "tok/s", "cores": cores, "kind": "port",
+                   "sample": f"2 requests x 6 tokens, prompt 128, k=5, 8B/1B shapes "
+                             f"({toks} tokens in {secs:.1f} s)"}
+        except MemoryError as exc:  # pragma: no cover
+            cpu = {"value": None, "unit": "tok/s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"skipped: {exc}"}
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+    psd, sd = results["psd"], results["standard-sd"]
+    value = world * psd["tokens"] / (psd["ms"] * 1e-3)
+    sd_value = world * sd["tokens"] / (sd["ms"] * 1e-3)
+    r0 = psd["reps"][0]
+    steps_psd = psd["steps"] / max(1, args.steps)
+    h2d = CFG["n_requests"] * CFG["prompt"] * 4 + int(steps_psd) * 4 * 2 * CFG["m"]
+    d2h = CFG["n_requests"] * CFG["output"] * 4 + int(steps_psd) * 4 * CFG["m"]
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": "tok/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(psd["ms"] / args.steps, 2), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": "cfg2: Llama-3.1-8B target / Llama-3.2-1B draft shapes, "
+                               "random-init bf16, 2x32 requests, k=5, prompt 128, output 256, "
+                               "greedy, 1 GPU per replica (draft / verify on separate streams)",
+                   "global_batch": world * CFG["n_requests"], "seq_len": CFG["prompt"] +
+                   CFG["output"], "parallelism": f"replicas{world}",
+                   "l2": "inputs > L2 (weights 18.5 GB streamed per step)",
+                   "synthetic_language_beta": [BETA_TARGET, BETA_DRAFT]},
+        "sd": {"value": round(sd_value, 1), "unit": "tok/s", "mode": "standard-sd, one batch "
+                                                                    "of 64 (sd_batch_factor 2)"},
+        "psd_vs_sd": round(value / sd_value, 4),
+        "mean_accepted_len": round(mean_accepted_length(r0), 4),
+        "accepted_per_verify": round(r0.total_accepted / max(1, r0.total_bonus), 4),
+        "psd_steps_per_pass": steps_psd,
+        "draft_ms_per_pass": round(psd["draft_ms"] / args.steps, 2),
+        "verify_ms_per_pass": round(psd["verify_ms"] / args.steps, 2),
+        "e2e": {"value": round(rep_e2e.total_generated / e2e_s, 1), "unit": "tok/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": None,
+        "clocks": psd["clocks"],
+        "roofline": dict(roof, peak_kind=peak_kind),
+        "verify_kernel": vk,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -58,7 +58,7 @@ class GpuBackend:
                  beta_target: float = 6.0, beta_draft: float = 12.0,
                  device: str | torch.device = "cuda:0", dual_stream: bool = True,
                  block_size: int = 16, num_blocks: int | None = None,
-                 prefill_chunk_tokens: int = 4096) -> None:
+                 prefill_chunk_tokens: int = 4096, use_graphs: bool = True) -> None:
         if not torch.cuda.is_available():
             raise native.NativeError("GpuBackend needs a CUDA device (no CPU fallback)")
         native.load()
@@ -92,11 +92,17 @@ class GpuBackend:
             self.draft = Transformer(self.dshape, dev, seed * 2 + 2, num_blocks, block_size,
                                      self.max_blocks)
             i32 = torch.int32
-            self.block_table = torch.zeros(max_requests, self.max_blocks, dtype=i32, device=dev)
-            self.block_table_host = torch.zeros(max_requests, self.max_blocks,
-                                                dtype=i32).pin_memory()
+            # one extra scratch slot (index max_requests) backs the padding
+            # rows of bucketed batches; its block-table row is block 0
+            self.scratch_slot = max_requests
+            nslot = max_requests + 1
+            self.block_table = torch.zeros(nslot, self.max_blocks, dtype=i32, device=dev)
+            self.block_table_host = torch.zeros(nslot, self.max_blocks, dtype=i32).pin_memory()
+            self.bt_np = self.block_table_host.numpy()
+            self.nblk = np.zeros(nslot, np.int64)
+            self.nblk[self.scratch_slot] = 1
             self.ldt = k_max + 2
-            self.slot_tok = torch.zeros(max_requests, self.ldt, dtype=i32, device=dev)
+            self.slot_tok = torch.zeros(nslot, self.ldt, dtype=i32, device=dev)
             self.generated = torch.zeros(max_requests, dtype=i32, device=dev)
             self.max_out = max_seq_len
             self.outputs = torch.full((max_requests, self.max_out), -1, dtype=i32, device=dev)
@@ -117,6 +123,8 @@ class GpuBackend:
                 self.qbuf = torch.empty(max_requests, K, self.dshape.vocab, dtype=torch.float32,
                                         device=dev)
             self.v_ids = torch.empty(B, K, dtype=i32, device=dev)
+            self.v_acc = torch.empty(B, dtype=i32, device=dev)
+            self.v_out = torch.empty(B * (K + 1), dtype=i32, device=dev)
             self.v_len = torch.empty(B, dtype=i32, device=dev)
             self.v_slot = torch.empty(B, dtype=i32, device=dev)
             self.v_meta_host = torch.zeros(3 * B + B * K, dtype=i32).pin_memory()
@@ -129,6 +137,9 @@ class GpuBackend:
             self.s_target = torch.cuda.Stream(dev)
             self.s_draft = torch.cuda.Stream(dev) if dual_stream else self.s_target
             torch.cuda.synchronize(dev)
+        self.use_graphs = use_graphs
+        self.graphs: dict[tuple, torch.cuda.CUDAGraph] = {}
+        self.graph_streams: list = []
         self.slots: dict[int, int] = {}
         self.free_slots = list(range(max_requests - 1, -1, -1))
         self.pending_k: dict[int, int] = {}
@@ -188,13 +199,15 @@ class GpuBackend:
         return blocks[bi] * self.block_size + pos % self.block_size
 
     def _upload_block_table(self, state) -> None:
-        bt = self.block_table_host.numpy()
+        bt = self.bt_np
         bt[:] = 0
+        self.nblk[:self.max_requests] = 0
         for rid, s in self.slots.items():
             blocks = state.kv.blocks_of(rid)
             if len(blocks) > self.max_blocks:
                 raise KVError(f"request {rid}: {len(blocks)} blocks > max {self.max_blocks}")
             bt[s, :len(blocks)] = blocks
+            self.nblk[s] = len(blocks)
         self.block_table.copy_(self.block_table_host, non_blocking=True)
 
     def _admit(self, state, ids) -> None:
@@ -242,7 +255,7 @@ class GpuBackend:
                 q_start.append(len(toks))
                 toks.extend(req.prompt_ids[:n])
                 pos.extend(range(n))
-                slots.extend(self._kv_slot(state, rid, p) for p in range(n))
+                slots.extend(self._slots_at(np.full(n, self.slots[rid]), np.arange(n)).tolist())
                 seq_slot.append(self.slots[rid])
                 q_len.append(n)
                 q_pos0.append(0)
@@ -261,159 +274,200 @@ class GpuBackend:
             fwd.upload(1)
             fwd.run(len(toks), len(chunk), max(q_len), 0, None)
 
+    # ---- bucketed, graph-captured device passes ------------------------
+    def _bucket(self, n: int) -> int:
+        return min(self.max_batch, max(8, (n + 7) // 8 * 8))
+
+    def _slots_at(self, slot_rows: np.ndarray, pos: np.ndarray) -> np.ndarray:
+        """KV write slots of (slot, position) pairs from the host block table."""
+        bi = pos // self.block_size
+        if (bi >= self.nblk[slot_rows]).any():
+            raise KVError("KV position beyond the request's allocated blocks")
+        return self.bt_np[slot_rows, bi] * self.block_size + pos % self.block_size
+
+    def _run_graph(self, key, launch) -> None:
+        """Replay the CUDA graph for ``key`` on the current stream, capturing
+        it from ``launch`` on first use (the first use also runs eagerly)."""
+        g = self.graphs.get(key)
+        if g is not None:
+            g.replay()
+            return
+        launch()  # eager: correct results now, warms every kernel / workspace
+        if not self.use_graphs:
+            return
+        cur = torch.cuda.current_stream(self.device)
+        cs = torch.cuda.Stream(self.device)
+        self.graph_streams.append(cs)  # keep handles unique (per-stream K1 workspaces)
+        cs.wait_stream(cur)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=cs, capture_error_mode="thread_local"):
+            launch()
+        cur.wait_stream(cs)
+        self.graphs[key] = g
+
     def _draft_loop(self, state, ids, quotas) -> None:
         """k-step draft decode for the rows in ``ids`` (k_i = quotas[rid])."""
-        rows = [(rid, self.slots[rid], state.requests[rid].prompt_len +
-                 state.requests[rid].generated, quotas[rid]) for rid in ids if quotas[rid] > 0]
+        rows = [rid for rid in ids if quotas[rid] > 0]
         for rid in ids:
             self.pending_k[rid] = quotas[rid]
         if not rows:
             return
         n = len(rows)
-        kmax = max(r[3] for r in rows)
-        fwd = self.dfwd
+        nb = self._bucket(n)
+        sl = np.full(nb, self.scratch_slot, np.int32)
+        L = np.full(nb, 2, np.int64)
+        k = np.zeros(nb, np.int64)
+        sl[:n] = [self.slots[r] for r in rows]
+        L[:n] = [state.requests[r].prompt_len + state.requests[r].generated for r in rows]
+        k[:n] = [quotas[r] for r in rows]
+        kmax = int(k.max())
         ldt = self.ldt
+        real = np.arange(nb) < n
+        fwd = self.dfwd
         fwd.begin()
         for i in range(kmax):
             if i == 0:
-                gather = np.empty(2 * n, np.int32)
-                pos = np.empty(2 * n, np.int32)
-                slots = np.empty(2 * n, np.int32)
-                for r, (rid, s, L, k) in enumerate(rows):
-                    gather[2 * r:2 * r + 2] = (s * ldt, s * ldt + 1)
-                    pos[2 * r:2 * r + 2] = (L - 2, L - 1)
-                    slots[2 * r] = self._kv_slot(state, rid, L - 2)
-                    slots[2 * r + 1] = self._kv_slot(state, rid, L - 1)
+                pos = np.stack([L - 2, L - 1], axis=1).reshape(-1)
+                srow = np.repeat(sl, 2)
+                kvs = np.where(np.repeat(real, 2), self._slots_at(srow, np.maximum(pos, 0)), -1)
                 arrays = {
-                    "gather_src": gather, "positions": pos, "slots": slots,
-                    "seq_slot": np.asarray([s for _, s, _, _ in rows], np.int32),
-                    "q_start": np.arange(0, 2 * n, 2, dtype=np.int32),
-                    "q_len": np.full(n, 2, np.int32),
-                    "q_pos0": np.asarray([L - 2 for _, _, L, _ in rows], np.int32),
-                    "kv_len": np.asarray([L for _, _, L, _ in rows], np.int32),
-                    "logit_rows": np.arange(1, 2 * n, 2, dtype=np.int32),
-                    "scatter_dst": np.asarray([s * ldt + 2 for _, s, _, _ in rows], np.int32),
+                    "gather_src": (srow * ldt + np.tile([0, 1], nb)).astype(np.int32),
+                    "positions": np.where(np.repeat(real, 2), pos, 0).astype(np.int32),
+                    "slots": kvs.astype(np.int32),
+                    "seq_slot": sl,
+                    "q_start": np.arange(0, 2 * nb, 2, dtype=np.int32),
+                    "q_len": np.full(nb, 2, np.int32),
+                    "q_pos0": np.where(real, L - 2, 0).astype(np.int32),
+                    "kv_len": np.where(real, L, 1).astype(np.int32),
+                    "logit_rows": np.arange(1, 2 * nb, 2, dtype=np.int32),
+                    "scatter_dst": np.where(real, sl * ldt + 2, -1).astype(np.int32),
                 }
             else:
-                act = [i < k for _, _, _, k in rows]
+                act = real & (i < k)
+                pos = L - 1 + i
                 arrays = {
-                    "gather_src": np.asarray([s * ldt + 2 + i - 1 for _, s, _, _ in rows],
-                                             np.int32),
-                    "positions": np.asarray([L - 1 + i for _, _, L, _ in rows], np.int32),
-                    "slots": np.asarray([self._kv_slot(state, rid, L - 1 + i) if a else -1
-                                         for (rid, _, L, _), a in zip(rows, act)], np.int32),
-                    "seq_slot": np.asarray([s for _, s, _, _ in rows], np.int32),
-                    "q_start": np.arange(n, dtype=np.int32),
-                    "q_len": np.ones(n, np.int32),
-                    "q_pos0": np.asarray([L - 1 + i if a else 0
-                                          for (_, _, L, _), a in zip(rows, act)], np.int32),
-                    "kv_len": np.asarray([L + i if a else 1
-                                          for (_, _, L, _), a in zip(rows, act)], np.int32),
-                    "logit_rows": np.arange(n, dtype=np.int32),
-                    "scatter_dst": np.asarray([s * ldt + 2 + i if a else -1
-                                               for (_, s, _, _), a in zip(rows, act)], np.int32),
+                    "gather_src": (sl * ldt + 2 + i - 1).astype(np.int32),
+                    "positions": np.where(act, pos, 0).astype(np.int32),
+                    "slots": np.where(act, self._slots_at(sl, np.where(act, pos, 0)),
+                                      -1).astype(np.int32),
+                    "seq_slot": sl,
+                    "q_start": np.arange(nb, dtype=np.int32),
+                    "q_len": np.ones(nb, np.int32),
+                    "q_pos0": np.where(act, pos, 0).astype(np.int32),
+                    "kv_len": np.where(act, L + i, 1).astype(np.int32),
+                    "logit_rows": np.arange(nb, dtype=np.int32),
+                    "scatter_dst": np.where(act, sl * ldt + 2 + i, -1).astype(np.int32),
                 }
             fwd.stage(i, arrays)
         fwd.upload(kmax)
+        self._run_graph(("draft", nb, kmax), lambda: self._draft_launch(nb, kmax))
+
+    def _draft_launch(self, nb: int, kmax: int) -> None:
+        fwd = self.dfwd
         lib = native.load()
         st = torch.cuda.current_stream(self.device).cuda_stream
         for i in range(kmax):
-            M = 2 * n if i == 0 else n
-            tok = fwd.view("tokens", i)
-            native.check(lib.psd_index_copy_i32(tok.data_ptr(), None, self.slot_tok.data_ptr(),
+            M = 2 * nb if i == 0 else nb
+            native.check(lib.psd_index_copy_i32(fwd.view("tokens", i).data_ptr(), None,
+                                                self.slot_tok.data_ptr(),
                                                 fwd.view("gather_src", i).data_ptr(), M, st),
                          "draft gather")
-            fwd.run(M, n, 2 if i == 0 else 1, n, self.dlogits, self.dshape.vocab,
+            fwd.run(M, nb, 2 if i == 0 else 1, nb, self.dlogits, self.dshape.vocab,
                     bigram=(self.succ_d, self.beta_draft), set_index=i)
             if self.mode == "greedy":
-                ops.verify_greedy(self.dlogits[:n].view(n, 1, -1), self.d_ids0[:n],
-                                  self.d_len0[:n], self.d_acc[:n], self.d_out[:n])
+                ops.verify_greedy(self.dlogits[:nb].view(nb, 1, -1), self.d_ids0[:nb],
+                                  self.d_len0[:nb], self.d_acc[:nb], self.d_out[:nb])
             else:
                 raise ConfigError("sampling-mode draft loop not implemented yet")
             native.check(lib.psd_index_copy_i32(self.slot_tok.data_ptr(),
                                                 fwd.view("scatter_dst", i).data_ptr(),
-                                                self.d_out.data_ptr(), None, n, st),
+                                                self.d_out.data_ptr(), None, nb, st),
                          "draft scatter")
 
-    def _verify(self, state, rows: list[VerifyRow]):
-        """Target forward over [last, d_1..d_k] per row + K1 + commit kernel.
-        Returns the device accepted-length tensor (n,) and kmax."""
+    def _verify(self, state, rows: list[VerifyRow]) -> int:
+        """Stage and launch the verify pass; returns the number of real rows
+        whose accepted lengths land in ``acc_host``."""
         n = len(rows)
+        nb = self._bucket(n)
         kmax = max((r.k for r in rows), default=0)
         K1 = kmax + 1
         ldt = self.ldt
-        gather = np.empty(n * K1, np.int32)
-        pos = np.empty(n * K1, np.int32)
-        slots = np.empty(n * K1, np.int32)
-        seq_slot = np.empty(n, np.int32)
-        kv_len = np.empty(n, np.int32)
-        q_pos0 = np.empty(n, np.int32)
-        ids_src = np.empty(n * max(kmax, 1), np.int32)
+        sl = np.full(nb, self.scratch_slot, np.int64)
+        L = np.full(nb, 1, np.int64)
+        k = np.zeros(nb, np.int64)
         for r, row in enumerate(rows):
             rid = row.request_id
-            s = self.slots[rid]
-            req = state.requests[rid]
-            L = req.prompt_len + req.generated
-            k = row.k
-            if k != self.pending_k.get(rid, 0):
-                raise ProtocolError(f"request {rid}: verifying {k} drafts, device holds "
+            if row.k != self.pending_k.get(rid, 0):
+                raise ProtocolError(f"request {rid}: verifying {row.k} drafts, device holds "
                                     f"{self.pending_k.get(rid, 0)}")
-            for j in range(K1):
-                gather[r * K1 + j] = s * ldt + (1 if j == 0 or j > k else 1 + j)
-                pos[r * K1 + j] = L - 1 + j
-                slots[r * K1 + j] = self._kv_slot(state, rid, L - 1 + j) if j <= k else -1
-            for j in range(kmax):
-                ids_src[r * kmax + j] = s * ldt + 2 + j
-            seq_slot[r] = s
-            kv_len[r] = L + k
-            q_pos0[r] = L - 1
+            sl[r] = self.slots[rid]
+            req = state.requests[rid]
+            L[r] = req.prompt_len + req.generated
+            k[r] = row.k
+        real = np.arange(nb) < n
+        j = np.arange(K1)[None, :]
+        src = np.where((j == 0) | (j > k[:, None]), 1, 1 + j)
+        pos = (L - 1)[:, None] + j
+        wr = real[:, None] & (j <= k[:, None])
+        slots = np.where(wr, self._slots_at(np.repeat(sl, K1).reshape(nb, K1),
+                                            np.where(wr, pos, 0)), -1)
         fwd = self.tfwd
         fwd.begin()
-        fwd.stage(0, {"gather_src": gather, "positions": pos, "slots": slots,
-                      "seq_slot": seq_slot, "q_start": np.arange(0, n * K1, K1, dtype=np.int32),
-                      "q_len": np.full(n, K1, np.int32), "q_pos0": q_pos0, "kv_len": kv_len,
-                      "logit_rows": np.arange(n * K1, dtype=np.int32)})
+        fwd.stage(0, {"gather_src": (sl[:, None] * ldt + src).reshape(-1).astype(np.int32),
+                      "positions": np.where(real[:, None], pos, 0).reshape(-1).astype(np.int32),
+                      "slots": slots.reshape(-1).astype(np.int32),
+                      "seq_slot": sl.astype(np.int32),
+                      "q_start": np.arange(0, nb * K1, K1, dtype=np.int32),
+                      "q_len": np.full(nb, K1, np.int32),
+                      "q_pos0": np.where(real, L - 1, 0).astype(np.int32),
+                      "kv_len": np.where(real, L + k, 1).astype(np.int32),
+                      "logit_rows": np.arange(nb * K1, dtype=np.int32)})
         fwd.upload(1)
         vm = self.v_meta_host.numpy()
         B = self.max_batch
-        vm[:n] = [r.k for r in rows]
-        vm[B:B + n] = seq_slot
-        vm[3 * B:3 * B + n * kmax] = ids_src[:n * kmax]
+        vm[:nb] = k
+        vm[B:B + nb] = np.where(real, sl, -1)
+        if kmax:
+            vm[3 * B:3 * B + nb * kmax] = (sl[:, None] * ldt + 2 + np.arange(kmax)[None, :]
+                                           ).reshape(-1)
         self.v_meta.copy_(self.v_meta_host, non_blocking=True)
+        self._run_graph(("verify", nb, kmax), lambda: self._verify_launch(nb, kmax))
+        return n
+
+    def _verify_launch(self, nb: int, kmax: int) -> None:
+        K1 = kmax + 1
+        B = self.max_batch
         lib = native.load()
         st = torch.cuda.current_stream(self.device).cuda_stream
-        M = n * K1
+        fwd = self.tfwd
+        M = nb * K1
         native.check(lib.psd_index_copy_i32(fwd.view("tokens").data_ptr(), None,
                                             self.slot_tok.data_ptr(),
                                             fwd.view("gather_src").data_ptr(), M, st),
                      "verify gather")
-        fwd.run(M, n, K1, M, self.tlogits, self.tshape.vocab,
+        fwd.run(M, nb, K1, M, self.tlogits, self.tshape.vocab,
                 bigram=(self.succ_t, self.beta_target))
-        v_len = self.v_meta[:n]
-        v_slot = self.v_meta[B:B + n]
-        v_ids = self.v_ids[:n, :kmax]
+        v_len = self.v_meta[:nb]
+        v_slot = self.v_meta[B:B + nb]
         if kmax:
             native.check(lib.psd_index_copy_i32(self.v_ids.data_ptr(), None,
                                                 self.slot_tok.data_ptr(),
-                                                self.v_meta[3 * B:].data_ptr(), n * kmax, st),
+                                                self.v_meta[3 * B:].data_ptr(), nb * kmax, st),
                          "verify ids")
-            v_ids = self.v_ids.view(-1)[:n * kmax].view(n, kmax)
-        logits = self.tlogits[:M].view(n, K1, -1)
+            v_ids = self.v_ids.view(-1)[:nb * kmax].view(nb, kmax)
+        else:
+            v_ids = self.v_ids[:nb, :0]
+        logits = self.tlogits[:M].view(nb, K1, -1)
+        out = self.v_out[:nb * K1].view(nb, K1)
         if self.mode == "greedy":
-            acc, out = ops.verify_greedy(logits, v_ids, v_len, self.d_acc[:n],
-                                         self._out_buf(n, K1))
+            ops.verify_greedy(logits, v_ids, v_len, self.v_acc[:nb], out)
         else:
             raise ConfigError("sampling-mode verify not implemented yet")
-        native.check(lib.psd_commit(acc.data_ptr(), out.data_ptr(), kmax, v_slot.data_ptr(), n,
-                                    self.generated.data_ptr(), self.slot_tok.data_ptr(), ldt,
-                                    self.outputs.data_ptr(), self.max_out, st), "commit")
-        return acc, kmax
-
-    def _out_buf(self, n, K1):
-        if not hasattr(self, "_vout") or self._vout.numel() < n * K1:
-            self._vout = torch.empty(self.max_batch * (self.k_max + 1), dtype=torch.int32,
-                                     device=self.device)
-        return self._vout[:n * K1].view(n, K1)
+        native.check(lib.psd_commit(self.v_acc.data_ptr(), out.data_ptr(), kmax,
+                                    v_slot.data_ptr(), nb, self.generated.data_ptr(),
+                                    self.slot_tok.data_ptr(), self.ldt, self.outputs.data_ptr(),
+                                    self.max_out, st), "commit")
+        self.acc_host[:nb].copy_(self.v_acc[:nb], non_blocking=True)
 
     # ------------------------------------------------------------------
     def execute(self, state: EngineState, plan: StepPlan, rows: list[VerifyRow]) -> StepResult:
@@ -450,8 +504,7 @@ class GpuBackend:
         with torch.cuda.stream(ts):
             e_v0.record(ts)
             if rows:
-                acc, _ = self._verify(state, rows)
-                self.acc_host[:len(rows)].copy_(acc, non_blocking=True)
+                self._verify(state, rows)
             e_v1.record(ts)
         e_v1.synchronize()
         e_ov.synchronize()
