@@ -83,11 +83,19 @@ __global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, int Hq, in
   const int s = slot[m];
   const int half = D / 2;
   const int nh = Hq + Hkv;  // heads that get rotated
+  __shared__ float s_cos[128], s_sin[128];
+  for (int i = threadIdx.x; i < half; i += blockDim.x) {
+    float sn, cs;
+    sincosf((float)p * inv_freq[i], &sn, &cs);
+    s_cos[i] = cs;
+    s_sin[i] = sn;
+  }
+  __syncthreads();
   const __nv_bfloat16* row = qkv + (size_t)m * (Hq + 2 * Hkv) * D;
   for (int idx = threadIdx.x; idx < nh * half; idx += blockDim.x) {
     const int h = idx / half, i = idx % half;
-    float sn, cs;
-    sincosf((float)p * inv_freq[i], &sn, &cs);
+    if (h >= Hq && s < 0) continue;
+    const float cs = s_cos[i], sn = s_sin[i];
     float a = __bfloat162float(row[h * D + i]);
     float b = __bfloat162float(row[h * D + i + half]);
     if (bias) {  // qkv bias (Qwen2), rounded to bf16 like the projection output
@@ -99,7 +107,7 @@ __global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, int Hq, in
     if (h < Hq) {
       q_out[((size_t)m * Hq + h) * D + i] = r0;
       q_out[((size_t)m * Hq + h) * D + i + half] = r1;
-    } else if (s >= 0) {
+    } else {
       const size_t o = ((size_t)s * Hkv + (h - Hq)) * D;
       kc[o + i] = r0;
       kc[o + i + half] = r1;
@@ -107,30 +115,64 @@ __global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, int Hq, in
   }
   if (s >= 0) {
     const __nv_bfloat16* vrow = row + (size_t)(Hq + Hkv) * D;
-    const __nv_bfloat16* vb = bias ? bias + (size_t)(Hq + Hkv) * D : nullptr;
-    for (int idx = threadIdx.x; idx < Hkv * D; idx += blockDim.x)
-      vc[(size_t)s * Hkv * D + idx] =
-          vb ? __float2bfloat16(__bfloat162float(vrow[idx]) + __bfloat162float(vb[idx])) : vrow[idx];
+    __nv_bfloat16* vdst = vc + (size_t)s * Hkv * D;
+    if (bias) {
+      const __nv_bfloat16* vb = bias + (size_t)(Hq + Hkv) * D;
+      for (int idx = threadIdx.x; idx < Hkv * D; idx += blockDim.x)
+        vdst[idx] = __float2bfloat16(__bfloat162float(vrow[idx]) + __bfloat162float(vb[idx]));
+    } else {
+      for (int idx = threadIdx.x; idx < Hkv * D / 8; idx += blockDim.x)
+        reinterpret_cast<uint4*>(vdst)[idx] = reinterpret_cast<const uint4*>(vrow)[idx];
+    }
   }
 }
 
 // ---- paged multi-query attention (causal within the query window, GQA) ---------
-// One CTA per (sequence, kv head, query chunk).  Query rows of the chunk: the
-// chunk's tokens x the G = Hq / Hkv heads sharing this kv head.  KV streamed
-// in tiles of 32 keys through shared memory; online softmax in fp32.
+// One CTA (4 warps) per (sequence, kv head, query chunk).  Query rows of the
+// chunk = its tokens x the G = Hq / Hkv heads sharing this kv head (<= 64
+// rows; warp w owns rows 16w..16w+15).  Keys stream through shared memory in
+// tiles of 64 (cp.async, double buffered, zero-filled past the last key);
+// S = Q K^T and O += P V run on tensor cores (mma.sync m16n8k16 bf16 -> fp32),
+// softmax is online in fp32 registers (FlashAttention-2 register layout).
 constexpr int ATT_THREADS = 128;
-constexpr int ATT_KT = 32;        // keys per tile
-constexpr int ATT_MAXR = 64;      // query rows per CTA
-constexpr int ATT_MAXD = 128;
+constexpr int ATT_MAXR = 64;   // query rows per CTA
 
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4],
+                                               uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void ldmatrix_x4_trans(uint32_t (&r)[4], const void* p) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(a));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src),
+               "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+template <int D, int KT>
 __global__ void __launch_bounds__(ATT_THREADS)
 attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ kc,
                  const __nv_bfloat16* __restrict__ vc, const int32_t* __restrict__ block_table,
                  int max_blocks, const int32_t* __restrict__ seq_slot,
                  const int32_t* __restrict__ q_start, const int32_t* __restrict__ q_len,
                  const int32_t* __restrict__ q_pos0, const int32_t* __restrict__ kv_len, int Hq,
-                 int Hkv, int D, int bs, float scale, int tok_per_chunk,
+                 int Hkv, int bs, float scale_log2, int tok_per_chunk,
                  __nv_bfloat16* __restrict__ out) {
+  constexpr int P = D + 8;  // smem row pitch (conflict-free fragment loads)
   const int seq = blockIdx.x, hk = blockIdx.y, chunk = blockIdx.z;
   const int G = Hq / Hkv;
   const int ql = q_len[seq];
@@ -140,120 +182,168 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
   const int R = nt * G;
   const int kvl = kv_len[seq];
   const int qs = q_start[seq];
-  const int first_pos = q_pos0[seq];  // position of query token 0
-  // query t attends keys 0 .. min(first_pos + t, kvl - 1)
+  const int first_pos = q_pos0[seq];
   const int last_key = min(first_pos + t0 + nt - 1, kvl - 1);
   const int* bt = block_table + (size_t)seq_slot[seq] * max_blocks;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, c = lane & 3;
 
-  __shared__ __nv_bfloat16 sQ[ATT_MAXR][ATT_MAXD + 8];
-  __shared__ __nv_bfloat16 sK[ATT_KT][ATT_MAXD + 8];
-  __shared__ __nv_bfloat16 sV[ATT_KT][ATT_MAXD + 8];
-  __shared__ float sS[ATT_MAXR][ATT_KT + 1];
-  __shared__ float sAlpha[ATT_MAXR], sM[ATT_MAXR], sL[ATT_MAXR];
+  extern __shared__ __align__(16) uint8_t att_smem[];
+  typedef __nv_bfloat16 Row[P];
+  Row* sQ = reinterpret_cast<Row*>(att_smem);
+  Row (*sK)[KT] = reinterpret_cast<Row(*)[KT]>(att_smem + sizeof(Row) * ATT_MAXR);
+  Row (*sV)[KT] = reinterpret_cast<Row(*)[KT]>(att_smem + sizeof(Row) * (ATT_MAXR + 2 * KT));
 
-  for (int idx = tid; idx < R * D; idx += ATT_THREADS) {
-    const int r = idx / D, d = idx % D;
-    const int t = r / G, g = r % G;
-    sQ[r][d] = q[((size_t)(qs + t0 + t) * Hq + hk * G + g) * D + d];
+  // Q rows (zero rows past R)
+  for (int idx = tid; idx < ATT_MAXR * (D / 8); idx += ATT_THREADS) {
+    const int r = idx / (D / 8), cc = idx % (D / 8);
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r < R) {
+      const int t = r / G, gg = r % G;
+      v = *reinterpret_cast<const uint4*>(q + ((size_t)(qs + t0 + t) * Hq + hk * G + gg) * D +
+                                          cc * 8);
+    }
+    *reinterpret_cast<uint4*>(&sQ[r][cc * 8]) = v;
   }
-  for (int r = tid; r < R; r += ATT_THREADS) { sM[r] = -INFINITY; sL[r] = 0.f; }
-  // PV ownership: item = (row, 4-dim group)
-  const int dq = D / 4;
-  const int nitems = R * dq;
-  float acc[ATT_MAXR * ATT_MAXD / 4 / ATT_THREADS][4];
-  constexpr int MAXIT = ATT_MAXR * ATT_MAXD / 4 / ATT_THREADS;
-#pragma unroll
-  for (int i = 0; i < MAXIT; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+  auto load_tile = [&](int kt, int buf) {
+    for (int idx = tid; idx < KT * (D / 8); idx += ATT_THREADS) {
+      const int j = idx / (D / 8), cc = idx % (D / 8);
+      const int key = kt * KT + j;
+      const bool ok = key <= last_key;
+      size_t o = 0;
+      if (ok) o = (((size_t)bt[key / bs] * bs + key % bs) * Hkv + hk) * D + cc * 8;
+      cp_async16(&sK[buf][j][cc * 8], kc + o, ok);
+      cp_async16(&sV[buf][j][cc * 8], vc + o, ok);
+    }
+    cp_async_commit();
+  };
+  const int ntiles = last_key / KT + 1;
+  load_tile(0, 0);
   __syncthreads();
 
-  for (int k0 = 0; k0 <= last_key; k0 += ATT_KT) {
-    // load K / V tile (keys k0 .. k0+31) from the paged cache
-    for (int idx = tid; idx < ATT_KT * (D / 8); idx += ATT_THREADS) {
-      const int j = idx / (D / 8), c = idx % (D / 8);
-      const int key = k0 + j;
-      uint4 kv4 = make_uint4(0, 0, 0, 0), vv4 = kv4;
-      if (key <= last_key) {
-        const int blk = bt[key / bs];
-        const size_t o = (((size_t)blk * bs + key % bs) * Hkv + hk) * D + c * 8;
-        kv4 = *reinterpret_cast<const uint4*>(kc + o);
-        vv4 = *reinterpret_cast<const uint4*>(vc + o);
-      }
-      *reinterpret_cast<uint4*>(&sK[j][c * 8]) = kv4;
-      *reinterpret_cast<uint4*>(&sV[j][c * 8]) = vv4;
-    }
-    __syncthreads();
-    // scores
-    for (int idx = tid; idx < R * ATT_KT; idx += ATT_THREADS) {
-      const int r = idx / ATT_KT, j = idx % ATT_KT;
-      const int key = k0 + j;
-      const int qpos = min(first_pos + t0 + r / G, kvl - 1);
-      float s = -INFINITY;
-      if (key <= qpos) {
-        s = 0.f;
-        const __nv_bfloat162* kr = reinterpret_cast<const __nv_bfloat162*>(&sK[j][0]);
-        const __nv_bfloat162* qr = reinterpret_cast<const __nv_bfloat162*>(&sQ[r][0]);
-#pragma unroll 8
-        for (int d2 = 0; d2 < D / 2; ++d2) {
-          const float2 kf = __bfloat1622float2(kr[d2]);
-          const float2 qf = __bfloat1622float2(qr[d2]);
-          s += qf.x * kf.x + qf.y * kf.y;
-        }
-        s *= scale;
-      }
-      sS[r][j] = s;
-    }
-    __syncthreads();
-    // online softmax, one warp per row
-    for (int r = tid >> 5; r < R; r += ATT_THREADS / 32) {
-      const int lane = tid & 31;
-      const float s = sS[r][lane];
-      const float mt = warp_max(s);
-      const float mo = sM[r];
-      const float mn = fmaxf(mo, mt);
-      const float pexp = (s == -INFINITY) ? 0.f : __expf(s - mn);
-      const float ps = warp_sum(pexp);
-      sS[r][lane] = pexp;
-      if (lane == 0) {
-        const float al = (mo == -INFINITY) ? 0.f : __expf(mo - mn);
-        sAlpha[r] = al;
-        sL[r] = sL[r] * al + ps;
-        sM[r] = mn;
-      }
-    }
-    __syncthreads();
-    // O = alpha O + P V
+  const bool active = warp * 16 < R;
+  const int r0 = warp * 16 + g, r1 = r0 + 8;
+  const int lim0 = r0 < R ? min(first_pos + t0 + r0 / G, kvl - 1) : -1;
+  const int lim1 = r1 < R ? min(first_pos + t0 + r1 / G, kvl - 1) : -1;
+  uint32_t qf[D / 16][4];
+  if (active) {
 #pragma unroll
-    for (int i = 0; i < MAXIT; ++i) {
-      const int it = tid + i * ATT_THREADS;
-      if (it < nitems) {
-        const int r = it / dq, d = (it % dq) * 4;
-        const float al = sAlpha[r];
-        float a0 = acc[i][0] * al, a1 = acc[i][1] * al, a2 = acc[i][2] * al, a3 = acc[i][3] * al;
-#pragma unroll 8
-        for (int j = 0; j < ATT_KT; ++j) {
-          const float pj = sS[r][j];
-          const float2 v01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sV[j][d]));
-          const float2 v23 =
-              __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sV[j][d + 2]));
-          a0 += pj * v01.x; a1 += pj * v01.y; a2 += pj * v23.x; a3 += pj * v23.y;
+    for (int kk = 0; kk < D / 16; ++kk) {
+      qf[kk][0] = *reinterpret_cast<const uint32_t*>(&sQ[r0][kk * 16 + 2 * c]);
+      qf[kk][1] = *reinterpret_cast<const uint32_t*>(&sQ[r1][kk * 16 + 2 * c]);
+      qf[kk][2] = *reinterpret_cast<const uint32_t*>(&sQ[r0][kk * 16 + 8 + 2 * c]);
+      qf[kk][3] = *reinterpret_cast<const uint32_t*>(&sQ[r1][kk * 16 + 8 + 2 * c]);
+    }
+  }
+  float o[D / 8][4];
+#pragma unroll
+  for (int n = 0; n < D / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+
+  for (int kt = 0; kt < ntiles; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < ntiles) {
+      load_tile(kt + 1, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (active) {
+      float sacc[KT / 8][4];
+#pragma unroll
+      for (int n = 0; n < KT / 8; ++n) sacc[n][0] = sacc[n][1] = sacc[n][2] = sacc[n][3] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+#pragma unroll
+        for (int n = 0; n < KT / 8; ++n) {
+          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&sK[buf][n * 8 + g][kk * 16 + 2 * c]);
+          const uint32_t b1 =
+              *reinterpret_cast<const uint32_t*>(&sK[buf][n * 8 + g][kk * 16 + 8 + 2 * c]);
+          mma_bf16_16816(sacc[n], qf[kk], b0, b1);
         }
-        acc[i][0] = a0; acc[i][1] = a1; acc[i][2] = a2; acc[i][3] = a3;
+      }
+      // mask, scale (log2 domain), online softmax
+      float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+      for (int n = 0; n < KT / 8; ++n) {
+        const int key = kt * KT + n * 8 + 2 * c;
+        sacc[n][0] = key <= lim0 ? sacc[n][0] * scale_log2 : -INFINITY;
+        sacc[n][1] = key + 1 <= lim0 ? sacc[n][1] * scale_log2 : -INFINITY;
+        sacc[n][2] = key <= lim1 ? sacc[n][2] * scale_log2 : -INFINITY;
+        sacc[n][3] = key + 1 <= lim1 ? sacc[n][3] * scale_log2 : -INFINITY;
+        mx0 = fmaxf(mx0, fmaxf(sacc[n][0], sacc[n][1]));
+        mx1 = fmaxf(mx1, fmaxf(sacc[n][2], sacc[n][3]));
+      }
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+      const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+      const float base0 = mn0 == -INFINITY ? 0.f : mn0;
+      const float base1 = mn1 == -INFINITY ? 0.f : mn1;
+      const float al0 = exp2f(m0 - base0), al1 = exp2f(m1 - base1);
+      m0 = mn0;
+      m1 = mn1;
+      float ps0 = 0.f, ps1 = 0.f;
+      uint32_t pf[KT / 16][4];
+#pragma unroll
+      for (int n = 0; n < KT / 8; ++n) {
+        const float p0 = exp2f(sacc[n][0] - base0), p1 = exp2f(sacc[n][1] - base0);
+        const float p2 = exp2f(sacc[n][2] - base1), p3 = exp2f(sacc[n][3] - base1);
+        ps0 += p0 + p1;
+        ps1 += p2 + p3;
+        const int kk = n >> 1;
+        if ((n & 1) == 0) {
+          pf[kk][0] = pack_bf16(p0, p1);
+          pf[kk][1] = pack_bf16(p2, p3);
+        } else {
+          pf[kk][2] = pack_bf16(p0, p1);
+          pf[kk][3] = pack_bf16(p2, p3);
+        }
+      }
+      l0 = l0 * al0 + ps0;
+      l1 = l1 * al1 + ps1;
+#pragma unroll
+      for (int n = 0; n < D / 8; ++n) {
+        o[n][0] *= al0; o[n][1] *= al0; o[n][2] *= al1; o[n][3] *= al1;
+      }
+#pragma unroll
+      for (int kk = 0; kk < KT / 16; ++kk) {
+#pragma unroll
+        for (int n = 0; n < D / 8; n += 2) {
+          // 4 8x8 matrices: keys kk*16+{0..7, 8..15} x dims n*8.., (n+1)*8..
+          uint32_t vb[4];
+          const int mat = lane >> 3, rr = lane & 7;
+          const int krow = kk * 16 + (mat & 1) * 8 + rr;
+          const int dcol = (n + (mat >> 1)) * 8;
+          ldmatrix_x4_trans(vb, &sV[buf][krow][dcol]);
+          mma_bf16_16816(o[n], pf[kk], vb[0], vb[1]);
+          mma_bf16_16816(o[n + 1], pf[kk], vb[2], vb[3]);
+        }
       }
     }
     __syncthreads();
   }
+  if (!active) return;
+  // the 4 threads of a row group hold disjoint key columns: reduce l
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  const float inv0 = l0 > 0.f ? 1.f / l0 : 0.f, inv1 = l1 > 0.f ? 1.f / l1 : 0.f;
 #pragma unroll
-  for (int i = 0; i < MAXIT; ++i) {
-    const int it = tid + i * ATT_THREADS;
-    if (it < nitems) {
-      const int r = it / dq, d = (it % dq) * 4;
-      const int t = r / G, g = r % G;
-      const float inv = 1.f / sL[r];
-      __nv_bfloat16* o = out + ((size_t)(qs + t0 + t) * Hq + hk * G + g) * D + d;
-      *reinterpret_cast<__nv_bfloat162*>(o) = __floats2bfloat162_rn(acc[i][0] * inv, acc[i][1] * inv);
-      *reinterpret_cast<__nv_bfloat162*>(o + 2) =
-          __floats2bfloat162_rn(acc[i][2] * inv, acc[i][3] * inv);
+  for (int n = 0; n < D / 8; ++n) {
+    const int d = n * 8 + 2 * c;
+    if (r0 < R) {
+      const int t = r0 / G, gg = r0 % G;
+      *reinterpret_cast<__nv_bfloat162*>(out + ((size_t)(qs + t0 + t) * Hq + hk * G + gg) * D + d) =
+          __floats2bfloat162_rn(o[n][0] * inv0, o[n][1] * inv0);
+    }
+    if (r1 < R) {
+      const int t = r1 / G, gg = r1 % G;
+      *reinterpret_cast<__nv_bfloat162*>(out + ((size_t)(qs + t0 + t) * Hq + hk * G + gg) * D + d) =
+          __floats2bfloat162_rn(o[n][2] * inv1, o[n][3] * inv1);
     }
   }
 }
@@ -395,8 +485,8 @@ int psd_rope_kv(const void* qkv, int M, int Hq, int Hkv, int D, const int32_t* p
                 const int32_t* slots, const float* inv_freq, const void* qkv_bias, void* q_out,
                 void* k_cache, void* v_cache, void* stream) {
   if (M <= 0) return 0;
-  if (D % 2 || D > 256) return (int)cudaErrorInvalidValue;
-  rope_kv_kernel<<<M, 128, 0, (cudaStream_t)stream>>>(
+  if (D % 8 || D > 256) return (int)cudaErrorInvalidValue;
+  rope_kv_kernel<<<M, 256, 0, (cudaStream_t)stream>>>(
       static_cast<const __nv_bfloat16*>(qkv), Hq, Hkv, D, positions, slots, inv_freq,
       static_cast<const __nv_bfloat16*>(qkv_bias), static_cast<__nv_bfloat16*>(q_out), static_cast<__nv_bfloat16*>(k_cache),
       static_cast<__nv_bfloat16*>(v_cache));
@@ -409,16 +499,32 @@ int psd_attention(const void* q, const void* k_cache, const void* v_cache,
                   const int32_t* kv_len, int num_seqs, int max_q_len, int Hq, int Hkv, int D,
                   int block_size, float scale, void* out, void* stream) {
   if (num_seqs <= 0) return 0;
-  if (D > ATT_MAXD || D % 8 || Hq % Hkv) return (int)cudaErrorInvalidValue;
+  if (Hq % Hkv) return (int)cudaErrorInvalidValue;
   const int G = Hq / Hkv;
   if (G > ATT_MAXR) return (int)cudaErrorInvalidValue;
   const int tpc = ATT_MAXR / G;
   const int chunks = (max_q_len + tpc - 1) / tpc;
   dim3 grid(num_seqs, Hkv, chunks);
-  attention_kernel<<<grid, ATT_THREADS, 0, (cudaStream_t)stream>>>(
-      static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k_cache),
-      static_cast<const __nv_bfloat16*>(v_cache), block_table, max_blocks, seq_slot, q_start, q_len,
-      q_pos0, kv_len, Hq, Hkv, D, block_size, scale, tpc, static_cast<__nv_bfloat16*>(out));
+  const float sl2 = scale * 1.44269504088896341f;
+  static bool attr_done[3] = {false, false, false};
+  auto args = [&](auto kern, int kt, int d) {
+    const int smem = (ATT_MAXR + 4 * kt) * (d + 8) * 2;
+    const int slot = d == 32 ? 0 : d == 64 ? 1 : 2;
+    if (!attr_done[slot]) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      attr_done[slot] = true;
+    }
+    kern<<<grid, ATT_THREADS, smem, (cudaStream_t)stream>>>(
+        static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k_cache),
+        static_cast<const __nv_bfloat16*>(v_cache), block_table, max_blocks, seq_slot, q_start,
+        q_len, q_pos0, kv_len, Hq, Hkv, block_size, sl2, tpc, static_cast<__nv_bfloat16*>(out));
+  };
+  switch (D) {
+    case 32: args(attention_kernel<32, 64>, 64, 32); break;
+    case 64: args(attention_kernel<64, 64>, 64, 64); break;
+    case 128: args(attention_kernel<128, 32>, 32, 128); break;
+    default: return (int)cudaErrorInvalidValue;
+  }
   return (int)cudaGetLastError();
 }
 
