@@ -80,19 +80,28 @@ int psd_gemm_plan(int M, int N, int K, int epi, int splits_hint, int* splits_out
 int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, int N, void* Y,
                   int ldy, int epi, const void* R, int ldr, int splits_hint, void* workspace,
                   size_t workspace_bytes, void* stream);
+/* fp32 split-K partials P[z][m][n] (z < *splits_used, row pitch N); the
+ * consumer kernel (psd_add_rmsnorm, psd_rope_kv) reduces them in z order, so
+ * no separate reduction launch is needed.  Fewer splits are used when
+ * p_bytes cannot hold splits*M*N floats. */
+int psd_gemm_partials(const void* X, int ldx, int M, int K, const void* W, int ldw, int N,
+                      float* P, size_t p_bytes, int splits_hint, int* splits_used, void* stream);
 
 /* ---- K3/K3'/K4: forward-pass building blocks (bf16 storage, fp32 math) ----
  * Same seam as K2 (the virtual pass durations).  Row-major activations. */
 int psd_embed(const int32_t* tokens, int M, const void* table, int H, void* out, void* stream);
-/* y[m] = x[rows ? rows[m] : m] * rsqrt(mean(x^2) + eps) * w */
-int psd_rmsnorm(const void* x, int ldx, const int32_t* rows, const void* w, void* y, int ldy,
-                int M, int H, float eps, void* stream);
-/* qkv [M, (Hq+2Hkv) D] (+ optional bias) -> rotate-half RoPE on q, k;
- * q -> q_out [M, Hq, D]; k, v -> caches [blocks*block_size, Hkv, D] at slot
- * slots[m] (negative: not written). */
-int psd_rope_kv(const void* qkv, int M, int Hq, int Hkv, int D, const int32_t* positions,
-                const int32_t* slots, const float* inv_freq, const void* qkv_bias, void* q_out,
-                void* k_cache, void* v_cache, void* stream);
+/* src = rows ? rows[m] : m; v = bf16(x[src] + sum_z partials[z*slice + src*ldp])
+ * (no add when partials == NULL; v written back to x when write_back);
+ * y[m] = v * rsqrt(mean(v^2) + eps) * w.  H <= 8192. */
+int psd_add_rmsnorm(void* x, int ldx, const float* partials, int S, size_t slice, int ldp,
+                    const int32_t* rows, const void* w, void* y, int ldy, int M, int H, float eps,
+                    int write_back, void* stream);
+/* qkv = bf16(sum_z qkv_partials[z*slice + m*(Hq+2Hkv)D + j]) (+ optional bias)
+ * -> rotate-half RoPE on q, k; q -> q_out [M, Hq, D]; k, v -> caches
+ * [blocks*block_size, Hkv, D] at slot slots[m] (negative: not written). */
+int psd_rope_kv(const float* qkv_partials, int S, size_t slice, int M, int Hq, int Hkv, int D,
+                const int32_t* positions, const int32_t* slots, const float* inv_freq,
+                const void* qkv_bias, void* q_out, void* k_cache, void* v_cache, void* stream);
 /* Paged multi-query attention, GQA.  Sequence s: query tokens q_start[s] ..
  * +q_len[s]-1 at positions q_pos0[s] + t; token t attends keys
  * 0 .. min(q_pos0[s] + t, kv_len[s] - 1) read through

@@ -36,6 +36,8 @@ using namespace psd;
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int kThreads = 192;
+constexpr int kPrefetch = 0;  // k-blocks of weights prefetched into L2 ahead of use (0 = off;
+                               // measured slower on B200: the TMA issue slots are the cost)
 
 struct GemmArgs {
   int M, N, K;
@@ -101,9 +103,14 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUt
     if (lane == 0) {
       const uint64_t pol_w = policy_evict_first();
       const uint64_t pol_x = policy_evict_last();
+      const uint64_t pol_pf = policy_evict_last();
+      // L2 prefetch runs kPrefetch k-blocks ahead of the smem ring
+      const int npf = kPrefetch > 0 ? min(nkb, kPrefetch) : 0;
+      for (int i = 0; i < npf; ++i) tma_prefetch_l2_2d(&tmW, (kb0 + i) * BK, n0, pol_pf);
       for (int i = 0; i < nkb; ++i) {
         const int s = i % C::STAGES;
         const uint32_t ph = (i / C::STAGES) & 1;
+        if (kPrefetch > 0 && i + kPrefetch < nkb) tma_prefetch_l2_2d(&tmW, (kb0 + i + kPrefetch) * BK, n0, pol_pf);
         mbar_wait(empty + s, ph ^ 1);
         mbar_arrive_expect_tx(full + s, C::STAGE);
         const int kc = (kb0 + i) * BK;
@@ -324,6 +331,34 @@ int psd_gemm_plan(int M, int N, int K, int epi, int splits_hint, int* splits_out
   if (workspace_bytes) *workspace_bytes = splits > 1 ? (size_t)splits * M * N * sizeof(float) : 0;
   (void)epi;
   return 0;
+}
+
+int psd_gemm_partials(const void* X, int ldx, int M, int K, const void* W, int ldw, int N,
+                      float* P, size_t p_bytes, int splits_hint, int* splits_used, void* stream) {
+  if (!X || !W || !P) return (int)cudaErrorInvalidValue;
+  if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(W)) & 15)
+    return (int)cudaErrorMisalignedAddress;
+  if ((ldx % 8) || (ldw % 8)) return (int)cudaErrorMisalignedAddress;
+  int splits = 1;
+  int rc = psd_gemm_plan(M, N, K, PSD_EPI_PARTIAL, splits_hint, &splits, nullptr);
+  if (rc) return rc;
+  while (splits > 1 && (size_t)splits * M * N * sizeof(float) > p_bytes) --splits;
+  if ((size_t)splits * M * N * sizeof(float) > p_bytes) return (int)cudaErrorInvalidValue;
+  rc = psd_gemm_plan(M, N, K, PSD_EPI_PARTIAL, splits, &splits, nullptr);
+  if (rc) return rc;
+  const int bn = token_tile(M);
+  CUtensorMap mw, mx;
+  if ((rc = make_map(&mw, W, N, K, ldw, BM))) return rc;
+  if ((rc = make_map(&mx, X, M, K, ldx, bn))) return rc;
+  GemmArgs g;
+  g.M = M; g.N = N; g.K = K;
+  g.kb_total = (K + BK - 1) / BK;
+  g.kb_per_split = (g.kb_total + splits - 1) / splits;
+  splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
+  g.Y = P; g.ldy = N; g.R = nullptr; g.ldr = 0;
+  if (splits_used) *splits_used = splits;
+  dim3 grid(N / BM, (M + bn - 1) / bn, splits);
+  return launch_epi<PSD_EPI_PARTIAL>(bn, mw, mx, g, grid, (cudaStream_t)stream);
 }
 
 int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, int N, void* Y,

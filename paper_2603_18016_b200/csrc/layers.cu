@@ -36,44 +36,86 @@ __global__ void embed_kernel(const int32_t* __restrict__ tok, const __nv_bfloat1
     dst[i] = t < 0 ? make_uint4(0, 0, 0, 0) : src[i];
 }
 
-// ---- RMSNorm (fp32 statistics) ------------------------------------------------
-__global__ void rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, int ldx,
-                               const int32_t* __restrict__ rows,
-                               const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ y,
-                               int ldy, int H, float eps) {
+// ---- residual add of split-K partials + RMSNorm (fp32 statistics) ---------------
+// v = bf16(x[src] + sum_s P[s][src]) (sum in s order; skipped when P == null),
+// optionally written back to x (the residual stream), y[m] = v * rsqrt(mean(v^2)
+// + eps) * w.  src = rows ? rows[m] : m.  The GEMMs before a norm (O proj, down
+// proj) leave fp32 split-K partials, so this one kernel is their reduction,
+// the residual add and the norm.
+constexpr int NORM_THREADS = 256;
+constexpr int NORM_MAX_PER_THREAD = 32;  // H <= 8192
+
+template <int NV>  // NV = float2 pairs per thread (H / 2 / NORM_THREADS rounded up)
+__global__ void __launch_bounds__(NORM_THREADS)
+add_rmsnorm_kernel(__nv_bfloat16* __restrict__ x, int ldx, const float* __restrict__ P, int S,
+                   size_t slice, int ldp, const int32_t* __restrict__ rows,
+                   const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ y, int ldy,
+                   int H, float eps, int write_back) {
   const int m = blockIdx.x;
   const int src = rows ? rows[m] : m;
-  const __nv_bfloat162* xr = reinterpret_cast<const __nv_bfloat162*>(x + (size_t)src * ldx);
+  __nv_bfloat162* xr = reinterpret_cast<__nv_bfloat162*>(x + (size_t)src * ldx);
+  const float2* pr = P ? reinterpret_cast<const float2*>(P + (size_t)src * ldp) : nullptr;
+  const size_t slice2 = slice / 2;
+  float2 v[NV];
   float ss = 0.f;
-  for (int i = threadIdx.x; i < H / 2; i += blockDim.x) {
-    const float2 v = __bfloat1622float2(xr[i]);
-    ss += v.x * v.x + v.y * v.y;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int i = threadIdx.x + k * NORM_THREADS;
+    if (i < H / 2) {
+      float2 xv = __bfloat1622float2(xr[i]);
+      if (pr) {
+        float2 acc = pr[i];
+        for (int z = 1; z < S; ++z) {
+          const float2 pz = pr[z * slice2 + i];
+          acc.x += pz.x;
+          acc.y += pz.y;
+        }
+        const __nv_bfloat162 nb = __floats2bfloat162_rn(acc.x + xv.x, acc.y + xv.y);
+        if (write_back) xr[i] = nb;
+        xv = __bfloat1622float2(nb);
+      }
+      v[k] = xv;
+      ss += xv.x * xv.x + xv.y * xv.y;
+    }
   }
   __shared__ float red[32];
   ss = warp_sum(ss);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
   if (threadIdx.x < 32) {
-    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
-    v = warp_sum(v);
-    if (threadIdx.x == 0) red[0] = v;
+    float t = threadIdx.x < (NORM_THREADS >> 5) ? red[threadIdx.x] : 0.f;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) red[0] = t;
   }
   __syncthreads();
   const float inv = rsqrtf(red[0] / H + eps);
   const __nv_bfloat162* wr = reinterpret_cast<const __nv_bfloat162*>(w);
   __nv_bfloat162* yr = reinterpret_cast<__nv_bfloat162*>(y + (size_t)m * ldy);
-  for (int i = threadIdx.x; i < H / 2; i += blockDim.x) {
-    const float2 v = __bfloat1622float2(xr[i]);
-    const float2 g = __bfloat1622float2(wr[i]);
-    yr[i] = __floats2bfloat162_rn(v.x * inv * g.x, v.y * inv * g.y);
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int i = threadIdx.x + k * NORM_THREADS;
+    if (i < H / 2) {
+      const float2 g = __bfloat1622float2(wr[i]);
+      yr[i] = __floats2bfloat162_rn(v[k].x * inv * g.x, v[k].y * inv * g.y);
+    }
   }
 }
 
 // ---- RoPE + paged KV write ------------------------------------------------------
 // qkv [M, (Hq + 2 Hkv) D]; q_out [M, Hq, D]; caches [blocks, bs, Hkv, D].
 // rotate-half convention: pairs (i, i + D/2), angle = pos * inv_freq[i].
-__global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, int Hq, int Hkv, int D,
-                               const int32_t* __restrict__ pos, const int32_t* __restrict__ slot,
+// qkv value j of token m: bf16(sum_s P[s][m][j]) -- the QKV GEMM's split-K
+// partials are reduced here
+__device__ __forceinline__ float qkv_at(const float* __restrict__ P, int S, size_t slice,
+                                        size_t off) {
+  float acc = 0.f;
+  for (int z = 0; z < S; ++z) acc += P[z * slice + off];
+  return __bfloat162float(__float2bfloat16(acc));
+}
+
+__global__ void rope_kv_kernel(const float* __restrict__ P, int S, size_t slice, int Hq, int Hkv,
+                               int D, const int32_t* __restrict__ pos,
+                               const int32_t* __restrict__ slot,
                                const float* __restrict__ inv_freq,
                                const __nv_bfloat16* __restrict__ bias,
                                __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ kc,
@@ -91,13 +133,13 @@ __global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, int Hq, in
     s_sin[i] = sn;
   }
   __syncthreads();
-  const __nv_bfloat16* row = qkv + (size_t)m * (Hq + 2 * Hkv) * D;
+  const size_t row = (size_t)m * (Hq + 2 * Hkv) * D;
   for (int idx = threadIdx.x; idx < nh * half; idx += blockDim.x) {
     const int h = idx / half, i = idx % half;
     if (h >= Hq && s < 0) continue;
     const float cs = s_cos[i], sn = s_sin[i];
-    float a = __bfloat162float(row[h * D + i]);
-    float b = __bfloat162float(row[h * D + i + half]);
+    float a = qkv_at(P, S, slice, row + h * D + i);
+    float b = qkv_at(P, S, slice, row + h * D + i + half);
     if (bias) {  // qkv bias (Qwen2), rounded to bf16 like the projection output
       a = __bfloat162float(__float2bfloat16(a + __bfloat162float(bias[h * D + i])));
       b = __bfloat162float(__float2bfloat16(b + __bfloat162float(bias[h * D + i + half])));
@@ -114,15 +156,13 @@ __global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, int Hq, in
     }
   }
   if (s >= 0) {
-    const __nv_bfloat16* vrow = row + (size_t)(Hq + Hkv) * D;
+    const size_t vrow = row + (size_t)(Hq + Hkv) * D;
     __nv_bfloat16* vdst = vc + (size_t)s * Hkv * D;
-    if (bias) {
-      const __nv_bfloat16* vb = bias + (size_t)(Hq + Hkv) * D;
-      for (int idx = threadIdx.x; idx < Hkv * D; idx += blockDim.x)
-        vdst[idx] = __float2bfloat16(__bfloat162float(vrow[idx]) + __bfloat162float(vb[idx]));
-    } else {
-      for (int idx = threadIdx.x; idx < Hkv * D / 8; idx += blockDim.x)
-        reinterpret_cast<uint4*>(vdst)[idx] = reinterpret_cast<const uint4*>(vrow)[idx];
+    const __nv_bfloat16* vb = bias ? bias + (size_t)(Hq + Hkv) * D : nullptr;
+    for (int idx = threadIdx.x; idx < Hkv * D; idx += blockDim.x) {
+      float v = qkv_at(P, S, slice, vrow + idx);
+      if (vb) v = __bfloat162float(__float2bfloat16(v + __bfloat162float(vb[idx])));
+      vdst[idx] = __float2bfloat16(v);
     }
   }
 }
@@ -136,6 +176,7 @@ __global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, int Hq, in
 // softmax is online in fp32 registers (FlashAttention-2 register layout).
 constexpr int ATT_THREADS = 128;
 constexpr int ATT_MAXR = 64;   // query rows per CTA
+constexpr int ATT_STAGES = 4;  // K/V tiles in flight
 
 __device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4],
                                                uint32_t b0, uint32_t b1) {
@@ -163,7 +204,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-template <int D, int KT>
+template <int D, int KT, int NS>
 __global__ void __launch_bounds__(ATT_THREADS)
 attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ kc,
                  const __nv_bfloat16* __restrict__ vc, const int32_t* __restrict__ block_table,
@@ -192,7 +233,7 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
   typedef __nv_bfloat16 Row[P];
   Row* sQ = reinterpret_cast<Row*>(att_smem);
   Row (*sK)[KT] = reinterpret_cast<Row(*)[KT]>(att_smem + sizeof(Row) * ATT_MAXR);
-  Row (*sV)[KT] = reinterpret_cast<Row(*)[KT]>(att_smem + sizeof(Row) * (ATT_MAXR + 2 * KT));
+  Row (*sV)[KT] = reinterpret_cast<Row(*)[KT]>(att_smem + sizeof(Row) * (ATT_MAXR + NS * KT));
 
   // Q rows (zero rows past R)
   for (int idx = tid; idx < ATT_MAXR * (D / 8); idx += ATT_THREADS) {
@@ -218,7 +259,12 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
     cp_async_commit();
   };
   const int ntiles = last_key / KT + 1;
-  load_tile(0, 0);
+  // NS-stage cp.async ring: tiles 0 .. NS-2 in flight before the first use
+#pragma unroll
+  for (int t = 0; t < NS - 1; ++t) {
+    if (t < ntiles) load_tile(t, t);
+    else cp_async_commit();
+  }
   __syncthreads();
 
   const bool active = warp * 16 < R;
@@ -241,13 +287,11 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
 
   for (int kt = 0; kt < ntiles; ++kt) {
-    const int buf = kt & 1;
-    if (kt + 1 < ntiles) {
-      load_tile(kt + 1, buf ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    const int buf = kt % NS;
+    // keep NS-1 tiles in flight: issue tile kt+NS-1 (or an empty group)
+    if (kt + NS - 1 < ntiles) load_tile(kt + NS - 1, (kt + NS - 1) % NS);
+    else cp_async_commit();
+    cp_async_wait<NS - 1>();
     __syncthreads();
     if (active) {
       float sacc[KT / 8][4];
@@ -471,23 +515,32 @@ int psd_embed(const int32_t* tokens, int M, const void* table, int H, void* out,
   return (int)cudaGetLastError();
 }
 
-int psd_rmsnorm(const void* x, int ldx, const int32_t* rows, const void* w, void* y, int ldy, int M,
-                int H, float eps, void* stream) {
+int psd_add_rmsnorm(void* x, int ldx, const float* partials, int S, size_t slice, int ldp,
+                    const int32_t* rows, const void* w, void* y, int ldy, int M, int H, float eps,
+                    int write_back, void* stream) {
   if (M <= 0) return 0;
-  if (H % 2) return (int)cudaErrorInvalidValue;
-  rmsnorm_kernel<<<M, 256, 0, (cudaStream_t)stream>>>(
-      static_cast<const __nv_bfloat16*>(x), ldx, rows, static_cast<const __nv_bfloat16*>(w),
-      static_cast<__nv_bfloat16*>(y), ldy, H, eps);
+  if (H % 2 || H > 2 * NORM_THREADS * NORM_MAX_PER_THREAD / 2) return (int)cudaErrorInvalidValue;
+  auto go = [&](auto kern) {
+    kern<<<M, NORM_THREADS, 0, (cudaStream_t)stream>>>(
+        static_cast<__nv_bfloat16*>(x), ldx, partials, S, slice, ldp, rows,
+        static_cast<const __nv_bfloat16*>(w), static_cast<__nv_bfloat16*>(y), ldy, H, eps,
+        write_back);
+  };
+  const int nv = (H / 2 + NORM_THREADS - 1) / NORM_THREADS;
+  if (nv <= 2) go(add_rmsnorm_kernel<2>);
+  else if (nv <= 4) go(add_rmsnorm_kernel<4>);
+  else if (nv <= 8) go(add_rmsnorm_kernel<8>);
+  else go(add_rmsnorm_kernel<16>);
   return (int)cudaGetLastError();
 }
 
-int psd_rope_kv(const void* qkv, int M, int Hq, int Hkv, int D, const int32_t* positions,
-                const int32_t* slots, const float* inv_freq, const void* qkv_bias, void* q_out,
-                void* k_cache, void* v_cache, void* stream) {
+int psd_rope_kv(const float* qkv_partials, int S, size_t slice, int M, int Hq, int Hkv, int D,
+                const int32_t* positions, const int32_t* slots, const float* inv_freq,
+                const void* qkv_bias, void* q_out, void* k_cache, void* v_cache, void* stream) {
   if (M <= 0) return 0;
   if (D % 8 || D > 256) return (int)cudaErrorInvalidValue;
   rope_kv_kernel<<<M, 256, 0, (cudaStream_t)stream>>>(
-      static_cast<const __nv_bfloat16*>(qkv), Hq, Hkv, D, positions, slots, inv_freq,
+      qkv_partials, S, slice, Hq, Hkv, D, positions, slots, inv_freq,
       static_cast<const __nv_bfloat16*>(qkv_bias), static_cast<__nv_bfloat16*>(q_out), static_cast<__nv_bfloat16*>(k_cache),
       static_cast<__nv_bfloat16*>(v_cache));
   return (int)cudaGetLastError();
@@ -508,7 +561,7 @@ int psd_attention(const void* q, const void* k_cache, const void* v_cache,
   const float sl2 = scale * 1.44269504088896341f;
   static bool attr_done[3] = {false, false, false};
   auto args = [&](auto kern, int kt, int d) {
-    const int smem = (ATT_MAXR + 4 * kt) * (d + 8) * 2;
+    const int smem = (ATT_MAXR + 2 * ATT_STAGES * kt) * (d + 8) * 2;
     const int slot = d == 32 ? 0 : d == 64 ? 1 : 2;
     if (!attr_done[slot]) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -520,9 +573,9 @@ int psd_attention(const void* q, const void* k_cache, const void* v_cache,
         q_len, q_pos0, kv_len, Hq, Hkv, block_size, sl2, tpc, static_cast<__nv_bfloat16*>(out));
   };
   switch (D) {
-    case 32: args(attention_kernel<32, 64>, 64, 32); break;
-    case 64: args(attention_kernel<64, 64>, 64, 64); break;
-    case 128: args(attention_kernel<128, 32>, 32, 128); break;
+    case 32: args(attention_kernel<32, 64, ATT_STAGES>, 64, 32); break;
+    case 64: args(attention_kernel<64, 64, ATT_STAGES>, 64, 64); break;
+    case 128: args(attention_kernel<128, 32, ATT_STAGES>, 32, 128); break;
     default: return (int)cudaErrorInvalidValue;
   }
   return (int)cudaGetLastError();

@@ -59,6 +59,16 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
       : "memory");
 }
+// bulk tensor prefetch into L2 (no shared memory, no barrier): keeps HBM
+// requests in flight beyond what the smem ring can hold
+__device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap* map, int c0, int c1,
+                                                   uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.prefetch.tensor.2d.L2.global.tile.L2::cache_hint [%0, {%1, %2}], %3;" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
 // L2 eviction policies (createpolicy.fractional)
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;

@@ -33,8 +33,9 @@ SIGNATURES: dict[str, tuple] = {
     "psd_gemm_plan": (_i, [_i, _i, _i, _i, _i, _c.POINTER(_i), _c.POINTER(_sz)]),
     "psd_gemm_bf16": (_i, [_p, _i, _i, _i, _p, _i, _i, _p, _i, _i, _p, _i, _i, _p, _sz, _p]),
     "psd_embed": (_i, [_p, _i, _p, _i, _p, _p]),
-    "psd_rmsnorm": (_i, [_p, _i, _p, _p, _p, _i, _i, _i, _f, _p]),
-    "psd_rope_kv": (_i, [_p, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "psd_add_rmsnorm": (_i, [_p, _i, _p, _i, _sz, _i, _p, _p, _p, _i, _i, _i, _f, _i, _p]),
+    "psd_rope_kv": (_i, [_p, _i, _sz, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "psd_gemm_partials": (_i, [_p, _i, _i, _i, _p, _i, _i, _p, _sz, _i, _c.POINTER(_i), _p]),
     "psd_attention": (_i, [_p, _p, _p, _p, _i, _p, _p, _p, _p, _p, _i, _i, _i, _i, _i, _i, _f,
                            _p, _p]),
     "psd_bigram_bias": (_i, [_p, _i64, _p, _i, _p, _i, _f, _p]),
@@ -44,7 +45,7 @@ SIGNATURES: dict[str, tuple] = {
     "psd_fill_uniform_bf16": (_i, [_p, _sz, _c.c_uint64, _f, _p]),
 }
 
-EPI_BF16, EPI_F32, EPI_RESID, EPI_SILU = 0, 1, 2, 3
+EPI_BF16, EPI_F32, EPI_RESID, EPI_SILU, EPI_PARTIAL = 0, 1, 2, 3, 4
 
 _lib = None
 

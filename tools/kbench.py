@@ -1,0 +1,209 @@
+"""Per-kernel microbenchmarks at the cfg2 shapes (CUDA events, L2-cold weights).
+
+    python tools/kbench.py [--json out.json]
+
+Each line: kernel, shape, us/launch, algorithmic bytes, GB/s, fraction of the
+measured HBM peak.  Weight-streaming kernels rotate over several copies so
+every launch reads its weights from HBM, as in the real forward (each layer
+has its own weights).
+"""
+import argparse
+import ctypes
+import json
+import math
+import sys
+
+sys.path.insert(0, ".")
+import torch  # noqa: E402
+
+from paper_2603_18016_b200 import native, ops  # noqa: E402
+from paper_2603_18016_b200.verify_bench import algorithmic_bytes, make_inputs  # noqa: E402
+
+try:
+    PEAK = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"]
+except OSError:
+    PEAK = 6461.2
+dev = torch.device("cuda:0")
+lib = native.load()
+bf = torch.bfloat16
+rows = []
+
+
+def timeit(fn, iters=40):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / iters * 1e3
+
+
+def report(name, shape, us, nbytes, flops=0):
+    gbs = nbytes / (us * 1e-6) / 1e9
+    r = {"kernel": name, "shape": shape, "us": round(us, 2), "bytes": nbytes,
+         "GBps": round(gbs, 1), "frac_hbm": round(gbs / PEAK, 3)}
+    if flops:
+        r["TFLOPs"] = round(flops / (us * 1e-6) / 1e12, 1)
+    rows.append(r)
+    print(f"{name:28s} {shape:34s} {us:9.2f} us {gbs:8.0f} GB/s {100 * gbs / PEAK:5.1f}%"
+          + (f" {r['TFLOPs']:7.1f} TF/s" if flops else ""), flush=True)
+
+
+def gemm_case(tag, M, N, K, epi, copies=6):
+    x = torch.randn(M, K, device=dev).to(bf)
+    ws = [(torch.randn(N, K, device=dev) * 0.02).to(bf) for _ in range(copies)]
+    if epi == "partial":
+        part = torch.empty(8 * M * N, dtype=torch.float32, device=dev)
+        sp = ctypes.c_int()
+        st = torch.cuda.current_stream().cuda_stream
+        it = [0]
+
+        def fn():
+            w = ws[it[0] % copies]
+            it[0] += 1
+            rc = lib.psd_gemm_partials(x.data_ptr(), K, M, K, w.data_ptr(), K, N, part.data_ptr(),
+                                       part.numel() * 4, 0, ctypes.byref(sp), st)
+            assert rc == 0
+        us = timeit(fn)
+        out_bytes = sp.value * M * N * 4
+        tag = f"{tag} (S={sp.value})"
+    else:
+        e = {"bf16": native.EPI_BF16, "silu": native.EPI_SILU, "f32": native.EPI_F32}[epi]
+        n_out = N // 2 if epi == "silu" else N
+        out = torch.empty(M, n_out, dtype=torch.float32 if epi == "f32" else bf, device=dev)
+        wsp = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
+        it = [0]
+
+        def fn():
+            ops.gemm(x, ws[it[0] % copies], out=out, epi=e, workspace=wsp)
+            it[0] += 1
+        us = timeit(fn)
+        out_bytes = out.numel() * out.element_size()
+    nbytes = N * K * 2 + M * K * 2 + out_bytes
+    report(f"gemm {tag}", f"M={M} N={N} K={K}", us, nbytes, 2 * M * N * K)
+
+
+def attn_case(tag, nseq, ql, ctx, Hq, Hkv, D):
+    bs = 16
+    nblk_seq = (ctx + ql + bs) // bs + 1
+    nb = nseq * nblk_seq + 1
+    kc = torch.randn(nb * bs, Hkv, D, device=dev).to(bf)
+    vc = torch.randn(nb * bs, Hkv, D, device=dev).to(bf)
+    bt = torch.arange(1, 1 + nseq * nblk_seq, dtype=torch.int32, device=dev).view(nseq, nblk_seq)
+    q = torch.randn(nseq * ql, Hq, D, device=dev).to(bf)
+    out = torch.empty_like(q)
+    i32 = lambda v: torch.tensor(v, dtype=torch.int32, device=dev)  # noqa: E731
+    seq_slot = i32(list(range(nseq)))
+    q_start = i32([i * ql for i in range(nseq)])
+    q_len = i32([ql] * nseq)
+    q_pos0 = i32([ctx] * nseq)
+    kv_len = i32([ctx + ql] * nseq)
+    st = torch.cuda.current_stream().cuda_stream
+
+    def fn():
+        rc = lib.psd_attention(q.data_ptr(), kc.data_ptr(), vc.data_ptr(), bt.data_ptr(),
+                               nblk_seq, seq_slot.data_ptr(), q_start.data_ptr(), q_len.data_ptr(),
+                               q_pos0.data_ptr(), kv_len.data_ptr(), nseq, ql, Hq, Hkv, D, bs,
+                               1 / math.sqrt(D), out.data_ptr(), st)
+        assert rc == 0
+    us = timeit(fn)
+    nbytes = nseq * (ctx + ql) * Hkv * D * 2 * 2 + q.numel() * 2 * 2
+    report(f"attention {tag}", f"seqs={nseq} q={ql} ctx={ctx} D={D}", us, nbytes)
+
+
+def norm_case(tag, M, H, S):
+    x = torch.randn(M, H, device=dev).to(bf)
+    P = torch.randn(S * M * H, device=dev)
+    w = torch.ones(H, device=dev).to(bf)
+    y = torch.empty_like(x)
+    st = torch.cuda.current_stream().cuda_stream
+
+    def fn():
+        rc = lib.psd_add_rmsnorm(x.data_ptr(), H, P.data_ptr(), S, M * H, H, None, w.data_ptr(),
+                                 y.data_ptr(), H, M, H, 1e-5, 1, st)
+        assert rc == 0
+    us = timeit(fn)
+    report(f"add_rmsnorm {tag}", f"M={M} H={H} S={S}", us, M * H * (2 + 2 + 2 + 4 * S))
+
+
+def rope_case(tag, M, Hq, Hkv, D, S):
+    N = (Hq + 2 * Hkv) * D
+    P = torch.randn(S * M * N, device=dev)
+    q = torch.empty(M, Hq, D, dtype=bf, device=dev)
+    kc = torch.empty(M + 16, Hkv, D, dtype=bf, device=dev)
+    vc = torch.empty_like(kc)
+    pos = torch.arange(M, dtype=torch.int32, device=dev) + 100
+    slots = torch.arange(M, dtype=torch.int32, device=dev)
+    inv = torch.rand(D // 2, device=dev) * 0.5
+    st = torch.cuda.current_stream().cuda_stream
+
+    def fn():
+        rc = lib.psd_rope_kv(P.data_ptr(), S, M * N, M, Hq, Hkv, D, pos.data_ptr(),
+                             slots.data_ptr(), inv.data_ptr(), None, q.data_ptr(), kc.data_ptr(),
+                             vc.data_ptr(), st)
+        assert rc == 0
+    us = timeit(fn)
+    report(f"rope_kv {tag}", f"M={M} S={S}", us, M * N * 4 * S + M * N * 2)
+
+
+def verify_case(tag, B, K, V, sampling):
+    sets = [make_inputs(B, K, V, sampling, dev, seed=i) for i in range(3)]
+    it = [0]
+
+    def fn():
+        t, d, ids, ln, u = sets[it[0] % 3]
+        it[0] += 1
+        if sampling:
+            ops.verify_sample(t, d, ids, ln, u)
+        else:
+            ops.verify_greedy(t, ids, ln)
+    us = timeit(fn)
+    report(f"K1 {tag}", f"B={B} k={K} V={V}", us, algorithmic_bytes(B, K, V, sampling))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--json", default=None)
+    ap.add_argument("--only", default="")
+    a = ap.parse_args()
+    sel = a.only.split(",") if a.only else None
+
+    def want(k):
+        return sel is None or k in sel
+    if want("gemm"):
+        # 8B verify (M = 32 x 6)
+        gemm_case("8B qkv", 192, 6144, 4096, "partial")
+        gemm_case("8B o", 192, 4096, 4096, "partial")
+        gemm_case("8B gate/up", 192, 28672, 4096, "silu")
+        gemm_case("8B down", 192, 4096, 14336, "partial")
+        gemm_case("8B lm_head", 192, 128256, 4096, "f32", copies=2)
+        # 1B draft (M = 32, first step 64)
+        gemm_case("1B qkv", 32, 3072, 2048, "partial")
+        gemm_case("1B o", 32, 2048, 2048, "partial")
+        gemm_case("1B gate/up", 32, 16384, 2048, "silu")
+        gemm_case("1B down", 32, 2048, 8192, "partial")
+        gemm_case("1B lm_head", 32, 128256, 2048, "f32", copies=2)
+        gemm_case("1B gate/up M64", 64, 16384, 2048, "silu")
+    if want("attn"):
+        attn_case("8B verify", 32, 6, 300, 32, 8, 128)
+        attn_case("1B draft", 32, 1, 300, 32, 8, 64)
+        attn_case("1B draft step0", 32, 2, 300, 32, 8, 64)
+    if want("norm"):
+        norm_case("8B", 192, 4096, 4)
+        norm_case("1B", 32, 2048, 6)
+        rope_case("8B", 192, 32, 8, 128, 3)
+        rope_case("1B", 32, 32, 8, 64, 6)
+    if want("k1"):
+        verify_case("greedy cfg2", 32, 5, 128256, False)
+        verify_case("sample cfg2", 32, 5, 128256, True)
+        verify_case("draft argmax", 32, 0, 128256, False)
+    if a.json:
+        json.dump({"peak_gbps": PEAK, "rows": rows}, open(a.json, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
