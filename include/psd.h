@@ -68,8 +68,11 @@ int psd_verify_sample(const float* target_logits, int64_t t_stride_b, int64_t t_
  * acc + R, Y may alias R), PSD_EPI_SILU (W rows packed per 128-row tile as 64
  * gate rows then the 64 matching up rows; Y [M, N/2] bf16 = silu(g) * u).
  * N must be a multiple of 128, K and the leading dims multiples of 8.
- * splits_hint 0 = automatic split-K (fp32 partials in `workspace`, sized by
- * psd_gemm_plan; with too little workspace fewer splits are used). */
+ * splits_hint 0 (default) = stream-K persistent kernel: one CTA per SM,
+ * balanced weight k-blocks per SM, cut tiles finished by their last-arriving
+ * contributor; `workspace` (psd_gemm_plan bytes) must be ZEROED once at
+ * allocation and not shared by concurrently running GEMMs (it is left zeroed).
+ * splits_hint >= 1 = legacy grid split-K (fp32 partials + reduction). */
 #define PSD_EPI_BF16 0
 #define PSD_EPI_F32 1
 #define PSD_EPI_RESID 2
@@ -96,12 +99,12 @@ int psd_embed(const int32_t* tokens, int M, const void* table, int H, void* out,
 int psd_add_rmsnorm(void* x, int ldx, const float* partials, int S, size_t slice, int ldp,
                     const int32_t* rows, const void* w, void* y, int ldy, int M, int H, float eps,
                     int write_back, void* stream);
-/* qkv = bf16(sum_z qkv_partials[z*slice + m*(Hq+2Hkv)D + j]) (+ optional bias)
- * -> rotate-half RoPE on q, k; q -> q_out [M, Hq, D]; k, v -> caches
- * [blocks*block_size, Hkv, D] at slot slots[m] (negative: not written). */
-int psd_rope_kv(const float* qkv_partials, int S, size_t slice, int M, int Hq, int Hkv, int D,
-                const int32_t* positions, const int32_t* slots, const float* inv_freq,
-                const void* qkv_bias, void* q_out, void* k_cache, void* v_cache, void* stream);
+/* qkv [M, (Hq+2Hkv) D] bf16 (+ optional bias) -> rotate-half RoPE on q, k;
+ * q -> q_out [M, Hq, D]; k, v -> caches [blocks*block_size, Hkv, D] at slot
+ * slots[m] (negative: not written). */
+int psd_rope_kv(const void* qkv, int M, int Hq, int Hkv, int D, const int32_t* positions,
+                const int32_t* slots, const float* inv_freq, const void* qkv_bias, void* q_out,
+                void* k_cache, void* v_cache, void* stream);
 /* Paged multi-query attention, GQA.  Sequence s: query tokens q_start[s] ..
  * +q_len[s]-1 at positions q_pos0[s] + t; token t attends keys
  * 0 .. min(q_pos0[s] + t, kv_len[s] - 1) read through

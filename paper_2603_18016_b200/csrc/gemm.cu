@@ -25,6 +25,7 @@
 // Epilogues: bf16 store, fp32 store (LM-head logits), residual add (x += W o),
 // fused SiLU(gate) * up (weights packed gate/up per 64-row half tile).
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "../../include/psd.h"
@@ -36,10 +37,18 @@ using namespace psd;
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int kThreads = 192;
-constexpr int kPrefetch = 0;  // k-blocks of weights prefetched into L2 ahead of use (0 = off;
-                               // measured slower on B200: the TMA issue slots are the cost)
+// weight k-blocks prefetched into L2 ahead of the smem ring; 0 = off.
+// PSD_GEMM_PREFETCH overrides (tuning experiments)
+int prefetch_depth() {
+  static int v = [] {
+    const char* e = getenv("PSD_GEMM_PREFETCH");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
 
 struct GemmArgs {
+  int prefetch;  // weight k-blocks prefetched into L2 ahead of the smem ring
   int M, N, K;
   int kb_total, kb_per_split;
   void* Y;
@@ -105,12 +114,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUt
       const uint64_t pol_x = policy_evict_last();
       const uint64_t pol_pf = policy_evict_last();
       // L2 prefetch runs kPrefetch k-blocks ahead of the smem ring
-      const int npf = kPrefetch > 0 ? min(nkb, kPrefetch) : 0;
+      const int pf = g.prefetch;
+      const int npf = pf > 0 ? min(nkb, pf) : 0;
       for (int i = 0; i < npf; ++i) tma_prefetch_l2_2d(&tmW, (kb0 + i) * BK, n0, pol_pf);
       for (int i = 0; i < nkb; ++i) {
         const int s = i % C::STAGES;
         const uint32_t ph = (i / C::STAGES) & 1;
-        if (kPrefetch > 0 && i + kPrefetch < nkb) tma_prefetch_l2_2d(&tmW, (kb0 + i + kPrefetch) * BK, n0, pol_pf);
+        if (pf > 0 && i + pf < nkb) tma_prefetch_l2_2d(&tmW, (kb0 + i + pf) * BK, n0, pol_pf);
         mbar_wait(empty + s, ph ^ 1);
         mbar_arrive_expect_tx(full + s, C::STAGE);
         const int kc = (kb0 + i) * BK;
@@ -197,6 +207,265 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUt
   if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
 }
 
+// ---- stream-K persistent variant ---------------------------------------------
+// Work = tiles x k-blocks "units" in tile-major order (tile t = n_tile * MT +
+// m_tile, so neighbouring units share weights); CTA c of G takes units
+// [c U / G, (c+1) U / G).  Every SM gets the same number of weight k-blocks,
+// so there are no wave-quantisation tails (224 gate/up tiles on 148 SMs
+// would otherwise run 1.51 waves) and no separate split-K launch.  A tile cut
+// by a CTA boundary is finished by whichever of its contributors arrives
+// last (atomic ticket): it sums every contributor's fp32 partial in CTA order
+// (deterministic), applies the epilogue and resets the ticket.  Nobody waits,
+// so concurrent persistent kernels on two streams cannot deadlock.  The TMEM
+// accumulator is double buffered: segment j+1's MMAs overlap j's epilogue.
+struct SKArgs {
+  int M, N, K;
+  int KB, MT, tiles, G;
+  long long U;
+  void* Y;
+  int ldy;
+  const __nv_bfloat16* R;
+  int ldr;
+  float* part;    // [G][2][BN * 128]
+  int* tickets;   // [tiles], zero between launches
+};
+
+struct Seg {
+  int t, kb0, kb1, first;  // tile, k-block range, is the CTA's first segment
+};
+
+__device__ __forceinline__ long long sk_bound(long long c, const SKArgs& g) {
+  return c * g.U / g.G;
+}
+// CTA holding unit u
+__device__ __forceinline__ int sk_owner(long long u, const SKArgs& g) {
+  long long c = u * g.G / g.U;
+  while (c + 1 < g.G && sk_bound(c + 1, g) <= u) ++c;
+  while (c > 0 && sk_bound(c, g) > u) --c;
+  return (int)c;
+}
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+               const SKArgs g) {
+  using C = Cfg<BN>;
+  constexpr int ACC_COLS = BN;  // one accumulator slot
+  constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
+                                         : 2 * BN <= 256 ? 256 : 512;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;   // [2] accumulator ready
+  uint64_t* tempty = tfull + 2;          // [2] accumulator drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* s_flag = reinterpret_cast<int*>(tmem_slot + 1);
+  float* xchg = reinterpret_cast<float*>(full + 32);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x;
+  const long long u0 = sk_bound(c, g), u1 = sk_bound(c + 1, g);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmW);
+    tma_prefetch(&tmX);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull + a, 1);
+      mbar_init(tempty + a, 4);  // one arrive per epilogue warp
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // segment iterator (identical sequence in every role)
+  auto next_seg = [&](long long& u, Seg& sg) -> bool {
+    if (u >= u1) return false;
+    sg.t = (int)(u / g.KB);
+    sg.kb0 = (int)(u % g.KB);
+    sg.kb1 = (int)min((long long)g.KB, sg.kb0 + (u1 - u));
+    sg.first = u == u0;
+    u += sg.kb1 - sg.kb0;
+    return true;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_w = policy_evict_first();
+      const uint64_t pol_x = policy_evict_last();
+      long long u = u0;
+      Seg sg;
+      int i = 0;
+      while (next_seg(u, sg)) {
+        const int n0 = (sg.t / g.MT) * BM, m0 = (sg.t % g.MT) * BN;
+        for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++i) {
+          const int s = i % C::STAGES;
+          const uint32_t ph = (i / C::STAGES) & 1;
+          mbar_wait(empty + s, ph ^ 1);
+          mbar_arrive_expect_tx(full + s, C::STAGE);
+          tma_load_2d(sA + s * C::A_BYTES, &tmW, full + s, kb * BK, n0, pol_w);
+          tma_load_2d(sB + s * C::B_BYTES, &tmX, full + s, kb * BK, m0, pol_x);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+      long long u = u0;
+      Seg sg;
+      int i = 0, j = 0;
+      while (next_seg(u, sg)) {
+        const int a = j & 1;
+        const uint32_t aph = (j >> 1) & 1;
+        mbar_wait(tempty + a, aph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + a * ACC_COLS;
+        for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++i) {
+          const int s = i % C::STAGES;
+          const uint32_t ph = (i / C::STAGES) & 1;
+          mbar_wait(full + s, ph);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(sA + s * C::A_BYTES);
+          const uint32_t sb = smem_u32(sB + s * C::B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            mma_bf16(d, umma_desc_sw128(sa + kk * 32), umma_desc_sw128(sb + kk * 32), idesc,
+                     (kb != sg.kb0 || kk != 0) ? 1u : 0u);
+          mma_commit(empty + s);
+        }
+        mma_commit(tfull + a);
+        ++j;
+      }
+    }
+    __syncwarp();
+  } else {
+    const int q = warp & 3;
+    const int row = 32 * q + lane;  // tile row (weight row) of this thread
+    long long u = u0;
+    Seg sg;
+    int j = 0;
+    while (next_seg(u, sg)) {
+      const int a = j & 1;
+      const uint32_t aph = (j >> 1) & 1;
+      mbar_wait(tfull + a, aph);
+      tc_fence_after();
+      const uint32_t tbase = tmem + a * ACC_COLS + ((uint32_t)(32 * q) << 16);
+      const int n0 = (sg.t / g.MT) * BM, m0 = (sg.t % g.MT) * BN;
+      const bool split = sg.kb0 != 0 || sg.kb1 != g.KB;
+      int owner = c, last = c;
+      bool finisher = true;
+      if (split) {
+        // publish this segment's partial, take a ticket
+        owner = sk_owner((long long)sg.t * g.KB, g);
+        last = sk_owner((long long)sg.t * g.KB + g.KB - 1, g);
+        float* mine = g.part + ((size_t)c * 2 + (sg.first ? 0 : 1)) * (BN * BM);
+#pragma unroll 1
+        for (int col = 0; col < BN; col += 16) {
+          uint32_t r[16];
+          tmem_ld16(tbase + (uint32_t)col, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int k = 0; k < 16; ++k) mine[(col + k) * BM + row] = __uint_as_float(r[k]);
+        }
+        __threadfence();
+        named_bar_sync(1, 128);
+        if (threadIdx.x == 64) {
+          const int tk = atomicAdd(g.tickets + sg.t, 1);
+          *s_flag = tk == last - owner;
+        }
+        named_bar_sync(1, 128);
+        finisher = *s_flag;
+        if (finisher) __threadfence();
+      }
+      if (finisher) {
+#pragma unroll 1
+        for (int col = 0; col < BN; col += 16) {
+          uint32_t r[16];
+          tmem_ld16(tbase + (uint32_t)col, r);
+          tmem_ld_wait();
+          float v[16];
+          if (split) {
+            // sum contributors in CTA order (own values from TMEM)
+#pragma unroll
+            for (int k = 0; k < 16; ++k) v[k] = 0.f;
+            for (int cc = owner; cc <= last; ++cc) {
+              if (cc == c) {
+#pragma unroll
+                for (int k = 0; k < 16; ++k) v[k] += __uint_as_float(r[k]);
+              } else {
+                const bool first_of_cc = sk_bound(cc, g) >= (long long)sg.t * g.KB;
+                const float* pp = g.part + ((size_t)cc * 2 + (first_of_cc ? 0 : 1)) * (BN * BM);
+#pragma unroll
+                for (int k = 0; k < 16; ++k) v[k] += __ldcg(pp + (col + k) * BM + row);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(r[k]);
+          }
+          if constexpr (EPI == PSD_EPI_SILU) {
+            if (q >= 2) {
+#pragma unroll
+              for (int k = 0; k < 16; ++k) xchg[((q - 2) * 32 + lane) * 17 + k] = v[k];
+            }
+            named_bar_sync(1, 128);
+            if (q < 2) {
+              const int jo = (n0 / BM) * 64 + 32 * q + lane;
+              __nv_bfloat16* Y = static_cast<__nv_bfloat16*>(g.Y);
+#pragma unroll
+              for (int k = 0; k < 16; ++k) {
+                const int m = m0 + col + k;
+                if (m < g.M)
+                  Y[(size_t)m * g.ldy + jo] =
+                      __float2bfloat16(silu(v[k]) * xchg[(q * 32 + lane) * 17 + k]);
+              }
+            }
+            named_bar_sync(1, 128);
+          } else {
+            const int n = n0 + row;
+            if (n < g.N) {
+#pragma unroll
+              for (int k = 0; k < 16; ++k) {
+                const int m = m0 + col + k;
+                if (m >= g.M) break;
+                if constexpr (EPI == PSD_EPI_F32) {
+                  static_cast<float*>(g.Y)[(size_t)m * g.ldy + n] = v[k];
+                } else if constexpr (EPI == PSD_EPI_RESID) {
+                  __nv_bfloat16* Y = static_cast<__nv_bfloat16*>(g.Y);
+                  const float rv = __bfloat162float(g.R[(size_t)m * g.ldr + n]);
+                  Y[(size_t)m * g.ldy + n] = __float2bfloat16(v[k] + rv);
+                } else {
+                  static_cast<__nv_bfloat16*>(g.Y)[(size_t)m * g.ldy + n] = __float2bfloat16(v[k]);
+                }
+              }
+            }
+          }
+        }
+        if (split && threadIdx.x == 64) g.tickets[sg.t] = 0;  // reusable next launch
+      }
+      // release this accumulator slot
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + a);
+      ++j;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
+}
+
 // ---- split-K reduction with the same epilogues ------------------------------
 __global__ void gemm_reduce_kernel(const float* __restrict__ P, int splits, int M, int N, int epi,
                                    void* Y, int ldy, const __nv_bfloat16* R, int ldr) {
@@ -279,18 +548,32 @@ int launch_bn(const CUtensorMap& mw, const CUtensorMap& mx, const GemmArgs& g, d
   return (int)cudaGetLastError();
 }
 
+template <int BN, int EPI>
+int launch_sk_bn(const CUtensorMap& mw, const CUtensorMap& mx, const SKArgs& g, cudaStream_t st) {
+  using C = Cfg<BN>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_sk_kernel<BN, EPI>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return (int)e;
+    attr_done = true;
+  }
+  gemm_sk_kernel<BN, EPI><<<g.G, kThreads, C::SMEM, st>>>(mw, mx, g);
+  return (int)cudaGetLastError();
+}
+
 template <int EPI>
-int launch_epi(int bn, const CUtensorMap& mw, const CUtensorMap& mx, const GemmArgs& g, dim3 grid,
-               cudaStream_t st) {
+int launch_sk(int bn, const CUtensorMap& mw, const CUtensorMap& mx, const SKArgs& g,
+              cudaStream_t st) {
   switch (bn) {
-    case 32: return launch_bn<32, EPI>(mw, mx, g, grid, st);
-    case 64: return launch_bn<64, EPI>(mw, mx, g, grid, st);
-    case 96: return launch_bn<96, EPI>(mw, mx, g, grid, st);
-    case 128: return launch_bn<128, EPI>(mw, mx, g, grid, st);
-    case 160: return launch_bn<160, EPI>(mw, mx, g, grid, st);
-    case 192: return launch_bn<192, EPI>(mw, mx, g, grid, st);
-    case 224: return launch_bn<224, EPI>(mw, mx, g, grid, st);
-    case 256: return launch_bn<256, EPI>(mw, mx, g, grid, st);
+    case 32: return launch_sk_bn<32, EPI>(mw, mx, g, st);
+    case 64: return launch_sk_bn<64, EPI>(mw, mx, g, st);
+    case 96: return launch_sk_bn<96, EPI>(mw, mx, g, st);
+    case 128: return launch_sk_bn<128, EPI>(mw, mx, g, st);
+    case 160: return launch_sk_bn<160, EPI>(mw, mx, g, st);
+    case 192: return launch_sk_bn<192, EPI>(mw, mx, g, st);
+    case 224: return launch_sk_bn<224, EPI>(mw, mx, g, st);
+    case 256: return launch_sk_bn<256, EPI>(mw, mx, g, st);
   }
   return (int)cudaErrorInvalidValue;
 }
@@ -308,6 +591,52 @@ int token_tile(int M) {
   }
   return std::max(32, (M + 31) / 32 * 32);
 }
+
+int num_sms() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+// stream-K geometry + workspace bytes (partials, then tickets)
+struct SKPlan {
+  int bn, KB, MT, tiles, G;
+  long long U;
+  size_t part_bytes, ticket_bytes;
+};
+SKPlan sk_plan(int M, int N, int K) {
+  SKPlan p;
+  p.bn = token_tile(M);
+  p.KB = (K + BK - 1) / BK;
+  p.MT = (M + p.bn - 1) / p.bn;
+  p.tiles = (N / BM) * p.MT;
+  p.U = (long long)p.tiles * p.KB;
+  p.G = (int)std::min<long long>(num_sms(), p.U);
+  p.part_bytes = (size_t)p.G * 2 * p.bn * BM * sizeof(float);
+  p.ticket_bytes = ((size_t)p.tiles * sizeof(int) + 255) & ~size_t(255);
+  return p;
+}
+
+template <int EPI>
+int launch_epi(int bn, const CUtensorMap& mw, const CUtensorMap& mx, const GemmArgs& g, dim3 grid,
+               cudaStream_t st) {
+  switch (bn) {
+    case 32: return launch_bn<32, EPI>(mw, mx, g, grid, st);
+    case 64: return launch_bn<64, EPI>(mw, mx, g, grid, st);
+    case 96: return launch_bn<96, EPI>(mw, mx, g, grid, st);
+    case 128: return launch_bn<128, EPI>(mw, mx, g, grid, st);
+    case 160: return launch_bn<160, EPI>(mw, mx, g, grid, st);
+    case 192: return launch_bn<192, EPI>(mw, mx, g, grid, st);
+    case 224: return launch_bn<224, EPI>(mw, mx, g, grid, st);
+    case 256: return launch_bn<256, EPI>(mw, mx, g, grid, st);
+  }
+  return (int)cudaErrorInvalidValue;
+}
+
 
 }  // namespace
 
@@ -328,8 +657,14 @@ int psd_gemm_plan(int M, int N, int K, int epi, int splits_hint, int* splits_out
   const int per = (kb_total + splits - 1) / splits;
   splits = (kb_total + per - 1) / per;
   if (splits_out) *splits_out = splits;
-  if (workspace_bytes) *workspace_bytes = splits > 1 ? (size_t)splits * M * N * sizeof(float) : 0;
-  (void)epi;
+  if (workspace_bytes) {
+    if (splits_hint == 0 && epi != PSD_EPI_PARTIAL) {
+      const SKPlan p = sk_plan(M, N, K);  // stream-K path
+      *workspace_bytes = p.part_bytes + p.ticket_bytes;
+    } else {
+      *workspace_bytes = splits > 1 ? (size_t)splits * M * N * sizeof(float) : 0;
+    }
+  }
   return 0;
 }
 
@@ -351,6 +686,7 @@ int psd_gemm_partials(const void* X, int ldx, int M, int K, const void* W, int l
   if ((rc = make_map(&mw, W, N, K, ldw, BM))) return rc;
   if ((rc = make_map(&mx, X, M, K, ldx, bn))) return rc;
   GemmArgs g;
+  g.prefetch = prefetch_depth();
   g.M = M; g.N = N; g.K = K;
   g.kb_total = (K + BK - 1) / BK;
   g.kb_per_split = (g.kb_total + splits - 1) / splits;
@@ -369,6 +705,31 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
   if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(W)) & 15)
     return (int)cudaErrorMisalignedAddress;
   if ((ldx % 8) || (ldw % 8)) return (int)cudaErrorMisalignedAddress;
+  if (splits_hint == 0) {
+    // stream-K persistent path (default)
+    if (M <= 0 || N <= 0 || K <= 0 || (K % 8) || (N % BM)) return (int)cudaErrorInvalidValue;
+    const SKPlan p = sk_plan(M, N, K);
+    if (!workspace || workspace_bytes < p.part_bytes + p.ticket_bytes)
+      return (int)cudaErrorInvalidValue;
+    CUtensorMap mw, mx;
+    int rc;
+    if ((rc = make_map(&mw, W, N, K, ldw, BM))) return rc;
+    if ((rc = make_map(&mx, X, M, K, ldx, p.bn))) return rc;
+    SKArgs g;
+    g.M = M; g.N = N; g.K = K;
+    g.KB = p.KB; g.MT = p.MT; g.tiles = p.tiles; g.G = p.G; g.U = p.U;
+    g.Y = Y; g.ldy = ldy; g.R = static_cast<const __nv_bfloat16*>(R); g.ldr = ldr;
+    g.part = static_cast<float*>(workspace);
+    g.tickets = reinterpret_cast<int*>(static_cast<char*>(workspace) + p.part_bytes);
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (epi) {
+      case PSD_EPI_BF16: return launch_sk<PSD_EPI_BF16>(p.bn, mw, mx, g, st);
+      case PSD_EPI_F32: return launch_sk<PSD_EPI_F32>(p.bn, mw, mx, g, st);
+      case PSD_EPI_RESID: return launch_sk<PSD_EPI_RESID>(p.bn, mw, mx, g, st);
+      case PSD_EPI_SILU: return launch_sk<PSD_EPI_SILU>(p.bn, mw, mx, g, st);
+    }
+    return (int)cudaErrorInvalidValue;
+  }
   int splits = 1;
   size_t need = 0;
   int rc = psd_gemm_plan(M, N, K, epi, splits_hint, &splits, &need);
@@ -385,6 +746,7 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
   if ((rc = make_map(&mw, W, N, K, ldw, BM))) return rc;
   if ((rc = make_map(&mx, X, M, K, ldx, bn))) return rc;
   GemmArgs g;
+  g.prefetch = prefetch_depth();
   g.M = M; g.N = N; g.K = K;
   g.kb_total = (K + BK - 1) / BK;
   g.kb_per_split = (g.kb_total + splits - 1) / splits;

@@ -45,7 +45,7 @@ __global__ void embed_kernel(const int32_t* __restrict__ tok, const __nv_bfloat1
 constexpr int NORM_THREADS = 256;
 constexpr int NORM_MAX_PER_THREAD = 32;  // H <= 8192
 
-template <int NV>  // NV = float2 pairs per thread (H / 2 / NORM_THREADS rounded up)
+template <int NV>  // NV = 8-wide chunks per thread (H / 8 / NORM_THREADS rounded up)
 __global__ void __launch_bounds__(NORM_THREADS)
 add_rmsnorm_kernel(__nv_bfloat16* __restrict__ x, int ldx, const float* __restrict__ P, int S,
                    size_t slice, int ldp, const int32_t* __restrict__ rows,
@@ -53,29 +53,41 @@ add_rmsnorm_kernel(__nv_bfloat16* __restrict__ x, int ldx, const float* __restri
                    int H, float eps, int write_back) {
   const int m = blockIdx.x;
   const int src = rows ? rows[m] : m;
-  __nv_bfloat162* xr = reinterpret_cast<__nv_bfloat162*>(x + (size_t)src * ldx);
-  const float2* pr = P ? reinterpret_cast<const float2*>(P + (size_t)src * ldp) : nullptr;
-  const size_t slice2 = slice / 2;
-  float2 v[NV];
+  __nv_bfloat16* xr = x + (size_t)src * ldx;
+  const float* pr = P ? P + (size_t)src * ldp : nullptr;
+  float v[NV][8];
   float ss = 0.f;
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
-    const int i = threadIdx.x + k * NORM_THREADS;
-    if (i < H / 2) {
-      float2 xv = __bfloat1622float2(xr[i]);
+    const int e = (threadIdx.x + k * NORM_THREADS) * 8;
+    if (e < H) {
+      uint4 u = *reinterpret_cast<const uint4*>(xr + e);
+      const __nv_bfloat16* b8 = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) v[k][t] = __bfloat162float(b8[t]);
       if (pr) {
-        float2 acc = pr[i];
+        float acc[8];
+        const float4* p4 = reinterpret_cast<const float4*>(pr + e);
+        float4 a0 = p4[0], a1 = p4[1];
+        acc[0] = a0.x; acc[1] = a0.y; acc[2] = a0.z; acc[3] = a0.w;
+        acc[4] = a1.x; acc[5] = a1.y; acc[6] = a1.z; acc[7] = a1.w;
         for (int z = 1; z < S; ++z) {
-          const float2 pz = pr[z * slice2 + i];
-          acc.x += pz.x;
-          acc.y += pz.y;
+          const float4* pz = reinterpret_cast<const float4*>(pr + z * slice + e);
+          const float4 c0 = pz[0], c1 = pz[1];
+          acc[0] += c0.x; acc[1] += c0.y; acc[2] += c0.z; acc[3] += c0.w;
+          acc[4] += c1.x; acc[5] += c1.y; acc[6] += c1.z; acc[7] += c1.w;
         }
-        const __nv_bfloat162 nb = __floats2bfloat162_rn(acc.x + xv.x, acc.y + xv.y);
-        if (write_back) xr[i] = nb;
-        xv = __bfloat1622float2(nb);
+        uint4 o;
+        __nv_bfloat16* o8 = reinterpret_cast<__nv_bfloat16*>(&o);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          o8[t] = __float2bfloat16(acc[t] + v[k][t]);
+          v[k][t] = __bfloat162float(o8[t]);
+        }
+        if (write_back) *reinterpret_cast<uint4*>(xr + e) = o;
       }
-      v[k] = xv;
-      ss += xv.x * xv.x + xv.y * xv.y;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) ss += v[k][t] * v[k][t];
     }
   }
   __shared__ float red[32];
@@ -89,14 +101,18 @@ add_rmsnorm_kernel(__nv_bfloat16* __restrict__ x, int ldx, const float* __restri
   }
   __syncthreads();
   const float inv = rsqrtf(red[0] / H + eps);
-  const __nv_bfloat162* wr = reinterpret_cast<const __nv_bfloat162*>(w);
-  __nv_bfloat162* yr = reinterpret_cast<__nv_bfloat162*>(y + (size_t)m * ldy);
+  __nv_bfloat16* yr = y + (size_t)m * ldy;
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
-    const int i = threadIdx.x + k * NORM_THREADS;
-    if (i < H / 2) {
-      const float2 g = __bfloat1622float2(wr[i]);
-      yr[i] = __floats2bfloat162_rn(v[k].x * inv * g.x, v[k].y * inv * g.y);
+    const int e = (threadIdx.x + k * NORM_THREADS) * 8;
+    if (e < H) {
+      uint4 wu = *reinterpret_cast<const uint4*>(w + e);
+      const __nv_bfloat16* w8 = reinterpret_cast<const __nv_bfloat16*>(&wu);
+      uint4 o;
+      __nv_bfloat16* o8 = reinterpret_cast<__nv_bfloat16*>(&o);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) o8[t] = __float2bfloat16(v[k][t] * inv * __bfloat162float(w8[t]));
+      *reinterpret_cast<uint4*>(yr + e) = o;
     }
   }
 }
@@ -104,27 +120,20 @@ add_rmsnorm_kernel(__nv_bfloat16* __restrict__ x, int ldx, const float* __restri
 // ---- RoPE + paged KV write ------------------------------------------------------
 // qkv [M, (Hq + 2 Hkv) D]; q_out [M, Hq, D]; caches [blocks, bs, Hkv, D].
 // rotate-half convention: pairs (i, i + D/2), angle = pos * inv_freq[i].
-// qkv value j of token m: bf16(sum_s P[s][m][j]) -- the QKV GEMM's split-K
-// partials are reduced here
-__device__ __forceinline__ float qkv_at(const float* __restrict__ P, int S, size_t slice,
-                                        size_t off) {
-  float acc = 0.f;
-  for (int z = 0; z < S; ++z) acc += P[z * slice + off];
-  return __bfloat162float(__float2bfloat16(acc));
-}
-
-__global__ void rope_kv_kernel(const float* __restrict__ P, int S, size_t slice, int Hq, int Hkv,
-                               int D, const int32_t* __restrict__ pos,
-                               const int32_t* __restrict__ slot,
-                               const float* __restrict__ inv_freq,
-                               const __nv_bfloat16* __restrict__ bias,
-                               __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ kc,
-                               __nv_bfloat16* __restrict__ vc) {
+// One CTA per token.  Work item = (head, 8-wide chunk of the first half):
+// one 16-byte load of x[i..i+7] and one of x[i+half..], 8 rotations, 16-byte
+// stores -- every load of a thread is independent (no serial latency chain).
+__global__ void __launch_bounds__(256)
+rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, int Hq, int Hkv, int D,
+               const int32_t* __restrict__ pos, const int32_t* __restrict__ slot,
+               const float* __restrict__ inv_freq, const __nv_bfloat16* __restrict__ bias,
+               __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ kc,
+               __nv_bfloat16* __restrict__ vc) {
   const int m = blockIdx.x;
   const int p = pos[m];
   const int s = slot[m];
   const int half = D / 2;
-  const int nh = Hq + Hkv;  // heads that get rotated
+  const int cpr = half / 8;  // 8-wide chunks per half row
   __shared__ float s_cos[128], s_sin[128];
   for (int i = threadIdx.x; i < half; i += blockDim.x) {
     float sn, cs;
@@ -133,37 +142,46 @@ __global__ void rope_kv_kernel(const float* __restrict__ P, int S, size_t slice,
     s_sin[i] = sn;
   }
   __syncthreads();
-  const size_t row = (size_t)m * (Hq + 2 * Hkv) * D;
-  for (int idx = threadIdx.x; idx < nh * half; idx += blockDim.x) {
-    const int h = idx / half, i = idx % half;
-    if (h >= Hq && s < 0) continue;
-    const float cs = s_cos[i], sn = s_sin[i];
-    float a = qkv_at(P, S, slice, row + h * D + i);
-    float b = qkv_at(P, S, slice, row + h * D + i + half);
-    if (bias) {  // qkv bias (Qwen2), rounded to bf16 like the projection output
-      a = __bfloat162float(__float2bfloat16(a + __bfloat162float(bias[h * D + i])));
-      b = __bfloat162float(__float2bfloat16(b + __bfloat162float(bias[h * D + i + half])));
+  const __nv_bfloat16* row = qkv + (size_t)m * (Hq + 2 * Hkv) * D;
+  const int nrot = (s >= 0 ? Hq + Hkv : Hq) * cpr;
+  const int nv = s >= 0 ? Hkv * D / 8 : 0;
+  for (int idx = threadIdx.x; idx < nrot + nv; idx += blockDim.x) {
+    if (idx >= nrot) {  // V: straight copy (+ bias)
+      const int e = (idx - nrot) * 8;
+      uint4 v = *reinterpret_cast<const uint4*>(row + (size_t)(Hq + Hkv) * D + e);
+      if (bias) {
+        __nv_bfloat16* vv = reinterpret_cast<__nv_bfloat16*>(&v);
+        const __nv_bfloat16* bb = bias + (size_t)(Hq + Hkv) * D + e;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          vv[k] = __float2bfloat16(__bfloat162float(vv[k]) + __bfloat162float(bb[k]));
+      }
+      *reinterpret_cast<uint4*>(vc + (size_t)s * Hkv * D + e) = v;
+      continue;
     }
-    const __nv_bfloat16 r0 = __float2bfloat16(a * cs - b * sn);
-    const __nv_bfloat16 r1 = __float2bfloat16(b * cs + a * sn);
-    if (h < Hq) {
-      q_out[((size_t)m * Hq + h) * D + i] = r0;
-      q_out[((size_t)m * Hq + h) * D + i + half] = r1;
-    } else {
-      const size_t o = ((size_t)s * Hkv + (h - Hq)) * D;
-      kc[o + i] = r0;
-      kc[o + i + half] = r1;
+    const int h = idx / cpr, i0 = (idx % cpr) * 8;
+    uint4 ua = *reinterpret_cast<const uint4*>(row + h * D + i0);
+    uint4 ub = *reinterpret_cast<const uint4*>(row + h * D + i0 + half);
+    __nv_bfloat16* a8 = reinterpret_cast<__nv_bfloat16*>(&ua);
+    __nv_bfloat16* b8 = reinterpret_cast<__nv_bfloat16*>(&ub);
+    uint4 ra, rb;
+    __nv_bfloat16* ra8 = reinterpret_cast<__nv_bfloat16*>(&ra);
+    __nv_bfloat16* rb8 = reinterpret_cast<__nv_bfloat16*>(&rb);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      float a = __bfloat162float(a8[k]), b = __bfloat162float(b8[k]);
+      if (bias) {  // qkv bias (Qwen2), rounded to bf16 like the projection output
+        a = __bfloat162float(__float2bfloat16(a + __bfloat162float(bias[h * D + i0 + k])));
+        b = __bfloat162float(__float2bfloat16(b + __bfloat162float(bias[h * D + i0 + k + half])));
+      }
+      const float cs = s_cos[i0 + k], sn = s_sin[i0 + k];
+      ra8[k] = __float2bfloat16(a * cs - b * sn);
+      rb8[k] = __float2bfloat16(b * cs + a * sn);
     }
-  }
-  if (s >= 0) {
-    const size_t vrow = row + (size_t)(Hq + Hkv) * D;
-    __nv_bfloat16* vdst = vc + (size_t)s * Hkv * D;
-    const __nv_bfloat16* vb = bias ? bias + (size_t)(Hq + Hkv) * D : nullptr;
-    for (int idx = threadIdx.x; idx < Hkv * D; idx += blockDim.x) {
-      float v = qkv_at(P, S, slice, vrow + idx);
-      if (vb) v = __bfloat162float(__float2bfloat16(v + __bfloat162float(vb[idx])));
-      vdst[idx] = __float2bfloat16(v);
-    }
+    __nv_bfloat16* dst = h < Hq ? q_out + ((size_t)m * Hq + h) * D
+                                : kc + ((size_t)s * Hkv + (h - Hq)) * D;
+    *reinterpret_cast<uint4*>(dst + i0) = ra;
+    *reinterpret_cast<uint4*>(dst + i0 + half) = rb;
   }
 }
 
@@ -177,6 +195,7 @@ __global__ void rope_kv_kernel(const float* __restrict__ P, int S, size_t slice,
 constexpr int ATT_THREADS = 128;
 constexpr int ATT_MAXR = 64;   // query rows per CTA
 constexpr int ATT_STAGES = 4;  // K/V tiles in flight
+constexpr int ATT_MAX_BLOCKS = 512;  // block-table entries staged in smem (8192 tokens)
 
 __device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4],
                                                uint32_t b0, uint32_t b1) {
@@ -225,9 +244,14 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
   const int qs = q_start[seq];
   const int first_pos = q_pos0[seq];
   const int last_key = min(first_pos + t0 + nt - 1, kvl - 1);
-  const int* bt = block_table + (size_t)seq_slot[seq] * max_blocks;
+  const int* btg = block_table + (size_t)seq_slot[seq] * max_blocks;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, c = lane & 3;
+  // the sequence's block-table row, staged once (no dependent global load
+  // in front of every tile's cp.async)
+  __shared__ int bt[ATT_MAX_BLOCKS];
+  const int nblk_used = min(last_key / bs + 1, ATT_MAX_BLOCKS);
+  for (int i = tid; i < nblk_used; i += ATT_THREADS) bt[i] = btg[i];
 
   extern __shared__ __align__(16) uint8_t att_smem[];
   typedef __nv_bfloat16 Row[P];
@@ -259,6 +283,7 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
     cp_async_commit();
   };
   const int ntiles = last_key / KT + 1;
+  __syncthreads();  // bt staged
   // NS-stage cp.async ring: tiles 0 .. NS-2 in flight before the first use
 #pragma unroll
   for (int t = 0; t < NS - 1; ++t) {
@@ -519,28 +544,27 @@ int psd_add_rmsnorm(void* x, int ldx, const float* partials, int S, size_t slice
                     const int32_t* rows, const void* w, void* y, int ldy, int M, int H, float eps,
                     int write_back, void* stream) {
   if (M <= 0) return 0;
-  if (H % 2 || H > 2 * NORM_THREADS * NORM_MAX_PER_THREAD / 2) return (int)cudaErrorInvalidValue;
+  if (H % 8 || H > 8 * NORM_THREADS * 4) return (int)cudaErrorInvalidValue;
   auto go = [&](auto kern) {
     kern<<<M, NORM_THREADS, 0, (cudaStream_t)stream>>>(
         static_cast<__nv_bfloat16*>(x), ldx, partials, S, slice, ldp, rows,
         static_cast<const __nv_bfloat16*>(w), static_cast<__nv_bfloat16*>(y), ldy, H, eps,
         write_back);
   };
-  const int nv = (H / 2 + NORM_THREADS - 1) / NORM_THREADS;
-  if (nv <= 2) go(add_rmsnorm_kernel<2>);
-  else if (nv <= 4) go(add_rmsnorm_kernel<4>);
-  else if (nv <= 8) go(add_rmsnorm_kernel<8>);
-  else go(add_rmsnorm_kernel<16>);
+  const int nv = (H / 8 + NORM_THREADS - 1) / NORM_THREADS;
+  if (nv <= 1) go(add_rmsnorm_kernel<1>);
+  else if (nv <= 2) go(add_rmsnorm_kernel<2>);
+  else go(add_rmsnorm_kernel<4>);
   return (int)cudaGetLastError();
 }
 
-int psd_rope_kv(const float* qkv_partials, int S, size_t slice, int M, int Hq, int Hkv, int D,
-                const int32_t* positions, const int32_t* slots, const float* inv_freq,
-                const void* qkv_bias, void* q_out, void* k_cache, void* v_cache, void* stream) {
+int psd_rope_kv(const void* qkv, int M, int Hq, int Hkv, int D, const int32_t* positions,
+                const int32_t* slots, const float* inv_freq, const void* qkv_bias, void* q_out,
+                void* k_cache, void* v_cache, void* stream) {
   if (M <= 0) return 0;
-  if (D % 8 || D > 256) return (int)cudaErrorInvalidValue;
+  if (D % 16 || D > 256) return (int)cudaErrorInvalidValue;
   rope_kv_kernel<<<M, 256, 0, (cudaStream_t)stream>>>(
-      qkv_partials, S, slice, Hq, Hkv, D, positions, slots, inv_freq,
+      static_cast<const __nv_bfloat16*>(qkv), Hq, Hkv, D, positions, slots, inv_freq,
       static_cast<const __nv_bfloat16*>(qkv_bias), static_cast<__nv_bfloat16*>(q_out), static_cast<__nv_bfloat16*>(k_cache),
       static_cast<__nv_bfloat16*>(v_cache));
   return (int)cudaGetLastError();
@@ -554,7 +578,7 @@ int psd_attention(const void* q, const void* k_cache, const void* v_cache,
   if (num_seqs <= 0) return 0;
   if (Hq % Hkv) return (int)cudaErrorInvalidValue;
   const int G = Hq / Hkv;
-  if (G > ATT_MAXR) return (int)cudaErrorInvalidValue;
+  if (G > ATT_MAXR || max_blocks > ATT_MAX_BLOCKS) return (int)cudaErrorInvalidValue;
   const int tpc = ATT_MAXR / G;
   const int chunks = (max_q_len + tpc - 1) / tpc;
   dim3 grid(num_seqs, Hkv, chunks);

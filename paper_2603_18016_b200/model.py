@@ -238,20 +238,18 @@ class Forward:
         self.act = torch.empty(T, s.ffn_padded, dtype=bf, device=dev)
         self.xf = torch.empty(max_logit_rows, s.hidden, dtype=bf, device=dev)
         self.prev = torch.empty(max_logit_rows, dtype=torch.int32, device=dev)
-        self.ws = torch.empty(workspace_bytes, dtype=torch.uint8, device=dev)
-        # fp32 split-K partials of the QKV / O / down GEMMs (one buffer, reused
-        # in sequence: each is consumed before the next GEMM overwrites it)
+        # stream-K GEMM workspace (partials + tickets): zeroed once, left zeroed
         import ctypes
-        self._nsplit = ctypes.byref(ctypes.c_int(1))
-        need = 0
         lib = native.load()
-        for mm in sorted({T, max_logit_rows, min(T, 64), min(T, 320)}):
+        need = 0
+        for mm in sorted({T, max_logit_rows, min(T, 64), min(T, 320), 32, 2 * max_seqs}):
             for (n_out, k_in) in ((s.qkv_out, s.hidden), (s.hidden, s.heads * s.head_dim),
-                                  (s.hidden, s.ffn_padded)):
-                sp = ctypes.c_int()
-                lib.psd_gemm_plan(mm, n_out, k_in, native.EPI_PARTIAL, 0, ctypes.byref(sp), None)
-                need = max(need, sp.value * mm * n_out)
-        self.part = torch.empty(need, dtype=torch.float32, device=dev)
+                                  (2 * s.ffn_padded, s.hidden), (s.hidden, s.ffn_padded),
+                                  (s.vocab, s.hidden)):
+                wb = ctypes.c_size_t()
+                lib.psd_gemm_plan(mm, n_out, k_in, native.EPI_BF16, 0, None, ctypes.byref(wb))
+                need = max(need, wb.value)
+        self.ws = torch.zeros(max(need, 1 << 20), dtype=torch.uint8, device=dev)
         sizes = {"tokens": T, "positions": T, "slots": T, "seq_slot": max_seqs,
                  "q_start": max_seqs, "q_len": max_seqs, "q_pos0": max_seqs, "kv_len": max_seqs,
                  "logit_rows": max_logit_rows, "gather_src": T, "scatter_dst": max_logit_rows}
@@ -316,22 +314,19 @@ class Forward:
                            st), "psd_embed")
         scale = 1.0 / math.sqrt(s.head_dim)
         ws, wsn = self.ws.data_ptr(), self.ws.numel()
-        part, partn = self.part.data_ptr(), self.part.numel() * 4
-        nsp = self._nsplit
         Dq = s.heads * s.head_dim
         Fp = s.ffn_padded
-        prev_S = 0  # splits of the pending down-proj partials (0 = none)
+        X = self.x.data_ptr()
         for li, L in enumerate(m.layers):
             kc = m.kv[li, 0]
             vc = m.kv[li, 1]
-            # residual += down-proj partials of the previous layer; attn norm
-            _chk(lib.psd_add_rmsnorm(self.x.data_ptr(), H, part if prev_S else None, prev_S,
-                                     M * H, H, None, L["attn_norm"].data_ptr(),
-                                     self.xn.data_ptr(), H, M, H, s.rms_eps, 1, st), "add+norm")
-            _chk(lib.psd_gemm_partials(self.xn.data_ptr(), H, M, H, L["wqkv"].data_ptr(), H,
-                                       s.qkv_out, part, partn, 0, nsp, st), "gemm qkv")
-            _chk(lib.psd_rope_kv(part, nsp._obj.value, M * s.qkv_out, M, s.heads, s.kv_heads,
-                                 s.head_dim, v["positions"].data_ptr(), v["slots"].data_ptr(),
+            _chk(lib.psd_add_rmsnorm(X, H, None, 0, 0, H, None, L["attn_norm"].data_ptr(),
+                                     self.xn.data_ptr(), H, M, H, s.rms_eps, 0, st), "attn norm")
+            _chk(lib.psd_gemm_bf16(self.xn.data_ptr(), H, M, H, L["wqkv"].data_ptr(), H,
+                                   s.qkv_out, self.qkv.data_ptr(), s.qkv_out, native.EPI_BF16,
+                                   None, 0, 0, ws, wsn, st), "gemm qkv")
+            _chk(lib.psd_rope_kv(self.qkv.data_ptr(), M, s.heads, s.kv_heads, s.head_dim,
+                                 v["positions"].data_ptr(), v["slots"].data_ptr(),
                                  m.inv_freq.data_ptr(),
                                  L["bqkv"].data_ptr() if L["bqkv"] is not None else None,
                                  self.q.data_ptr(), kc.data_ptr(), vc.data_ptr(), st), "rope_kv")
@@ -342,23 +337,21 @@ class Forward:
                                    v["kv_len"].data_ptr(), n_seqs, max_q_len, s.heads,
                                    s.kv_heads, s.head_dim, m.block_size, scale,
                                    self.attn.data_ptr(), st), "attention")
-            _chk(lib.psd_gemm_partials(self.attn.data_ptr(), Dq, M, Dq, L["wo"].data_ptr(), Dq, H,
-                                       part, partn, 0, nsp, st), "gemm o")
-            _chk(lib.psd_add_rmsnorm(self.x.data_ptr(), H, part, nsp._obj.value, M * H, H, None,
-                                     L["mlp_norm"].data_ptr(), self.xn.data_ptr(), H, M, H,
-                                     s.rms_eps, 1, st), "add+norm")
+            _chk(lib.psd_gemm_bf16(self.attn.data_ptr(), Dq, M, Dq, L["wo"].data_ptr(), Dq, H, X,
+                                   H, native.EPI_RESID, X, H, 0, ws, wsn, st), "gemm o")
+            _chk(lib.psd_add_rmsnorm(X, H, None, 0, 0, H, None, L["mlp_norm"].data_ptr(),
+                                     self.xn.data_ptr(), H, M, H, s.rms_eps, 0, st), "mlp norm")
             _chk(lib.psd_gemm_bf16(self.xn.data_ptr(), H, M, H, L["wgu"].data_ptr(), H, 2 * Fp,
                                    self.act.data_ptr(), Fp, native.EPI_SILU, None, 0, 0, ws, wsn,
                                    st), "gemm gate/up")
-            _chk(lib.psd_gemm_partials(self.act.data_ptr(), Fp, M, Fp, L["wdown"].data_ptr(), Fp,
-                                       H, part, partn, 0, nsp, st), "gemm down")
-            prev_S = nsp._obj.value
+            _chk(lib.psd_gemm_bf16(self.act.data_ptr(), Fp, M, Fp, L["wdown"].data_ptr(), Fp, H,
+                                   X, H, native.EPI_RESID, X, H, 0, ws, wsn, st), "gemm down")
         if n_logit_rows == 0 or logits is None:
             return  # prefill: only the KV cache is needed
         R = n_logit_rows
-        _chk(lib.psd_add_rmsnorm(self.x.data_ptr(), H, part, prev_S, M * H, H,
-                                 v["logit_rows"].data_ptr(), m.final_norm.data_ptr(),
-                                 self.xf.data_ptr(), H, R, H, s.rms_eps, 0, st), "final norm")
+        _chk(lib.psd_add_rmsnorm(X, H, None, 0, 0, H, v["logit_rows"].data_ptr(),
+                                 m.final_norm.data_ptr(), self.xf.data_ptr(), H, R, H, s.rms_eps,
+                                 0, st), "final norm")
         ld = logits_ld or s.vocab
         _chk(lib.psd_gemm_bf16(self.xf.data_ptr(), H, R, H, m.lm_head.data_ptr(), H, s.vocab,
                                logits.data_ptr(), ld, native.EPI_F32, None, 0, 0, ws, wsn, st),

@@ -34,7 +34,7 @@ SIGNATURES: dict[str, tuple] = {
     "psd_gemm_bf16": (_i, [_p, _i, _i, _i, _p, _i, _i, _p, _i, _i, _p, _i, _i, _p, _sz, _p]),
     "psd_embed": (_i, [_p, _i, _p, _i, _p, _p]),
     "psd_add_rmsnorm": (_i, [_p, _i, _p, _i, _sz, _i, _p, _p, _p, _i, _i, _i, _f, _i, _p]),
-    "psd_rope_kv": (_i, [_p, _i, _sz, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "psd_rope_kv": (_i, [_p, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _p, _p]),
     "psd_gemm_partials": (_i, [_p, _i, _i, _i, _p, _i, _i, _p, _sz, _i, _c.POINTER(_i), _p]),
     "psd_attention": (_i, [_p, _p, _p, _p, _i, _p, _p, _p, _p, _p, _i, _i, _i, _i, _i, _i, _f,
                            _p, _p]),

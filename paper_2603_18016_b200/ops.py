@@ -160,9 +160,11 @@ def gemm(x: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None,
     if epi == native.EPI_RESID:
         if residual is None or residual.dtype != torch.bfloat16 or residual.stride(1) != 1:
             raise ConfigError("gemm: EPI_RESID needs a bf16 residual [M, N]")
+    if splits < 0:  # legacy split-K with automatic split count
+        splits, _ = gemm_plan(M, N, K, native.EPI_PARTIAL, 0)
     nsplit, need = gemm_plan(M, N, K, epi, splits)
     if need and (workspace is None or workspace.numel() * workspace.element_size() < need):
-        workspace = torch.empty(need, dtype=torch.uint8, device=x.device)
+        workspace = torch.zeros(need, dtype=torch.uint8, device=x.device)
     lib = native.load()
     native.check(lib.psd_gemm_bf16(
         x.data_ptr(), x.stride(0), M, K, w.data_ptr(), w.stride(0), N, out.data_ptr(),

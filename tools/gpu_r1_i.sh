@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 300 python tools/kbench.py --json gpurun_out/kbench1.json > gpurun_out/kbench1.log 2>&1
+timeout 300 python -m pytest tests/test_psd_gpu.py tests/test_gemm_gpu.py -x -q > gpurun_out/pytest_k.log 2>&1
+timeout 300 python tools/prof_step.py 48 0 1 > gpurun_out/prof_step_single4.log 2>&1
+echo done

@@ -30,13 +30,22 @@ rows = []
 
 
 def timeit(fn, iters=40):
+    """Device time per call: the calls are captured in a CUDA graph so the
+    host's launch rate does not pace the GPU (as in the real forward)."""
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
+        for _ in range(iters):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(iters):
-        fn()
+    g.replay()
     e1.record()
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / iters * 1e3
@@ -53,16 +62,16 @@ def report(name, shape, us, nbytes, flops=0):
           + (f" {r['TFLOPs']:7.1f} TF/s" if flops else ""), flush=True)
 
 
-def gemm_case(tag, M, N, K, epi, copies=6):
+def gemm_case(tag, M, N, K, epi, copies=6, legacy=False):
     x = torch.randn(M, K, device=dev).to(bf)
     ws = [(torch.randn(N, K, device=dev) * 0.02).to(bf) for _ in range(copies)]
     if epi == "partial":
         part = torch.empty(8 * M * N, dtype=torch.float32, device=dev)
         sp = ctypes.c_int()
-        st = torch.cuda.current_stream().cuda_stream
         it = [0]
 
         def fn():
+            st = torch.cuda.current_stream().cuda_stream
             w = ws[it[0] % copies]
             it[0] += 1
             rc = lib.psd_gemm_partials(x.data_ptr(), K, M, K, w.data_ptr(), K, N, part.data_ptr(),
@@ -75,11 +84,12 @@ def gemm_case(tag, M, N, K, epi, copies=6):
         e = {"bf16": native.EPI_BF16, "silu": native.EPI_SILU, "f32": native.EPI_F32}[epi]
         n_out = N // 2 if epi == "silu" else N
         out = torch.empty(M, n_out, dtype=torch.float32 if epi == "f32" else bf, device=dev)
-        wsp = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
+        wsp = torch.zeros(64 << 20, dtype=torch.uint8, device=dev)
         it = [0]
 
         def fn():
-            ops.gemm(x, ws[it[0] % copies], out=out, epi=e, workspace=wsp)
+            ops.gemm(x, ws[it[0] % copies], out=out, epi=e, workspace=wsp,
+                     splits=-1 if legacy else 0)
             it[0] += 1
         us = timeit(fn)
         out_bytes = out.numel() * out.element_size()
@@ -102,9 +112,8 @@ def attn_case(tag, nseq, ql, ctx, Hq, Hkv, D):
     q_len = i32([ql] * nseq)
     q_pos0 = i32([ctx] * nseq)
     kv_len = i32([ctx + ql] * nseq)
-    st = torch.cuda.current_stream().cuda_stream
-
     def fn():
+        st = torch.cuda.current_stream().cuda_stream
         rc = lib.psd_attention(q.data_ptr(), kc.data_ptr(), vc.data_ptr(), bt.data_ptr(),
                                nblk_seq, seq_slot.data_ptr(), q_start.data_ptr(), q_len.data_ptr(),
                                q_pos0.data_ptr(), kv_len.data_ptr(), nseq, ql, Hq, Hkv, D, bs,
@@ -120,9 +129,8 @@ def norm_case(tag, M, H, S):
     P = torch.randn(S * M * H, device=dev)
     w = torch.ones(H, device=dev).to(bf)
     y = torch.empty_like(x)
-    st = torch.cuda.current_stream().cuda_stream
-
     def fn():
+        st = torch.cuda.current_stream().cuda_stream
         rc = lib.psd_add_rmsnorm(x.data_ptr(), H, P.data_ptr(), S, M * H, H, None, w.data_ptr(),
                                  y.data_ptr(), H, M, H, 1e-5, 1, st)
         assert rc == 0
@@ -139,9 +147,8 @@ def rope_case(tag, M, Hq, Hkv, D, S):
     pos = torch.arange(M, dtype=torch.int32, device=dev) + 100
     slots = torch.arange(M, dtype=torch.int32, device=dev)
     inv = torch.rand(D // 2, device=dev) * 0.5
-    st = torch.cuda.current_stream().cuda_stream
-
     def fn():
+        st = torch.cuda.current_stream().cuda_stream
         rc = lib.psd_rope_kv(P.data_ptr(), S, M * N, M, Hq, Hkv, D, pos.data_ptr(),
                              slots.data_ptr(), inv.data_ptr(), None, q.data_ptr(), kc.data_ptr(),
                              vc.data_ptr(), st)
@@ -176,16 +183,18 @@ def main():
         return sel is None or k in sel
     if want("gemm"):
         # 8B verify (M = 32 x 6)
-        gemm_case("8B qkv", 192, 6144, 4096, "partial")
-        gemm_case("8B o", 192, 4096, 4096, "partial")
+        gemm_case("8B qkv", 192, 6144, 4096, "bf16")
+        gemm_case("8B o", 192, 4096, 4096, "bf16")
         gemm_case("8B gate/up", 192, 28672, 4096, "silu")
-        gemm_case("8B down", 192, 4096, 14336, "partial")
+        gemm_case("8B down", 192, 4096, 14336, "bf16")
+        gemm_case("8B gate/up legacy", 192, 28672, 4096, "silu", legacy=True)
         gemm_case("8B lm_head", 192, 128256, 4096, "f32", copies=2)
         # 1B draft (M = 32, first step 64)
-        gemm_case("1B qkv", 32, 3072, 2048, "partial")
-        gemm_case("1B o", 32, 2048, 2048, "partial")
+        gemm_case("1B qkv", 32, 3072, 2048, "bf16")
+        gemm_case("1B o", 32, 2048, 2048, "bf16")
         gemm_case("1B gate/up", 32, 16384, 2048, "silu")
-        gemm_case("1B down", 32, 2048, 8192, "partial")
+        gemm_case("1B down", 32, 2048, 8192, "bf16")
+        gemm_case("1B down legacy", 32, 2048, 8192, "bf16", legacy=True)
         gemm_case("1B lm_head", 32, 128256, 2048, "f32", copies=2)
         gemm_case("1B gate/up M64", 64, 16384, 2048, "silu")
     if want("attn"):
