@@ -37,6 +37,7 @@ using namespace psd;
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int kThreads = 192;
+constexpr int kMaxTiles = 1 << 16;  // stream-K tickets reserved at the workspace head
 // weight k-blocks prefetched into L2 ahead of the smem ring; 0 = off.
 // PSD_GEMM_PREFETCH overrides (tuning experiments)
 int prefetch_depth() {
@@ -617,7 +618,9 @@ SKPlan sk_plan(int M, int N, int K) {
   p.U = (long long)p.tiles * p.KB;
   p.G = (int)std::min<long long>(num_sms(), p.U);
   p.part_bytes = (size_t)p.G * 2 * p.bn * BM * sizeof(float);
-  p.ticket_bytes = ((size_t)p.tiles * sizeof(int) + 255) & ~size_t(255);
+  // tickets live at a FIXED offset (start of the workspace) so GEMMs of any
+  // shape can share one workspace: each leaves its tickets zeroed
+  p.ticket_bytes = (size_t)kMaxTiles * sizeof(int);
   return p;
 }
 
@@ -709,7 +712,7 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
     // stream-K persistent path (default)
     if (M <= 0 || N <= 0 || K <= 0 || (K % 8) || (N % BM)) return (int)cudaErrorInvalidValue;
     const SKPlan p = sk_plan(M, N, K);
-    if (!workspace || workspace_bytes < p.part_bytes + p.ticket_bytes)
+    if (!workspace || workspace_bytes < p.part_bytes + p.ticket_bytes || p.tiles > kMaxTiles)
       return (int)cudaErrorInvalidValue;
     CUtensorMap mw, mx;
     int rc;
@@ -719,8 +722,8 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
     g.M = M; g.N = N; g.K = K;
     g.KB = p.KB; g.MT = p.MT; g.tiles = p.tiles; g.G = p.G; g.U = p.U;
     g.Y = Y; g.ldy = ldy; g.R = static_cast<const __nv_bfloat16*>(R); g.ldr = ldr;
-    g.part = static_cast<float*>(workspace);
-    g.tickets = reinterpret_cast<int*>(static_cast<char*>(workspace) + p.part_bytes);
+    g.tickets = static_cast<int*>(workspace);
+    g.part = reinterpret_cast<float*>(static_cast<char*>(workspace) + p.ticket_bytes);
     cudaStream_t st = (cudaStream_t)stream;
     switch (epi) {
       case PSD_EPI_BF16: return launch_sk<PSD_EPI_BF16>(p.bn, mw, mx, g, st);
