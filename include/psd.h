@@ -58,6 +58,15 @@ int psd_verify_sample(const float* target_logits, int64_t t_stride_b, int64_t t_
                       const float* uniforms, float temperature, int B, int K,
                       int32_t* accepted_len, int32_t* out_tokens, void* workspace,
                       size_t workspace_bytes, void* stream);
+/* as psd_verify_sample, but request b's draft rows start at
+ * draft_logits + draft_rows[b] * d_stride_row (per-slot draft storage) */
+int psd_verify_sample_rows(const float* target_logits, int64_t t_stride_b, int64_t t_stride_i,
+                           int V, const float* draft_logits, const int32_t* draft_rows,
+                           int64_t d_stride_row, int64_t d_stride_i, int Vd,
+                           const int32_t* draft_ids, const int32_t* draft_len,
+                           const float* uniforms, float temperature, int B, int K,
+                           int32_t* accepted_len, int32_t* out_tokens, void* workspace,
+                           size_t workspace_bytes, void* stream);
 
 /* ---- K2: bf16 GEMM on tcgen05 (TMEM accumulators, TMA, mbarrier ring) -----
  *   Y[m, n] = epi( sum_k X[m*ldx + k] * W[n*ldw + k] )   X [M,K], W [N,K] bf16
@@ -83,6 +92,15 @@ int psd_gemm_plan(int M, int N, int K, int epi, int splits_hint, int* splits_out
 int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, int N, void* Y,
                   int ldy, int epi, const void* R, int ldr, int splits_hint, void* workspace,
                   size_t workspace_bytes, void* stream);
+/* Pre-tiled weights: [N/128][ceil(K/64)][128][64] bf16 with the 128-byte
+ * swizzle applied, so every (128-row, 64-col) weight tile is one contiguous,
+ * already-swizzled 16 KB block loaded with a single 1-D bulk copy (sequential
+ * HBM bursts, no tensor-map walk).  psd_gemm_tiled = stream-K GEMM on them. */
+size_t psd_tiled_weight_bytes(int N, int K);
+int psd_tile_weights(const void* W, int N, int K, int ldw, void* tiled, void* stream);
+int psd_gemm_tiled(const void* X, int ldx, int M, int K, const void* W_tiled, int N, void* Y,
+                   int ldy, int epi, const void* R, int ldr, void* workspace,
+                   size_t workspace_bytes, void* stream);
 /* fp32 split-K partials P[z][m][n] (z < *splits_used, row pitch N); the
  * consumer kernel (psd_add_rmsnorm, psd_rope_kv) reduces them in z order, so
  * no separate reduction launch is needed.  Fewer splits are used when
@@ -117,9 +135,13 @@ int psd_attention(const void* q, const void* k_cache, const void* v_cache,
 /* synthetic-language logit bias: logits[m, successor[prev_tokens[m]]] += beta */
 int psd_bigram_bias(float* logits, int64_t ld, const int32_t* prev_tokens, int M,
                     const int32_t* successor, int V, float beta, void* stream);
-/* out[b*n + i] = Philox4x32-10((seed), counter (request_ids[b], verify_index[b], i, 0)) in [0,1) */
+/* out[b*n + i] = Philox4x32-10(key seed, counter (request_ids[b], verify_index[b],
+ * base + i, 0)), top 24 bits / 2^24, in [0, 1) */
 int psd_philox_uniforms(uint64_t seed, const int32_t* request_ids, const int32_t* verify_index,
-                        int B, int n, float* out, void* stream);
+                        int B, int n, int base, float* out, void* stream);
+/* dst[dst_rows[r] * dst_ld + c] = src[r * src_ld + c], c < ncols (negative row: skip) */
+int psd_copy_rows_f32(float* dst, const int32_t* dst_rows, int64_t dst_ld, const float* src,
+                      int64_t src_ld, int nrows, int ncols, void* stream);
 
 /* ---- K5 / glue: KV commit of accepted tokens, token routing ---------------
  * psd_commit replaces the commit rule + KV write accounting of a verified row

@@ -229,6 +229,7 @@ struct SKArgs {
   int ldr;
   float* part;    // [G][2][BN * 128]
   int* tickets;   // [tiles], zero between launches
+  const __nv_bfloat16* Wt;  // pre-tiled weights (TILED variant)
 };
 
 struct Seg {
@@ -246,7 +247,7 @@ __device__ __forceinline__ int sk_owner(long long u, const SKArgs& g) {
   return (int)c;
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, bool TILED>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                const SKArgs g) {
@@ -315,7 +316,14 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           const uint32_t ph = (i / C::STAGES) & 1;
           mbar_wait(empty + s, ph ^ 1);
           mbar_arrive_expect_tx(full + s, C::STAGE);
-          tma_load_2d(sA + s * C::A_BYTES, &tmW, full + s, kb * BK, n0, pol_w);
+          if constexpr (TILED) {
+            // pre-tiled, pre-swizzled weights: one contiguous 16 KB block
+            const __nv_bfloat16* src =
+                g.Wt + ((size_t)(n0 / BM) * g.KB + kb) * (size_t)(BM * BK);
+            bulk_load(sA + s * C::A_BYTES, src, C::A_BYTES, full + s, pol_w);
+          } else {
+            tma_load_2d(sA + s * C::A_BYTES, &tmW, full + s, kb * BK, n0, pol_w);
+          }
           tma_load_2d(sB + s * C::B_BYTES, &tmX, full + s, kb * BK, m0, pol_x);
         }
       }
@@ -549,34 +557,62 @@ int launch_bn(const CUtensorMap& mw, const CUtensorMap& mx, const GemmArgs& g, d
   return (int)cudaGetLastError();
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, bool TILED>
 int launch_sk_bn(const CUtensorMap& mw, const CUtensorMap& mx, const SKArgs& g, cudaStream_t st) {
   using C = Cfg<BN>;
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_sk_kernel<BN, EPI>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_sk_kernel<BN, EPI, TILED>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return (int)e;
     attr_done = true;
   }
-  gemm_sk_kernel<BN, EPI><<<g.G, kThreads, C::SMEM, st>>>(mw, mx, g);
+  gemm_sk_kernel<BN, EPI, TILED><<<g.G, kThreads, C::SMEM, st>>>(mw, mx, g);
   return (int)cudaGetLastError();
 }
 
-template <int EPI>
+template <int EPI, bool TILED = false>
 int launch_sk(int bn, const CUtensorMap& mw, const CUtensorMap& mx, const SKArgs& g,
               cudaStream_t st) {
   switch (bn) {
-    case 32: return launch_sk_bn<32, EPI>(mw, mx, g, st);
-    case 64: return launch_sk_bn<64, EPI>(mw, mx, g, st);
-    case 96: return launch_sk_bn<96, EPI>(mw, mx, g, st);
-    case 128: return launch_sk_bn<128, EPI>(mw, mx, g, st);
-    case 160: return launch_sk_bn<160, EPI>(mw, mx, g, st);
-    case 192: return launch_sk_bn<192, EPI>(mw, mx, g, st);
-    case 224: return launch_sk_bn<224, EPI>(mw, mx, g, st);
-    case 256: return launch_sk_bn<256, EPI>(mw, mx, g, st);
+    case 32: return launch_sk_bn<32, EPI, TILED>(mw, mx, g, st);
+    case 64: return launch_sk_bn<64, EPI, TILED>(mw, mx, g, st);
+    case 96: return launch_sk_bn<96, EPI, TILED>(mw, mx, g, st);
+    case 128: return launch_sk_bn<128, EPI, TILED>(mw, mx, g, st);
+    case 160: return launch_sk_bn<160, EPI, TILED>(mw, mx, g, st);
+    case 192: return launch_sk_bn<192, EPI, TILED>(mw, mx, g, st);
+    case 224: return launch_sk_bn<224, EPI, TILED>(mw, mx, g, st);
+    case 256: return launch_sk_bn<256, EPI, TILED>(mw, mx, g, st);
   }
   return (int)cudaErrorInvalidValue;
+}
+
+// [N, K] row-major -> [N/128][KB][128][64] with the 128-byte swizzle applied
+// (16-byte chunk j of row r stored at chunk j ^ (r & 7)), K zero-padded
+__global__ void tile_weights_kernel(const __nv_bfloat16* __restrict__ W, int N, int K, int ldw,
+                                    __nv_bfloat16* __restrict__ T) {
+  const int KB = (K + BK - 1) / BK;
+  const size_t nchunks = (size_t)N * KB * 8;
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < nchunks;
+       q += (size_t)gridDim.x * blockDim.x) {
+    const int jd = q & 7;
+    const int r = (q >> 3) & 127;
+    const size_t tk = q >> 10;  // (tile, kb)
+    const int kb = (int)(tk % KB);
+    const int tile = (int)(tk / KB);
+    const int j = jd ^ (r & 7);
+    const int n = tile * BM + r;
+    const int k = kb * BK + j * 8;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (k + 8 <= K) {
+      v = *reinterpret_cast<const uint4*>(W + (size_t)n * ldw + k);
+    } else if (k < K) {
+      __nv_bfloat16 tmp[8];
+      for (int e = 0; e < 8; ++e) tmp[e] = k + e < K ? W[(size_t)n * ldw + k + e] : __float2bfloat16(0.f);
+      v = *reinterpret_cast<uint4*>(tmp);
+    }
+    reinterpret_cast<uint4*>(T)[q] = v;
+  }
 }
 
 int token_tile(int M) {
@@ -671,6 +707,49 @@ int psd_gemm_plan(int M, int N, int K, int epi, int splits_hint, int* splits_out
   return 0;
 }
 
+size_t psd_tiled_weight_bytes(int N, int K) {
+  return (size_t)N * ((K + BK - 1) / BK) * BK * sizeof(__nv_bfloat16);
+}
+
+int psd_tile_weights(const void* W, int N, int K, int ldw, void* tiled, void* stream) {
+  if (!W || !tiled || N % BM || K % 8 || ldw % 8) return (int)cudaErrorInvalidValue;
+  tile_weights_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(
+      static_cast<const __nv_bfloat16*>(W), N, K, ldw, static_cast<__nv_bfloat16*>(tiled));
+  return (int)cudaGetLastError();
+}
+
+int psd_gemm_tiled(const void* X, int ldx, int M, int K, const void* W_tiled, int N, void* Y,
+                   int ldy, int epi, const void* R, int ldr, void* workspace,
+                   size_t workspace_bytes, void* stream) {
+  if (!X || !W_tiled || !Y || epi < 0 || epi > PSD_EPI_SILU) return (int)cudaErrorInvalidValue;
+  if (epi == PSD_EPI_RESID && !R) return (int)cudaErrorInvalidValue;
+  if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(W_tiled)) & 15)
+    return (int)cudaErrorMisalignedAddress;
+  if (ldx % 8) return (int)cudaErrorMisalignedAddress;
+  if (M <= 0 || N <= 0 || K <= 0 || (K % 8) || (N % BM)) return (int)cudaErrorInvalidValue;
+  const SKPlan p = sk_plan(M, N, K);
+  if (!workspace || workspace_bytes < p.part_bytes + p.ticket_bytes || p.tiles > kMaxTiles)
+    return (int)cudaErrorInvalidValue;
+  CUtensorMap mx;
+  int rc;
+  if ((rc = make_map(&mx, X, M, K, ldx, p.bn))) return rc;
+  SKArgs g;
+  g.M = M; g.N = N; g.K = K;
+  g.KB = p.KB; g.MT = p.MT; g.tiles = p.tiles; g.G = p.G; g.U = p.U;
+  g.Y = Y; g.ldy = ldy; g.R = static_cast<const __nv_bfloat16*>(R); g.ldr = ldr;
+  g.tickets = static_cast<int*>(workspace);
+  g.part = reinterpret_cast<float*>(static_cast<char*>(workspace) + p.ticket_bytes);
+  g.Wt = static_cast<const __nv_bfloat16*>(W_tiled);
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (epi) {
+    case PSD_EPI_BF16: return launch_sk<PSD_EPI_BF16, true>(p.bn, mx, mx, g, st);
+    case PSD_EPI_F32: return launch_sk<PSD_EPI_F32, true>(p.bn, mx, mx, g, st);
+    case PSD_EPI_RESID: return launch_sk<PSD_EPI_RESID, true>(p.bn, mx, mx, g, st);
+    case PSD_EPI_SILU: return launch_sk<PSD_EPI_SILU, true>(p.bn, mx, mx, g, st);
+  }
+  return (int)cudaErrorInvalidValue;
+}
+
 int psd_gemm_partials(const void* X, int ldx, int M, int K, const void* W, int ldw, int N,
                       float* P, size_t p_bytes, int splits_hint, int* splits_used, void* stream) {
   if (!X || !W || !P) return (int)cudaErrorInvalidValue;
@@ -724,6 +803,7 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
     g.Y = Y; g.ldy = ldy; g.R = static_cast<const __nv_bfloat16*>(R); g.ldr = ldr;
     g.tickets = static_cast<int*>(workspace);
     g.part = reinterpret_cast<float*>(static_cast<char*>(workspace) + p.ticket_bytes);
+    g.Wt = nullptr;
     cudaStream_t st = (cudaStream_t)stream;
     switch (epi) {
       case PSD_EPI_BF16: return launch_sk<PSD_EPI_BF16>(p.bn, mw, mx, g, st);

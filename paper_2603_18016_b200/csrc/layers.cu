@@ -439,12 +439,12 @@ __host__ __device__ inline void philox_round(uint32_t (&c)[4], uint32_t k0, uint
 }
 
 __global__ void philox_uniform_kernel(uint64_t seed, const int32_t* __restrict__ rid,
-                                      const int32_t* __restrict__ jv, int B, int n,
+                                      const int32_t* __restrict__ jv, int B, int n, int base,
                                       float* __restrict__ out) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= B * n) return;
   const int b = idx / n, i = idx % n;
-  uint32_t c[4] = {(uint32_t)rid[b], (uint32_t)jv[b], (uint32_t)i, 0u};
+  uint32_t c[4] = {(uint32_t)rid[b], (uint32_t)jv[b], (uint32_t)(base + i), 0u};
   uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
@@ -504,9 +504,32 @@ __global__ void fill_uniform_kernel(__nv_bfloat16* __restrict__ out, size_t n, u
   }
 }
 
+// dst[dst_rows[r] * dst_ld + c] = src[r * src_ld + c] (negative row: skip)
+__global__ void copy_rows_kernel(float* __restrict__ dst, const int32_t* __restrict__ dst_rows,
+                                 int64_t dst_ld, const float* __restrict__ src, int64_t src_ld,
+                                 int ncols) {
+  const int r = blockIdx.y;
+  const int dr = dst_rows[r];
+  if (dr < 0) return;
+  const float4* s4 = reinterpret_cast<const float4*>(src + r * src_ld);
+  float4* d4 = reinterpret_cast<float4*>(dst + dr * dst_ld);
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncols / 4; c += gridDim.x * blockDim.x)
+    d4[c] = s4[c];
+}
+
 }  // namespace
 
 extern "C" {
+
+int psd_copy_rows_f32(float* dst, const int32_t* dst_rows, int64_t dst_ld, const float* src,
+                      int64_t src_ld, int nrows, int ncols, void* stream) {
+  if (nrows <= 0) return 0;
+  if ((ncols & 3) || (dst_ld & 3) || (src_ld & 3)) return (int)cudaErrorMisalignedAddress;
+  dim3 grid(16, nrows);
+  copy_rows_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(dst, dst_rows, dst_ld, src, src_ld,
+                                                           ncols);
+  return (int)cudaGetLastError();
+}
 
 int psd_index_copy_i32(int32_t* dst, const int32_t* dst_idx, const int32_t* src,
                        const int32_t* src_idx, int n, void* stream) {
@@ -614,10 +637,10 @@ int psd_bigram_bias(float* logits, int64_t ld, const int32_t* prev_tokens, int M
 }
 
 int psd_philox_uniforms(uint64_t seed, const int32_t* request_ids, const int32_t* verify_index,
-                        int B, int n, float* out, void* stream) {
+                        int B, int n, int base, float* out, void* stream) {
   if (B * n <= 0) return 0;
   philox_uniform_kernel<<<(B * n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
-      seed, request_ids, verify_index, B, n, out);
+      seed, request_ids, verify_index, B, n, base, out);
   return (int)cudaGetLastError();
 }
 

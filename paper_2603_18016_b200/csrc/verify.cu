@@ -40,6 +40,7 @@ struct Plan {
 struct Params {
   const float* t; int64_t tsb, tsi; int V;
   const float* d; int64_t dsb, dsi; int Vd;
+  const int32_t* d_rows;  // optional: draft rows of request b start at d + d_rows[b] * dsb
   const int32_t* ids; const int32_t* len; const float* u;
   float c; int B, K;  // c = psd_scale(1/T)
   int32_t* acc; int32_t* out;
@@ -94,7 +95,8 @@ verify_stats(const Params p) {
   const int n = is_draft ? p.Vd : p.V;
   const bool active = (is_draft ? i < kb : i <= kb) && slice * PSD_SLICE < n;
   if (!active) return;
-  const float* row = is_draft ? p.d + b * p.dsb + i * p.dsi : p.t + b * p.tsb + i * p.tsi;
+  const int db = p.d_rows ? p.d_rows[b] : b;
+  const float* row = is_draft ? p.d + db * p.dsb + i * p.dsi : p.t + b * p.tsb + i * p.tsi;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int base = slice * PSD_SLICE;
 
@@ -222,7 +224,7 @@ verify_stats(const Params p) {
       if constexpr (SAMPLE) {
         if (x >= 0 && x < p.V) {
           const float* tr = p.t + b * p.tsb + lane * p.tsi;
-          const float* drw = p.d + b * p.dsb + lane * p.dsi;
+          const float* drw = p.d + (int64_t)(p.d_rows ? p.d_rows[b] : b) * p.dsb + lane * p.dsi;
           const float et = psd_weight(__ldg(tr + x), p.c, psd_bias(sMt[lane], p.c));
           const float ed =
               x < p.Vd ? psd_weight(__ldg(drw + x), p.c, psd_bias(sMd[lane], p.c)) : 0.0f;
@@ -326,7 +328,7 @@ verify_sample(const Params p) {
   WeightCtx w;
   w.V = p.V; w.Vd = p.Vd; w.c = p.c;
   w.t = p.t + b * p.tsb + pl.row * p.tsi;
-  w.d = p.d + b * p.dsb + pl.row * p.dsi;
+  w.d = p.d + (int64_t)(p.d_rows ? p.d_rows[b] : b) * p.dsb + pl.row * p.dsi;
   w.bt = psd_bias(pl.Mt, p.c); w.bd = psd_bias(pl.Md, p.c); w.St = pl.St; w.Sd = pl.Sd;
   w.residual = pl.mode == 1;
 
@@ -501,6 +503,39 @@ int psd_verify_sample(const float* target_logits, int64_t t_stride_b, int64_t t_
   char* w = static_cast<char*>(ws);
   p.t = target_logits; p.tsb = t_stride_b; p.tsi = t_stride_i; p.V = V;
   p.d = draft_logits; p.dsb = d_stride_b; p.dsi = d_stride_i; p.Vd = Vd;
+  p.ids = draft_ids; p.len = draft_len; p.u = uniforms;
+  p.c = psd_scale(1.0f / temperature); p.B = B; p.K = K; p.acc = accepted_len; p.out = out_tokens;
+  p.cnt_a = reinterpret_cast<int*>(w + L.cnt_a); p.cnt_b = reinterpret_cast<int*>(w + L.cnt_b);
+  p.part = reinterpret_cast<float2*>(w + L.part); p.plan = reinterpret_cast<Plan*>(w + L.plan);
+  p.wblk = reinterpret_cast<float*>(w + L.wblk);
+  p.NS = (V + PSD_SLICE - 1) / PSD_SLICE; p.NB = (V + PSD_SBLK - 1) / PSD_SBLK;
+  p.R = 2 * K + 1;
+  dim3 grid(p.NS, B * p.R);
+  verify_stats<true><<<grid, kThreads, 0, (cudaStream_t)stream>>>(p);
+  dim3 grid2(p.NB, B);
+  verify_sample<<<grid2, kThreads, 0, (cudaStream_t)stream>>>(p);
+  return (int)cudaGetLastError();
+}
+
+int psd_verify_sample_rows(const float* target_logits, int64_t t_stride_b, int64_t t_stride_i,
+                           int V, const float* draft_logits, const int32_t* draft_rows,
+                           int64_t d_stride_row, int64_t d_stride_i, int Vd,
+                      const int32_t* draft_ids, const int32_t* draft_len, const float* uniforms,
+                      float temperature, int B, int K, int32_t* accepted_len,
+                      int32_t* out_tokens, void* ws, size_t ws_bytes, void* stream) {
+  const WsLayout L = layout(B, K, V, Vd, 1);
+  int rc = check_common(target_logits, t_stride_b, t_stride_i, V, B, K, ws, ws_bytes, L.total);
+  if (rc) return rc;
+  if (!draft_logits || Vd <= 0 || Vd > V || !uniforms || !(temperature > 0.0f))
+    return (int)cudaErrorInvalidValue;
+  if ((Vd & 3) || (d_stride_row & 3) || (d_stride_i & 3) ||
+      (reinterpret_cast<uintptr_t>(draft_logits) & 15))
+    return (int)cudaErrorMisalignedAddress;
+  Params p{};
+  char* w = static_cast<char*>(ws);
+  p.t = target_logits; p.tsb = t_stride_b; p.tsi = t_stride_i; p.V = V;
+  p.d = draft_logits; p.dsb = d_stride_row; p.dsi = d_stride_i; p.Vd = Vd;
+  p.d_rows = draft_rows;
   p.ids = draft_ids; p.len = draft_len; p.u = uniforms;
   p.c = psd_scale(1.0f / temperature); p.B = B; p.K = K; p.acc = accepted_len; p.out = out_tokens;
   p.cnt_a = reinterpret_cast<int*>(w + L.cnt_a); p.cnt_b = reinterpret_cast<int*>(w + L.cnt_b);

@@ -35,11 +35,17 @@ SIGNATURES: dict[str, tuple] = {
     "psd_embed": (_i, [_p, _i, _p, _i, _p, _p]),
     "psd_add_rmsnorm": (_i, [_p, _i, _p, _i, _sz, _i, _p, _p, _p, _i, _i, _i, _f, _i, _p]),
     "psd_rope_kv": (_i, [_p, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "psd_tiled_weight_bytes": (_sz, [_i, _i]),
+    "psd_tile_weights": (_i, [_p, _i, _i, _i, _p, _p]),
+    "psd_gemm_tiled": (_i, [_p, _i, _i, _i, _p, _i, _p, _i, _i, _p, _i, _p, _sz, _p]),
     "psd_gemm_partials": (_i, [_p, _i, _i, _i, _p, _i, _i, _p, _sz, _i, _c.POINTER(_i), _p]),
     "psd_attention": (_i, [_p, _p, _p, _p, _i, _p, _p, _p, _p, _p, _i, _i, _i, _i, _i, _i, _f,
                            _p, _p]),
     "psd_bigram_bias": (_i, [_p, _i64, _p, _i, _p, _i, _f, _p]),
-    "psd_philox_uniforms": (_i, [_c.c_uint64, _p, _p, _i, _i, _p, _p]),
+    "psd_philox_uniforms": (_i, [_c.c_uint64, _p, _p, _i, _i, _i, _p, _p]),
+    "psd_copy_rows_f32": (_i, [_p, _p, _i64, _p, _i64, _i, _i, _p]),
+    "psd_verify_sample_rows": (_i, [_p, _i64, _i64, _i, _p, _p, _i64, _i64, _i, _p, _p, _p, _f,
+                                    _i, _i, _p, _p, _p, _sz, _p]),
     "psd_commit": (_i, [_p, _p, _i, _p, _i, _p, _p, _i, _p, _i, _p]),
     "psd_index_copy_i32": (_i, [_p, _p, _p, _p, _i, _p]),
     "psd_fill_uniform_bf16": (_i, [_p, _sz, _c.c_uint64, _f, _p]),

@@ -105,3 +105,31 @@ def test_tiny_model_gemm_shapes(cuda_device, M, N, K, epi):
         ref = torch.nn.functional.silu(gt) * up
     err = (y.float() - ref).abs().max().item()
     assert err <= 1e-2 * ref.abs().max().item() + 1e-3, err
+
+
+@pytest.mark.parametrize("M,N,K,epi", [(192, 1024, 4096, "bf16"), (32, 2048, 1000, "silu"),
+                                       (63, 1024, 256, "f32"), (300, 512, 704, "bf16")])
+def test_gemm_pretiled_weights(cuda_device, M, N, K, epi):
+    dev = cuda_device
+    g = torch.Generator(device=dev).manual_seed(M * 3 + N + K)
+    x = torch.randn(M, K, device=dev, generator=g).to(bf)
+    w = (torch.randn(N, K, device=dev, generator=g) * 0.05).to(bf)
+    lib = native.load()
+    st = torch.cuda.current_stream().cuda_stream
+    t = torch.empty(lib.psd_tiled_weight_bytes(N, K) // 2, dtype=bf, device=dev)
+    assert lib.psd_tile_weights(w.data_ptr(), N, K, K, t.data_ptr(), st) == 0
+    e = {"bf16": native.EPI_BF16, "silu": native.EPI_SILU, "f32": native.EPI_F32}[epi]
+    n_out = N // 2 if epi == "silu" else N
+    y = torch.empty(M, n_out, dtype=torch.float32 if epi == "f32" else bf, device=dev)
+    ws = _shared_ws(dev)
+    assert lib.psd_gemm_tiled(x.data_ptr(), K, M, K, t.data_ptr(), N, y.data_ptr(), n_out, e,
+                              None, 0, ws.data_ptr(), ws.numel(), st) == 0
+    torch.cuda.synchronize()
+    ref = x.float() @ w.float().T
+    if epi == "silu":
+        F = N // 2
+        gt = ref.view(M, F // 64, 2, 64)[:, :, 0].reshape(M, F)
+        up = ref.view(M, F // 64, 2, 64)[:, :, 1].reshape(M, F)
+        ref = torch.nn.functional.silu(gt) * up
+    err = (y.float() - ref).abs().max().item()
+    assert err <= 1e-2 * ref.abs().max().item() + 1e-3, err

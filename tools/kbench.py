@@ -62,9 +62,33 @@ def report(name, shape, us, nbytes, flops=0):
           + (f" {r['TFLOPs']:7.1f} TF/s" if flops else ""), flush=True)
 
 
-def gemm_case(tag, M, N, K, epi, copies=6, legacy=False):
+def gemm_case(tag, M, N, K, epi, copies=6, legacy=False, tiled=False):
     x = torch.randn(M, K, device=dev).to(bf)
     ws = [(torch.randn(N, K, device=dev) * 0.02).to(bf) for _ in range(copies)]
+    if tiled:
+        tws = []
+        for w in ws:
+            t = torch.empty(lib.psd_tiled_weight_bytes(N, K) // 2, dtype=bf, device=dev)
+            assert lib.psd_tile_weights(w.data_ptr(), N, K, K, t.data_ptr(),
+                                        torch.cuda.current_stream().cuda_stream) == 0
+            tws.append(t)
+        e = {"bf16": native.EPI_BF16, "silu": native.EPI_SILU, "f32": native.EPI_F32}[epi]
+        n_out = N // 2 if epi == "silu" else N
+        out = torch.empty(M, n_out, dtype=torch.float32 if epi == "f32" else bf, device=dev)
+        wsp = torch.zeros(64 << 20, dtype=torch.uint8, device=dev)
+        it = [0]
+
+        def fn():
+            st = torch.cuda.current_stream().cuda_stream
+            rc = lib.psd_gemm_tiled(x.data_ptr(), K, M, K, tws[it[0] % copies].data_ptr(), N,
+                                    out.data_ptr(), n_out, e, None, 0, wsp.data_ptr(),
+                                    wsp.numel(), st)
+            assert rc == 0
+            it[0] += 1
+        us = timeit(fn)
+        nbytes = N * K * 2 + M * K * 2 + out.numel() * out.element_size()
+        report(f"gemm {tag} tiled", f"M={M} N={N} K={K}", us, nbytes, 2 * M * N * K)
+        return
     if epi == "partial":
         part = torch.empty(8 * M * N, dtype=torch.float32, device=dev)
         sp = ctypes.c_int()
@@ -188,6 +212,11 @@ def main():
         gemm_case("8B gate/up", 192, 28672, 4096, "silu")
         gemm_case("8B down", 192, 4096, 14336, "bf16")
         gemm_case("8B gate/up legacy", 192, 28672, 4096, "silu", legacy=True)
+        gemm_case("8B qkv", 192, 6144, 4096, "bf16", tiled=True)
+        gemm_case("8B o", 192, 4096, 4096, "bf16", tiled=True)
+        gemm_case("8B gate/up", 192, 28672, 4096, "silu", tiled=True)
+        gemm_case("8B down", 192, 4096, 14336, "bf16", tiled=True)
+        gemm_case("8B lm_head", 192, 128256, 4096, "f32", copies=2, tiled=True)
         gemm_case("8B lm_head", 192, 128256, 4096, "f32", copies=2)
         # 1B draft (M = 32, first step 64)
         gemm_case("1B qkv", 32, 3072, 2048, "bf16")
@@ -195,6 +224,11 @@ def main():
         gemm_case("1B gate/up", 32, 16384, 2048, "silu")
         gemm_case("1B down", 32, 2048, 8192, "bf16")
         gemm_case("1B down legacy", 32, 2048, 8192, "bf16", legacy=True)
+        gemm_case("1B qkv", 32, 3072, 2048, "bf16", tiled=True)
+        gemm_case("1B o", 32, 2048, 2048, "bf16", tiled=True)
+        gemm_case("1B gate/up", 32, 16384, 2048, "silu", tiled=True)
+        gemm_case("1B down", 32, 2048, 8192, "bf16", tiled=True)
+        gemm_case("1B lm_head", 32, 128256, 2048, "f32", copies=2, tiled=True)
         gemm_case("1B lm_head", 32, 128256, 2048, "f32", copies=2)
         gemm_case("1B gate/up M64", 64, 16384, 2048, "silu")
     if want("attn"):
