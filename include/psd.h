@@ -74,8 +74,9 @@ int psd_verify_sample_rows(const float* target_logits, int64_t t_stride_b, int64
  * .duration(...) (pkg/src/specsim/engine.py:338, 359-360, 378, 402, 429;
  * request_model.py:112-117) with the real contractions of the forwards.
  * epi: PSD_EPI_BF16 (Y bf16), PSD_EPI_F32 (Y fp32), PSD_EPI_RESID (Y bf16 =
- * acc + R, Y may alias R), PSD_EPI_SILU (W rows packed per 128-row tile as 64
- * gate rows then the 64 matching up rows; Y [M, N/2] bf16 = silu(g) * u).
+ * acc + R, Y may alias R), PSD_EPI_SILU (W rows packed per 128-row tile: for
+ * q = 0..3, rows 32q..32q+15 are gate features tile*64+16q+0..15 and rows
+ * 32q+16..32q+31 the matching up features; Y [M, N/2] bf16 = silu(g) * u).
  * N must be a multiple of 128, K and the leading dims multiples of 8.
  * splits_hint 0 (default) = stream-K persistent kernel: one CTA per SM,
  * balanced weight k-blocks per SM, cut tiles finished by their last-arriving
@@ -111,6 +112,12 @@ int psd_gemm_partials(const void* X, int ldx, int M, int K, const void* W, int l
 /* ---- K3/K3'/K4: forward-pass building blocks (bf16 storage, fp32 math) ----
  * Same seam as K2 (the virtual pass durations).  Row-major activations. */
 int psd_embed(const int32_t* tokens, int M, const void* table, int H, void* out, void* stream);
+/* as psd_rope_kv, reading qkv = bf16(sum_z qkv_partials[z*slice + ...]) (the
+ * QKV GEMM's split-K reduction fused into the RoPE pass) */
+int psd_rope_kv_partials(const float* qkv_partials, int S, size_t slice, int M, int Hq, int Hkv,
+                         int D, const int32_t* positions, const int32_t* slots,
+                         const float* inv_freq, const void* qkv_bias, void* q_out,
+                         void* k_cache, void* v_cache, void* stream);
 /* src = rows ? rows[m] : m; v = bf16(x[src] + sum_z partials[z*slice + src*ldp])
  * (no add when partials == NULL; v written back to x when write_back);
  * y[m] = v * rsqrt(mean(v^2) + eps) * w.  H <= 8192. */

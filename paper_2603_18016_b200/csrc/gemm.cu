@@ -159,26 +159,18 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUt
       tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c, r);
       tmem_ld_wait();
       if constexpr (EPI == PSD_EPI_SILU) {
-        // rows 0-63 of the tile: gate j, rows 64-127: up j (j = tile*64 + row%64)
-        if (q >= 2) {
+        // packed weights: in quarter q, rows 32q..32q+15 = gate f, rows
+        // 32q+16..32q+31 = up f (f = tile*64 + 16q + lane%16): one shuffle
+        // pairs them inside the warp
+        const int jo = blockIdx.x * 64 + 16 * q + (lane & 15);
+        __nv_bfloat16* Y = static_cast<__nv_bfloat16*>(g.Y);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) xchg[((q - 2) * 32 + lane) * 17 + j] = __uint_as_float(r[j]);
+        for (int j = 0; j < 16; ++j) {
+          const float mine = __uint_as_float(r[j]);
+          const float up = __shfl_down_sync(0xffffffffu, mine, 16);
+          const int m = m0 + c + j;
+          if (lane < 16 && m < g.M) Y[(size_t)m * g.ldy + jo] = __float2bfloat16(silu(mine) * up);
         }
-        named_bar_sync(1, 128);
-        if (q < 2) {
-          const int jo = blockIdx.x * 64 + 32 * q + lane;
-          __nv_bfloat16* Y = static_cast<__nv_bfloat16*>(g.Y);
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int m = m0 + c + j;
-            if (m < g.M) {
-              const float gt = __uint_as_float(r[j]);
-              const float up = xchg[(q * 32 + lane) * 17 + j];
-              Y[(size_t)m * g.ldy + jo] = __float2bfloat16(silu(gt) * up);
-            }
-          }
-        }
-        named_bar_sync(1, 128);
       } else {
         if (n < g.N) {
 #pragma unroll
@@ -424,23 +416,15 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
             for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(r[k]);
           }
           if constexpr (EPI == PSD_EPI_SILU) {
-            if (q >= 2) {
+            const int jo = (n0 / BM) * 64 + 16 * q + (lane & 15);
+            __nv_bfloat16* Y = static_cast<__nv_bfloat16*>(g.Y);
 #pragma unroll
-              for (int k = 0; k < 16; ++k) xchg[((q - 2) * 32 + lane) * 17 + k] = v[k];
+            for (int k = 0; k < 16; ++k) {
+              const float up = __shfl_down_sync(0xffffffffu, v[k], 16);
+              const int m = m0 + col + k;
+              if (lane < 16 && m < g.M)
+                Y[(size_t)m * g.ldy + jo] = __float2bfloat16(silu(v[k]) * up);
             }
-            named_bar_sync(1, 128);
-            if (q < 2) {
-              const int jo = (n0 / BM) * 64 + 32 * q + lane;
-              __nv_bfloat16* Y = static_cast<__nv_bfloat16*>(g.Y);
-#pragma unroll
-              for (int k = 0; k < 16; ++k) {
-                const int m = m0 + col + k;
-                if (m < g.M)
-                  Y[(size_t)m * g.ldy + jo] =
-                      __float2bfloat16(silu(v[k]) * xchg[(q * 32 + lane) * 17 + k]);
-              }
-            }
-            named_bar_sync(1, 128);
           } else {
             const int n = n0 + row;
             if (n < g.N) {
@@ -485,8 +469,8 @@ __global__ void gemm_reduce_kernel(const float* __restrict__ P, int splits, int 
        idx += (size_t)gridDim.x * blockDim.x) {
     const int m = idx / Nout, n = idx % Nout;
     if (epi == PSD_EPI_SILU) {
-      const int t = n / 64, jl = n % 64;
-      const size_t ig = (size_t)m * N + t * 128 + jl, iu = ig + 64;
+      const int t = n / 64, r = n % 64;
+      const size_t ig = (size_t)m * N + t * 128 + (r / 16) * 32 + r % 16, iu = ig + 16;
       float gs = 0.f, us = 0.f;
       for (int s = 0; s < splits; ++s) {
         gs += P[s * slice + ig];

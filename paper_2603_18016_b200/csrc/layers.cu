@@ -123,8 +123,37 @@ add_rmsnorm_kernel(__nv_bfloat16* __restrict__ x, int ldx, const float* __restri
 // One CTA per token.  Work item = (head, 8-wide chunk of the first half):
 // one 16-byte load of x[i..i+7] and one of x[i+half..], 8 rotations, 16-byte
 // stores -- every load of a thread is independent (no serial latency chain).
+// 8 consecutive qkv values of token-row `row` starting at column e: bf16 input,
+// or bf16(sum of S fp32 split-K partials) -- the QKV GEMM's reduction fused here
+struct QkvSrc {
+  const __nv_bfloat16* bf;
+  const float* P;
+  int S;
+  size_t slice;
+  __device__ __forceinline__ void load8(size_t off, float (&v)[8]) const {
+    if (P) {
+      const float4* p4 = reinterpret_cast<const float4*>(P + off);
+      float4 a = p4[0], b = p4[1];
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+      for (int z = 1; z < S; ++z) {
+        const float4* q4 = reinterpret_cast<const float4*>(P + z * slice + off);
+        a = q4[0]; b = q4[1];
+        v[0] += a.x; v[1] += a.y; v[2] += a.z; v[3] += a.w;
+        v[4] += b.x; v[5] += b.y; v[6] += b.z; v[7] += b.w;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = __bfloat162float(__float2bfloat16(v[k]));
+    } else {
+      uint4 u = *reinterpret_cast<const uint4*>(bf + off);
+      const __nv_bfloat16* h8 = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = __bfloat162float(h8[k]);
+    }
+  }
+};
+
 __global__ void __launch_bounds__(256)
-rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, int Hq, int Hkv, int D,
+rope_kv_kernel(const QkvSrc src, int Hq, int Hkv, int D,
                const int32_t* __restrict__ pos, const int32_t* __restrict__ slot,
                const float* __restrict__ inv_freq, const __nv_bfloat16* __restrict__ bias,
                __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ kc,
@@ -142,34 +171,33 @@ rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, int Hq, int Hkv, int D,
     s_sin[i] = sn;
   }
   __syncthreads();
-  const __nv_bfloat16* row = qkv + (size_t)m * (Hq + 2 * Hkv) * D;
+  const size_t row = (size_t)m * (Hq + 2 * Hkv) * D;
   const int nrot = (s >= 0 ? Hq + Hkv : Hq) * cpr;
   const int nv = s >= 0 ? Hkv * D / 8 : 0;
   for (int idx = threadIdx.x; idx < nrot + nv; idx += blockDim.x) {
-    if (idx >= nrot) {  // V: straight copy (+ bias)
+    if (idx >= nrot) {  // V: copy (+ bias)
       const int e = (idx - nrot) * 8;
-      uint4 v = *reinterpret_cast<const uint4*>(row + (size_t)(Hq + Hkv) * D + e);
-      if (bias) {
-        __nv_bfloat16* vv = reinterpret_cast<__nv_bfloat16*>(&v);
-        const __nv_bfloat16* bb = bias + (size_t)(Hq + Hkv) * D + e;
+      float vf[8];
+      src.load8(row + (size_t)(Hq + Hkv) * D + e, vf);
+      uint4 v;
+      __nv_bfloat16* vv = reinterpret_cast<__nv_bfloat16*>(&v);
+      const __nv_bfloat16* bb = bias ? bias + (size_t)(Hq + Hkv) * D + e : nullptr;
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          vv[k] = __float2bfloat16(__bfloat162float(vv[k]) + __bfloat162float(bb[k]));
-      }
+      for (int k = 0; k < 8; ++k)
+        vv[k] = __float2bfloat16(bb ? vf[k] + __bfloat162float(bb[k]) : vf[k]);
       *reinterpret_cast<uint4*>(vc + (size_t)s * Hkv * D + e) = v;
       continue;
     }
     const int h = idx / cpr, i0 = (idx % cpr) * 8;
-    uint4 ua = *reinterpret_cast<const uint4*>(row + h * D + i0);
-    uint4 ub = *reinterpret_cast<const uint4*>(row + h * D + i0 + half);
-    __nv_bfloat16* a8 = reinterpret_cast<__nv_bfloat16*>(&ua);
-    __nv_bfloat16* b8 = reinterpret_cast<__nv_bfloat16*>(&ub);
+    float a8[8], b8[8];
+    src.load8(row + h * D + i0, a8);
+    src.load8(row + h * D + i0 + half, b8);
     uint4 ra, rb;
     __nv_bfloat16* ra8 = reinterpret_cast<__nv_bfloat16*>(&ra);
     __nv_bfloat16* rb8 = reinterpret_cast<__nv_bfloat16*>(&rb);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      float a = __bfloat162float(a8[k]), b = __bfloat162float(b8[k]);
+      float a = a8[k], b = b8[k];
       if (bias) {  // qkv bias (Qwen2), rounded to bf16 like the projection output
         a = __bfloat162float(__float2bfloat16(a + __bfloat162float(bias[h * D + i0 + k])));
         b = __bfloat162float(__float2bfloat16(b + __bfloat162float(bias[h * D + i0 + k + half])));
@@ -581,13 +609,36 @@ int psd_add_rmsnorm(void* x, int ldx, const float* partials, int S, size_t slice
   return (int)cudaGetLastError();
 }
 
+static int rope_launch(const QkvSrc& src, int M, int Hq, int Hkv, int D,
+                       const int32_t* positions, const int32_t* slots, const float* inv_freq,
+                       const void* qkv_bias, void* q_out, void* k_cache, void* v_cache,
+                       void* stream);
+
+int psd_rope_kv_partials(const float* qkv_partials, int S, size_t slice, int M, int Hq, int Hkv,
+                         int D, const int32_t* positions, const int32_t* slots,
+                         const float* inv_freq, const void* qkv_bias, void* q_out,
+                         void* k_cache, void* v_cache, void* stream) {
+  QkvSrc src{nullptr, qkv_partials, S, slice};
+  return rope_launch(src, M, Hq, Hkv, D, positions, slots, inv_freq, qkv_bias, q_out, k_cache,
+                     v_cache, stream);
+}
+
 int psd_rope_kv(const void* qkv, int M, int Hq, int Hkv, int D, const int32_t* positions,
                 const int32_t* slots, const float* inv_freq, const void* qkv_bias, void* q_out,
                 void* k_cache, void* v_cache, void* stream) {
+  QkvSrc src{static_cast<const __nv_bfloat16*>(qkv), nullptr, 0, 0};
+  return rope_launch(src, M, Hq, Hkv, D, positions, slots, inv_freq, qkv_bias, q_out, k_cache,
+                     v_cache, stream);
+}
+
+static int rope_launch(const QkvSrc& src, int M, int Hq, int Hkv, int D,
+                       const int32_t* positions, const int32_t* slots, const float* inv_freq,
+                       const void* qkv_bias, void* q_out, void* k_cache, void* v_cache,
+                       void* stream) {
   if (M <= 0) return 0;
   if (D % 16 || D > 256) return (int)cudaErrorInvalidValue;
   rope_kv_kernel<<<M, 256, 0, (cudaStream_t)stream>>>(
-      static_cast<const __nv_bfloat16*>(qkv), Hq, Hkv, D, positions, slots, inv_freq,
+      src, Hq, Hkv, D, positions, slots, inv_freq,
       static_cast<const __nv_bfloat16*>(qkv_bias), static_cast<__nv_bfloat16*>(q_out), static_cast<__nv_bfloat16*>(k_cache),
       static_cast<__nv_bfloat16*>(v_cache));
   return (int)cudaGetLastError();

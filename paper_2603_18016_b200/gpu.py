@@ -120,8 +120,18 @@ class GpuBackend:
                                        device=dev)
             self.dlogits = torch.empty(B, self.dshape.vocab, dtype=torch.float32, device=dev)
             if mode == "sample":
-                self.qbuf = torch.empty(max_requests, K, self.dshape.vocab, dtype=torch.float32,
+                # per-slot draft distributions q (fp32 logits after the bias);
+                # K1 reads request b's rows at qbuf[slot_b] (verify_sample_rows)
+                self.qbuf = torch.empty(nslot * K, self.dshape.vocab, dtype=torch.float32,
                                         device=dev)
+                self.d_u = torch.empty(K, B, dtype=torch.float32, device=dev)
+                self.v_u = torch.empty(B, K + 1, dtype=torch.float32, device=dev)
+                # per-row (request id, committed length) keys of the uniforms
+                self.d_key_host = torch.zeros(2 * B + K * B, dtype=i32).pin_memory()
+                self.d_key = torch.zeros(2 * B + K * B, dtype=i32, device=dev)
+                self.v_key_host = torch.zeros(2 * B, dtype=i32).pin_memory()
+                self.v_key = torch.zeros(2 * B, dtype=i32, device=dev)
+                self.d_dummy = torch.zeros(B, 1, 4, dtype=torch.float32, device=dev)
             self.v_ids = torch.empty(B, K, dtype=i32, device=dev)
             self.v_acc = torch.empty(B, dtype=i32, device=dev)
             self.v_out = torch.empty(B * (K + 1), dtype=i32, device=dev)
@@ -137,6 +147,9 @@ class GpuBackend:
             self.s_target = torch.cuda.Stream(dev)
             self.s_draft = torch.cuda.Stream(dev) if dual_stream else self.s_target
             torch.cuda.synchronize(dev)
+        self.seed_draft = (seed * 0x9E3779B1 + 0xD7A7) & 0xFFFFFFFFFFFF
+        self.seed_verify = (seed * 0x85EBCA77 + 0x7E51) & 0xFFFFFFFFFFFF
+        self.capture_verify = None  # set to a list to record K1 inputs (tests)
         self.use_graphs = use_graphs
         self.graphs: dict[tuple, torch.cuda.CUDAGraph] = {}
         self.graph_streams: list = []
@@ -360,6 +373,16 @@ class GpuBackend:
                 }
             fwd.stage(i, arrays)
         fwd.upload(kmax)
+        if self.mode == "sample":
+            kh = self.d_key_host.numpy()
+            B = self.max_batch
+            kh[:nb] = [r for r in rows] + [0] * (nb - n)
+            kh[B:B + nb] = L
+            # q storage row of (row r, step i): slot * k_max + i (scratch slot for padding)
+            K = self.k_max
+            for i in range(kmax):
+                kh[2 * B + i * B:2 * B + i * B + nb] = np.where(real & (i < k), sl * K + i, -1)
+            self.d_key.copy_(self.d_key_host, non_blocking=True)
         self._run_graph(("draft", nb, kmax), lambda: self._draft_launch(nb, kmax))
 
     def _draft_launch(self, nb: int, kmax: int) -> None:
@@ -378,7 +401,19 @@ class GpuBackend:
                 ops.verify_greedy(self.dlogits[:nb].view(nb, 1, -1), self.d_ids0[:nb],
                                   self.d_len0[:nb], self.d_acc[:nb], self.d_out[:nb])
             else:
-                raise ConfigError("sampling-mode draft loop not implemented yet")
+                B = self.max_batch
+                V = self.dshape.vocab
+                # keep q for the verifier, then sample the draft token from q
+                native.check(lib.psd_copy_rows_f32(
+                    self.qbuf.data_ptr(), self.d_key[2 * B + i * B:].data_ptr(), V,
+                    self.dlogits.data_ptr(), V, nb, V, st), "q rows")
+                u = self.d_u[i, :nb]
+                native.check(lib.psd_philox_uniforms(
+                    self.seed_draft, self.d_key.data_ptr(), self.d_key[B:].data_ptr(), nb, 1, i,
+                    u.data_ptr(), st), "draft uniforms")
+                ops.verify_sample(self.dlogits[:nb].view(nb, 1, -1), self.d_dummy[:nb, :0],
+                                  self.d_ids0[:nb], self.d_len0[:nb], u.view(nb, 1),
+                                  self.temperature, self.d_acc[:nb], self.d_out[:nb])
             native.check(lib.psd_index_copy_i32(self.slot_tok.data_ptr(),
                                                 fwd.view("scatter_dst", i).data_ptr(),
                                                 self.d_out.data_ptr(), None, nb, st),
@@ -431,7 +466,25 @@ class GpuBackend:
             vm[3 * B:3 * B + nb * kmax] = (sl[:, None] * ldt + 2 + np.arange(kmax)[None, :]
                                            ).reshape(-1)
         self.v_meta.copy_(self.v_meta_host, non_blocking=True)
+        if self.mode == "sample":
+            kh = self.v_key_host.numpy()
+            kh[:nb] = [r.request_id for r in rows] + [0] * (nb - n)
+            kh[B:B + nb] = L
+            self.v_key.copy_(self.v_key_host, non_blocking=True)
         self._run_graph(("verify", nb, kmax), lambda: self._verify_launch(nb, kmax))
+        if self.capture_verify is not None:
+            torch.cuda.current_stream(self.device).synchronize()
+            V = self.tshape.vocab
+            rec = {"target": self.tlogits[:nb * K1].view(nb, K1, V)[:n].cpu().numpy(),
+                   "ids": self.v_ids.view(-1)[:nb * kmax].view(nb, kmax)[:n].cpu().numpy(),
+                   "len": k[:n].astype(np.int32), "acc": self.v_acc[:n].cpu().numpy(),
+                   "out": self.v_out[:nb * K1].view(nb, K1)[:n].cpu().numpy()}
+            if self.mode == "sample":
+                Vd = self.dshape.vocab
+                q = self.qbuf.view(-1, self.k_max, Vd)
+                rec["draft"] = q[torch.as_tensor(sl[:n])][:, :kmax].cpu().numpy()
+                rec["uniforms"] = self.v_u.view(-1)[:nb * K1].view(nb, K1)[:n].cpu().numpy()
+            self.capture_verify.append(rec)
         return n
 
     def _verify_launch(self, nb: int, kmax: int) -> None:
@@ -462,7 +515,17 @@ class GpuBackend:
         if self.mode == "greedy":
             ops.verify_greedy(logits, v_ids, v_len, self.v_acc[:nb], out)
         else:
-            raise ConfigError("sampling-mode verify not implemented yet")
+            native.check(lib.psd_philox_uniforms(
+                self.seed_verify, self.v_key.data_ptr(), self.v_key[B:].data_ptr(), nb, K1, 0,
+                self.v_u.data_ptr(), st), "verify uniforms")
+            Vd = self.dshape.vocab
+            ws = ops._verify_workspace(self.device, nb, kmax, self.tshape.vocab, Vd, True)
+            native.check(lib.psd_verify_sample_rows(
+                logits.data_ptr(), K1 * self.tshape.vocab, self.tshape.vocab,
+                self.tshape.vocab, self.qbuf.data_ptr(), v_slot.data_ptr(), self.k_max * Vd, Vd,
+                Vd, v_ids.data_ptr(), v_len.data_ptr(), self.v_u.data_ptr(), self.temperature, nb,
+                kmax, self.v_acc.data_ptr(), out.data_ptr(), ws.data_ptr(), ws.numel(), st),
+                "verify_sample_rows")
         native.check(lib.psd_commit(self.v_acc.data_ptr(), out.data_ptr(), kmax,
                                     v_slot.data_ptr(), nb, self.generated.data_ptr(),
                                     self.slot_tok.data_ptr(), self.ldt, self.outputs.data_ptr(),

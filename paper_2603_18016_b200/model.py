@@ -33,7 +33,7 @@ import torch
 from . import native
 from .errors import ConfigError
 
-__all__ = ["ModelShape", "PRESETS", "Transformer", "Forward", "successor_table",
+__all__ = ["ModelShape", "PRESETS", "Transformer", "Forward", "pack_gate_up", "successor_table",
            "tensor_seed", "rope_inv_freq"]
 
 INIT_STD = 0.02
@@ -108,6 +108,16 @@ def rope_inv_freq(shape: ModelShape) -> np.ndarray:
     return inv.astype(np.float32)
 
 
+def pack_gate_up(gate: torch.Tensor, up: torch.Tensor) -> torch.Tensor:
+    """[F, H] gate and up -> [2F, H] in the PSD_EPI_SILU order: per 128-row
+    tile and per 32-row quarter q, 16 gate rows then the 16 matching up rows
+    (so one warp shuffle pairs them in the GEMM epilogue)."""
+    F, H = gate.shape
+    g = gate.view(F // 64, 4, 16, H)
+    u = up.view(F // 64, 4, 16, H)
+    return torch.stack([g, u], dim=2).reshape(2 * F, H).contiguous()
+
+
 def tensor_seed(model_seed: int, layer: int, which: int) -> int:
     """Per-tensor init seed (also used by oracle/model.py)."""
     return (model_seed * 1_000_003 + (layer + 1) * 101 + which) & 0x7FFFFFFF
@@ -171,9 +181,7 @@ class Transformer:
             up = torch.zeros(Fp, H, dtype=bf, device=dev)
             fill(gate[:F], tensor_seed(seed, li, self.W_GATE))
             fill(up[:F], tensor_seed(seed, li, self.W_UP))
-            # pack per 128-row tile: 64 gate rows then the matching 64 up rows
-            wgu = torch.cat([gate.view(Fp // 64, 64, H), up.view(Fp // 64, 64, H)], dim=1)
-            wgu = wgu.reshape(2 * Fp, H).contiguous()
+            wgu = pack_gate_up(gate, up)
             del gate, up
             down = torch.zeros(H, Fp, dtype=bf, device=dev)
             dtmp = fill(torch.empty(H, F, dtype=bf, device=dev), tensor_seed(seed, li, self.W_DOWN))
@@ -250,6 +258,17 @@ class Forward:
                 lib.psd_gemm_plan(mm, n_out, k_in, native.EPI_BF16, 0, None, ctypes.byref(wb))
                 need = max(need, wb.value)
         self.ws = torch.zeros(max(need, 1 << 20), dtype=torch.uint8, device=dev)
+        # fp32 split-K partials of the QKV / O / down GEMMs (one buffer, reused
+        # in sequence: each is consumed before the next GEMM overwrites it)
+        self._nsplit = ctypes.byref(ctypes.c_int(1))
+        pneed = 0
+        for mm in sorted({T, max_logit_rows, min(T, 64), min(T, 320), 32, 2 * max_seqs}):
+            for (n_out, k_in) in ((s.qkv_out, s.hidden), (s.hidden, s.heads * s.head_dim),
+                                  (s.hidden, s.ffn_padded)):
+                sp = ctypes.c_int()
+                lib.psd_gemm_plan(mm, n_out, k_in, native.EPI_PARTIAL, 0, ctypes.byref(sp), None)
+                pneed = max(pneed, sp.value * mm * n_out)
+        self.part = torch.empty(pneed, dtype=torch.float32, device=dev)
         sizes = {"tokens": T, "positions": T, "slots": T, "seq_slot": max_seqs,
                  "q_start": max_seqs, "q_len": max_seqs, "q_pos0": max_seqs, "kv_len": max_seqs,
                  "logit_rows": max_logit_rows, "gather_src": T, "scatter_dst": max_logit_rows}
@@ -314,22 +333,29 @@ class Forward:
                            st), "psd_embed")
         scale = 1.0 / math.sqrt(s.head_dim)
         ws, wsn = self.ws.data_ptr(), self.ws.numel()
+        part, partn = self.part.data_ptr(), self.part.numel() * 4
+        nsp = self._nsplit
         Dq = s.heads * s.head_dim
         Fp = s.ffn_padded
         X = self.x.data_ptr()
+        # QKV / O / down: grid split-K GEMMs (few weight tiles) whose fp32
+        # partials are reduced inside the consumer kernel (RoPE, add+RMSNorm);
+        # gate/up and the LM head: stream-K persistent GEMMs
+        prev_S = 0  # splits of the pending down-proj partials (0 = none)
         for li, L in enumerate(m.layers):
             kc = m.kv[li, 0]
             vc = m.kv[li, 1]
-            _chk(lib.psd_add_rmsnorm(X, H, None, 0, 0, H, None, L["attn_norm"].data_ptr(),
-                                     self.xn.data_ptr(), H, M, H, s.rms_eps, 0, st), "attn norm")
-            _chk(lib.psd_gemm_bf16(self.xn.data_ptr(), H, M, H, L["wqkv"].data_ptr(), H,
-                                   s.qkv_out, self.qkv.data_ptr(), s.qkv_out, native.EPI_BF16,
-                                   None, 0, 0, ws, wsn, st), "gemm qkv")
-            _chk(lib.psd_rope_kv(self.qkv.data_ptr(), M, s.heads, s.kv_heads, s.head_dim,
-                                 v["positions"].data_ptr(), v["slots"].data_ptr(),
-                                 m.inv_freq.data_ptr(),
-                                 L["bqkv"].data_ptr() if L["bqkv"] is not None else None,
-                                 self.q.data_ptr(), kc.data_ptr(), vc.data_ptr(), st), "rope_kv")
+            _chk(lib.psd_add_rmsnorm(X, H, part if prev_S else None, prev_S, M * H, H, None,
+                                     L["attn_norm"].data_ptr(), self.xn.data_ptr(), H, M, H,
+                                     s.rms_eps, 1, st), "add+attn norm")
+            _chk(lib.psd_gemm_partials(self.xn.data_ptr(), H, M, H, L["wqkv"].data_ptr(), H,
+                                       s.qkv_out, part, partn, 0, nsp, st), "gemm qkv")
+            _chk(lib.psd_rope_kv_partials(part, nsp._obj.value, M * s.qkv_out, M, s.heads,
+                                          s.kv_heads, s.head_dim, v["positions"].data_ptr(),
+                                          v["slots"].data_ptr(), m.inv_freq.data_ptr(),
+                                          L["bqkv"].data_ptr() if L["bqkv"] is not None else None,
+                                          self.q.data_ptr(), kc.data_ptr(), vc.data_ptr(), st),
+                 "rope_kv")
             _chk(lib.psd_attention(self.q.data_ptr(), kc.data_ptr(), vc.data_ptr(),
                                    self.block_table.data_ptr(), self.block_table.shape[1],
                                    v["seq_slot"].data_ptr(), v["q_start"].data_ptr(),
@@ -337,19 +363,21 @@ class Forward:
                                    v["kv_len"].data_ptr(), n_seqs, max_q_len, s.heads,
                                    s.kv_heads, s.head_dim, m.block_size, scale,
                                    self.attn.data_ptr(), st), "attention")
-            _chk(lib.psd_gemm_bf16(self.attn.data_ptr(), Dq, M, Dq, L["wo"].data_ptr(), Dq, H, X,
-                                   H, native.EPI_RESID, X, H, 0, ws, wsn, st), "gemm o")
-            _chk(lib.psd_add_rmsnorm(X, H, None, 0, 0, H, None, L["mlp_norm"].data_ptr(),
-                                     self.xn.data_ptr(), H, M, H, s.rms_eps, 0, st), "mlp norm")
+            _chk(lib.psd_gemm_partials(self.attn.data_ptr(), Dq, M, Dq, L["wo"].data_ptr(), Dq, H,
+                                       part, partn, 0, nsp, st), "gemm o")
+            _chk(lib.psd_add_rmsnorm(X, H, part, nsp._obj.value, M * H, H, None,
+                                     L["mlp_norm"].data_ptr(), self.xn.data_ptr(), H, M, H,
+                                     s.rms_eps, 1, st), "add+mlp norm")
             _chk(lib.psd_gemm_bf16(self.xn.data_ptr(), H, M, H, L["wgu"].data_ptr(), H, 2 * Fp,
                                    self.act.data_ptr(), Fp, native.EPI_SILU, None, 0, 0, ws, wsn,
                                    st), "gemm gate/up")
-            _chk(lib.psd_gemm_bf16(self.act.data_ptr(), Fp, M, Fp, L["wdown"].data_ptr(), Fp, H,
-                                   X, H, native.EPI_RESID, X, H, 0, ws, wsn, st), "gemm down")
+            _chk(lib.psd_gemm_partials(self.act.data_ptr(), Fp, M, Fp, L["wdown"].data_ptr(), Fp,
+                                       H, part, partn, 0, nsp, st), "gemm down")
+            prev_S = nsp._obj.value
         if n_logit_rows == 0 or logits is None:
             return  # prefill: only the KV cache is needed
         R = n_logit_rows
-        _chk(lib.psd_add_rmsnorm(X, H, None, 0, 0, H, v["logit_rows"].data_ptr(),
+        _chk(lib.psd_add_rmsnorm(X, H, part, prev_S, M * H, H, v["logit_rows"].data_ptr(),
                                  m.final_norm.data_ptr(), self.xf.data_ptr(), H, R, H, s.rms_eps,
                                  0, st), "final norm")
         ld = logits_ld or s.vocab

@@ -43,6 +43,7 @@ SIGNATURES: dict[str, tuple] = {
                            _p, _p]),
     "psd_bigram_bias": (_i, [_p, _i64, _p, _i, _p, _i, _f, _p]),
     "psd_philox_uniforms": (_i, [_c.c_uint64, _p, _p, _i, _i, _i, _p, _p]),
+    "psd_rope_kv_partials": (_i, [_p, _i, _sz, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _p, _p]),
     "psd_copy_rows_f32": (_i, [_p, _p, _i64, _p, _i64, _i, _i, _p]),
     "psd_verify_sample_rows": (_i, [_p, _i64, _i64, _i, _p, _p, _i64, _i64, _i, _p, _p, _p, _f,
                                     _i, _i, _p, _p, _p, _sz, _p]),

@@ -60,8 +60,9 @@ def test_gemm_silu_mul(cuda_device, M, splits):
     x = torch.randn(M, K, device=cuda_device, generator=g).to(torch.bfloat16)
     wg = (torch.randn(F, K, device=cuda_device, generator=g) * 0.05).to(torch.bfloat16)
     wu = (torch.randn(F, K, device=cuda_device, generator=g) * 0.05).to(torch.bfloat16)
-    packed = torch.cat([wg.view(F // 64, 64, K), wu.view(F // 64, 64, K)], dim=1).reshape(2 * F, K)
-    y = ops.gemm(x, packed.contiguous(), epi=native.EPI_SILU, splits=splits)
+    from paper_2603_18016_b200.model import pack_gate_up
+    packed = pack_gate_up(wg, wu)
+    y = ops.gemm(x, packed, epi=native.EPI_SILU, splits=splits)
     torch.cuda.synchronize()
     gt = _ref(x, wg)
     ref = torch.nn.functional.silu(gt) * _ref(x, wu)

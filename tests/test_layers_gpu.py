@@ -100,8 +100,8 @@ def test_tiny_model_gemm_shapes(cuda_device, M, N, K, epi):
     ref = x.float() @ w.float().T
     if epi == "silu":
         F = N // 2
-        gt = ref.view(M, F // 64, 2, 64)[:, :, 0].reshape(M, F)
-        up = ref.view(M, F // 64, 2, 64)[:, :, 1].reshape(M, F)
+        gt = ref.view(M, F // 64, 4, 2, 16)[:, :, :, 0].reshape(M, F)
+        up = ref.view(M, F // 64, 4, 2, 16)[:, :, :, 1].reshape(M, F)
         ref = torch.nn.functional.silu(gt) * up
     err = (y.float() - ref).abs().max().item()
     assert err <= 1e-2 * ref.abs().max().item() + 1e-3, err
@@ -128,8 +128,8 @@ def test_gemm_pretiled_weights(cuda_device, M, N, K, epi):
     ref = x.float() @ w.float().T
     if epi == "silu":
         F = N // 2
-        gt = ref.view(M, F // 64, 2, 64)[:, :, 0].reshape(M, F)
-        up = ref.view(M, F // 64, 2, 64)[:, :, 1].reshape(M, F)
+        gt = ref.view(M, F // 64, 4, 2, 16)[:, :, :, 0].reshape(M, F)
+        up = ref.view(M, F // 64, 4, 2, 16)[:, :, :, 1].reshape(M, F)
         ref = torch.nn.functional.silu(gt) * up
     err = (y.float() - ref).abs().max().item()
     assert err <= 1e-2 * ref.abs().max().item() + 1e-3, err

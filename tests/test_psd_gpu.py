@@ -123,3 +123,24 @@ def test_greedy_psd_equals_sd_on_gpu(cuda_device):
                      prefill_chunk_tokens=512)
     ss, _ = _tiny_run("standard-sd", gb2)
     assert [r.output_ids for r in ps.request_list()] == [r.output_ids for r in ss.request_list()]
+
+
+@pytest.mark.parametrize("temperature", [1.0, 0.7])
+def test_sampling_psd_k1_bit_exact_on_real_logits(cuda_device, temperature):
+    """Sampling mode end to end: every verification K1 ran inside the PSD loop
+    is replayed through the CPU oracle on the same (GPU-produced) logits and
+    uniforms -> identical accepted lengths and tokens."""
+    from oracle import verify as ov
+    gb = GpuBackend("tiny-target", "tiny-draft", max_requests=16, max_batch=16, k_max=4,
+                    max_seq_len=128, seed=3, beta_target=1.0, beta_draft=1.0,
+                    mode="sample", temperature=temperature, prefill_chunk_tokens=512)
+    gb.capture_verify = []
+    st, rep = _tiny_run("psd", gb)
+    assert rep.finished == 16 and all(len(r.output_ids) == 32 for r in st.request_list())
+    assert len(gb.capture_verify) >= 5
+    for rec in gb.capture_verify:
+        acc, out = ov.verify_sample(rec["target"], rec["draft"], rec["ids"], rec["len"],
+                                    rec["uniforms"], temperature)
+        np.testing.assert_array_equal(acc, rec["acc"])
+        np.testing.assert_array_equal(out, rec["out"])
+    assert 0 < rep.total_accepted < rep.total_drafted

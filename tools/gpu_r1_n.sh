@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 300 python -m pytest tests/test_layers_gpu.py -q > gpurun_out/pytest_n.log 2>&1
+timeout 300 python tools/kbench.py --only gemm > gpurun_out/kbench5.log 2>&1
+echo done

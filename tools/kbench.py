@@ -205,6 +205,18 @@ def main():
 
     def want(k):
         return sel is None or k in sel
+    if want("gemmx"):
+        gemm_case("8B gu as f32", 192, 28672, 4096, "f32")
+        gemm_case("8B gu as bf16", 192, 28672, 4096, "bf16")
+        gemm_case("8B gu silu", 192, 28672, 4096, "silu")
+        gemm_case("8B N57344 bf16", 192, 57344, 4096, "bf16", copies=3)
+        gemm_case("8B N114688 bf16", 192, 114688, 4096, "bf16", copies=2)
+        gemm_case("1B gu as f32", 32, 16384, 2048, "f32")
+        gemm_case("1B gu silu", 32, 16384, 2048, "silu")
+        gemm_case("1B N65536 f32", 32, 65536, 2048, "f32", copies=3)
+        gemm_case("M128 gu bf16", 128, 28672, 4096, "bf16")
+        gemm_case("M64 gu bf16", 64, 28672, 4096, "bf16")
+        gemm_case("M256 gu bf16", 256, 28672, 4096, "bf16")
     if want("gemm"):
         # 8B verify (M = 32 x 6)
         gemm_case("8B qkv", 192, 6144, 4096, "bf16")
