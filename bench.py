@@ -252,10 +252,9 @@ def run_reference(args) -> None:
 
 def run_ours(args) -> None:
     import torch
-    world, rank, local = _dist()
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", init_method="env://")
+
+    from paper_2603_18016_b200 import dist as pd
+    world, rank, local = pd.init("nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     from paper_2603_18016_b200 import mean_accepted_length, run
@@ -272,6 +271,8 @@ def run_ours(args) -> None:
         if world > 1:
             torch.distributed.barrier()
 
+    launches = {}
+
     def one(mode):
         return run(_config(mode), _workload(rank), backend=be)
 
@@ -286,16 +287,14 @@ def run_ours(args) -> None:
         e0.record()
         reps = []
         stats0 = dict(be.stats)
+        l0 = be.launches
         for _ in range(args.steps):
             reps.append(one(mode)[1])
         e1.record()
         barrier()
-        ms = e0.elapsed_time(e1)
-        if world > 1:
-            t = torch.tensor([ms], device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            ms = t.item()
-        tokens = sum(r.total_generated for r in reps)
+        launches[mode] = be.launches - l0
+        ms_local = e0.elapsed_time(e1)
+        tokens, ms = pd.aggregate(sum(r.total_generated for r in reps), ms_local, dev)
         results[mode] = {"ms": ms, "tokens": tokens, "reps": reps,
                          "clocks": clocks.stop() if clocks else None,
                          "draft_ms": be.stats["draft_ms"] - stats0["draft_ms"],
@@ -319,13 +318,13 @@ def run_ours(args) -> None:
             cpu = {"value": None, "unit": "tok/s", "cores": os.cpu_count(), "kind": "port",
                    "sample": f"skipped: {exc}"}
     if rank != 0:
-        if world > 1:
-            torch.distributed.destroy_process_group()
+        pd.finalize()
         return
     psd, sd = results["psd"], results["standard-sd"]
-    value = world * psd["tokens"] / (psd["ms"] * 1e-3)
-    sd_value = world * sd["tokens"] / (sd["ms"] * 1e-3)
+    value = psd["tokens"] / (psd["ms"] * 1e-3)  # tokens summed over ranks / max time
+    sd_value = sd["tokens"] / (sd["ms"] * 1e-3)
     r0 = psd["reps"][0]
+    steps_sd = sd["steps"] / max(1, args.steps)
     steps_psd = psd["steps"] / max(1, args.steps)
     h2d = CFG["n_requests"] * CFG["prompt"] * 4 + int(steps_psd) * 4 * 2 * CFG["m"]
     d2h = CFG["n_requests"] * CFG["output"] * 4 + int(steps_psd) * 4 * CFG["m"]
@@ -341,8 +340,12 @@ def run_ours(args) -> None:
                    CFG["output"], "parallelism": f"replicas{world}",
                    "l2": "inputs > L2 (weights 18.5 GB streamed per step)",
                    "synthetic_language_beta": [BETA_TARGET, BETA_DRAFT]},
-        "sd": {"value": round(sd_value, 1), "unit": "tok/s", "mode": "standard-sd, one batch "
-                                                                    "of 64 (sd_batch_factor 2)"},
+        "sd": {"value": round(sd_value, 1), "unit": "tok/s",
+               "mode": "standard-sd, one batch of 64 (sd_batch_factor 2)",
+               "steps_per_pass": steps_sd,
+               "draft_ms_per_pass": round(sd["draft_ms"] / args.steps, 2),
+               "verify_ms_per_pass": round(sd["verify_ms"] / args.steps, 2),
+               "gpu_launches": launches.get("standard-sd")},
         "psd_vs_sd": round(value / sd_value, 4),
         "mean_accepted_len": round(mean_accepted_length(r0), 4),
         "accepted_per_verify": round(r0.total_accepted / max(1, r0.total_bonus), 4),
@@ -351,15 +354,14 @@ def run_ours(args) -> None:
         "verify_ms_per_pass": round(psd["verify_ms"] / args.steps, 2),
         "e2e": {"value": round(rep_e2e.total_generated / e2e_s, 1), "unit": "tok/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "gpu_launches": None,
+        "gpu_launches": launches.get("psd"),
         "clocks": psd["clocks"],
         "roofline": dict(roof, peak_kind=peak_kind),
         "verify_kernel": vk,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
-        torch.distributed.destroy_process_group()
+    pd.finalize()
 
 
 def main() -> None:

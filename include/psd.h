@@ -163,6 +163,9 @@ int psd_commit(const int32_t* accepted_len, const int32_t* out_tokens, int K,
 /* dst[dst_idx ? dst_idx[i] : i] = src[src_idx ? src_idx[i] : i], negative dst skipped */
 int psd_index_copy_i32(int32_t* dst, const int32_t* dst_idx, const int32_t* src,
                        const int32_t* src_idx, int n, void* stream);
+/* kernels enqueued by this library so far (host-side counter; a captured
+ * CUDA graph's launches are counted once, at capture) */
+long long psd_launch_count(void);
 /* deterministic random init: (u - 1/2) * span, u = splitmix64(seed, i) >> 40 / 2^24 */
 int psd_fill_uniform_bf16(void* out, size_t n, uint64_t seed, float span, void* stream);
 

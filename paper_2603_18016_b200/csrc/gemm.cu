@@ -29,6 +29,7 @@
 #include <mutex>
 
 #include "../../include/psd.h"
+#include "common.h"
 #include "sm100.cuh"
 
 namespace {
@@ -537,6 +538,7 @@ int launch_bn(const CUtensorMap& mw, const CUtensorMap& mx, const GemmArgs& g, d
     if (e != cudaSuccess) return (int)e;
     attr_done = true;
   }
+  psd::count_launches();
   gemm_kernel<BN, EPI><<<grid, kThreads, C::SMEM, st>>>(mw, mx, g);
   return (int)cudaGetLastError();
 }
@@ -551,6 +553,7 @@ int launch_sk_bn(const CUtensorMap& mw, const CUtensorMap& mx, const SKArgs& g, 
     if (e != cudaSuccess) return (int)e;
     attr_done = true;
   }
+  psd::count_launches();
   gemm_sk_kernel<BN, EPI, TILED><<<g.G, kThreads, C::SMEM, st>>>(mw, mx, g);
   return (int)cudaGetLastError();
 }
@@ -697,6 +700,7 @@ size_t psd_tiled_weight_bytes(int N, int K) {
 
 int psd_tile_weights(const void* W, int N, int K, int ldw, void* tiled, void* stream) {
   if (!W || !tiled || N % BM || K % 8 || ldw % 8) return (int)cudaErrorInvalidValue;
+  psd::count_launches();
   tile_weights_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(
       static_cast<const __nv_bfloat16*>(W), N, K, ldw, static_cast<__nv_bfloat16*>(tiled));
   return (int)cudaGetLastError();
@@ -828,6 +832,7 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
     const int Nout = epi == PSD_EPI_SILU ? N / 2 : N;
     const size_t total = (size_t)M * Nout;
     const int blocks = (int)std::min<size_t>((total + 255) / 256, 148 * 8);
+    psd::count_launches();
     gemm_reduce_kernel<<<blocks, 256, 0, st>>>(static_cast<const float*>(workspace), splits, M, N,
                                                epi, Y, ldy, static_cast<const __nv_bfloat16*>(R),
                                                ldr);

@@ -11,6 +11,7 @@
 #include <stdint.h>
 
 #include "../../include/psd.h"
+#include "common.h"
 
 namespace {
 
@@ -549,11 +550,14 @@ __global__ void copy_rows_kernel(float* __restrict__ dst, const int32_t* __restr
 
 extern "C" {
 
+long long psd_launch_count(void) { return psd::launch_counter().load(); }
+
 int psd_copy_rows_f32(float* dst, const int32_t* dst_rows, int64_t dst_ld, const float* src,
                       int64_t src_ld, int nrows, int ncols, void* stream) {
   if (nrows <= 0) return 0;
   if ((ncols & 3) || (dst_ld & 3) || (src_ld & 3)) return (int)cudaErrorMisalignedAddress;
   dim3 grid(16, nrows);
+  psd::count_launches();
   copy_rows_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(dst, dst_rows, dst_ld, src, src_ld,
                                                            ncols);
   return (int)cudaGetLastError();
@@ -562,6 +566,7 @@ int psd_copy_rows_f32(float* dst, const int32_t* dst_rows, int64_t dst_ld, const
 int psd_index_copy_i32(int32_t* dst, const int32_t* dst_idx, const int32_t* src,
                        const int32_t* src_idx, int n, void* stream) {
   if (n <= 0) return 0;
+  psd::count_launches();
   index_copy_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(dst, dst_idx, src, src_idx, n);
   return (int)cudaGetLastError();
 }
@@ -570,6 +575,7 @@ int psd_commit(const int32_t* accepted_len, const int32_t* out_tokens, int K,
                const int32_t* row_slot, int n, int32_t* generated, int32_t* slot_tokens,
                int slot_tokens_ld, int32_t* outputs, int outputs_ld, void* stream) {
   if (n <= 0) return 0;
+  psd::count_launches();
   commit_kernel<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(
       accepted_len, out_tokens, K, row_slot, n, generated, slot_tokens, slot_tokens_ld, outputs,
       outputs_ld);
@@ -578,6 +584,7 @@ int psd_commit(const int32_t* accepted_len, const int32_t* out_tokens, int K,
 
 int psd_fill_uniform_bf16(void* out, size_t n, uint64_t seed, float span, void* stream) {
   if (n == 0) return 0;
+  psd::count_launches();
   fill_uniform_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(static_cast<__nv_bfloat16*>(out),
                                                                 n, seed, span);
   return (int)cudaGetLastError();
@@ -586,6 +593,7 @@ int psd_fill_uniform_bf16(void* out, size_t n, uint64_t seed, float span, void* 
 int psd_embed(const int32_t* tokens, int M, const void* table, int H, void* out, void* stream) {
   if (M <= 0) return 0;
   if (H % 8) return (int)cudaErrorInvalidValue;
+  psd::count_launches();
   embed_kernel<<<M, 128, 0, (cudaStream_t)stream>>>(
       tokens, static_cast<const __nv_bfloat16*>(table), static_cast<__nv_bfloat16*>(out), H);
   return (int)cudaGetLastError();
@@ -597,6 +605,7 @@ int psd_add_rmsnorm(void* x, int ldx, const float* partials, int S, size_t slice
   if (M <= 0) return 0;
   if (H % 8 || H > 8 * NORM_THREADS * 4) return (int)cudaErrorInvalidValue;
   auto go = [&](auto kern) {
+    psd::count_launches();
     kern<<<M, NORM_THREADS, 0, (cudaStream_t)stream>>>(
         static_cast<__nv_bfloat16*>(x), ldx, partials, S, slice, ldp, rows,
         static_cast<const __nv_bfloat16*>(w), static_cast<__nv_bfloat16*>(y), ldy, H, eps,
@@ -637,6 +646,7 @@ static int rope_launch(const QkvSrc& src, int M, int Hq, int Hkv, int D,
                        void* stream) {
   if (M <= 0) return 0;
   if (D % 16 || D > 256) return (int)cudaErrorInvalidValue;
+  psd::count_launches();
   rope_kv_kernel<<<M, 256, 0, (cudaStream_t)stream>>>(
       src, Hq, Hkv, D, positions, slots, inv_freq,
       static_cast<const __nv_bfloat16*>(qkv_bias), static_cast<__nv_bfloat16*>(q_out), static_cast<__nv_bfloat16*>(k_cache),
@@ -665,6 +675,7 @@ int psd_attention(const void* q, const void* k_cache, const void* v_cache,
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       attr_done[slot] = true;
     }
+    psd::count_launches();
     kern<<<grid, ATT_THREADS, smem, (cudaStream_t)stream>>>(
         static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k_cache),
         static_cast<const __nv_bfloat16*>(v_cache), block_table, max_blocks, seq_slot, q_start,
@@ -682,6 +693,7 @@ int psd_attention(const void* q, const void* k_cache, const void* v_cache,
 int psd_bigram_bias(float* logits, int64_t ld, const int32_t* prev_tokens, int M,
                     const int32_t* successor, int V, float beta, void* stream) {
   if (M <= 0) return 0;
+  psd::count_launches();
   bigram_bias_kernel<<<(M + 127) / 128, 128, 0, (cudaStream_t)stream>>>(logits, ld, prev_tokens, M,
                                                                       successor, V, beta);
   return (int)cudaGetLastError();
@@ -690,6 +702,7 @@ int psd_bigram_bias(float* logits, int64_t ld, const int32_t* prev_tokens, int M
 int psd_philox_uniforms(uint64_t seed, const int32_t* request_ids, const int32_t* verify_index,
                         int B, int n, int base, float* out, void* stream) {
   if (B * n <= 0) return 0;
+  psd::count_launches();
   philox_uniform_kernel<<<(B * n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
       seed, request_ids, verify_index, B, n, base, out);
   return (int)cudaGetLastError();

@@ -24,6 +24,7 @@
 #include <stdint.h>
 
 #include "../../include/psd.h"
+#include "common.h"
 #include "../../include/psd_canon.h"
 
 namespace {
@@ -482,6 +483,7 @@ int psd_verify_greedy(const float* target_logits, int64_t t_stride_b, int64_t t_
   p.wblk = reinterpret_cast<float*>(w + L.wblk);
   p.NS = (V + PSD_SLICE - 1) / PSD_SLICE; p.NB = (V + PSD_SBLK - 1) / PSD_SBLK; p.R = K + 1;
   dim3 grid(p.NS, B * p.R);
+  psd::count_launches();
   verify_stats<false><<<grid, kThreads, 0, (cudaStream_t)stream>>>(p);
   return (int)cudaGetLastError();
 }
@@ -511,8 +513,10 @@ int psd_verify_sample(const float* target_logits, int64_t t_stride_b, int64_t t_
   p.NS = (V + PSD_SLICE - 1) / PSD_SLICE; p.NB = (V + PSD_SBLK - 1) / PSD_SBLK;
   p.R = 2 * K + 1;
   dim3 grid(p.NS, B * p.R);
+  psd::count_launches();
   verify_stats<true><<<grid, kThreads, 0, (cudaStream_t)stream>>>(p);
   dim3 grid2(p.NB, B);
+  psd::count_launches();
   verify_sample<<<grid2, kThreads, 0, (cudaStream_t)stream>>>(p);
   return (int)cudaGetLastError();
 }
@@ -544,8 +548,10 @@ int psd_verify_sample_rows(const float* target_logits, int64_t t_stride_b, int64
   p.NS = (V + PSD_SLICE - 1) / PSD_SLICE; p.NB = (V + PSD_SBLK - 1) / PSD_SBLK;
   p.R = 2 * K + 1;
   dim3 grid(p.NS, B * p.R);
+  psd::count_launches();
   verify_stats<true><<<grid, kThreads, 0, (cudaStream_t)stream>>>(p);
   dim3 grid2(p.NB, B);
+  psd::count_launches();
   verify_sample<<<grid2, kThreads, 0, (cudaStream_t)stream>>>(p);
   return (int)cudaGetLastError();
 }

@@ -153,6 +153,8 @@ class GpuBackend:
         self.use_graphs = use_graphs
         self.graphs: dict[tuple, torch.cuda.CUDAGraph] = {}
         self.graph_streams: list = []
+        self.graph_launches: dict[tuple, int] = {}
+        self.launches = 0  # kernels of libpsd.so executed (graph replays included)
         self.slots: dict[int, int] = {}
         self.free_slots = list(range(max_requests - 1, -1, -1))
         self.pending_k: dict[int, int] = {}
@@ -285,7 +287,9 @@ class GpuBackend:
                           "q_pos0": np.asarray(q_pos0, np.int32),
                           "kv_len": np.asarray(kv_len, np.int32)})
             fwd.upload(1)
+            c0 = native.load().psd_launch_count()
             fwd.run(len(toks), len(chunk), max(q_len), 0, None)
+            self.launches += native.load().psd_launch_count() - c0
 
     # ---- bucketed, graph-captured device passes ------------------------
     def _bucket(self, n: int) -> int:
@@ -301,11 +305,15 @@ class GpuBackend:
     def _run_graph(self, key, launch) -> None:
         """Replay the CUDA graph for ``key`` on the current stream, capturing
         it from ``launch`` on first use (the first use also runs eagerly)."""
+        lib = native.load()
         g = self.graphs.get(key)
         if g is not None:
             g.replay()
+            self.launches += self.graph_launches[key]
             return
+        c0 = lib.psd_launch_count()
         launch()  # eager: correct results now, warms every kernel / workspace
+        self.launches += lib.psd_launch_count() - c0
         if not self.use_graphs:
             return
         cur = torch.cuda.current_stream(self.device)
@@ -313,8 +321,10 @@ class GpuBackend:
         self.graph_streams.append(cs)  # keep handles unique (per-stream K1 workspaces)
         cs.wait_stream(cur)
         g = torch.cuda.CUDAGraph()
+        c0 = lib.psd_launch_count()
         with torch.cuda.graph(g, stream=cs, capture_error_mode="thread_local"):
             launch()
+        self.graph_launches[key] = lib.psd_launch_count() - c0
         cur.wait_stream(cs)
         self.graphs[key] = g
 

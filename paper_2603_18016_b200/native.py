@@ -50,6 +50,7 @@ SIGNATURES: dict[str, tuple] = {
     "psd_commit": (_i, [_p, _p, _i, _p, _i, _p, _p, _i, _p, _i, _p]),
     "psd_index_copy_i32": (_i, [_p, _p, _p, _p, _i, _p]),
     "psd_fill_uniform_bf16": (_i, [_p, _sz, _c.c_uint64, _f, _p]),
+    "psd_launch_count": (_c.c_longlong, []),
 }
 
 EPI_BF16, EPI_F32, EPI_RESID, EPI_SILU, EPI_PARTIAL = 0, 1, 2, 3, 4
@@ -61,8 +62,8 @@ def header_symbols() -> list[str]:
     """Every function declared in include/psd.h."""
     with open(HEADER) as fh:
         text = fh.read()
-    return sorted(set(re.findall(r"^\s*(?:int|size_t|void|float)\s+\**(psd_\w+)\s*\(", text,
-                                 re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|void|float|long long)\s+\**(psd_\w+)\s*\(",
+                                 text, re.M)))
 
 
 def load():
