@@ -108,7 +108,10 @@ def _workload(seed: int):
 
 
 def _config(mode: str):
+    """psd | standard-sd (one batch of 2m = all 64) | sd-m (batches of m = 32)."""
     from paper_2603_18016_b200 import SimConfig
+    if mode == "sd-m":
+        return SimConfig(mode="standard-sd", m=CFG["m"], k=CFG["k"], sd_batch_factor=1)
     return SimConfig(mode=mode, m=CFG["m"], k=CFG["k"],
                      sd_batch_factor=2 if mode == "standard-sd" else 1)
 
@@ -277,7 +280,7 @@ def run_ours(args) -> None:
         return run(_config(mode), _workload(rank), backend=be)
 
     results = {}
-    for mode in ("psd", "standard-sd"):
+    for mode in ("psd", "standard-sd", "sd-m"):
         for _ in range(args.warmup):
             one(mode)
         barrier()
@@ -320,7 +323,7 @@ def run_ours(args) -> None:
     if rank != 0:
         pd.finalize()
         return
-    psd, sd = results["psd"], results["standard-sd"]
+    psd, sd, sdm = results["psd"], results["standard-sd"], results["sd-m"]
     value = psd["tokens"] / (psd["ms"] * 1e-3)  # tokens summed over ranks / max time
     sd_value = sd["tokens"] / (sd["ms"] * 1e-3)
     r0 = psd["reps"][0]
@@ -346,7 +349,10 @@ def run_ours(args) -> None:
                "draft_ms_per_pass": round(sd["draft_ms"] / args.steps, 2),
                "verify_ms_per_pass": round(sd["verify_ms"] / args.steps, 2),
                "gpu_launches": launches.get("standard-sd")},
+        "sd_m": {"value": round(sdm["tokens"] / (sdm["ms"] * 1e-3), 1), "unit": "tok/s",
+                 "mode": "standard-sd, batches of m=32 (sd_batch_factor 1), the PSD batch size"},
         "psd_vs_sd": round(value / sd_value, 4),
+        "psd_vs_sd_m": round(value / (sdm["tokens"] / (sdm["ms"] * 1e-3)), 4),
         "mean_accepted_len": round(mean_accepted_length(r0), 4),
         "accepted_per_verify": round(r0.total_accepted / max(1, r0.total_bonus), 4),
         "psd_steps_per_pass": steps_psd,

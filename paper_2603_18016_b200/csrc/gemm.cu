@@ -71,7 +71,7 @@ struct Cfg {
   static constexpr int SMEM = 1024 + STAGES * STAGE + 256 + XCHG_BYTES;
 };
 
-__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+__device__ __forceinline__ float silu(float x) { return x * __frcp_rn(1.0f + __expf(-x)); }
 
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -422,9 +422,14 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
               const float up = __shfl_down_sync(0xffffffffu, v[k], 16);
-              const int m = m0 + col + k;
-              if (lane < 16 && m < g.M)
-                Y[(size_t)m * g.ldy + jo] = __float2bfloat16(silu(v[k]) * up);
+              v[k] = silu(v[k]) * up;  // all lanes: no divergence in the math
+            }
+            if (lane < 16) {
+#pragma unroll
+              for (int k = 0; k < 16; ++k) {
+                const int m = m0 + col + k;
+                if (m < g.M) Y[(size_t)m * g.ldy + jo] = __float2bfloat16(v[k]);
+              }
             }
           } else {
             const int n = n0 + row;

@@ -6,6 +6,8 @@
 // 429) together with gemm.cu.  All of these are HBM / latency bound and run
 // on CUDA cores with 128-bit accesses; none is GEMM-shaped enough to pay for
 // tensor-core staging at the BASELINE shapes (<= 64 query rows per KV head).
+#include <algorithm>
+
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -223,7 +225,7 @@ rope_kv_kernel(const QkvSrc src, int Hq, int Hkv, int D,
 // softmax is online in fp32 registers (FlashAttention-2 register layout).
 constexpr int ATT_THREADS = 128;
 constexpr int ATT_MAXR = 64;   // query rows per CTA
-constexpr int ATT_STAGES = 4;  // K/V tiles in flight
+constexpr int ATT_STAGES = 2;  // tile groups in flight (each group = one tile per key group)
 constexpr int ATT_MAX_BLOCKS = 512;  // block-table entries staged in smem (8192 tokens)
 
 __device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4],
@@ -252,6 +254,12 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// Warp roles: RG = ceil(rows / 16) row groups x KG = 4 / RG key groups.  Warp
+// (rg, kg) owns query rows 16rg..16rg+15 and every KG-th key tile; tiles are
+// streamed in groups of KG (one per key group) through an NS-stage cp.async
+// ring, so a decode step (4-8 rows) keeps all 4 warps busy on 4 tiles at a
+// time.  The key groups' (max, sum, O) states are merged through shared
+// memory at the end (same math as split-KV flash decoding, no global traffic).
 template <int D, int KT, int NS>
 __global__ void __launch_bounds__(ATT_THREADS)
 attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ kc,
@@ -259,9 +267,10 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
                  int max_blocks, const int32_t* __restrict__ seq_slot,
                  const int32_t* __restrict__ q_start, const int32_t* __restrict__ q_len,
                  const int32_t* __restrict__ q_pos0, const int32_t* __restrict__ kv_len, int Hq,
-                 int Hkv, int bs, float scale_log2, int tok_per_chunk,
+                 int Hkv, int bs, float scale_log2, int tok_per_chunk, int RG,
                  __nv_bfloat16* __restrict__ out) {
   constexpr int P = D + 8;  // smem row pitch (conflict-free fragment loads)
+  const int KG = 4 / RG;
   const int seq = blockIdx.x, hk = blockIdx.y, chunk = blockIdx.z;
   const int G = Hq / Hkv;
   const int ql = q_len[seq];
@@ -276,8 +285,7 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
   const int* btg = block_table + (size_t)seq_slot[seq] * max_blocks;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, c = lane & 3;
-  // the sequence's block-table row, staged once (no dependent global load
-  // in front of every tile's cp.async)
+  const int rg = warp % RG, kg = warp / RG;
   __shared__ int bt[ATT_MAX_BLOCKS];
   const int nblk_used = min(last_key / bs + 1, ATT_MAX_BLOCKS);
   for (int i = tid; i < nblk_used; i += ATT_THREADS) bt[i] = btg[i];
@@ -285,10 +293,11 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
   extern __shared__ __align__(16) uint8_t att_smem[];
   typedef __nv_bfloat16 Row[P];
   Row* sQ = reinterpret_cast<Row*>(att_smem);
-  Row (*sK)[KT] = reinterpret_cast<Row(*)[KT]>(att_smem + sizeof(Row) * ATT_MAXR);
-  Row (*sV)[KT] = reinterpret_cast<Row(*)[KT]>(att_smem + sizeof(Row) * (ATT_MAXR + NS * KT));
+  Row* ring = reinterpret_cast<Row*>(att_smem + sizeof(Row) * ATT_MAXR);
+  // stage s, key group j: K rows at ring[((s*KG + j)*2) * KT], V rows right after
+  auto sK = [&](int st, int j) { return ring + ((st * KG + j) * 2) * KT; };
+  auto sV = [&](int st, int j) { return ring + ((st * KG + j) * 2 + 1) * KT; };
 
-  // Q rows (zero rows past R)
   for (int idx = tid; idx < ATT_MAXR * (D / 8); idx += ATT_THREADS) {
     const int r = idx / (D / 8), cc = idx % (D / 8);
     uint4 v = make_uint4(0, 0, 0, 0);
@@ -299,30 +308,32 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
     }
     *reinterpret_cast<uint4*>(&sQ[r][cc * 8]) = v;
   }
-  auto load_tile = [&](int kt, int buf) {
-    for (int idx = tid; idx < KT * (D / 8); idx += ATT_THREADS) {
-      const int j = idx / (D / 8), cc = idx % (D / 8);
-      const int key = kt * KT + j;
+  const int ntiles = last_key / KT + 1;
+  const int ngroups = (ntiles + KG - 1) / KG;
+  __syncthreads();  // bt staged
+  auto load_group = [&](int gi, int st) {
+    const int per = KT * (D / 8);
+    for (int idx = tid; idx < KG * per; idx += ATT_THREADS) {
+      const int j = idx / per, rem = idx % per;
+      const int r = rem / (D / 8), cc = rem % (D / 8);
+      const int key = (gi * KG + j) * KT + r;
       const bool ok = key <= last_key;
       size_t o = 0;
       if (ok) o = (((size_t)bt[key / bs] * bs + key % bs) * Hkv + hk) * D + cc * 8;
-      cp_async16(&sK[buf][j][cc * 8], kc + o, ok);
-      cp_async16(&sV[buf][j][cc * 8], vc + o, ok);
+      cp_async16(&sK(st, j)[r][cc * 8], kc + o, ok);
+      cp_async16(&sV(st, j)[r][cc * 8], vc + o, ok);
     }
     cp_async_commit();
   };
-  const int ntiles = last_key / KT + 1;
-  __syncthreads();  // bt staged
-  // NS-stage cp.async ring: tiles 0 .. NS-2 in flight before the first use
 #pragma unroll
   for (int t = 0; t < NS - 1; ++t) {
-    if (t < ntiles) load_tile(t, t);
+    if (t < ngroups) load_group(t, t);
     else cp_async_commit();
   }
   __syncthreads();
 
-  const bool active = warp * 16 < R;
-  const int r0 = warp * 16 + g, r1 = r0 + 8;
+  const bool active = kg < KG && rg * 16 < R;
+  const int r0 = rg * 16 + g, r1 = r0 + 8;
   const int lim0 = r0 < R ? min(first_pos + t0 + r0 / G, kvl - 1) : -1;
   const int lim1 = r1 < R ? min(first_pos + t0 + r1 / G, kvl - 1) : -1;
   uint32_t qf[D / 16][4];
@@ -340,14 +351,16 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
   for (int n = 0; n < D / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
 
-  for (int kt = 0; kt < ntiles; ++kt) {
-    const int buf = kt % NS;
-    // keep NS-1 tiles in flight: issue tile kt+NS-1 (or an empty group)
-    if (kt + NS - 1 < ntiles) load_tile(kt + NS - 1, (kt + NS - 1) % NS);
+  for (int gi = 0; gi < ngroups; ++gi) {
+    const int st = gi % NS;
+    if (gi + NS - 1 < ngroups) load_group(gi + NS - 1, (gi + NS - 1) % NS);
     else cp_async_commit();
     cp_async_wait<NS - 1>();
     __syncthreads();
-    if (active) {
+    const int kt = gi * KG + kg;
+    if (active && kt < ntiles) {
+      Row* K = sK(st, kg);
+      Row* V = sV(st, kg);
       float sacc[KT / 8][4];
 #pragma unroll
       for (int n = 0; n < KT / 8; ++n) sacc[n][0] = sacc[n][1] = sacc[n][2] = sacc[n][3] = 0.f;
@@ -355,13 +368,12 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
       for (int kk = 0; kk < D / 16; ++kk) {
 #pragma unroll
         for (int n = 0; n < KT / 8; ++n) {
-          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&sK[buf][n * 8 + g][kk * 16 + 2 * c]);
+          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&K[n * 8 + g][kk * 16 + 2 * c]);
           const uint32_t b1 =
-              *reinterpret_cast<const uint32_t*>(&sK[buf][n * 8 + g][kk * 16 + 8 + 2 * c]);
+              *reinterpret_cast<const uint32_t*>(&K[n * 8 + g][kk * 16 + 8 + 2 * c]);
           mma_bf16_16816(sacc[n], qf[kk], b0, b1);
         }
       }
-      // mask, scale (log2 domain), online softmax
       float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
       for (int n = 0; n < KT / 8; ++n) {
@@ -410,12 +422,11 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
       for (int kk = 0; kk < KT / 16; ++kk) {
 #pragma unroll
         for (int n = 0; n < D / 8; n += 2) {
-          // 4 8x8 matrices: keys kk*16+{0..7, 8..15} x dims n*8.., (n+1)*8..
           uint32_t vb[4];
           const int mat = lane >> 3, rr = lane & 7;
           const int krow = kk * 16 + (mat & 1) * 8 + rr;
           const int dcol = (n + (mat >> 1)) * 8;
-          ldmatrix_x4_trans(vb, &sV[buf][krow][dcol]);
+          ldmatrix_x4_trans(vb, &V[krow][dcol]);
           mma_bf16_16816(o[n], pf[kk], vb[0], vb[1]);
           mma_bf16_16816(o[n + 1], pf[kk], vb[2], vb[3]);
         }
@@ -423,12 +434,69 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
     }
     __syncthreads();
   }
-  if (!active) return;
-  // the 4 threads of a row group hold disjoint key columns: reduce l
+  // the 4 threads of a row quad hold disjoint key columns: reduce l
   l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
   l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  if (KG > 1) {
+    // merge key-group states: warp (rg, kg>0) publishes, warp (rg, 0) merges
+    cp_async_wait<0>();
+    __syncthreads();
+    float* scr = reinterpret_cast<float*>(ring);  // ring is free now
+    const int slot_floats = 16 * D + 32;          // o[16][D], m[16], l[16]
+    if (active && kg > 0) {
+      float* sp = scr + (rg * KG + kg) * slot_floats;
+#pragma unroll
+      for (int n = 0; n < D / 8; ++n) {
+        const int d = n * 8 + 2 * c;
+        sp[g * D + d] = o[n][0];
+        sp[g * D + d + 1] = o[n][1];
+        sp[(g + 8) * D + d] = o[n][2];
+        sp[(g + 8) * D + d + 1] = o[n][3];
+      }
+      if (c == 0) {
+        sp[16 * D + g] = m0;
+        sp[16 * D + g + 8] = m1;
+        sp[16 * D + 16 + g] = l0;
+        sp[16 * D + 16 + g + 8] = l1;
+      }
+    }
+    __syncthreads();
+    if (active && kg == 0) {
+      float M0 = m0, M1 = m1;
+      for (int j = 1; j < KG; ++j) {
+        const float* sp = scr + (rg * KG + j) * slot_floats;
+        M0 = fmaxf(M0, sp[16 * D + g]);
+        M1 = fmaxf(M1, sp[16 * D + g + 8]);
+      }
+      const float w00 = M0 == -INFINITY ? 0.f : exp2f(m0 - M0);
+      const float w10 = M1 == -INFINITY ? 0.f : exp2f(m1 - M1);
+      l0 *= w00;
+      l1 *= w10;
+#pragma unroll
+      for (int n = 0; n < D / 8; ++n) {
+        o[n][0] *= w00; o[n][1] *= w00; o[n][2] *= w10; o[n][3] *= w10;
+      }
+      for (int j = 1; j < KG; ++j) {
+        const float* sp = scr + (rg * KG + j) * slot_floats;
+        const float mj0 = sp[16 * D + g], mj1 = sp[16 * D + g + 8];
+        const float wj0 = mj0 == -INFINITY ? 0.f : exp2f(mj0 - M0);
+        const float wj1 = mj1 == -INFINITY ? 0.f : exp2f(mj1 - M1);
+        l0 += sp[16 * D + 16 + g] * wj0;
+        l1 += sp[16 * D + 16 + g + 8] * wj1;
+#pragma unroll
+        for (int n = 0; n < D / 8; ++n) {
+          const int d = n * 8 + 2 * c;
+          o[n][0] += sp[g * D + d] * wj0;
+          o[n][1] += sp[g * D + d + 1] * wj0;
+          o[n][2] += sp[(g + 8) * D + d] * wj1;
+          o[n][3] += sp[(g + 8) * D + d + 1] * wj1;
+        }
+      }
+    }
+  }
+  if (!active || kg != 0) return;
   const float inv0 = l0 > 0.f ? 1.f / l0 : 0.f, inv1 = l1 > 0.f ? 1.f / l1 : 0.f;
 #pragma unroll
   for (int n = 0; n < D / 8; ++n) {
@@ -665,26 +733,27 @@ int psd_attention(const void* q, const void* k_cache, const void* v_cache,
   if (G > ATT_MAXR || max_blocks > ATT_MAX_BLOCKS) return (int)cudaErrorInvalidValue;
   const int tpc = ATT_MAXR / G;
   const int chunks = (max_q_len + tpc - 1) / tpc;
+  // rows per CTA -> row groups; the other warps become key groups
+  const int rmax = std::min(ATT_MAXR, std::min(max_q_len, tpc) * G);
+  int RG = (rmax + 15) / 16;
+  if (RG == 3) RG = 4;  // 4 / RG must be an integer number of key groups
+  const int KG = 4 / RG;
   dim3 grid(num_seqs, Hkv, chunks);
   const float sl2 = scale * 1.44269504088896341f;
-  static bool attr_done[3] = {false, false, false};
-  auto args = [&](auto kern, int kt, int d) {
-    const int smem = (ATT_MAXR + 2 * ATT_STAGES * kt) * (d + 8) * 2;
-    const int slot = d == 32 ? 0 : d == 64 ? 1 : 2;
-    if (!attr_done[slot]) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      attr_done[slot] = true;
-    }
+  auto go = [&](auto kern, int kt, int d) {
+    const int smem = (ATT_MAXR + 2 * ATT_STAGES * KG * kt) * (d + 8) * 2;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     psd::count_launches();
     kern<<<grid, ATT_THREADS, smem, (cudaStream_t)stream>>>(
         static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k_cache),
         static_cast<const __nv_bfloat16*>(v_cache), block_table, max_blocks, seq_slot, q_start,
-        q_len, q_pos0, kv_len, Hq, Hkv, block_size, sl2, tpc, static_cast<__nv_bfloat16*>(out));
+        q_len, q_pos0, kv_len, Hq, Hkv, block_size, sl2, tpc, RG,
+        static_cast<__nv_bfloat16*>(out));
   };
   switch (D) {
-    case 32: args(attention_kernel<32, 64, ATT_STAGES>, 64, 32); break;
-    case 64: args(attention_kernel<64, 64, ATT_STAGES>, 64, 64); break;
-    case 128: args(attention_kernel<128, 32, ATT_STAGES>, 32, 128); break;
+    case 32: go(attention_kernel<32, 64, ATT_STAGES>, 64, 32); break;
+    case 64: go(attention_kernel<64, 32, ATT_STAGES>, 32, 64); break;
+    case 128: go(attention_kernel<128, 32, ATT_STAGES>, 32, 128); break;
     default: return (int)cudaErrorInvalidValue;
   }
   return (int)cudaGetLastError();
