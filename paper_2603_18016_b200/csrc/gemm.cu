@@ -41,6 +41,14 @@ constexpr int kThreads = 192;
 constexpr int kMaxTiles = 1 << 16;  // stream-K tickets reserved at the workspace head
 // weight k-blocks prefetched into L2 ahead of the smem ring; 0 = off.
 // PSD_GEMM_PREFETCH overrides (tuning experiments)
+int silu_mode() {
+  static int v = [] {
+    const char* e = getenv("PSD_SILU_MODE");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 int prefetch_depth() {
   static int v = [] {
     const char* e = getenv("PSD_GEMM_PREFETCH");
@@ -223,6 +231,7 @@ struct SKArgs {
   float* part;    // [G][2][BN * 128]
   int* tickets;   // [tiles], zero between launches
   const __nv_bfloat16* Wt;  // pre-tiled weights (TILED variant)
+  int silu_mode;            // tuning experiment: 0 silu(g)*u, 1 g*u, 2 g only
 };
 
 struct Seg {
@@ -420,9 +429,16 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
             const int jo = (n0 / BM) * 64 + 16 * q + (lane & 15);
             __nv_bfloat16* Y = static_cast<__nv_bfloat16*>(g.Y);
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
-              const float up = __shfl_down_sync(0xffffffffu, v[k], 16);
-              v[k] = silu(v[k]) * up;  // all lanes: no divergence in the math
+            if (g.silu_mode == 2) {
+            } else if (g.silu_mode == 1) {
+#pragma unroll
+              for (int k = 0; k < 16; ++k) v[k] *= __shfl_down_sync(0xffffffffu, v[k], 16);
+            } else {
+#pragma unroll
+              for (int k = 0; k < 16; ++k) {
+                const float up = __shfl_down_sync(0xffffffffu, v[k], 16);
+                v[k] = silu(v[k]) * up;  // all lanes: no divergence in the math
+              }
             }
             if (lane < 16) {
 #pragma unroll
@@ -733,6 +749,7 @@ int psd_gemm_tiled(const void* X, int ldx, int M, int K, const void* W_tiled, in
   g.tickets = static_cast<int*>(workspace);
   g.part = reinterpret_cast<float*>(static_cast<char*>(workspace) + p.ticket_bytes);
   g.Wt = static_cast<const __nv_bfloat16*>(W_tiled);
+  g.silu_mode = silu_mode();
   cudaStream_t st = (cudaStream_t)stream;
   switch (epi) {
     case PSD_EPI_BF16: return launch_sk<PSD_EPI_BF16, true>(p.bn, mx, mx, g, st);
@@ -797,6 +814,7 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
     g.tickets = static_cast<int*>(workspace);
     g.part = reinterpret_cast<float*>(static_cast<char*>(workspace) + p.ticket_bytes);
     g.Wt = nullptr;
+    g.silu_mode = silu_mode();
     cudaStream_t st = (cudaStream_t)stream;
     switch (epi) {
       case PSD_EPI_BF16: return launch_sk<PSD_EPI_BF16>(p.bn, mw, mx, g, st);

@@ -144,3 +144,33 @@ def test_sampling_psd_k1_bit_exact_on_real_logits(cuda_device, temperature):
         np.testing.assert_array_equal(acc, rec["acc"])
         np.testing.assert_array_equal(out, rec["out"])
     assert 0 < rep.total_accepted < rep.total_drafted
+
+
+def test_continuous_batching_preemption_and_k_overrides_on_gpu(cuda_device):
+    """SURVEY §8(f) ranks 1-2 on the GPU path: poisson arrivals (admission while
+    other requests decode), preemption of decoding requests, per-request draft
+    depth; greedy tokens still equal the CPU oracle's for every request."""
+    from paper_2603_18016_b200 import (LengthSpec, Preemption, WorkloadSpec, generate_requests)
+
+    spec = WorkloadSpec(arrival="poisson", rate=0.02, count=12,
+                        prompt_len=LengthSpec("uniform", lo=4, hi=20),
+                        output_len=LengthSpec("uniform", lo=8, hi=40))
+    cfg = SimConfig(mode="psd", m=4, k=4, k_overrides=(1, 2, 3, 4, 4, 3, 2, 1))
+    pre = [Preemption(0, 0.0)]  # request 0 arrives first: evicted at its first sync point
+
+    def go(backend):
+        reqs = generate_requests(spec, 11)
+        return run(cfg, reqs, pre, backend=backend)
+
+    gb = GpuBackend("tiny-target", "tiny-draft", max_requests=16, max_batch=8, k_max=4,
+                    max_seq_len=128, seed=0, beta_target=3.0, beta_draft=12.0,
+                    prefill_chunk_tokens=512)
+    gs, grep = go(gb)
+    cs, crep = go(CpuBackend("tiny-target", "tiny-draft", seed=0, beta_target=3.0,
+                             beta_draft=12.0))
+    assert grep.preempted == crep.preempted == 1
+    assert grep.finished == crep.finished == 11
+    for a, b in zip(gs.request_list(), cs.request_list()):
+        assert a.state == b.state
+        if a.state.value == "finished":  # greedy output is schedule independent
+            assert a.output_ids == b.output_ids and len(a.output_ids) == a.target_output_len
