@@ -264,10 +264,26 @@ def run_ours(args) -> None:
     from paper_2603_18016_b200.gpu import GpuBackend
 
     hbm_peak, bf16_peak, peak_kind = _peaks()
+    pairs = args.layout == "pairs"
+    if pairs and world % 2:
+        raise SystemExit("--layout pairs needs an even number of GPUs")
+    # replicas: every rank = target + draft on one GPU (two streams)
+    # pairs: even rank = target GPU (scheduler), odd rank = dedicated draft GPU
+    roles = ("target", "draft") if not pairs else (("target",) if rank % 2 == 0 else ("draft",))
+    replica = rank // 2 if pairs else rank
     be = GpuBackend(CFG["target"], CFG["draft"], max_requests=CFG["n_requests"],
                     max_batch=CFG["n_requests"], k_max=CFG["k"],
-                    max_seq_len=CFG["prompt"] + CFG["output"] + 16, seed=rank,
-                    beta_target=BETA_TARGET, beta_draft=BETA_DRAFT, device=dev)
+                    max_seq_len=CFG["prompt"] + CFG["output"] + 16, seed=replica,
+                    beta_target=BETA_TARGET, beta_draft=BETA_DRAFT, device=dev, roles=roles)
+    is_draft_rank = pairs and rank % 2 == 1
+    backend = be
+    if pairs:
+        from paper_2603_18016_b200.pair import (DraftServer, GpuDraftEngine, GpuTargetEngine,
+                                                PairLink, PairTarget)
+        peer = rank + 1 if rank % 2 == 0 else rank - 1
+        link = PairLink(peer, dev)
+        if not is_draft_rank:
+            backend = PairTarget(GpuTargetEngine(be), link)
 
     def barrier():
         torch.cuda.synchronize()
@@ -277,38 +293,57 @@ def run_ours(args) -> None:
     launches = {}
 
     def one(mode):
-        return run(_config(mode), _workload(rank), backend=be)
+        return run(_config(mode), _workload(rank), backend=backend)
 
     results = {}
     for mode in ("psd", "standard-sd", "sd-m"):
+        if is_draft_rank:
+            # serve warm-up + timed passes of this mode, then join the timing reduction
+            DraftServer(GpuDraftEngine(be), link).serve()
+            barrier()
+            DraftServer(GpuDraftEngine(be), link).serve()
+            barrier()
+            pd.aggregate(0, 0.0, dev)
+            results[mode] = None
+            continue
         for _ in range(args.warmup):
             one(mode)
+        if pairs:
+            backend.stop()
         barrier()
         clocks = Clocks(local) if mode == "psd" else None
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
         reps = []
-        stats0 = dict(be.stats)
+        stats0 = dict(backend.stats)
         l0 = be.launches
         for _ in range(args.steps):
             reps.append(one(mode)[1])
         e1.record()
+        if pairs:
+            backend.stop()
         barrier()
         launches[mode] = be.launches - l0
         ms_local = e0.elapsed_time(e1)
         tokens, ms = pd.aggregate(sum(r.total_generated for r in reps), ms_local, dev)
         results[mode] = {"ms": ms, "tokens": tokens, "reps": reps,
                          "clocks": clocks.stop() if clocks else None,
-                         "draft_ms": be.stats["draft_ms"] - stats0["draft_ms"],
-                         "verify_ms": be.stats["verify_ms"] - stats0["verify_ms"],
-                         "steps": be.stats["steps"] - stats0["steps"]}
+                         "draft_ms": backend.stats["draft_ms"] - stats0["draft_ms"],
+                         "verify_ms": backend.stats["verify_ms"] - stats0["verify_ms"],
+                         "steps": backend.stats["steps"] - stats0["steps"]}
     # end to end through the public API with host prompts / host outputs
     barrier()
+    if is_draft_rank:
+        DraftServer(GpuDraftEngine(be), link).serve()
+        pd.finalize()
+        return
     t0 = time.perf_counter()
     st, rep_e2e = one("psd")
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
+    if pairs:
+        backend.stop()
     roof, vk = kernel_rooflines(be, hbm_peak)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -339,8 +374,9 @@ def run_ours(args) -> None:
         "config": {"workload": "cfg2: Llama-3.1-8B target / Llama-3.2-1B draft shapes, "
                                "random-init bf16, 2x32 requests, k=5, prompt 128, output 256, "
                                "greedy, 1 GPU per replica (draft / verify on separate streams)",
-                   "global_batch": world * CFG["n_requests"], "seq_len": CFG["prompt"] +
-                   CFG["output"], "parallelism": f"replicas{world}",
+                   "global_batch": (world // 2 if pairs else world) * CFG["n_requests"],
+                   "seq_len": CFG["prompt"] + CFG["output"],
+                   "parallelism": f"pairs{world // 2}" if pairs else f"replicas{world}",
                    "l2": "inputs > L2 (weights 18.5 GB streamed per step)",
                    "synthetic_language_beta": [BETA_TARGET, BETA_DRAFT]},
         "sd": {"value": round(sd_value, 1), "unit": "tok/s",
@@ -377,6 +413,9 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--layout", default="replicas", choices=["replicas", "pairs"],
+                    help="replicas: each GPU runs target+draft (two streams); pairs: "
+                         "dedicated draft GPU per target GPU (NCCL hand-off, pair.py)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

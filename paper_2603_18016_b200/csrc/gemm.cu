@@ -79,7 +79,17 @@ struct Cfg {
   static constexpr int SMEM = 1024 + STAGES * STAGE + 256 + XCHG_BYTES;
 };
 
-__device__ __forceinline__ float silu(float x) { return x * __frcp_rn(1.0f + __expf(-x)); }
+// silu(x) = x * sigmoid(x) = 0.5 x (1 + tanh(x / 2)): one MUFU.TANH per element
+// (an IEEE reciprocal here measured +27 us on the 8B gate/up GEMM epilogue)
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float silu(float x) {
+  const float h = 0.5f * x;
+  return fmaf(h, tanh_approx(h), h);
+}
 
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)

@@ -58,7 +58,8 @@ class GpuBackend:
                  beta_target: float = 6.0, beta_draft: float = 12.0,
                  device: str | torch.device = "cuda:0", dual_stream: bool = True,
                  block_size: int = 16, num_blocks: int | None = None,
-                 prefill_chunk_tokens: int = 4096, use_graphs: bool = True) -> None:
+                 prefill_chunk_tokens: int = 4096, use_graphs: bool = True,
+                 roles: tuple = ("target", "draft")) -> None:
         if not torch.cuda.is_available():
             raise native.NativeError("GpuBackend needs a CUDA device (no CPU fallback)")
         native.load()
@@ -86,11 +87,13 @@ class GpuBackend:
         self.prefill_chunk = prefill_chunk_tokens
         self.beta_target, self.beta_draft = beta_target, beta_draft
         dev = self.device
+        self.roles = set(roles)
+        has_t, has_d = "target" in self.roles, "draft" in self.roles
         with torch.cuda.device(dev):
             self.target = Transformer(self.tshape, dev, seed * 2 + 1, num_blocks, block_size,
-                                      self.max_blocks)
+                                      self.max_blocks) if has_t else None
             self.draft = Transformer(self.dshape, dev, seed * 2 + 2, num_blocks, block_size,
-                                     self.max_blocks)
+                                     self.max_blocks) if has_d else None
             i32 = torch.int32
             # one extra scratch slot (index max_requests) backs the padding
             # rows of bucketed batches; its block-table row is block 0
@@ -112,13 +115,17 @@ class GpuBackend:
             B, K = max_batch, k_max
             vt_tokens = max(B * (K + 1), prefill_chunk_tokens)
             vd_tokens = max(2 * B, prefill_chunk_tokens)
-            self.tfwd = Forward(self.target, vt_tokens, max(B, 256), B * (K + 1), self.block_table,
-                                sets=1)
+            self.tfwd = Forward(self.target, vt_tokens, max(B, 256), B * (K + 1),
+                                self.block_table, sets=1) if has_t else None
             self.dfwd = Forward(self.draft, vd_tokens, max(B, 256), B, self.block_table,
-                                sets=K + 1)
+                                sets=K + 1) if has_d else None
             self.tlogits = torch.empty(B * (K + 1), self.tshape.vocab, dtype=torch.float32,
-                                       device=dev)
-            self.dlogits = torch.empty(B, self.dshape.vocab, dtype=torch.float32, device=dev)
+                                       device=dev) if has_t else None
+            self.dlogits = torch.empty(B, self.dshape.vocab, dtype=torch.float32,
+                                       device=dev) if has_d else None
+            if mode == "sample" and not (has_t and has_d):
+                raise ConfigError("sampling mode with a dedicated draft GPU is not supported yet "
+                                  "(the verifier needs the draft distributions q)")
             if mode == "sample":
                 # per-slot draft distributions q (fp32 logits after the bias);
                 # K1 reads request b's rows at qbuf[slot_b] (verify_sample_rows)
@@ -140,6 +147,7 @@ class GpuBackend:
             self.v_meta_host = torch.zeros(3 * B + B * K, dtype=i32).pin_memory()
             self.v_meta = torch.zeros(3 * B + B * K, dtype=i32, device=dev)
             self.acc_host = torch.zeros(B, dtype=i32).pin_memory()
+            self.out_host = torch.zeros(B * (K + 1), dtype=i32).pin_memory()
             self.d_out = torch.empty(B, 1, dtype=i32, device=dev)
             self.d_acc = torch.empty(B, dtype=i32, device=dev)
             self.d_len0 = torch.zeros(B, dtype=i32, device=dev)
@@ -227,51 +235,79 @@ class GpuBackend:
 
     def _admit(self, state, ids) -> None:
         """Assign slots and initialise slot tokens for new requests."""
-        n = len(ids)
-        idx = np.empty(3 * n, dtype=np.int32)
-        val = np.empty(3 * n, dtype=np.int32)
-        for i, rid in enumerate(ids):
+        triples = []
+        for rid in ids:
             if not self.free_slots:
                 raise ProtocolError("GpuBackend: out of request slots")
             s = self.free_slots.pop()
             self.slots[rid] = s
             p = state.requests[rid].prompt_ids
-            idx[3 * i:3 * i + 3] = (s * self.ldt, s * self.ldt + 1, -1)
-            val[3 * i:3 * i + 3] = (p[-2], p[-1], 0)
+            triples.append((s, p[-2], p[-1]))
+        self._init_slots(triples, reset_generated=True)
+
+    def _init_slots(self, triples, reset_generated: bool = False) -> None:
+        """slot_tok[s, 0:2] = (tok_prev, tok_last) for (s, tok_prev, tok_last)."""
+        n = len(triples)
+        if n == 0:
+            return
+        idx = np.empty(2 * n, dtype=np.int32)
+        val = np.empty(2 * n, dtype=np.int32)
+        for i, (s, tp, tl) in enumerate(triples):
+            idx[2 * i:2 * i + 2] = (s * self.ldt, s * self.ldt + 1)
+            val[2 * i:2 * i + 2] = (tp, tl)
         dev = self.device
         stage = torch.from_numpy(np.concatenate([idx, val])).pin_memory().to(dev,
                                                                             non_blocking=True)
         st = torch.cuda.current_stream(dev).cuda_stream
         lib = native.load()
         native.check(lib.psd_index_copy_i32(self.slot_tok.data_ptr(), stage.data_ptr(),
-                                            stage[3 * n:].data_ptr(), None, 3 * n, st),
+                                            stage[2 * n:].data_ptr(), None, 2 * n, st),
                      "slot init")
-        sl = torch.tensor([self.slots[r] for r in ids], dtype=torch.int64)
-        self.generated[sl.to(dev)] = 0
+        self.launches += 1
+        if reset_generated:
+            sl = torch.tensor([t[0] for t in triples], dtype=torch.int64)
+            self.generated[sl.to(dev)] = 0
+
+    def _set_slot_values(self, pairs) -> None:
+        """slot_tok.view(-1)[flat] = value for (flat, value) pairs (draft ids
+        arriving from a dedicated draft GPU)."""
+        n = len(pairs)
+        if n == 0:
+            return
+        arr = np.asarray(pairs, dtype=np.int32).T.reshape(-1)
+        stage = torch.from_numpy(arr).pin_memory().to(self.device, non_blocking=True)
+        st = torch.cuda.current_stream(self.device).cuda_stream
+        native.check(native.load().psd_index_copy_i32(
+            self.slot_tok.data_ptr(), stage.data_ptr(), stage[n:].data_ptr(), None, n, st),
+            "slot values")
+        self.launches += 1
 
     def _prefill(self, state, ids, fwd: Forward, logits_model: str) -> None:
-        """Prompt tokens 0..p-2 of each new request through one model."""
+        self._prefill_rows([(self.slots[rid], state.requests[rid].prompt_ids) for rid in ids],
+                           fwd)
+
+    def _prefill_rows(self, rows, fwd: Forward) -> None:
+        """Prompt tokens 0..p-2 of each (slot, prompt_ids) through one model."""
         chunks, cur, cur_tok = [], [], 0
-        for rid in ids:
-            n = state.requests[rid].prompt_len - 1
+        for row in rows:
+            n = len(row[1]) - 1
             if cur and cur_tok + n > self.prefill_chunk:
                 chunks.append(cur)
                 cur, cur_tok = [], 0
-            cur.append(rid)
+            cur.append(row)
             cur_tok += n
         if cur:
             chunks.append(cur)
         for chunk in chunks:
             toks, pos, slots = [], [], []
             seq_slot, q_start, q_len, q_pos0, kv_len = [], [], [], [], []
-            for rid in chunk:
-                req = state.requests[rid]
-                n = req.prompt_len - 1
+            for slot, prompt in chunk:
+                n = len(prompt) - 1
                 q_start.append(len(toks))
-                toks.extend(req.prompt_ids[:n])
+                toks.extend(prompt[:n])
                 pos.extend(range(n))
-                slots.extend(self._slots_at(np.full(n, self.slots[rid]), np.arange(n)).tolist())
-                seq_slot.append(self.slots[rid])
+                slots.extend(self._slots_at(np.full(n, slot), np.arange(n)).tolist())
+                seq_slot.append(slot)
                 q_len.append(n)
                 q_pos0.append(0)
                 kv_len.append(n)
@@ -330,19 +366,26 @@ class GpuBackend:
 
     def _draft_loop(self, state, ids, quotas) -> None:
         """k-step draft decode for the rows in ``ids`` (k_i = quotas[rid])."""
-        rows = [rid for rid in ids if quotas[rid] > 0]
         for rid in ids:
             self.pending_k[rid] = quotas[rid]
-        if not rows:
+        self._draft_rows([(rid, self.slots[rid],
+                           state.requests[rid].prompt_len + state.requests[rid].generated,
+                           quotas[rid]) for rid in ids if quotas[rid] > 0])
+
+    def _draft_rows(self, draft_rows) -> None:
+        """k-step draft decode of (rid, slot, committed length L, k) rows; the
+        drafts land in slot_tok[slot, 2..2+k)."""
+        if not draft_rows:
             return
+        rows = [r[0] for r in draft_rows]
         n = len(rows)
         nb = self._bucket(n)
         sl = np.full(nb, self.scratch_slot, np.int32)
         L = np.full(nb, 2, np.int64)
         k = np.zeros(nb, np.int64)
-        sl[:n] = [self.slots[r] for r in rows]
-        L[:n] = [state.requests[r].prompt_len + state.requests[r].generated for r in rows]
-        k[:n] = [quotas[r] for r in rows]
+        sl[:n] = [r[1] for r in draft_rows]
+        L[:n] = [r[2] for r in draft_rows]
+        k[:n] = [r[3] for r in draft_rows]
         kmax = int(k.max())
         ldt = self.ldt
         real = np.arange(nb) < n
@@ -541,6 +584,7 @@ class GpuBackend:
                                     self.slot_tok.data_ptr(), self.ldt, self.outputs.data_ptr(),
                                     self.max_out, st), "commit")
         self.acc_host[:nb].copy_(self.v_acc[:nb], non_blocking=True)
+        self.out_host[:nb * K1].copy_(self.v_out[:nb * K1], non_blocking=True)
 
     # ------------------------------------------------------------------
     def execute(self, state: EngineState, plan: StepPlan, rows: list[VerifyRow]) -> StepResult:

@@ -1,0 +1,354 @@
+"""PSD with a dedicated draft GPU: target rank + draft rank over torch.distributed.
+
+The paper's deployment: the drafter runs on its own
+GPU, the verifier on another; drafts cross to the verifier and sampler
+outputs flow back, "one exchange step per PSD step".  The
+reference only charges this hand-off as ``comm_overhead`` (engine.py:439, 442).
+
+Rank ``t`` (even) runs the scheduler and the target model; rank ``t+1`` runs
+the draft model and serves commands.  Per PSD step, one message goes
+target -> draft (new admissions with prompts, KV block tables, the tokens
+committed by the previous verification, the rows to draft serially / overlapped)
+and one or two replies come back (draft ids).  The overlapped batch is
+drafted on the draft GPU *while* the target GPU verifies the other batch --
+the overlap the reference only models as max(verify, draft).
+
+The protocol is engine-agnostic: ``GpuTargetEngine`` / ``GpuDraftEngine``
+wrap :class:`~.gpu.GpuBackend` (roles "target" / "draft"); the CPU tests
+(tests/test_pair_gloo.py) plug the numpy oracle engines into the same classes
+over gloo.  Transport = ``dist.send``/``recv`` of small int32 tensors (NCCL:
+on-device; gloo: host).
+"""
+
+from __future__ import annotations
+
+import time
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .scheduler import EngineState, StepPlan, StepResult, VerifyRow
+from .workload import attach_prompt_ids
+
+__all__ = ["PairLink", "PairTarget", "DraftServer", "GpuTargetEngine", "GpuDraftEngine"]
+
+MAGIC = 0x50534450  # "PSDP"
+K_STEP, K_STOP = 0, 1
+
+
+class PairLink:
+    """Length-prefixed int32 messages to / from one peer rank."""
+
+    def __init__(self, peer: int, device=None) -> None:
+        self.peer = peer
+        self.device = device  # CUDA device for NCCL, None for gloo
+        self.bytes_sent = 0
+        self.bytes_recv = 0
+
+    def _t(self, arr: np.ndarray) -> torch.Tensor:
+        t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.int32))
+        return t.to(self.device) if self.device is not None else t
+
+    def send(self, arr: np.ndarray) -> None:
+        arr = np.asarray(arr, dtype=np.int32)
+        dist.send(self._t(np.asarray([arr.size], np.int32)), self.peer)
+        if arr.size:
+            dist.send(self._t(arr), self.peer)
+        self.bytes_sent += 4 * (arr.size + 1)
+
+    def recv(self) -> np.ndarray:
+        hdr = self._t(np.zeros(1, np.int32))
+        dist.recv(hdr, self.peer)
+        n = int(hdr.cpu()[0])
+        if n == 0:
+            return np.zeros(0, np.int32)
+        buf = self._t(np.zeros(n, np.int32))
+        dist.recv(buf, self.peer)
+        self.bytes_recv += 4 * (n + 1)
+        return buf.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# message codec
+# ---------------------------------------------------------------------------
+def encode_step(admit, commits, serial, overlap, table) -> np.ndarray:
+    """admit: [(rid, slot, prompt)]; commits: [(rid, slot, tokens)];
+    serial / overlap: [(rid, slot, L, k)]; table: int32 [slots, max_blocks]."""
+    out = [MAGIC, K_STEP, len(admit), len(commits), len(serial), len(overlap),
+           table.shape[0], table.shape[1]]
+    for rid, slot, prompt in admit:
+        out += [rid, slot, len(prompt)] + list(prompt)
+    for rid, slot, toks in commits:
+        out += [rid, slot, len(toks)] + list(toks)
+    for rows in (serial, overlap):
+        for r in rows:
+            out += list(r)
+    return np.concatenate([np.asarray(out, np.int32), table.reshape(-1).astype(np.int32)])
+
+
+def decode_step(msg: np.ndarray) -> dict:
+    if msg[0] != MAGIC:
+        raise RuntimeError("PSD pair protocol: bad message")
+    kind = int(msg[1])
+    if kind == K_STOP:
+        return {"stop": True}
+    na, nc, ns, no, tr, tc = (int(x) for x in msg[2:8])
+    i = 8
+    admit, commits = [], []
+    for _ in range(na):
+        rid, slot, n = (int(x) for x in msg[i:i + 3])
+        admit.append((rid, slot, msg[i + 3:i + 3 + n].tolist()))
+        i += 3 + n
+    for _ in range(nc):
+        rid, slot, n = (int(x) for x in msg[i:i + 3])
+        commits.append((rid, slot, msg[i + 3:i + 3 + n].tolist()))
+        i += 3 + n
+    serial = [tuple(int(x) for x in msg[i + 4 * j:i + 4 * j + 4]) for j in range(ns)]
+    i += 4 * ns
+    overlap = [tuple(int(x) for x in msg[i + 4 * j:i + 4 * j + 4]) for j in range(no)]
+    i += 4 * no
+    table = msg[i:i + tr * tc].reshape(tr, tc)
+    return {"stop": False, "admit": admit, "commits": commits, "serial": serial,
+            "overlap": overlap, "table": table}
+
+
+def encode_drafts(rows, drafts: dict, ms: float) -> np.ndarray:
+    out = [MAGIC, len(rows), int(ms * 1000)]
+    for r in rows:
+        d = drafts[r[0]]
+        out += [r[0], len(d)] + list(d)
+    return np.asarray(out, np.int32)
+
+
+def decode_drafts(msg: np.ndarray) -> tuple[dict, float]:
+    if msg[0] != MAGIC:
+        raise RuntimeError("PSD pair protocol: bad draft reply")
+    n, ms = int(msg[1]), msg[2] / 1000.0
+    i = 3
+    out = {}
+    for _ in range(n):
+        rid, k = int(msg[i]), int(msg[i + 1])
+        out[rid] = msg[i + 2:i + 2 + k].tolist()
+        i += 2 + k
+    return out, ms
+
+
+# ---------------------------------------------------------------------------
+# protocol roles
+# ---------------------------------------------------------------------------
+class PairTarget:
+    """Scheduler backend on the target rank (Backend protocol)."""
+
+    def __init__(self, engine, link: PairLink) -> None:
+        self.engine = engine
+        self.link = link
+        self.block_pool = getattr(engine, "block_pool", None)
+        self.pending_commits: list = []
+        self.stats = {"draft_ms": 0.0, "verify_ms": 0.0, "prefill_ms": 0.0, "steps": 0,
+                      "wait_ms": 0.0}
+
+    def bind(self, state: EngineState) -> None:
+        self.engine.bind(state)
+
+    def estimate(self, state, plan):
+        return 0.0, 0.0, 0.0
+
+    def planned_commit(self, state, rid, k_i, draft_time):
+        return min(k_i + 1, state.requests[rid].remaining)
+
+    def commit(self, state, rid, tokens):
+        state.kv.trim_to_written(rid)
+
+    def retire(self, state, rid):
+        self.engine.retire(state, rid)
+
+    def execute(self, state: EngineState, plan: StepPlan, rows: list[VerifyRow]) -> StepResult:
+        eng = self.engine
+        t0 = time.perf_counter()
+        admit = eng.admit(state, plan.prefill_ids)
+        table = eng.tables(state)
+
+        def draft_rows(ids):
+            out = []
+            for rid in ids:
+                k = plan.quotas[rid]
+                eng.expect_drafts(rid, k)
+                if k > 0:
+                    req = state.requests[rid]
+                    out.append((rid, eng.slot_of(rid), req.prompt_len + req.generated, k))
+            return out
+
+        serial = draft_rows(plan.serial_draft_ids)
+        overlap = draft_rows(plan.overlap_draft_ids)
+        self.link.send(encode_step(admit, self.pending_commits, serial, overlap, table))
+        self.pending_commits = []
+        eng.prefill(state, plan.prefill_ids)
+        t1 = time.perf_counter()
+        serial_ms = 0.0
+        if serial:
+            drafts, serial_ms = decode_drafts(self.link.recv())
+            eng.inject(drafts)
+        t2 = time.perf_counter()
+        accepted, committed, verify_ms = eng.verify(state, rows) if rows else ({}, {}, 0.0)
+        t3 = time.perf_counter()
+        overlap_ms = 0.0
+        if overlap:
+            drafts, overlap_ms = decode_drafts(self.link.recv())
+            eng.inject(drafts)
+        t4 = time.perf_counter()
+        for rid, toks in committed.items():
+            self.pending_commits.append((rid, eng.slot_of(rid), toks))
+        ms = lambda a, b: (b - a) * 1e3  # noqa: E731
+        self.stats["steps"] += 1
+        self.stats["draft_ms"] += serial_ms + overlap_ms
+        self.stats["verify_ms"] += verify_ms
+        self.stats["prefill_ms"] += ms(t0, t1)
+        self.stats["wait_ms"] += ms(t1, t2) + ms(t3, t4)
+        return StepResult(ms(t0, t1), serial_ms, overlap_ms, verify_ms, ms(t0, t4), accepted)
+
+    def stop(self) -> None:
+        self.link.send(np.asarray([MAGIC, K_STOP], np.int32))
+
+
+class DraftServer:
+    """Command loop on the draft rank."""
+
+    def __init__(self, engine, link: PairLink) -> None:
+        self.engine = engine
+        self.link = link
+        self.steps = 0
+
+    def serve(self) -> int:
+        eng = self.engine
+        while True:
+            cmd = decode_step(self.link.recv())
+            if cmd["stop"]:
+                return self.steps
+            eng.set_tables(cmd["table"])
+            eng.commit(cmd["commits"])  # before admissions: a freed slot may be reused
+            eng.admit(cmd["admit"])
+            eng.prefill(cmd["admit"])
+            for rows in (cmd["serial"], cmd["overlap"]):
+                if rows:
+                    t0 = time.perf_counter()
+                    drafts = eng.draft(rows)
+                    self.link.send(encode_drafts(rows, drafts, (time.perf_counter() - t0) * 1e3))
+            self.steps += 1
+
+
+# ---------------------------------------------------------------------------
+# GPU engines (GpuBackend with one role each)
+# ---------------------------------------------------------------------------
+class GpuTargetEngine:
+    """Target half of :class:`~.gpu.GpuBackend` behind the pair protocol."""
+
+    def __init__(self, backend) -> None:
+        self.be = backend
+        self.block_pool = backend.block_pool
+        self.last2: dict[int, tuple[int, int]] = {}
+
+    def bind(self, state):
+        self.be.bind(state)
+
+    def slot_of(self, rid):
+        return self.be.slots[rid]
+
+    def admit(self, state, ids):
+        be = self.be
+        with torch.cuda.stream(be.s_target):
+            be._admit(state, ids)
+        out = []
+        for rid in ids:
+            p = state.requests[rid].prompt_ids
+            self.last2[rid] = (p[-2], p[-1])
+            out.append((rid, be.slots[rid], list(p)))
+        return out
+
+    def tables(self, state):
+        be = self.be
+        with torch.cuda.stream(be.s_target):
+            be._upload_block_table(state)
+        return be.bt_np.copy()
+
+    def expect_drafts(self, rid, k):
+        self.be.pending_k[rid] = k
+
+    def prefill(self, state, ids):
+        be = self.be
+        if ids:
+            with torch.cuda.stream(be.s_target):
+                be._prefill(state, ids, be.tfwd, "target")
+
+    def inject(self, drafts: dict):
+        be = self.be
+        pairs = []
+        for rid, ids in drafts.items():
+            s = be.slots[rid]
+            pairs += [(s * be.ldt + 2 + i, t) for i, t in enumerate(ids)]
+        with torch.cuda.stream(be.s_target):
+            be._set_slot_values(pairs)
+
+    def verify(self, state, rows):
+        be = self.be
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(be.s_target):
+            ev0.record()
+            n = be._verify(state, rows)
+            ev1.record()
+        ev1.synchronize()
+        acc = be.acc_host.numpy()[:n]
+        out = be.out_host.numpy()
+        K1 = max((r.k for r in rows), default=0) + 1
+        accepted, committed = {}, {}
+        for r, row in enumerate(rows):
+            a = int(acc[r])
+            toks = out[r * K1:r * K1 + a + 1].tolist()
+            committed[row.request_id] = toks
+            if row.k > 0:
+                accepted[row.request_id] = a
+            be.pending_k.pop(row.request_id, None)
+        return accepted, committed, ev0.elapsed_time(ev1)
+
+    def retire(self, state, rid):
+        self.be.retire(state, rid)
+        self.last2.pop(rid, None)
+
+
+class GpuDraftEngine:
+    """Draft half of :class:`~.gpu.GpuBackend` behind the pair protocol."""
+
+    def __init__(self, backend) -> None:
+        self.be = backend
+        self.last2: dict[int, tuple[int, int]] = {}
+
+    def set_tables(self, table):
+        be = self.be
+        be.bt_np[:] = table
+        be.nblk[:] = (table != 0).sum(axis=1)
+        be.nblk[be.scratch_slot] = 1
+        be.block_table.copy_(be.block_table_host, non_blocking=True)
+
+    def admit(self, rows):
+        for rid, slot, prompt in rows:
+            self.last2[rid] = (prompt[-2], prompt[-1])
+        self.be._init_slots([(slot, p[-2], p[-1]) for _, slot, p in rows])
+
+    def commit(self, rows):
+        triples = []
+        for rid, slot, toks in rows:
+            prev = self.last2.get(rid, (0, 0))
+            seq = [prev[1]] + list(toks)
+            self.last2[rid] = (seq[-2], seq[-1])
+            triples.append((slot, seq[-2], seq[-1]))
+        self.be._init_slots(triples)
+
+    def prefill(self, rows):
+        if rows:
+            self.be._prefill_rows([(slot, p) for _, slot, p in rows], self.be.dfwd)
+
+    def draft(self, rows):
+        be = self.be
+        be._draft_rows(rows)
+        st = be.slot_tok.cpu().numpy()  # synchronises the draft stream
+        return {rid: st[slot, 2:2 + k].tolist() for rid, slot, _, k in rows}

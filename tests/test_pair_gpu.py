@@ -1,0 +1,74 @@
+"""Dedicated-draft-GPU PSD with the real GPU engines, two processes on one GPU.
+
+The driver's boxes have one GPU, so both ranks share cuda:0 and talk over gloo
+(host tensors); on a multi-GPU node bench.py --layout pairs uses NCCL between
+two devices with the same engines.  Output tokens must equal the
+single-process GpuBackend run.
+"""
+
+import os
+import socket
+
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+KW = dict(max_requests=16, max_batch=16, k_max=4, max_seq_len=128, seed=0, beta_target=2.0,
+          beta_draft=12.0, prefill_chunk_tokens=512)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _cfg_reqs():
+    from paper_2603_18016_b200 import SimConfig, make_requests
+    return SimConfig(mode="psd", m=4, k=4), make_requests([9, 14, 20, 7, 12, 16, 5, 30],
+                                                         prompt_len=10)
+
+
+def _worker(rank, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE="2",
+                      RANK=str(rank), LOCAL_RANK=str(rank))
+    import torch.distributed as dist
+
+    from paper_2603_18016_b200 import run
+    from paper_2603_18016_b200.gpu import GpuBackend
+    from paper_2603_18016_b200.pair import (DraftServer, GpuDraftEngine, GpuTargetEngine,
+                                            PairLink, PairTarget)
+    dist.init_process_group("gloo", init_method="env://")
+    if rank == 0:
+        gb = GpuBackend("tiny-target", "tiny-draft", roles=("target",), **KW)
+        be = PairTarget(GpuTargetEngine(gb), PairLink(1))
+        cfg, reqs = _cfg_reqs()
+        st, rep = run(cfg, reqs, backend=be)
+        be.stop()
+        q.put(("out", [r.output_ids for r in st.request_list()], rep.finished))
+    else:
+        gb = GpuBackend("tiny-target", "tiny-draft", roles=("draft",), **KW)
+        q.put(("steps", DraftServer(GpuDraftEngine(gb), PairLink(0)).serve()))
+    dist.destroy_process_group()
+
+
+def test_pair_gpu_engines_match_single_process(cuda_device):
+    from paper_2603_18016_b200 import run
+    from paper_2603_18016_b200.gpu import GpuBackend
+    cfg, reqs = _cfg_reqs()
+    st, rep = run(cfg, reqs, backend=GpuBackend("tiny-target", "tiny-draft", **KW))
+    ref = [r.output_ids for r in st.request_list()]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict((m[0], m[1:]) for m in (q.get(timeout=600) for _ in procs))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert got["out"][1] == 8
+    assert got["out"][0] == ref
+    assert got["steps"][0] > 0
