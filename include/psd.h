@@ -133,12 +133,19 @@ int psd_rope_kv(const void* qkv, int M, int Hq, int Hkv, int D, const int32_t* p
 /* Paged multi-query attention, GQA.  Sequence s: query tokens q_start[s] ..
  * +q_len[s]-1 at positions q_pos0[s] + t; token t attends keys
  * 0 .. min(q_pos0[s] + t, kv_len[s] - 1) read through
- * block_table[seq_slot[s] * max_blocks + key / block_size]. */
+ * block_table[seq_slot[s] * max_blocks + key / block_size].
+ * max_kv_len (host hint, >= every kv_len) enables split-KV: the keys of a
+ * (sequence, kv head) are cut across CTAs whose partial softmax states the
+ * last-arriving CTA merges (workspace: psd_attention_workspace_bytes, zeroed
+ * once; NULL or 0 disables splitting). */
+size_t psd_attention_workspace_bytes(int num_seqs, int Hkv, int max_q_len, int Hq, int D,
+                                     int max_kv_len);
 int psd_attention(const void* q, const void* k_cache, const void* v_cache,
                   const int32_t* block_table, int max_blocks, const int32_t* seq_slot,
                   const int32_t* q_start, const int32_t* q_len, const int32_t* q_pos0,
                   const int32_t* kv_len, int num_seqs, int max_q_len, int Hq, int Hkv, int D,
-                  int block_size, float scale, void* out, void* stream);
+                  int block_size, float scale, void* out, int max_kv_len, void* workspace,
+                  size_t workspace_bytes, void* stream);
 /* synthetic-language logit bias: logits[m, successor[prev_tokens[m]]] += beta */
 int psd_bigram_bias(float* logits, int64_t ld, const int32_t* prev_tokens, int M,
                     const int32_t* successor, int V, float beta, void* stream);

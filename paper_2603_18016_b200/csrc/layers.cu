@@ -267,11 +267,12 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
                  int max_blocks, const int32_t* __restrict__ seq_slot,
                  const int32_t* __restrict__ q_start, const int32_t* __restrict__ q_len,
                  const int32_t* __restrict__ q_pos0, const int32_t* __restrict__ kv_len, int Hq,
-                 int Hkv, int bs, float scale_log2, int tok_per_chunk, int RG,
+                 int Hkv, int bs, float scale_log2, int tok_per_chunk, int RG, int S,
+                 float* __restrict__ ws, int* __restrict__ tickets,
                  __nv_bfloat16* __restrict__ out) {
   constexpr int P = D + 8;  // smem row pitch (conflict-free fragment loads)
   const int KG = 4 / RG;
-  const int seq = blockIdx.x, hk = blockIdx.y, chunk = blockIdx.z;
+  const int seq = blockIdx.x, hk = blockIdx.y, chunk = blockIdx.z / S, split = blockIdx.z % S;
   const int G = Hq / Hkv;
   const int ql = q_len[seq];
   const int t0 = chunk * tok_per_chunk;
@@ -308,7 +309,10 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
     }
     *reinterpret_cast<uint4*>(&sQ[r][cc * 8]) = v;
   }
-  const int ntiles = last_key / KT + 1;
+  const int ntiles_all = last_key / KT + 1;
+  // this split's key tiles [ta, tb)
+  const int ta = split * ntiles_all / S, tb = (split + 1) * ntiles_all / S;
+  const int ntiles = tb - ta;
   const int ngroups = (ntiles + KG - 1) / KG;
   __syncthreads();  // bt staged
   auto load_group = [&](int gi, int st) {
@@ -316,8 +320,9 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
     for (int idx = tid; idx < KG * per; idx += ATT_THREADS) {
       const int j = idx / per, rem = idx % per;
       const int r = rem / (D / 8), cc = rem % (D / 8);
-      const int key = (gi * KG + j) * KT + r;
-      const bool ok = key <= last_key;
+      const int tile = ta + gi * KG + j;
+      const int key = tile * KT + r;
+      const bool ok = key <= last_key && tile < tb;
       size_t o = 0;
       if (ok) o = (((size_t)bt[key / bs] * bs + key % bs) * Hkv + hk) * D + cc * 8;
       cp_async16(&sK(st, j)[r][cc * 8], kc + o, ok);
@@ -357,8 +362,8 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
     else cp_async_commit();
     cp_async_wait<NS - 1>();
     __syncthreads();
-    const int kt = gi * KG + kg;
-    if (active && kt < ntiles) {
+    const int kt = ta + gi * KG + kg;
+    if (active && kt < tb) {
       Row* K = sK(st, kg);
       Row* V = sV(st, kg);
       float sacc[KT / 8][4];
@@ -496,6 +501,57 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
       }
     }
   }
+  if (S > 1) {
+    // split-KV: publish this split's (o, m, l) per row; the last split to
+    // arrive merges all S in split order (deterministic) and writes the output
+    const int unit = (seq * Hkv + hk) * (gridDim.z / S) + chunk;
+    const int RW = D + 2;
+    float* base = ws + (size_t)unit * S * ATT_MAXR * RW;
+    if (active && kg == 0) {
+      float* mine = base + (size_t)split * ATT_MAXR * RW;
+#pragma unroll
+      for (int n = 0; n < D / 8; ++n) {
+        const int d = n * 8 + 2 * c;
+        mine[r0 * RW + d] = o[n][0];
+        mine[r0 * RW + d + 1] = o[n][1];
+        mine[r1 * RW + d] = o[n][2];
+        mine[r1 * RW + d + 1] = o[n][3];
+      }
+      if (c == 0) {
+        mine[r0 * RW + D] = m0;
+        mine[r0 * RW + D + 1] = l0;
+        mine[r1 * RW + D] = m1;
+        mine[r1 * RW + D + 1] = l1;
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    __shared__ int s_last;
+    if (tid == 0) s_last = atomicAdd(tickets + unit, 1) == S - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (int idx = tid; idx < R * (D / 2); idx += ATT_THREADS) {
+      const int r = idx / (D / 2), d = (idx % (D / 2)) * 2;
+      float M = -INFINITY;
+      for (int sp = 0; sp < S; ++sp) M = fmaxf(M, __ldcg(base + ((size_t)sp * ATT_MAXR + r) * RW + D));
+      float L = 0.f, a0 = 0.f, a1 = 0.f;
+      for (int sp = 0; sp < S; ++sp) {
+        const float* pr = base + ((size_t)sp * ATT_MAXR + r) * RW;
+        const float ms = __ldcg(pr + D);
+        const float w = ms == -INFINITY ? 0.f : exp2f(ms - M);
+        L += __ldcg(pr + D + 1) * w;
+        a0 += __ldcg(pr + d) * w;
+        a1 += __ldcg(pr + d + 1) * w;
+      }
+      const float inv = L > 0.f ? 1.f / L : 0.f;
+      const int t = r / G, gg = r % G;
+      *reinterpret_cast<__nv_bfloat162*>(out + ((size_t)(qs + t0 + t) * Hq + hk * G + gg) * D + d) =
+          __floats2bfloat162_rn(a0 * inv, a1 * inv);
+    }
+    if (tid == 0) tickets[unit] = 0;
+    return;
+  }
   if (!active || kg != 0) return;
   const float inv0 = l0 > 0.f ? 1.f / l0 : 0.f, inv1 = l1 > 0.f ? 1.f / l1 : 0.f;
 #pragma unroll
@@ -512,6 +568,17 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
           __floats2bfloat162_rn(o[n][2] * inv1, o[n][3] * inv1);
     }
   }
+}
+
+// key splits for split-KV: a decode/verify CTA's latency is its serial chain
+// of key tiles, so split until every CTA has <= ~128 keys or the grid holds
+// ~4 waves of 148 SMs (>= 32 keys per split)
+int att_splits(int ctas, int max_kv_len) {
+  if (max_kv_len <= 0) return 1;
+  int S = 1;
+  while (S < 8 && (ctas * S < 4 * 148 || max_kv_len / S > 128) && max_kv_len / (S * 2) >= 32)
+    S *= 2;
+  return S;
 }
 
 // ---- synthetic-language bias (shared by draft and target) -----------------------
@@ -722,11 +789,22 @@ static int rope_launch(const QkvSrc& src, int M, int Hq, int Hkv, int D,
   return (int)cudaGetLastError();
 }
 
+size_t psd_attention_workspace_bytes(int num_seqs, int Hkv, int max_q_len, int Hq, int D,
+                                     int max_kv_len) {
+  const int G = Hq / Hkv;
+  const int tpc = ATT_MAXR / std::max(1, G);
+  const int chunks = (max_q_len + tpc - 1) / tpc;
+  const int S = att_splits(num_seqs * Hkv * chunks, max_kv_len);
+  const size_t units = (size_t)num_seqs * Hkv * chunks;
+  return 4096 * sizeof(int) + units * S * ATT_MAXR * (D + 2) * sizeof(float);
+}
+
 int psd_attention(const void* q, const void* k_cache, const void* v_cache,
                   const int32_t* block_table, int max_blocks, const int32_t* seq_slot,
                   const int32_t* q_start, const int32_t* q_len, const int32_t* q_pos0,
                   const int32_t* kv_len, int num_seqs, int max_q_len, int Hq, int Hkv, int D,
-                  int block_size, float scale, void* out, void* stream) {
+                  int block_size, float scale, void* out, int max_kv_len, void* workspace,
+                  size_t workspace_bytes, void* stream) {
   if (num_seqs <= 0) return 0;
   if (Hq % Hkv) return (int)cudaErrorInvalidValue;
   const int G = Hq / Hkv;
@@ -738,7 +816,15 @@ int psd_attention(const void* q, const void* k_cache, const void* v_cache,
   int RG = (rmax + 15) / 16;
   if (RG == 3) RG = 4;  // 4 / RG must be an integer number of key groups
   const int KG = 4 / RG;
-  dim3 grid(num_seqs, Hkv, chunks);
+  int S = att_splits(num_seqs * Hkv * chunks, max_kv_len);
+  const size_t units = (size_t)num_seqs * Hkv * chunks;
+  if (S > 1 && (!workspace || units > 4096 ||
+                workspace_bytes < 4096 * sizeof(int) + units * S * ATT_MAXR * (D + 2) * 4))
+    S = 1;  // no (or too little) workspace: no split
+  int* tickets = static_cast<int*>(workspace);
+  float* wsf = workspace ? reinterpret_cast<float*>(static_cast<char*>(workspace) + 4096 * 4)
+                         : nullptr;
+  dim3 grid(num_seqs, Hkv, chunks * S);
   const float sl2 = scale * 1.44269504088896341f;
   auto go = [&](auto kern, int kt, int d) {
     const int smem = (ATT_MAXR + 2 * ATT_STAGES * KG * kt) * (d + 8) * 2;
@@ -747,7 +833,7 @@ int psd_attention(const void* q, const void* k_cache, const void* v_cache,
     kern<<<grid, ATT_THREADS, smem, (cudaStream_t)stream>>>(
         static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k_cache),
         static_cast<const __nv_bfloat16*>(v_cache), block_table, max_blocks, seq_slot, q_start,
-        q_len, q_pos0, kv_len, Hq, Hkv, block_size, sl2, tpc, RG,
+        q_len, q_pos0, kv_len, Hq, Hkv, block_size, sl2, tpc, RG, S, wsf, tickets,
         static_cast<__nv_bfloat16*>(out));
   };
   switch (D) {

@@ -230,7 +230,7 @@ class Forward:
 
     def __init__(self, model: Transformer, max_tokens: int, max_seqs: int,
                  max_logit_rows: int, block_table: torch.Tensor, sets: int = 1,
-                 workspace_bytes: int = 64 << 20) -> None:
+                 workspace_bytes: int = 64 << 20, max_kv_len: int = 0) -> None:
         s = model.shape
         dev = model.device
         self.model = model
@@ -258,6 +258,11 @@ class Forward:
                 lib.psd_gemm_plan(mm, n_out, k_in, native.EPI_BF16, 0, None, ctypes.byref(wb))
                 need = max(need, wb.value)
         self.ws = torch.zeros(max(need, 1 << 20), dtype=torch.uint8, device=dev)
+        # split-KV attention workspace (tickets + partial softmax states), zeroed
+        self.max_kv_len = max_kv_len
+        aw = lib.psd_attention_workspace_bytes(max_seqs, s.kv_heads, 16, s.heads, s.head_dim,
+                                               max_kv_len) if max_kv_len else 0
+        self.att_ws = torch.zeros(max(aw, 16384), dtype=torch.uint8, device=dev)
         # fp32 split-K partials of the QKV / O / down GEMMs (one buffer, reused
         # in sequence: each is consumed before the next GEMM overwrites it)
         self._nsplit = ctypes.byref(ctypes.c_int(1))
@@ -362,7 +367,9 @@ class Forward:
                                    v["q_len"].data_ptr(), v["q_pos0"].data_ptr(),
                                    v["kv_len"].data_ptr(), n_seqs, max_q_len, s.heads,
                                    s.kv_heads, s.head_dim, m.block_size, scale,
-                                   self.attn.data_ptr(), st), "attention")
+                                   self.attn.data_ptr(), self.max_kv_len if M <= 4 * n_seqs * 4
+                                   else 0, self.att_ws.data_ptr(), self.att_ws.numel(), st),
+                 "attention")
             _chk(lib.psd_gemm_partials(self.attn.data_ptr(), Dq, M, Dq, L["wo"].data_ptr(), Dq, H,
                                        part, partn, 0, nsp, st), "gemm o")
             _chk(lib.psd_add_rmsnorm(X, H, part, nsp._obj.value, M * H, H, None,

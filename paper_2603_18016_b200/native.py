@@ -40,7 +40,8 @@ SIGNATURES: dict[str, tuple] = {
     "psd_gemm_tiled": (_i, [_p, _i, _i, _i, _p, _i, _p, _i, _i, _p, _i, _p, _sz, _p]),
     "psd_gemm_partials": (_i, [_p, _i, _i, _i, _p, _i, _i, _p, _sz, _i, _c.POINTER(_i), _p]),
     "psd_attention": (_i, [_p, _p, _p, _p, _i, _p, _p, _p, _p, _p, _i, _i, _i, _i, _i, _i, _f,
-                           _p, _p]),
+                           _p, _i, _p, _sz, _p]),
+    "psd_attention_workspace_bytes": (_sz, [_i, _i, _i, _i, _i, _i]),
     "psd_bigram_bias": (_i, [_p, _i64, _p, _i, _p, _i, _f, _p]),
     "psd_philox_uniforms": (_i, [_c.c_uint64, _p, _p, _i, _i, _i, _p, _p]),
     "psd_rope_kv_partials": (_i, [_p, _i, _sz, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _p, _p]),

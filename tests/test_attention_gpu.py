@@ -70,16 +70,23 @@ def test_attention_matches_torch(cuda_device, D, Hq, Hkv):
     seqs = [(6, 140, 146), (6, 7, 10), (2, 30, 32), (1, 63, 64), (40, 0, 40), (6, 0, 1),
             (5, 300, 305)]
     q, kc, vc, bt, meta = _case(cuda_device, D, Hq, Hkv, seqs)
-    out = torch.empty_like(q)
     lib = native.load()
     st = torch.cuda.current_stream().cuda_stream
-    rc = lib.psd_attention(q.data_ptr(), kc.data_ptr(), vc.data_ptr(), bt.data_ptr(), bt.shape[1],
-                           meta["seq_slot"].data_ptr(), meta["q_start"].data_ptr(),
-                           meta["q_len"].data_ptr(), meta["q_pos0"].data_ptr(),
-                           meta["kv_len"].data_ptr(), len(seqs), max(s[0] for s in seqs), Hq, Hkv,
-                           D, 16, 1.0 / math.sqrt(D), out.data_ptr(), st)
-    assert rc == 0
-    torch.cuda.synchronize()
     ref = _ref(q, kc, vc, bt, meta, seqs, Hq, Hkv, D)
-    err = (out.float() - ref).abs().max().item()
-    assert err < 2e-2, err
+    maxq = max(s[0] for s in seqs)
+    maxkv = max(max(kv, p0 + ql) for ql, p0, kv in seqs)
+    ws = torch.zeros(lib.psd_attention_workspace_bytes(len(seqs), Hkv, maxq, Hq, D, 1024) +
+                     16384, dtype=torch.uint8, device=cuda_device)
+    for kvhint in (0, maxkv, 1024):  # no split, split-KV, more splits
+        out = torch.full_like(q, float("nan"))
+        for _ in range(2):  # tickets are self-resetting
+            rc = lib.psd_attention(q.data_ptr(), kc.data_ptr(), vc.data_ptr(), bt.data_ptr(),
+                                   bt.shape[1], meta["seq_slot"].data_ptr(),
+                                   meta["q_start"].data_ptr(), meta["q_len"].data_ptr(),
+                                   meta["q_pos0"].data_ptr(), meta["kv_len"].data_ptr(),
+                                   len(seqs), maxq, Hq, Hkv, D, 16, 1.0 / math.sqrt(D),
+                                   out.data_ptr(), kvhint, ws.data_ptr(), ws.numel(), st)
+            assert rc == 0
+        torch.cuda.synchronize()
+        err = (out.float() - ref).abs().max().item()
+        assert err < 2e-2, (kvhint, err)

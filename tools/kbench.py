@@ -136,13 +136,22 @@ def attn_case(tag, nseq, ql, ctx, Hq, Hkv, D):
     q_len = i32([ql] * nseq)
     q_pos0 = i32([ctx] * nseq)
     kv_len = i32([ctx + ql] * nseq)
+    aws = torch.zeros(lib.psd_attention_workspace_bytes(nseq, Hkv, ql, Hq, D, 400) + 16384,
+                      dtype=torch.uint8, device=dev)
+    kvh = [0]
+
     def fn():
         st = torch.cuda.current_stream().cuda_stream
         rc = lib.psd_attention(q.data_ptr(), kc.data_ptr(), vc.data_ptr(), bt.data_ptr(),
                                nblk_seq, seq_slot.data_ptr(), q_start.data_ptr(), q_len.data_ptr(),
                                q_pos0.data_ptr(), kv_len.data_ptr(), nseq, ql, Hq, Hkv, D, bs,
-                               1 / math.sqrt(D), out.data_ptr(), st)
+                               1 / math.sqrt(D), out.data_ptr(), kvh[0], aws.data_ptr(),
+                               aws.numel(), st)
         assert rc == 0
+    us = timeit(fn)
+    report(f"attention {tag} nosplit", f"seqs={nseq} q={ql} ctx={ctx} D={D}", us,
+           nseq * (ctx + ql) * Hkv * D * 2 * 2 + q.numel() * 2 * 2)
+    kvh[0] = 400
     us = timeit(fn)
     nbytes = nseq * (ctx + ql) * Hkv * D * 2 * 2 + q.numel() * 2 * 2
     report(f"attention {tag}", f"seqs={nseq} q={ql} ctx={ctx} D={D}", us, nbytes)
