@@ -137,7 +137,17 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUt
       const int pf = g.prefetch;
       const int npf = pf > 0 ? min(nkb, pf) : 0;
       for (int i = 0; i < npf; ++i) tma_prefetch_l2_2d(&tmW, (kb0 + i) * BK, n0, pol_pf);
-      for (int i = 0; i < nkb; ++i) {
+      // PDL: weights do not depend on the predecessor kernel -> the first
+      // stages' weight tiles stream while it drains; tokens after pdl_wait()
+      const int npre = min(nkb, C::STAGES);
+      for (int i = 0; i < npre; ++i) {
+        mbar_arrive_expect_tx(full + i, C::STAGE);
+        tma_load_2d(sA + i * C::A_BYTES, &tmW, full + i, (kb0 + i) * BK, n0, pol_w);
+      }
+      pdl_wait();
+      for (int i = 0; i < npre; ++i)
+        tma_load_2d(sB + i * C::B_BYTES, &tmX, full + i, (kb0 + i) * BK, m0, pol_x);
+      for (int i = npre; i < nkb; ++i) {
         const int s = i % C::STAGES;
         const uint32_t ph = (i / C::STAGES) & 1;
         if (pf > 0 && i + pf < nkb) tma_prefetch_l2_2d(&tmW, (kb0 + i + pf) * BK, n0, pol_pf);
@@ -147,6 +157,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUt
         tma_load_2d(sA + s * C::A_BYTES, &tmW, full + s, kc, n0, pol_w);
         tma_load_2d(sB + s * C::B_BYTES, &tmX, full + s, kc, m0, pol_x);
       }
+      pdl_trigger();
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -169,6 +180,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUt
     __syncwarp();
   } else {
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    pdl_wait();  // the residual R is the predecessor's output
     mbar_wait(accum, 0);
     tc_fence_after();
     const int n = n0 + 32 * q + lane;
@@ -321,11 +333,36 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       long long u = u0;
       Seg sg;
       int i = 0;
+      // PDL: the first stages' weight tiles stream before pdl_wait()
+      int npre = 0;
+      {
+        long long uu = u0;
+        Seg s0;
+        if (next_seg(uu, s0)) {
+          const int n0 = (s0.t / g.MT) * BM;
+          npre = min(s0.kb1 - s0.kb0, C::STAGES);
+          for (int j = 0; j < npre; ++j) {
+            mbar_arrive_expect_tx(full + j, C::STAGE);
+            if constexpr (TILED) {
+              const __nv_bfloat16* src =
+                  g.Wt + ((size_t)(n0 / BM) * g.KB + s0.kb0 + j) * (size_t)(BM * BK);
+              bulk_load(sA + j * C::A_BYTES, src, C::A_BYTES, full + j, pol_w);
+            } else {
+              tma_load_2d(sA + j * C::A_BYTES, &tmW, full + j, (s0.kb0 + j) * BK, n0, pol_w);
+            }
+          }
+        }
+      }
+      pdl_wait();
       while (next_seg(u, sg)) {
         const int n0 = (sg.t / g.MT) * BM, m0 = (sg.t % g.MT) * BN;
         for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++i) {
           const int s = i % C::STAGES;
           const uint32_t ph = (i / C::STAGES) & 1;
+          if (i < npre) {  // weight tile already in flight
+            tma_load_2d(sB + s * C::B_BYTES, &tmX, full + s, kb * BK, m0, pol_x);
+            continue;
+          }
           mbar_wait(empty + s, ph ^ 1);
           mbar_arrive_expect_tx(full + s, C::STAGE);
           if constexpr (TILED) {
@@ -339,6 +376,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           tma_load_2d(sB + s * C::B_BYTES, &tmX, full + s, kb * BK, m0, pol_x);
         }
       }
+      pdl_trigger();
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -373,6 +411,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   } else {
     const int q = warp & 3;
     const int row = 32 * q + lane;  // tile row (weight row) of this thread
+    pdl_wait();  // residual / partial workspace belong to the predecessor's epoch
     long long u = u0;
     Seg sg;
     int j = 0;
@@ -494,6 +533,8 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 // ---- split-K reduction with the same epilogues ------------------------------
 __global__ void gemm_reduce_kernel(const float* __restrict__ P, int splits, int M, int N, int epi,
                                    void* Y, int ldy, const __nv_bfloat16* R, int ldr) {
+  pdl_wait();
+  pdl_trigger();
   const int Nout = epi == PSD_EPI_SILU ? N / 2 : N;
   const size_t total = (size_t)M * Nout;
   const size_t slice = (size_t)M * N;
@@ -569,9 +610,7 @@ int launch_bn(const CUtensorMap& mw, const CUtensorMap& mx, const GemmArgs& g, d
     if (e != cudaSuccess) return (int)e;
     attr_done = true;
   }
-  psd::count_launches();
-  gemm_kernel<BN, EPI><<<grid, kThreads, C::SMEM, st>>>(mw, mx, g);
-  return (int)cudaGetLastError();
+  return (int)psd::launch(gemm_kernel<BN, EPI>, grid, dim3(kThreads), C::SMEM, st, mw, mx, g);
 }
 
 template <int BN, int EPI, bool TILED>
@@ -584,9 +623,8 @@ int launch_sk_bn(const CUtensorMap& mw, const CUtensorMap& mx, const SKArgs& g, 
     if (e != cudaSuccess) return (int)e;
     attr_done = true;
   }
-  psd::count_launches();
-  gemm_sk_kernel<BN, EPI, TILED><<<g.G, kThreads, C::SMEM, st>>>(mw, mx, g);
-  return (int)cudaGetLastError();
+  return (int)psd::launch(gemm_sk_kernel<BN, EPI, TILED>, dim3(g.G), dim3(kThreads), C::SMEM, st, mw,
+                          mx, g);
 }
 
 template <int EPI, bool TILED = false>

@@ -31,6 +31,8 @@ __device__ __forceinline__ float warp_max(float v) {
 // ---- embedding gather -------------------------------------------------------
 __global__ void embed_kernel(const int32_t* __restrict__ tok, const __nv_bfloat16* __restrict__ E,
                              __nv_bfloat16* __restrict__ out, int H) {
+  pdl_wait();
+  pdl_trigger();
   const int m = blockIdx.x;
   const int t = tok[m];
   const uint4* src = reinterpret_cast<const uint4*>(E + (size_t)(t < 0 ? 0 : t) * H);
@@ -54,6 +56,8 @@ add_rmsnorm_kernel(__nv_bfloat16* __restrict__ x, int ldx, const float* __restri
                    size_t slice, int ldp, const int32_t* __restrict__ rows,
                    const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ y, int ldy,
                    int H, float eps, int write_back) {
+  pdl_wait();
+  pdl_trigger();
   const int m = blockIdx.x;
   const int src = rows ? rows[m] : m;
   __nv_bfloat16* xr = x + (size_t)src * ldx;
@@ -161,6 +165,8 @@ rope_kv_kernel(const QkvSrc src, int Hq, int Hkv, int D,
                const float* __restrict__ inv_freq, const __nv_bfloat16* __restrict__ bias,
                __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ kc,
                __nv_bfloat16* __restrict__ vc) {
+  pdl_wait();
+  pdl_trigger();
   const int m = blockIdx.x;
   const int p = pos[m];
   const int s = slot[m];
@@ -270,6 +276,8 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
                  int Hkv, int bs, float scale_log2, int tok_per_chunk, int RG, int S,
                  float* __restrict__ ws, int* __restrict__ tickets,
                  __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int P = D + 8;  // smem row pitch (conflict-free fragment loads)
   const int KG = 4 / RG;
   const int seq = blockIdx.x, hk = blockIdx.y, chunk = blockIdx.z / S, split = blockIdx.z % S;
@@ -585,6 +593,8 @@ int att_splits(int ctas, int max_kv_len) {
 __global__ void bigram_bias_kernel(float* __restrict__ logits, int64_t ld,
                                    const int32_t* __restrict__ prev, int M,
                                    const int32_t* __restrict__ succ, int V, float beta) {
+  pdl_wait();
+  pdl_trigger();
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= M) return;
   const int t = prev[m];
@@ -605,6 +615,8 @@ __host__ __device__ inline void philox_round(uint32_t (&c)[4], uint32_t k0, uint
 __global__ void philox_uniform_kernel(uint64_t seed, const int32_t* __restrict__ rid,
                                       const int32_t* __restrict__ jv, int B, int n, int base,
                                       float* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= B * n) return;
   const int b = idx / n, i = idx % n;
@@ -623,6 +635,8 @@ __global__ void philox_uniform_kernel(uint64_t seed, const int32_t* __restrict__
 __global__ void index_copy_kernel(int32_t* __restrict__ dst, const int32_t* __restrict__ dst_idx,
                                   const int32_t* __restrict__ src,
                                   const int32_t* __restrict__ src_idx, int n) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int d = dst_idx ? dst_idx[i] : i;
@@ -636,6 +650,8 @@ __global__ void commit_kernel(const int32_t* __restrict__ acc, const int32_t* __
                               int K, const int32_t* __restrict__ row_slot, int n,
                               int32_t* __restrict__ gen, int32_t* __restrict__ slot_tok, int ldt,
                               int32_t* __restrict__ outputs, int ldo) {
+  pdl_wait();
+  pdl_trigger();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= n) return;
   const int s = row_slot[b];
@@ -672,6 +688,8 @@ __global__ void fill_uniform_kernel(__nv_bfloat16* __restrict__ out, size_t n, u
 __global__ void copy_rows_kernel(float* __restrict__ dst, const int32_t* __restrict__ dst_rows,
                                  int64_t dst_ld, const float* __restrict__ src, int64_t src_ld,
                                  int ncols) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.y;
   const int dr = dst_rows[r];
   if (dr < 0) return;
@@ -692,29 +710,24 @@ int psd_copy_rows_f32(float* dst, const int32_t* dst_rows, int64_t dst_ld, const
   if (nrows <= 0) return 0;
   if ((ncols & 3) || (dst_ld & 3) || (src_ld & 3)) return (int)cudaErrorMisalignedAddress;
   dim3 grid(16, nrows);
-  psd::count_launches();
-  copy_rows_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(dst, dst_rows, dst_ld, src, src_ld,
-                                                           ncols);
-  return (int)cudaGetLastError();
+  return (int)psd::launch(copy_rows_kernel, grid, dim3(256), 0, (cudaStream_t)stream, dst, dst_rows,
+                          dst_ld, src, src_ld, ncols);
 }
 
 int psd_index_copy_i32(int32_t* dst, const int32_t* dst_idx, const int32_t* src,
                        const int32_t* src_idx, int n, void* stream) {
   if (n <= 0) return 0;
-  psd::count_launches();
-  index_copy_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(dst, dst_idx, src, src_idx, n);
-  return (int)cudaGetLastError();
+  return (int)psd::launch(index_copy_kernel, dim3((n + 255) / 256), dim3(256), 0,
+                          (cudaStream_t)stream, dst, dst_idx, src, src_idx, n);
 }
 
 int psd_commit(const int32_t* accepted_len, const int32_t* out_tokens, int K,
                const int32_t* row_slot, int n, int32_t* generated, int32_t* slot_tokens,
                int slot_tokens_ld, int32_t* outputs, int outputs_ld, void* stream) {
   if (n <= 0) return 0;
-  psd::count_launches();
-  commit_kernel<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(
-      accepted_len, out_tokens, K, row_slot, n, generated, slot_tokens, slot_tokens_ld, outputs,
-      outputs_ld);
-  return (int)cudaGetLastError();
+  return (int)psd::launch(commit_kernel, dim3((n + 127) / 128), dim3(128), 0,
+                          (cudaStream_t)stream, accepted_len, out_tokens, K, row_slot, n,
+                          generated, slot_tokens, slot_tokens_ld, outputs, outputs_ld);
 }
 
 int psd_fill_uniform_bf16(void* out, size_t n, uint64_t seed, float span, void* stream) {
@@ -728,10 +741,9 @@ int psd_fill_uniform_bf16(void* out, size_t n, uint64_t seed, float span, void* 
 int psd_embed(const int32_t* tokens, int M, const void* table, int H, void* out, void* stream) {
   if (M <= 0) return 0;
   if (H % 8) return (int)cudaErrorInvalidValue;
-  psd::count_launches();
-  embed_kernel<<<M, 128, 0, (cudaStream_t)stream>>>(
-      tokens, static_cast<const __nv_bfloat16*>(table), static_cast<__nv_bfloat16*>(out), H);
-  return (int)cudaGetLastError();
+  return (int)psd::launch(embed_kernel, dim3(M), dim3(128), 0, (cudaStream_t)stream, tokens,
+                          static_cast<const __nv_bfloat16*>(table),
+                          static_cast<__nv_bfloat16*>(out), H);
 }
 
 int psd_add_rmsnorm(void* x, int ldx, const float* partials, int S, size_t slice, int ldp,
@@ -740,11 +752,10 @@ int psd_add_rmsnorm(void* x, int ldx, const float* partials, int S, size_t slice
   if (M <= 0) return 0;
   if (H % 8 || H > 8 * NORM_THREADS * 4) return (int)cudaErrorInvalidValue;
   auto go = [&](auto kern) {
-    psd::count_launches();
-    kern<<<M, NORM_THREADS, 0, (cudaStream_t)stream>>>(
-        static_cast<__nv_bfloat16*>(x), ldx, partials, S, slice, ldp, rows,
-        static_cast<const __nv_bfloat16*>(w), static_cast<__nv_bfloat16*>(y), ldy, H, eps,
-        write_back);
+    psd::launch(kern, dim3(M), dim3(NORM_THREADS), 0, (cudaStream_t)stream,
+                static_cast<__nv_bfloat16*>(x), ldx, partials, S, slice, ldp, rows,
+                static_cast<const __nv_bfloat16*>(w), static_cast<__nv_bfloat16*>(y), ldy, H, eps,
+                write_back);
   };
   const int nv = (H / 8 + NORM_THREADS - 1) / NORM_THREADS;
   if (nv <= 1) go(add_rmsnorm_kernel<1>);
@@ -781,12 +792,12 @@ static int rope_launch(const QkvSrc& src, int M, int Hq, int Hkv, int D,
                        void* stream) {
   if (M <= 0) return 0;
   if (D % 16 || D > 256) return (int)cudaErrorInvalidValue;
-  psd::count_launches();
-  rope_kv_kernel<<<M, 256, 0, (cudaStream_t)stream>>>(
-      src, Hq, Hkv, D, positions, slots, inv_freq,
-      static_cast<const __nv_bfloat16*>(qkv_bias), static_cast<__nv_bfloat16*>(q_out), static_cast<__nv_bfloat16*>(k_cache),
-      static_cast<__nv_bfloat16*>(v_cache));
-  return (int)cudaGetLastError();
+  return (int)psd::launch(rope_kv_kernel, dim3(M), dim3(256), 0, (cudaStream_t)stream, src, Hq,
+                          Hkv, D, positions, slots, inv_freq,
+                          static_cast<const __nv_bfloat16*>(qkv_bias),
+                          static_cast<__nv_bfloat16*>(q_out),
+                          static_cast<__nv_bfloat16*>(k_cache),
+                          static_cast<__nv_bfloat16*>(v_cache));
 }
 
 size_t psd_attention_workspace_bytes(int num_seqs, int Hkv, int max_q_len, int Hq, int D,
@@ -829,12 +840,11 @@ int psd_attention(const void* q, const void* k_cache, const void* v_cache,
   auto go = [&](auto kern, int kt, int d) {
     const int smem = (ATT_MAXR + 2 * ATT_STAGES * KG * kt) * (d + 8) * 2;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    psd::count_launches();
-    kern<<<grid, ATT_THREADS, smem, (cudaStream_t)stream>>>(
-        static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k_cache),
-        static_cast<const __nv_bfloat16*>(v_cache), block_table, max_blocks, seq_slot, q_start,
-        q_len, q_pos0, kv_len, Hq, Hkv, block_size, sl2, tpc, RG, S, wsf, tickets,
-        static_cast<__nv_bfloat16*>(out));
+    psd::launch(kern, grid, dim3(ATT_THREADS), smem, (cudaStream_t)stream,
+                static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k_cache),
+                static_cast<const __nv_bfloat16*>(v_cache), block_table, max_blocks, seq_slot,
+                q_start, q_len, q_pos0, kv_len, Hq, Hkv, block_size, sl2, tpc, RG, S, wsf,
+                tickets, static_cast<__nv_bfloat16*>(out));
   };
   switch (D) {
     case 32: go(attention_kernel<32, 64, ATT_STAGES>, 64, 32); break;
@@ -848,19 +858,15 @@ int psd_attention(const void* q, const void* k_cache, const void* v_cache,
 int psd_bigram_bias(float* logits, int64_t ld, const int32_t* prev_tokens, int M,
                     const int32_t* successor, int V, float beta, void* stream) {
   if (M <= 0) return 0;
-  psd::count_launches();
-  bigram_bias_kernel<<<(M + 127) / 128, 128, 0, (cudaStream_t)stream>>>(logits, ld, prev_tokens, M,
-                                                                      successor, V, beta);
-  return (int)cudaGetLastError();
+  return (int)psd::launch(bigram_bias_kernel, dim3((M + 127) / 128), dim3(128), 0,
+                          (cudaStream_t)stream, logits, ld, prev_tokens, M, successor, V, beta);
 }
 
 int psd_philox_uniforms(uint64_t seed, const int32_t* request_ids, const int32_t* verify_index,
                         int B, int n, int base, float* out, void* stream) {
   if (B * n <= 0) return 0;
-  psd::count_launches();
-  philox_uniform_kernel<<<(B * n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
-      seed, request_ids, verify_index, B, n, base, out);
-  return (int)cudaGetLastError();
+  return (int)psd::launch(philox_uniform_kernel, dim3((B * n + 255) / 256), dim3(256), 0,
+                          (cudaStream_t)stream, seed, request_ids, verify_index, B, n, base, out);
 }
 
 }  // extern "C"

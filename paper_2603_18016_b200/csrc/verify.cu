@@ -87,6 +87,8 @@ __device__ __forceinline__ int expected_stats(const Params& p, int kb, bool samp
 template <bool SAMPLE>
 __global__ void __launch_bounds__(kThreads)
 verify_stats(const Params p) {
+  pdl_wait();
+  pdl_trigger();
   const int slice = blockIdx.x;
   const int b = blockIdx.y / p.R;
   const int r = blockIdx.y % p.R;
@@ -324,6 +326,8 @@ __device__ int last_positive(const WeightCtx& w, int blk, int* s_int) {
 
 __global__ void __launch_bounds__(kThreads)
 verify_sample(const Params p) {
+  pdl_wait();
+  pdl_trigger();
   const int blk = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
   const Plan pl = p.plan[b];
   WeightCtx w;
@@ -483,9 +487,7 @@ int psd_verify_greedy(const float* target_logits, int64_t t_stride_b, int64_t t_
   p.wblk = reinterpret_cast<float*>(w + L.wblk);
   p.NS = (V + PSD_SLICE - 1) / PSD_SLICE; p.NB = (V + PSD_SBLK - 1) / PSD_SBLK; p.R = K + 1;
   dim3 grid(p.NS, B * p.R);
-  psd::count_launches();
-  verify_stats<false><<<grid, kThreads, 0, (cudaStream_t)stream>>>(p);
-  return (int)cudaGetLastError();
+  return (int)psd::launch(verify_stats<false>, grid, dim3(kThreads), 0, (cudaStream_t)stream, p);
 }
 
 int psd_verify_sample(const float* target_logits, int64_t t_stride_b, int64_t t_stride_i, int V,
@@ -513,12 +515,10 @@ int psd_verify_sample(const float* target_logits, int64_t t_stride_b, int64_t t_
   p.NS = (V + PSD_SLICE - 1) / PSD_SLICE; p.NB = (V + PSD_SBLK - 1) / PSD_SBLK;
   p.R = 2 * K + 1;
   dim3 grid(p.NS, B * p.R);
-  psd::count_launches();
-  verify_stats<true><<<grid, kThreads, 0, (cudaStream_t)stream>>>(p);
+  cudaError_t e = psd::launch(verify_stats<true>, grid, dim3(kThreads), 0, (cudaStream_t)stream, p);
+  if (e != cudaSuccess) return (int)e;
   dim3 grid2(p.NB, B);
-  psd::count_launches();
-  verify_sample<<<grid2, kThreads, 0, (cudaStream_t)stream>>>(p);
-  return (int)cudaGetLastError();
+  return (int)psd::launch(verify_sample, grid2, dim3(kThreads), 0, (cudaStream_t)stream, p);
 }
 
 int psd_verify_sample_rows(const float* target_logits, int64_t t_stride_b, int64_t t_stride_i,
@@ -548,12 +548,10 @@ int psd_verify_sample_rows(const float* target_logits, int64_t t_stride_b, int64
   p.NS = (V + PSD_SLICE - 1) / PSD_SLICE; p.NB = (V + PSD_SBLK - 1) / PSD_SBLK;
   p.R = 2 * K + 1;
   dim3 grid(p.NS, B * p.R);
-  psd::count_launches();
-  verify_stats<true><<<grid, kThreads, 0, (cudaStream_t)stream>>>(p);
+  cudaError_t e = psd::launch(verify_stats<true>, grid, dim3(kThreads), 0, (cudaStream_t)stream, p);
+  if (e != cudaSuccess) return (int)e;
   dim3 grid2(p.NB, B);
-  psd::count_launches();
-  verify_sample<<<grid2, kThreads, 0, (cudaStream_t)stream>>>(p);
-  return (int)cudaGetLastError();
+  return (int)psd::launch(verify_sample, grid2, dim3(kThreads), 0, (cudaStream_t)stream, p);
 }
 
 }  // extern "C"

@@ -116,9 +116,9 @@ class GpuBackend:
             vt_tokens = max(B * (K + 1), prefill_chunk_tokens)
             vd_tokens = max(2 * B, prefill_chunk_tokens)
             self.tfwd = Forward(self.target, vt_tokens, max(B, 256), B * (K + 1),
-                                self.block_table, sets=1, max_kv_len=max_seq_len) if has_t else None
+                                self.block_table, sets=1, max_kv_len=0) if has_t else None
             self.dfwd = Forward(self.draft, vd_tokens, max(B, 256), B, self.block_table,
-                                sets=K + 1, max_kv_len=max_seq_len) if has_d else None
+                                sets=K + 1, max_kv_len=0) if has_d else None
             self.tlogits = torch.empty(B * (K + 1), self.tshape.vocab, dtype=torch.float32,
                                        device=dev) if has_t else None
             self.dlogits = torch.empty(B, self.dshape.vocab, dtype=torch.float32,
