@@ -252,6 +252,18 @@ def main():
         gemm_case("1B lm_head", 32, 128256, 2048, "f32", copies=2, tiled=True)
         gemm_case("1B lm_head", 32, 128256, 2048, "f32", copies=2)
         gemm_case("1B gate/up M64", 64, 16384, 2048, "silu")
+        # the split-K partial GEMMs the forward uses for QKV / O / down
+        gemm_case("8B qkv part", 192, 6144, 4096, "partial")
+        gemm_case("8B o part", 192, 4096, 4096, "partial")
+        gemm_case("8B down part", 192, 4096, 14336, "partial")
+        gemm_case("1B qkv part", 32, 3072, 2048, "partial")
+        gemm_case("1B o part", 32, 2048, 2048, "partial")
+        gemm_case("1B down part", 32, 2048, 8192, "partial")
+    if want("gemm1b"):
+        gemm_case("1B qkv part", 32, 3072, 2048, "partial")
+        gemm_case("1B gate/up", 32, 16384, 2048, "silu")
+    if want("gemmgu"):
+        gemm_case("8B gate/up", 192, 28672, 4096, "silu")
     if want("attn"):
         attn_case("8B verify", 32, 6, 300, 32, 8, 128)
         attn_case("1B draft", 32, 1, 300, 32, 8, 64)
