@@ -188,6 +188,27 @@ def kernel_rooflines(backend, hbm_peak: float) -> tuple[dict, dict]:
     return roof, vk
 
 
+def draft_hiding(states) -> dict:
+    """Exposed drafting: per overlapped PSD step, exposed =
+    max(0, t_step - t_prefill - t_verify); hidden fraction = 1 - sum(exposed) /
+    sum(t_draft).  Durations are CUDA-event ms from GpuBackend.execute."""
+    exposed = drafted = step = 0.0
+    n = 0
+    for state in states:
+        for rec in state.step_log:
+            if rec.fallback or rec.target_batch is None or rec.draft_duration <= 0.0:
+                continue
+            e = max(0.0, rec.step_duration - rec.prefill_duration - rec.verify_duration)
+            exposed += e
+            drafted += rec.draft_duration
+            step += rec.step_duration
+            n += 1
+    if n == 0 or drafted <= 0.0:
+        return {"draft_hidden_frac": None, "exposed_draft_frac_of_step": None, "steps": 0}
+    return {"draft_hidden_frac": round(1.0 - exposed / drafted, 4),
+            "exposed_draft_frac_of_step": round(exposed / step, 4), "steps": n}
+
+
 def cpu_sample(steps: int = 1, n_req: int = 2, out_len: int = 6):
     """The CPU oracle PSD (numpy + C verify) on a bounded sample of the
     workload: same model shapes, k, prompt length; n_req requests of out_len
@@ -315,11 +336,13 @@ def run_ours(args) -> None:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        reps = []
+        reps, states = [], []
         stats0 = dict(backend.stats)
         l0 = be.launches
         for _ in range(args.steps):
-            reps.append(one(mode)[1])
+            st_, rep_ = one(mode)
+            reps.append(rep_)
+            states.append(st_)
         e1.record()
         if pairs:
             backend.stop()
@@ -327,7 +350,7 @@ def run_ours(args) -> None:
         launches[mode] = be.launches - l0
         ms_local = e0.elapsed_time(e1)
         tokens, ms = pd.aggregate(sum(r.total_generated for r in reps), ms_local, dev)
-        results[mode] = {"ms": ms, "tokens": tokens, "reps": reps,
+        results[mode] = {"ms": ms, "tokens": tokens, "reps": reps, "states": states,
                          "clocks": clocks.stop() if clocks else None,
                          "draft_ms": backend.stats["draft_ms"] - stats0["draft_ms"],
                          "verify_ms": backend.stats["verify_ms"] - stats0["verify_ms"],
@@ -392,6 +415,7 @@ def run_ours(args) -> None:
         "mean_accepted_len": round(mean_accepted_length(r0), 4),
         "accepted_per_verify": round(r0.total_accepted / max(1, r0.total_bonus), 4),
         "psd_steps_per_pass": steps_psd,
+        "draft_hiding": draft_hiding(psd["states"]),
         "draft_ms_per_pass": round(psd["draft_ms"] / args.steps, 2),
         "verify_ms_per_pass": round(psd["verify_ms"] / args.steps, 2),
         "e2e": {"value": round(rep_e2e.total_generated / e2e_s, 1), "unit": "tok/s",

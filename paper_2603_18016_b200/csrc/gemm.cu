@@ -254,6 +254,7 @@ struct SKArgs {
   int* tickets;   // [tiles], zero between launches
   const __nv_bfloat16* Wt;  // pre-tiled weights (TILED variant)
   int silu_mode;            // tuning experiment: 0 silu(g)*u, 1 g*u, 2 g only
+  int prefetch;             // weight k-blocks prefetched into L2 ahead of the ring
 };
 
 struct Seg {
@@ -353,12 +354,25 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           }
         }
       }
+      // L2 prefetch of the weight k-blocks g.prefetch units ahead of the ring
+      // (keeps HBM requests in flight beyond what the smem stages hold)
+      const int pf = TILED ? 0 : g.prefetch;
+      long long upf = u0 + npre;
+      const long long upf_end = u1;
+      auto prefetch_to = [&](long long limit) {
+        for (; upf < limit && upf < upf_end; ++upf) {
+          const int tt = (int)(upf / g.KB), kk = (int)(upf % g.KB);
+          tma_prefetch_l2_2d(&tmW, kk * BK, (tt / g.MT) * BM, pol_w);
+        }
+      };
+      if (pf > 0) prefetch_to(u0 + npre + pf);
       pdl_wait();
       while (next_seg(u, sg)) {
         const int n0 = (sg.t / g.MT) * BM, m0 = (sg.t % g.MT) * BN;
         for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++i) {
           const int s = i % C::STAGES;
           const uint32_t ph = (i / C::STAGES) & 1;
+          if (pf > 0) prefetch_to(u0 + i + 1 + pf);
           if (i < npre) {  // weight tile already in flight
             tma_load_2d(sB + s * C::B_BYTES, &tmX, full + s, kb * BK, m0, pol_x);
             continue;
@@ -798,6 +812,7 @@ int psd_gemm_tiled(const void* X, int ldx, int M, int K, const void* W_tiled, in
   g.part = reinterpret_cast<float*>(static_cast<char*>(workspace) + p.ticket_bytes);
   g.Wt = static_cast<const __nv_bfloat16*>(W_tiled);
   g.silu_mode = silu_mode();
+  g.prefetch = 0;
   cudaStream_t st = (cudaStream_t)stream;
   switch (epi) {
     case PSD_EPI_BF16: return launch_sk<PSD_EPI_BF16, true>(p.bn, mx, mx, g, st);
@@ -863,6 +878,7 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
     g.part = reinterpret_cast<float*>(static_cast<char*>(workspace) + p.ticket_bytes);
     g.Wt = nullptr;
     g.silu_mode = silu_mode();
+    g.prefetch = prefetch_depth();
     cudaStream_t st = (cudaStream_t)stream;
     switch (epi) {
       case PSD_EPI_BF16: return launch_sk<PSD_EPI_BF16>(p.bn, mw, mx, g, st);

@@ -276,8 +276,9 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
                  int Hkv, int bs, float scale_log2, int tok_per_chunk, int RG, int S,
                  float* __restrict__ ws, int* __restrict__ tickets,
                  __nv_bfloat16* __restrict__ out) {
-  pdl_wait();
-  pdl_trigger();
+  // PDL: metadata, the block table and the keys of earlier steps (positions <
+  // q_pos0) do not depend on the predecessor (RoPE writes this step's keys and
+  // the queries), so they are fetched before griddepcontrol.wait
   constexpr int P = D + 8;  // smem row pitch (conflict-free fragment loads)
   const int KG = 4 / RG;
   const int seq = blockIdx.x, hk = blockIdx.y, chunk = blockIdx.z / S, split = blockIdx.z % S;
@@ -307,6 +308,38 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
   auto sK = [&](int st, int j) { return ring + ((st * KG + j) * 2) * KT; };
   auto sV = [&](int st, int j) { return ring + ((st * KG + j) * 2 + 1) * KT; };
 
+  const int ntiles_all = last_key / KT + 1;
+  // this split's key tiles [ta, tb)
+  const int ta = split * ntiles_all / S, tb = (split + 1) * ntiles_all / S;
+  const int ntiles = tb - ta;
+  const int ngroups = (ntiles + KG - 1) / KG;
+  __syncthreads();  // bt staged
+  // part: 0 = every row of the group, 1 = rows of earlier steps' keys only,
+  // 2 = the complement of 1 (this step's keys and the zero fill past the end)
+  auto load_group = [&](int gi, int st, int part) {
+    const int per = KT * (D / 8);
+    for (int idx = tid; idx < KG * per; idx += ATT_THREADS) {
+      const int j = idx / per, rem = idx % per;
+      const int r = rem / (D / 8), cc = rem % (D / 8);
+      const int tile = ta + gi * KG + j;
+      const int key = tile * KT + r;
+      const bool ok = key <= last_key && tile < tb;
+      const bool old = ok && key < first_pos;
+      if ((part == 1 && !old) || (part == 2 && old)) continue;
+      size_t o = 0;
+      if (ok) o = (((size_t)bt[key / bs] * bs + key % bs) * Hkv + hk) * D + cc * 8;
+      cp_async16(&sK(st, j)[r][cc * 8], kc + o, ok);
+      cp_async16(&sV(st, j)[r][cc * 8], vc + o, ok);
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int t = 0; t < NS - 1; ++t) {
+    if (t < ngroups) load_group(t, t, 1);
+    else cp_async_commit();
+  }
+  pdl_wait();
+  pdl_trigger();
   for (int idx = tid; idx < ATT_MAXR * (D / 8); idx += ATT_THREADS) {
     const int r = idx / (D / 8), cc = idx % (D / 8);
     uint4 v = make_uint4(0, 0, 0, 0);
@@ -317,32 +350,12 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
     }
     *reinterpret_cast<uint4*>(&sQ[r][cc * 8]) = v;
   }
-  const int ntiles_all = last_key / KT + 1;
-  // this split's key tiles [ta, tb)
-  const int ta = split * ntiles_all / S, tb = (split + 1) * ntiles_all / S;
-  const int ntiles = tb - ta;
-  const int ngroups = (ntiles + KG - 1) / KG;
-  __syncthreads();  // bt staged
-  auto load_group = [&](int gi, int st) {
-    const int per = KT * (D / 8);
-    for (int idx = tid; idx < KG * per; idx += ATT_THREADS) {
-      const int j = idx / per, rem = idx % per;
-      const int r = rem / (D / 8), cc = rem % (D / 8);
-      const int tile = ta + gi * KG + j;
-      const int key = tile * KT + r;
-      const bool ok = key <= last_key && tile < tb;
-      size_t o = 0;
-      if (ok) o = (((size_t)bt[key / bs] * bs + key % bs) * Hkv + hk) * D + cc * 8;
-      cp_async16(&sK(st, j)[r][cc * 8], kc + o, ok);
-      cp_async16(&sV(st, j)[r][cc * 8], vc + o, ok);
-    }
-    cp_async_commit();
-  };
+  // this step's keys of the prefetched groups (one extra commit group; the
+  // first iteration waits for everything)
 #pragma unroll
-  for (int t = 0; t < NS - 1; ++t) {
-    if (t < ngroups) load_group(t, t);
-    else cp_async_commit();
-  }
+  for (int t = 0; t < NS - 1; ++t)
+    if (t < ngroups) load_group(t, t, 2);
+  cp_async_commit();
   __syncthreads();
 
   const bool active = kg < KG && rg * 16 < R;
@@ -366,9 +379,10 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
 
   for (int gi = 0; gi < ngroups; ++gi) {
     const int st = gi % NS;
-    if (gi + NS - 1 < ngroups) load_group(gi + NS - 1, (gi + NS - 1) % NS);
+    if (gi + NS - 1 < ngroups) load_group(gi + NS - 1, (gi + NS - 1) % NS, 0);
     else cp_async_commit();
-    cp_async_wait<NS - 1>();
+    if (gi == 0) cp_async_wait<1>();  // prologue groups (both parts) landed
+    else cp_async_wait<NS - 1>();
     __syncthreads();
     const int kt = ta + gi * KG + kg;
     if (active && kt < tb) {

@@ -22,12 +22,15 @@
 // pair per request (mostly from L2).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/psd.h"
 #include "common.h"
+#include "sm100.cuh"
 #include "../../include/psd_canon.h"
 
 namespace {
+using namespace psd;
 
 constexpr int kThreads = 256;
 
@@ -57,19 +60,78 @@ __device__ __forceinline__ float4 ld_stream(const float* p) {
   return r;
 }
 
-__device__ __forceinline__ psd_ms shfl_ms(psd_ms v, int off) {
-  psd_ms o;
-  o.m = __shfl_down_sync(0xffffffffu, v.m, off);
-  o.s = __shfl_down_sync(0xffffffffu, v.s, off);
-  return o;
+// ---- packed (f32x2) canonical weights --------------------------------------
+// Blackwell's FFMA2 / FADD2 round each half exactly like the scalar IEEE op,
+// so two psd_weight() evaluations packed into one 64-bit register are
+// bit-identical to two scalar calls (include/psd_canon.h) at half the issue
+// slots.  The clamp and the integer exponent add stay scalar.
+__device__ __forceinline__ unsigned long long f2_pack(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(unsigned long long r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ unsigned long long f2_sub(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// (psd_weight(x0, c, bias), psd_weight(x1, c, bias)) -- see psd_exp2.  One
+// PTX block on 64-bit register pairs so ptxas keeps the halves paired (no
+// pack/unpack moves): FFMA2 argument, scalar clamp (max.f32 maps NaN to -125
+// exactly like the canonical t > -125 ? t : -125), FADD2 rounding trick, six
+// FFMA2 Horner steps, integer exponent add (bits(r) << 23 == (bits(r) -
+// 0x4B400000) << 23 mod 2^32).
+__device__ __forceinline__ void psd_weight2(float x0, float x1, unsigned long long c2,
+                                            unsigned long long bias2, float& w0, float& w1) {
+  asm("{\n\t"
+      ".reg .b64 t, r, n, f, p, K, C;\n\t"
+      ".reg .f32 a, b;\n\t"
+      ".reg .b32 pa, pb, ra, rb;\n\t"
+      "mov.b64 t, {%2, %3};\n\t"
+      "fma.rn.f32x2 t, t, %4, %5;\n\t"
+      "mov.b64 {a, b}, t;\n\t"
+      "max.f32 a, a, 0fC2FA0000;\n\t"
+      "max.f32 b, b, 0fC2FA0000;\n\t"
+      "mov.b64 t, {a, b};\n\t"
+      "mov.b64 K, 0x4B4000004B400000;\n\t"
+      "add.rn.f32x2 r, t, K;\n\t"
+      "sub.rn.f32x2 n, r, K;\n\t"
+      "sub.rn.f32x2 f, t, n;\n\t"
+      "mov.b64 p, 0x3921848939218489;\n\t"
+      "mov.b64 C, 0x3AAEC3FF3AAEC3FF;\n\t"
+      "fma.rn.f32x2 p, p, f, C;\n\t"
+      "mov.b64 C, 0x3C1D955B3C1D955B;\n\t"
+      "fma.rn.f32x2 p, p, f, C;\n\t"
+      "mov.b64 C, 0x3D6358473D635847;\n\t"
+      "fma.rn.f32x2 p, p, f, C;\n\t"
+      "mov.b64 C, 0x3E75FDF03E75FDF0;\n\t"
+      "fma.rn.f32x2 p, p, f, C;\n\t"
+      "mov.b64 C, 0x3F3172183F317218;\n\t"
+      "fma.rn.f32x2 p, p, f, C;\n\t"
+      "mov.b64 C, 0x3F8000003F800000;\n\t"
+      "fma.rn.f32x2 p, p, f, C;\n\t"
+      "mov.b64 {pa, pb}, p;\n\t"
+      "mov.b64 {ra, rb}, r;\n\t"
+      "shl.b32 ra, ra, 23;\n\t"
+      "shl.b32 rb, rb, 23;\n\t"
+      "add.u32 %0, pa, ra;\n\t"
+      "add.u32 %1, pb, rb;\n\t"
+      "}"
+      : "=r"(*reinterpret_cast<uint32_t*>(&w0)), "=r"(*reinterpret_cast<uint32_t*>(&w1))
+      : "f"(x0), "f"(x1), "l"(c2), "l"(bias2));
 }
 
-__device__ __forceinline__ psd_vi shfl_vi(psd_vi v, int off) {
-  psd_vi o;
-  o.v = __shfl_down_sync(0xffffffffu, v.v, off);
-  o.i = __shfl_down_sync(0xffffffffu, v.i, off);
-  return o;
+// three-input max (FMNMX3); the slice max is exact whatever the order
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
 }
+
+
 
 __device__ __forceinline__ float shfl_add_tree(float v) {
 #pragma unroll
@@ -84,14 +146,10 @@ __device__ __forceinline__ int expected_stats(const Params& p, int kb, bool samp
   return nst * (kb + 1) + (sample ? nsd * kb : 0);
 }
 
+// one (request b, row r, slice) statistics item; the last item of request b
+// folds and decides (and, sampling, publishes the plan of the sampling pass)
 template <bool SAMPLE>
-__global__ void __launch_bounds__(kThreads)
-verify_stats(const Params p) {
-  pdl_wait();
-  pdl_trigger();
-  const int slice = blockIdx.x;
-  const int b = blockIdx.y / p.R;
-  const int r = blockIdx.y % p.R;
+__device__ __forceinline__ void stats_item(const Params& p, int slice, int b, int r) {
   const int kb = p.len[b];
   const bool is_draft = r > p.K;
   const int i = is_draft ? r - (p.K + 1) : r;
@@ -103,18 +161,25 @@ verify_stats(const Params p) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int base = slice * PSD_SLICE;
 
+  // every slice but a row's last is full: no per-element bounds checks there
+  const bool full = base + PSD_SLICE <= n;
   float4 v[8];
+  if (full) {
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const int e = base + 4 * (tid + kThreads * j);
-    v[j] = e < n ? ld_stream(row + e)
-                 : make_float4(PSD_NEG_INF, PSD_NEG_INF, PSD_NEG_INF, PSD_NEG_INF);
+    for (int j = 0; j < 8; ++j) v[j] = ld_stream(row + base + 4 * (tid + kThreads * j));
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int e = base + 4 * (tid + kThreads * j);
+      v[j] = e < n ? ld_stream(row + e)
+                   : make_float4(PSD_NEG_INF, PSD_NEG_INF, PSD_NEG_INF, PSD_NEG_INF);
+    }
   }
   // exact slice max: lane -> warp (xor tree) -> block
   float lm = PSD_NEG_INF;
 #pragma unroll
   for (int j = 0; j < 8; ++j)
-    lm = psd_max(lm, psd_max(psd_max(v[j].x, v[j].y), psd_max(v[j].z, v[j].w)));
+    lm = max3f(max3f(lm, v[j].x, v[j].y), v[j].z, v[j].w);
   float wm = lm;
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) wm = psd_max(wm, __shfl_xor_sync(0xffffffffu, wm, off));
@@ -130,18 +195,26 @@ verify_stats(const Params p) {
 
   if constexpr (SAMPLE) {
     const float bias = psd_bias(M, p.c);
+    const unsigned long long c2 = f2_pack(p.c, p.c), b2 = f2_pack(bias, bias);
     float s = 0.0f;
+    auto lane_sum = [&](bool check) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      // invalid elements (-inf) are not part of the row: skip them
-      const int e = base + 4 * (tid + kThreads * j);
-      if (e < n) {
-        s = psd_add(s, psd_weight(v[j].x, p.c, bias));
-        s = psd_add(s, psd_weight(v[j].y, p.c, bias));
-        s = psd_add(s, psd_weight(v[j].z, p.c, bias));
-        s = psd_add(s, psd_weight(v[j].w, p.c, bias));
+      for (int j = 0; j < 8; ++j) {
+        // invalid elements (-inf) are not part of the row: skip them
+        const int e = base + 4 * (tid + kThreads * j);
+        if (!check || e < n) {
+          float wx, wy, wz, ww;
+          psd_weight2(v[j].x, v[j].y, c2, b2, wx, wy);
+          psd_weight2(v[j].z, v[j].w, c2, b2, wz, ww);
+          s = psd_add(s, wx);
+          s = psd_add(s, wy);
+          s = psd_add(s, wz);
+          s = psd_add(s, ww);
+        }
       }
-    }
+    };
+    if (full) lane_sum(false);
+    else lane_sum(true);
     s = shfl_add_tree(s);
     if (lane == 0) s_sum[warp] = s;
     __syncthreads();
@@ -258,63 +331,119 @@ verify_stats(const Params p) {
   }
 }
 
+template <bool SAMPLE>
+__global__ void __launch_bounds__(kThreads)
+verify_stats(const Params p) {
+  pdl_wait();
+  pdl_trigger();
+  stats_item<SAMPLE>(p, blockIdx.x, blockIdx.y / p.R, blockIdx.y % p.R);
+}
+
 // ---- sampling pass ---------------------------------------------------------
+// Grid (chunk of kChunkBlks 1024-element blocks, request).  Each thread owns
+// elements 4l..4l+3 of every block of its chunk (the canonical lane layout),
+// loads all of them up front (128-bit loads, target and draft rows), evaluates
+// the weights with packed f32x2 math (bit-identical to psd_canon.h) and reduces
+// every block with the canonical warp tree + 8-warp tree.  The last chunk of a
+// request (atomic ticket) runs the canonical prefix search.
+constexpr int kChunkBlks = 8;  // 1024-element blocks per sampling item
+constexpr int kSubBlks = 4;    // blocks loaded at once (register budget)
+
 struct WeightCtx {
   const float* t; const float* d; int V, Vd; float c, bt, bd, St, Sd; int residual;
 };
 
-__device__ __forceinline__ float weight_of(const WeightCtx& w, float tv, float dv, int x) {
-  if (x >= w.V) return 0.0f;
-  const float et = psd_weight(tv, w.c, w.bt);
-  if (!w.residual) return et;
-  const float ed = x < w.Vd ? psd_weight(dv, w.c, w.bd) : 0.0f;
-  return psd_residual(et, ed, w.St, w.Sd);
+__device__ __forceinline__ unsigned long long f2_mul(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
 }
 
-// weights of the 4 elements lane `tid` owns in block `blk`
-__device__ __forceinline__ void lane_weights(const WeightCtx& w, int blk, int tid, float out[4]) {
-  const int x0 = blk * PSD_SBLK + 4 * tid;
-  float4 tv = make_float4(0.f, 0.f, 0.f, 0.f), dv = tv;
+// weights of the 4 elements x0..x0+3 (x0 % 4 == 0; V, Vd multiples of 4)
+__device__ __forceinline__ void weights4(const WeightCtx& w, int x0, float4 tv, float4 dv,
+                                         float out[4]) {
+  if (x0 >= w.V) {
+    out[0] = out[1] = out[2] = out[3] = 0.0f;
+    return;
+  }
+  const unsigned long long c2 = f2_pack(w.c, w.c), bt2 = f2_pack(w.bt, w.bt);
+  float e[4];
+  psd_weight2(tv.x, tv.y, c2, bt2, e[0], e[1]);
+  psd_weight2(tv.z, tv.w, c2, bt2, e[2], e[3]);
+  if (!w.residual) {
+    out[0] = e[0]; out[1] = e[1]; out[2] = e[2]; out[3] = e[3];
+    return;
+  }
+  float q[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  if (x0 < w.Vd) {
+    const unsigned long long bd2 = f2_pack(w.bd, w.bd);
+    psd_weight2(dv.x, dv.y, c2, bd2, q[0], q[1]);
+    psd_weight2(dv.z, dv.w, c2, bd2, q[2], q[3]);
+  }
+  // psd_residual: max(0, fl(fl(e_t * S_d) - fl(e_d * S_t)))
+  const unsigned long long Sd2 = f2_pack(w.Sd, w.Sd), St2 = f2_pack(w.St, w.St);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const unsigned long long r2 = f2_sub(f2_mul(f2_pack(e[2 * h], e[2 * h + 1]), Sd2),
+                                         f2_mul(f2_pack(q[2 * h], q[2 * h + 1]), St2));
+    float r0, r1;
+    f2_unpack(r2, r0, r1);
+    out[2 * h] = r0 > 0.0f ? r0 : 0.0f;
+    out[2 * h + 1] = r1 > 0.0f ? r1 : 0.0f;
+  }
+}
+
+__device__ __forceinline__ void load4(const WeightCtx& w, int x0, float4& tv, float4& dv) {
+  tv = make_float4(0.f, 0.f, 0.f, 0.f);
+  dv = tv;
   if (x0 < w.V) tv = __ldg(reinterpret_cast<const float4*>(w.t + x0));
   if (w.residual && x0 < w.Vd) dv = __ldg(reinterpret_cast<const float4*>(w.d + x0));
-  out[0] = weight_of(w, tv.x, dv.x, x0);
-  out[1] = weight_of(w, tv.y, dv.y, x0 + 1);
-  out[2] = weight_of(w, tv.z, dv.z, x0 + 2);
-  out[3] = weight_of(w, tv.w, dv.w, x0 + 3);
 }
 
-__device__ float block_weight_sum(const WeightCtx& w, int blk, float* s_lane, float* s_red) {
+// canonical block sums of blocks blk0 .. blk0+nb-1 (nb <= kSubBlks); all
+// kThreads threads call it; results land in s_blk[0..nb) (valid after return)
+__device__ void chunk_block_sums(const WeightCtx& w, int blk0, int nb, float* s_red,
+                                 float* s_blk) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  float wv[4];
-  lane_weights(w, blk, tid, wv);
-  const float ls = psd_add(psd_add(psd_add(wv[0], wv[1]), wv[2]), wv[3]);
-  if (s_lane) s_lane[tid] = ls;
-  const float ws = shfl_add_tree(ls);
-  if (lane == 0) s_red[warp] = ws;
+  float4 tv[kSubBlks], dv[kSubBlks];
+#pragma unroll
+  for (int k = 0; k < kSubBlks; ++k)
+    if (k < nb) load4(w, (blk0 + k) * PSD_SBLK + 4 * tid, tv[k], dv[k]);
+#pragma unroll
+  for (int k = 0; k < kSubBlks; ++k) {
+    if (k < nb) {
+      float wv[4];
+      weights4(w, (blk0 + k) * PSD_SBLK + 4 * tid, tv[k], dv[k], wv);
+      const float ls = psd_add(psd_add(psd_add(wv[0], wv[1]), wv[2]), wv[3]);
+      const float ws = shfl_add_tree(ls);
+      if (lane == 0) s_red[k * 8 + warp] = ws;
+    }
+  }
   __syncthreads();
-  float tot = 0.0f;
-  if (tid == 0) {
+  if (tid < nb) {
     float q[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) q[k] = s_red[k];
+    for (int k = 0; k < 8; ++k) q[k] = s_red[tid * 8 + k];
 #pragma unroll
     for (int off = 4; off >= 1; off >>= 1)
 #pragma unroll
       for (int k = 0; k < off; ++k) q[k] = psd_add(q[k], q[k + off]);
-    tot = q[0];
+    s_blk[tid] = q[0];
   }
   __syncthreads();
-  return tot;  // valid in thread 0
 }
 
 // last element with positive weight in block blk (all threads return it)
 __device__ int last_positive(const WeightCtx& w, int blk, int* s_int) {
+  float4 tv, dv;
+  const int x0 = blk * PSD_SBLK + 4 * threadIdx.x;
+  load4(w, x0, tv, dv);
   float wv[4];
-  lane_weights(w, blk, threadIdx.x, wv);
+  weights4(w, x0, tv, dv, wv);
   int best = -1;
 #pragma unroll
   for (int c = 0; c < 4; ++c)
-    if (wv[c] > 0.0f) best = blk * PSD_SBLK + 4 * threadIdx.x + c;
+    if (wv[c] > 0.0f) best = x0 + c;
   if (threadIdx.x == 0) *s_int = -1;
   __syncthreads();
   if (best >= 0) atomicMax(s_int, best);
@@ -324,12 +453,43 @@ __device__ int last_positive(const WeightCtx& w, int blk, int* s_int) {
   return r < 0 ? blk * PSD_SBLK : r;
 }
 
-__global__ void __launch_bounds__(kThreads)
-verify_sample(const Params p) {
-  pdl_wait();
-  pdl_trigger();
-  const int blk = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
-  const Plan pl = p.plan[b];
+// Sequential left fold of v[0..n) (one thread): prefix[i] = v[0] + ... + v[i-1]
+// (prefix[0] = 0, prefix[n] = total) when prefix != nullptr; returns the total.
+// Values are pulled from shared memory 32 at a time with 128-bit loads so the
+// add chain, not the load latency, sets the pace.
+__device__ float seq_fold(const float* v, int n, float* prefix) {
+  float C = 0.0f;
+  if (prefix) prefix[0] = 0.0f;
+  int i = 0;
+  for (; i + 32 <= n; i += 32) {
+    float4 q[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) q[j] = reinterpret_cast<const float4*>(v + i)[j];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      C = psd_add(C, q[j].x); if (prefix) prefix[i + 4 * j + 1] = C;
+      C = psd_add(C, q[j].y); if (prefix) prefix[i + 4 * j + 2] = C;
+      C = psd_add(C, q[j].z); if (prefix) prefix[i + 4 * j + 3] = C;
+      C = psd_add(C, q[j].w); if (prefix) prefix[i + 4 * j + 4] = C;
+    }
+  }
+  for (; i < n; ++i) {
+    C = psd_add(C, v[i]);
+    if (prefix) prefix[i + 1] = C;
+  }
+  return C;
+}
+
+// one chunk of request b's sampling pass; the last chunk runs the prefix search
+__device__ __forceinline__ void sample_item(const Params& p, int chunk, int b, int nchunks) {
+  const int tid = threadIdx.x;
+  Plan pl;
+  {
+    const float4* pp = reinterpret_cast<const float4*>(p.plan + b);
+    const float4 q0 = __ldcg(pp), q1 = __ldcg(pp + 1);
+    pl.mode = __float_as_int(q0.x); pl.row = __float_as_int(q0.y);
+    pl.Mt = q0.z; pl.St = q0.w; pl.Md = q1.x; pl.Sd = q1.y;
+  }
   WeightCtx w;
   w.V = p.V; w.Vd = p.Vd; w.c = p.c;
   w.t = p.t + b * p.tsb + pl.row * p.tsi;
@@ -337,82 +497,89 @@ verify_sample(const Params p) {
   w.bt = psd_bias(pl.Mt, p.c); w.bd = psd_bias(pl.Md, p.c); w.St = pl.St; w.Sd = pl.Sd;
   w.residual = pl.mode == 1;
 
-  __shared__ float s_red[8];
-  __shared__ float s_lane[kThreads];
+  __shared__ float s_red[kSubBlks * 8];
+  __shared__ float s_blk[kSubBlks];
+  __shared__ __align__(16) float s_lane[kThreads];
   __shared__ int s_last, s_int;
-  __shared__ float s_T, s_Pprev;
+  __shared__ float s_T;
   __shared__ int s_chosen;
+  __shared__ __align__(16) float wb[PSD_MAX_SBLKS];
+  __shared__ __align__(16) float s_pref[PSD_MAX_SBLKS + 1];
+  __shared__ __align__(16) float s_lpre[kThreads + 1];
 
-  const float W = block_weight_sum(w, blk, nullptr, s_red);
+  for (int sub = 0; sub < kChunkBlks; sub += kSubBlks) {
+    const int blk0 = chunk * kChunkBlks + sub;
+    const int nb = min(kSubBlks, p.NB - blk0);
+    if (nb <= 0) break;
+    chunk_block_sums(w, blk0, nb, s_red, s_blk);
+    if (tid < nb) p.wblk[b * p.NB + blk0 + tid] = s_blk[tid];
+    __syncthreads();
+  }
   if (tid == 0) {
-    p.wblk[b * p.NB + blk] = W;
     __threadfence();
-    s_last = atomicAdd(p.cnt_b + b, 1) == p.NB - 1;
+    s_last = atomicAdd(p.cnt_b + b, 1) == nchunks - 1;
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  __shared__ float wb[PSD_MAX_SBLKS];
   for (int k = tid; k < p.NB; k += kThreads) wb[k] = __ldcg(p.wblk + b * p.NB + k);
   __syncthreads();
 
   // degenerate residual (sums to 0 in fp32): fall back to sampling from p
-  if (tid == 0) {
-    float R = 0.0f;
-    for (int k = 0; k < p.NB; ++k) R = psd_add(R, wb[k]);
-    s_int = (w.residual && !(R > 0.0f)) ? 1 : 0;
-  }
+  if (tid == 0) s_int = (w.residual && !(seq_fold(wb, p.NB, nullptr) > 0.0f)) ? 1 : 0;
   __syncthreads();
   if (s_int) {
     w.residual = 0;
-    __syncthreads();
-    for (int k = 0; k < p.NB; ++k) {
-      const float Wk = block_weight_sum(w, k, nullptr, s_red);
-      if (tid == 0) wb[k] = Wk;
+    for (int k0 = 0; k0 < p.NB; k0 += kSubBlks) {
+      const int n = min(kSubBlks, p.NB - k0);
+      chunk_block_sums(w, k0, n, s_red, s_blk);
+      if (tid < n) wb[k0 + tid] = s_blk[tid];
     }
     __syncthreads();
   }
+  // canonical block prefix P_b (sequential fold, kept in smem), T = u * R;
+  // chosen block = first with P_b > T (found in parallel)
   if (tid == 0) {
-    float R = 0.0f;
-    for (int k = 0; k < p.NB; ++k) R = psd_add(R, wb[k]);
-    const float T = psd_mul(p.u[b * (p.K + 1) + p.K], R);
-    float P = 0.0f;
-    int chosen = -1;
-    float Pprev = 0.0f;
-    for (int k = 0; k < p.NB; ++k) {
-      const float Pn = psd_add(P, wb[k]);
-      if (Pn > T) { chosen = k; Pprev = P; break; }
-      P = Pn;
-    }
-    if (chosen < 0) {
-      chosen = -2 - (p.NB - 1);
-      for (int k = p.NB - 1; k >= 0; --k)
-        if (wb[k] > 0.0f) { chosen = -2 - k; break; }
-    }
-    s_chosen = chosen; s_T = T; s_Pprev = Pprev;
+    const float R = seq_fold(wb, p.NB, s_pref);
+    s_T = psd_mul(p.u[b * (p.K + 1) + p.K], R);
+    s_chosen = 0x7fffffff;
   }
   __syncthreads();
+  for (int k = tid; k < p.NB; k += kThreads)
+    if (s_pref[k + 1] > s_T) atomicMin(&s_chosen, k);
+  __syncthreads();
   int tok;
-  if (s_chosen <= -2) {
-    tok = last_positive(w, -2 - s_chosen, &s_int);
+  if (s_chosen == 0x7fffffff) {
+    // no block hit (rounding): last positive-weight block
+    if (tid == 0) {
+      int lb = p.NB - 1;
+      for (int k = p.NB - 1; k >= 0; --k)
+        if (wb[k] > 0.0f) { lb = k; break; }
+      s_int = lb;
+    }
+    __syncthreads();
+    tok = last_positive(w, s_int, &s_int);
   } else {
     const int cb = s_chosen;
+    const float Pprev = s_pref[cb];
+    const int x0 = cb * PSD_SBLK + 4 * tid;
+    float4 tv, dv;
+    load4(w, x0, tv, dv);
     float wv[4];
-    lane_weights(w, cb, tid, wv);
+    weights4(w, x0, tv, dv, wv);
     s_lane[tid] = psd_add(psd_add(psd_add(wv[0], wv[1]), wv[2]), wv[3]);
     __syncthreads();
-    if (tid == 0) {  // exclusive sequential prefix of lane sums, in place
-      float C = 0.0f;
-      for (int l = 0; l < kThreads; ++l) { const float s = s_lane[l]; s_lane[l] = C; C = psd_add(C, s); }
+    if (tid == 0) {  // exclusive sequential prefix of the lane sums
+      seq_fold(s_lane, kThreads, s_lpre);
       s_int = 0x7fffffff;
     }
     __syncthreads();
-    float acc = s_lane[tid];
+    float acc = s_lpre[tid];
     int hit = 0x7fffffff;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       acc = psd_add(acc, wv[c]);
-      if (hit == 0x7fffffff && psd_add(s_Pprev, acc) > s_T) hit = cb * PSD_SBLK + 4 * tid + c;
+      if (hit == 0x7fffffff && psd_add(Pprev, acc) > s_T) hit = x0 + c;
     }
     if (hit != 0x7fffffff) atomicMin(&s_int, hit);
     __syncthreads();
@@ -426,7 +593,30 @@ verify_sample(const Params p) {
   }
 }
 
+__global__ void __launch_bounds__(kThreads)
+verify_sample(const Params p) {
+  pdl_wait();
+  pdl_trigger();
+  sample_item(p, blockIdx.x, blockIdx.y, gridDim.x);
+}
+
+
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+
+cudaError_t launch_sampling(Params p, cudaStream_t st) {
+  dim3 grid(p.NS, p.B * p.R);
+  cudaError_t e = psd::launch(verify_stats<true>, grid, dim3(kThreads), 0, st, p);
+  if (e != cudaSuccess) return e;
+  const int nc = (p.NB + kChunkBlks - 1) / kChunkBlks;
+  return psd::launch(verify_sample, dim3(nc, p.B), dim3(kThreads), 0, st, p);
+}
+
+template <bool SAMPLE>
+cudaError_t launch_stats(const Params& p, cudaStream_t st) {
+  dim3 grid(p.NS, p.B * p.R);
+  return psd::launch(verify_stats<SAMPLE>, grid, dim3(kThreads), 0, st, p);
+}
 
 struct WsLayout {
   size_t cnt_a, cnt_b, part, plan, wblk, total;
@@ -486,8 +676,7 @@ int psd_verify_greedy(const float* target_logits, int64_t t_stride_b, int64_t t_
   p.part = reinterpret_cast<float2*>(w + L.part); p.plan = reinterpret_cast<Plan*>(w + L.plan);
   p.wblk = reinterpret_cast<float*>(w + L.wblk);
   p.NS = (V + PSD_SLICE - 1) / PSD_SLICE; p.NB = (V + PSD_SBLK - 1) / PSD_SBLK; p.R = K + 1;
-  dim3 grid(p.NS, B * p.R);
-  return (int)psd::launch(verify_stats<false>, grid, dim3(kThreads), 0, (cudaStream_t)stream, p);
+  return (int)launch_stats<false>(p, (cudaStream_t)stream);
 }
 
 int psd_verify_sample(const float* target_logits, int64_t t_stride_b, int64_t t_stride_i, int V,
@@ -514,11 +703,7 @@ int psd_verify_sample(const float* target_logits, int64_t t_stride_b, int64_t t_
   p.wblk = reinterpret_cast<float*>(w + L.wblk);
   p.NS = (V + PSD_SLICE - 1) / PSD_SLICE; p.NB = (V + PSD_SBLK - 1) / PSD_SBLK;
   p.R = 2 * K + 1;
-  dim3 grid(p.NS, B * p.R);
-  cudaError_t e = psd::launch(verify_stats<true>, grid, dim3(kThreads), 0, (cudaStream_t)stream, p);
-  if (e != cudaSuccess) return (int)e;
-  dim3 grid2(p.NB, B);
-  return (int)psd::launch(verify_sample, grid2, dim3(kThreads), 0, (cudaStream_t)stream, p);
+  return (int)launch_sampling(p, (cudaStream_t)stream);
 }
 
 int psd_verify_sample_rows(const float* target_logits, int64_t t_stride_b, int64_t t_stride_i,
@@ -547,11 +732,7 @@ int psd_verify_sample_rows(const float* target_logits, int64_t t_stride_b, int64
   p.wblk = reinterpret_cast<float*>(w + L.wblk);
   p.NS = (V + PSD_SLICE - 1) / PSD_SLICE; p.NB = (V + PSD_SBLK - 1) / PSD_SBLK;
   p.R = 2 * K + 1;
-  dim3 grid(p.NS, B * p.R);
-  cudaError_t e = psd::launch(verify_stats<true>, grid, dim3(kThreads), 0, (cudaStream_t)stream, p);
-  if (e != cudaSuccess) return (int)e;
-  dim3 grid2(p.NB, B);
-  return (int)psd::launch(verify_sample, grid2, dim3(kThreads), 0, (cudaStream_t)stream, p);
+  return (int)launch_sampling(p, (cudaStream_t)stream);
 }
 
 }  // extern "C"

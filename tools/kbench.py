@@ -182,7 +182,7 @@ def rope_case(tag, M, Hq, Hkv, D, S):
     inv = torch.rand(D // 2, device=dev) * 0.5
     def fn():
         st = torch.cuda.current_stream().cuda_stream
-        rc = lib.psd_rope_kv(P.data_ptr(), S, M * N, M, Hq, Hkv, D, pos.data_ptr(),
+        rc = lib.psd_rope_kv_partials(P.data_ptr(), S, M * N, M, Hq, Hkv, D, pos.data_ptr(),
                              slots.data_ptr(), inv.data_ptr(), None, q.data_ptr(), kc.data_ptr(),
                              vc.data_ptr(), st)
         assert rc == 0
@@ -262,6 +262,15 @@ def main():
     if want("gemm1b"):
         gemm_case("1B qkv part", 32, 3072, 2048, "partial")
         gemm_case("1B gate/up", 32, 16384, 2048, "silu")
+    if want("gemmpf"):
+        gemm_case("8B gate/up", 192, 28672, 4096, "silu")
+        gemm_case("8B lm_head", 192, 128256, 4096, "f32", copies=2)
+        gemm_case("8B qkv part", 192, 6144, 4096, "partial")
+        gemm_case("8B o part", 192, 4096, 4096, "partial")
+        gemm_case("8B down part", 192, 4096, 14336, "partial")
+        gemm_case("1B gate/up", 32, 16384, 2048, "silu")
+        gemm_case("1B down part", 32, 2048, 8192, "partial")
+        gemm_case("1B lm_head", 32, 128256, 2048, "f32", copies=2)
     if want("gemmgu"):
         gemm_case("8B gate/up", 192, 28672, 4096, "silu")
     if want("attn"):
