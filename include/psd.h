@@ -176,6 +176,41 @@ long long psd_launch_count(void);
 /* deterministic random init: (u - 1/2) * span, u = splitmix64(seed, i) >> 40 / 2^24 */
 int psd_fill_uniform_bf16(void* out, size_t n, uint64_t seed, float span, void* stream);
 
+/* ---- fused k-step greedy draft decode (csrc/decode_mk.cu) -------------------
+ * One persistent kernel runs all k draft steps of a batch (embedding, every
+ * layer, LM head, argmax, scatter of the draft token into slot_tok).  The
+ * model and the forward buffers are bound once; psd_mk_launch enqueues one
+ * launch (graph-capturable once a (nb, steps) program was built eagerly).
+ * Replaces the per-kernel draft forward of model.py for head_dim 32/64, greedy. */
+typedef struct {
+  int layers, hidden, heads, kv_heads, head_dim, ffn /* padded to 64 */, vocab;
+  float eps, attn_scale, beta;
+  int block_size, max_blocks, grid /* 0 = all SMs */, max_tokens;
+  /* 9 per layer: wqkv, wo, wgu (packed), wdown, attn_norm, mlp_norm, bqkv|NULL, k cache, v cache */
+  const void* const* layer_ptrs;
+  const void* embed;
+  const void* lm_head;
+  const void* final_norm;
+  const float* inv_freq;
+  const int32_t* successor; /* synthetic-language successor table (beta = 0: unused) */
+  const int32_t* block_table;
+  void* x; void* xn; void* attn; void* act; void* xf; /* forward buffers, >= 64 rows */
+  float* part;   /* split-K partials */
+  void* argpart; /* (vocab / 128) * 64 float2 */
+  int32_t* slot_tok;
+  int32_t* meta; int set_stride; int field_offsets[11];
+} psd_mk_model;
+size_t psd_mk_smem_bytes(void);
+void* psd_mk_create(const psd_mk_model* model);
+void psd_mk_destroy(void* handle);
+int psd_mk_grid(void* handle);
+int psd_mk_launch(void* handle, int nb, int steps, void* stream);
+/* Diagnostics: ops of a built (nb, steps) program (-1: not built), and a launch
+ * that records per-CTA per-op %globaltimer stamps (entry, inputs ready, done)
+ * into trace[grid][n_ops][3] (u64). */
+int psd_mk_n_ops(void* handle, int nb, int steps);
+int psd_mk_launch_traced(void* handle, int nb, int steps, void* trace, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -59,7 +59,8 @@ class GpuBackend:
                  device: str | torch.device = "cuda:0", dual_stream: bool = True,
                  block_size: int = 16, num_blocks: int | None = None,
                  prefill_chunk_tokens: int = 4096, use_graphs: bool = True,
-                 roles: tuple = ("target", "draft")) -> None:
+                 roles: tuple = ("target", "draft"), fused_draft: bool | None = None,
+                 mk_grid: int = 0) -> None:
         if not torch.cuda.is_available():
             raise native.NativeError("GpuBackend needs a CUDA device (no CPU fallback)")
         native.load()
@@ -152,9 +153,26 @@ class GpuBackend:
             self.d_acc = torch.empty(B, dtype=i32, device=dev)
             self.d_len0 = torch.zeros(B, dtype=i32, device=dev)
             self.d_ids0 = torch.zeros(B, 0, dtype=i32, device=dev)
-            self.s_target = torch.cuda.Stream(dev)
-            self.s_draft = torch.cuda.Stream(dev) if dual_stream else self.s_target
+            # stream priorities (PSD_STREAM_PRIO=none|draft|target) measured no
+            # gain for the overlapped step (profiles/r01b_stream_priority.txt)
+            import os
+            prio = os.environ.get("PSD_STREAM_PRIO", "none")
+            hi, lo = -1, 0
+            self.s_target = torch.cuda.Stream(dev, priority=hi if prio == "target" else lo)
+            self.s_draft = (torch.cuda.Stream(dev, priority=hi if prio == "draft" else lo)
+                            if dual_stream else self.s_target)
             torch.cuda.synchronize(dev)
+        # fused k-step greedy draft decode (csrc/decode_mk.cu): one persistent
+        # kernel per draft loop instead of ~130 launches per step.
+        # PSD_FUSED_DRAFT=0 keeps the per-kernel forward (A/B runs).
+        import os
+        self.mk = None
+        want_mk = fused_draft if fused_draft is not None else \
+            os.environ.get("PSD_FUSED_DRAFT", "0") == "1"
+        if want_mk and has_d and mode == "greedy":
+            grid = mk_grid or int(os.environ.get("PSD_MK_GRID", "0"))
+            with torch.cuda.device(dev):
+                self.mk = self._make_mk(grid)
         self.seed_draft = (seed * 0x9E3779B1 + 0xD7A7) & 0xFFFFFFFFFFFF
         self.seed_verify = (seed * 0x85EBCA77 + 0x7E51) & 0xFFFFFFFFFFFF
         self.capture_verify = None  # set to a list to record K1 inputs (tests)
@@ -168,6 +186,47 @@ class GpuBackend:
         self.pending_k: dict[int, int] = {}
         self.stats = {"draft_ms": 0.0, "verify_ms": 0.0, "prefill_ms": 0.0, "steps": 0}
         self._state: EngineState | None = None
+
+    def _make_mk(self, grid: int):
+        """Bind the draft model and its forward buffers to the fused decode
+        kernel; None when the shape is outside its envelope (head_dim 32/64,
+        hidden <= 4096, <= 16 query rows per kv head)."""
+        import ctypes
+        lib = native.load()
+        m, f, s = self.draft, self.dfwd, self.dshape
+        ptrs = []
+        for li, L in enumerate(m.layers):
+            ptrs += [L["wqkv"].data_ptr(), L["wo"].data_ptr(), L["wgu"].data_ptr(),
+                     L["wdown"].data_ptr(), L["attn_norm"].data_ptr(), L["mlp_norm"].data_ptr(),
+                     L["bqkv"].data_ptr() if L["bqkv"] is not None else 0,
+                     m.kv[li, 0].data_ptr(), m.kv[li, 1].data_ptr()]
+        self._mk_ptrs = (ctypes.c_void_p * len(ptrs))(*ptrs)
+        self._mk_argpart = torch.empty(s.vocab // 128 * 64 * 2, dtype=torch.float32,
+                                       device=self.device)
+        mm = native.MkModel()
+        mm.layers, mm.hidden, mm.heads, mm.kv_heads = s.layers, s.hidden, s.heads, s.kv_heads
+        mm.head_dim, mm.ffn, mm.vocab = s.head_dim, s.ffn_padded, s.vocab
+        mm.eps, mm.attn_scale, mm.beta = s.rms_eps, 1.0 / (s.head_dim ** 0.5), self.beta_draft
+        mm.block_size, mm.max_blocks, mm.grid = self.block_size, self.max_blocks, grid
+        mm.max_tokens = f.max_tokens
+        mm.layer_ptrs = ctypes.cast(self._mk_ptrs, ctypes.c_void_p)
+        mm.embed, mm.lm_head = m.embed.data_ptr(), m.lm_head.data_ptr()
+        mm.final_norm, mm.inv_freq = m.final_norm.data_ptr(), m.inv_freq.data_ptr()
+        mm.successor, mm.block_table = self.succ_d.data_ptr(), self.block_table.data_ptr()
+        mm.x, mm.xn, mm.attn = f.x.data_ptr(), f.xn.data_ptr(), f.attn.data_ptr()
+        mm.act, mm.xf, mm.part = f.act.data_ptr(), f.xf.data_ptr(), f.part.data_ptr()
+        mm.argpart, mm.slot_tok = self._mk_argpart.data_ptr(), self.slot_tok.data_ptr()
+        mm.meta, mm.set_stride = f.meta.data_ptr(), f.set_size
+        from .model import META_FIELDS
+        for i, name in enumerate(META_FIELDS):
+            mm.field_offsets[i] = f._offsets[name][0]
+        h = lib.psd_mk_create(ctypes.byref(mm))
+        return h or None
+
+    def close(self) -> None:
+        if getattr(self, "mk", None):
+            native.load().psd_mk_destroy(self.mk)
+            self.mk = None
 
     # ------------------------------------------------------------------
     # Backend protocol
@@ -353,7 +412,8 @@ class GpuBackend:
         if not self.use_graphs:
             return
         cur = torch.cuda.current_stream(self.device)
-        cs = torch.cuda.Stream(self.device)
+        # captured kernel nodes keep the capture stream's priority
+        cs = torch.cuda.Stream(self.device, priority=cur.priority)
         self.graph_streams.append(cs)  # keep handles unique (per-stream K1 workspaces)
         cs.wait_stream(cur)
         g = torch.cuda.CUDAGraph()
@@ -442,6 +502,9 @@ class GpuBackend:
         fwd = self.dfwd
         lib = native.load()
         st = torch.cuda.current_stream(self.device).cuda_stream
+        if self.mk is not None and 2 * nb <= 64:
+            native.check(lib.psd_mk_launch(self.mk, nb, kmax, st), "fused draft decode")
+            return
         for i in range(kmax):
             M = 2 * nb if i == 0 else nb
             native.check(lib.psd_index_copy_i32(fwd.view("tokens", i).data_ptr(), None,

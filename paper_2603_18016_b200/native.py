@@ -52,7 +52,28 @@ SIGNATURES: dict[str, tuple] = {
     "psd_index_copy_i32": (_i, [_p, _p, _p, _p, _i, _p]),
     "psd_fill_uniform_bf16": (_i, [_p, _sz, _c.c_uint64, _f, _p]),
     "psd_launch_count": (_c.c_longlong, []),
+    "psd_mk_smem_bytes": (_sz, []),
+    "psd_mk_create": (_p, [_p]),
+    "psd_mk_destroy": (None, [_p]),
+    "psd_mk_grid": (_i, [_p]),
+    "psd_mk_launch": (_i, [_p, _i, _i, _p]),
+    "psd_mk_n_ops": (_i, [_p, _i, _i]),
+    "psd_mk_launch_traced": (_i, [_p, _i, _i, _p, _p]),
 }
+
+
+class MkModel(_c.Structure):
+    """psd_mk_model (include/psd.h): the draft model + forward buffers bound to
+    the fused k-step decode kernel."""
+
+    _fields_ = [(n, _i) for n in ("layers", "hidden", "heads", "kv_heads", "head_dim", "ffn",
+                                  "vocab")] + \
+        [(n, _f) for n in ("eps", "attn_scale", "beta")] + \
+        [(n, _i) for n in ("block_size", "max_blocks", "grid", "max_tokens")] + \
+        [(n, _p) for n in ("layer_ptrs", "embed", "lm_head", "final_norm", "inv_freq",
+                           "successor", "block_table", "x", "xn", "attn", "act", "xf", "part",
+                           "argpart", "slot_tok", "meta")] + \
+        [("set_stride", _i), ("field_offsets", _i * 11)]
 
 EPI_BF16, EPI_F32, EPI_RESID, EPI_SILU, EPI_PARTIAL = 0, 1, 2, 3, 4
 
@@ -63,7 +84,7 @@ def header_symbols() -> list[str]:
     """Every function declared in include/psd.h."""
     with open(HEADER) as fh:
         text = fh.read()
-    return sorted(set(re.findall(r"^\s*(?:int|size_t|void|float|long long)\s+\**(psd_\w+)\s*\(",
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|void|float|long long)\s*\**\s*(psd_\w+)\s*\(",
                                  text, re.M)))
 
 

@@ -174,3 +174,24 @@ def test_continuous_batching_preemption_and_k_overrides_on_gpu(cuda_device):
         assert a.state == b.state
         if a.state.value == "finished":  # greedy output is schedule independent
             assert a.output_ids == b.output_ids and len(a.output_ids) == a.target_output_len
+
+
+@pytest.mark.parametrize("draft", ["llama-3.2-1b", "tiny-draft"])
+def test_fused_draft_decode_matches_per_kernel_forward(cuda_device, draft):
+    """The fused k-step draft decode (csrc/decode_mk.cu, one persistent kernel)
+    proposes the same draft tokens as the per-kernel forward: identical
+    drafted / accepted counts in every step and identical outputs."""
+    target = "llama-3.2-1b" if draft == "llama-3.2-1b" else "tiny-target"
+    kw = dict(max_requests=16, max_batch=16, k_max=4, max_seq_len=128, seed=5,
+              beta_target=6.0, beta_draft=12.0, prefill_chunk_tokens=512)
+    fused = GpuBackend(target, draft, fused_draft=True, **kw)
+    assert fused.mk is not None
+    plain = GpuBackend(target, draft, fused_draft=False, **kw)
+    assert plain.mk is None
+    fs, frep = _tiny_run("psd", fused)
+    ps, prep = _tiny_run("psd", plain)
+    assert [r.output_ids for r in fs.request_list()] == [r.output_ids for r in ps.request_list()]
+    assert [(s.drafted_tokens, s.accepted_tokens) for s in fs.step_log] == \
+        [(s.drafted_tokens, s.accepted_tokens) for s in ps.step_log]
+    assert frep.total_accepted > 0
+    fused.close()
