@@ -27,6 +27,7 @@
 // launch.  All CTAs are co-resident (grid <= #SMs, 1 CTA per SM), so the
 // in-order waits cannot deadlock.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -52,7 +53,7 @@ constexpr int kCompute = 128;  // warps 2..5
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int B_BYTES = BN * BK * 2;
 constexpr int STAGE = A_BYTES + B_BYTES;
-constexpr int STAGES = 5;
+constexpr int STAGES = 6;
 constexpr int TMEM_COLS = 2 * BN;
 // attention (head_dim <= 64, <= 16 query rows per (sequence, kv head))
 constexpr int ATT_D = 64;
@@ -145,6 +146,33 @@ __device__ __forceinline__ void wait_op(const Params& p, int j) {
   }
 }
 __device__ __forceinline__ void cbar() { named_bar_sync(1, kCompute); }
+
+// sum of S <= 16 split-K partials (base[z * slice], z ascending: P0 + P1 + ...)
+// with every load issued before the first add (one L2 latency, not S)
+__device__ __forceinline__ float sum_splits(const float* base, size_t slice, int S) {
+  float v[16];
+#pragma unroll
+  for (int z = 0; z < 16; ++z) v[z] = z < S ? __ldcg(base + z * slice) : 0.f;
+  float a = v[0];
+#pragma unroll
+  for (int z = 1; z < 16; ++z)
+    if (z < S) a += v[z];
+  return a;
+}
+__device__ __forceinline__ float4 sum_splits4(const float* base, size_t slice, int S) {
+  float4 v[16];
+#pragma unroll
+  for (int z = 0; z < 16; ++z)
+    v[z] = z < S ? __ldcg(reinterpret_cast<const float4*>(base + z * slice))
+                 : make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 a = v[0];
+#pragma unroll
+  for (int z = 1; z < 16; ++z)
+    if (z < S) {
+      a.x += v[z].x; a.y += v[z].y; a.z += v[z].z; a.w += v[z].w;
+    }
+  return a;
+}
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -404,16 +432,9 @@ __device__ void norm_row(const Params& p, const bf16* xsrc, bf16* xdst, const fl
       for (int t = 0; t < 8; ++t) v[k][t] = __bfloat162float(b8[t]);
       if (P) {
         float acc[8];
-        const float4* p4 = reinterpret_cast<const float4*>(P + e);
-        float4 a0 = __ldcg(p4), a1 = __ldcg(p4 + 1);
+        const float4 a0 = sum_splits4(P + e, slice, S), a1 = sum_splits4(P + e + 4, slice, S);
         acc[0] = a0.x; acc[1] = a0.y; acc[2] = a0.z; acc[3] = a0.w;
         acc[4] = a1.x; acc[5] = a1.y; acc[6] = a1.z; acc[7] = a1.w;
-        for (int z = 1; z < S; ++z) {
-          const float4* pz = reinterpret_cast<const float4*>(P + z * slice + e);
-          const float4 c0 = __ldcg(pz), c1 = __ldcg(pz + 1);
-          acc[0] += c0.x; acc[1] += c0.y; acc[2] += c0.z; acc[3] += c0.w;
-          acc[4] += c1.x; acc[5] += c1.y; acc[6] += c1.z; acc[7] += c1.w;
-        }
         uint4 o;
         bf16* o8 = reinterpret_cast<bf16*>(&o);
 #pragma unroll
@@ -495,6 +516,38 @@ __device__ void rope_attn(const Params& p, const Op& o, int unit, const Smem& sm
   const size_t slice = (size_t)M * NQKV;
   const int R = ql * G;
   constexpr int half = D / 2;
+  // ---- block table + earlier steps' keys of the first tile group ------------
+  const int last_key = min(p0 + ql - 1, kvl - 1);
+  const int* btg = p.block_table + (size_t)srow * p.max_blocks;
+  const int nblk = min(last_key / p.bs + 1, ATT_MAX_BLOCKS);
+  for (int i = ct; i < nblk; i += kCompute) sm.bt[i] = btg[i];
+  cbar();
+  typedef bf16 Row[ATT_P];
+  Row* ring = sm.ring;
+  auto sK = [&](int st, int j) { return ring + ((st * ATT_KG + j) * 2) * ATT_KT; };
+  auto sV = [&](int st, int j) { return ring + ((st * ATT_KG + j) * 2 + 1) * ATT_KT; };
+  const int ntiles = last_key / ATT_KT + 1;
+  const int ngroups = (ntiles + ATT_KG - 1) / ATT_KG;
+  // part: 0 all rows, 1 keys of earlier steps only (< p0), 2 the complement
+  auto load_group = [&](int gi, int st, int part) {
+    constexpr int per = ATT_KT * (D / 8);
+    for (int idx = ct; idx < ATT_KG * per; idx += kCompute) {
+      const int j = idx / per, rem = idx % per;
+      const int r = rem / (D / 8), cc = rem % (D / 8);
+      const int key = (gi * ATT_KG + j) * ATT_KT + r;
+      const bool ok = key <= last_key;
+      const bool old = ok && key < p0;
+      if ((part == 1 && !old) || (part == 2 && old)) continue;
+      size_t off = 0;
+      if (ok) off = (((size_t)sm.bt[key / p.bs] * p.bs + key % p.bs) * p.Hkv + hk) * D + cc * 8;
+      cp16(&sK(st, j)[r][cc * 8], L.kc + off, ok);
+      cp16(&sV(st, j)[r][cc * 8], L.vc + off, ok);
+    }
+    asm volatile("cp.async.commit_group;");
+  };
+  load_group(0, 0, 1);
+  if (ngroups > 1) load_group(1, 1, 1);
+  else asm volatile("cp.async.commit_group;");
   // ---- RoPE + KV write + Q into smem --------------------------------------
   for (int t = 0; t < ql; ++t) {
     const int m = qs + t;
@@ -513,8 +566,7 @@ __device__ void rope_attn(const Params& p, const Op& o, int unit, const Smem& sm
       if (idx >= nrot) {
         const int i = idx - nrot;
         const int col = (p.Hq + p.Hkv + hk) * D + i;
-        float a = 0.f;
-        for (int z = 0; z < o.S; ++z) a += __ldcg(o.P + z * slice + (size_t)m * NQKV + col);
+        float a = sum_splits(o.P + (size_t)m * NQKV + col, slice, o.S);
         a = __bfloat162float(__float2bfloat16(a));
         if (L.bqkv) a = a + __bfloat162float(L.bqkv[col]);
         if (sl >= 0) L.vc[((size_t)sl * p.Hkv + hk) * D + i] = __float2bfloat16(a);
@@ -523,11 +575,8 @@ __device__ void rope_attn(const Params& p, const Op& o, int unit, const Smem& sm
       const int hh = idx / half, i = idx % half;  // hh < G: q head hk*G+hh; hh == G: k head
       const int head = hh < G ? hk * G + hh : p.Hq + hk;
       const int col = head * D + i;
-      float a = 0.f, b = 0.f;
-      for (int z = 0; z < o.S; ++z) {
-        a += __ldcg(o.P + z * slice + (size_t)m * NQKV + col);
-        b += __ldcg(o.P + z * slice + (size_t)m * NQKV + col + half);
-      }
+      float a = sum_splits(o.P + (size_t)m * NQKV + col, slice, o.S);
+      float b = sum_splits(o.P + (size_t)m * NQKV + col + half, slice, o.S);
       a = __bfloat162float(__float2bfloat16(a));
       b = __bfloat162float(__float2bfloat16(b));
       if (L.bqkv) {
@@ -551,33 +600,11 @@ __device__ void rope_attn(const Params& p, const Op& o, int unit, const Smem& sm
   for (int idx = ct; idx < (ATT_ROWS - R) * D; idx += kCompute)
     sm.sQ[R + idx / D][idx % D] = __float2bfloat16(0.f);
   __threadfence();  // this step's K / V rows are read back below (through L2)
-  // ---- attention ------------------------------------------------------------
-  const int last_key = min(p0 + ql - 1, kvl - 1);
-  const int* btg = p.block_table + (size_t)srow * p.max_blocks;
-  const int nblk = min(last_key / p.bs + 1, ATT_MAX_BLOCKS);
-  for (int i = ct; i < nblk; i += kCompute) sm.bt[i] = btg[i];
   cbar();
-  typedef bf16 Row[ATT_P];
-  Row* ring = sm.ring;
-  auto sK = [&](int st, int j) { return ring + ((st * ATT_KG + j) * 2) * ATT_KT; };
-  auto sV = [&](int st, int j) { return ring + ((st * ATT_KG + j) * 2 + 1) * ATT_KT; };
-  const int ntiles = last_key / ATT_KT + 1;
-  const int ngroups = (ntiles + ATT_KG - 1) / ATT_KG;
-  auto load_group = [&](int gi, int st) {
-    constexpr int per = ATT_KT * (D / 8);
-    for (int idx = ct; idx < ATT_KG * per; idx += kCompute) {
-      const int j = idx / per, rem = idx % per;
-      const int r = rem / (D / 8), cc = rem % (D / 8);
-      const int key = (gi * ATT_KG + j) * ATT_KT + r;
-      const bool ok = key <= last_key;
-      size_t off = 0;
-      if (ok) off = (((size_t)sm.bt[key / p.bs] * p.bs + key % p.bs) * p.Hkv + hk) * D + cc * 8;
-      cp16(&sK(st, j)[r][cc * 8], L.kc + off, ok);
-      cp16(&sV(st, j)[r][cc * 8], L.vc + off, ok);
-    }
-    asm volatile("cp.async.commit_group;");
-  };
-  load_group(0, 0);
+  // ---- attention ------------------------------------------------------------
+  load_group(0, 0, 2);  // this step's keys (and the zero fill) of groups 0, 1
+  if (ngroups > 1) load_group(1, 1, 2);
+  else asm volatile("cp.async.commit_group;");
   const int g = lane >> 2, c = lane & 3;
   const int r0 = g, r1 = g + 8;
   const int lim0 = r0 < R ? min(p0 + r0 / G, kvl - 1) : -1;
@@ -595,11 +622,14 @@ __device__ void rope_attn(const Params& p, const Op& o, int unit, const Smem& sm
   for (int n = 0; n < D / 8; ++n) oacc[n][0] = oacc[n][1] = oacc[n][2] = oacc[n][3] = 0.f;
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
   const int kg = cw;
+  // groups 0 and 1 are in flight (4 commit groups); group gi + 2 is issued
+  // once group gi's stage is consumed
   for (int gi = 0; gi < ngroups; ++gi) {
     const int st = gi % ATT_NS;
-    if (gi + 1 < ngroups) load_group(gi + 1, (gi + 1) % ATT_NS);
-    else asm volatile("cp.async.commit_group;");
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    // outstanding after group gi: group gi + 1's last commit (gi = 0: part 2 of
+    // group 1; gi >= 1: group gi + 1, issued at the end of iteration gi - 1)
+    if (gi + 1 < ngroups) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;" ::: "memory");
     cbar();
     const int kt = gi * ATT_KG + kg;
     if (kt < ntiles) {
@@ -676,6 +706,7 @@ __device__ void rope_attn(const Params& p, const Op& o, int unit, const Smem& sm
       }
     }
     cbar();
+    if (gi + 2 < ngroups) load_group(gi + 2, st, 0);
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
@@ -1225,6 +1256,7 @@ int psd_mk_launch_traced(void* handle, int nb, int steps, void* trace, void* str
   for (int f = 0; f < F_COUNT; ++f) p.off[f] = m.field_offsets[f];
   p.layers = h->d_layers;
   p.trace = static_cast<unsigned long long*>(trace);
+
   return (int)psd::launch(decode_mk_kernel, dim3(h->G), dim3(kThreads), SMEM_TOTAL,
                           (cudaStream_t)stream, p);
 }
