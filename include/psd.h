@@ -88,6 +88,9 @@ int psd_verify_sample_rows(const float* target_logits, int64_t t_stride_b, int64
 #define PSD_EPI_RESID 2
 #define PSD_EPI_SILU 3
 #define PSD_EPI_PARTIAL 4 /* internal: split-K partials */
+/* Cap the CTAs of subsequently enqueued (or captured) GEMM grids (0 = all SMs):
+ * the verify forward runs beside the draft loop on one GPU. */
+void psd_gemm_set_max_ctas(int n);
 int psd_gemm_plan(int M, int N, int K, int epi, int splits_hint, int* splits_out,
                   size_t* workspace_bytes);
 int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, int N, void* Y,
@@ -156,6 +159,10 @@ int psd_philox_uniforms(uint64_t seed, const int32_t* request_ids, const int32_t
 /* dst[dst_rows[r] * dst_ld + c] = src[r * src_ld + c], c < ncols (negative row: skip) */
 int psd_copy_rows_f32(float* dst, const int32_t* dst_rows, int64_t dst_ld, const float* src,
                       int64_t src_ld, int nrows, int ncols, void* stream);
+/* dst[r * dst_ld + c] = src[src_rows[r] * src_ld + c] (negative row: skip): packs the
+ * draft distributions q of drafted rows for the hand-off to a target GPU */
+int psd_gather_rows_f32(float* dst, int64_t dst_ld, const float* src, const int32_t* src_rows,
+                        int64_t src_ld, int nrows, int ncols, void* stream);
 
 /* ---- K5 / glue: KV commit of accepted tokens, token routing ---------------
  * psd_commit replaces the commit rule + KV write accounting of a verified row

@@ -700,14 +700,16 @@ __global__ void fill_uniform_kernel(__nv_bfloat16* __restrict__ out, size_t n, u
 
 // dst[dst_rows[r] * dst_ld + c] = src[r * src_ld + c] (negative row: skip)
 __global__ void copy_rows_kernel(float* __restrict__ dst, const int32_t* __restrict__ dst_rows,
-                                 int64_t dst_ld, const float* __restrict__ src, int64_t src_ld,
+                                 int64_t dst_ld, const float* __restrict__ src,
+                                 const int32_t* __restrict__ src_rows, int64_t src_ld,
                                  int ncols) {
   pdl_wait();
   pdl_trigger();
   const int r = blockIdx.y;
-  const int dr = dst_rows[r];
-  if (dr < 0) return;
-  const float4* s4 = reinterpret_cast<const float4*>(src + r * src_ld);
+  const int dr = dst_rows ? dst_rows[r] : r;
+  const int sr = src_rows ? src_rows[r] : r;
+  if (dr < 0 || sr < 0) return;
+  const float4* s4 = reinterpret_cast<const float4*>(src + sr * src_ld);
   float4* d4 = reinterpret_cast<float4*>(dst + dr * dst_ld);
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncols / 4; c += gridDim.x * blockDim.x)
     d4[c] = s4[c];
@@ -725,7 +727,16 @@ int psd_copy_rows_f32(float* dst, const int32_t* dst_rows, int64_t dst_ld, const
   if ((ncols & 3) || (dst_ld & 3) || (src_ld & 3)) return (int)cudaErrorMisalignedAddress;
   dim3 grid(16, nrows);
   return (int)psd::launch(copy_rows_kernel, grid, dim3(256), 0, (cudaStream_t)stream, dst, dst_rows,
-                          dst_ld, src, src_ld, ncols);
+                          dst_ld, src, (const int32_t*)nullptr, src_ld, ncols);
+}
+
+int psd_gather_rows_f32(float* dst, int64_t dst_ld, const float* src, const int32_t* src_rows,
+                        int64_t src_ld, int nrows, int ncols, void* stream) {
+  if (nrows <= 0) return 0;
+  if ((ncols & 3) || (dst_ld & 3) || (src_ld & 3)) return (int)cudaErrorMisalignedAddress;
+  dim3 grid(16, nrows);
+  return (int)psd::launch(copy_rows_kernel, grid, dim3(256), 0, (cudaStream_t)stream, dst,
+                          (const int32_t*)nullptr, dst_ld, src, src_rows, src_ld, ncols);
 }
 
 int psd_index_copy_i32(int32_t* dst, const int32_t* dst_idx, const int32_t* src,

@@ -124,10 +124,9 @@ class GpuBackend:
                                        device=dev) if has_t else None
             self.dlogits = torch.empty(B, self.dshape.vocab, dtype=torch.float32,
                                        device=dev) if has_d else None
-            if mode == "sample" and not (has_t and has_d):
-                raise ConfigError("sampling mode with a dedicated draft GPU is not supported yet "
-                                  "(the verifier needs the draft distributions q)")
             if mode == "sample":
+                # with a dedicated draft GPU (pair.py) the draft rank ships the q
+                # rows of every drafted token to the target rank's qbuf
                 # per-slot draft distributions q (fp32 logits after the bias);
                 # K1 reads request b's rows at qbuf[slot_b] (verify_sample_rows)
                 self.qbuf = torch.empty(nslot * K, self.dshape.vocab, dtype=torch.float32,
@@ -173,6 +172,9 @@ class GpuBackend:
             grid = mk_grid or int(os.environ.get("PSD_MK_GRID", "0"))
             with torch.cuda.device(dev):
                 self.mk = self._make_mk(grid)
+        # verify GEMM grids capped below the SM count when the draft loop runs
+        # beside them (dual stream): PSD_VERIFY_CTAS (0 = all SMs)
+        self.verify_ctas = int(os.environ.get("PSD_VERIFY_CTAS", "116")) if dual_stream else 0
         self.seed_draft = (seed * 0x9E3779B1 + 0xD7A7) & 0xFFFFFFFFFFFF
         self.seed_verify = (seed * 0x85EBCA77 + 0x7E51) & 0xFFFFFFFFFFFF
         self.capture_verify = None  # set to a list to record K1 inputs (tests)
@@ -604,6 +606,14 @@ class GpuBackend:
         return n
 
     def _verify_launch(self, nb: int, kmax: int) -> None:
+        lib = native.load()
+        lib.psd_gemm_set_max_ctas(self.verify_ctas)
+        try:
+            self._verify_launch_inner(nb, kmax)
+        finally:
+            lib.psd_gemm_set_max_ctas(0)
+
+    def _verify_launch_inner(self, nb: int, kmax: int) -> None:
         K1 = kmax + 1
         B = self.max_batch
         lib = native.load()

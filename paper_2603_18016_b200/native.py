@@ -46,12 +46,14 @@ SIGNATURES: dict[str, tuple] = {
     "psd_philox_uniforms": (_i, [_c.c_uint64, _p, _p, _i, _i, _i, _p, _p]),
     "psd_rope_kv_partials": (_i, [_p, _i, _sz, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _p, _p]),
     "psd_copy_rows_f32": (_i, [_p, _p, _i64, _p, _i64, _i, _i, _p]),
+    "psd_gather_rows_f32": (_i, [_p, _i64, _p, _p, _i64, _i, _i, _p]),
     "psd_verify_sample_rows": (_i, [_p, _i64, _i64, _i, _p, _p, _i64, _i64, _i, _p, _p, _p, _f,
                                     _i, _i, _p, _p, _p, _sz, _p]),
     "psd_commit": (_i, [_p, _p, _i, _p, _i, _p, _p, _i, _p, _i, _p]),
     "psd_index_copy_i32": (_i, [_p, _p, _p, _p, _i, _p]),
     "psd_fill_uniform_bf16": (_i, [_p, _sz, _c.c_uint64, _f, _p]),
     "psd_launch_count": (_c.c_longlong, []),
+    "psd_gemm_set_max_ctas": (None, [_i]),
     "psd_mk_smem_bytes": (_sz, []),
     "psd_mk_create": (_p, [_p]),
     "psd_mk_destroy": (None, [_p]),

@@ -57,6 +57,20 @@ class PairLink:
             dist.send(self._t(arr), self.peer)
         self.bytes_sent += 4 * (arr.size + 1)
 
+    def send_rows(self, rows: torch.Tensor) -> None:
+        """fp32 [n, V] rows (the draft distributions q), device to device on
+        NCCL, through the host on gloo."""
+        t = rows if self.device is not None else rows.cpu()
+        dist.send(t.contiguous(), self.peer)
+        self.bytes_sent += t.numel() * 4
+
+    def recv_rows(self, n: int, v: int, device) -> torch.Tensor:
+        buf = torch.empty(n, v, dtype=torch.float32,
+                          device=self.device if self.device is not None else "cpu")
+        dist.recv(buf, self.peer)
+        self.bytes_recv += buf.numel() * 4
+        return buf if device is None else buf.to(device, non_blocking=True)
+
     def recv(self) -> np.ndarray:
         hdr = self._t(np.zeros(1, np.int32))
         dist.recv(hdr, self.peer)
@@ -189,6 +203,7 @@ class PairTarget:
         if serial:
             drafts, serial_ms = decode_drafts(self.link.recv())
             eng.inject(drafts)
+            self._recv_q(serial, drafts)
         t2 = time.perf_counter()
         accepted, committed, verify_ms = eng.verify(state, rows) if rows else ({}, {}, 0.0)
         t3 = time.perf_counter()
@@ -196,6 +211,7 @@ class PairTarget:
         if overlap:
             drafts, overlap_ms = decode_drafts(self.link.recv())
             eng.inject(drafts)
+            self._recv_q(overlap, drafts)
         t4 = time.perf_counter()
         for rid, toks in committed.items():
             self.pending_commits.append((rid, eng.slot_of(rid), toks))
@@ -206,6 +222,16 @@ class PairTarget:
         self.stats["prefill_ms"] += ms(t0, t1)
         self.stats["wait_ms"] += ms(t1, t2) + ms(t3, t4)
         return StepResult(ms(t0, t1), serial_ms, overlap_ms, verify_ms, ms(t0, t4), accepted)
+
+    def _recv_q(self, rows, drafts) -> None:
+        """Sampling mode: the draft distributions of the drafted tokens follow
+        the draft ids (one [sum k, V_draft] fp32 message, rows in draft order)."""
+        vq = getattr(self.engine, "q_vocab", 0)
+        if not vq:
+            return
+        n = sum(len(drafts[r[0]]) for r in rows)
+        if n:
+            self.engine.inject_q(rows, drafts, self.link.recv_rows(n, vq, self.engine.device))
 
     def stop(self) -> None:
         self.link.send(np.asarray([MAGIC, K_STOP], np.int32))
@@ -234,6 +260,9 @@ class DraftServer:
                     t0 = time.perf_counter()
                     drafts = eng.draft(rows)
                     self.link.send(encode_drafts(rows, drafts, (time.perf_counter() - t0) * 1e3))
+                    q = eng.q_rows(rows) if getattr(eng, "q_vocab", 0) else None
+                    if q is not None and q.shape[0]:
+                        self.link.send_rows(q)
             self.steps += 1
 
 
@@ -288,6 +317,32 @@ class GpuTargetEngine:
             pairs += [(s * be.ldt + 2 + i, t) for i, t in enumerate(ids)]
         with torch.cuda.stream(be.s_target):
             be._set_slot_values(pairs)
+
+    @property
+    def q_vocab(self) -> int:
+        return self.be.dshape.vocab if self.be.mode == "sample" else 0
+
+    @property
+    def device(self):
+        return self.be.device
+
+    def inject_q(self, rows, drafts, q: torch.Tensor) -> None:
+        """q rows in draft order -> qbuf[slot * k_max + i] (what K1 reads)."""
+        be = self.be
+        dst = []
+        for rid, slot, _, _ in rows:
+            dst += [slot * be.k_max + i for i in range(len(drafts[rid]))]
+        idx = torch.from_numpy(np.asarray(dst, np.int32)).pin_memory()
+        # q arrived in the current stream's order (NCCL recv / host copy)
+        be.s_target.wait_stream(torch.cuda.current_stream(be.device))
+        with torch.cuda.stream(be.s_target):
+            idx_d = idx.to(be.device, non_blocking=True)
+            from . import native
+            V = be.dshape.vocab
+            native.check(native.load().psd_copy_rows_f32(
+                be.qbuf.data_ptr(), idx_d.data_ptr(), V, q.data_ptr(), V, len(dst), V,
+                torch.cuda.current_stream(be.device).cuda_stream), "q rows in")
+            q.record_stream(be.s_target)
 
     def verify(self, state, rows):
         be = self.be
@@ -352,3 +407,25 @@ class GpuDraftEngine:
         be._draft_rows(rows)
         st = be.slot_tok.cpu().numpy()  # synchronises the draft stream
         return {rid: st[slot, 2:2 + k].tolist() for rid, slot, _, k in rows}
+
+    @property
+    def q_vocab(self) -> int:
+        return self.be.dshape.vocab if self.be.mode == "sample" else 0
+
+    def q_rows(self, rows) -> torch.Tensor:
+        """Sampling mode: the q rows of the drafted tokens, packed in draft
+        order ([sum k, V_draft] fp32 on the draft GPU)."""
+        be = self.be
+        src = []
+        for _, slot, _, k in rows:
+            src += [slot * be.k_max + i for i in range(k)]
+        V = be.dshape.vocab
+        out = torch.empty(len(src), V, dtype=torch.float32, device=be.device)
+        if src:
+            from . import native
+            idx = torch.from_numpy(np.asarray(src, np.int32)).to(be.device)
+            native.check(native.load().psd_gather_rows_f32(
+                out.data_ptr(), V, be.qbuf.data_ptr(), idx.data_ptr(), V, len(src), V,
+                torch.cuda.current_stream(be.device).cuda_stream), "q rows out")
+            torch.cuda.current_stream(be.device).synchronize()
+        return out

@@ -30,7 +30,7 @@ def _cfg_reqs():
                                                          prompt_len=10)
 
 
-def _worker(rank, port, q):
+def _worker(rank, port, q, extra=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE="2",
                       RANK=str(rank), LOCAL_RANK=str(rank))
     import torch.distributed as dist
@@ -41,14 +41,14 @@ def _worker(rank, port, q):
                                             PairLink, PairTarget)
     dist.init_process_group("gloo", init_method="env://")
     if rank == 0:
-        gb = GpuBackend("tiny-target", "tiny-draft", roles=("target",), **KW)
+        gb = GpuBackend("tiny-target", "tiny-draft", roles=("target",), **KW, **(extra or {}))
         be = PairTarget(GpuTargetEngine(gb), PairLink(1))
         cfg, reqs = _cfg_reqs()
         st, rep = run(cfg, reqs, backend=be)
         be.stop()
         q.put(("out", [r.output_ids for r in st.request_list()], rep.finished))
     else:
-        gb = GpuBackend("tiny-target", "tiny-draft", roles=("draft",), **KW)
+        gb = GpuBackend("tiny-target", "tiny-draft", roles=("draft",), **KW, **(extra or {}))
         q.put(("steps", DraftServer(GpuDraftEngine(gb), PairLink(0)).serve()))
     dist.destroy_process_group()
 
@@ -72,3 +72,38 @@ def test_pair_gpu_engines_match_single_process(cuda_device):
     assert got["out"][1] == 8
     assert got["out"][0] == ref
     assert got["steps"][0] > 0
+
+
+def test_pair_gpu_sampling_ships_q_rows(cuda_device):
+    """Sampling mode across the pair: the draft rank sends the draft
+    distributions q of every drafted token after the ids; the target's K1
+    reads them from its qbuf.  Same weights, logits and Philox uniforms on both
+    sides -> token-for-token identical to the single-process sampling run."""
+    from paper_2603_18016_b200 import run
+    from paper_2603_18016_b200.gpu import GpuBackend
+    extra = dict(mode="sample", temperature=1.0)
+    cfg, reqs = _cfg_reqs()
+    kw = dict(KW, beta_target=1.0, beta_draft=1.0)
+    st, rep = run(cfg, reqs, backend=GpuBackend("tiny-target", "tiny-draft", **kw, **extra))
+    ref = [r.output_ids for r in st.request_list()]
+    assert 0 < rep.total_accepted < rep.total_drafted
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    extra_kw = dict(extra, beta_target=1.0, beta_draft=1.0)
+    procs = [ctx.Process(target=_worker_kw, args=(r, port, q, extra_kw)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict((m[0], m[1:]) for m in (q.get(timeout=600) for _ in procs))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert got["out"][1] == 8
+    assert got["out"][0] == ref
+
+
+def _worker_kw(rank, port, q, extra):
+    """_worker with KW entries overridden by ``extra``."""
+    global KW
+    KW = {k: v for k, v in KW.items() if k not in extra}
+    _worker(rank, port, q, extra)
