@@ -149,6 +149,19 @@ int psd_attention(const void* q, const void* k_cache, const void* v_cache,
                   const int32_t* kv_len, int num_seqs, int max_q_len, int Hq, int Hkv, int D,
                   int block_size, float scale, void* out, int max_kv_len, void* workspace,
                   size_t workspace_bytes, void* stream);
+/* psd_attention with the RoPE + paged-KV write fused in (decode / verify passes:
+ * max_q_len <= 64 / (Hq / Hkv)): reads the QKV split-K partials (S slices of
+ * `slice` floats) instead of q, rotates Q / K per token position, writes this
+ * pass's K / V rows into the caches and attends.  cudaErrorInvalidValue when the
+ * pass needs several query chunks per sequence (use psd_rope_kv_partials +
+ * psd_attention). */
+int psd_attention_rope(const float* qkv_partials, int S, size_t slice, const int32_t* positions,
+                       const int32_t* slots, const float* inv_freq, const void* qkv_bias,
+                       void* k_cache, void* v_cache, const int32_t* block_table, int max_blocks,
+                       const int32_t* seq_slot, const int32_t* q_start, const int32_t* q_len,
+                       const int32_t* q_pos0, const int32_t* kv_len, int num_seqs, int max_q_len,
+                       int Hq, int Hkv, int D, int block_size, float scale, void* out,
+                       void* stream);
 /* synthetic-language logit bias: logits[m, successor[prev_tokens[m]]] += beta */
 int psd_bigram_bias(float* logits, int64_t ld, const int32_t* prev_tokens, int M,
                     const int32_t* successor, int V, float beta, void* stream);

@@ -242,6 +242,11 @@ __device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+__device__ __forceinline__ void ldmatrix_x4(uint32_t (&r)[4], const void* p) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(a));
+}
 __device__ __forceinline__ void ldmatrix_x4_trans(uint32_t (&r)[4], const void* p) {
   const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -266,7 +271,37 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 // ring, so a decode step (4-8 rows) keeps all 4 warps busy on 4 tiles at a
 // time.  The key groups' (max, sum, O) states are merged through shared
 // memory at the end (same math as split-KV flash decoding, no global traffic).
-template <int D, int KT, int NS>
+// Fused RoPE (decode / verify passes, one query chunk per sequence): the CTA of
+// (sequence, kv head) reduces the QKV split-K partials of its G query heads and
+// its K / V head for the sequence's tokens, rotates Q and K, writes this step's
+// K / V rows into the paged cache and Q straight into shared memory -- no
+// separate RoPE launch and no Q round trip through HBM.
+__device__ __forceinline__ void vc_w(const __nv_bfloat16* vc, size_t off, float a) {
+  const_cast<__nv_bfloat16*>(vc)[off] = __float2bfloat16(a);
+}
+
+struct RopeSrc {
+  const float* P;  // QKV split-K partials [S][M][(Hq + 2 Hkv) D]
+  int S;
+  size_t slice;
+  const int32_t* positions;
+  const int32_t* slots;
+  const float* inv_freq;
+  const __nv_bfloat16* bias;  // qkv bias or null
+};
+
+__device__ __forceinline__ float sum_parts(const RopeSrc& rs, size_t off) {
+  float v[16];
+#pragma unroll
+  for (int z = 0; z < 16; ++z) v[z] = z < rs.S ? __ldcg(rs.P + z * rs.slice + off) : 0.f;
+  float a = v[0];
+#pragma unroll
+  for (int z = 1; z < 16; ++z)
+    if (z < rs.S) a += v[z];
+  return __bfloat162float(__float2bfloat16(a));  // the projection output is bf16
+}
+
+template <int D, int KT, int NS, bool ROPE>
 __global__ void __launch_bounds__(ATT_THREADS)
 attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ kc,
                  const __nv_bfloat16* __restrict__ vc, const int32_t* __restrict__ block_table,
@@ -275,7 +310,7 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
                  const int32_t* __restrict__ q_pos0, const int32_t* __restrict__ kv_len, int Hq,
                  int Hkv, int bs, float scale_log2, int tok_per_chunk, int RG, int S,
                  float* __restrict__ ws, int* __restrict__ tickets,
-                 __nv_bfloat16* __restrict__ out) {
+                 __nv_bfloat16* __restrict__ out, const RopeSrc rs) {
   // PDL: metadata, the block table and the keys of earlier steps (positions <
   // q_pos0) do not depend on the predecessor (RoPE writes this step's keys and
   // the queries), so they are fetched before griddepcontrol.wait
@@ -297,7 +332,7 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
   const int g = lane >> 2, c = lane & 3;
   const int rg = warp % RG, kg = warp / RG;
   __shared__ int bt[ATT_MAX_BLOCKS];
-  const int nblk_used = min(last_key / bs + 1, ATT_MAX_BLOCKS);
+  const int nblk_used = min((last_key >> (__ffs(bs) - 1)) + 1, ATT_MAX_BLOCKS);
   for (int i = tid; i < nblk_used; i += ATT_THREADS) bt[i] = btg[i];
 
   extern __shared__ __align__(16) uint8_t att_smem[];
@@ -316,20 +351,37 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
   __syncthreads();  // bt staged
   // part: 0 = every row of the group, 1 = rows of earlier steps' keys only,
   // 2 = the complement of 1 (this step's keys and the zero fill past the end)
+  // every thread copies the same (row, 16-byte chunk) positions of each tile:
+  // KT * D / 8 chunks per tile over 128 threads (a whole multiple for D >= 32),
+  // so the index math is hoisted and the block-table lookup is a shift / mask
+  // (block_size is a power of two)
+  constexpr int CPR = D / 8;                       // 16-byte chunks per row
+  constexpr int PER_T = KT * CPR / ATT_THREADS;    // chunks per thread per tile
+  static_assert(KT * CPR % ATT_THREADS == 0, "tile chunks must tile the CTA");
+  const int bs_shift = __ffs(bs) - 1;
+  const size_t head_off = (size_t)hk * D;
   auto load_group = [&](int gi, int st, int part) {
-    const int per = KT * (D / 8);
-    for (int idx = tid; idx < KG * per; idx += ATT_THREADS) {
-      const int j = idx / per, rem = idx % per;
-      const int r = rem / (D / 8), cc = rem % (D / 8);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (j >= KG) break;
       const int tile = ta + gi * KG + j;
-      const int key = tile * KT + r;
-      const bool ok = key <= last_key && tile < tb;
-      const bool old = ok && key < first_pos;
-      if ((part == 1 && !old) || (part == 2 && old)) continue;
-      size_t o = 0;
-      if (ok) o = (((size_t)bt[key / bs] * bs + key % bs) * Hkv + hk) * D + cc * 8;
-      cp_async16(&sK(st, j)[r][cc * 8], kc + o, ok);
-      cp_async16(&sV(st, j)[r][cc * 8], vc + o, ok);
+      Row* K = sK(st, j);
+      Row* V = sV(st, j);
+#pragma unroll
+      for (int i = 0; i < PER_T; ++i) {
+        const int idx = tid + ATT_THREADS * i;
+        const int r = idx / CPR, cc = idx % CPR;  // compile-time divisors
+        const int key = tile * KT + r;
+        const bool ok = key <= last_key && tile < tb;
+        const bool old = ok && key < first_pos;
+        if ((part == 1 && !old) || (part == 2 && old)) continue;
+        size_t o = 0;
+        if (ok)
+          o = ((((size_t)bt[key >> bs_shift] << bs_shift) + (key & (bs - 1))) * Hkv) * D +
+              head_off + cc * 8;
+        cp_async16(&K[r][cc * 8], kc + o, ok);
+        cp_async16(&V[r][cc * 8], vc + o, ok);
+      }
     }
     cp_async_commit();
   };
@@ -340,15 +392,66 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
   }
   pdl_wait();
   pdl_trigger();
-  for (int idx = tid; idx < ATT_MAXR * (D / 8); idx += ATT_THREADS) {
-    const int r = idx / (D / 8), cc = idx % (D / 8);
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (r < R) {
-      const int t = r / G, gg = r % G;
-      v = *reinterpret_cast<const uint4*>(q + ((size_t)(qs + t0 + t) * Hq + hk * G + gg) * D +
-                                          cc * 8);
+  if constexpr (ROPE) {
+    // rotate-half RoPE of (token t, head h, pair i): G query heads + the K head,
+    // then the V head copied; bf16 rounding points as in rope_kv_kernel
+    constexpr int half = D / 2;
+    const int NQKV = (Hq + 2 * Hkv) * D;
+    const int nrot = nt * (G + 1) * half;
+    for (int idx = tid; idx < nrot + nt * D; idx += ATT_THREADS) {
+      if (idx >= nrot) {
+        const int t = (idx - nrot) / D, i = (idx - nrot) % D;
+        const int m = qs + t0 + t;
+        const int sl = rs.slots[m];
+        if (sl < 0) continue;
+        const int col = (Hq + Hkv + hk) * D + i;
+        float a = sum_parts(rs, (size_t)m * NQKV + col);
+        if (rs.bias) a = a + __bfloat162float(rs.bias[col]);
+        vc_w(vc, ((size_t)sl * Hkv + hk) * D + i, a);
+        continue;
+      }
+      const int t = idx / ((G + 1) * half), rem = idx % ((G + 1) * half);
+      const int hh = rem / half, i = rem % half;
+      const int m = qs + t0 + t;
+      const int head = hh < G ? hk * G + hh : Hq + hk;
+      const int col = head * D + i;
+      float a = sum_parts(rs, (size_t)m * NQKV + col);
+      float b = sum_parts(rs, (size_t)m * NQKV + col + half);
+      if (rs.bias) {
+        a = __bfloat162float(__float2bfloat16(a + __bfloat162float(rs.bias[col])));
+        b = __bfloat162float(__float2bfloat16(b + __bfloat162float(rs.bias[col + half])));
+      }
+      float sn, cs;
+      sincosf((float)rs.positions[m] * rs.inv_freq[i], &sn, &cs);
+      const __nv_bfloat16 ra = __float2bfloat16(a * cs - b * sn);
+      const __nv_bfloat16 rb = __float2bfloat16(b * cs + a * sn);
+      if (hh < G) {
+        sQ[t * G + hh][i] = ra;
+        sQ[t * G + hh][i + half] = rb;
+      } else {
+        const int sl = rs.slots[m];
+        if (sl >= 0) {
+          __nv_bfloat16* dst = const_cast<__nv_bfloat16*>(kc) + ((size_t)sl * Hkv + hk) * D;
+          dst[i] = ra;
+          dst[i + half] = rb;
+        }
+      }
     }
-    *reinterpret_cast<uint4*>(&sQ[r][cc * 8]) = v;
+    for (int idx = tid; idx < (ATT_MAXR - R) * D; idx += ATT_THREADS)
+      sQ[R + idx / D][idx % D] = __float2bfloat16(0.f);
+    __threadfence();  // this step's K / V rows are read back below through L2
+    __syncthreads();
+  } else {
+    for (int idx = tid; idx < ATT_MAXR * (D / 8); idx += ATT_THREADS) {
+      const int r = idx / (D / 8), cc = idx % (D / 8);
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (r < R) {
+        const int t = r / G, gg = r % G;
+        v = *reinterpret_cast<const uint4*>(q + ((size_t)(qs + t0 + t) * Hq + hk * G + gg) * D +
+                                            cc * 8);
+      }
+      *reinterpret_cast<uint4*>(&sQ[r][cc * 8]) = v;
+    }
   }
   // this step's keys of the prefetched groups (one extra commit group; the
   // first iteration waits for everything)
@@ -391,14 +494,17 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
       float sacc[KT / 8][4];
 #pragma unroll
       for (int n = 0; n < KT / 8; ++n) sacc[n][0] = sacc[n][1] = sacc[n][2] = sacc[n][3] = 0.f;
+      // K fragments with ldmatrix.x4: matrices (keys 8n.., dims 16kk..), (.., 16kk+8..),
+      // (keys 8n+8.., 16kk..), (.., 16kk+8..) -> b0/b1 of key blocks n and n+1
+      const int lrow = lane & 7, lmat = lane >> 3;
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk) {
 #pragma unroll
-        for (int n = 0; n < KT / 8; ++n) {
-          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&K[n * 8 + g][kk * 16 + 2 * c]);
-          const uint32_t b1 =
-              *reinterpret_cast<const uint32_t*>(&K[n * 8 + g][kk * 16 + 8 + 2 * c]);
-          mma_bf16_16816(sacc[n], qf[kk], b0, b1);
+        for (int n = 0; n < KT / 8; n += 2) {
+          uint32_t kb[4];
+          ldmatrix_x4(kb, &K[(n + (lmat >> 1)) * 8 + lrow][kk * 16 + (lmat & 1) * 8]);
+          mma_bf16_16816(sacc[n], qf[kk], kb[0], kb[1]);
+          mma_bf16_16816(sacc[n + 1], qf[kk], kb[2], kb[3]);
         }
       }
       float mx0 = -INFINITY, mx1 = -INFINITY;
@@ -835,16 +941,18 @@ size_t psd_attention_workspace_bytes(int num_seqs, int Hkv, int max_q_len, int H
   return 4096 * sizeof(int) + units * S * ATT_MAXR * (D + 2) * sizeof(float);
 }
 
-int psd_attention(const void* q, const void* k_cache, const void* v_cache,
-                  const int32_t* block_table, int max_blocks, const int32_t* seq_slot,
-                  const int32_t* q_start, const int32_t* q_len, const int32_t* q_pos0,
-                  const int32_t* kv_len, int num_seqs, int max_q_len, int Hq, int Hkv, int D,
-                  int block_size, float scale, void* out, int max_kv_len, void* workspace,
-                  size_t workspace_bytes, void* stream) {
+static int attention_launch(const void* q, const void* k_cache, const void* v_cache,
+                            const int32_t* block_table, int max_blocks, const int32_t* seq_slot,
+                            const int32_t* q_start, const int32_t* q_len, const int32_t* q_pos0,
+                            const int32_t* kv_len, int num_seqs, int max_q_len, int Hq, int Hkv,
+                            int D, int block_size, float scale, void* out, int max_kv_len,
+                            void* workspace, size_t workspace_bytes, const RopeSrc* rope,
+                            void* stream) {
   if (num_seqs <= 0) return 0;
   if (Hq % Hkv) return (int)cudaErrorInvalidValue;
   const int G = Hq / Hkv;
   if (G > ATT_MAXR || max_blocks > ATT_MAX_BLOCKS) return (int)cudaErrorInvalidValue;
+  if (block_size <= 0 || (block_size & (block_size - 1))) return (int)cudaErrorInvalidValue;
   const int tpc = ATT_MAXR / G;
   const int chunks = (max_q_len + tpc - 1) / tpc;
   // rows per CTA -> row groups; the other warps become key groups
@@ -852,16 +960,19 @@ int psd_attention(const void* q, const void* k_cache, const void* v_cache,
   int RG = (rmax + 15) / 16;
   if (RG == 3) RG = 4;  // 4 / RG must be an integer number of key groups
   const int KG = 4 / RG;
-  int S = att_splits(num_seqs * Hkv * chunks, max_kv_len);
+  int S = rope ? 1 : att_splits(num_seqs * Hkv * chunks, max_kv_len);
   const size_t units = (size_t)num_seqs * Hkv * chunks;
   if (S > 1 && (!workspace || units > 4096 ||
                 workspace_bytes < 4096 * sizeof(int) + units * S * ATT_MAXR * (D + 2) * 4))
     S = 1;  // no (or too little) workspace: no split
+  // fused RoPE needs every token of a sequence in one CTA
+  if (rope && (chunks != 1 || (rope->S > 16))) return (int)cudaErrorInvalidValue;
   int* tickets = static_cast<int*>(workspace);
   float* wsf = workspace ? reinterpret_cast<float*>(static_cast<char*>(workspace) + 4096 * 4)
                          : nullptr;
   dim3 grid(num_seqs, Hkv, chunks * S);
   const float sl2 = scale * 1.44269504088896341f;
+  const RopeSrc rs = rope ? *rope : RopeSrc{};
   auto go = [&](auto kern, int kt, int d) {
     const int smem = (ATT_MAXR + 2 * ATT_STAGES * KG * kt) * (d + 8) * 2;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -869,15 +980,57 @@ int psd_attention(const void* q, const void* k_cache, const void* v_cache,
                 static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k_cache),
                 static_cast<const __nv_bfloat16*>(v_cache), block_table, max_blocks, seq_slot,
                 q_start, q_len, q_pos0, kv_len, Hq, Hkv, block_size, sl2, tpc, RG, S, wsf,
-                tickets, static_cast<__nv_bfloat16*>(out));
+                tickets, static_cast<__nv_bfloat16*>(out), rs);
   };
   switch (D) {
-    case 32: go(attention_kernel<32, 64, ATT_STAGES>, 64, 32); break;
-    case 64: go(attention_kernel<64, 32, ATT_STAGES>, 32, 64); break;
-    case 128: go(attention_kernel<128, 32, ATT_STAGES>, 32, 128); break;
+    case 32:
+      if (rope) go(attention_kernel<32, 64, ATT_STAGES, true>, 64, 32);
+      else go(attention_kernel<32, 64, ATT_STAGES, false>, 64, 32);
+      break;
+    case 64:
+      if (rope) go(attention_kernel<64, 32, ATT_STAGES, true>, 32, 64);
+      else go(attention_kernel<64, 32, ATT_STAGES, false>, 32, 64);
+      break;
+    case 128:
+      if (rope) go(attention_kernel<128, 32, ATT_STAGES, true>, 32, 128);
+      else go(attention_kernel<128, 32, ATT_STAGES, false>, 32, 128);
+      break;
     default: return (int)cudaErrorInvalidValue;
   }
   return (int)cudaGetLastError();
+}
+
+int psd_attention(const void* q, const void* k_cache, const void* v_cache,
+                  const int32_t* block_table, int max_blocks, const int32_t* seq_slot,
+                  const int32_t* q_start, const int32_t* q_len, const int32_t* q_pos0,
+                  const int32_t* kv_len, int num_seqs, int max_q_len, int Hq, int Hkv, int D,
+                  int block_size, float scale, void* out, int max_kv_len, void* workspace,
+                  size_t workspace_bytes, void* stream) {
+  return attention_launch(q, k_cache, v_cache, block_table, max_blocks, seq_slot, q_start, q_len,
+                          q_pos0, kv_len, num_seqs, max_q_len, Hq, Hkv, D, block_size, scale, out,
+                          max_kv_len, workspace, workspace_bytes, nullptr, stream);
+}
+
+int psd_attention_rope(const float* qkv_partials, int S, size_t slice, const int32_t* positions,
+                       const int32_t* slots, const float* inv_freq, const void* qkv_bias,
+                       void* k_cache, void* v_cache, const int32_t* block_table, int max_blocks,
+                       const int32_t* seq_slot, const int32_t* q_start, const int32_t* q_len,
+                       const int32_t* q_pos0, const int32_t* kv_len, int num_seqs, int max_q_len,
+                       int Hq, int Hkv, int D, int block_size, float scale, void* out,
+                       void* stream) {
+  if (!qkv_partials || S <= 0 || !positions || !slots || !inv_freq)
+    return (int)cudaErrorInvalidValue;
+  RopeSrc rs;
+  rs.P = qkv_partials;
+  rs.S = S;
+  rs.slice = slice;
+  rs.positions = positions;
+  rs.slots = slots;
+  rs.inv_freq = inv_freq;
+  rs.bias = static_cast<const __nv_bfloat16*>(qkv_bias);
+  return attention_launch(nullptr, k_cache, v_cache, block_table, max_blocks, seq_slot, q_start,
+                          q_len, q_pos0, kv_len, num_seqs, max_q_len, Hq, Hkv, D, block_size,
+                          scale, out, 0, nullptr, 0, &rs, stream);
 }
 
 int psd_bigram_bias(float* logits, int64_t ld, const int32_t* prev_tokens, int M,

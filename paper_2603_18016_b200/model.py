@@ -284,6 +284,8 @@ class Forward:
             o += sizes[name]
         self.set_size = o
         self.sets = sets
+        import os
+        self.fuse_rope = os.environ.get("PSD_FUSED_ROPE", "1") == "1"
         self.meta = torch.zeros(sets, o, dtype=torch.int32, device=dev)
         # ring of pinned staging buffers: an async H2D copy reads its buffer
         # when it executes, so a buffer is rewritten only after its copy ran
@@ -347,6 +349,10 @@ class Forward:
         # partials are reduced inside the consumer kernel (RoPE, add+RMSNorm);
         # gate/up and the LM head: stream-K persistent GEMMs
         prev_S = 0  # splits of the pending down-proj partials (0 = none)
+        # draft decode (<= 2 query tokens per sequence): RoPE fused into the
+        # attention kernel (-3 % per draft step); at verify widths (k + 1 tokens)
+        # the separate RoPE kernel's parallelism wins (+3 % when fused)
+        fuse_rope = self.fuse_rope and max_q_len <= 2
         for li, L in enumerate(m.layers):
             kc = m.kv[li, 0]
             vc = m.kv[li, 1]
@@ -355,21 +361,33 @@ class Forward:
                                      s.rms_eps, 1, st), "add+attn norm")
             _chk(lib.psd_gemm_partials(self.xn.data_ptr(), H, M, H, L["wqkv"].data_ptr(), H,
                                        s.qkv_out, part, partn, 0, nsp, st), "gemm qkv")
-            _chk(lib.psd_rope_kv_partials(part, nsp._obj.value, M * s.qkv_out, M, s.heads,
-                                          s.kv_heads, s.head_dim, v["positions"].data_ptr(),
-                                          v["slots"].data_ptr(), m.inv_freq.data_ptr(),
-                                          L["bqkv"].data_ptr() if L["bqkv"] is not None else None,
-                                          self.q.data_ptr(), kc.data_ptr(), vc.data_ptr(), st),
-                 "rope_kv")
-            _chk(lib.psd_attention(self.q.data_ptr(), kc.data_ptr(), vc.data_ptr(),
-                                   self.block_table.data_ptr(), self.block_table.shape[1],
-                                   v["seq_slot"].data_ptr(), v["q_start"].data_ptr(),
-                                   v["q_len"].data_ptr(), v["q_pos0"].data_ptr(),
-                                   v["kv_len"].data_ptr(), n_seqs, max_q_len, s.heads,
-                                   s.kv_heads, s.head_dim, m.block_size, scale,
-                                   self.attn.data_ptr(), self.max_kv_len if M <= 4 * n_seqs * 4
-                                   else 0, self.att_ws.data_ptr(), self.att_ws.numel(), st),
-                 "attention")
+            if fuse_rope:
+                # decode / verify: RoPE + KV write inside the attention kernel
+                _chk(lib.psd_attention_rope(
+                    part, nsp._obj.value, M * s.qkv_out, v["positions"].data_ptr(),
+                    v["slots"].data_ptr(), m.inv_freq.data_ptr(),
+                    L["bqkv"].data_ptr() if L["bqkv"] is not None else None, kc.data_ptr(),
+                    vc.data_ptr(), self.block_table.data_ptr(), self.block_table.shape[1],
+                    v["seq_slot"].data_ptr(), v["q_start"].data_ptr(), v["q_len"].data_ptr(),
+                    v["q_pos0"].data_ptr(), v["kv_len"].data_ptr(), n_seqs, max_q_len, s.heads,
+                    s.kv_heads, s.head_dim, m.block_size, scale, self.attn.data_ptr(), st),
+                    "attention+rope")
+            else:
+                _chk(lib.psd_rope_kv_partials(part, nsp._obj.value, M * s.qkv_out, M, s.heads,
+                                              s.kv_heads, s.head_dim, v["positions"].data_ptr(),
+                                              v["slots"].data_ptr(), m.inv_freq.data_ptr(),
+                                              L["bqkv"].data_ptr() if L["bqkv"] is not None else None,
+                                              self.q.data_ptr(), kc.data_ptr(), vc.data_ptr(), st),
+                     "rope_kv")
+                _chk(lib.psd_attention(self.q.data_ptr(), kc.data_ptr(), vc.data_ptr(),
+                                       self.block_table.data_ptr(), self.block_table.shape[1],
+                                       v["seq_slot"].data_ptr(), v["q_start"].data_ptr(),
+                                       v["q_len"].data_ptr(), v["q_pos0"].data_ptr(),
+                                       v["kv_len"].data_ptr(), n_seqs, max_q_len, s.heads,
+                                       s.kv_heads, s.head_dim, m.block_size, scale,
+                                       self.attn.data_ptr(), self.max_kv_len if M <= 4 * n_seqs * 4
+                                       else 0, self.att_ws.data_ptr(), self.att_ws.numel(), st),
+                     "attention")
             _chk(lib.psd_gemm_partials(self.attn.data_ptr(), Dq, M, Dq, L["wo"].data_ptr(), Dq, H,
                                        part, partn, 0, nsp, st), "gemm o")
             _chk(lib.psd_add_rmsnorm(X, H, part, nsp._obj.value, M * H, H, None,

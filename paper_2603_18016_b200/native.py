@@ -42,6 +42,8 @@ SIGNATURES: dict[str, tuple] = {
     "psd_attention": (_i, [_p, _p, _p, _p, _i, _p, _p, _p, _p, _p, _i, _i, _i, _i, _i, _i, _f,
                            _p, _i, _p, _sz, _p]),
     "psd_attention_workspace_bytes": (_sz, [_i, _i, _i, _i, _i, _i]),
+    "psd_attention_rope": (_i, [_p, _i, _sz, _p, _p, _p, _p, _p, _p, _p, _i, _p, _p, _p, _p, _p,
+                                _i, _i, _i, _i, _i, _i, _f, _p, _p]),
     "psd_bigram_bias": (_i, [_p, _i64, _p, _i, _p, _i, _f, _p]),
     "psd_philox_uniforms": (_i, [_c.c_uint64, _p, _p, _i, _i, _i, _p, _p]),
     "psd_rope_kv_partials": (_i, [_p, _i, _sz, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _p, _p]),

@@ -273,6 +273,10 @@ def main():
         gemm_case("1B lm_head", 32, 128256, 2048, "f32", copies=2)
     if want("gemmgu"):
         gemm_case("8B gate/up", 192, 28672, 4096, "silu")
+    if want("attn1b"):
+        attn_case("1B draft", 32, 1, 300, 32, 8, 64)
+    if want("attn8b"):
+        attn_case("8B verify", 32, 6, 300, 32, 8, 128)
     if want("attn"):
         attn_case("8B verify", 32, 6, 300, 32, 8, 128)
         attn_case("1B draft", 32, 1, 300, 32, 8, 64)
