@@ -131,6 +131,17 @@ def _time_kernel(fn, iters: int = 20) -> float:
     return e0.elapsed_time(e1) / iters
 
 
+def _ncu_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum of one launch of the
+    roofline kernel from the committed ncu --set full capture (profiles/)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01b_ncu_traffic.json")) as fh:
+            t = json.load(fh)["gate_up_M192_N28672_K4096"]
+        return t["dram_read"] + t["dram_write"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def kernel_rooflines(backend, hbm_peak: float) -> tuple[dict, dict]:
     """Dominant kernel (verify-forward gate/up GEMM) and K1 at the workload shapes."""
     import torch
@@ -156,7 +167,7 @@ def kernel_rooflines(backend, hbm_peak: float) -> tuple[dict, dict]:
     roof = {"kernel": "gemm_kernel<192,SILU> (verify gate/up, M=192 N=28672 K=4096)",
             "bound": "hbm", "achieved": round(nbytes / (ms * 1e-3) / 1e9, 1),
             "peak": hbm_peak, "unit": "GB/s",
-            "frac": round(nbytes / (ms * 1e-3) / 1e9 / hbm_peak, 4), "traffic": None,
+            "frac": round(nbytes / (ms * 1e-3) / 1e9 / hbm_peak, 4), "traffic": _ncu_traffic(),
             "bytes_per_launch": nbytes, "us_per_launch": round(ms * 1e3, 2),
             "tflops": round(2 * M * w.shape[0] * s.hidden / (ms * 1e-3) / 1e12, 1)}
     B, K, V = CFG["m"], CFG["k"], s.vocab
