@@ -164,7 +164,7 @@ def kernel_rooflines(backend, hbm_peak: float) -> tuple[dict, dict]:
 
     ms = _time_kernel(gemm, 64)
     nbytes = w.numel() * 2 + x.numel() * 2 + out.numel() * 2
-    roof = {"kernel": "gemm_kernel<192,SILU> (verify gate/up, M=192 N=28672 K=4096)",
+    roof = {"kernel": "gemm_sk_kernel<192,SILU> (verify gate/up, M=192 N=28672 K=4096)",
             "bound": "hbm", "achieved": round(nbytes / (ms * 1e-3) / 1e9, 1),
             "peak": hbm_peak, "unit": "GB/s",
             "frac": round(nbytes / (ms * 1e-3) / 1e9 / hbm_peak, 4), "traffic": _ncu_traffic(),

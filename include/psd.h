@@ -195,6 +195,12 @@ int psd_index_copy_i32(int32_t* dst, const int32_t* dst_idx, const int32_t* src,
 long long psd_launch_count(void);
 /* deterministic random init: (u - 1/2) * span, u = splitmix64(seed, i) >> 40 / 2^24 */
 int psd_fill_uniform_bf16(void* out, size_t n, uint64_t seed, float span, void* stream);
+/* The [rows x cols] block at (row0, col0) of the virtual [* x full_cols] tensor
+ * psd_fill_uniform_bf16 would produce with `seed` (row pitch ld): the weights of
+ * a tensor-parallel shard, generated in place. */
+int psd_fill_uniform_bf16_block(void* out, int64_t ld, int rows, int cols, int64_t full_cols,
+                                int64_t row0, int64_t col0, uint64_t seed, float span,
+                                void* stream);
 
 /* ---- fused k-step greedy draft decode (csrc/decode_mk.cu) -------------------
  * One persistent kernel runs all k draft steps of a batch (embedding, every

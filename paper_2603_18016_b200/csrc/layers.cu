@@ -804,6 +804,23 @@ __global__ void fill_uniform_kernel(__nv_bfloat16* __restrict__ out, size_t n, u
   }
 }
 
+// rows [row0, row0 + rows) x cols [col0, col0 + cols) of a virtual row-major
+// tensor with `full_cols` columns, filled as fill_uniform_kernel would fill the
+// whole tensor (element index row * full_cols + col) -> a tensor-parallel shard
+// is generated in place, identical to the corresponding block of the full tensor
+__global__ void fill_uniform_block_kernel(__nv_bfloat16* __restrict__ out, int64_t ld, int rows,
+                                          int cols, int64_t full_cols, int64_t row0,
+                                          int64_t col0, uint64_t seed, float span) {
+  const size_t n = (size_t)rows * cols;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int64_t r = (int64_t)(i / cols), c = (int64_t)(i % cols);
+    const uint64_t idx = (uint64_t)((row0 + r) * full_cols + col0 + c);
+    const float u = (float)(splitmix_at(seed, idx) >> 40) * (1.0f / 16777216.0f);
+    out[r * ld + c] = __float2bfloat16((u - 0.5f) * span);
+  }
+}
+
 // dst[dst_rows[r] * dst_ld + c] = src[r * src_ld + c] (negative row: skip)
 __global__ void copy_rows_kernel(float* __restrict__ dst, const int32_t* __restrict__ dst_rows,
                                  int64_t dst_ld, const float* __restrict__ src,
@@ -866,6 +883,16 @@ int psd_fill_uniform_bf16(void* out, size_t n, uint64_t seed, float span, void* 
   psd::count_launches();
   fill_uniform_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(static_cast<__nv_bfloat16*>(out),
                                                                 n, seed, span);
+  return (int)cudaGetLastError();
+}
+
+int psd_fill_uniform_bf16_block(void* out, int64_t ld, int rows, int cols, int64_t full_cols,
+                                int64_t row0, int64_t col0, uint64_t seed, float span,
+                                void* stream) {
+  if (rows <= 0 || cols <= 0) return 0;
+  psd::count_launches();
+  fill_uniform_block_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(
+      static_cast<__nv_bfloat16*>(out), ld, rows, cols, full_cols, row0, col0, seed, span);
   return (int)cudaGetLastError();
 }
 

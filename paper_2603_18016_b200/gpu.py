@@ -60,7 +60,7 @@ class GpuBackend:
                  block_size: int = 16, num_blocks: int | None = None,
                  prefill_chunk_tokens: int = 4096, use_graphs: bool = True,
                  roles: tuple = ("target", "draft"), fused_draft: bool | None = None,
-                 mk_grid: int = 0) -> None:
+                 mk_grid: int = 0, tp=None) -> None:
         if not torch.cuda.is_available():
             raise native.NativeError("GpuBackend needs a CUDA device (no CPU fallback)")
         native.load()
@@ -91,8 +91,12 @@ class GpuBackend:
         self.roles = set(roles)
         has_t, has_d = "target" in self.roles, "draft" in self.roles
         with torch.cuda.device(dev):
+            # tp = (rank, size, process group): the target is a tensor-parallel
+            # shard (model.py); every TP rank runs the same scheduler (SPMD), the
+            # draft is replicated and K1 runs on the all-gathered logits
+            self.tp = tp
             self.target = Transformer(self.tshape, dev, seed * 2 + 1, num_blocks, block_size,
-                                      self.max_blocks) if has_t else None
+                                      self.max_blocks, tp=tp) if has_t else None
             self.draft = Transformer(self.dshape, dev, seed * 2 + 2, num_blocks, block_size,
                                      self.max_blocks) if has_d else None
             i32 = torch.int32

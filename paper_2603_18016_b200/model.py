@@ -88,6 +88,8 @@ PRESETS: dict[str, ModelShape] = {
                                None, tie_embeddings=True, qkv_bias=True, rms_eps=1e-6),
     # BASELINE config 1: tiny random-init pair
     "tiny-target": ModelShape("tiny-target", 1024, 256, 4, 8, 2, 32, 688, 10000.0),
+    # tiny target whose QKV shards stay 128-row aligned at TP = 2 (tests)
+    "tiny-target-tp": ModelShape("tiny-target-tp", 1024, 256, 4, 8, 4, 32, 688, 10000.0),
     "tiny-draft": ModelShape("tiny-draft", 1024, 128, 2, 4, 2, 32, 344, 10000.0),
 }
 
@@ -150,7 +152,12 @@ class Transformer:
     W_QKV, W_O, W_GATE, W_UP, W_DOWN, W_EMB, W_LM, B_QKV = range(8)
 
     def __init__(self, shape: ModelShape, device: torch.device, seed: int, num_blocks: int,
-                 block_size: int = 16, max_blocks_per_seq: int = 64) -> None:
+                 block_size: int = 16, max_blocks_per_seq: int = 64, tp=None) -> None:
+        self.tp = tp  # (rank, size, process group) or None
+        self.full_vocab = shape.vocab
+        if tp is not None and tp[1] > 1:
+            self._init_tp_shard(shape, device, seed, num_blocks, block_size, max_blocks_per_seq)
+            return
         if shape.qkv_out % 128 or shape.hidden % 128 or shape.vocab % 128:
             raise ConfigError(f"{shape.name}: GEMM output dims must be multiples of 128")
         self.shape = shape
@@ -208,6 +215,93 @@ class Transformer:
                               dtype=bf, device=dev)
         self.block_table = torch.zeros(0, dtype=torch.int32, device=dev)
 
+    def _init_tp_shard(self, full: ModelShape, device, seed, num_blocks, block_size,
+                       max_blocks) -> None:
+        """Megatron-style tensor-parallel shard of the target:
+        column-parallel QKV (this rank's query / kv heads) and gate/up (an FFN
+        slice), row-parallel O and down (their input columns; outputs are
+        partial sums, all-reduced in Forward.run), vocab-parallel LM head (a
+        vocab slice, all-gathered into full logit rows).  Every shard is the
+        exact block of the full random-init tensor (psd_fill_uniform_bf16_block),
+        so a TP forward computes the same function as the unsharded model."""
+        r, T, _ = self.tp
+        s = full
+        if s.heads % T or s.kv_heads % T or s.vocab % T:
+            raise ConfigError(f"{s.name}: heads / kv heads / vocab must divide by TP={T}")
+        D, H = s.head_dim, s.hidden
+        hq, hkv = s.heads // T, s.kv_heads // T
+        f_tp = -(-s.ffn // (64 * T)) * 64 * T
+        fl = f_tp // T
+        vs = s.vocab // T
+        vs_pad = -(-vs // 128) * 128
+        local = ModelShape(f"{s.name}-tp{r}of{T}", vs_pad, H, s.layers, hq, hkv, D, fl,
+                           s.rope_theta, s.rope_scaling, False, s.qkv_bias, s.rms_eps)
+        if local.qkv_out % 128 or H % 128:
+            raise ConfigError(f"{s.name}: TP={T} shard QKV rows {local.qkv_out} not 128-aligned")
+        self.shape = local
+        self.vocab_shard = vs
+        self.device = device
+        self.seed = seed
+        self.block_size = block_size
+        self.num_blocks = num_blocks
+        self.max_blocks = max_blocks
+        lib = native.load()
+        self._lib = lib
+        bf = torch.bfloat16
+        dev = device
+        st = _stream_ptr(dev)
+
+        def block(dst, rows, cols, full_cols, row0, col0, tseed):
+            _chk(lib.psd_fill_uniform_bf16_block(dst.data_ptr(), dst.stride(0), rows, cols,
+                                                 full_cols, row0, col0, tseed, INIT_SPAN, st),
+                 "psd_fill_uniform_bf16_block")
+
+        q0, k0, v0 = r * hq * D, s.heads * D + r * hkv * D, (s.heads + s.kv_heads) * D + r * hkv * D
+        self.layers = []
+        for li in range(s.layers):
+            tq = tensor_seed(seed, li, self.W_QKV)
+            wqkv = torch.empty(local.qkv_out, H, dtype=bf, device=dev)
+            block(wqkv[:hq * D], hq * D, H, H, q0, 0, tq)
+            block(wqkv[hq * D:(hq + hkv) * D], hkv * D, H, H, k0, 0, tq)
+            block(wqkv[(hq + hkv) * D:], hkv * D, H, H, v0, 0, tq)
+            wo = torch.empty(H, hq * D, dtype=bf, device=dev)
+            block(wo, H, hq * D, s.heads * D, 0, r * hq * D, tensor_seed(seed, li, self.W_O))
+            gate = torch.zeros(fl, H, dtype=bf, device=dev)
+            up = torch.zeros(fl, H, dtype=bf, device=dev)
+            real = max(0, min(s.ffn, (r + 1) * fl) - r * fl)
+            if real:
+                block(gate, real, H, H, r * fl, 0, tensor_seed(seed, li, self.W_GATE))
+                block(up, real, H, H, r * fl, 0, tensor_seed(seed, li, self.W_UP))
+            wgu = pack_gate_up(gate, up)
+            del gate, up
+            down = torch.zeros(H, fl, dtype=bf, device=dev)
+            if real:
+                block(down, H, real, s.ffn, 0, r * fl, tensor_seed(seed, li, self.W_DOWN))
+            bias = None
+            if s.qkv_bias:
+                tb = tensor_seed(seed, li, self.B_QKV)
+                bias = torch.empty(local.qkv_out, 1, dtype=bf, device=dev)
+                block(bias[:hq * D], hq * D, 1, 1, q0, 0, tb)
+                block(bias[hq * D:(hq + hkv) * D], hkv * D, 1, 1, k0, 0, tb)
+                block(bias[(hq + hkv) * D:], hkv * D, 1, 1, v0, 0, tb)
+                bias = bias.view(-1)
+            self.layers.append({
+                "attn_norm": torch.ones(H, dtype=bf, device=dev),
+                "wqkv": wqkv, "wo": wo,
+                "mlp_norm": torch.ones(H, dtype=bf, device=dev),
+                "wgu": wgu, "wdown": down, "bqkv": bias,
+            })
+        # embedding replicated (every token id is looked up on every rank)
+        self.embed = torch.empty(s.vocab, H, dtype=bf, device=dev)
+        block(self.embed, s.vocab, H, H, 0, 0, tensor_seed(seed, -1, self.W_EMB))
+        self.lm_head = torch.zeros(vs_pad, H, dtype=bf, device=dev)
+        lm_seed = tensor_seed(seed, -1, self.W_EMB if s.tie_embeddings else self.W_LM)
+        block(self.lm_head, vs, H, H, r * vs, 0, lm_seed)
+        self.final_norm = torch.ones(H, dtype=bf, device=dev)
+        self.inv_freq = torch.from_numpy(rope_inv_freq(s)).to(dev)
+        self.kv = torch.zeros(s.layers, 2, num_blocks * block_size, hkv, D, dtype=bf, device=dev)
+        self.block_table = torch.zeros(0, dtype=torch.int32, device=dev)
+
     def kv_bytes_per_block(self) -> int:
         s = self.shape
         return s.layers * 2 * self.block_size * s.kv_heads * s.head_dim * 2
@@ -246,6 +340,10 @@ class Forward:
         self.act = torch.empty(T, s.ffn_padded, dtype=bf, device=dev)
         self.xf = torch.empty(max_logit_rows, s.hidden, dtype=bf, device=dev)
         self.prev = torch.empty(max_logit_rows, dtype=torch.int32, device=dev)
+        if model.tp is not None and model.tp[1] > 1:
+            self.lshard = torch.empty(max_logit_rows * s.vocab, dtype=torch.float32, device=dev)
+            self.lgather = torch.empty(model.tp[1] * max_logit_rows * s.vocab,
+                                       dtype=torch.float32, device=dev)
         # stream-K GEMM workspace (partials + tickets): zeroed once, left zeroed
         import ctypes
         lib = native.load()
@@ -294,6 +392,23 @@ class Forward:
         self._host_np = self.meta_host.numpy()
         self._events = [None] * self.ring
         self._cur = 0
+
+    # ---- tensor parallelism (target TP) ---------------------
+    def _allreduce(self, n: int) -> None:
+        """Sum the ranks' row-parallel partial outputs (fp32 split-K partials:
+        the sum is linear, so the consumer's split reduction stays unchanged)."""
+        import torch.distributed as dist
+        dist.all_reduce(self.part[:n], group=self.model.tp[2])
+
+    def _gather_logits(self, logits: torch.Tensor, ld: int, R: int) -> None:
+        import torch.distributed as dist
+        m = self.model
+        T = m.tp[1]
+        vp, vs = m.shape.vocab, m.vocab_shard
+        parts = list(self.lgather[:T * R * vp].view(T, R * vp).unbind(0))
+        dist.all_gather(parts, self.lshard[:R * vp], group=m.tp[2])
+        full = logits.view(-1)[:R * ld].view(R, ld)[:, :T * vs].view(R, T, vs)
+        full.copy_(self.lgather[:T * R * vp].view(T, R, vp)[:, :, :vs].permute(1, 0, 2))
 
     def view(self, name: str, set_index: int = 0) -> torch.Tensor:
         o, n = self._offsets[name]
@@ -348,6 +463,7 @@ class Forward:
         # QKV / O / down: grid split-K GEMMs (few weight tiles) whose fp32
         # partials are reduced inside the consumer kernel (RoPE, add+RMSNorm);
         # gate/up and the LM head: stream-K persistent GEMMs
+        tp = m.tp if (m.tp is not None and m.tp[1] > 1) else None
         prev_S = 0  # splits of the pending down-proj partials (0 = none)
         # draft decode (<= 2 query tokens per sequence): RoPE fused into the
         # attention kernel (-3 % per draft step); at verify widths (k + 1 tokens)
@@ -390,6 +506,8 @@ class Forward:
                      "attention")
             _chk(lib.psd_gemm_partials(self.attn.data_ptr(), Dq, M, Dq, L["wo"].data_ptr(), Dq, H,
                                        part, partn, 0, nsp, st), "gemm o")
+            if tp:  # row-parallel O: sum the ranks' partial outputs
+                self._allreduce(nsp._obj.value * M * H)
             _chk(lib.psd_add_rmsnorm(X, H, part, nsp._obj.value, M * H, H, None,
                                      L["mlp_norm"].data_ptr(), self.xn.data_ptr(), H, M, H,
                                      s.rms_eps, 1, st), "add+mlp norm")
@@ -398,6 +516,8 @@ class Forward:
                                    st), "gemm gate/up")
             _chk(lib.psd_gemm_partials(self.act.data_ptr(), Fp, M, Fp, L["wdown"].data_ptr(), Fp,
                                        H, part, partn, 0, nsp, st), "gemm down")
+            if tp:  # row-parallel down
+                self._allreduce(nsp._obj.value * M * H)
             prev_S = nsp._obj.value
         if n_logit_rows == 0 or logits is None:
             return  # prefill: only the KV cache is needed
@@ -405,10 +525,18 @@ class Forward:
         _chk(lib.psd_add_rmsnorm(X, H, part, prev_S, M * H, H, v["logit_rows"].data_ptr(),
                                  m.final_norm.data_ptr(), self.xf.data_ptr(), H, R, H, s.rms_eps,
                                  0, st), "final norm")
-        ld = logits_ld or s.vocab
-        _chk(lib.psd_gemm_bf16(self.xf.data_ptr(), H, R, H, m.lm_head.data_ptr(), H, s.vocab,
-                               logits.data_ptr(), ld, native.EPI_F32, None, 0, 0, ws, wsn, st),
-             "gemm lm_head")
+        V = m.full_vocab
+        ld = logits_ld or V
+        if tp:
+            # vocab-parallel LM head: this rank's slice, all-gathered into full rows
+            _chk(lib.psd_gemm_bf16(self.xf.data_ptr(), H, R, H, m.lm_head.data_ptr(), H, s.vocab,
+                                   self.lshard.data_ptr(), s.vocab, native.EPI_F32, None, 0, 0,
+                                   ws, wsn, st), "gemm lm_head shard")
+            self._gather_logits(logits, ld, R)
+        else:
+            _chk(lib.psd_gemm_bf16(self.xf.data_ptr(), H, R, H, m.lm_head.data_ptr(), H, s.vocab,
+                                   logits.data_ptr(), ld, native.EPI_F32, None, 0, 0, ws, wsn, st),
+                 "gemm lm_head")
         if bigram is not None:
             succ, beta = bigram
             if beta != 0.0:
@@ -416,4 +544,4 @@ class Forward:
                 _chk(lib.psd_index_copy_i32(self.prev.data_ptr(), None, v["tokens"].data_ptr(),
                                             v["logit_rows"].data_ptr(), R, st), "prev tokens")
                 _chk(lib.psd_bigram_bias(logits.data_ptr(), ld, self.prev.data_ptr(), R,
-                                         succ.data_ptr(), s.vocab, float(beta), st), "bigram")
+                                         succ.data_ptr(), V, float(beta), st), "bigram")

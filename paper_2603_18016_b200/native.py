@@ -54,6 +54,8 @@ SIGNATURES: dict[str, tuple] = {
     "psd_commit": (_i, [_p, _p, _i, _p, _i, _p, _p, _i, _p, _i, _p]),
     "psd_index_copy_i32": (_i, [_p, _p, _p, _p, _i, _p]),
     "psd_fill_uniform_bf16": (_i, [_p, _sz, _c.c_uint64, _f, _p]),
+    "psd_fill_uniform_bf16_block": (_i, [_p, _i64, _i, _i, _i64, _i64, _i64, _c.c_uint64, _f,
+                                         _p]),
     "psd_launch_count": (_c.c_longlong, []),
     "psd_gemm_set_max_ctas": (None, [_i]),
     "psd_mk_smem_bytes": (_sz, []),
