@@ -41,6 +41,10 @@ sys.path.insert(0, ROOT)
 
 CFG = dict(target="llama-3.1-8b", draft="llama-3.2-1b", m=32, n_requests=64, k=5,
            prompt=128, output=256)
+# BASELINE config 4 (--layout tp): Llama-3.1-70B target tensor-parallel over all
+# ranks, Llama-3.2-1B draft replicated on each, 2 x 64 requests, k = 4
+CFG4 = dict(target="llama-3.1-70b", draft="llama-3.2-1b", m=64, n_requests=128, k=4,
+            prompt=128, output=256)
 BETA_TARGET = 7.0
 BETA_DRAFT = 16.0
 METRIC = "PSD output tok/s vs sequential SD, mean accepted len; verify-kernel HBM GB/s"
@@ -297,14 +301,20 @@ def run_ours(args) -> None:
 
     hbm_peak, bf16_peak, peak_kind = _peaks()
     pairs = args.layout == "pairs"
+    tp_layout = args.layout == "tp"
+    if tp_layout:
+        CFG.update(CFG4)
     if pairs and world % 2:
         raise SystemExit("--layout pairs needs an even number of GPUs")
     # replicas: every rank = target + draft on one GPU (two streams)
     # pairs: even rank = target GPU (scheduler), odd rank = dedicated draft GPU
     roles = ("target", "draft") if not pairs else (("target",) if rank % 2 == 0 else ("draft",))
     replica = rank // 2 if pairs else rank
+    tp = (rank, world, torch.distributed.group.WORLD) if tp_layout and world > 1 else None
+    if tp_layout:
+        replica = 0  # one replica spread over all ranks (SPMD scheduler)
     be = GpuBackend(CFG["target"], CFG["draft"], max_requests=CFG["n_requests"],
-                    max_batch=CFG["n_requests"], k_max=CFG["k"],
+                    max_batch=CFG["n_requests"], k_max=CFG["k"], tp=tp,
                     max_seq_len=CFG["prompt"] + CFG["output"] + 16, seed=replica,
                     beta_target=BETA_TARGET, beta_draft=BETA_DRAFT, device=dev, roles=roles)
     is_draft_rank = pairs and rank % 2 == 1
@@ -361,6 +371,8 @@ def run_ours(args) -> None:
         launches[mode] = be.launches - l0
         ms_local = e0.elapsed_time(e1)
         tokens, ms = pd.aggregate(sum(r.total_generated for r in reps), ms_local, dev)
+        if tp_layout:
+            tokens //= world  # every TP rank emits the same tokens
         results[mode] = {"ms": ms, "tokens": tokens, "reps": reps, "states": states,
                          "clocks": clocks.stop() if clocks else None,
                          "draft_ms": backend.stats["draft_ms"] - stats0["draft_ms"],
@@ -404,13 +416,19 @@ def run_ours(args) -> None:
         "metric": METRIC, "value": round(value, 1), "unit": "tok/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(psd["ms"] / args.steps, 2), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": "cfg2: Llama-3.1-8B target / Llama-3.2-1B draft shapes, "
-                               "random-init bf16, 2x32 requests, k=5, prompt 128, output 256, "
-                               "greedy, 1 GPU per replica (draft / verify on separate streams)",
-                   "global_batch": (world // 2 if pairs else world) * CFG["n_requests"],
+        "scaling": "strong" if tp_layout else "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic",
+        "config": {"workload": ("cfg4: Llama-3.1-70B target (tensor-parallel over all GPUs) / "
+                                "Llama-3.2-1B draft shapes, random-init bf16, 2x64 requests, "
+                                "k=4, prompt 128, output 256, greedy" if tp_layout else
+                                "cfg2: Llama-3.1-8B target / Llama-3.2-1B draft shapes, "
+                                "random-init bf16, 2x32 requests, k=5, prompt 128, output 256, "
+                                "greedy, 1 GPU per replica (draft / verify on separate streams)"),
+                   "global_batch": (1 if tp_layout else world // 2 if pairs else world)
+                   * CFG["n_requests"],
                    "seq_len": CFG["prompt"] + CFG["output"],
-                   "parallelism": f"pairs{world // 2}" if pairs else f"replicas{world}",
+                   "parallelism": (f"tp{world}" if tp_layout else
+                                   f"pairs{world // 2}" if pairs else f"replicas{world}"),
                    "l2": "inputs > L2 (weights 18.5 GB streamed per step)",
                    "synthetic_language_beta": [BETA_TARGET, BETA_DRAFT]},
         "sd": {"value": round(sd_value, 1), "unit": "tok/s",
@@ -448,9 +466,10 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--layout", default="replicas", choices=["replicas", "pairs"],
+    ap.add_argument("--layout", default="replicas", choices=["replicas", "pairs", "tp"],
                     help="replicas: each GPU runs target+draft (two streams); pairs: "
-                         "dedicated draft GPU per target GPU (NCCL hand-off, pair.py)")
+                         "dedicated draft GPU per target GPU (NCCL hand-off, pair.py); tp: "
+                         "BASELINE config 4, 70B target tensor-parallel over all GPUs")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
