@@ -45,6 +45,9 @@ CFG = dict(target="llama-3.1-8b", draft="llama-3.2-1b", m=32, n_requests=64, k=5
 # ranks, Llama-3.2-1B draft replicated on each, 2 x 64 requests, k = 4
 CFG4 = dict(target="llama-3.1-70b", draft="llama-3.2-1b", m=64, n_requests=128, k=4,
             prompt=128, output=256)
+# the 70B's random logits spread ~sqrt(8192 / 4096) wider than the 8B's, so its
+# synthetic-language bias scales with it (same acceptance regime as cfg2)
+BETA_TARGET_CFG4 = 10.0
 BETA_TARGET = 7.0
 BETA_DRAFT = 16.0
 METRIC = "PSD output tok/s vs sequential SD, mean accepted len; verify-kernel HBM GB/s"
@@ -168,10 +171,12 @@ def kernel_rooflines(backend, hbm_peak: float) -> tuple[dict, dict]:
 
     ms = _time_kernel(gemm, 64)
     nbytes = w.numel() * 2 + x.numel() * 2 + out.numel() * 2
-    roof = {"kernel": "gemm_sk_kernel<192,SILU> (verify gate/up, M=192 N=28672 K=4096)",
+    roof = {"kernel": f"gemm_sk_kernel<SILU> (verify gate/up, M={M} N={w.shape[0]} "
+                      f"K={s.hidden})",
             "bound": "hbm", "achieved": round(nbytes / (ms * 1e-3) / 1e9, 1),
             "peak": hbm_peak, "unit": "GB/s",
-            "frac": round(nbytes / (ms * 1e-3) / 1e9 / hbm_peak, 4), "traffic": _ncu_traffic(),
+            "frac": round(nbytes / (ms * 1e-3) / 1e9 / hbm_peak, 4), "traffic": (_ncu_traffic() if (M, w.shape[0], s.hidden) == (192, 28672, 4096)
+                                   else None),
             "bytes_per_launch": nbytes, "us_per_launch": round(ms * 1e3, 2),
             "tflops": round(2 * M * w.shape[0] * s.hidden / (ms * 1e-3) / 1e12, 1)}
     B, K, V = CFG["m"], CFG["k"], s.vocab
@@ -304,6 +309,8 @@ def run_ours(args) -> None:
     tp_layout = args.layout == "tp"
     if tp_layout:
         CFG.update(CFG4)
+        global BETA_TARGET
+        BETA_TARGET = BETA_TARGET_CFG4
     if pairs and world % 2:
         raise SystemExit("--layout pairs needs an even number of GPUs")
     # replicas: every rank = target + draft on one GPU (two streams)
