@@ -67,3 +67,23 @@ def test_gemm_silu_mul(cuda_device, M, splits):
     gt = _ref(x, wg)
     ref = torch.nn.functional.silu(gt) * _ref(x, wu)
     _close(y, ref, K)
+
+
+@pytest.mark.parametrize("M,N,K", [(192, 6144, 4096), (192, 4096, 14336), (32, 3072, 2048),
+                                   (32, 2048, 8192), (320, 2560, 8192)])
+def test_gemm_partials_sum(cuda_device, M, N, K):
+    """psd_gemm_partials: the sum of the returned split slices equals x @ w.T
+    (split-K reduced through DSMEM inside a (1, 1, S) cluster when S <= 8)."""
+    import ctypes
+    g = torch.Generator(device=cuda_device).manual_seed(M + N + K)
+    x = torch.randn(M, K, device=cuda_device, generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device=cuda_device, generator=g) * 0.05).to(torch.bfloat16)
+    part = torch.full((16 * M * N,), float("nan"), device=cuda_device)
+    sp = ctypes.c_int()
+    lib = native.load()
+    native.check(lib.psd_gemm_partials(x.data_ptr(), K, M, K, w.data_ptr(), K, N,
+                                       part.data_ptr(), part.numel() * 4, 0, ctypes.byref(sp),
+                                       torch.cuda.current_stream().cuda_stream), "partials")
+    torch.cuda.synchronize()
+    got = part[:sp.value * M * N].view(sp.value, M, N).sum(0)
+    _close(got, _ref(x, w), K)
