@@ -1046,6 +1046,13 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
   if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(W)) & 15)
     return (int)cudaErrorMisalignedAddress;
   if ((ldx % 8) || (ldw % 8)) return (int)cudaErrorMisalignedAddress;
+  if (splits_hint == 0 && M > 0 && N % BM == 0) {
+    // one wave of whole-K tiles (>= 3/4 of the SMs busy, no tail): the plain
+    // grid kernel beats stream-K, whose fix-ups buy nothing here (1B draft
+    // gate/up at M = 32: 14.3 vs 19.8 us, profiles/r01b_kbench_gemm_splits.txt)
+    const int tiles = (N / BM) * ((M + token_tile(M) - 1) / token_tile(M));
+    if (tiles <= num_sms() && 4 * tiles >= 3 * num_sms()) splits_hint = 1;
+  }
   if (splits_hint == 0) {
     // stream-K persistent path (default)
     if (M <= 0 || N <= 0 || K <= 0 || (K % 8) || (N % BM)) return (int)cudaErrorInvalidValue;

@@ -62,7 +62,7 @@ def report(name, shape, us, nbytes, flops=0):
           + (f" {r['TFLOPs']:7.1f} TF/s" if flops else ""), flush=True)
 
 
-def gemm_case(tag, M, N, K, epi, copies=6, legacy=False, tiled=False):
+def gemm_case(tag, M, N, K, epi, copies=6, legacy=False, tiled=False, splits=None):
     x = torch.randn(M, K, device=dev).to(bf)
     ws = [(torch.randn(N, K, device=dev) * 0.02).to(bf) for _ in range(copies)]
     if tiled:
@@ -111,9 +111,10 @@ def gemm_case(tag, M, N, K, epi, copies=6, legacy=False, tiled=False):
         wsp = torch.zeros(64 << 20, dtype=torch.uint8, device=dev)
         it = [0]
 
+        sp_arg = splits if splits is not None else (-1 if legacy else 0)
+
         def fn():
-            ops.gemm(x, ws[it[0] % copies], out=out, epi=e, workspace=wsp,
-                     splits=-1 if legacy else 0)
+            ops.gemm(x, ws[it[0] % copies], out=out, epi=e, workspace=wsp, splits=sp_arg)
             it[0] += 1
         us = timeit(fn)
         out_bytes = out.numel() * out.element_size()
@@ -271,6 +272,12 @@ def main():
         gemm_case("1B gate/up", 32, 16384, 2048, "silu")
         gemm_case("1B down part", 32, 2048, 8192, "partial")
         gemm_case("1B lm_head", 32, 128256, 2048, "f32", copies=2)
+    if want("gemmsp"):
+        for sp in (None, 1, 2):
+            gemm_case(f"1B gate/up sp{sp}", 32, 16384, 2048, "silu", splits=sp)
+            gemm_case(f"1B gate/up M64 sp{sp}", 64, 16384, 2048, "silu", splits=sp)
+            gemm_case(f"8B gate/up sp{sp}", 192, 28672, 4096, "silu", splits=sp)
+            gemm_case(f"1B lm sp{sp}", 32, 128256, 2048, "f32", copies=2, splits=sp)
     if want("gemmgu"):
         gemm_case("8B gate/up", 192, 28672, 4096, "silu")
     if want("attn1b"):
