@@ -90,16 +90,17 @@ def gemm_case(tag, M, N, K, epi, copies=6, legacy=False, tiled=False, splits=Non
         report(f"gemm {tag} tiled", f"M={M} N={N} K={K}", us, nbytes, 2 * M * N * K)
         return
     if epi == "partial":
-        part = torch.empty(8 * M * N, dtype=torch.float32, device=dev)
+        part = torch.empty(16 * M * N, dtype=torch.float32, device=dev)
         sp = ctypes.c_int()
         it = [0]
+        hint = splits or 0
 
         def fn():
             st = torch.cuda.current_stream().cuda_stream
             w = ws[it[0] % copies]
             it[0] += 1
             rc = lib.psd_gemm_partials(x.data_ptr(), K, M, K, w.data_ptr(), K, N, part.data_ptr(),
-                                       part.numel() * 4, 0, ctypes.byref(sp), st)
+                                       part.numel() * 4, hint, ctypes.byref(sp), st)
             assert rc == 0
         us = timeit(fn)
         out_bytes = sp.value * M * N * 4
@@ -278,6 +279,12 @@ def main():
             gemm_case(f"1B gate/up M64 sp{sp}", 64, 16384, 2048, "silu", splits=sp)
             gemm_case(f"8B gate/up sp{sp}", 192, 28672, 4096, "silu", splits=sp)
             gemm_case(f"1B lm sp{sp}", 32, 128256, 2048, "f32", copies=2, splits=sp)
+    if want("gemmpart"):
+        for (tag, M, N, K) in (("1B qkv", 32, 3072, 2048), ("1B o", 32, 2048, 2048),
+                               ("1B down", 32, 2048, 8192), ("8B qkv", 192, 6144, 4096),
+                               ("8B o", 192, 4096, 4096), ("8B down", 192, 4096, 14336)):
+            for sp in (None, 2, 3, 4, 6, 8, 12, 16):
+                gemm_case(f"{tag} part", M, N, K, "partial", splits=sp)
     if want("gemmgu"):
         gemm_case("8B gate/up", 192, 28672, 4096, "silu")
     if want("attn1b"):
