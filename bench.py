@@ -48,6 +48,12 @@ CFG4 = dict(target="llama-3.1-70b", draft="llama-3.2-1b", m=64, n_requests=128, 
 # the 70B's random logits spread ~sqrt(8192 / 4096) wider than the 8B's, so its
 # synthetic-language bias scales with it (same acceptance regime as cfg2)
 BETA_TARGET_CFG4 = 10.0
+# BASELINE config 3 (--workload cfg3): Qwen2.5-7B target / Qwen2.5-0.5B draft,
+# temperature-1.0 rejection sampling over the 152k vocabulary (V_draft 151936 <
+# V_target 152064), 2 x 32 requests, k = 4; both models on one GPU here
+CFG3 = dict(target="qwen2.5-7b", draft="qwen2.5-0.5b", m=32, n_requests=64, k=4,
+            prompt=128, output=256)
+BETAS_CFG3 = (14.0, 14.0)  # sampling at T = 1: bias e^14 dominates 152k near-uniform logits
 BETA_TARGET = 7.0
 BETA_DRAFT = 16.0
 METRIC = "PSD output tok/s vs sequential SD, mean accepted len; verify-kernel HBM GB/s"
@@ -307,10 +313,14 @@ def run_ours(args) -> None:
     hbm_peak, bf16_peak, peak_kind = _peaks()
     pairs = args.layout == "pairs"
     tp_layout = args.layout == "tp"
+    global BETA_TARGET, BETA_DRAFT
     if tp_layout:
         CFG.update(CFG4)
-        global BETA_TARGET
         BETA_TARGET = BETA_TARGET_CFG4
+    sampling = args.workload == "cfg3"
+    if sampling:
+        CFG.update(CFG3)
+        BETA_TARGET, BETA_DRAFT = BETAS_CFG3
     if pairs and world % 2:
         raise SystemExit("--layout pairs needs an even number of GPUs")
     # replicas: every rank = target + draft on one GPU (two streams)
@@ -323,7 +333,8 @@ def run_ours(args) -> None:
     be = GpuBackend(CFG["target"], CFG["draft"], max_requests=CFG["n_requests"],
                     max_batch=CFG["n_requests"], k_max=CFG["k"], tp=tp,
                     max_seq_len=CFG["prompt"] + CFG["output"] + 16, seed=replica,
-                    beta_target=BETA_TARGET, beta_draft=BETA_DRAFT, device=dev, roles=roles)
+                    beta_target=BETA_TARGET, beta_draft=BETA_DRAFT, device=dev, roles=roles,
+                    mode="sample" if sampling else "greedy", temperature=1.0)
     is_draft_rank = pairs and rank % 2 == 1
     backend = be
     if pairs:
@@ -425,7 +436,11 @@ def run_ours(args) -> None:
         "ms_per_step": round(psd["ms"] / args.steps, 2), "higher_is_better": True,
         "scaling": "strong" if tp_layout else "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic",
-        "config": {"workload": ("cfg4: Llama-3.1-70B target (tensor-parallel over all GPUs) / "
+        "config": {"workload": ("cfg3: Qwen2.5-7B target / Qwen2.5-0.5B draft shapes, "
+                                "random-init bf16, 2x32 requests, k=4, prompt 128, output 256, "
+                                "T=1.0 rejection sampling, both models on one GPU"
+                                if sampling else
+                                "cfg4: Llama-3.1-70B target (tensor-parallel over all GPUs) / "
                                 "Llama-3.2-1B draft shapes, random-init bf16, 2x64 requests, "
                                 "k=4, prompt 128, output 256, greedy" if tp_layout else
                                 "cfg2: Llama-3.1-8B target / Llama-3.2-1B draft shapes, "
@@ -473,6 +488,9 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3"],
+                    help="cfg2: 8B / 1B greedy (the headline); cfg3: Qwen2.5-7B / 0.5B, "
+                         "T = 1.0 rejection sampling over the 152k vocabulary")
     ap.add_argument("--layout", default="replicas", choices=["replicas", "pairs", "tp"],
                     help="replicas: each GPU runs target+draft (two streams); pairs: "
                          "dedicated draft GPU per target GPU (NCCL hand-off, pair.py); tp: "
