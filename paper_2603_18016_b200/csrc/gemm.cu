@@ -40,26 +40,7 @@ constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int kThreads = 192;
 constexpr int kMaxTiles = 1 << 16;  // stream-K tickets reserved at the workspace head
-// weight k-blocks prefetched into L2 ahead of the smem ring; 0 = off.
-// PSD_GEMM_PREFETCH overrides (tuning experiments)
-int silu_mode() {
-  static int v = [] {
-    const char* e = getenv("PSD_SILU_MODE");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
-int prefetch_depth() {
-  static int v = [] {
-    const char* e = getenv("PSD_GEMM_PREFETCH");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
 struct GemmArgs {
-  int prefetch;  // weight k-blocks prefetched into L2 ahead of the smem ring
   int M, N, K;
   int kb_total, kb_per_split;
   void* Y;
@@ -76,8 +57,7 @@ struct Cfg {
   static constexpr int MAXS = (200 * 1024) / STAGE;
   static constexpr int STAGES = MAXS > 8 ? 8 : MAXS;
   static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
-  static constexpr int XCHG_BYTES = 64 * 17 * 4;
-  static constexpr int SMEM = 1024 + STAGES * STAGE + 256 + XCHG_BYTES;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + 256;
 };
 
 // silu(x) = x * sigmoid(x) = 0.5 x (1 + tanh(x / 2)): one MUFU.TANH per element
@@ -155,7 +135,6 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUt
   uint64_t* empty = full + C::STAGES;
   uint64_t* accum = empty + C::STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
-  float* xchg = reinterpret_cast<float*>(full + 32);  // after the 256 B barrier area
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * BM, m0 = blockIdx.y * BN, z = blockIdx.z;
@@ -182,11 +161,6 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUt
     if (lane == 0) {
       const uint64_t pol_w = policy_evict_first();
       const uint64_t pol_x = policy_evict_last();
-      const uint64_t pol_pf = policy_evict_last();
-      // L2 prefetch runs kPrefetch k-blocks ahead of the smem ring
-      const int pf = g.prefetch;
-      const int npf = pf > 0 ? min(nkb, pf) : 0;
-      for (int i = 0; i < npf; ++i) tma_prefetch_l2_2d(&tmW, (kb0 + i) * BK, n0, pol_pf);
       // PDL: weights do not depend on the predecessor kernel -> the first
       // stages' weight tiles stream while it drains; tokens after pdl_wait()
       const int npre = min(nkb, C::STAGES);
@@ -200,7 +174,6 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUt
       for (int i = npre; i < nkb; ++i) {
         const int s = i % C::STAGES;
         const uint32_t ph = (i / C::STAGES) & 1;
-        if (pf > 0 && i + pf < nkb) tma_prefetch_l2_2d(&tmW, (kb0 + i + pf) * BK, n0, pol_pf);
         mbar_wait(empty + s, ph ^ 1);
         mbar_arrive_expect_tx(full + s, C::STAGE);
         const int kc = (kb0 + i) * BK;
@@ -379,8 +352,6 @@ struct SKArgs {
   float* part;    // [G][2][BN * 128]
   int* tickets;   // [tiles], zero between launches
   const __nv_bfloat16* Wt;  // pre-tiled weights (TILED variant)
-  int silu_mode;            // tuning experiment: 0 silu(g)*u, 1 g*u, 2 g only
-  int prefetch;             // weight k-blocks prefetched into L2 ahead of the ring
 };
 
 struct Seg {
@@ -417,7 +388,6 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   uint64_t* tempty = tfull + 2;          // [2] accumulator drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   int* s_flag = reinterpret_cast<int*>(tmem_slot + 1);
-  float* xchg = reinterpret_cast<float*>(full + 32);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x;
@@ -480,25 +450,12 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           }
         }
       }
-      // L2 prefetch of the weight k-blocks g.prefetch units ahead of the ring
-      // (keeps HBM requests in flight beyond what the smem stages hold)
-      const int pf = TILED ? 0 : g.prefetch;
-      long long upf = u0 + npre;
-      const long long upf_end = u1;
-      auto prefetch_to = [&](long long limit) {
-        for (; upf < limit && upf < upf_end; ++upf) {
-          const int tt = (int)(upf / g.KB), kk = (int)(upf % g.KB);
-          tma_prefetch_l2_2d(&tmW, kk * BK, (tt / g.MT) * BM, pol_w);
-        }
-      };
-      if (pf > 0) prefetch_to(u0 + npre + pf);
       pdl_wait();
       while (next_seg(u, sg)) {
         const int n0 = (sg.t / g.MT) * BM, m0 = (sg.t % g.MT) * BN;
         for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++i) {
           const int s = i % C::STAGES;
           const uint32_t ph = (i / C::STAGES) & 1;
-          if (pf > 0) prefetch_to(u0 + i + 1 + pf);
           if (i < npre) {  // weight tile already in flight
             tma_load_2d(sB + s * C::B_BYTES, &tmX, full + s, kb * BK, m0, pol_x);
             continue;
@@ -618,16 +575,9 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
             const int jo = (n0 / BM) * 64 + 16 * q + (lane & 15);
             __nv_bfloat16* Y = static_cast<__nv_bfloat16*>(g.Y);
 #pragma unroll
-            if (g.silu_mode == 2) {
-            } else if (g.silu_mode == 1) {
-#pragma unroll
-              for (int k = 0; k < 16; ++k) v[k] *= __shfl_down_sync(0xffffffffu, v[k], 16);
-            } else {
-#pragma unroll
-              for (int k = 0; k < 16; ++k) {
-                const float up = __shfl_down_sync(0xffffffffu, v[k], 16);
-                v[k] = silu(v[k]) * up;  // all lanes: no divergence in the math
-              }
+            for (int k = 0; k < 16; ++k) {
+              const float up = __shfl_down_sync(0xffffffffu, v[k], 16);
+              v[k] = silu(v[k]) * up;  // all lanes: no divergence in the math
             }
             if (lane < 16) {
 #pragma unroll
@@ -995,8 +945,6 @@ int psd_gemm_tiled(const void* X, int ldx, int M, int K, const void* W_tiled, in
   g.tickets = static_cast<int*>(workspace);
   g.part = reinterpret_cast<float*>(static_cast<char*>(workspace) + p.ticket_bytes);
   g.Wt = static_cast<const __nv_bfloat16*>(W_tiled);
-  g.silu_mode = silu_mode();
-  g.prefetch = 0;
   cudaStream_t st = (cudaStream_t)stream;
   switch (epi) {
     case PSD_EPI_BF16: return launch_sk<PSD_EPI_BF16, true>(p.bn, mx, mx, g, st);
@@ -1026,7 +974,6 @@ int psd_gemm_partials(const void* X, int ldx, int M, int K, const void* W, int l
   if ((rc = make_map(&mw, W, N, K, ldw, BM))) return rc;
   if ((rc = make_map(&mx, X, M, K, ldx, pair ? bn / 2 : bn))) return rc;
   GemmArgs g;
-  g.prefetch = prefetch_depth();
   g.M = M; g.N = N; g.K = K;
   g.kb_total = (K + BK - 1) / BK;
   g.kb_per_split = (g.kb_total + splits - 1) / splits;
@@ -1070,8 +1017,6 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
     g.tickets = static_cast<int*>(workspace);
     g.part = reinterpret_cast<float*>(static_cast<char*>(workspace) + p.ticket_bytes);
     g.Wt = nullptr;
-    g.silu_mode = silu_mode();
-    g.prefetch = prefetch_depth();
     cudaStream_t st = (cudaStream_t)stream;
     switch (epi) {
       case PSD_EPI_BF16: return launch_sk<PSD_EPI_BF16>(p.bn, mw, mx, g, st);
@@ -1098,7 +1043,6 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
   if ((rc = make_map(&mw, W, N, K, ldw, BM))) return rc;
   if ((rc = make_map(&mx, X, M, K, ldx, pair ? bn / 2 : bn))) return rc;
   GemmArgs g;
-  g.prefetch = prefetch_depth();
   g.M = M; g.N = N; g.K = K;
   g.kb_total = (K + BK - 1) / BK;
   g.kb_per_split = (g.kb_total + splits - 1) / splits;
