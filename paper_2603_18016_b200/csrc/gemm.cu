@@ -49,14 +49,17 @@ struct GemmArgs {
   int ldr;
 };
 
-template <int BN>
+// NT token tiles of BN rows per weight tile (NT = 2 for 256 < M <= 512: every
+// weight byte is streamed once instead of once per token tile)
+template <int BN, int NT = 1>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = NT * BN * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int MAXS = (200 * 1024) / STAGE;
   static constexpr int STAGES = MAXS > 8 ? 8 : MAXS;
-  static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  static constexpr int TMEM_COLS = NT * BN <= 32 ? 32 : NT * BN <= 64 ? 64
+                                 : NT * BN <= 128 ? 128 : NT * BN <= 256 ? 256 : 512;
   static constexpr int SMEM = 1024 + STAGES * STAGE + 256;
 };
 
@@ -121,11 +124,11 @@ __device__ __forceinline__ void tile_epilogue(const GemmArgs& g, uint32_t tmem, 
     }
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, int NT = 1>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
             const GemmArgs g) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, NT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -137,7 +140,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUt
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * BM, m0 = blockIdx.y * BN, z = blockIdx.z;
+  const int n0 = blockIdx.x * BM, m0 = blockIdx.y * (NT * BN), z = blockIdx.z;
   const int kb0 = z * g.kb_per_split;
   const int nkb = min(g.kb_total, kb0 + g.kb_per_split) - kb0;
 
@@ -152,6 +155,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUt
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  constexpr int TB = BN * BK * 2;  // bytes of one token tile's k-block
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -170,7 +174,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUt
       }
       pdl_wait();
       for (int i = 0; i < npre; ++i)
-        tma_load_2d(sB + i * C::B_BYTES, &tmX, full + i, (kb0 + i) * BK, m0, pol_x);
+#pragma unroll
+        for (int h = 0; h < NT; ++h)
+          tma_load_2d(sB + i * C::B_BYTES + h * TB, &tmX, full + i, (kb0 + i) * BK, m0 + h * BN,
+                      pol_x);
       for (int i = npre; i < nkb; ++i) {
         const int s = i % C::STAGES;
         const uint32_t ph = (i / C::STAGES) & 1;
@@ -178,7 +185,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUt
         mbar_arrive_expect_tx(full + s, C::STAGE);
         const int kc = (kb0 + i) * BK;
         tma_load_2d(sA + s * C::A_BYTES, &tmW, full + s, kc, n0, pol_w);
-        tma_load_2d(sB + s * C::B_BYTES, &tmX, full + s, kc, m0, pol_x);
+#pragma unroll
+        for (int h = 0; h < NT; ++h)
+          tma_load_2d(sB + s * C::B_BYTES + h * TB, &tmX, full + s, kc, m0 + h * BN, pol_x);
       }
       pdl_trigger();
     }
@@ -194,8 +203,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUt
         const uint32_t b = smem_u32(sB + s * C::B_BYTES);
 #pragma unroll
         for (int kk = 0; kk < BK / 16; ++kk)
-          mma_bf16(tmem, umma_desc_sw128(a + kk * 32), umma_desc_sw128(b + kk * 32), idesc,
-                   (i | kk) != 0);
+#pragma unroll
+          for (int h = 0; h < NT; ++h)
+            mma_bf16(tmem + h * BN, umma_desc_sw128(a + kk * 32),
+                     umma_desc_sw128(b + h * TB + kk * 32), idesc, (i | kk) != 0);
         mma_commit(empty + s);
       }
       mma_commit(accum);
@@ -206,7 +217,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUt
     pdl_wait();  // the residual R is the predecessor's output
     mbar_wait(accum, 0);
     tc_fence_after();
-    tile_epilogue<BN, EPI>(g, tmem, n0, m0, z, q, lane, blockIdx.x);
+    // the NT token tiles are contiguous in tokens and in TMEM columns: one
+    // NT * BN wide epilogue
+    tile_epilogue<NT * BN, EPI>(g, tmem, n0, m0, z, q, lane, blockIdx.x);
   }
   tc_fence_before();
   __syncthreads();
@@ -369,14 +382,16 @@ __device__ __forceinline__ int sk_owner(long long u, const SKArgs& g) {
   return (int)c;
 }
 
-template <int BN, int EPI, bool TILED>
+template <int BN, int EPI, bool TILED, int NT = 1>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                const SKArgs g) {
-  using C = Cfg<BN>;
-  constexpr int ACC_COLS = BN;  // one accumulator slot
-  constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
-                                         : 2 * BN <= 256 ? 256 : 512;
+  using C = Cfg<BN, NT>;
+  constexpr int ACC_COLS = NT * BN;           // one accumulator slot (NT token tiles)
+  constexpr int NACC = NT == 1 ? 2 : 1;       // TMEM double buffer when it fits
+  constexpr int TB = BN * BK * 2;             // bytes of one token tile's k-block
+  constexpr int TMEM_COLS = NACC * ACC_COLS <= 32 ? 32 : NACC * ACC_COLS <= 64 ? 64
+                          : NACC * ACC_COLS <= 128 ? 128 : NACC * ACC_COLS <= 256 ? 256 : 512;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -452,12 +467,15 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       }
       pdl_wait();
       while (next_seg(u, sg)) {
-        const int n0 = (sg.t / g.MT) * BM, m0 = (sg.t % g.MT) * BN;
+        const int n0 = (sg.t / g.MT) * BM, m0 = (sg.t % g.MT) * ACC_COLS;
         for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++i) {
           const int s = i % C::STAGES;
           const uint32_t ph = (i / C::STAGES) & 1;
           if (i < npre) {  // weight tile already in flight
-            tma_load_2d(sB + s * C::B_BYTES, &tmX, full + s, kb * BK, m0, pol_x);
+#pragma unroll
+            for (int h = 0; h < NT; ++h)
+              tma_load_2d(sB + s * C::B_BYTES + h * TB, &tmX, full + s, kb * BK, m0 + h * BN,
+                          pol_x);
             continue;
           }
           mbar_wait(empty + s, ph ^ 1);
@@ -470,7 +488,10 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           } else {
             tma_load_2d(sA + s * C::A_BYTES, &tmW, full + s, kb * BK, n0, pol_w);
           }
-          tma_load_2d(sB + s * C::B_BYTES, &tmX, full + s, kb * BK, m0, pol_x);
+#pragma unroll
+          for (int h = 0; h < NT; ++h)
+            tma_load_2d(sB + s * C::B_BYTES + h * TB, &tmX, full + s, kb * BK, m0 + h * BN,
+                        pol_x);
         }
       }
       pdl_trigger();
@@ -482,8 +503,8 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       Seg sg;
       int i = 0, j = 0;
       while (next_seg(u, sg)) {
-        const int a = j & 1;
-        const uint32_t aph = (j >> 1) & 1;
+        const int a = j % NACC;
+        const uint32_t aph = (j / NACC) & 1;
         mbar_wait(tempty + a, aph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + a * ACC_COLS;
@@ -496,8 +517,11 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           const uint32_t sb = smem_u32(sB + s * C::B_BYTES);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk)
-            mma_bf16(d, umma_desc_sw128(sa + kk * 32), umma_desc_sw128(sb + kk * 32), idesc,
-                     (kb != sg.kb0 || kk != 0) ? 1u : 0u);
+#pragma unroll
+            for (int h = 0; h < NT; ++h)
+              mma_bf16(d + h * BN, umma_desc_sw128(sa + kk * 32),
+                       umma_desc_sw128(sb + h * TB + kk * 32), idesc,
+                       (kb != sg.kb0 || kk != 0) ? 1u : 0u);
           mma_commit(empty + s);
         }
         mma_commit(tfull + a);
@@ -513,12 +537,12 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     Seg sg;
     int j = 0;
     while (next_seg(u, sg)) {
-      const int a = j & 1;
-      const uint32_t aph = (j >> 1) & 1;
+      const int a = j % NACC;
+      const uint32_t aph = (j / NACC) & 1;
       mbar_wait(tfull + a, aph);
       tc_fence_after();
       const uint32_t tbase = tmem + a * ACC_COLS + ((uint32_t)(32 * q) << 16);
-      const int n0 = (sg.t / g.MT) * BM, m0 = (sg.t % g.MT) * BN;
+      const int n0 = (sg.t / g.MT) * BM, m0 = (sg.t % g.MT) * ACC_COLS;
       const bool split = sg.kb0 != 0 || sg.kb1 != g.KB;
       int owner = c, last = c;
       bool finisher = true;
@@ -526,9 +550,9 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         // publish this segment's partial, take a ticket
         owner = sk_owner((long long)sg.t * g.KB, g);
         last = sk_owner((long long)sg.t * g.KB + g.KB - 1, g);
-        float* mine = g.part + ((size_t)c * 2 + (sg.first ? 0 : 1)) * (BN * BM);
+        float* mine = g.part + ((size_t)c * 2 + (sg.first ? 0 : 1)) * (ACC_COLS * BM);
 #pragma unroll 1
-        for (int col = 0; col < BN; col += 16) {
+        for (int col = 0; col < ACC_COLS; col += 16) {
           uint32_t r[16];
           tmem_ld16(tbase + (uint32_t)col, r);
           tmem_ld_wait();
@@ -547,7 +571,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       }
       if (finisher) {
 #pragma unroll 1
-        for (int col = 0; col < BN; col += 16) {
+        for (int col = 0; col < ACC_COLS; col += 16) {
           uint32_t r[16];
           tmem_ld16(tbase + (uint32_t)col, r);
           tmem_ld_wait();
@@ -562,7 +586,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
                 for (int k = 0; k < 16; ++k) v[k] += __uint_as_float(r[k]);
               } else {
                 const bool first_of_cc = sk_bound(cc, g) >= (long long)sg.t * g.KB;
-                const float* pp = g.part + ((size_t)cc * 2 + (first_of_cc ? 0 : 1)) * (BN * BM);
+                const float* pp = g.part + ((size_t)cc * 2 + (first_of_cc ? 0 : 1)) * (ACC_COLS * BM);
 #pragma unroll
                 for (int k = 0; k < 16; ++k) v[k] += __ldcg(pp + (col + k) * BM + row);
               }
@@ -718,18 +742,59 @@ int launch2_bn(const CUtensorMap& mw, const CUtensorMap& mx, const GemmArgs& g, 
                                   mx, g);
 }
 
-template <int BN, int EPI, bool TILED>
+template <int BN, int EPI, bool TILED, int NT = 1>
 int launch_sk_bn(const CUtensorMap& mw, const CUtensorMap& mx, const SKArgs& g, cudaStream_t st) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, NT>;
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_sk_kernel<BN, EPI, TILED>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_sk_kernel<BN, EPI, TILED, NT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return (int)e;
     attr_done = true;
   }
-  return (int)psd::launch(gemm_sk_kernel<BN, EPI, TILED>, dim3(g.G), dim3(kThreads), C::SMEM, st, mw,
-                          mx, g);
+  return (int)psd::launch(gemm_sk_kernel<BN, EPI, TILED, NT>, dim3(g.G), dim3(kThreads), C::SMEM,
+                          st, mw, mx, g);
+}
+
+// two token tiles per weight tile (256 < M <= 512)
+template <int EPI>
+int launch_sk_nt2(int bn, const CUtensorMap& mw, const CUtensorMap& mx, const SKArgs& g,
+                  cudaStream_t st) {
+  switch (bn) {
+    case 128: return launch_sk_bn<128, EPI, false, 2>(mw, mx, g, st);
+    case 160: return launch_sk_bn<160, EPI, false, 2>(mw, mx, g, st);
+    case 192: return launch_sk_bn<192, EPI, false, 2>(mw, mx, g, st);
+    case 224: return launch_sk_bn<224, EPI, false, 2>(mw, mx, g, st);
+    case 256: return launch_sk_bn<256, EPI, false, 2>(mw, mx, g, st);
+  }
+  return (int)cudaErrorInvalidValue;
+}
+
+template <int BN, int EPI, int NT>
+int launch_bn_nt(const CUtensorMap& mw, const CUtensorMap& mx, const GemmArgs& g, dim3 grid,
+                 cudaStream_t st) {
+  using C = Cfg<BN, NT>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN, EPI, NT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return (int)e;
+    attr_done = true;
+  }
+  return (int)psd::launch(gemm_kernel<BN, EPI, NT>, grid, dim3(kThreads), C::SMEM, st, mw, mx, g);
+}
+
+template <int EPI>
+int launch_epi_nt2(int bn, const CUtensorMap& mw, const CUtensorMap& mx, const GemmArgs& g,
+                   dim3 grid, cudaStream_t st) {
+  switch (bn) {
+    case 128: return launch_bn_nt<128, EPI, 2>(mw, mx, g, grid, st);
+    case 160: return launch_bn_nt<160, EPI, 2>(mw, mx, g, grid, st);
+    case 192: return launch_bn_nt<192, EPI, 2>(mw, mx, g, grid, st);
+    case 224: return launch_bn_nt<224, EPI, 2>(mw, mx, g, grid, st);
+    case 256: return launch_bn_nt<256, EPI, 2>(mw, mx, g, grid, st);
+  }
+  return (int)cudaErrorInvalidValue;
 }
 
 template <int EPI, bool TILED = false>
@@ -790,6 +855,32 @@ int token_tile(int M) {
   return std::max(32, (M + 31) / 32 * 32);
 }
 
+// token geometry: bn rows per token tile, nt token tiles per weight tile (2 for
+// 256 < M <= 512, so weights stream once), mt token-tile groups.  PSD_GEMM_NT2=0
+// keeps one token tile per CTA (A/B runs)
+struct TokGeo {
+  int bn, nt, mt;
+};
+int nt2_enabled() {
+  static int v = [] {
+    const char* e = getenv("PSD_GEMM_NT2");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+TokGeo tok_geo(int M, bool allow_nt2 = true) {
+  TokGeo t;
+  if (allow_nt2 && M > 256 && M <= 512 && nt2_enabled()) {
+    t.bn = std::min(256, ((M + 1) / 2 + 31) / 32 * 32);
+    t.nt = 2;
+  } else {
+    t.bn = token_tile(M);
+    t.nt = 1;
+  }
+  t.mt = (M + t.nt * t.bn - 1) / (t.nt * t.bn);
+  return t;
+}
+
 // CTA budget of the GEMM grids (0 = every SM); psd_gemm_set_max_ctas.  Capping
 // the verify GEMMs leaves SMs free for the concurrently running draft kernels.
 std::atomic<int>& max_ctas_cap() {
@@ -816,19 +907,24 @@ int num_sms_raw() {
 
 // stream-K geometry + workspace bytes (partials, then tickets)
 struct SKPlan {
-  int bn, KB, MT, tiles, G;
+  int bn, nt, KB, MT, tiles, G;
   long long U;
   size_t part_bytes, ticket_bytes;
 };
-SKPlan sk_plan(int M, int N, int K) {
+// stream-K keeps one TMEM accumulator when it holds two token tiles (no epilogue
+// overlap), which only pays when a CTA covers >= 2 weight tiles
+// (70B gate/up at M = 320: 426 -> 294 us; 8B gate/up at M = 384: 110 -> 117 us)
+SKPlan sk_plan(int M, int N, int K, bool allow_nt2 = true) {
   SKPlan p;
-  p.bn = token_tile(M);
+  const TokGeo tg = tok_geo(M, allow_nt2 && (N / BM) >= 2 * num_sms());
+  p.bn = tg.bn;
+  p.nt = tg.nt;
   p.KB = (K + BK - 1) / BK;
-  p.MT = (M + p.bn - 1) / p.bn;
+  p.MT = tg.mt;
   p.tiles = (N / BM) * p.MT;
   p.U = (long long)p.tiles * p.KB;
   p.G = (int)std::min<long long>(num_sms(), p.U);
-  p.part_bytes = (size_t)p.G * 2 * p.bn * BM * sizeof(float);
+  p.part_bytes = (size_t)p.G * 2 * p.nt * p.bn * BM * sizeof(float);
   // tickets live at a FIXED offset (start of the workspace) so GEMMs of any
   // shape can share one workspace: each leaves its tickets zeroed
   p.ticket_bytes = (size_t)kMaxTiles * sizeof(int);
@@ -888,8 +984,8 @@ void psd_gemm_set_max_ctas(int n) { max_ctas_cap().store(n > 0 ? n : 0); }
 int psd_gemm_plan(int M, int N, int K, int epi, int splits_hint, int* splits_out,
                   size_t* workspace_bytes) {
   if (M <= 0 || N <= 0 || K <= 0 || (K % 8) || (N % BM)) return (int)cudaErrorInvalidValue;
-  const int bn = token_tile(M);
-  const int tiles = (N / BM) * ((M + bn - 1) / bn);
+  const TokGeo tg = tok_geo(M);
+  const int tiles = (N / BM) * tg.mt;
   const int kb_total = (K + BK - 1) / BK;
   int splits = splits_hint;
   if (splits <= 0) {
@@ -932,7 +1028,7 @@ int psd_gemm_tiled(const void* X, int ldx, int M, int K, const void* W_tiled, in
     return (int)cudaErrorMisalignedAddress;
   if (ldx % 8) return (int)cudaErrorMisalignedAddress;
   if (M <= 0 || N <= 0 || K <= 0 || (K % 8) || (N % BM)) return (int)cudaErrorInvalidValue;
-  const SKPlan p = sk_plan(M, N, K);
+  const SKPlan p = sk_plan(M, N, K, false);  // pre-tiled weights: one token tile per CTA
   if (!workspace || workspace_bytes < p.part_bytes + p.ticket_bytes || p.tiles > kMaxTiles)
     return (int)cudaErrorInvalidValue;
   CUtensorMap mx;
@@ -968,8 +1064,9 @@ int psd_gemm_partials(const void* X, int ldx, int M, int K, const void* W, int l
   if ((size_t)splits * M * N * sizeof(float) > p_bytes) return (int)cudaErrorInvalidValue;
   rc = psd_gemm_plan(M, N, K, PSD_EPI_PARTIAL, splits, &splits, nullptr);
   if (rc) return rc;
-  const int bn = token_tile(M);
-  const bool pair = pair_enabled() && (N / BM) % 2 == 0;
+  const TokGeo tg = tok_geo(M);
+  const int bn = tg.bn;
+  const bool pair = tg.nt == 1 && pair_enabled() && (N / BM) % 2 == 0;
   CUtensorMap mw, mx;
   if ((rc = make_map(&mw, W, N, K, ldw, BM))) return rc;
   if ((rc = make_map(&mx, X, M, K, ldx, pair ? bn / 2 : bn))) return rc;
@@ -980,7 +1077,9 @@ int psd_gemm_partials(const void* X, int ldx, int M, int K, const void* W, int l
   splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
   g.Y = P; g.ldy = N; g.R = nullptr; g.ldr = 0;
   if (splits_used) *splits_used = splits;
-  dim3 grid(N / BM, (M + bn - 1) / bn, splits);
+  dim3 grid(N / BM, tg.mt, splits);
+  if (tg.nt == 2)
+    return launch_epi_nt2<PSD_EPI_PARTIAL>(bn, mw, mx, g, grid, (cudaStream_t)stream);
   if (pair) return launch_epi2<PSD_EPI_PARTIAL>(bn, mw, mx, g, grid, (cudaStream_t)stream);
   return launch_epi<PSD_EPI_PARTIAL>(bn, mw, mx, g, grid, (cudaStream_t)stream);
 }
@@ -997,8 +1096,9 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
     // one wave of whole-K tiles (>= 3/4 of the SMs busy, no tail): the plain
     // grid kernel beats stream-K, whose fix-ups buy nothing here (1B draft
     // gate/up at M = 32: 14.3 vs 19.8 us, profiles/r01b_kbench_gemm_splits.txt)
-    const int tiles = (N / BM) * ((M + token_tile(M) - 1) / token_tile(M));
-    if (tiles <= num_sms() && 4 * tiles >= 3 * num_sms()) splits_hint = 1;
+    const TokGeo tg = tok_geo(M);
+    const int tiles = (N / BM) * tg.mt;
+    if (tg.nt == 1 && tiles <= num_sms() && 4 * tiles >= 3 * num_sms()) splits_hint = 1;
   }
   if (splits_hint == 0) {
     // stream-K persistent path (default)
@@ -1018,6 +1118,15 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
     g.part = reinterpret_cast<float*>(static_cast<char*>(workspace) + p.ticket_bytes);
     g.Wt = nullptr;
     cudaStream_t st = (cudaStream_t)stream;
+    if (p.nt == 2) {
+      switch (epi) {
+        case PSD_EPI_BF16: return launch_sk_nt2<PSD_EPI_BF16>(p.bn, mw, mx, g, st);
+        case PSD_EPI_F32: return launch_sk_nt2<PSD_EPI_F32>(p.bn, mw, mx, g, st);
+        case PSD_EPI_RESID: return launch_sk_nt2<PSD_EPI_RESID>(p.bn, mw, mx, g, st);
+        case PSD_EPI_SILU: return launch_sk_nt2<PSD_EPI_SILU>(p.bn, mw, mx, g, st);
+      }
+      return (int)cudaErrorInvalidValue;
+    }
     switch (epi) {
       case PSD_EPI_BF16: return launch_sk<PSD_EPI_BF16>(p.bn, mw, mx, g, st);
       case PSD_EPI_F32: return launch_sk<PSD_EPI_F32>(p.bn, mw, mx, g, st);
@@ -1037,8 +1146,9 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
     if (rc) return rc;
     if (splits > 1 && (!workspace || workspace_bytes < need)) splits = 1;
   }
-  const int bn = token_tile(M);
-  const bool pair = pair_enabled() && (N / BM) % 2 == 0;
+  const TokGeo tg = tok_geo(M);
+  const int bn = tg.bn;
+  const bool pair = tg.nt == 1 && pair_enabled() && (N / BM) % 2 == 0;
   CUtensorMap mw, mx;
   if ((rc = make_map(&mw, W, N, K, ldw, BM))) return rc;
   if ((rc = make_map(&mx, X, M, K, ldx, pair ? bn / 2 : bn))) return rc;
@@ -1049,11 +1159,12 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
   splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
   g.Y = splits > 1 ? workspace : Y;
   g.ldy = ldy; g.R = static_cast<const __nv_bfloat16*>(R); g.ldr = ldr;
-  dim3 grid(N / BM, (M + bn - 1) / bn, splits);
+  dim3 grid(N / BM, tg.mt, splits);
   cudaStream_t st = (cudaStream_t)stream;
   if (splits > 1) {
-    rc = pair ? launch_epi2<PSD_EPI_PARTIAL>(bn, mw, mx, g, grid, st)
-              : launch_epi<PSD_EPI_PARTIAL>(bn, mw, mx, g, grid, st);
+    rc = tg.nt == 2 ? launch_epi_nt2<PSD_EPI_PARTIAL>(bn, mw, mx, g, grid, st)
+         : pair ? launch_epi2<PSD_EPI_PARTIAL>(bn, mw, mx, g, grid, st)
+                : launch_epi<PSD_EPI_PARTIAL>(bn, mw, mx, g, grid, st);
     if (rc) return rc;
     const int Nout = epi == PSD_EPI_SILU ? N / 2 : N;
     const size_t total = (size_t)M * Nout;
@@ -1063,6 +1174,15 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
                                                epi, Y, ldy, static_cast<const __nv_bfloat16*>(R),
                                                ldr);
     return (int)cudaGetLastError();
+  }
+  if (tg.nt == 2) {
+    switch (epi) {
+      case PSD_EPI_BF16: return launch_epi_nt2<PSD_EPI_BF16>(bn, mw, mx, g, grid, st);
+      case PSD_EPI_F32: return launch_epi_nt2<PSD_EPI_F32>(bn, mw, mx, g, grid, st);
+      case PSD_EPI_RESID: return launch_epi_nt2<PSD_EPI_RESID>(bn, mw, mx, g, grid, st);
+      case PSD_EPI_SILU: return launch_epi_nt2<PSD_EPI_SILU>(bn, mw, mx, g, grid, st);
+    }
+    return (int)cudaErrorInvalidValue;
   }
   if (pair) {
     switch (epi) {

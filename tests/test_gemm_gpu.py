@@ -26,7 +26,8 @@ def _close(got, ref, K):
 
 @pytest.mark.parametrize("M,N,K", [(32, 3072, 2048), (192, 6144, 4096), (160, 4608, 3584),
                                    (1, 128, 64), (37, 256, 192), (320, 2560, 8192),
-                                   (64, 1024, 1000), (700, 512, 512), (192, 8192, 4096), (32, 128256, 2048)])
+                                   (64, 1024, 1000), (700, 512, 512), (192, 8192, 4096), (32, 128256, 2048),
+                                   (384, 4096, 4096), (300, 1024, 2048), (512, 2048, 1024)])
 @pytest.mark.parametrize("splits", [0, 1])
 def test_gemm_bf16(cuda_device, M, N, K, splits):
     g = torch.Generator(device=cuda_device).manual_seed(M * 7 + N + K)
@@ -53,7 +54,7 @@ def test_gemm_f32_and_resid(cuda_device, splits):
     _close(r, _ref(x, w) + r0.float(), K)
 
 
-@pytest.mark.parametrize("M,splits", [(32, 0), (192, 1), (192, 0)])
+@pytest.mark.parametrize("M,splits", [(32, 0), (192, 1), (192, 0), (384, 0), (320, 1), (300, 2)])
 def test_gemm_silu_mul(cuda_device, M, splits):
     g = torch.Generator(device=cuda_device).manual_seed(9)
     F, K = 1024, 2048
@@ -70,7 +71,7 @@ def test_gemm_silu_mul(cuda_device, M, splits):
 
 
 @pytest.mark.parametrize("M,N,K", [(192, 6144, 4096), (192, 4096, 14336), (32, 3072, 2048),
-                                   (32, 2048, 8192), (320, 2560, 8192)])
+                                   (32, 2048, 8192), (320, 2560, 8192), (384, 6144, 4096)])
 def test_gemm_partials_sum(cuda_device, M, N, K):
     """psd_gemm_partials: the sum of the returned split slices equals x @ w.T
     (split-K reduced through DSMEM inside a (1, 1, S) cluster when S <= 8)."""

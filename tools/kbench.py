@@ -285,6 +285,13 @@ def main():
                                ("8B o", 192, 4096, 4096), ("8B down", 192, 4096, 14336)):
             for sp in (None, 2, 3, 4, 6, 8, 12, 16):
                 gemm_case(f"{tag} part", M, N, K, "partial", splits=sp)
+    if want("gemmnt"):
+        gemm_case("8B gate/up M384", 384, 28672, 4096, "silu")
+        gemm_case("8B qkv part M384", 384, 6144, 4096, "partial")
+        gemm_case("8B down part M384", 384, 4096, 14336, "partial")
+        gemm_case("8B lm M384", 384, 128256, 4096, "f32", copies=2)
+        gemm_case("70B gate/up M320", 320, 57344, 8192, "silu", copies=2)
+        gemm_case("70B down part M320", 320, 8192, 28672, "partial", copies=2)
     if want("gemmgu"):
         gemm_case("8B gate/up", 192, 28672, 4096, "silu")
     if want("attn1b"):
