@@ -43,27 +43,6 @@ inline cudaError_t launch(void (*kernel)(Params...), dim3 grid, dim3 block, size
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
-// launch as clusters of `cluster_x` CTAs along x (CTA pairs for cta_group::2)
-template <typename... Params, typename... Args>
-inline cudaError_t launch_cluster(void (*kernel)(Params...), dim3 grid, dim3 block, size_t smem,
-                                  cudaStream_t st, int cluster_x, Args&&... args) {
-  count_launches();
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
-  attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = cluster_x;
-  attr[1].val.clusterDim.y = 1;
-  attr[1].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
-}
 }  // namespace psd
 
 #ifdef __CUDACC__

@@ -226,123 +226,6 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUt
   if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
 }
 
-// ---- CTA-pair variant (cta_group::2) ----------------------------------------------
-// Two CTAs of a cluster share one 256 x BN tile: each holds its 128 weight rows
-// (UMMA A, M = 256 across the pair) and HALF of the token tile (UMMA B is
-// N-split across the pair), the leader issues tcgen05.mma.cta_group::2 and each
-// CTA's TMEM receives its own 128 accumulator rows.  Per SM and k-block the
-// ring holds 16 KB of weights + BN*64 B of tokens instead of + BN*128 B, so
-// ~40% more weight bytes are in flight per SM (the verify GEMMs at M = 192 are
-// bound by in-flight bytes per SM, not by HBM).
-template <int BN>
-struct Cfg2 {
-  static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = (BN / 2) * BK * 2;
-  static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int MAXS = (200 * 1024) / STAGE;
-  static constexpr int STAGES = MAXS > 10 ? 10 : MAXS;
-  static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
-  static constexpr int SMEM = 1024 + STAGES * STAGE + 256;
-};
-
-template <int BN, int EPI>
-__global__ void __launch_bounds__(kThreads, 1)
-gemm2_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-             const GemmArgs g) {
-  using C = Cfg2<BN>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
-  uint64_t* empty = full + C::STAGES;
-  uint64_t* accum = empty + C::STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
-  const bool leader = rank == 0;
-  const int n0 = blockIdx.x * BM;  // = pair * 256 + rank * 128
-  const int m0 = blockIdx.y * BN, z = blockIdx.z;
-  const int kb0 = z * g.kb_per_split;
-  const int nkb = min(g.kb_total, kb0 + g.kb_per_split) - kb0;
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tmW);
-    tma_prefetch(&tmX);
-    for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(empty + s, 1);
-    }
-    mbar_init(accum, 1);
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc2(tmem_slot, C::TMEM_COLS);
-  tc_fence_before();
-  cluster_sync();  // both CTAs' barriers exist before any remote completion
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      const uint64_t pol_w = policy_evict_first();
-      const uint64_t pol_x = policy_evict_last();
-      const int mb = m0 + (int)rank * (BN / 2);
-      const int npre = min(nkb, C::STAGES);
-      // PDL: weight tiles stream while the predecessor drains; tokens after
-      for (int i = 0; i < npre; ++i) {
-        const uint32_t fb = mapa_shared(full + i, 0);
-        if (leader) mbar_arrive_expect_tx(full + i, 2 * C::STAGE);
-        tma_load_2d_pair(sA + i * C::A_BYTES, &tmW, fb, (kb0 + i) * BK, n0, pol_w);
-      }
-      pdl_wait();
-      for (int i = 0; i < npre; ++i)
-        tma_load_2d_pair(sB + i * C::B_BYTES, &tmX, mapa_shared(full + i, 0), (kb0 + i) * BK, mb,
-                         pol_x);
-      for (int i = npre; i < nkb; ++i) {
-        const int s = i % C::STAGES;
-        const uint32_t ph = (i / C::STAGES) & 1;
-        mbar_wait(empty + s, ph ^ 1);
-        const uint32_t fb = mapa_shared(full + s, 0);
-        if (leader) mbar_arrive_expect_tx(full + s, 2 * C::STAGE);
-        const int kc = (kb0 + i) * BK;
-        tma_load_2d_pair(sA + s * C::A_BYTES, &tmW, fb, kc, n0, pol_w);
-        tma_load_2d_pair(sB + s * C::B_BYTES, &tmX, fb, kc, mb, pol_x);
-      }
-      pdl_trigger();
-    }
-  } else if (warp == 1) {
-    if (lane == 0 && leader) {
-      constexpr uint32_t idesc = umma_idesc_bf16(2 * BM, BN);
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % C::STAGES;
-        const uint32_t ph = (i / C::STAGES) & 1;
-        mbar_wait(full + s, ph);
-        tc_fence_after();
-        const uint32_t a = smem_u32(sA + s * C::A_BYTES);
-        const uint32_t b = smem_u32(sB + s * C::B_BYTES);
-#pragma unroll
-        for (int kk = 0; kk < BK / 16; ++kk)
-          mma_bf16_pair(tmem, umma_desc_sw128(a + kk * 32), umma_desc_sw128(b + kk * 32), idesc,
-                        (i | kk) != 0);
-        mma_commit_pair(empty + s);
-      }
-      mma_commit_pair(accum);
-    }
-    __syncwarp();
-  } else {
-    const int q = warp & 3;
-    pdl_wait();
-    mbar_wait(accum, 0);
-    tc_fence_after();
-    tile_epilogue<BN, EPI>(g, tmem, n0, m0, z, q, lane, blockIdx.x);
-  }
-  tc_fence_before();
-  cluster_sync();  // the peer's TMEM / smem stay alive until the pair is done
-  if (warp == 1) tmem_dealloc2(tmem, C::TMEM_COLS);
-}
-
 // ---- stream-K persistent variant ---------------------------------------------
 // Work = tiles x k-blocks "units" in tile-major order (tile t = n_tile * MT +
 // m_tile, so neighbouring units share weights); CTA c of G takes units
@@ -727,20 +610,6 @@ int launch_bn(const CUtensorMap& mw, const CUtensorMap& mx, const GemmArgs& g, d
   return (int)psd::launch(gemm_kernel<BN, EPI>, grid, dim3(kThreads), C::SMEM, st, mw, mx, g);
 }
 
-template <int BN, int EPI>
-int launch2_bn(const CUtensorMap& mw, const CUtensorMap& mx, const GemmArgs& g, dim3 grid,
-               cudaStream_t st) {
-  using C = Cfg2<BN>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(gemm2_kernel<BN, EPI>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    if (e != cudaSuccess) return (int)e;
-    attr_done = true;
-  }
-  return (int)psd::launch_cluster(gemm2_kernel<BN, EPI>, grid, dim3(kThreads), C::SMEM, st, 2, mw,
-                                  mx, g);
-}
 
 template <int BN, int EPI, bool TILED, int NT = 1>
 int launch_sk_bn(const CUtensorMap& mw, const CUtensorMap& mx, const SKArgs& g, cudaStream_t st) {
@@ -931,33 +800,6 @@ SKPlan sk_plan(int M, int N, int K, bool allow_nt2 = true) {
   return p;
 }
 
-// PSD_GEMM_PAIR=1 runs the grid split-K GEMMs on CTA pairs (cta_group::2).  Off
-// by default: correct, but measured 15-20% slower than single-CTA tiles at the
-// cfg2 shapes (profiles/r01b_kbench_gemm_pair.txt)
-int pair_enabled() {
-  static int v = [] {
-    const char* e = getenv("PSD_GEMM_PAIR");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
-template <int EPI>
-int launch_epi2(int bn, const CUtensorMap& mw, const CUtensorMap& mx, const GemmArgs& g,
-                dim3 grid, cudaStream_t st) {
-  switch (bn) {
-    case 32: return launch2_bn<32, EPI>(mw, mx, g, grid, st);
-    case 64: return launch2_bn<64, EPI>(mw, mx, g, grid, st);
-    case 96: return launch2_bn<96, EPI>(mw, mx, g, grid, st);
-    case 128: return launch2_bn<128, EPI>(mw, mx, g, grid, st);
-    case 160: return launch2_bn<160, EPI>(mw, mx, g, grid, st);
-    case 192: return launch2_bn<192, EPI>(mw, mx, g, grid, st);
-    case 224: return launch2_bn<224, EPI>(mw, mx, g, grid, st);
-    case 256: return launch2_bn<256, EPI>(mw, mx, g, grid, st);
-  }
-  return (int)cudaErrorInvalidValue;
-}
-
 template <int EPI>
 int launch_epi(int bn, const CUtensorMap& mw, const CUtensorMap& mx, const GemmArgs& g, dim3 grid,
                cudaStream_t st) {
@@ -1066,10 +908,9 @@ int psd_gemm_partials(const void* X, int ldx, int M, int K, const void* W, int l
   if (rc) return rc;
   const TokGeo tg = tok_geo(M);
   const int bn = tg.bn;
-  const bool pair = tg.nt == 1 && pair_enabled() && (N / BM) % 2 == 0;
   CUtensorMap mw, mx;
   if ((rc = make_map(&mw, W, N, K, ldw, BM))) return rc;
-  if ((rc = make_map(&mx, X, M, K, ldx, pair ? bn / 2 : bn))) return rc;
+  if ((rc = make_map(&mx, X, M, K, ldx, bn))) return rc;
   GemmArgs g;
   g.M = M; g.N = N; g.K = K;
   g.kb_total = (K + BK - 1) / BK;
@@ -1080,7 +921,6 @@ int psd_gemm_partials(const void* X, int ldx, int M, int K, const void* W, int l
   dim3 grid(N / BM, tg.mt, splits);
   if (tg.nt == 2)
     return launch_epi_nt2<PSD_EPI_PARTIAL>(bn, mw, mx, g, grid, (cudaStream_t)stream);
-  if (pair) return launch_epi2<PSD_EPI_PARTIAL>(bn, mw, mx, g, grid, (cudaStream_t)stream);
   return launch_epi<PSD_EPI_PARTIAL>(bn, mw, mx, g, grid, (cudaStream_t)stream);
 }
 
@@ -1148,10 +988,9 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
   }
   const TokGeo tg = tok_geo(M);
   const int bn = tg.bn;
-  const bool pair = tg.nt == 1 && pair_enabled() && (N / BM) % 2 == 0;
   CUtensorMap mw, mx;
   if ((rc = make_map(&mw, W, N, K, ldw, BM))) return rc;
-  if ((rc = make_map(&mx, X, M, K, ldx, pair ? bn / 2 : bn))) return rc;
+  if ((rc = make_map(&mx, X, M, K, ldx, bn))) return rc;
   GemmArgs g;
   g.M = M; g.N = N; g.K = K;
   g.kb_total = (K + BK - 1) / BK;
@@ -1163,8 +1002,7 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
   cudaStream_t st = (cudaStream_t)stream;
   if (splits > 1) {
     rc = tg.nt == 2 ? launch_epi_nt2<PSD_EPI_PARTIAL>(bn, mw, mx, g, grid, st)
-         : pair ? launch_epi2<PSD_EPI_PARTIAL>(bn, mw, mx, g, grid, st)
-                : launch_epi<PSD_EPI_PARTIAL>(bn, mw, mx, g, grid, st);
+                    : launch_epi<PSD_EPI_PARTIAL>(bn, mw, mx, g, grid, st);
     if (rc) return rc;
     const int Nout = epi == PSD_EPI_SILU ? N / 2 : N;
     const size_t total = (size_t)M * Nout;
@@ -1181,15 +1019,6 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
       case PSD_EPI_F32: return launch_epi_nt2<PSD_EPI_F32>(bn, mw, mx, g, grid, st);
       case PSD_EPI_RESID: return launch_epi_nt2<PSD_EPI_RESID>(bn, mw, mx, g, grid, st);
       case PSD_EPI_SILU: return launch_epi_nt2<PSD_EPI_SILU>(bn, mw, mx, g, grid, st);
-    }
-    return (int)cudaErrorInvalidValue;
-  }
-  if (pair) {
-    switch (epi) {
-      case PSD_EPI_BF16: return launch_epi2<PSD_EPI_BF16>(bn, mw, mx, g, grid, st);
-      case PSD_EPI_F32: return launch_epi2<PSD_EPI_F32>(bn, mw, mx, g, grid, st);
-      case PSD_EPI_RESID: return launch_epi2<PSD_EPI_RESID>(bn, mw, mx, g, grid, st);
-      case PSD_EPI_SILU: return launch_epi2<PSD_EPI_SILU>(bn, mw, mx, g, grid, st);
     }
     return (int)cudaErrorInvalidValue;
   }
