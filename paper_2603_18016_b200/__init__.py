@@ -22,6 +22,7 @@ from .acceptance import AcceptanceModel, acceptance_stream, accepted_count, expe
 from .batches import BatchManager
 from .errors import (CapacityError, ConfigError, KVError, NativeError, NumericError,
                      ProtocolError, SpecsimError, WorkloadError)
+from .ktune import KTuner
 from .kvtable import AllocationContext, BlockPool, KVBlockTable, blocks_needed
 from .metrics import (MetricsReport, accepted_per_verify, compute_metrics,
                       mean_accepted_length, percentile_nearest_rank, render_metrics,
@@ -38,6 +39,7 @@ from .workload import (LengthSpec, WorkloadSpec, attach_prompt_ids, generate_req
 __version__ = "0.1.0"
 
 __all__ = [
+    "KTuner",
     "AcceptanceModel", "AllocationContext", "BatchManager", "BlockPool",
     "CapacityError", "ConfigError", "EngineState", "FinishRecord", "KVBlockTable",
     "KVError", "KvStepRecord", "LatencyModel", "LengthSpec", "MetricsReport",

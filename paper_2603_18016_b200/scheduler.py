@@ -177,6 +177,7 @@ class EngineState:
     finish_log: list[FinishRecord] = field(default_factory=list)
     sd_members: dict[int, None] = field(default_factory=dict)
     backend: Backend | None = None
+    k_tuner: object | None = None  # ktune.KTuner: online draft depth (None = config.k)
 
     def request_list(self) -> list[Request]:
         return [self.requests[rid] for rid in sorted(self.requests)]
@@ -238,7 +239,10 @@ def _quota(state: EngineState, rid: int) -> int:
     """k_i = min(configured depth, remaining - 1): the commit (accepted + one
     bonus) can never overshoot the output budget."""
     left = state.requests[rid].remaining - 1
-    return min(state.config.draft_len(rid), left if left > 0 else 0)
+    depth = state.config.draft_len(rid)
+    if state.k_tuner is not None and not state.config.k_overrides:
+        depth = min(depth, state.k_tuner.k)
+    return min(depth, left if left > 0 else 0)
 
 
 def _grow(state: EngineState, ctx: AllocationContext,
@@ -507,6 +511,8 @@ def step_once(state: EngineState, config: SimConfig | None = None) -> StepRecord
     rec = _sd_step(state) if state.config.mode == "standard-sd" else _psd_step(state)
     state.step_log.append(rec)
     state.step_index = rec.step_index
+    if state.k_tuner is not None:
+        state.k_tuner.observe(rec)
     return rec
 
 
@@ -539,9 +545,11 @@ def new_state(config: SimConfig, workload: list[Request],
 
 def run(config: SimConfig, workload: list[Request],
         preemptions: list[Preemption] | None = None, max_steps: int = 5_000_000,
-        backend: Backend | None = None) -> tuple[EngineState, MetricsReport]:
-    """Run to completion; returns the final state and its metrics."""
+        backend: Backend | None = None, k_tuner=None) -> tuple[EngineState, MetricsReport]:
+    """Run to completion; returns the final state and its metrics.  ``k_tuner``
+    (ktune.KTuner) picks the draft depth online (<= config.k) from the step log."""
     state = new_state(config, workload, backend)
+    state.k_tuner = k_tuner
     if preemptions:
         for pre in preemptions:
             if pre.request_index not in state.requests:

@@ -195,3 +195,21 @@ def test_fused_draft_decode_matches_per_kernel_forward(cuda_device, draft):
         [(s.drafted_tokens, s.accepted_tokens) for s in ps.step_log]
     assert frep.total_accepted > 0
     fused.close()
+
+
+def test_online_k_tuner_on_gpu_keeps_greedy_tokens(cuda_device):
+    """the online draft-depth tuner (ktune.KTuner) on
+    measured CUDA-event durations.  Greedy output does not depend on the
+    draft depth, so tokens must equal the fixed-k run's; the tuner must have
+    estimated acceptance and timings and changed depth within [1, k]."""
+    from paper_2603_18016_b200 import KTuner
+    kw = dict(max_requests=16, max_batch=16, k_max=4, max_seq_len=128, seed=0, beta_target=3.0,
+              beta_draft=12.0, prefill_chunk_tokens=512)
+    ref, _ = _tiny_run("psd", GpuBackend("tiny-target", "tiny-draft", **kw))
+    tuner = KTuner(k_max=4, mode="psd", warmup=2)
+    cfg = SimConfig(mode="psd", m=8, k=4)
+    st, rep = run(cfg, make_requests([32] * 16, prompt_len=16),
+                  backend=GpuBackend("tiny-target", "tiny-draft", **kw), k_tuner=tuner)
+    assert [r.output_ids for r in st.request_list()] == [r.output_ids for r in ref.request_list()]
+    assert tuner.p is not None and tuner.d and tuner.v
+    assert all(1 <= h[1] <= 4 for h in tuner.history)
