@@ -352,11 +352,19 @@ def run_ours(args) -> None:
 
     launches = {}
 
+    tuners = []
+
     def one(mode):
+        if mode == "psd-ktune":  # online draft depth
+            from paper_2603_18016_b200 import KTuner
+            t = KTuner(k_max=CFG["k"], mode="psd", warmup=3)
+            tuners.append(t)
+            return run(_config("psd"), _workload(rank), backend=backend, k_tuner=t)
         return run(_config(mode), _workload(rank), backend=backend)
 
     results = {}
-    for mode in ("psd", "standard-sd", "sd-m"):
+    modes = ("psd", "standard-sd", "sd-m") + (("psd-ktune",) if args.ktune else ())
+    for mode in modes:
         if is_draft_rank:
             # serve warm-up + timed passes of this mode, then join the timing reduction
             DraftServer(GpuDraftEngine(be), link).serve()
@@ -461,6 +469,11 @@ def run_ours(args) -> None:
                "gpu_launches": launches.get("standard-sd")},
         "sd_m": {"value": round(sdm["tokens"] / (sdm["ms"] * 1e-3), 1), "unit": "tok/s",
                  "mode": "standard-sd, batches of m=32 (sd_batch_factor 1), the PSD batch size"},
+        "psd_ktune": ({"value": round(results["psd-ktune"]["tokens"]
+                                      / (results["psd-ktune"]["ms"] * 1e-3), 1),
+                       "unit": "tok/s", "final_k": tuners[-1].k if tuners else None,
+                       "p_est": round(tuners[-1].p, 4) if tuners and tuners[-1].p else None}
+                      if "psd-ktune" in results and results["psd-ktune"] else None),
         "psd_vs_sd": round(value / sd_value, 4),
         "psd_vs_sd_m": round(value / (sdm["tokens"] / (sdm["ms"] * 1e-3)), 4),
         "mean_accepted_len": round(mean_accepted_length(r0), 4),
@@ -488,6 +501,8 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ktune", action="store_true",
+                    help="also run PSD with the online draft-depth tuner (ktune.KTuner)")
     ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3"],
                     help="cfg2: 8B / 1B greedy (the headline); cfg3: Qwen2.5-7B / 0.5B, "
                          "T = 1.0 rejection sampling over the 152k vocabulary")
