@@ -292,6 +292,12 @@ def main():
         gemm_case("8B lm M384", 384, 128256, 4096, "f32", copies=2)
         gemm_case("70B gate/up M320", 320, 57344, 8192, "silu", copies=2)
         gemm_case("70B down part M320", 320, 8192, 28672, "partial", copies=2)
+    if want("gemmmw"):
+        gemm_case("8B gate/up", 192, 28672, 4096, "silu")
+        gemm_case("8B lm", 192, 128256, 4096, "f32", copies=2)
+        gemm_case("8B gate/up M96", 96, 28672, 4096, "silu")
+        gemm_case("8B gate/up M256", 256, 28672, 4096, "silu")
+        gemm_case("Qwen7B gate/up M160", 160, 37888, 3584, "silu")
     if want("gemmgu"):
         gemm_case("8B gate/up", 192, 28672, 4096, "silu")
     if want("attn1b"):
