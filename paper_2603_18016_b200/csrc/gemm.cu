@@ -51,15 +51,15 @@ struct GemmArgs {
 
 // NT token tiles of BN rows per weight tile (NT = 2 for 256 < M <= 512: every
 // weight byte is streamed once instead of once per token tile)
-template <int BN, int NT = 1, int MW = 1>
+template <int BN, int NT = 1>
 struct Cfg {
-  static constexpr int A_BYTES = MW * BM * BK * 2;
+  static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = NT * BN * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int MAXS = (200 * 1024) / STAGE;
   static constexpr int STAGES = MAXS > 8 ? 8 : MAXS;
-  static constexpr int TMEM_COLS = MW * NT * BN <= 32 ? 32 : MW * NT * BN <= 64 ? 64
-                                 : MW * NT * BN <= 128 ? 128 : MW * NT * BN <= 256 ? 256 : 512;
+  static constexpr int TMEM_COLS = NT * BN <= 32 ? 32 : NT * BN <= 64 ? 64
+                                 : NT * BN <= 128 ? 128 : NT * BN <= 256 ? 256 : 512;
   static constexpr int SMEM = 1024 + STAGES * STAGE + 256;
 };
 
@@ -265,17 +265,13 @@ __device__ __forceinline__ int sk_owner(long long u, const SKArgs& g) {
   return (int)c;
 }
 
-// MW weight tiles per unit (MW = 2: two 128-row tiles share every token
-// k-block -> half the token bytes per weight byte); NT token tiles per unit
-template <int BN, int EPI, bool TILED, int NT = 1, int MW = 1>
+template <int BN, int EPI, bool TILED, int NT = 1>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                const SKArgs g) {
-  using C = Cfg<BN, NT, MW>;
-  constexpr int TC = NT * BN;                 // token columns of one weight tile
-  constexpr int ACC_COLS = MW * TC;           // one accumulator slot: weight tile w at w * TC
-  constexpr int NACC = 2 * ACC_COLS <= 512 ? 2 : 1;  // TMEM double buffer when it fits
-  constexpr int AB1 = BM * BK * 2;            // bytes of one weight tile's k-block
+  using C = Cfg<BN, NT>;
+  constexpr int ACC_COLS = NT * BN;           // one accumulator slot (NT token tiles)
+  constexpr int NACC = NT == 1 ? 2 : 1;       // TMEM double buffer when it fits
   constexpr int TB = BN * BK * 2;             // bytes of one token tile's k-block
   constexpr int TMEM_COLS = NACC * ACC_COLS <= 32 ? 32 : NACC * ACC_COLS <= 64 ? 64
                           : NACC * ACC_COLS <= 128 ? 128 : NACC * ACC_COLS <= 256 ? 256 : 512;
@@ -338,7 +334,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         long long uu = u0;
         Seg s0;
         if (next_seg(uu, s0)) {
-          const int n0 = (s0.t / g.MT) * (BM * MW);
+          const int n0 = (s0.t / g.MT) * BM;
           npre = min(s0.kb1 - s0.kb0, C::STAGES);
           for (int j = 0; j < npre; ++j) {
             mbar_arrive_expect_tx(full + j, C::STAGE);
@@ -347,17 +343,14 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
                   g.Wt + ((size_t)(n0 / BM) * g.KB + s0.kb0 + j) * (size_t)(BM * BK);
               bulk_load(sA + j * C::A_BYTES, src, C::A_BYTES, full + j, pol_w);
             } else {
-#pragma unroll
-              for (int w = 0; w < MW; ++w)
-                tma_load_2d(sA + j * C::A_BYTES + w * AB1, &tmW, full + j, (s0.kb0 + j) * BK,
-                            n0 + w * BM, pol_w);
+              tma_load_2d(sA + j * C::A_BYTES, &tmW, full + j, (s0.kb0 + j) * BK, n0, pol_w);
             }
           }
         }
       }
       pdl_wait();
       while (next_seg(u, sg)) {
-        const int n0 = (sg.t / g.MT) * (BM * MW), m0 = (sg.t % g.MT) * TC;
+        const int n0 = (sg.t / g.MT) * BM, m0 = (sg.t % g.MT) * ACC_COLS;
         for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++i) {
           const int s = i % C::STAGES;
           const uint32_t ph = (i / C::STAGES) & 1;
@@ -376,10 +369,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
                 g.Wt + ((size_t)(n0 / BM) * g.KB + kb) * (size_t)(BM * BK);
             bulk_load(sA + s * C::A_BYTES, src, C::A_BYTES, full + s, pol_w);
           } else {
-#pragma unroll
-            for (int w = 0; w < MW; ++w)
-              tma_load_2d(sA + s * C::A_BYTES + w * AB1, &tmW, full + s, kb * BK, n0 + w * BM,
-                          pol_w);
+            tma_load_2d(sA + s * C::A_BYTES, &tmW, full + s, kb * BK, n0, pol_w);
           }
 #pragma unroll
           for (int h = 0; h < NT; ++h)
@@ -411,12 +401,10 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk)
 #pragma unroll
-            for (int w = 0; w < MW; ++w)
-#pragma unroll
-              for (int h = 0; h < NT; ++h)
-                mma_bf16(d + w * TC + h * BN, umma_desc_sw128(sa + w * AB1 + kk * 32),
-                         umma_desc_sw128(sb + h * TB + kk * 32), idesc,
-                         (kb != sg.kb0 || kk != 0) ? 1u : 0u);
+            for (int h = 0; h < NT; ++h)
+              mma_bf16(d + h * BN, umma_desc_sw128(sa + kk * 32),
+                       umma_desc_sw128(sb + h * TB + kk * 32), idesc,
+                       (kb != sg.kb0 || kk != 0) ? 1u : 0u);
           mma_commit(empty + s);
         }
         mma_commit(tfull + a);
@@ -437,7 +425,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       mbar_wait(tfull + a, aph);
       tc_fence_after();
       const uint32_t tbase = tmem + a * ACC_COLS + ((uint32_t)(32 * q) << 16);
-      const int n0 = (sg.t / g.MT) * (BM * MW), m0 = (sg.t % g.MT) * TC;
+      const int n0 = (sg.t / g.MT) * BM, m0 = (sg.t % g.MT) * ACC_COLS;
       const bool split = sg.kb0 != 0 || sg.kb1 != g.KB;
       int owner = c, last = c;
       bool finisher = true;
@@ -490,9 +478,8 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 #pragma unroll
             for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(r[k]);
           }
-          const int wt = col / TC, mcol = col - wt * TC;  // weight tile, token column
           if constexpr (EPI == PSD_EPI_SILU) {
-            const int jo = (n0 / BM + wt) * 64 + 16 * q + (lane & 15);
+            const int jo = (n0 / BM) * 64 + 16 * q + (lane & 15);
             __nv_bfloat16* Y = static_cast<__nv_bfloat16*>(g.Y);
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
@@ -502,16 +489,16 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
             if (lane < 16) {
 #pragma unroll
               for (int k = 0; k < 16; ++k) {
-                const int m = m0 + mcol + k;
+                const int m = m0 + col + k;
                 if (m < g.M) Y[(size_t)m * g.ldy + jo] = __float2bfloat16(v[k]);
               }
             }
           } else {
-            const int n = n0 + wt * BM + row;
+            const int n = n0 + row;
             if (n < g.N) {
 #pragma unroll
               for (int k = 0; k < 16; ++k) {
-                const int m = m0 + mcol + k;
+                const int m = m0 + col + k;
                 if (m >= g.M) break;
                 if constexpr (EPI == PSD_EPI_F32) {
                   static_cast<float*>(g.Y)[(size_t)m * g.ldy + n] = v[k];
@@ -624,33 +611,18 @@ int launch_bn(const CUtensorMap& mw, const CUtensorMap& mx, const GemmArgs& g, d
 }
 
 
-template <int BN, int EPI, bool TILED, int NT = 1, int MW = 1>
+template <int BN, int EPI, bool TILED, int NT = 1>
 int launch_sk_bn(const CUtensorMap& mw, const CUtensorMap& mx, const SKArgs& g, cudaStream_t st) {
-  using C = Cfg<BN, NT, MW>;
+  using C = Cfg<BN, NT>;
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_sk_kernel<BN, EPI, TILED, NT, MW>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_sk_kernel<BN, EPI, TILED, NT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return (int)e;
     attr_done = true;
   }
-  return (int)psd::launch(gemm_sk_kernel<BN, EPI, TILED, NT, MW>, dim3(g.G), dim3(kThreads),
-                          C::SMEM, st, mw, mx, g);
-}
-
-// two weight tiles per unit sharing each token k-block (96 <= M <= 256)
-template <int EPI>
-int launch_sk_mw2(int bn, const CUtensorMap& mw, const CUtensorMap& mx, const SKArgs& g,
-                  cudaStream_t st) {
-  switch (bn) {
-    case 96: return launch_sk_bn<96, EPI, false, 1, 2>(mw, mx, g, st);
-    case 128: return launch_sk_bn<128, EPI, false, 1, 2>(mw, mx, g, st);
-    case 160: return launch_sk_bn<160, EPI, false, 1, 2>(mw, mx, g, st);
-    case 192: return launch_sk_bn<192, EPI, false, 1, 2>(mw, mx, g, st);
-    case 224: return launch_sk_bn<224, EPI, false, 1, 2>(mw, mx, g, st);
-    case 256: return launch_sk_bn<256, EPI, false, 1, 2>(mw, mx, g, st);
-  }
-  return (int)cudaErrorInvalidValue;
+  return (int)psd::launch(gemm_sk_kernel<BN, EPI, TILED, NT>, dim3(g.G), dim3(kThreads), C::SMEM,
+                          st, mw, mx, g);
 }
 
 // two token tiles per weight tile (256 < M <= 512)
@@ -804,35 +776,24 @@ int num_sms_raw() {
 
 // stream-K geometry + workspace bytes (partials, then tickets)
 struct SKPlan {
-  int bn, nt, mw, KB, MT, tiles, G;
+  int bn, nt, KB, MT, tiles, G;
   long long U;
   size_t part_bytes, ticket_bytes;
 };
 // stream-K keeps one TMEM accumulator when it holds two token tiles (no epilogue
 // overlap), which only pays when a CTA covers >= 2 weight tiles
 // (70B gate/up at M = 320: 426 -> 294 us; 8B gate/up at M = 384: 110 -> 117 us)
-// PSD_GEMM_MW2=1: two weight tiles per stream-K unit for 96 <= M <= 256 (A/B)
-int mw2_enabled() {
-  static int v = [] {
-    const char* e = getenv("PSD_GEMM_MW2");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
 SKPlan sk_plan(int M, int N, int K, bool allow_nt2 = true) {
   SKPlan p;
   const TokGeo tg = tok_geo(M, allow_nt2 && (N / BM) >= 2 * num_sms());
   p.bn = tg.bn;
   p.nt = tg.nt;
-  p.mw = (allow_nt2 && tg.nt == 1 && tg.mt == 1 && tg.bn >= 96 && (N / BM) % 2 == 0 &&
-          mw2_enabled()) ? 2 : 1;
   p.KB = (K + BK - 1) / BK;
   p.MT = tg.mt;
-  p.tiles = (N / (BM * p.mw)) * p.MT;
+  p.tiles = (N / BM) * p.MT;
   p.U = (long long)p.tiles * p.KB;
   p.G = (int)std::min<long long>(num_sms(), p.U);
-  p.part_bytes = (size_t)p.G * 2 * p.mw * p.nt * p.bn * BM * sizeof(float);
+  p.part_bytes = (size_t)p.G * 2 * p.nt * p.bn * BM * sizeof(float);
   // tickets live at a FIXED offset (start of the workspace) so GEMMs of any
   // shape can share one workspace: each leaves its tickets zeroed
   p.ticket_bytes = (size_t)kMaxTiles * sizeof(int);
@@ -997,15 +958,6 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
     g.part = reinterpret_cast<float*>(static_cast<char*>(workspace) + p.ticket_bytes);
     g.Wt = nullptr;
     cudaStream_t st = (cudaStream_t)stream;
-    if (p.mw == 2) {
-      switch (epi) {
-        case PSD_EPI_BF16: return launch_sk_mw2<PSD_EPI_BF16>(p.bn, mw, mx, g, st);
-        case PSD_EPI_F32: return launch_sk_mw2<PSD_EPI_F32>(p.bn, mw, mx, g, st);
-        case PSD_EPI_RESID: return launch_sk_mw2<PSD_EPI_RESID>(p.bn, mw, mx, g, st);
-        case PSD_EPI_SILU: return launch_sk_mw2<PSD_EPI_SILU>(p.bn, mw, mx, g, st);
-      }
-      return (int)cudaErrorInvalidValue;
-    }
     if (p.nt == 2) {
       switch (epi) {
         case PSD_EPI_BF16: return launch_sk_nt2<PSD_EPI_BF16>(p.bn, mw, mx, g, st);
