@@ -67,6 +67,21 @@ int psd_verify_sample_rows(const float* target_logits, int64_t t_stride_b, int64
                            const float* uniforms, float temperature, int B, int K,
                            int32_t* accepted_len, int32_t* out_tokens, void* workspace,
                            size_t workspace_bytes, void* stream);
+/* psd_verify_sample_rows with cached draft-row statistics: d_stats (float2
+ * (M, S) per draft row, row (b, i) at d_stats[draft_rows[b] * d_stats_ld + i];
+ * NULL: computed from the draft rows) skips re-reading the draft rows, and
+ * t_stats_out[t_stats_rows[b]] (NULL: not written; negative row: skipped)
+ * receives the (M, S) of target row 0 -- the draft sampler (K = 0) publishes
+ * the statistics of the distribution it sampled from.  Same canonical
+ * arithmetic either way, so results are bit-identical. */
+int psd_verify_sample_ext(const float* target_logits, int64_t t_stride_b, int64_t t_stride_i,
+                          int V, const float* draft_logits, const int32_t* draft_rows,
+                          int64_t d_stride_row, int64_t d_stride_i, int Vd,
+                          const int32_t* draft_ids, const int32_t* draft_len,
+                          const float* uniforms, float temperature, int B, int K,
+                          int32_t* accepted_len, int32_t* out_tokens, const void* d_stats,
+                          int64_t d_stats_ld, void* t_stats_out, const int32_t* t_stats_rows,
+                          void* ws, size_t ws_bytes, void* stream);
 
 /* ---- K2: bf16 GEMM on tcgen05 (TMEM accumulators, TMA, mbarrier ring) -----
  *   Y[m, n] = epi( sum_k X[m*ldx + k] * W[n*ldw + k] )   X [M,K], W [N,K] bf16

@@ -51,6 +51,14 @@ struct Params {
   int* cnt_a; int* cnt_b;
   float2* part; Plan* plan; float* wblk;
   int NS, NB, R;
+  // cached softmax statistics (M, S) of the draft rows: row (b, i) at
+  // d_stats[d_rows[b] * d_stats_ld + i].  The draft sampler computed them with
+  // the same canonical arithmetic when it drew the token, so the verifier does
+  // not stream the draft rows again (null: computed here)
+  const float2* d_stats; int64_t d_stats_ld;
+  // output: (M, S) of target row 0 of request b to t_stats_out[t_stats_rows[b]]
+  // (skipped for a negative row) -- how the draft sampler publishes them
+  float2* t_stats_out; const int32_t* t_stats_rows;
 };
 
 __device__ __forceinline__ float4 ld_stream(const float* p) {
@@ -143,7 +151,7 @@ __device__ __forceinline__ float shfl_add_tree(float v) {
 __device__ __forceinline__ int expected_stats(const Params& p, int kb, bool sample) {
   const int nst = (p.V + PSD_SLICE - 1) / PSD_SLICE;
   const int nsd = (p.Vd + PSD_SLICE - 1) / PSD_SLICE;
-  return nst * (kb + 1) + (sample ? nsd * kb : 0);
+  return nst * (kb + 1) + (sample && !p.d_stats ? nsd * kb : 0);
 }
 
 // one (request b, row r, slice) statistics item; the last item of request b
@@ -154,7 +162,7 @@ __device__ __forceinline__ void stats_item(const Params& p, int slice, int b, in
   const bool is_draft = r > p.K;
   const int i = is_draft ? r - (p.K + 1) : r;
   const int n = is_draft ? p.Vd : p.V;
-  const bool active = (is_draft ? i < kb : i <= kb) && slice * PSD_SLICE < n;
+  const bool active = (is_draft ? i < kb && !p.d_stats : i <= kb) && slice * PSD_SLICE < n;
   if (!active) return;
   const int db = p.d_rows ? p.d_rows[b] : b;
   const float* row = is_draft ? p.d + db * p.dsb + i * p.dsi : p.t + b * p.tsb + i * p.tsi;
@@ -268,12 +276,20 @@ __device__ __forceinline__ void stats_item(const Params& p, int slice, int b, in
   __shared__ int sG[PSD_MAX_K + 1];
   const int nst = (p.V + PSD_SLICE - 1) / PSD_SLICE;
   const int nsd = (p.Vd + PSD_SLICE - 1) / PSD_SLICE;
-  const int nrows = SAMPLE ? 2 * kb + 1 : kb + 1;
+  const int nrows = SAMPLE && !p.d_stats ? 2 * kb + 1 : kb + 1;
   // stage every partial of request b in shared memory (parallel loads)
   for (int q = tid; q < nrows * p.NS; q += kThreads) {
     const int rowi = q / p.NS, sl = q % p.NS;
     const int rr = rowi > kb ? p.K + 1 + (rowi - (kb + 1)) : rowi;
     s_part[q] = __ldcg(p.part + (b * p.R + rr) * p.NS + sl);
+  }
+  if constexpr (SAMPLE) {
+    if (p.d_stats && tid < kb) {
+      const float2 st = __ldcg(p.d_stats + (int64_t)(p.d_rows ? p.d_rows[b] : b) * p.d_stats_ld +
+                               tid);
+      sMd[tid] = st.x;
+      sSd[tid] = st.y;
+    }
   }
   __syncthreads();
   if (tid < nrows) {
@@ -316,6 +332,12 @@ __device__ __forceinline__ void stats_item(const Params& p, int slice, int b, in
     if (lane <= p.K) o[lane] = lane < a ? x : (!SAMPLE && lane == a ? sG[a] : -1);
     if (lane == 0) {
       p.acc[b] = a;
+      if (p.t_stats_out) {
+        const int dst = p.t_stats_rows[b];
+        if constexpr (SAMPLE) {
+          if (dst >= 0) p.t_stats_out[dst] = make_float2(sMt[0], sSt[0]);
+        }
+      }
       if constexpr (SAMPLE) {
         Plan pl;
         pl.row = a;
@@ -712,6 +734,21 @@ int psd_verify_sample_rows(const float* target_logits, int64_t t_stride_b, int64
                       const int32_t* draft_ids, const int32_t* draft_len, const float* uniforms,
                       float temperature, int B, int K, int32_t* accepted_len,
                       int32_t* out_tokens, void* ws, size_t ws_bytes, void* stream) {
+  return psd_verify_sample_ext(target_logits, t_stride_b, t_stride_i, V, draft_logits, draft_rows,
+                               d_stride_row, d_stride_i, Vd, draft_ids, draft_len, uniforms,
+                               temperature, B, K, accepted_len, out_tokens, nullptr, 0, nullptr,
+                               nullptr, ws, ws_bytes, stream);
+}
+
+int psd_verify_sample_ext(const float* target_logits, int64_t t_stride_b, int64_t t_stride_i,
+                          int V, const float* draft_logits, const int32_t* draft_rows,
+                          int64_t d_stride_row, int64_t d_stride_i, int Vd,
+                          const int32_t* draft_ids, const int32_t* draft_len,
+                          const float* uniforms, float temperature, int B, int K,
+                          int32_t* accepted_len, int32_t* out_tokens, const void* d_stats,
+                          int64_t d_stats_ld, void* t_stats_out, const int32_t* t_stats_rows,
+                          void* ws, size_t ws_bytes, void* stream) {
+  if (t_stats_out && !t_stats_rows) return (int)cudaErrorInvalidValue;
   const WsLayout L = layout(B, K, V, Vd, 1);
   int rc = check_common(target_logits, t_stride_b, t_stride_i, V, B, K, ws, ws_bytes, L.total);
   if (rc) return rc;
@@ -725,6 +762,10 @@ int psd_verify_sample_rows(const float* target_logits, int64_t t_stride_b, int64
   p.t = target_logits; p.tsb = t_stride_b; p.tsi = t_stride_i; p.V = V;
   p.d = draft_logits; p.dsb = d_stride_row; p.dsi = d_stride_i; p.Vd = Vd;
   p.d_rows = draft_rows;
+  p.d_stats = static_cast<const float2*>(d_stats);
+  p.d_stats_ld = d_stats_ld;
+  p.t_stats_out = static_cast<float2*>(t_stats_out);
+  p.t_stats_rows = t_stats_rows;
   p.ids = draft_ids; p.len = draft_len; p.u = uniforms;
   p.c = psd_scale(1.0f / temperature); p.B = B; p.K = K; p.acc = accepted_len; p.out = out_tokens;
   p.cnt_a = reinterpret_cast<int*>(w + L.cnt_a); p.cnt_b = reinterpret_cast<int*>(w + L.cnt_b);

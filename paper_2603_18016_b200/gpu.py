@@ -135,6 +135,9 @@ class GpuBackend:
                 # K1 reads request b's rows at qbuf[slot_b] (verify_sample_rows)
                 self.qbuf = torch.empty(nslot * K, self.dshape.vocab, dtype=torch.float32,
                                         device=dev)
+                # their canonical (max, sum): written by the draft sampler, read by
+                # K1 instead of re-streaming the q rows (psd_verify_sample_ext)
+                self.qstats = torch.zeros(nslot * K, 2, dtype=torch.float32, device=dev)
                 self.d_u = torch.empty(K, B, dtype=torch.float32, device=dev)
                 self.v_u = torch.empty(B, K + 1, dtype=torch.float32, device=dev)
                 # per-row (request id, committed length) keys of the uniforms
@@ -179,6 +182,8 @@ class GpuBackend:
         # verify GEMM grids capped below the SM count when the draft loop runs
         # beside them (dual stream): PSD_VERIFY_CTAS (0 = all SMs)
         self.verify_ctas = int(os.environ.get("PSD_VERIFY_CTAS", "116")) if dual_stream else 0
+        # PSD_QSTATS_CACHE=0 makes K1 re-read the draft rows (A/B runs)
+        self.qstats_cache = os.environ.get("PSD_QSTATS_CACHE", "1") == "1"
         self.seed_draft = (seed * 0x9E3779B1 + 0xD7A7) & 0xFFFFFFFFFFFF
         self.seed_verify = (seed * 0x85EBCA77 + 0x7E51) & 0xFFFFFFFFFFFF
         self.capture_verify = None  # set to a list to record K1 inputs (tests)
@@ -535,7 +540,9 @@ class GpuBackend:
                     u.data_ptr(), st), "draft uniforms")
                 ops.verify_sample(self.dlogits[:nb].view(nb, 1, -1), self.d_dummy[:nb, :0],
                                   self.d_ids0[:nb], self.d_len0[:nb], u.view(nb, 1),
-                                  self.temperature, self.d_acc[:nb], self.d_out[:nb])
+                                  self.temperature, self.d_acc[:nb], self.d_out[:nb],
+                                  t_stats_out=self.qstats,
+                                  t_stats_rows=self.d_key[2 * B + i * B:2 * B + i * B + nb])
             native.check(lib.psd_index_copy_i32(self.slot_tok.data_ptr(),
                                                 fwd.view("scatter_dst", i).data_ptr(),
                                                 self.d_out.data_ptr(), None, nb, st),
@@ -650,12 +657,16 @@ class GpuBackend:
                 self.v_u.data_ptr(), st), "verify uniforms")
             Vd = self.dshape.vocab
             ws = ops._verify_workspace(self.device, nb, kmax, self.tshape.vocab, Vd, True)
-            native.check(lib.psd_verify_sample_rows(
+            # the q statistics are cached when this process drew the drafts; a
+            # dedicated draft GPU (pair.py) ships only the q rows
+            cached = "draft" in self.roles and self.qstats_cache
+            native.check(lib.psd_verify_sample_ext(
                 logits.data_ptr(), K1 * self.tshape.vocab, self.tshape.vocab,
                 self.tshape.vocab, self.qbuf.data_ptr(), v_slot.data_ptr(), self.k_max * Vd, Vd,
                 Vd, v_ids.data_ptr(), v_len.data_ptr(), self.v_u.data_ptr(), self.temperature, nb,
-                kmax, self.v_acc.data_ptr(), out.data_ptr(), ws.data_ptr(), ws.numel(), st),
-                "verify_sample_rows")
+                kmax, self.v_acc.data_ptr(), out.data_ptr(),
+                self.qstats.data_ptr() if cached else None, self.k_max, None, None,
+                ws.data_ptr(), ws.numel(), st), "verify_sample_ext")
         native.check(lib.psd_commit(self.v_acc.data_ptr(), out.data_ptr(), kmax,
                                     v_slot.data_ptr(), nb, self.generated.data_ptr(),
                                     self.slot_tok.data_ptr(), self.ldt, self.outputs.data_ptr(),

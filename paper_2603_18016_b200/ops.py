@@ -85,11 +85,16 @@ def verify_greedy(target_logits: torch.Tensor, draft_ids: torch.Tensor,
 def verify_sample(target_logits: torch.Tensor, draft_logits: torch.Tensor,
                   draft_ids: torch.Tensor, draft_len: torch.Tensor, uniforms: torch.Tensor,
                   temperature: float = 1.0, accepted_len: torch.Tensor | None = None,
-                  out_tokens: torch.Tensor | None = None):
+                  out_tokens: torch.Tensor | None = None, d_stats: torch.Tensor | None = None,
+                  t_stats_out: torch.Tensor | None = None,
+                  t_stats_rows: torch.Tensor | None = None):
     """Speculative rejection sampling (K1).
 
     target_logits [B, K+1, V], draft_logits [B, K, Vd] fp32 (Vd <= V);
     uniforms [B, K+1] fp32 in [0, 1).  Returns (accepted_len, out_tokens).
+    d_stats [B, K, 2] fp32: cached (max, sum) of the draft rows (not re-read);
+    t_stats_out [*, 2] + t_stats_rows [B] int32: receive the (max, sum) of
+    target row 0 (psd_verify_sample_ext).
     """
     _check(target_logits, "target_logits", torch.float32, 3)
     _check(draft_logits, "draft_logits", torch.float32, 3)
@@ -114,6 +119,19 @@ def verify_sample(target_logits: torch.Tensor, draft_logits: torch.Tensor,
         draft_logits, Vd = target_logits, V
     db, di = _rows_view(draft_logits, "draft_logits")
     lib = native.load()
+    if d_stats is not None or t_stats_out is not None:
+        if d_stats is not None:
+            _check(d_stats, "d_stats", torch.float32, 3)
+        native.check(lib.psd_verify_sample_ext(
+            target_logits.data_ptr(), sb, si, V, draft_logits.data_ptr(), None, db, di, Vd,
+            draft_ids.contiguous().data_ptr(), draft_len.contiguous().data_ptr(),
+            uniforms.contiguous().data_ptr(), float(temperature), B, K, accepted_len.data_ptr(),
+            out_tokens.data_ptr(), d_stats.data_ptr() if d_stats is not None else None,
+            d_stats.stride(0) // 2 if d_stats is not None else 0,
+            t_stats_out.data_ptr() if t_stats_out is not None else None,
+            t_stats_rows.data_ptr() if t_stats_rows is not None else None,
+            ws.data_ptr(), ws.numel(), _stream_ptr(dev)), "psd_verify_sample_ext")
+        return accepted_len, out_tokens
     native.check(lib.psd_verify_sample(
         target_logits.data_ptr(), sb, si, V, draft_logits.data_ptr(), db, di, Vd,
         draft_ids.contiguous().data_ptr(), draft_len.contiguous().data_ptr(),

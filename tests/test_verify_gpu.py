@@ -90,3 +90,35 @@ def test_gpu_golden_vectors(cuda_device):
         ga, go = _run_gpu(t, d, ids, ln, u, c["greedy"], c["temperature"])
         assert ga.tolist() == c["accepted_len"], c["name"]
         assert go.tolist() == c["out_tokens"], c["name"]
+
+
+@pytest.mark.parametrize("B,K,V,Vd,temperature", [(32, 5, 128256, 128256, 1.0),
+                                                  (8, 8, 152064, 151936, 0.7),
+                                                  (5, 3, 8192, 8192, 1.3)])
+def test_cached_draft_stats_bit_exact(cuda_device, B, K, V, Vd, temperature):
+    """psd_verify_sample_ext: the draft sampler's pass (K = 0 over the draft
+    rows) publishes each row's canonical (max, sum); K1 given those cached
+    statistics skips re-reading the draft rows and still matches the oracle
+    (and the uncached kernel) bit for bit."""
+    t, d, ids, ln, u = _gen.verify_case(B * 7 + K, B, K, V, tau=0.6, greedy=False, Vd=Vd)
+    dev = cuda_device
+    dd = torch.from_numpy(d).to(dev)
+    rows = dd.reshape(B * K, 1, Vd)
+    stats = torch.full((B, K, 2), float("nan"), device=dev)
+    zeros = torch.zeros(B * K, dtype=torch.int32, device=dev)
+    ops.verify_sample(rows, rows[:, :0], torch.zeros(B * K, 0, dtype=torch.int32, device=dev),
+                      zeros, torch.rand(B * K, 1, device=dev), temperature,
+                      t_stats_out=stats.view(B * K, 2),
+                      t_stats_rows=torch.arange(B * K, dtype=torch.int32, device=dev))
+    tt = torch.from_numpy(t).to(dev)
+    ii = torch.from_numpy(np.ascontiguousarray(ids)).to(dev)
+    ll = torch.from_numpy(ln).to(dev)
+    uu = torch.from_numpy(u).to(dev)
+    acc, out = ops.verify_sample(tt, dd, ii, ll, uu, temperature, d_stats=stats)
+    acc0, out0 = ops.verify_sample(tt, dd, ii, ll, uu, temperature)
+    torch.cuda.synchronize()
+    ea, eo = ov.verify_sample(t, d, ids, ln, u, temperature)
+    np.testing.assert_array_equal(acc.cpu().numpy(), ea)
+    np.testing.assert_array_equal(out.cpu().numpy(), eo)
+    np.testing.assert_array_equal(acc0.cpu().numpy(), ea)
+    np.testing.assert_array_equal(out0.cpu().numpy(), eo)

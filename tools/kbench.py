@@ -192,17 +192,28 @@ def rope_case(tag, M, Hq, Hkv, D, S):
     report(f"rope_kv {tag}", f"M={M} S={S}", us, M * N * 4 * S + M * N * 2)
 
 
-def verify_case(tag, B, K, V, sampling):
+def verify_case(tag, B, K, V, sampling, cached=False):
     sets = [make_inputs(B, K, V, sampling, dev, seed=i) for i in range(3)]
+    stats = []
+    if cached:  # the draft sampler's (max, sum) of every q row (psd_verify_sample_ext)
+        for t, d, ids, ln, u in sets:
+            st = torch.empty(B, K, 2, device=dev)
+            rows = d.reshape(B * K, 1, -1)
+            ops.verify_sample(rows, rows[:, :0], torch.zeros(B * K, 0, dtype=torch.int32,
+                                                             device=dev),
+                              torch.zeros(B * K, dtype=torch.int32, device=dev),
+                              torch.rand(B * K, 1, device=dev), t_stats_out=st.view(B * K, 2),
+                              t_stats_rows=torch.arange(B * K, dtype=torch.int32, device=dev))
+            stats.append(st)
     it = [0]
 
     def fn():
         t, d, ids, ln, u = sets[it[0] % 3]
-        it[0] += 1
         if sampling:
-            ops.verify_sample(t, d, ids, ln, u)
+            ops.verify_sample(t, d, ids, ln, u, d_stats=stats[it[0] % 3] if cached else None)
         else:
             ops.verify_greedy(t, ids, ln)
+        it[0] += 1
     us = timeit(fn)
     report(f"K1 {tag}", f"B={B} k={K} V={V}", us, algorithmic_bytes(B, K, V, sampling))
 
@@ -316,6 +327,7 @@ def main():
     if want("k1"):
         verify_case("greedy cfg2", 32, 5, 128256, False)
         verify_case("sample cfg2", 32, 5, 128256, True)
+        verify_case("sample cfg2 cachedq", 32, 5, 128256, True, cached=True)
         verify_case("draft argmax", 32, 0, 128256, False)
     if a.json:
         json.dump({"peak_gbps": PEAK, "rows": rows}, open(a.json, "w"), indent=1)
