@@ -88,6 +88,9 @@ PRESETS: dict[str, ModelShape] = {
                                None, tie_embeddings=True, qkv_bias=True, rms_eps=1e-6),
     # BASELINE config 1: tiny random-init pair
     "tiny-target": ModelShape("tiny-target", 1024, 256, 4, 8, 2, 32, 688, 10000.0),
+    # tiny Qwen2-style model (qkv bias, tied embeddings): the bias paths in tests
+    "tiny-qwen": ModelShape("tiny-qwen", 1024, 128, 2, 4, 2, 32, 344, 1000000.0, None,
+                            tie_embeddings=True, qkv_bias=True, rms_eps=1e-6),
     # tiny target whose QKV shards stay 128-row aligned at TP = 2 (tests)
     "tiny-target-tp": ModelShape("tiny-target-tp", 1024, 256, 4, 8, 4, 32, 688, 10000.0),
     "tiny-draft": ModelShape("tiny-draft", 1024, 128, 2, 4, 2, 32, 344, 10000.0),

@@ -213,3 +213,55 @@ def test_online_k_tuner_on_gpu_keeps_greedy_tokens(cuda_device):
     assert [r.output_ids for r in st.request_list()] == [r.output_ids for r in ref.request_list()]
     assert tuner.p is not None and tuner.d and tuner.v
     assert all(1 <= h[1] <= 4 for h in tuner.history)
+
+
+@pytest.mark.parametrize("preset", ["tiny-qwen", "tiny-draft", "tiny-target"])
+def test_decode_step_matches_oracle(cuda_device, preset):
+    """Decode passes (1-2 query tokens per sequence) take the fused RoPE + KV
+    write + attention kernel (psd_attention_rope), incl. the Qwen2 qkv bias;
+    their logits match the numpy oracle within rtol 1e-2 after a prefill."""
+    shape = PRESETS[preset]
+    dev = cuda_device
+    m = Transformer(shape, dev, seed=21, num_blocks=16, block_size=16, max_blocks_per_seq=8)
+    bt = torch.zeros(4, 8, dtype=torch.int32, device=dev)
+    bt[0, :4] = torch.tensor([1, 2, 3, 4])
+    bt[1, :4] = torch.tensor([5, 6, 7, 8])
+    fwd = Forward(m, 128, 8, 64, bt)
+    rng = np.random.default_rng(3)
+    lens = [19, 33]
+    toks = [rng.integers(0, shape.vocab, n).tolist() for n in lens]
+    nxt = [rng.integers(0, shape.vocab, q).tolist() for q in (1, 2)]
+
+    def slot(s, p):
+        return bt[s, p // 16].item() * 16 + p % 16
+
+    def stage_run(seq_toks, p0s, logits_rows):
+        flat = np.concatenate(seq_toks).astype(np.int32)
+        pos = np.concatenate([np.arange(p0, p0 + len(t)) for t, p0 in zip(seq_toks, p0s)])
+        slots = np.concatenate([[slot(s, p0 + i) for i in range(len(t))]
+                                for s, (t, p0) in enumerate(zip(seq_toks, p0s))])
+        qs = np.cumsum([0] + [len(t) for t in seq_toks])[:-1]
+        fwd.begin()
+        fwd.stage(0, {"tokens": flat, "positions": pos.astype(np.int32),
+                      "slots": slots.astype(np.int32), "seq_slot": np.asarray([0, 1], np.int32),
+                      "q_start": qs.astype(np.int32),
+                      "q_len": np.asarray([len(t) for t in seq_toks], np.int32),
+                      "q_pos0": np.asarray(p0s, np.int32),
+                      "kv_len": np.asarray([p0 + len(t) for t, p0 in zip(seq_toks, p0s)],
+                                           np.int32),
+                      "logit_rows": np.asarray(logits_rows, np.int32)})
+        fwd.upload(1)
+        out = torch.empty(len(logits_rows), shape.vocab, dtype=torch.float32, device=dev)
+        fwd.run(len(flat), 2, max(len(t) for t in seq_toks), len(logits_rows), out, shape.vocab)
+        torch.cuda.synchronize()
+        return out.cpu().numpy()
+
+    stage_run(toks, [0, 0], [0])                     # prefill (unfused RoPE path)
+    got = stage_run(nxt, lens, [0, 1, 2])            # decode: fused RoPE + attention
+    om = OracleModel(shape, 21)
+    caches = [om.new_cache(64), om.new_cache(64)]
+    om.forward([(toks[0], 0), (toks[1], 0)], caches)
+    h = om.forward([(nxt[0], lens[0]), (nxt[1], lens[1])], caches)
+    ref = om.logits(h, np.concatenate(nxt))
+    err = np.abs(got - ref).max()
+    assert err <= 1e-2 * np.abs(ref).max(), err
