@@ -51,12 +51,12 @@ struct GemmArgs {
 
 // NT token tiles of BN rows per weight tile (NT = 2 for 256 < M <= 512: every
 // weight byte is streamed once instead of once per token tile)
-template <int BN, int NT = 1>
+template <int BN, int NT = 1, int SMEM_KB = 200>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = NT * BN * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int MAXS = (200 * 1024) / STAGE;
+  static constexpr int MAXS = (SMEM_KB * 1024) / STAGE;
   static constexpr int STAGES = MAXS > 8 ? 8 : MAXS;
   static constexpr int TMEM_COLS = NT * BN <= 32 ? 32 : NT * BN <= 64 ? 64
                                  : NT * BN <= 128 ? 128 : NT * BN <= 256 ? 256 : 512;
@@ -248,7 +248,14 @@ struct SKArgs {
   float* part;    // [G][2][BN * 128]
   int* tickets;   // [tiles], zero between launches
   const __nv_bfloat16* Wt;  // pre-tiled weights (TILED variant)
+  unsigned long long* trace;  // optional [G][8] globaltimer ns (psd_gemm_set_trace)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 struct Seg {
   int t, kb0, kb1, first;  // tile, k-block range, is the CTA's first segment
@@ -265,14 +272,15 @@ __device__ __forceinline__ int sk_owner(long long u, const SKArgs& g) {
   return (int)c;
 }
 
-template <int BN, int EPI, bool TILED, int NT = 1>
+template <int BN, int EPI, bool TILED, int NT = 1, int SMEM_KB = 200>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                const SKArgs g) {
-  using C = Cfg<BN, NT>;
+  using C = Cfg<BN, NT, SMEM_KB>;
   constexpr int ACC_COLS = NT * BN;           // one accumulator slot (NT token tiles)
   constexpr int NACC = NT == 1 ? 2 : 1;       // TMEM double buffer when it fits
   constexpr int TB = BN * BK * 2;             // bytes of one token tile's k-block
+  constexpr int EG = 4;                       // epilogue: 16-column groups per round
   constexpr int TMEM_COLS = NACC * ACC_COLS <= 32 ? 32 : NACC * ACC_COLS <= 64 ? 64
                           : NACC * ACC_COLS <= 128 ? 128 : NACC * ACC_COLS <= 256 ? 256 : 512;
   extern __shared__ uint8_t smem_raw[];
@@ -292,6 +300,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   const long long u0 = sk_bound(c, g), u1 = sk_bound(c + 1, g);
 
   if (warp == 0 && lane == 0) {
+    if (g.trace) g.trace[c * 8 + 0] = gtimer();
     tma_prefetch(&tmW);
     tma_prefetch(&tmX);
     for (int s = 0; s < C::STAGES; ++s) {
@@ -396,6 +405,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           const uint32_t ph = (i / C::STAGES) & 1;
           mbar_wait(full + s, ph);
           tc_fence_after();
+          if (i == 0 && g.trace) g.trace[c * 8 + 1] = gtimer();
           const uint32_t sa = smem_u32(sA + s * C::A_BYTES);
           const uint32_t sb = smem_u32(sB + s * C::B_BYTES);
 #pragma unroll
@@ -410,6 +420,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         mma_commit(tfull + a);
         ++j;
       }
+      if (g.trace) g.trace[c * 8 + 2] = gtimer();
     }
     __syncwarp();
   } else {
@@ -424,90 +435,133 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       const uint32_t aph = (j / NACC) & 1;
       mbar_wait(tfull + a, aph);
       tc_fence_after();
+      if (g.trace && threadIdx.x == 64) g.trace[c * 8 + 3] = gtimer();
       const uint32_t tbase = tmem + a * ACC_COLS + ((uint32_t)(32 * q) << 16);
       const int n0 = (sg.t / g.MT) * BM, m0 = (sg.t % g.MT) * ACC_COLS;
       const bool split = sg.kb0 != 0 || sg.kb1 != g.KB;
       int owner = c, last = c;
       bool finisher = true;
       if (split) {
-        // publish this segment's partial, take a ticket
         owner = sk_owner((long long)sg.t * g.KB, g);
         last = sk_owner((long long)sg.t * g.KB + g.KB - 1, g);
-        float* mine = g.part + ((size_t)c * 2 + (sg.first ? 0 : 1)) * (ACC_COLS * BM);
+        int* flag = s_flag + (j & 1);
+        // every other contributor already published: finish without
+        // publishing (the usual case for the tile a CTA ends on, i.e. the tail)
+        if (threadIdx.x == 64) *flag = ld_acquire_gpu(g.tickets + sg.t) == last - owner;
+        named_bar_sync(1, 128);
+        finisher = *flag;
+        if (g.trace && finisher && threadIdx.x == 64) g.trace[c * 8 + 6] += 1;
+        if (!finisher) {
+          // publish this segment's partial, take a ticket
+          float* mine = g.part + ((size_t)c * 2 + (sg.first ? 0 : 1)) * (ACC_COLS * BM);
 #pragma unroll 1
-        for (int col = 0; col < ACC_COLS; col += 16) {
-          uint32_t r[16];
-          tmem_ld16(tbase + (uint32_t)col, r);
-          tmem_ld_wait();
+          for (int col0 = 0; col0 < ACC_COLS; col0 += 16 * EG) {
+            uint32_t r[EG][16];
 #pragma unroll
-          for (int k = 0; k < 16; ++k) mine[(col + k) * BM + row] = __uint_as_float(r[k]);
+            for (int e = 0; e < EG; ++e)
+              if (col0 + 16 * e < ACC_COLS) tmem_ld16(tbase + (uint32_t)(col0 + 16 * e), r[e]);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < EG; ++e)
+              if (col0 + 16 * e < ACC_COLS) {
+#pragma unroll
+                for (int k = 0; k < 16; ++k)
+                  mine[(col0 + 16 * e + k) * BM + row] = __uint_as_float(r[e][k]);
+              }
+          }
+          __threadfence();
+          named_bar_sync(1, 128);
+          if (threadIdx.x == 64) {
+            const int tk = atomicAdd(g.tickets + sg.t, 1);
+            *flag = tk == last - owner;
+          }
+          named_bar_sync(1, 128);
+          finisher = *flag;
         }
-        __threadfence();
-        named_bar_sync(1, 128);
-        if (threadIdx.x == 64) {
-          const int tk = atomicAdd(g.tickets + sg.t, 1);
-          *s_flag = tk == last - owner;
-        }
-        named_bar_sync(1, 128);
-        finisher = *s_flag;
         if (finisher) __threadfence();
       }
       if (finisher) {
+        // EG column groups per round: one TMEM wait and one L2 round trip for
+        // the contributors' partials per 16*EG columns (the finisher of the
+        // last tile is the kernel's tail)
 #pragma unroll 1
-        for (int col = 0; col < ACC_COLS; col += 16) {
-          uint32_t r[16];
-          tmem_ld16(tbase + (uint32_t)col, r);
+        for (int col0 = 0; col0 < ACC_COLS; col0 += 16 * EG) {
+          uint32_t r[EG][16];
+#pragma unroll
+          for (int e = 0; e < EG; ++e)
+            if (col0 + 16 * e < ACC_COLS) tmem_ld16(tbase + (uint32_t)(col0 + 16 * e), r[e]);
           tmem_ld_wait();
-          float v[16];
+          float v[EG][16];
           if (split) {
             // sum contributors in CTA order (own values from TMEM)
 #pragma unroll
-            for (int k = 0; k < 16; ++k) v[k] = 0.f;
+            for (int e = 0; e < EG; ++e)
+#pragma unroll
+              for (int k = 0; k < 16; ++k) v[e][k] = 0.f;
             for (int cc = owner; cc <= last; ++cc) {
               if (cc == c) {
 #pragma unroll
-                for (int k = 0; k < 16; ++k) v[k] += __uint_as_float(r[k]);
+                for (int e = 0; e < EG; ++e)
+#pragma unroll
+                  for (int k = 0; k < 16; ++k) v[e][k] += __uint_as_float(r[e][k]);
               } else {
                 const bool first_of_cc = sk_bound(cc, g) >= (long long)sg.t * g.KB;
                 const float* pp = g.part + ((size_t)cc * 2 + (first_of_cc ? 0 : 1)) * (ACC_COLS * BM);
+                float w[EG][16];
 #pragma unroll
-                for (int k = 0; k < 16; ++k) v[k] += __ldcg(pp + (col + k) * BM + row);
+                for (int e = 0; e < EG; ++e)
+                  if (col0 + 16 * e < ACC_COLS) {
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) w[e][k] = __ldcg(pp + (col0 + 16 * e + k) * BM + row);
+                  }
+#pragma unroll
+                for (int e = 0; e < EG; ++e)
+#pragma unroll
+                  for (int k = 0; k < 16; ++k) v[e][k] += w[e][k];
               }
             }
           } else {
 #pragma unroll
-            for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(r[k]);
+            for (int e = 0; e < EG; ++e)
+#pragma unroll
+              for (int k = 0; k < 16; ++k) v[e][k] = __uint_as_float(r[e][k]);
           }
-          if constexpr (EPI == PSD_EPI_SILU) {
-            const int jo = (n0 / BM) * 64 + 16 * q + (lane & 15);
-            __nv_bfloat16* Y = static_cast<__nv_bfloat16*>(g.Y);
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
-              const float up = __shfl_down_sync(0xffffffffu, v[k], 16);
-              v[k] = silu(v[k]) * up;  // all lanes: no divergence in the math
-            }
-            if (lane < 16) {
+          for (int e = 0; e < EG; ++e) {
+            const int col = col0 + 16 * e;
+            if (col >= ACC_COLS) break;
+            if constexpr (EPI == PSD_EPI_SILU) {
+              const int jo = (n0 / BM) * 64 + 16 * q + (lane & 15);
+              __nv_bfloat16* Y = static_cast<__nv_bfloat16*>(g.Y);
 #pragma unroll
               for (int k = 0; k < 16; ++k) {
-                const int m = m0 + col + k;
-                if (m < g.M) Y[(size_t)m * g.ldy + jo] = __float2bfloat16(v[k]);
+                const float up = __shfl_down_sync(0xffffffffu, v[e][k], 16);
+                v[e][k] = silu(v[e][k]) * up;  // all lanes: no divergence in the math
               }
-            }
-          } else {
-            const int n = n0 + row;
-            if (n < g.N) {
+              if (lane < 16) {
 #pragma unroll
-              for (int k = 0; k < 16; ++k) {
-                const int m = m0 + col + k;
-                if (m >= g.M) break;
-                if constexpr (EPI == PSD_EPI_F32) {
-                  static_cast<float*>(g.Y)[(size_t)m * g.ldy + n] = v[k];
-                } else if constexpr (EPI == PSD_EPI_RESID) {
-                  __nv_bfloat16* Y = static_cast<__nv_bfloat16*>(g.Y);
-                  const float rv = __bfloat162float(g.R[(size_t)m * g.ldr + n]);
-                  Y[(size_t)m * g.ldy + n] = __float2bfloat16(v[k] + rv);
-                } else {
-                  static_cast<__nv_bfloat16*>(g.Y)[(size_t)m * g.ldy + n] = __float2bfloat16(v[k]);
+                for (int k = 0; k < 16; ++k) {
+                  const int m = m0 + col + k;
+                  if (m < g.M) Y[(size_t)m * g.ldy + jo] = __float2bfloat16(v[e][k]);
+                }
+              }
+            } else {
+              const int n = n0 + row;
+              if (n < g.N) {
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                  const int m = m0 + col + k;
+                  if (m >= g.M) break;
+                  if constexpr (EPI == PSD_EPI_F32) {
+                    static_cast<float*>(g.Y)[(size_t)m * g.ldy + n] = v[e][k];
+                  } else if constexpr (EPI == PSD_EPI_RESID) {
+                    __nv_bfloat16* Y = static_cast<__nv_bfloat16*>(g.Y);
+                    const float rv = __bfloat162float(g.R[(size_t)m * g.ldr + n]);
+                    Y[(size_t)m * g.ldy + n] = __float2bfloat16(v[e][k] + rv);
+                  } else {
+                    static_cast<__nv_bfloat16*>(g.Y)[(size_t)m * g.ldy + n] =
+                        __float2bfloat16(v[e][k]);
+                  }
                 }
               }
             }
@@ -520,6 +574,10 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty + a);
       ++j;
+    }
+    if (g.trace && threadIdx.x == 64) {
+      g.trace[c * 8 + 4] = gtimer();
+      g.trace[c * 8 + 5] = j;
     }
   }
   tc_fence_before();
@@ -611,18 +669,24 @@ int launch_bn(const CUtensorMap& mw, const CUtensorMap& mx, const GemmArgs& g, d
 }
 
 
-template <int BN, int EPI, bool TILED, int NT = 1>
-int launch_sk_bn(const CUtensorMap& mw, const CUtensorMap& mx, const SKArgs& g, cudaStream_t st) {
-  using C = Cfg<BN, NT>;
+template <int BN, int EPI, bool TILED, int NT = 1, int SMEM_KB = 200>
+int launch_sk_bn_s(const CUtensorMap& mw, const CUtensorMap& mx, const SKArgs& g,
+                   cudaStream_t st) {
+  using C = Cfg<BN, NT, SMEM_KB>;
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_sk_kernel<BN, EPI, TILED, NT>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_sk_kernel<BN, EPI, TILED, NT, SMEM_KB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return (int)e;
     attr_done = true;
   }
-  return (int)psd::launch(gemm_sk_kernel<BN, EPI, TILED, NT>, dim3(g.G), dim3(kThreads), C::SMEM,
-                          st, mw, mx, g);
+  return (int)psd::launch(gemm_sk_kernel<BN, EPI, TILED, NT, SMEM_KB>, dim3(g.G), dim3(kThreads),
+                          C::SMEM, st, mw, mx, g);
+}
+
+template <int BN, int EPI, bool TILED, int NT = 1>
+int launch_sk_bn(const CUtensorMap& mw, const CUtensorMap& mx, const SKArgs& g, cudaStream_t st) {
+  return launch_sk_bn_s<BN, EPI, TILED, NT, 200>(mw, mx, g, st);
 }
 
 // two token tiles per weight tile (256 < M <= 512)
@@ -757,6 +821,12 @@ std::atomic<int>& max_ctas_cap() {
   return v;
 }
 
+// stream-K timeline buffer (psd_gemm_set_trace; null = off)
+std::atomic<unsigned long long*>& sk_trace() {
+  static std::atomic<unsigned long long*> v{nullptr};
+  return v;
+}
+
 int num_sms_raw();
 int num_sms() {
   const int cap = max_ctas_cap().load(std::memory_order_relaxed);
@@ -823,6 +893,10 @@ extern "C" {
 
 void psd_gemm_set_max_ctas(int n) { max_ctas_cap().store(n > 0 ? n : 0); }
 
+void psd_gemm_set_trace(void* trace) {
+  sk_trace().store(static_cast<unsigned long long*>(trace));
+}
+
 int psd_gemm_plan(int M, int N, int K, int epi, int splits_hint, int* splits_out,
                   size_t* workspace_bytes) {
   if (M <= 0 || N <= 0 || K <= 0 || (K % 8) || (N % BM)) return (int)cudaErrorInvalidValue;
@@ -882,6 +956,7 @@ int psd_gemm_tiled(const void* X, int ldx, int M, int K, const void* W_tiled, in
   g.Y = Y; g.ldy = ldy; g.R = static_cast<const __nv_bfloat16*>(R); g.ldr = ldr;
   g.tickets = static_cast<int*>(workspace);
   g.part = reinterpret_cast<float*>(static_cast<char*>(workspace) + p.ticket_bytes);
+  g.trace = sk_trace().load(std::memory_order_relaxed);
   g.Wt = static_cast<const __nv_bfloat16*>(W_tiled);
   cudaStream_t st = (cudaStream_t)stream;
   switch (epi) {
@@ -956,6 +1031,7 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
     g.Y = Y; g.ldy = ldy; g.R = static_cast<const __nv_bfloat16*>(R); g.ldr = ldr;
     g.tickets = static_cast<int*>(workspace);
     g.part = reinterpret_cast<float*>(static_cast<char*>(workspace) + p.ticket_bytes);
+    g.trace = sk_trace().load(std::memory_order_relaxed);
     g.Wt = nullptr;
     cudaStream_t st = (cudaStream_t)stream;
     if (p.nt == 2) {

@@ -60,6 +60,7 @@ SIGNATURES: dict[str, tuple] = {
                                          _p]),
     "psd_launch_count": (_c.c_longlong, []),
     "psd_gemm_set_max_ctas": (None, [_i]),
+    "psd_gemm_set_trace": (None, [_p]),
     "psd_mk_smem_bytes": (_sz, []),
     "psd_mk_create": (_p, [_p]),
     "psd_mk_destroy": (None, [_p]),
