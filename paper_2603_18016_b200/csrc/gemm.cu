@@ -480,6 +480,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         }
         if (finisher) __threadfence();
       }
+      if (g.trace && threadIdx.x == 64) g.trace[c * 8 + 7] = gtimer();
       if (finisher) {
         // EG column groups per round: one TMEM wait and one L2 round trip for
         // the contributors' partials per 16*EG columns (the finisher of the

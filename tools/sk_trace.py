@@ -33,7 +33,8 @@ def summarize(tag, tr):
             "mma_end": [(r[2] - t0) / 1e3 for r in rows],
             "last_acc": [(r[3] - t0) / 1e3 for r in rows],
             "epi_end": [(r[4] - t0) / 1e3 for r in rows],
-            "epi_tail": [(r[4] - r[3]) / 1e3 for r in rows]}
+            "epi_tail": [(r[4] - r[3]) / 1e3 for r in rows],
+            "epi_pre_rounds": [(r[7] - r[3]) / 1e3 for r in rows]}
     print(f"{tag}: {len(rows)} CTAs, span {max(cols['epi_end']):.2f} us, segments "
           f"{min(r[5] for r in rows)}-{max(r[5] for r in rows)}, fast finishes "
           f"{sum(r[6] for r in rows)}")
@@ -75,3 +76,5 @@ def case(tag, M, N, K, epi, copies=4):
 case("8B gate/up silu", 192, 28672, 4096, native.EPI_SILU)
 case("8B lm_head f32", 192, 128256, 4096, native.EPI_F32, copies=2)
 case("1B lm_head f32", 32, 128256, 2048, native.EPI_F32, copies=2)
+case("8B gate/up bf16", 192, 28672, 4096, native.EPI_BF16)
+case("8B gate/up M128 bf16", 128, 28672, 4096, native.EPI_BF16)
