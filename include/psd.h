@@ -106,9 +106,9 @@ int psd_verify_sample_ext(const float* target_logits, int64_t t_stride_b, int64_
 /* Cap the CTAs of subsequently enqueued (or captured) GEMM grids (0 = all SMs):
  * the verify forward runs beside the draft loop on one GPU. */
 void psd_gemm_set_max_ctas(int n);
-/* Diagnostics: a device buffer of [CTAs][8] u64 that subsequent stream-K GEMMs
+/* Diagnostics: a device buffer of [CTAs][16] u64 that subsequent stream-K GEMMs
  * fill with %globaltimer stamps per CTA (entry, first operands, last MMA
- * issued, last accumulator ready, epilogue done, segments, fast finishes);
+ * issued, last accumulator ready, epilogue done, segments, fast finishes, rounds);
  * NULL turns it off (default). */
 void psd_gemm_set_trace(void* trace);
 int psd_gemm_plan(int M, int N, int K, int epi, int splits_hint, int* splits_out,

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <mutex>
+#include <cstdio>
 #include <cstdlib>
 #include <utility>
 
@@ -27,6 +29,56 @@ inline int pdl_enabled() {
   return v;
 }
 
+// PSD_DEBUG_LAUNCH=1: report launches that fail or find their stream's
+// capture already invalidated (names the previous launch) on stderr
+inline int debug_launch() {
+  static int v = [] {
+    const char* e = getenv("PSD_DEBUG_LAUNCH");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+inline void debug_before(const void* k, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusInvalidated)
+    fprintf(stderr, "[psd] capture invalidated before %p\n", k);
+}
+inline void debug_after(const void* k, cudaError_t e, dim3 g, size_t smem, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (e != cudaSuccess || cs == cudaStreamCaptureStatusInvalidated)
+    fprintf(stderr, "[psd] launch %p grid (%u,%u,%u) smem %zu: %s%s\n", k, g.x, g.y, g.z, smem,
+            cudaGetErrorString(e), cs == cudaStreamCaptureStatusInvalidated ? " (capture invalidated)"
+                                                                           : "");
+}
+
+// raise a kernel's dynamic shared memory limit (call once per kernel, outside
+// stream capture: the first launch of every kernel is eager)
+inline cudaError_t set_smem_limit(const void* k, int bytes, cudaStream_t st = nullptr) {
+  const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (debug_launch()) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (st) cudaStreamIsCapturing(st, &cs);
+    fprintf(stderr, "[psd] smem limit %p = %d: %s%s\n", k, bytes, cudaGetErrorString(e),
+            cs == cudaStreamCaptureStatusNone ? "" : " (during capture)");
+  }
+  return e;
+}
+
+// set_smem_limit once per kernel (kernels sharing a signature share a
+// function-pointer type, so a per-type static flag would not do)
+inline cudaError_t ensure_smem_limit(const void* k, int bytes, cudaStream_t st = nullptr) {
+  static std::mutex mu;
+  static const void* done[64];
+  static int n = 0;
+  std::lock_guard<std::mutex> lock(mu);
+  for (int i = 0; i < n; ++i)
+    if (done[i] == k) return cudaSuccess;
+  const cudaError_t e = set_smem_limit(k, bytes, st);
+  if (e == cudaSuccess && n < 64) done[n++] = k;
+  return e;
+}
+
 template <typename... Params, typename... Args>
 inline cudaError_t launch(void (*kernel)(Params...), dim3 grid, dim3 block, size_t smem,
                           cudaStream_t st, Args&&... args) {
@@ -41,7 +93,10 @@ inline cudaError_t launch(void (*kernel)(Params...), dim3 grid, dim3 block, size
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+  if (debug_launch()) debug_before(reinterpret_cast<const void*>(kernel), st);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+  if (debug_launch()) debug_after(reinterpret_cast<const void*>(kernel), e, grid, smem, st);
+  return e;
 }
 }  // namespace psd
 

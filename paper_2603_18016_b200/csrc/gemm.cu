@@ -248,8 +248,19 @@ struct SKArgs {
   float* part;    // [G][2][BN * 128]
   int* tickets;   // [tiles], zero between launches
   const __nv_bfloat16* Wt;  // pre-tiled weights (TILED variant)
-  unsigned long long* trace;  // optional [G][8] globaltimer ns (psd_gemm_set_trace)
+  unsigned long long* trace;  // optional [G][16] globaltimer ns (psd_gemm_set_trace)
+  int D;                      // tiles 0..D-1 whole per CTA (c, c+G, ..), after its stream-K units
+  int tma_y;                  // finished tiles leave through TMA stores of tmY
+  CUtensorMap tmY;            // Y [M][N_out] (bf16 / f32), box 16 tokens x 128 (64 SiLU) rows
 };
+
+// finisher epilogue staging: 24 KB of rotating 16-token buffers (SiLU: 12 of
+// 16 x 64 bf16, bf16: 6 of 16 x 128, fp32: 3 of 16 x 128)
+constexpr int kEpBytes = 24 * 1024;
+template <int EPI>
+constexpr int ep_buf_bytes() {
+  return EPI == PSD_EPI_SILU ? 16 * 64 * 2 : EPI == PSD_EPI_F32 ? 16 * 128 * 4 : 16 * 128 * 2;
+}
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -275,7 +286,7 @@ __device__ __forceinline__ int sk_owner(long long u, const SKArgs& g) {
 template <int BN, int EPI, bool TILED, int NT = 1, int SMEM_KB = 200>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-               const SKArgs g) {
+               const __grid_constant__ SKArgs g) {
   using C = Cfg<BN, NT, SMEM_KB>;
   constexpr int ACC_COLS = NT * BN;           // one accumulator slot (NT token tiles)
   constexpr int NACC = NT == 1 ? 2 : 1;       // TMEM double buffer when it fits
@@ -288,7 +299,10 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
                                              ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
+  uint8_t* sEp = sB + C::STAGES * C::B_BYTES;  // kEpBytes of epilogue staging
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEp + kEpBytes);
+  constexpr int EPB = ep_buf_bytes<EPI>();
+  constexpr int NEPB = kEpBytes / EPB;  // >= 3: a buffer is rewritten NEPB groups later
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;   // [2] accumulator ready
   uint64_t* tempty = tfull + 2;          // [2] accumulator drained
@@ -300,7 +314,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   const long long u0 = sk_bound(c, g), u1 = sk_bound(c + 1, g);
 
   if (warp == 0 && lane == 0) {
-    if (g.trace) g.trace[c * 8 + 0] = gtimer();
+    if (g.trace) g.trace[c * 16 + 0] = gtimer();
     tma_prefetch(&tmW);
     tma_prefetch(&tmX);
     for (int s = 0; s < C::STAGES; ++s) {
@@ -320,29 +334,45 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   const uint32_t tmem = *tmem_slot;
 
   // segment iterator (identical sequence in every role)
-  auto next_seg = [&](long long& u, Seg& sg) -> bool {
-    if (u >= u1) return false;
-    sg.t = (int)(u / g.KB);
-    sg.kb0 = (int)(u % g.KB);
-    sg.kb1 = (int)min((long long)g.KB, sg.kb0 + (u1 - u));
-    sg.first = u == u0;
-    u += sg.kb1 - sg.kb0;
-    return true;
+  // first this CTA's stream-K units over tiles D.., then its whole tiles
+  // c, c+G, .. < D: a CTA ends on a whole tile, whose epilogue reads no partials
+  struct SegIt {
+    long long u;
+    int dp;
+  };
+  auto next_seg = [&](SegIt& it, Seg& sg) -> bool {
+    if (it.u < u1) {
+      sg.t = g.D + (int)(it.u / g.KB);
+      sg.kb0 = (int)(it.u % g.KB);
+      sg.kb1 = (int)min((long long)g.KB, sg.kb0 + (u1 - it.u));
+      sg.first = it.u == u0;
+      it.u += sg.kb1 - sg.kb0;
+      return true;
+    }
+    if (it.dp < g.D) {
+      sg.t = it.dp;
+      sg.kb0 = 0;
+      sg.kb1 = g.KB;
+      sg.first = 0;
+      it.dp += g.G;
+      return true;
+    }
+    return false;
   };
 
   if (warp == 0) {
     if (lane == 0) {
       const uint64_t pol_w = policy_evict_first();
       const uint64_t pol_x = policy_evict_last();
-      long long u = u0;
+      SegIt it{u0, c};
       Seg sg;
       int i = 0;
       // PDL: the first stages' weight tiles stream before pdl_wait()
       int npre = 0;
       {
-        long long uu = u0;
+        SegIt i0{u0, c};
         Seg s0;
-        if (next_seg(uu, s0)) {
+        if (next_seg(i0, s0)) {
           const int n0 = (s0.t / g.MT) * BM;
           npre = min(s0.kb1 - s0.kb0, C::STAGES);
           for (int j = 0; j < npre; ++j) {
@@ -358,7 +388,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         }
       }
       pdl_wait();
-      while (next_seg(u, sg)) {
+      while (next_seg(it, sg)) {
         const int n0 = (sg.t / g.MT) * BM, m0 = (sg.t % g.MT) * ACC_COLS;
         for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++i) {
           const int s = i % C::STAGES;
@@ -391,10 +421,10 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
-      long long u = u0;
+      SegIt it{u0, c};
       Seg sg;
       int i = 0, j = 0;
-      while (next_seg(u, sg)) {
+      while (next_seg(it, sg)) {
         const int a = j % NACC;
         const uint32_t aph = (j / NACC) & 1;
         mbar_wait(tempty + a, aph ^ 1);
@@ -405,7 +435,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           const uint32_t ph = (i / C::STAGES) & 1;
           mbar_wait(full + s, ph);
           tc_fence_after();
-          if (i == 0 && g.trace) g.trace[c * 8 + 1] = gtimer();
+          if (i == 0 && g.trace) g.trace[c * 16 + 1] = gtimer();
           const uint32_t sa = smem_u32(sA + s * C::A_BYTES);
           const uint32_t sb = smem_u32(sB + s * C::B_BYTES);
 #pragma unroll
@@ -420,37 +450,41 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         mma_commit(tfull + a);
         ++j;
       }
-      if (g.trace) g.trace[c * 8 + 2] = gtimer();
+      if (g.trace) g.trace[c * 16 + 2] = gtimer();
     }
     __syncwarp();
   } else {
     const int q = warp & 3;
     const int row = 32 * q + lane;  // tile row (weight row) of this thread
     pdl_wait();  // residual / partial workspace belong to the predecessor's epoch
-    long long u = u0;
+    SegIt it{u0, c};
     Seg sg;
-    int j = 0;
-    while (next_seg(u, sg)) {
+    int j = 0, eq = 0;
+    while (next_seg(it, sg)) {
       const int a = j % NACC;
       const uint32_t aph = (j / NACC) & 1;
-      mbar_wait(tfull + a, aph);
-      tc_fence_after();
-      if (g.trace && threadIdx.x == 64) g.trace[c * 8 + 3] = gtimer();
-      const uint32_t tbase = tmem + a * ACC_COLS + ((uint32_t)(32 * q) << 16);
       const int n0 = (sg.t / g.MT) * BM, m0 = (sg.t % g.MT) * ACC_COLS;
       const bool split = sg.kb0 != 0 || sg.kb1 != g.KB;
       int owner = c, last = c;
       bool finisher = true;
+      int* flag = s_flag + (j & 1);
       if (split) {
-        owner = sk_owner((long long)sg.t * g.KB, g);
-        last = sk_owner((long long)sg.t * g.KB + g.KB - 1, g);
-        int* flag = s_flag + (j & 1);
+        owner = sk_owner((long long)(sg.t - g.D) * g.KB, g);
+        last = sk_owner((long long)(sg.t - g.D) * g.KB + g.KB - 1, g);
         // every other contributor already published: finish without
-        // publishing (the usual case for the tile a CTA ends on, i.e. the tail)
+        // publishing (the usual case for the tile a CTA ends on, i.e. the
+        // tail).  Checked while this segment's MMAs are still running.
         if (threadIdx.x == 64) *flag = ld_acquire_gpu(g.tickets + sg.t) == last - owner;
         named_bar_sync(1, 128);
         finisher = *flag;
-        if (g.trace && finisher && threadIdx.x == 64) g.trace[c * 8 + 6] += 1;
+        if (finisher) __threadfence();
+      }
+      mbar_wait(tfull + a, aph);
+      tc_fence_after();
+      if (g.trace && threadIdx.x == 64) g.trace[c * 16 + 3] = gtimer();
+      const uint32_t tbase = tmem + a * ACC_COLS + ((uint32_t)(32 * q) << 16);
+      if (split) {
+        if (g.trace && finisher && threadIdx.x == 64) g.trace[c * 16 + 6] += 1;
         if (!finisher) {
           // publish this segment's partial, take a ticket
           float* mine = g.part + ((size_t)c * 2 + (sg.first ? 0 : 1)) * (ACC_COLS * BM);
@@ -477,21 +511,23 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           }
           named_bar_sync(1, 128);
           finisher = *flag;
+          if (finisher) __threadfence();
         }
-        if (finisher) __threadfence();
       }
-      if (g.trace && threadIdx.x == 64) g.trace[c * 8 + 7] = gtimer();
+      if (g.trace && threadIdx.x == 64) g.trace[c * 16 + 7] = gtimer();
       if (finisher) {
         // EG column groups per round: one TMEM wait and one L2 round trip for
         // the contributors' partials per 16*EG columns (the finisher of the
         // last tile is the kernel's tail)
 #pragma unroll 1
         for (int col0 = 0; col0 < ACC_COLS; col0 += 16 * EG) {
+          const int rnd = col0 / (16 * EG);
           uint32_t r[EG][16];
 #pragma unroll
           for (int e = 0; e < EG; ++e)
             if (col0 + 16 * e < ACC_COLS) tmem_ld16(tbase + (uint32_t)(col0 + 16 * e), r[e]);
           tmem_ld_wait();
+          if (g.trace && threadIdx.x == 64 && rnd < 4) g.trace[c * 16 + 8 + 2 * rnd] = gtimer();
           float v[EG][16];
           if (split) {
             // sum contributors in CTA order (own values from TMEM)
@@ -506,7 +542,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 #pragma unroll
                   for (int k = 0; k < 16; ++k) v[e][k] += __uint_as_float(r[e][k]);
               } else {
-                const bool first_of_cc = sk_bound(cc, g) >= (long long)sg.t * g.KB;
+                const bool first_of_cc = sk_bound(cc, g) >= (long long)(sg.t - g.D) * g.KB;
                 const float* pp = g.part + ((size_t)cc * 2 + (first_of_cc ? 0 : 1)) * (ACC_COLS * BM);
                 float w[EG][16];
 #pragma unroll
@@ -531,6 +567,44 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           for (int e = 0; e < EG; ++e) {
             const int col = col0 + 16 * e;
             if (col >= ACC_COLS) break;
+            if constexpr (EPI != PSD_EPI_RESID) {
+              if (g.tma_y) {
+                // stage 16 tokens x the tile's output rows in smem, one TMA
+                // store per group (rows m >= M are clipped by the tensor map)
+                uint8_t* buf = sEp + (eq % NEPB) * EPB;
+                if constexpr (EPI == PSD_EPI_SILU) {
+#pragma unroll
+                  for (int k = 0; k < 16; ++k) {
+                    const float up = __shfl_down_sync(0xffffffffu, v[e][k], 16);
+                    v[e][k] = silu(v[e][k]) * up;
+                  }
+                  if (lane < 16) {
+                    const uint32_t b = smem_u32(buf) + 2 * (16 * q + lane);
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) sts_b16(b + k * 128, __float2bfloat16(v[e][k]));
+                  }
+                } else if constexpr (EPI == PSD_EPI_F32) {
+                  const uint32_t b = smem_u32(buf) + 4 * row;
+#pragma unroll
+                  for (int k = 0; k < 16; ++k) sts_f32(b + k * 4 * BM, v[e][k]);
+                } else {
+                  const uint32_t b = smem_u32(buf) + 2 * row;
+#pragma unroll
+                  for (int k = 0; k < 16; ++k) sts_b16(b + k * 2 * BM, __float2bfloat16(v[e][k]));
+                }
+                fence_proxy_async_smem();
+                named_bar_sync(1, 128);
+                if (threadIdx.x == 64) {
+                  tma_store_2d(&g.tmY, buf, EPI == PSD_EPI_SILU ? (n0 / BM) * 64 : n0, m0 + col);
+                  bulk_commit();
+                  // <= NEPB-2 stores still reading smem: the buffer the
+                  // group after next writes is free
+                  bulk_wait_read<NEPB - 2>();
+                }
+                ++eq;
+                continue;
+              }
+            }
             if constexpr (EPI == PSD_EPI_SILU) {
               const int jo = (n0 / BM) * 64 + 16 * q + (lane & 15);
               __nv_bfloat16* Y = static_cast<__nv_bfloat16*>(g.Y);
@@ -567,6 +641,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
               }
             }
           }
+          if (g.trace && threadIdx.x == 64 && rnd < 4) g.trace[c * 16 + 9 + 2 * rnd] = gtimer();
         }
         if (split && threadIdx.x == 64) g.tickets[sg.t] = 0;  // reusable next launch
       }
@@ -576,9 +651,10 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       if (lane == 0) mbar_arrive(tempty + a);
       ++j;
     }
+    if (threadIdx.x == 64) bulk_wait<0>();  // TMA stores complete before exit
     if (g.trace && threadIdx.x == 64) {
-      g.trace[c * 8 + 4] = gtimer();
-      g.trace[c * 8 + 5] = j;
+      g.trace[c * 16 + 4] = gtimer();
+      g.trace[c * 16 + 5] = j;
     }
   }
   tc_fence_before();
@@ -655,14 +731,47 @@ int make_map(CUtensorMap* map, const void* base, int rows, int K, int ld, int bo
   return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
 }
 
+// Y [M][N_out] for the stream-K finisher's TMA stores: box 16 tokens x box_cols
+int make_out_map(CUtensorMap* map, void* Y, int M, int n_out, int ldy, int elt, int box_cols) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return (int)cudaErrorNotSupported;
+  cuuint64_t dims[2] = {(cuuint64_t)n_out, (cuuint64_t)M};
+  cuuint64_t strides[1] = {(cuuint64_t)ldy * elt};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, 16};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, elt == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                  2, Y, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
+}
+
+// PSD_GEMM_TMA_STORE=0 keeps the per-thread global stores (A/B switch)
+bool tma_store_enabled() {
+  static bool v = [] {
+    const char* e = getenv("PSD_GEMM_TMA_STORE");
+    return !(e && atoi(e) == 0);
+  }();
+  return v;
+}
+
+void set_out_map(SKArgs& g, int epi, void* Y, int M, int N, int ldy) {
+  g.tma_y = 0;
+  if (epi == PSD_EPI_RESID || !tma_store_enabled()) return;
+  const int elt = epi == PSD_EPI_F32 ? 4 : 2;
+  const int n_out = epi == PSD_EPI_SILU ? N / 2 : N;
+  if ((reinterpret_cast<uintptr_t>(Y) & 15) || ((size_t)ldy * elt) % 16) return;
+  if (make_out_map(&g.tmY, Y, M, n_out, ldy, elt, epi == PSD_EPI_SILU ? 64 : BM) == 0)
+    g.tma_y = 1;
+}
+
 template <int BN, int EPI>
 int launch_bn(const CUtensorMap& mw, const CUtensorMap& mx, const GemmArgs& g, dim3 grid,
               cudaStream_t st) {
   using C = Cfg<BN>;
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN, EPI>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e = psd::set_smem_limit((const void*)gemm_kernel<BN, EPI>, C::SMEM, st);
     if (e != cudaSuccess) return (int)e;
     attr_done = true;
   }
@@ -674,15 +783,17 @@ template <int BN, int EPI, bool TILED, int NT = 1, int SMEM_KB = 200>
 int launch_sk_bn_s(const CUtensorMap& mw, const CUtensorMap& mx, const SKArgs& g,
                    cudaStream_t st) {
   using C = Cfg<BN, NT, SMEM_KB>;
+  constexpr int SMEM = C::SMEM + kEpBytes;
+  static_assert(SMEM <= 227 * 1024, "stream-K GEMM shared memory");
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_sk_kernel<BN, EPI, TILED, NT, SMEM_KB>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e =
+        psd::set_smem_limit((const void*)gemm_sk_kernel<BN, EPI, TILED, NT, SMEM_KB>, SMEM, st);
     if (e != cudaSuccess) return (int)e;
     attr_done = true;
   }
   return (int)psd::launch(gemm_sk_kernel<BN, EPI, TILED, NT, SMEM_KB>, dim3(g.G), dim3(kThreads),
-                          C::SMEM, st, mw, mx, g);
+                          SMEM, st, mw, mx, g);
 }
 
 template <int BN, int EPI, bool TILED, int NT = 1>
@@ -710,8 +821,7 @@ int launch_bn_nt(const CUtensorMap& mw, const CUtensorMap& mx, const GemmArgs& g
   using C = Cfg<BN, NT>;
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN, EPI, NT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e = psd::set_smem_limit((const void*)gemm_kernel<BN, EPI, NT>, C::SMEM, st);
     if (e != cudaSuccess) return (int)e;
     attr_done = true;
   }
@@ -846,8 +956,17 @@ int num_sms_raw() {
 }
 
 // stream-K geometry + workspace bytes (partials, then tickets)
+// PSD_GEMM_SK_DP=0: pure stream-K over all tiles (A/B switch)
+bool sk_dp_enabled() {
+  static bool v = [] {
+    const char* e = getenv("PSD_GEMM_SK_DP");
+    return !(e && atoi(e) == 0);
+  }();
+  return v;
+}
+
 struct SKPlan {
-  int bn, nt, KB, MT, tiles, G;
+  int bn, nt, KB, MT, tiles, G, D;
   long long U;
   size_t part_bytes, ticket_bytes;
 };
@@ -862,8 +981,14 @@ SKPlan sk_plan(int M, int N, int K, bool allow_nt2 = true) {
   p.KB = (K + BK - 1) / BK;
   p.MT = tg.mt;
   p.tiles = (N / BM) * p.MT;
-  p.U = (long long)p.tiles * p.KB;
-  p.G = (int)std::min<long long>(num_sms(), p.U);
+  p.G = (int)std::min<long long>(num_sms(), (long long)p.tiles * p.KB);
+  // data-parallel + stream-K: each CTA takes tiles / G whole tiles and an
+  // equal share of the remaining tiles' k-blocks; a remainder that would cut
+  // every tile into more than ~2 pieces gets one more stream-K wave instead
+  p.D = sk_dp_enabled() ? p.G * (p.tiles / p.G) : 0;
+  if (p.D > 0 && p.D < p.tiles && (long long)(p.tiles - p.D) * p.KB < (long long)p.G * (p.KB / 2))
+    p.D -= p.G;
+  p.U = (long long)(p.tiles - p.D) * p.KB;
   p.part_bytes = (size_t)p.G * 2 * p.nt * p.bn * BM * sizeof(float);
   // tickets live at a FIXED offset (start of the workspace) so GEMMs of any
   // shape can share one workspace: each leaves its tickets zeroed
@@ -953,12 +1078,13 @@ int psd_gemm_tiled(const void* X, int ldx, int M, int K, const void* W_tiled, in
   if ((rc = make_map(&mx, X, M, K, ldx, p.bn))) return rc;
   SKArgs g;
   g.M = M; g.N = N; g.K = K;
-  g.KB = p.KB; g.MT = p.MT; g.tiles = p.tiles; g.G = p.G; g.U = p.U;
+  g.KB = p.KB; g.MT = p.MT; g.tiles = p.tiles; g.G = p.G; g.U = p.U; g.D = p.D;
   g.Y = Y; g.ldy = ldy; g.R = static_cast<const __nv_bfloat16*>(R); g.ldr = ldr;
   g.tickets = static_cast<int*>(workspace);
   g.part = reinterpret_cast<float*>(static_cast<char*>(workspace) + p.ticket_bytes);
   g.trace = sk_trace().load(std::memory_order_relaxed);
   g.Wt = static_cast<const __nv_bfloat16*>(W_tiled);
+  set_out_map(g, epi, Y, M, N, ldy);
   cudaStream_t st = (cudaStream_t)stream;
   switch (epi) {
     case PSD_EPI_BF16: return launch_sk<PSD_EPI_BF16, true>(p.bn, mx, mx, g, st);
@@ -1028,12 +1154,13 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
     if ((rc = make_map(&mx, X, M, K, ldx, p.bn))) return rc;
     SKArgs g;
     g.M = M; g.N = N; g.K = K;
-    g.KB = p.KB; g.MT = p.MT; g.tiles = p.tiles; g.G = p.G; g.U = p.U;
+    g.KB = p.KB; g.MT = p.MT; g.tiles = p.tiles; g.G = p.G; g.U = p.U; g.D = p.D;
     g.Y = Y; g.ldy = ldy; g.R = static_cast<const __nv_bfloat16*>(R); g.ldr = ldr;
     g.tickets = static_cast<int*>(workspace);
     g.part = reinterpret_cast<float*>(static_cast<char*>(workspace) + p.ticket_bytes);
     g.trace = sk_trace().load(std::memory_order_relaxed);
     g.Wt = nullptr;
+    set_out_map(g, epi, Y, M, N, ldy);
     cudaStream_t st = (cudaStream_t)stream;
     if (p.nt == 2) {
       switch (epi) {

@@ -1000,10 +1000,12 @@ static int attention_launch(const void* q, const void* k_cache, const void* v_ca
   dim3 grid(num_seqs, Hkv, chunks * S);
   const float sl2 = scale * 1.44269504088896341f;
   const RopeSrc rs = rope ? *rope : RopeSrc{};
+  cudaError_t err = cudaSuccess;
   auto go = [&](auto kern, int kt, int d) {
     const int smem = (ATT_MAXR + 2 * ATT_STAGES * KG * kt) * (d + 8) * 2;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    psd::launch(kern, grid, dim3(ATT_THREADS), smem, (cudaStream_t)stream,
+    if ((err = psd::ensure_smem_limit((const void*)kern, 200 * 1024, (cudaStream_t)stream)))
+      return;
+    err = psd::launch(kern, grid, dim3(ATT_THREADS), smem, (cudaStream_t)stream,
                 static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k_cache),
                 static_cast<const __nv_bfloat16*>(v_cache), block_table, max_blocks, seq_slot,
                 q_start, q_len, q_pos0, kv_len, Hq, Hkv, block_size, sl2, tpc, RG, S, wsf,
@@ -1024,7 +1026,7 @@ static int attention_launch(const void* q, const void* k_cache, const void* v_ca
       break;
     default: return (int)cudaErrorInvalidValue;
   }
-  return (int)cudaGetLastError();
+  return (int)err;
 }
 
 int psd_attention(const void* q, const void* k_cache, const void* v_cache,

@@ -13,7 +13,9 @@ import re
 from .errors import NativeError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpsd.so")
+# PSD_LIB: an alternative build of the same ABI (experiments / bisection)
+LIB_PATH = os.path.abspath(os.environ["PSD_LIB"]) if os.environ.get("PSD_LIB") else \
+    os.path.join(_HERE, "libpsd.so")
 HEADER = os.path.join(_HERE, "..", "include", "psd.h")
 
 _c = ctypes

@@ -88,3 +88,32 @@ def test_gemm_partials_sum(cuda_device, M, N, K):
     torch.cuda.synchronize()
     got = part[:sp.value * M * N].view(sp.value, M, N).sum(0)
     _close(got, _ref(x, w), K)
+
+
+@pytest.mark.parametrize("epi", [native.EPI_BF16, native.EPI_F32, native.EPI_SILU])
+@pytest.mark.parametrize("pad", [8, 1])
+@pytest.mark.parametrize("M", [37, 192])
+def test_gemm_strided_out(cuda_device, epi, pad, M):
+    """Stream-K output into a column slice of a wider buffer: a 16-byte aligned
+    row stride leaves through TMA stores (rows m >= M clipped by the tensor
+    map), an odd stride through per-thread stores; the padding is untouched."""
+    g = torch.Generator(device=cuda_device).manual_seed(M + pad + epi)
+    N, K = 2048, 1024
+    x = torch.randn(M, K, device=cuda_device, generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device=cuda_device, generator=g) * 0.05).to(torch.bfloat16)
+    n_out = N // 2 if epi == native.EPI_SILU else N
+    odt = torch.float32 if epi == native.EPI_F32 else torch.bfloat16
+    big = torch.full((M + 3, n_out + pad), 7.0, dtype=odt, device=cuda_device)
+    out = big[:M, :n_out]
+    ops.gemm(x, w, out=out, epi=epi, splits=0)
+    torch.cuda.synchronize()
+    if epi == native.EPI_SILU:
+        wg = torch.cat([w[t * 128 + q * 32: t * 128 + q * 32 + 16] for t in range(N // 128)
+                        for q in range(4)])
+        wu = torch.cat([w[t * 128 + q * 32 + 16: t * 128 + q * 32 + 32] for t in range(N // 128)
+                        for q in range(4)])
+        ref = torch.nn.functional.silu(_ref(x, wg)) * _ref(x, wu)
+    else:
+        ref = _ref(x, w)
+    _close(out, ref, K)
+    assert (big[:, n_out:] == 7.0).all() and (big[M:] == 7.0).all()

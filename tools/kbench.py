@@ -309,6 +309,13 @@ def main():
         gemm_case("8B gate/up M96", 96, 28672, 4096, "silu")
         gemm_case("8B gate/up M256", 256, 28672, 4096, "silu")
         gemm_case("Qwen7B gate/up M160", 160, 37888, 3584, "silu")
+    if want("gemmskp"):
+        # the split-K shapes through stream-K with an fp32 output (one slice)
+        for (tag, M, N, K) in (("8B qkv", 192, 6144, 4096), ("8B o", 192, 4096, 4096),
+                               ("8B down", 192, 4096, 14336), ("1B qkv", 32, 3072, 2048),
+                               ("1B o", 32, 2048, 2048), ("1B down", 32, 2048, 8192)):
+            gemm_case(f"{tag} part", M, N, K, "partial")
+            gemm_case(f"{tag} sk f32", M, N, K, "f32", splits=0)
     if want("gemmgu"):
         gemm_case("8B gate/up", 192, 28672, 4096, "silu")
     if want("attn1b"):

@@ -8,6 +8,7 @@ Prints percentiles over CTAs of: entry skew, first operands ready after entry,
 last MMA issued, last accumulator ready, epilogue done (all relative to the
 earliest CTA entry), plus segments per CTA and fast (no-publish) finishes.
 """
+import os
 import sys
 
 sys.path.insert(0, ".")
@@ -15,6 +16,8 @@ import torch  # noqa: E402
 
 from paper_2603_18016_b200 import native, ops  # noqa: E402
 
+if os.environ.get("PSD_LIB"):  # a variant build (experiments)
+    native.LIB_PATH = os.path.abspath(os.environ["PSD_LIB"])
 dev = torch.device("cuda:0")
 lib = native.load()
 bf = torch.bfloat16
@@ -35,6 +38,11 @@ def summarize(tag, tr):
             "epi_end": [(r[4] - t0) / 1e3 for r in rows],
             "epi_tail": [(r[4] - r[3]) / 1e3 for r in rows],
             "epi_pre_rounds": [(r[7] - r[3]) / 1e3 for r in rows]}
+    for k in range(4):
+        if all(r[8 + 2 * k] and r[9 + 2 * k] for r in rows):
+            cols[f"round{k}"] = [(r[9 + 2 * k] - r[8 + 2 * k]) / 1e3 for r in rows]
+            cols[f"gap_before_r{k}"] = [(r[8 + 2 * k] - (r[7] if k == 0 else r[7 + 2 * k])) / 1e3
+                                        for r in rows]
     print(f"{tag}: {len(rows)} CTAs, span {max(cols['epi_end']):.2f} us, segments "
           f"{min(r[5] for r in rows)}-{max(r[5] for r in rows)}, fast finishes "
           f"{sum(r[6] for r in rows)}")
@@ -49,7 +57,7 @@ def case(tag, M, N, K, epi, copies=4):
     n_out = N // 2 if epi == native.EPI_SILU else N
     out = torch.empty(M, n_out, dtype=torch.float32 if epi == native.EPI_F32 else bf, device=dev)
     wsp = torch.zeros(64 << 20, dtype=torch.uint8, device=dev)
-    tr = torch.zeros(1024, 8, dtype=torch.int64, device=dev)
+    tr = torch.zeros(1024, 16, dtype=torch.int64, device=dev)
     for i in range(4):
         ops.gemm(x, ws[i % copies], out=out, epi=epi, workspace=wsp)
     torch.cuda.synchronize()
