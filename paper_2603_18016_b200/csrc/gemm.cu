@@ -257,9 +257,17 @@ struct SKArgs {
 // finisher epilogue staging: 24 KB of rotating 16-token buffers (SiLU: 12 of
 // 16 x 64 bf16, bf16: 6 of 16 x 128, fp32: 3 of 16 x 128)
 constexpr int kEpBytes = 24 * 1024;
+#ifndef PSD_F32_TMA_STORE
+#define PSD_F32_TMA_STORE 1
+#endif
 template <int EPI>
 constexpr int ep_buf_bytes() {
   return EPI == PSD_EPI_SILU ? 16 * 64 * 2 : EPI == PSD_EPI_F32 ? 16 * 128 * 4 : 16 * 128 * 2;
+}
+// staging bytes of an epilogue kind (0: per-thread global stores)
+template <int EPI>
+constexpr int ep_stage_bytes() {
+  return EPI == PSD_EPI_RESID || (EPI == PSD_EPI_F32 && !PSD_F32_TMA_STORE) ? 0 : kEpBytes;
 }
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -299,10 +307,11 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
                                              ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint8_t* sEp = sB + C::STAGES * C::B_BYTES;  // kEpBytes of epilogue staging
-  uint64_t* full = reinterpret_cast<uint64_t*>(sEp + kEpBytes);
+  constexpr int EPS = ep_stage_bytes<EPI>();
+  uint8_t* sEp = sB + C::STAGES * C::B_BYTES;  // EPS bytes of epilogue staging
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEp + EPS);
   constexpr int EPB = ep_buf_bytes<EPI>();
-  constexpr int NEPB = kEpBytes / EPB;  // >= 3: a buffer is rewritten NEPB groups later
+  constexpr int NEPB = EPS / EPB;  // >= 3: a buffer is rewritten NEPB groups later
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;   // [2] accumulator ready
   uint64_t* tempty = tfull + 2;          // [2] accumulator drained
@@ -567,7 +576,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           for (int e = 0; e < EG; ++e) {
             const int col = col0 + 16 * e;
             if (col >= ACC_COLS) break;
-            if constexpr (EPI != PSD_EPI_RESID) {
+            if constexpr (EPS > 0) {
               if (g.tma_y) {
                 // stage 16 tokens x the tile's output rows in smem, one TMA
                 // store per group (rows m >= M are clipped by the tensor map)
@@ -758,6 +767,7 @@ bool tma_store_enabled() {
 void set_out_map(SKArgs& g, int epi, void* Y, int M, int N, int ldy) {
   g.tma_y = 0;
   if (epi == PSD_EPI_RESID || !tma_store_enabled()) return;
+  if (epi == PSD_EPI_F32 && !PSD_F32_TMA_STORE) return;
   const int elt = epi == PSD_EPI_F32 ? 4 : 2;
   const int n_out = epi == PSD_EPI_SILU ? N / 2 : N;
   if ((reinterpret_cast<uintptr_t>(Y) & 15) || ((size_t)ldy * elt) % 16) return;
@@ -783,7 +793,7 @@ template <int BN, int EPI, bool TILED, int NT = 1, int SMEM_KB = 200>
 int launch_sk_bn_s(const CUtensorMap& mw, const CUtensorMap& mx, const SKArgs& g,
                    cudaStream_t st) {
   using C = Cfg<BN, NT, SMEM_KB>;
-  constexpr int SMEM = C::SMEM + kEpBytes;
+  constexpr int SMEM = C::SMEM + ep_stage_bytes<EPI>();
   static_assert(SMEM <= 227 * 1024, "stream-K GEMM shared memory");
   static bool attr_done = false;
   if (!attr_done) {
