@@ -47,7 +47,23 @@ struct GemmArgs {
   int ldy;
   const __nv_bfloat16* R;
   int ldr;
+  int tma_y;        // the tile leaves through TMA stores of tmY
+  CUtensorMap tmY;  // Y [M][N_out] (2-D) or the partials [S][M][N] (3-D); box 16 tokens
 };
+
+// epilogue staging for TMA stores: 24 KB of rotating 16-token buffers (SiLU:
+// 12 of 16 x 64 bf16, bf16: 6 of 16 x 128, fp32 / partials: 3 of 16 x 128)
+constexpr int kEpBytes = 24 * 1024;
+template <int EPI>
+constexpr int ep_buf_bytes() {
+  return EPI == PSD_EPI_SILU ? 16 * 64 * 2
+       : (EPI == PSD_EPI_F32 || EPI == PSD_EPI_PARTIAL) ? 16 * 128 * 4 : 16 * 128 * 2;
+}
+// staging bytes of an epilogue kind (0: per-thread global stores)
+template <int EPI>
+constexpr int ep_stage_bytes() {
+  return EPI == PSD_EPI_RESID ? 0 : kEpBytes;
+}
 
 // NT token tiles of BN rows per weight tile (NT = 2 for 256 < M <= 512: every
 // weight byte is streamed once instead of once per token tile)
@@ -124,17 +140,80 @@ __device__ __forceinline__ void tile_epilogue(const GemmArgs& g, uint32_t tmem, 
     }
 }
 
+// the same epilogue through shared memory and TMA stores (warps 2-5, one
+// 16-token group per store; thread 64 issues)
+template <int BN, int EPI>
+__device__ __forceinline__ void tile_epilogue_tma(const GemmArgs& g, uint32_t tmem, int n0,
+                                                  int m0, int z, int q, int lane, int tile_x,
+                                                  uint8_t* sEp) {
+  constexpr int EG = 4;
+  constexpr int EPB = ep_buf_bytes<EPI>();
+  constexpr int NEPB = ep_stage_bytes<EPI>() / EPB;
+  const int row = 32 * q + lane;
+  const uint32_t tbase = tmem + ((uint32_t)(32 * q) << 16);
+  int eq = 0;
+#pragma unroll 1
+  for (int col0 = 0; col0 < BN; col0 += 16 * EG) {
+    uint32_t r[EG][16];
+#pragma unroll
+    for (int e = 0; e < EG; ++e)
+      if (col0 + 16 * e < BN) tmem_ld16(tbase + (uint32_t)(col0 + 16 * e), r[e]);
+    tmem_ld_wait();
+#pragma unroll
+    for (int e = 0; e < EG; ++e) {
+      const int col = col0 + 16 * e;
+      if (col >= BN) break;
+      uint8_t* buf = sEp + (eq % NEPB) * EPB;
+      const uint32_t b0 = smem_u32(buf);
+      if constexpr (EPI == PSD_EPI_SILU) {
+        float v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const float mine = __uint_as_float(r[e][k]);
+          const float up = __shfl_down_sync(0xffffffffu, mine, 16);
+          v[k] = silu(mine) * up;
+        }
+        if (lane < 16) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            sts_b16(b0 + 2 * (16 * q + lane) + k * 128, __float2bfloat16(v[k]));
+        }
+      } else if constexpr (EPI == PSD_EPI_BF16) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          sts_b16(b0 + 2 * row + k * 2 * BM, __float2bfloat16(__uint_as_float(r[e][k])));
+      } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) sts_f32(b0 + 4 * row + k * 4 * BM, __uint_as_float(r[e][k]));
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(1, 128);
+      if (threadIdx.x == 64) {
+        if constexpr (EPI == PSD_EPI_PARTIAL)
+          tma_store_3d(&g.tmY, buf, n0, m0 + col, z);
+        else
+          tma_store_2d(&g.tmY, buf, EPI == PSD_EPI_SILU ? tile_x * 64 : n0, m0 + col);
+        bulk_commit();
+        bulk_wait_read<NEPB - 2>();
+      }
+      ++eq;
+    }
+  }
+  if (threadIdx.x == 64) bulk_wait<0>();
+}
+
 template <int BN, int EPI, int NT = 1>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-            const GemmArgs g) {
+            const __grid_constant__ GemmArgs g) {
   using C = Cfg<BN, NT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
+  uint8_t* sEp = sB + C::STAGES * C::B_BYTES;  // epilogue staging
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEp + ep_stage_bytes<EPI>());
   uint64_t* empty = full + C::STAGES;
   uint64_t* accum = empty + C::STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
@@ -219,7 +298,15 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUt
     tc_fence_after();
     // the NT token tiles are contiguous in tokens and in TMEM columns: one
     // NT * BN wide epilogue
-    tile_epilogue<NT * BN, EPI>(g, tmem, n0, m0, z, q, lane, blockIdx.x);
+    if constexpr (ep_stage_bytes<EPI>() > 0) {
+      if (g.tma_y) {
+        tile_epilogue_tma<NT * BN, EPI>(g, tmem, n0, m0, z, q, lane, blockIdx.x, sEp);
+      } else {
+        tile_epilogue<NT * BN, EPI>(g, tmem, n0, m0, z, q, lane, blockIdx.x);
+      }
+    } else {
+      tile_epilogue<NT * BN, EPI>(g, tmem, n0, m0, z, q, lane, blockIdx.x);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -253,22 +340,6 @@ struct SKArgs {
   int tma_y;                  // finished tiles leave through TMA stores of tmY
   CUtensorMap tmY;            // Y [M][N_out] (bf16 / f32), box 16 tokens x 128 (64 SiLU) rows
 };
-
-// finisher epilogue staging: 24 KB of rotating 16-token buffers (SiLU: 12 of
-// 16 x 64 bf16, bf16: 6 of 16 x 128, fp32: 3 of 16 x 128)
-constexpr int kEpBytes = 24 * 1024;
-#ifndef PSD_F32_TMA_STORE
-#define PSD_F32_TMA_STORE 1
-#endif
-template <int EPI>
-constexpr int ep_buf_bytes() {
-  return EPI == PSD_EPI_SILU ? 16 * 64 * 2 : EPI == PSD_EPI_F32 ? 16 * 128 * 4 : 16 * 128 * 2;
-}
-// staging bytes of an epilogue kind (0: per-thread global stores)
-template <int EPI>
-constexpr int ep_stage_bytes() {
-  return EPI == PSD_EPI_RESID || (EPI == PSD_EPI_F32 && !PSD_F32_TMA_STORE) ? 0 : kEpBytes;
-}
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -764,10 +835,39 @@ bool tma_store_enabled() {
   return v;
 }
 
+// split-K partials [S][M][N] fp32 as a 3-D tensor (rows m >= M of a split clip)
+int make_part_map(CUtensorMap* map, void* P, int M, int N, int S) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return (int)cudaErrorNotSupported;
+  cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)M, (cuuint64_t)S};
+  cuuint64_t strides[2] = {(cuuint64_t)N * 4, (cuuint64_t)M * N * 4};
+  cuuint32_t box[3] = {(cuuint32_t)BM, 16, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, P, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
+}
+
+// grid kernels: partials (kernel epilogue PARTIAL) or the final output
+void set_grid_out_map(GemmArgs& g, int epi, void* Y, int M, int N, int ldy, int splits) {
+  g.tma_y = 0;
+  if (epi == PSD_EPI_RESID || !tma_store_enabled() || (reinterpret_cast<uintptr_t>(Y) & 15))
+    return;
+  if (epi == PSD_EPI_PARTIAL) {
+    if (make_part_map(&g.tmY, Y, M, N, splits) == 0) g.tma_y = 1;
+    return;
+  }
+  const int elt = epi == PSD_EPI_F32 ? 4 : 2;
+  const int n_out = epi == PSD_EPI_SILU ? N / 2 : N;
+  if (((size_t)ldy * elt) % 16) return;
+  if (make_out_map(&g.tmY, Y, M, n_out, ldy, elt, epi == PSD_EPI_SILU ? 64 : BM) == 0)
+    g.tma_y = 1;
+}
+
 void set_out_map(SKArgs& g, int epi, void* Y, int M, int N, int ldy) {
   g.tma_y = 0;
   if (epi == PSD_EPI_RESID || !tma_store_enabled()) return;
-  if (epi == PSD_EPI_F32 && !PSD_F32_TMA_STORE) return;
   const int elt = epi == PSD_EPI_F32 ? 4 : 2;
   const int n_out = epi == PSD_EPI_SILU ? N / 2 : N;
   if ((reinterpret_cast<uintptr_t>(Y) & 15) || ((size_t)ldy * elt) % 16) return;
@@ -781,11 +881,13 @@ int launch_bn(const CUtensorMap& mw, const CUtensorMap& mx, const GemmArgs& g, d
   using C = Cfg<BN>;
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = psd::set_smem_limit((const void*)gemm_kernel<BN, EPI>, C::SMEM, st);
+    cudaError_t e = psd::set_smem_limit((const void*)gemm_kernel<BN, EPI>,
+                                        C::SMEM + ep_stage_bytes<EPI>(), st);
     if (e != cudaSuccess) return (int)e;
     attr_done = true;
   }
-  return (int)psd::launch(gemm_kernel<BN, EPI>, grid, dim3(kThreads), C::SMEM, st, mw, mx, g);
+  return (int)psd::launch(gemm_kernel<BN, EPI>, grid, dim3(kThreads),
+                          C::SMEM + ep_stage_bytes<EPI>(), st, mw, mx, g);
 }
 
 
@@ -831,11 +933,13 @@ int launch_bn_nt(const CUtensorMap& mw, const CUtensorMap& mx, const GemmArgs& g
   using C = Cfg<BN, NT>;
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = psd::set_smem_limit((const void*)gemm_kernel<BN, EPI, NT>, C::SMEM, st);
+    cudaError_t e = psd::set_smem_limit((const void*)gemm_kernel<BN, EPI, NT>,
+                                        C::SMEM + ep_stage_bytes<EPI>(), st);
     if (e != cudaSuccess) return (int)e;
     attr_done = true;
   }
-  return (int)psd::launch(gemm_kernel<BN, EPI, NT>, grid, dim3(kThreads), C::SMEM, st, mw, mx, g);
+  return (int)psd::launch(gemm_kernel<BN, EPI, NT>, grid, dim3(kThreads),
+                          C::SMEM + ep_stage_bytes<EPI>(), st, mw, mx, g);
 }
 
 template <int EPI>
@@ -1129,6 +1233,7 @@ int psd_gemm_partials(const void* X, int ldx, int M, int K, const void* W, int l
   g.kb_per_split = (g.kb_total + splits - 1) / splits;
   splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
   g.Y = P; g.ldy = N; g.R = nullptr; g.ldr = 0;
+  set_grid_out_map(g, PSD_EPI_PARTIAL, P, M, N, N, splits);
   if (splits_used) *splits_used = splits;
   dim3 grid(N / BM, tg.mt, splits);
   if (tg.nt == 2)
@@ -1212,6 +1317,10 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
   splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
   g.Y = splits > 1 ? workspace : Y;
   g.ldy = ldy; g.R = static_cast<const __nv_bfloat16*>(R); g.ldr = ldr;
+  if (splits > 1)
+    set_grid_out_map(g, PSD_EPI_PARTIAL, workspace, M, N, N, splits);
+  else
+    set_grid_out_map(g, epi, Y, M, N, ldy, 1);
   dim3 grid(N / BM, tg.mt, splits);
   cudaStream_t st = (cudaStream_t)stream;
   if (splits > 1) {

@@ -26,6 +26,7 @@ tail is given back after the commit (KVBlockTable.trim_to_written).
 
 from __future__ import annotations
 
+import gc
 import time
 
 import numpy as np
@@ -429,8 +430,19 @@ class GpuBackend:
         cs.wait_stream(cur)
         g = torch.cuda.CUDAGraph()
         c0 = lib.psd_launch_count()
-        with torch.cuda.graph(g, stream=cs, capture_error_mode="thread_local"):
-            launch()
+        # a dead reference cycle holding an old CUDAGraph, collected while
+        # this stream captures, would destroy that graph mid-capture (an
+        # unsafe call that invalidates the capture): collect first, and keep
+        # the cyclic collector off until the capture ends
+        gc.collect()
+        gc_was_enabled = gc.isenabled()
+        gc.disable()
+        try:
+            with torch.cuda.graph(g, stream=cs, capture_error_mode="thread_local"):
+                launch()
+        finally:
+            if gc_was_enabled:
+                gc.enable()
         self.graph_launches[key] = lib.psd_launch_count() - c0
         cur.wait_stream(cs)
         self.graphs[key] = g

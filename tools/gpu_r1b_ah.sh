@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/ah_pytest.log 2>&1
+timeout 900 python bench.py > gpurun_out/ah_bench.log 2>&1
+timeout 300 python tools/kbench.py --only gemmpart > gpurun_out/ah_split_sweep.log 2>&1
+echo done

@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/ai_pytest.log 2>&1
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/ai_pytest2.log 2>&1
+timeout 900 python bench.py > gpurun_out/ai_bench.log 2>&1
+echo done

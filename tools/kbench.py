@@ -11,6 +11,7 @@ import argparse
 import ctypes
 import json
 import math
+import os
 import sys
 
 sys.path.insert(0, ".")
@@ -294,7 +295,7 @@ def main():
         for (tag, M, N, K) in (("1B qkv", 32, 3072, 2048), ("1B o", 32, 2048, 2048),
                                ("1B down", 32, 2048, 8192), ("8B qkv", 192, 6144, 4096),
                                ("8B o", 192, 4096, 4096), ("8B down", 192, 4096, 14336)):
-            for sp in (None, 2, 3, 4, 6, 8, 12, 16):
+            for sp in ((None,) if os.environ.get("KB_AUTO_ONLY") else (None, 2, 3, 4, 6, 8, 12, 16)):
                 gemm_case(f"{tag} part", M, N, K, "partial", splits=sp)
     if want("gemmnt"):
         gemm_case("8B gate/up M384", 384, 28672, 4096, "silu")
