@@ -183,6 +183,9 @@ class GpuBackend:
         # verify GEMM grids capped below the SM count when the draft loop runs
         # beside them (dual stream): PSD_VERIFY_CTAS (0 = all SMs)
         self.verify_ctas = int(os.environ.get("PSD_VERIFY_CTAS", "116")) if dual_stream else 0
+        # and the draft GEMM grids (persistent stream-K grids sized to the SMs
+        # the verify leaves free): PSD_DRAFT_CTAS (0 = all SMs)
+        self.draft_ctas = int(os.environ.get("PSD_DRAFT_CTAS", "0")) if dual_stream else 0
         # PSD_QSTATS_CACHE=0 makes K1 re-read the draft rows (A/B runs)
         self.qstats_cache = os.environ.get("PSD_QSTATS_CACHE", "1") == "1"
         self.seed_draft = (seed * 0x9E3779B1 + 0xD7A7) & 0xFFFFFFFFFFFF
@@ -519,7 +522,15 @@ class GpuBackend:
             for i in range(kmax):
                 kh[2 * B + i * B:2 * B + i * B + nb] = np.where(real & (i < k), sl * K + i, -1)
             self.d_key.copy_(self.d_key_host, non_blocking=True)
-        self._run_graph(("draft", nb, kmax), lambda: self._draft_launch(nb, kmax))
+        self._run_graph(("draft", nb, kmax), lambda: self._draft_launch_capped(nb, kmax))
+
+    def _draft_launch_capped(self, nb: int, kmax: int) -> None:
+        lib = native.load()
+        lib.psd_gemm_set_max_ctas(self.draft_ctas)
+        try:
+            self._draft_launch(nb, kmax)
+        finally:
+            lib.psd_gemm_set_max_ctas(0)
 
     def _draft_launch(self, nb: int, kmax: int) -> None:
         fwd = self.dfwd
