@@ -182,7 +182,7 @@ class GpuBackend:
                 self.mk = self._make_mk(grid)
         # verify GEMM grids capped below the SM count when the draft loop runs
         # beside them (dual stream): PSD_VERIFY_CTAS (0 = all SMs)
-        self.verify_ctas = int(os.environ.get("PSD_VERIFY_CTAS", "116")) if dual_stream else 0
+        self.verify_ctas = int(os.environ.get("PSD_VERIFY_CTAS", "92")) if dual_stream else 0
         # and the draft GEMM grids (persistent stream-K grids sized to the SMs
         # the verify leaves free): PSD_DRAFT_CTAS (0 = all SMs)
         self.draft_ctas = int(os.environ.get("PSD_DRAFT_CTAS", "0")) if dual_stream else 0
@@ -571,7 +571,7 @@ class GpuBackend:
                                                 self.d_out.data_ptr(), None, nb, st),
                          "draft scatter")
 
-    def _verify(self, state, rows: list[VerifyRow]) -> int:
+    def _verify(self, state, rows: list[VerifyRow], beside_draft: bool = False) -> int:
         """Stage and launch the verify pass; returns the number of real rows
         whose accepted lengths land in ``acc_host``."""
         n = len(rows)
@@ -623,7 +623,9 @@ class GpuBackend:
             kh[:nb] = [r.request_id for r in rows] + [0] * (nb - n)
             kh[B:B + nb] = L
             self.v_key.copy_(self.v_key_host, non_blocking=True)
-        self._run_graph(("verify", nb, kmax), lambda: self._verify_launch(nb, kmax))
+        capped = beside_draft and self.verify_ctas > 0
+        self._run_graph(("verify", nb, kmax, capped),
+                        lambda: self._verify_launch(nb, kmax, capped))
         if self.capture_verify is not None:
             torch.cuda.current_stream(self.device).synchronize()
             V = self.tshape.vocab
@@ -639,9 +641,9 @@ class GpuBackend:
             self.capture_verify.append(rec)
         return n
 
-    def _verify_launch(self, nb: int, kmax: int) -> None:
+    def _verify_launch(self, nb: int, kmax: int, capped: bool = False) -> None:
         lib = native.load()
-        lib.psd_gemm_set_max_ctas(self.verify_ctas)
+        lib.psd_gemm_set_max_ctas(self.verify_ctas if capped else 0)
         try:
             self._verify_launch_inner(nb, kmax)
         finally:
@@ -732,7 +734,9 @@ class GpuBackend:
         with torch.cuda.stream(ts):
             e_v0.record(ts)
             if rows:
-                self._verify(state, rows)
+                # capped GEMM grids only while drafts run beside the verify
+                self._verify(state, rows, beside_draft=any(
+                    plan.quotas.get(rid, 0) > 0 for rid in plan.overlap_draft_ids))
             e_v1.record(ts)
         e_v1.synchronize()
         e_ov.synchronize()
