@@ -117,3 +117,24 @@ def test_gemm_strided_out(cuda_device, epi, pad, M):
         ref = _ref(x, w)
     _close(out, ref, K)
     assert (big[:, n_out:] == 7.0).all() and (big[M:] == 7.0).all()
+
+
+@pytest.mark.parametrize("N,epi", [(28672, native.EPI_SILU), (19200, native.EPI_BF16),
+                                   (37888, native.EPI_BF16), (18944, native.EPI_F32)])
+def test_gemm_stream_k_schedules(cuda_device, N, epi):
+    """Stream-K tile schedules on 148 SMs: 224 tiles (148 whole tiles + a
+    stream-K share of 76), 150 (a 2-tile remainder: all tiles stream-K), 296
+    (whole tiles only, no stream-K units), 148 (one wave: the grid kernel)."""
+    g = torch.Generator(device=cuda_device).manual_seed(N + epi)
+    M, K = 192, 512
+    x = torch.randn(M, K, device=cuda_device, generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device=cuda_device, generator=g) * 0.05).to(torch.bfloat16)
+    y = ops.gemm(x, w, epi=epi, splits=0)
+    torch.cuda.synchronize()
+    if epi == native.EPI_SILU:
+        wg = w.view(N // 128, 4, 2, 16, K)[:, :, 0].reshape(N // 2, K)
+        wu = w.view(N // 128, 4, 2, 16, K)[:, :, 1].reshape(N // 2, K)
+        ref = torch.nn.functional.silu(_ref(x, wg)) * _ref(x, wu)
+    else:
+        ref = _ref(x, w)
+    _close(y, ref, K)
