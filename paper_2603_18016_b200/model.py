@@ -387,6 +387,8 @@ class Forward:
         self.sets = sets
         import os
         self.fuse_rope = os.environ.get("PSD_FUSED_ROPE", "1") == "1"
+        # widest per-sequence query count that takes the fused path
+        self.fuse_rope_max_q = int(os.environ.get("PSD_FUSED_ROPE_MAXQ", "2"))
         self.meta = torch.zeros(sets, o, dtype=torch.int32, device=dev)
         # ring of pinned staging buffers: an async H2D copy reads its buffer
         # when it executes, so a buffer is rewritten only after its copy ran
@@ -471,7 +473,7 @@ class Forward:
         # draft decode (<= 2 query tokens per sequence): RoPE fused into the
         # attention kernel (-3 % per draft step); at verify widths (k + 1 tokens)
         # the separate RoPE kernel's parallelism wins (+3 % when fused)
-        fuse_rope = self.fuse_rope and max_q_len <= 2
+        fuse_rope = self.fuse_rope and max_q_len <= self.fuse_rope_max_q
         for li, L in enumerate(m.layers):
             kc = m.kv[li, 0]
             vc = m.kv[li, 1]
