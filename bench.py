@@ -509,6 +509,11 @@ def run_ours(args) -> None:
         "accepted_per_verify": round(r0.total_accepted / max(1, r0.total_bonus), 4),
         "psd_steps_per_pass": steps_psd,
         "draft_hiding": draft_hiding(psd["states"]),
+        # CUDA-event time inside PSD steps vs the timed wall time: the rest is
+        # host scheduling between steps (the GPU idles there)
+        "device_step_ms_per_pass": round(sum(rec.step_duration for st in psd["states"]
+                                             for rec in st.step_log) / max(1, len(psd["states"])),
+                                         2),
         "draft_ms_per_pass": round(psd["draft_ms"] / args.steps, 2),
         "verify_ms_per_pass": round(psd["verify_ms"] / args.steps, 2),
         "e2e": {"value": round(rep_e2e.total_generated / e2e_s, 1), "unit": "tok/s",
