@@ -6,6 +6,7 @@
 // 429) together with gemm.cu.  All of these are HBM / latency bound and run
 // on CUDA cores with 128-bit accesses; none is GEMM-shaped enough to pay for
 // tensor-core staging at the BASELINE shapes (<= 64 query rows per KV head).
+#include <cstdlib>
 #include <algorithm>
 
 #include <cuda_bf16.h>
@@ -659,18 +660,35 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
     __syncthreads();
     if (!s_last) return;
     __threadfence();
+    // every split's R rows of (o, m, l), staged in the (now idle) key ring:
+    // one wave of independent 8-byte L2 loads instead of a dependent L2
+    // chain per output element; same split-order arithmetic either way
+    float* sm = reinterpret_cast<float*>(ring);
+    const bool staged = S * R * RW * 4 <= 2 * NS * KG * KT * P * 2;
+    if (staged) {
+      for (int sp = 0; sp < S; ++sp) {
+        const float2* src = reinterpret_cast<const float2*>(base + (size_t)sp * ATT_MAXR * RW);
+        float2* dst = reinterpret_cast<float2*>(sm + sp * R * RW);
+#pragma unroll 4
+        for (int i = tid; i < R * RW / 2; i += ATT_THREADS) dst[i] = __ldcg(src + i);
+      }
+      __syncthreads();
+    }
+    auto part = [&](int sp, int r) -> const float* {
+      return staged ? sm + (sp * R + r) * RW : base + ((size_t)sp * ATT_MAXR + r) * RW;
+    };
     for (int idx = tid; idx < R * (D / 2); idx += ATT_THREADS) {
       const int r = idx / (D / 2), d = (idx % (D / 2)) * 2;
       float M = -INFINITY;
-      for (int sp = 0; sp < S; ++sp) M = fmaxf(M, __ldcg(base + ((size_t)sp * ATT_MAXR + r) * RW + D));
+      for (int sp = 0; sp < S; ++sp) M = fmaxf(M, staged ? part(sp, r)[D] : __ldcg(part(sp, r) + D));
       float L = 0.f, a0 = 0.f, a1 = 0.f;
       for (int sp = 0; sp < S; ++sp) {
-        const float* pr = base + ((size_t)sp * ATT_MAXR + r) * RW;
-        const float ms = __ldcg(pr + D);
+        const float* pr = part(sp, r);
+        const float ms = staged ? pr[D] : __ldcg(pr + D);
         const float w = ms == -INFINITY ? 0.f : exp2f(ms - M);
-        L += __ldcg(pr + D + 1) * w;
-        a0 += __ldcg(pr + d) * w;
-        a1 += __ldcg(pr + d + 1) * w;
+        L += (staged ? pr[D + 1] : __ldcg(pr + D + 1)) * w;
+        a0 += (staged ? pr[d] : __ldcg(pr + d)) * w;
+        a1 += (staged ? pr[d + 1] : __ldcg(pr + d + 1)) * w;
       }
       const float inv = L > 0.f ? 1.f / L : 0.f;
       const int t = r / G, gg = r % G;
@@ -701,10 +719,20 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
 // key splits for split-KV: a decode/verify CTA's latency is its serial chain
 // of key tiles, so split until every CTA has <= ~128 keys or the grid holds
 // ~4 waves of 148 SMs (>= 32 keys per split)
+// PSD_ATT_MAX_SPLITS caps the split-KV factor (A/B runs)
+int att_max_splits() {
+  static int v = [] {
+    const char* e = getenv("PSD_ATT_MAX_SPLITS");
+    return e ? atoi(e) : 8;
+  }();
+  return v;
+}
+
 int att_splits(int ctas, int max_kv_len) {
   if (max_kv_len <= 0) return 1;
   int S = 1;
-  while (S < 8 && (ctas * S < 4 * 148 || max_kv_len / S > 128) && max_kv_len / (S * 2) >= 32)
+  const int smax = att_max_splits();
+  while (S < smax && (ctas * S < 4 * 148 || max_kv_len / S > 128) && max_kv_len / (S * 2) >= 32)
     S *= 2;
   return S;
 }
