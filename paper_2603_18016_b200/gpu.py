@@ -188,6 +188,8 @@ class GpuBackend:
         self.draft_ctas = int(os.environ.get("PSD_DRAFT_CTAS", "0")) if dual_stream else 0
         # PSD_QSTATS_CACHE=0 makes K1 re-read the draft rows (A/B runs)
         self.qstats_cache = os.environ.get("PSD_QSTATS_CACHE", "1") == "1"
+        # set when a dedicated draft GPU ships the q statistics with the q rows
+        self.qstats_remote = False
         self.seed_draft = (seed * 0x9E3779B1 + 0xD7A7) & 0xFFFFFFFFFFFF
         self.seed_verify = (seed * 0x85EBCA77 + 0x7E51) & 0xFFFFFFFFFFFF
         self.capture_verify = None  # set to a list to record K1 inputs (tests)
@@ -682,9 +684,9 @@ class GpuBackend:
                 self.v_u.data_ptr(), st), "verify uniforms")
             Vd = self.dshape.vocab
             ws = ops._verify_workspace(self.device, nb, kmax, self.tshape.vocab, Vd, True)
-            # the q statistics are cached when this process drew the drafts; a
-            # dedicated draft GPU (pair.py) ships only the q rows
-            cached = "draft" in self.roles and self.qstats_cache
+            # the q statistics are cached when this process drew the drafts, or
+            # shipped with the q rows by a dedicated draft GPU (pair.py)
+            cached = ("draft" in self.roles or self.qstats_remote) and self.qstats_cache
             native.check(lib.psd_verify_sample_ext(
                 logits.data_ptr(), K1 * self.tshape.vocab, self.tshape.vocab,
                 self.tshape.vocab, self.qbuf.data_ptr(), v_slot.data_ptr(), self.k_max * Vd, Vd,

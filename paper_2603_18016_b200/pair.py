@@ -225,13 +225,16 @@ class PairTarget:
 
     def _recv_q(self, rows, drafts) -> None:
         """Sampling mode: the draft distributions of the drafted tokens follow
-        the draft ids (one [sum k, V_draft] fp32 message, rows in draft order)."""
+        the draft ids (one [sum k, V_draft + 4] fp32 message, rows in draft
+        order, each row's canonical (max, sum) in columns V, V + 1)."""
         vq = getattr(self.engine, "q_vocab", 0)
         if not vq:
             return
         n = sum(len(drafts[r[0]]) for r in rows)
         if n:
-            self.engine.inject_q(rows, drafts, self.link.recv_rows(n, vq, self.engine.device))
+            # each row carries its canonical (max, sum) in two extra columns
+            self.engine.inject_q(rows, drafts,
+                                 self.link.recv_rows(n, vq + 4, self.engine.device))
 
     def stop(self) -> None:
         self.link.send(np.asarray([MAGIC, K_STOP], np.int32))
@@ -327,7 +330,9 @@ class GpuTargetEngine:
         return self.be.device
 
     def inject_q(self, rows, drafts, q: torch.Tensor) -> None:
-        """q rows in draft order -> qbuf[slot * k_max + i] (what K1 reads)."""
+        """q rows in draft order -> qbuf[slot * k_max + i] (what K1 reads);
+        their canonical (max, sum), the last two columns -> qstats, so K1
+        takes the cached-statistics path as in a single process."""
         be = self.be
         dst = []
         for rid, slot, _, _ in rows:
@@ -340,8 +345,10 @@ class GpuTargetEngine:
             from . import native
             V = be.dshape.vocab
             native.check(native.load().psd_copy_rows_f32(
-                be.qbuf.data_ptr(), idx_d.data_ptr(), V, q.data_ptr(), V, len(dst), V,
+                be.qbuf.data_ptr(), idx_d.data_ptr(), V, q.data_ptr(), V + 4, len(dst), V,
                 torch.cuda.current_stream(be.device).cuda_stream), "q rows in")
+            be.qstats.index_copy_(0, idx_d.long(), q[:, V:V + 2])
+            be.qstats_remote = True
             q.record_stream(be.s_target)
 
     def verify(self, state, rows):
@@ -414,18 +421,21 @@ class GpuDraftEngine:
 
     def q_rows(self, rows) -> torch.Tensor:
         """Sampling mode: the q rows of the drafted tokens, packed in draft
-        order ([sum k, V_draft] fp32 on the draft GPU)."""
+        order ([sum k, V_draft + 4] fp32 on the draft GPU, statistics after the row)."""
         be = self.be
         src = []
         for _, slot, _, k in rows:
             src += [slot * be.k_max + i for i in range(k)]
         V = be.dshape.vocab
-        out = torch.empty(len(src), V, dtype=torch.float32, device=be.device)
+        # [sum k, V + 4]: the q row, its canonical (max, sum) from the sampler,
+        # two pad columns (rows stay 16-byte aligned for the vector copies)
+        out = torch.zeros(len(src), V + 4, dtype=torch.float32, device=be.device)
         if src:
             from . import native
             idx = torch.from_numpy(np.asarray(src, np.int32)).to(be.device)
             native.check(native.load().psd_gather_rows_f32(
-                out.data_ptr(), V, be.qbuf.data_ptr(), idx.data_ptr(), V, len(src), V,
+                out.data_ptr(), V + 4, be.qbuf.data_ptr(), idx.data_ptr(), V, len(src), V,
                 torch.cuda.current_stream(be.device).cuda_stream), "q rows out")
+            out[:, V:V + 2] = be.qstats.index_select(0, idx.long())
             torch.cuda.current_stream(be.device).synchronize()
         return out
