@@ -1,5 +1,5 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 1200 python bench.py --workload cfg3 --no-cpu-baseline --steps 2 --warmup 2 > gpurun_out/bb_bench_cfg3.log 2>&1
-timeout 1200 python bench.py --layout tp --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/bb_bench_cfg4.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/bb_pytest.log 2>&1
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/bb_smoke.log 2>&1
 echo done
