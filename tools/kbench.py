@@ -160,6 +160,44 @@ def attn_case(tag, nseq, ql, ctx, Hq, Hkv, D):
     report(f"attention {tag}", f"seqs={nseq} q={ql} ctx={ctx} D={D}", us, nbytes)
 
 
+def attn_rope_case(tag, nseq, ql, ctx, Hq, Hkv, D, S):
+    """Decode attention with RoPE + KV write fused (psd_attention_rope), fed by
+    S fp32 split-K partials of the QKV projection, as in the draft loop."""
+    bs = 16
+    nblk_seq = (ctx + ql + bs) // bs + 1
+    nb = nseq * nblk_seq + 1
+    kc = torch.randn(nb * bs, Hkv, D, device=dev).to(bf)
+    vc = torch.randn(nb * bs, Hkv, D, device=dev).to(bf)
+    bt = torch.arange(1, 1 + nseq * nblk_seq, dtype=torch.int32, device=dev).view(nseq, nblk_seq)
+    M = nseq * ql
+    nqkv = (Hq + 2 * Hkv) * D
+    part = torch.randn(S * M * nqkv, device=dev) * 0.1
+    i32 = lambda v: torch.tensor(v, dtype=torch.int32, device=dev)  # noqa: E731
+    positions = i32([ctx + t for _ in range(nseq) for t in range(ql)])
+    slots = i32([int(bt[s_, (ctx + t) // bs]) * bs + (ctx + t) % bs
+                 for s_ in range(nseq) for t in range(ql)])
+    inv_freq = (10000.0 ** (-torch.arange(0, D, 2, device=dev).float() / D)).contiguous()
+    out = torch.empty(M, Hq, D, device=dev).to(bf)
+    seq_slot = i32(list(range(nseq)))
+    q_start = i32([i * ql for i in range(nseq)])
+    q_len = i32([ql] * nseq)
+    q_pos0 = i32([ctx] * nseq)
+    kv_len = i32([ctx + ql] * nseq)
+
+    def fn():
+        st = torch.cuda.current_stream().cuda_stream
+        rc = lib.psd_attention_rope(part.data_ptr(), S, M * nqkv, positions.data_ptr(),
+                                    slots.data_ptr(), inv_freq.data_ptr(), None, kc.data_ptr(),
+                                    vc.data_ptr(), bt.data_ptr(), nblk_seq, seq_slot.data_ptr(),
+                                    q_start.data_ptr(), q_len.data_ptr(), q_pos0.data_ptr(),
+                                    kv_len.data_ptr(), nseq, ql, Hq, Hkv, D, bs,
+                                    1 / math.sqrt(D), out.data_ptr(), st)
+        assert rc == 0
+    us = timeit(fn)
+    report(f"attention+rope {tag}", f"seqs={nseq} q={ql} ctx={ctx} D={D} S={S}", us,
+           nseq * (ctx + ql) * Hkv * D * 2 * 2 + S * M * nqkv * 4)
+
+
 def norm_case(tag, M, H, S):
     x = torch.randn(M, H, device=dev).to(bf)
     P = torch.randn(S * M * H, device=dev)
@@ -319,6 +357,9 @@ def main():
             gemm_case(f"{tag} sk f32", M, N, K, "f32", splits=0)
     if want("gemmgu"):
         gemm_case("8B gate/up", 192, 28672, 4096, "silu")
+    if want("attnrope"):
+        attn_rope_case("1B draft", 32, 1, 300, 32, 8, 64, 6)
+        attn_rope_case("1B draft step0", 32, 2, 300, 32, 8, 64, 6)
     if want("attn1b"):
         attn_case("1B draft", 32, 1, 300, 32, 8, 64)
     if want("attn8b"):
