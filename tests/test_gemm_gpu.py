@@ -138,3 +138,27 @@ def test_gemm_stream_k_schedules(cuda_device, N, epi):
     else:
         ref = _ref(x, w)
     _close(y, ref, K)
+
+
+def test_gemm_trace_timeline(cuda_device):
+    """psd_gemm_set_trace: every stream-K CTA stamps entry <= first operands <=
+    last MMA issued <= epilogue done, and its segment count; off again after."""
+    lib = native.load()
+    M, N, K = 192, 28672, 512
+    x = torch.randn(M, K, device=cuda_device).to(torch.bfloat16)
+    w = (torch.randn(N, K, device=cuda_device) * 0.05).to(torch.bfloat16)
+    tr = torch.zeros(1024, 16, dtype=torch.int64, device=cuda_device)
+    lib.psd_gemm_set_trace(tr.data_ptr())
+    try:
+        ops.gemm(x, w, epi=native.EPI_SILU, splits=0)
+        torch.cuda.synchronize()
+    finally:
+        lib.psd_gemm_set_trace(None)
+    rows = [r for r in tr.cpu().tolist() if r[0]]
+    assert len(rows) == torch.cuda.get_device_properties(cuda_device).multi_processor_count
+    for r in rows:
+        assert r[0] <= r[1] <= r[2] <= r[4] and r[5] >= 1
+    tr.zero_()
+    ops.gemm(x, w, epi=native.EPI_SILU, splits=0)
+    torch.cuda.synchronize()
+    assert int(tr.abs().sum()) == 0
