@@ -182,7 +182,19 @@ class GpuBackend:
                 self.mk = self._make_mk(grid)
         # verify GEMM grids capped below the SM count when the draft loop runs
         # beside them (dual stream): PSD_VERIFY_CTAS (0 = all SMs)
-        self.verify_ctas = int(os.environ.get("PSD_VERIFY_CTAS", "92")) if dual_stream else 0
+        # Default: 92 when a step's drafting streams a comparable weight volume
+        # (k x draft weights >= 1/4 of the target's; cfg2, cfg3), no cap when
+        # the verify dominates (cfg4: 70B target, where capping it only
+        # lengthens the critical path)
+        env_cap = os.environ.get("PSD_VERIFY_CTAS")
+        if not dual_stream or not (has_t and has_d):
+            self.verify_ctas = 0
+        elif env_cap is not None:
+            self.verify_ctas = int(env_cap)
+        else:
+            wb = lambda m: sum(t.numel() for L in m.layers for t in L.values()  # noqa: E731
+                               if isinstance(t, torch.Tensor)) + m.lm_head.numel()
+            self.verify_ctas = 92 if k_max * wb(self.draft) * 4 >= wb(self.target) else 0
         # and the draft GEMM grids (persistent stream-K grids sized to the SMs
         # the verify leaves free): PSD_DRAFT_CTAS (0 = all SMs)
         self.draft_ctas = int(os.environ.get("PSD_DRAFT_CTAS", "0")) if dual_stream else 0
