@@ -182,10 +182,10 @@ class GpuBackend:
                 self.mk = self._make_mk(grid)
         # verify GEMM grids capped below the SM count when the draft loop runs
         # beside them (dual stream): PSD_VERIFY_CTAS (0 = all SMs)
-        # Default: 92 when a step's drafting streams a comparable weight volume
-        # (k x draft weights >= 1/4 of the target's; cfg2, cfg3), no cap when
-        # the verify dominates (cfg4: 70B target, where capping it only
-        # lengthens the critical path)
+        # Default from the drafting / verify weight-volume ratio r = k x draft
+        # weights / target weights (measured optima, profiles/r01b_verify_cta_cap.txt):
+        # r >= 1/2 (cfg2, r = 0.82): 92; 1/4 <= r < 1/2 (cfg3, r = 0.28): 104;
+        # r < 1/4 (cfg4, r = 0.07): no cap -- the verify is the critical path
         env_cap = os.environ.get("PSD_VERIFY_CTAS")
         if not dual_stream or not (has_t and has_d):
             self.verify_ctas = 0
@@ -194,7 +194,8 @@ class GpuBackend:
         else:
             wb = lambda m: sum(t.numel() for L in m.layers for t in L.values()  # noqa: E731
                                if isinstance(t, torch.Tensor)) + m.lm_head.numel()
-            self.verify_ctas = 92 if k_max * wb(self.draft) * 4 >= wb(self.target) else 0
+            r = k_max * wb(self.draft) / max(1, wb(self.target))
+            self.verify_ctas = 92 if r >= 0.5 else 104 if r >= 0.25 else 0
         # and the draft GEMM grids (persistent stream-K grids sized to the SMs
         # the verify leaves free): PSD_DRAFT_CTAS (0 = all SMs)
         self.draft_ctas = int(os.environ.get("PSD_DRAFT_CTAS", "0")) if dual_stream else 0
