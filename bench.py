@@ -460,6 +460,17 @@ def run_ours(args) -> None:
         pd.finalize()
         return
     psd, sd, sdm = results["psd"], results["standard-sd"], results["sd-m"]
+
+    def outputs(res):
+        return [r.output_ids for st_ in res["states"] for r in st_.request_list()]
+    # greedy output is schedule independent: PSD, SD(2m) and SD(m) must emit
+    # the same tokens for every request of every timed pass (north star:
+    # identical greedy sequences); sampling compares the same way (uniforms
+    # are keyed by request and position, not by schedule)
+    po = outputs(psd)
+    ident = {"psd_vs_sd": po == outputs(sd), "psd_vs_sd_m": po == outputs(sdm),
+             "requests": len(po), "tokens": sum(len(x) for x in po),
+             "mismatched_requests": sum(a != b for a, b in zip(po, outputs(sd)))}
     value = psd["tokens"] / (psd["ms"] * 1e-3)  # tokens summed over ranks / max time
     sd_value = sd["tokens"] / (sd["ms"] * 1e-3)
     r0 = psd["reps"][0]
@@ -505,6 +516,7 @@ def run_ours(args) -> None:
                       if "psd-ktune" in results and results["psd-ktune"] else None),
         "psd_vs_sd": round(value / sd_value, 4),
         "psd_vs_sd_m": round(value / (sdm["tokens"] / (sdm["ms"] * 1e-3)), 4),
+        "greedy_identical": ident,
         "mean_accepted_len": round(mean_accepted_length(r0), 4),
         "accepted_per_verify": round(r0.total_accepted / max(1, r0.total_bonus), 4),
         "psd_steps_per_pass": steps_psd,

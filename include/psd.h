@@ -82,6 +82,29 @@ int psd_verify_sample_ext(const float* target_logits, int64_t t_stride_b, int64_
                           int32_t* accepted_len, int32_t* out_tokens, const void* d_stats,
                           int64_t d_stats_ld, void* t_stats_out, const int32_t* t_stats_rows,
                           void* ws, size_t ws_bytes, void* stream);
+/* Replay mode (GpuBackend(acceptance="replay")): as psd_verify_greedy /
+ * psd_verify_sample_ext, but request b accepts exactly min(forced_len[b], k_b)
+ * drafts whatever the logits say, then emits the target's token at that row
+ * (greedy: its argmax; sampling: the residual sample, or the bonus from p when
+ * every draft is kept).  Replaces the accepted count of a verified row with
+ * the reference's own draw, accepted_count(model, k, draft_time,
+ * acceptance_stream(seed, rid, j)) (pkg/src/specsim/acceptance_model.py:82-97,
+ * engine.py:250-256), so a GPU run's step log equals specsim's byte for byte
+ * while every pass runs on real logits. */
+int psd_verify_greedy_forced(const float* target_logits, int64_t t_stride_b, int64_t t_stride_i,
+                             int V, const int32_t* draft_ids, const int32_t* draft_len, int B,
+                             int K, const int32_t* forced_len, int32_t* accepted_len,
+                             int32_t* out_tokens, void* workspace, size_t workspace_bytes,
+                             void* stream);
+int psd_verify_sample_forced(const float* target_logits, int64_t t_stride_b, int64_t t_stride_i,
+                             int V, const float* draft_logits, const int32_t* draft_rows,
+                             int64_t d_stride_row, int64_t d_stride_i, int Vd,
+                             const int32_t* draft_ids, const int32_t* draft_len,
+                             const float* uniforms, float temperature, int B, int K,
+                             const int32_t* forced_len, int32_t* accepted_len,
+                             int32_t* out_tokens, const void* d_stats, int64_t d_stats_ld,
+                             void* t_stats_out, const int32_t* t_stats_rows, void* ws,
+                             size_t ws_bytes, void* stream);
 
 /* ---- K2: bf16 GEMM on tcgen05 (TMEM accumulators, TMA, mbarrier ring) -----
  *   Y[m, n] = epi( sum_k X[m*ldx + k] * W[n*ldw + k] )   X [M,K], W [N,K] bf16

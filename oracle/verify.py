@@ -44,6 +44,12 @@ def lib():
                                            _f32p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
                                            _i32p, _i32p, _f32p, ctypes.c_float, ctypes.c_int,
                                            ctypes.c_int, _i32p, _i32p]
+        L.oracle_verify_greedy_forced.restype = ctypes.c_int
+        L.oracle_verify_greedy_forced.argtypes = (L.oracle_verify_greedy.argtypes[:8] + [_i32p]
+                                                  + L.oracle_verify_greedy.argtypes[8:])
+        L.oracle_verify_sample_forced.restype = ctypes.c_int
+        L.oracle_verify_sample_forced.argtypes = (L.oracle_verify_sample.argtypes[:14] + [_i32p]
+                                                  + L.oracle_verify_sample.argtypes[14:])
         _lib = L
     return _lib
 
@@ -69,8 +75,10 @@ def row_stats(row: np.ndarray, temperature: float = 1.0) -> tuple[float, float]:
     return M.value, S.value
 
 
-def verify_greedy(target: np.ndarray, draft_ids: np.ndarray, draft_len: np.ndarray):
-    """target [B, K+1, V] f32, draft_ids [B, K] i32, draft_len [B] i32."""
+def verify_greedy(target: np.ndarray, draft_ids: np.ndarray, draft_len: np.ndarray,
+                  forced_len: np.ndarray | None = None):
+    """target [B, K+1, V] f32, draft_ids [B, K] i32, draft_len [B] i32;
+    forced_len [B] i32: replay mode (accept exactly min(forced, k_b))."""
     t = np.ascontiguousarray(target, dtype=np.float32)
     B, K1, V = t.shape
     K = K1 - 1
@@ -78,15 +86,21 @@ def verify_greedy(target: np.ndarray, draft_ids: np.ndarray, draft_len: np.ndarr
     ln = np.ascontiguousarray(draft_len, dtype=np.int32)
     acc = np.zeros(B, np.int32)
     out = np.zeros((B, K + 1), np.int32)
-    rc = lib().oracle_verify_greedy(_fp(t), K1 * V, V, V, _ip(ids), _ip(ln), B, K,
-                                    _ip(acc), _ip(out))
+    if forced_len is not None:
+        fl = np.ascontiguousarray(forced_len, dtype=np.int32)
+        rc = lib().oracle_verify_greedy_forced(_fp(t), K1 * V, V, V, _ip(ids), _ip(ln), B, K,
+                                               _ip(fl), _ip(acc), _ip(out))
+    else:
+        rc = lib().oracle_verify_greedy(_fp(t), K1 * V, V, V, _ip(ids), _ip(ln), B, K,
+                                        _ip(acc), _ip(out))
     if rc:
         raise ValueError("oracle_verify_greedy: bad arguments")
     return acc, out
 
 
 def verify_sample(target: np.ndarray, draft: np.ndarray, draft_ids: np.ndarray,
-                  draft_len: np.ndarray, uniforms: np.ndarray, temperature: float = 1.0):
+                  draft_len: np.ndarray, uniforms: np.ndarray, temperature: float = 1.0,
+                  forced_len: np.ndarray | None = None):
     """target [B, K+1, V], draft [B, K, Vd] f32; uniforms [B, K+1] f32."""
     t = np.ascontiguousarray(target, dtype=np.float32)
     d = np.ascontiguousarray(draft, dtype=np.float32)
@@ -100,9 +114,13 @@ def verify_sample(target: np.ndarray, draft: np.ndarray, draft_ids: np.ndarray,
     u = np.ascontiguousarray(uniforms, dtype=np.float32).reshape(B, K + 1)
     acc = np.zeros(B, np.int32)
     out = np.zeros((B, K + 1), np.int32)
-    rc = lib().oracle_verify_sample(_fp(t), K1 * V, V, V, _fp(d), max(K, 1) * Vd, Vd, Vd,
-                                    _ip(ids), _ip(ln), _fp(u), ctypes.c_float(temperature),
-                                    B, K, _ip(acc), _ip(out))
+    args = (_fp(t), K1 * V, V, V, _fp(d), max(K, 1) * Vd, Vd, Vd, _ip(ids), _ip(ln), _fp(u),
+            ctypes.c_float(temperature), B, K)
+    if forced_len is not None:
+        fl = np.ascontiguousarray(forced_len, dtype=np.int32)
+        rc = lib().oracle_verify_sample_forced(*args, _ip(fl), _ip(acc), _ip(out))
+    else:
+        rc = lib().oracle_verify_sample(*args, _ip(acc), _ip(out))
     if rc:
         raise ValueError("oracle_verify_sample: bad arguments")
     return acc, out

@@ -175,18 +175,28 @@ static int32_t prefix_sample(const weight_src* w, float u) {
  * draft logits row (b, i) at d + b*dsb + i*dsi, i in 0..K-1;
  * draft_ids[b*K + i]; uniforms[b*(K+1) + i] (i < K acceptance, i == K sample);
  * out_tokens[b*(K+1) + i], -1 past the emitted tokens. */
-int oracle_verify_greedy(const float* t, int64_t tsb, int64_t tsi, int V,
-                         const int32_t* draft_ids, const int32_t* draft_len, int B, int K,
-                         int32_t* accepted_len, int32_t* out_tokens) {
+/* forced_len (NULL: the real test): replay mode -- accept exactly
+ * min(forced_len[b], k_b) drafts whatever the logits say, then emit the
+ * target's token at that row (bonus / residual sample), as the GPU's
+ * psd_verify_*_forced do for GpuBackend(acceptance="replay"). */
+static int verify_greedy_impl(const float* t, int64_t tsb, int64_t tsi, int V,
+                              const int32_t* draft_ids, const int32_t* draft_len, int B, int K,
+                              const int32_t* forced_len, int32_t* accepted_len,
+                              int32_t* out_tokens) {
   for (int b = 0; b < B; ++b) {
     const int kb = draft_len[b];
     if (kb < 0 || kb > K) return 1;
     int a = 0;
     int32_t g = 0;
-    for (int i = 0; i <= kb; ++i) {
-      g = oracle_row_argmax(t + b * tsb + i * tsi, V);
-      if (i == kb || draft_ids[b * K + i] != g) break;
-      ++a;
+    if (forced_len) {
+      a = forced_len[b] < 0 ? 0 : (forced_len[b] > kb ? kb : forced_len[b]);
+      g = oracle_row_argmax(t + b * tsb + a * tsi, V);
+    } else {
+      for (int i = 0; i <= kb; ++i) {
+        g = oracle_row_argmax(t + b * tsb + i * tsi, V);
+        if (i == kb || draft_ids[b * K + i] != g) break;
+        ++a;
+      }
     }
     accepted_len[b] = a;
     for (int i = 0; i <= K; ++i) out_tokens[b * (K + 1) + i] = -1;
@@ -196,10 +206,26 @@ int oracle_verify_greedy(const float* t, int64_t tsb, int64_t tsi, int V,
   return 0;
 }
 
-int oracle_verify_sample(const float* t, int64_t tsb, int64_t tsi, int V, const float* d,
-                         int64_t dsb, int64_t dsi, int Vd, const int32_t* draft_ids,
-                         const int32_t* draft_len, const float* uniforms, float temperature,
-                         int B, int K, int32_t* accepted_len, int32_t* out_tokens) {
+int oracle_verify_greedy(const float* t, int64_t tsb, int64_t tsi, int V,
+                         const int32_t* draft_ids, const int32_t* draft_len, int B, int K,
+                         int32_t* accepted_len, int32_t* out_tokens) {
+  return verify_greedy_impl(t, tsb, tsi, V, draft_ids, draft_len, B, K, NULL, accepted_len,
+                            out_tokens);
+}
+
+int oracle_verify_greedy_forced(const float* t, int64_t tsb, int64_t tsi, int V,
+                                const int32_t* draft_ids, const int32_t* draft_len, int B, int K,
+                                const int32_t* forced_len, int32_t* accepted_len,
+                                int32_t* out_tokens) {
+  return verify_greedy_impl(t, tsb, tsi, V, draft_ids, draft_len, B, K, forced_len, accepted_len,
+                            out_tokens);
+}
+
+static int verify_sample_impl(const float* t, int64_t tsb, int64_t tsi, int V, const float* d,
+                              int64_t dsb, int64_t dsi, int Vd, const int32_t* draft_ids,
+                              const int32_t* draft_len, const float* uniforms, float temperature,
+                              int B, int K, const int32_t* forced_len, int32_t* accepted_len,
+                              int32_t* out_tokens) {
   const float inv_temp = 1.0f / temperature;
   const float c = psd_scale(inv_temp);
   for (int b = 0; b < B; ++b) {
@@ -207,16 +233,24 @@ int oracle_verify_sample(const float* t, int64_t tsb, int64_t tsi, int V, const 
     if (kb < 0 || kb > K) return 1;
     int a = 0;
     float Mt = 0, St = 0, Md = 0, Sd = 0;
-    for (; a < kb; ++a) {
-      const float* tr = t + b * tsb + a * tsi;
-      const float* dr = d + b * dsb + a * dsi;
-      oracle_row_stats(tr, V, inv_temp, &Mt, &St);
-      oracle_row_stats(dr, Vd, inv_temp, &Md, &Sd);
-      const int32_t x = draft_ids[b * K + a];
-      if (x < 0 || x >= V) break;
-      const float et = psd_weight(tr[x], c, psd_bias(Mt, c));
-      const float ed = x < Vd ? psd_weight(dr[x], c, psd_bias(Md, c)) : 0.0f;
-      if (!psd_accept(uniforms[b * (K + 1) + a], et, ed, St, Sd)) break;
+    if (forced_len) {
+      a = forced_len[b] < 0 ? 0 : (forced_len[b] > kb ? kb : forced_len[b]);
+      if (a < kb) {
+        oracle_row_stats(t + b * tsb + a * tsi, V, inv_temp, &Mt, &St);
+        oracle_row_stats(d + b * dsb + a * dsi, Vd, inv_temp, &Md, &Sd);
+      }
+    } else {
+      for (; a < kb; ++a) {
+        const float* tr = t + b * tsb + a * tsi;
+        const float* dr = d + b * dsb + a * dsi;
+        oracle_row_stats(tr, V, inv_temp, &Mt, &St);
+        oracle_row_stats(dr, Vd, inv_temp, &Md, &Sd);
+        const int32_t x = draft_ids[b * K + a];
+        if (x < 0 || x >= V) break;
+        const float et = psd_weight(tr[x], c, psd_bias(Mt, c));
+        const float ed = x < Vd ? psd_weight(dr[x], c, psd_bias(Md, c)) : 0.0f;
+        if (!psd_accept(uniforms[b * (K + 1) + a], et, ed, St, Sd)) break;
+      }
     }
     weight_src w;
     w.V = V;
@@ -245,4 +279,21 @@ int oracle_verify_sample(const float* t, int64_t tsb, int64_t tsi, int V, const 
     out_tokens[b * (K + 1) + a] = tok;
   }
   return 0;
+}
+
+int oracle_verify_sample(const float* t, int64_t tsb, int64_t tsi, int V, const float* d,
+                         int64_t dsb, int64_t dsi, int Vd, const int32_t* draft_ids,
+                         const int32_t* draft_len, const float* uniforms, float temperature,
+                         int B, int K, int32_t* accepted_len, int32_t* out_tokens) {
+  return verify_sample_impl(t, tsb, tsi, V, d, dsb, dsi, Vd, draft_ids, draft_len, uniforms,
+                            temperature, B, K, NULL, accepted_len, out_tokens);
+}
+
+int oracle_verify_sample_forced(const float* t, int64_t tsb, int64_t tsi, int V, const float* d,
+                                int64_t dsb, int64_t dsi, int Vd, const int32_t* draft_ids,
+                                const int32_t* draft_len, const float* uniforms,
+                                float temperature, int B, int K, const int32_t* forced_len,
+                                int32_t* accepted_len, int32_t* out_tokens) {
+  return verify_sample_impl(t, tsb, tsi, V, d, dsb, dsi, Vd, draft_ids, draft_len, uniforms,
+                            temperature, B, K, forced_len, accepted_len, out_tokens);
 }

@@ -143,7 +143,11 @@ def _backend(cfg: dict, sim: SimConfig, requests):
     longest = max(r.prompt_len + r.target_output_len for r in requests)
     msl = cfg["gpu.max_seq_len"].strip()
     k_max = max((sim.k,) + sim.k_overrides)
-    return GpuBackend(cfg["gpu.target"], cfg["gpu.draft"], max_requests=len(requests),
+    # slots for the requests that can run at once (two PSD batches of m, or one
+    # SD batch of m * sd_batch_factor), not for the whole workload
+    width = sim.m * max(1, sim.sd_batch_factor)
+    concurrent = min(len(requests), max(2 * sim.m, width))
+    return GpuBackend(cfg["gpu.target"], cfg["gpu.draft"], max_requests=concurrent,
                       max_batch=sim.m * max(1, sim.sd_batch_factor), k_max=k_max,
                       max_seq_len=int(msl) if msl else longest + k_max + 16,
                       mode=cfg["gpu.sampling"], temperature=_num(cfg, "gpu.temperature", float),

@@ -59,6 +59,11 @@ struct Params {
   // output: (M, S) of target row 0 of request b to t_stats_out[t_stats_rows[b]]
   // (skipped for a negative row) -- how the draft sampler publishes them
   float2* t_stats_out; const int32_t* t_stats_rows;
+  // replay mode (null: the real test): accept exactly min(forced[b], k_b)
+  // drafts, then emit the target's token at that row -- GpuBackend's
+  // acceptance="replay" commits the reference's coin-flip counts
+  // (acceptance_model.py:82-97) on real logits
+  const int32_t* forced;
 };
 
 __device__ __forceinline__ float4 ld_stream(const float* p) {
@@ -327,7 +332,8 @@ __device__ __forceinline__ void stats_item(const Params& p, int slice, int b, in
       }
     }
     const unsigned rej = __ballot_sync(0xffffffffu, !ok) & ((1u << kb) - 1u);
-    const int a = rej ? __ffs(rej) - 1 : kb;
+    int a = rej ? __ffs(rej) - 1 : kb;
+    if (p.forced) a = min(max(__ldg(p.forced + b), 0), kb);
     int32_t* o = p.out + b * (p.K + 1);
     if (lane <= p.K) o[lane] = lane < a ? x : (!SAMPLE && lane == a ? sG[a] : -1);
     if (lane == 0) {
@@ -686,6 +692,14 @@ int psd_verify_greedy(const float* target_logits, int64_t t_stride_b, int64_t t_
                       const int32_t* draft_ids, const int32_t* draft_len, int B, int K,
                       int32_t* accepted_len, int32_t* out_tokens, void* ws, size_t ws_bytes,
                       void* stream) {
+  return psd_verify_greedy_forced(target_logits, t_stride_b, t_stride_i, V, draft_ids, draft_len,
+                                  B, K, nullptr, accepted_len, out_tokens, ws, ws_bytes, stream);
+}
+
+int psd_verify_greedy_forced(const float* target_logits, int64_t t_stride_b, int64_t t_stride_i,
+                             int V, const int32_t* draft_ids, const int32_t* draft_len, int B,
+                             int K, const int32_t* forced_len, int32_t* accepted_len,
+                             int32_t* out_tokens, void* ws, size_t ws_bytes, void* stream) {
   const WsLayout L = layout(B, K, V, 0, 0);
   int rc = check_common(target_logits, t_stride_b, t_stride_i, V, B, K, ws, ws_bytes, L.total);
   if (rc) return rc;
@@ -694,6 +708,7 @@ int psd_verify_greedy(const float* target_logits, int64_t t_stride_b, int64_t t_
   p.t = target_logits; p.tsb = t_stride_b; p.tsi = t_stride_i; p.V = V;
   p.d = nullptr; p.Vd = 0; p.ids = draft_ids; p.len = draft_len; p.u = nullptr;
   p.c = psd_scale(1.0f); p.B = B; p.K = K; p.acc = accepted_len; p.out = out_tokens;
+  p.forced = forced_len;
   p.cnt_a = reinterpret_cast<int*>(w + L.cnt_a); p.cnt_b = reinterpret_cast<int*>(w + L.cnt_b);
   p.part = reinterpret_cast<float2*>(w + L.part); p.plan = reinterpret_cast<Plan*>(w + L.plan);
   p.wblk = reinterpret_cast<float*>(w + L.wblk);
@@ -748,6 +763,22 @@ int psd_verify_sample_ext(const float* target_logits, int64_t t_stride_b, int64_
                           int32_t* accepted_len, int32_t* out_tokens, const void* d_stats,
                           int64_t d_stats_ld, void* t_stats_out, const int32_t* t_stats_rows,
                           void* ws, size_t ws_bytes, void* stream) {
+  return psd_verify_sample_forced(target_logits, t_stride_b, t_stride_i, V, draft_logits,
+                                  draft_rows, d_stride_row, d_stride_i, Vd, draft_ids, draft_len,
+                                  uniforms, temperature, B, K, nullptr, accepted_len, out_tokens,
+                                  d_stats, d_stats_ld, t_stats_out, t_stats_rows, ws, ws_bytes,
+                                  stream);
+}
+
+int psd_verify_sample_forced(const float* target_logits, int64_t t_stride_b, int64_t t_stride_i,
+                             int V, const float* draft_logits, const int32_t* draft_rows,
+                             int64_t d_stride_row, int64_t d_stride_i, int Vd,
+                             const int32_t* draft_ids, const int32_t* draft_len,
+                             const float* uniforms, float temperature, int B, int K,
+                             const int32_t* forced_len, int32_t* accepted_len,
+                             int32_t* out_tokens, const void* d_stats, int64_t d_stats_ld,
+                             void* t_stats_out, const int32_t* t_stats_rows, void* ws,
+                             size_t ws_bytes, void* stream) {
   if (t_stats_out && !t_stats_rows) return (int)cudaErrorInvalidValue;
   const WsLayout L = layout(B, K, V, Vd, 1);
   int rc = check_common(target_logits, t_stride_b, t_stride_i, V, B, K, ws, ws_bytes, L.total);
@@ -766,6 +797,7 @@ int psd_verify_sample_ext(const float* target_logits, int64_t t_stride_b, int64_
   p.d_stats_ld = d_stats_ld;
   p.t_stats_out = static_cast<float2*>(t_stats_out);
   p.t_stats_rows = t_stats_rows;
+  p.forced = forced_len;
   p.ids = draft_ids; p.len = draft_len; p.u = uniforms;
   p.c = psd_scale(1.0f / temperature); p.B = B; p.K = K; p.acc = accepted_len; p.out = out_tokens;
   p.cnt_a = reinterpret_cast<int*>(w + L.cnt_a); p.cnt_b = reinterpret_cast<int*>(w + L.cnt_b);

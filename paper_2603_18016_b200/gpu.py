@@ -10,8 +10,9 @@ Replaces the reference's two abstractions:
     over the real logits.
 
 Batch parallelism: the skip batch's draft loop runs on the *draft stream*
-while the target batch is verified on the *target stream* (one GPU; or the
-draft model on its own device, see ``draft_device``).  The only host sync per
+while the target batch is verified on the *target stream* (one GPU; a
+dedicated draft GPU is the pair layout of pair.py, which runs one GpuBackend
+per role on two ranks).  The only host sync per
 step is the D2H of the verified rows' accepted lengths.
 
 Per-request device state lives in "slots" (one per running request):
@@ -61,12 +62,27 @@ class GpuBackend:
                  block_size: int = 16, num_blocks: int | None = None,
                  prefill_chunk_tokens: int = 4096, use_graphs: bool = True,
                  roles: tuple = ("target", "draft"), fused_draft: bool | None = None,
-                 mk_grid: int = 0, tp=None) -> None:
+                 mk_grid: int = 0, tp=None, acceptance: str = "kernel") -> None:
         if not torch.cuda.is_available():
             raise native.NativeError("GpuBackend needs a CUDA device (no CPU fallback)")
         native.load()
         if mode not in ("greedy", "sample"):
             raise ConfigError(f"mode must be greedy or sample, got {mode!r}")
+        if acceptance not in ("kernel", "replay"):
+            raise ConfigError(f"acceptance must be kernel or replay, got {acceptance!r}")
+        # replay: real draft / verify passes on real logits, but every verified
+        # row accepts the reference's own coin-flip count accepted_count(model,
+        # k, draft_time, acceptance_stream(seed, rid, j)) (acceptance_model.py:
+        # 50-52, 82-97; engine.py:250-256) through K1's forced mode, KV grants
+        # are sized exactly like the reference's (engine.py:162-175) and the
+        # scheduler sees the latency models' virtual durations -- so the step
+        # log, KV log and metrics equal specsim's byte for byte while the
+        # measured CUDA-event durations go to ``measured_log``
+        self.replay = acceptance == "replay"
+        self.measured_log: list = []
+        if self.replay:
+            from .sim import SimBackend
+            self._sim = SimBackend()
         if k_max > 16:
             raise ConfigError("k_max must be <= 16 (PSD_MAX_K)")
         self.tshape, self.dshape = _shape(target), _shape(draft)
@@ -142,7 +158,15 @@ class GpuBackend:
                 self.d_u = torch.empty(K, B, dtype=torch.float32, device=dev)
                 self.v_u = torch.empty(B, K + 1, dtype=torch.float32, device=dev)
                 # per-row (request id, committed length) keys of the uniforms
-                self.d_key_host = torch.zeros(2 * B + K * B, dtype=i32).pin_memory()
+                # a ring of pinned staging rows: an async H2D copy reads its row
+                # when it executes, so a row is rewritten only after the event
+                # recorded behind its copy has completed (two draft loops may be
+                # enqueued back to back without a host sync, e.g. startup steps)
+                self.d_key_ring = 4
+                self.d_key_host = torch.zeros(self.d_key_ring, 2 * B + K * B,
+                                              dtype=i32).pin_memory()
+                self.d_key_events = [None] * self.d_key_ring
+                self.d_key_cur = 0
                 self.d_key = torch.zeros(2 * B + K * B, dtype=i32, device=dev)
                 self.v_key_host = torch.zeros(2 * B, dtype=i32).pin_memory()
                 self.v_key = torch.zeros(2 * B, dtype=i32, device=dev)
@@ -152,6 +176,8 @@ class GpuBackend:
             self.v_out = torch.empty(B * (K + 1), dtype=i32, device=dev)
             self.v_len = torch.empty(B, dtype=i32, device=dev)
             self.v_slot = torch.empty(B, dtype=i32, device=dev)
+            # v_meta: [0, B) draft depths, [B, 2B) slots, [2B, 3B) replay counts,
+            # [3B, 3B + BK) slot_tok indices of the drafts
             self.v_meta_host = torch.zeros(3 * B + B * K, dtype=i32).pin_memory()
             self.v_meta = torch.zeros(3 * B + B * K, dtype=i32, device=dev)
             self.acc_host = torch.zeros(B, dtype=i32).pin_memory()
@@ -267,6 +293,15 @@ class GpuBackend:
                               f"block size {self.block_size}")
         if state.config.k > self.k_max or any(k > self.k_max for k in state.config.k_overrides):
             raise ConfigError(f"draft depth exceeds k_max={self.k_max}")
+        cfg = state.config
+        width = cfg.m * (max(1, cfg.sd_batch_factor) if cfg.mode == "standard-sd" else 1)
+        if width > self.max_batch:
+            raise ConfigError(f"batch width {width} (m={cfg.m}, mode {cfg.mode}) exceeds "
+                              f"max_batch={self.max_batch}")
+        running = cfg.m * (max(1, cfg.sd_batch_factor) if cfg.mode == "standard-sd" else 2)
+        if min(running, len(state.requests)) > self.max_requests:
+            raise ConfigError(f"up to {min(running, len(state.requests))} concurrent requests "
+                              f"need slots, max_requests={self.max_requests}")
         need = [r for r in state.requests.values() if r.prompt_ids is None]
         if need:
             attach_prompt_ids(need, self.dshape.vocab, self.seed)
@@ -278,14 +313,22 @@ class GpuBackend:
             if r.prompt_len + r.target_output_len + self.k_max + 1 > self.max_out:
                 raise ConfigError(f"request {r.id} exceeds max_seq_len={self.max_out}")
         self._state = state
+        if self.replay:
+            self._sim.bind(state)
 
     def estimate(self, state, plan):
+        if self.replay:  # the draft_time the reference's acceptance law sees
+            return self._sim.estimate(state, plan)
         return 0.0, 0.0, 0.0
 
     def planned_commit(self, state, rid, k_i, draft_time):
+        if self.replay:  # exact sizing: peek the row's acceptance stream
+            return self._sim.planned_commit(state, rid, k_i, draft_time)
         return min(k_i + 1, state.requests[rid].remaining)
 
     def commit(self, state, rid, tokens):
+        if self.replay:
+            return  # grants were exact (or eager k_i + 1, kept as the reference does)
         # roll back the reserved-but-rejected tail: keep blocks for the
         # committed tokens only (the reference's exact-size invariant)
         state.kv.trim_to_written(rid)
@@ -421,10 +464,17 @@ class GpuBackend:
         return min(self.max_batch, max(8, (n + 7) // 8 * 8))
 
     def _slots_at(self, slot_rows: np.ndarray, pos: np.ndarray) -> np.ndarray:
-        """KV write slots of (slot, position) pairs from the host block table."""
+        """KV write slots of (slot, position) pairs from the host block table.
+        Replay mode grants exactly the next commit, so draft / verify rows past
+        it (beyond the replayed acceptance, never committed) write nowhere (-1)."""
         bi = pos // self.block_size
-        if (bi >= self.nblk[slot_rows]).any():
-            raise KVError("KV position beyond the request's allocated blocks")
+        beyond = bi >= self.nblk[slot_rows]
+        if beyond.any():
+            if not self.replay:
+                raise KVError("KV position beyond the request's allocated blocks")
+            bi = np.where(beyond, 0, bi)
+            return np.where(beyond, -1,
+                            self.bt_np[slot_rows, bi] * self.block_size + pos % self.block_size)
         return self.bt_np[slot_rows, bi] * self.block_size + pos % self.block_size
 
     def _run_graph(self, key, launch) -> None:
@@ -528,7 +578,11 @@ class GpuBackend:
             fwd.stage(i, arrays)
         fwd.upload(kmax)
         if self.mode == "sample":
-            kh = self.d_key_host.numpy()
+            self.d_key_cur = (self.d_key_cur + 1) % self.d_key_ring
+            ev = self.d_key_events[self.d_key_cur]
+            if ev is not None:
+                ev.synchronize()
+            kh = self.d_key_host[self.d_key_cur].numpy()
             B = self.max_batch
             kh[:nb] = [r for r in rows] + [0] * (nb - n)
             kh[B:B + nb] = L
@@ -536,7 +590,10 @@ class GpuBackend:
             K = self.k_max
             for i in range(kmax):
                 kh[2 * B + i * B:2 * B + i * B + nb] = np.where(real & (i < k), sl * K + i, -1)
-            self.d_key.copy_(self.d_key_host, non_blocking=True)
+            self.d_key.copy_(self.d_key_host[self.d_key_cur], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            self.d_key_events[self.d_key_cur] = ev
         self._run_graph(("draft", nb, kmax), lambda: self._draft_launch_capped(nb, kmax))
 
     def _draft_launch_capped(self, nb: int, kmax: int) -> None:
@@ -629,6 +686,13 @@ class GpuBackend:
         B = self.max_batch
         vm[:nb] = k
         vm[B:B + nb] = np.where(real, sl, -1)
+        if self.replay:
+            from .acceptance import acceptance_stream, accepted_count
+            cfg = state.config
+            forced = [accepted_count(cfg.acceptance, r.k, r.draft_time,
+                                     acceptance_stream(cfg.seed, r.request_id, r.j))
+                      if r.k > 0 else 0 for r in rows]
+            vm[2 * B:2 * B + nb] = forced + [0] * (nb - n)
         if kmax:
             vm[3 * B:3 * B + nb * kmax] = (sl[:, None] * ldt + 2 + np.arange(kmax)[None, :]
                                            ).reshape(-1)
@@ -639,12 +703,13 @@ class GpuBackend:
             kh[B:B + nb] = L
             self.v_key.copy_(self.v_key_host, non_blocking=True)
         capped = beside_draft and self.verify_ctas > 0
-        self._run_graph(("verify", nb, kmax, capped),
+        self._run_graph(("verify", nb, kmax, capped, self.replay),
                         lambda: self._verify_launch(nb, kmax, capped))
         if self.capture_verify is not None:
             torch.cuda.current_stream(self.device).synchronize()
             V = self.tshape.vocab
-            rec = {"target": self.tlogits[:nb * K1].view(nb, K1, V)[:n].cpu().numpy(),
+            rec = {"forced": vm[2 * B:2 * B + n].copy() if self.replay else None,
+                   "target": self.tlogits[:nb * K1].view(nb, K1, V)[:n].cpu().numpy(),
                    "ids": self.v_ids.view(-1)[:nb * kmax].view(nb, kmax)[:n].cpu().numpy(),
                    "len": k[:n].astype(np.int32), "acc": self.v_acc[:n].cpu().numpy(),
                    "out": self.v_out[:nb * K1].view(nb, K1)[:n].cpu().numpy()}
@@ -679,6 +744,7 @@ class GpuBackend:
                 bigram=(self.succ_t, self.beta_target))
         v_len = self.v_meta[:nb]
         v_slot = self.v_meta[B:B + nb]
+        forced = self.v_meta[2 * B:2 * B + nb] if self.replay else None
         if kmax:
             native.check(lib.psd_index_copy_i32(self.v_ids.data_ptr(), None,
                                                 self.slot_tok.data_ptr(),
@@ -690,7 +756,7 @@ class GpuBackend:
         logits = self.tlogits[:M].view(nb, K1, -1)
         out = self.v_out[:nb * K1].view(nb, K1)
         if self.mode == "greedy":
-            ops.verify_greedy(logits, v_ids, v_len, self.v_acc[:nb], out)
+            ops.verify_greedy(logits, v_ids, v_len, self.v_acc[:nb], out, forced_len=forced)
         else:
             native.check(lib.psd_philox_uniforms(
                 self.seed_verify, self.v_key.data_ptr(), self.v_key[B:].data_ptr(), nb, K1, 0,
@@ -700,13 +766,13 @@ class GpuBackend:
             # the q statistics are cached when this process drew the drafts, or
             # shipped with the q rows by a dedicated draft GPU (pair.py)
             cached = ("draft" in self.roles or self.qstats_remote) and self.qstats_cache
-            native.check(lib.psd_verify_sample_ext(
+            native.check(lib.psd_verify_sample_forced(
                 logits.data_ptr(), K1 * self.tshape.vocab, self.tshape.vocab,
                 self.tshape.vocab, self.qbuf.data_ptr(), v_slot.data_ptr(), self.k_max * Vd, Vd,
                 Vd, v_ids.data_ptr(), v_len.data_ptr(), self.v_u.data_ptr(), self.temperature, nb,
-                kmax, self.v_acc.data_ptr(), out.data_ptr(),
-                self.qstats.data_ptr() if cached else None, self.k_max, None, None,
-                ws.data_ptr(), ws.numel(), st), "verify_sample_ext")
+                kmax, forced.data_ptr() if forced is not None else None, self.v_acc.data_ptr(),
+                out.data_ptr(), self.qstats.data_ptr() if cached else None, self.k_max, None,
+                None, ws.data_ptr(), ws.numel(), st), "verify_sample")
         native.check(lib.psd_commit(self.v_acc.data_ptr(), out.data_ptr(), kmax,
                                     v_slot.data_ptr(), nb, self.generated.data_ptr(),
                                     self.slot_tok.data_ptr(), self.ldt, self.outputs.data_ptr(),
@@ -773,4 +839,15 @@ class GpuBackend:
         self.stats["verify_ms"] += verify_ms
         self.stats["prefill_ms"] += prefill_ms
         self.stats["host_s"] = self.stats.get("host_s", 0.0) + (time.perf_counter() - t_host)
-        return StepResult(prefill_ms, serial_ms, overlap_ms, verify_ms, step_ms, accepted)
+        measured = StepResult(prefill_ms, serial_ms, overlap_ms, verify_ms, step_ms, accepted)
+        if self.replay:
+            # the scheduler advances on the reference's virtual durations (so
+            # arrivals and preemptions fire at the same steps as in specsim);
+            # the device really committed the replayed counts
+            virt = self._sim.execute(state, plan, rows)
+            if virt.accepted != accepted:
+                raise ProtocolError(f"replay: device accepted {accepted} != reference "
+                                    f"{virt.accepted}")
+            self.measured_log.append(measured)
+            return virt
+        return measured

@@ -29,7 +29,7 @@ from __future__ import annotations
 
 from .records import StepRecord
 
-__all__ = ["KTuner", "expected_chain_accepts", "invert_chain_accepts"]
+__all__ = ["KTuner", "expected_chain_accepts", "invert_chain_accepts", "invert_chain_accepts_rows"]
 
 
 def expected_chain_accepts(p: float, k: int) -> float:
@@ -59,6 +59,24 @@ def invert_chain_accepts(a: float, k: float) -> float:
     return 0.5 * (lo + hi)
 
 
+def invert_chain_accepts_rows(pairs) -> float:
+    """p with sum_i E[a | k_i, p] == sum_i a_i over verified rows (k_i, a_i),
+    k_i > 0 (bisection; every term is increasing in p)."""
+    total = sum(a for _, a in pairs)
+    if total <= 0:
+        return 0.0
+    if total >= sum(k for k, _ in pairs):
+        return 1.0
+    lo, hi = 0.0, 1.0
+    for _ in range(60):
+        mid = 0.5 * (lo + hi)
+        if sum(expected_chain_accepts(mid, k) for k, _ in pairs) < total:
+            lo = mid
+        else:
+            hi = mid
+    return 0.5 * (lo + hi)
+
+
 class KTuner:
     """Chooses the draft depth between steps from measured acceptance and
     timings.  ``k`` is the depth to draft next; ``history`` records (step,
@@ -80,18 +98,27 @@ class KTuner:
     def _avg(self, old, new):
         return new if old is None else (1.0 - self.ema) * old + self.ema * new
 
-    def observe(self, rec: StepRecord) -> None:
-        # the step drafted with the depth this tuner handed out before the step
-        # (PSD: for the skip batch, whose acceptance arrives one step later);
-        # its verified rows carry the depth they were drafted with
-        k_drafted = self.k
-        if rec.draft_duration > 0.0:
-            self.d = self._avg(self.d, rec.draft_duration / k_drafted)
-        rows = rec.bonus_tokens  # exactly one bonus per verified row
-        if rows <= 0 or rec.drafted_tokens <= 0:
-            return
-        k_obs = rec.drafted_tokens / rows
-        p = invert_chain_accepts(rec.accepted_tokens / rows, k_obs)
+    def observe(self, rec: StepRecord, verified=None, draft_steps: int | None = None) -> None:
+        """``verified``: the step's verified rows as (k_i, accepted) -- in PSD
+        they were drafted one step earlier, possibly at another depth and batch
+        size than this step's drafts, so acceptance is estimated from them
+        alone (rows with k_i = 0 are idle passes and carry no information).
+        ``draft_steps``: sequential draft steps behind ``rec.draft_duration``
+        (a startup step drafts two batches).  Without them (a bare StepRecord)
+        the record's aggregate counts are used."""
+        steps = draft_steps if draft_steps else self.k
+        if rec.draft_duration > 0.0 and steps > 0:
+            self.d = self._avg(self.d, rec.draft_duration / steps)
+        if verified is not None:
+            pairs = [(k, a) for k, a in verified if k > 0]
+            if not pairs:
+                return
+            p = invert_chain_accepts_rows(pairs)
+        else:
+            rows = rec.bonus_tokens  # exactly one bonus per verified row
+            if rows <= 0 or rec.drafted_tokens <= 0:
+                return
+            p = invert_chain_accepts(rec.accepted_tokens / rows, rec.drafted_tokens / rows)
         self.p = self._avg(self.p, p)
         if rec.verify_duration > 0.0:
             self.v = self._avg(self.v, rec.verify_duration)

@@ -55,6 +55,10 @@ SIGNATURES: dict[str, tuple] = {
                                     _i, _i, _p, _p, _p, _sz, _p]),
     "psd_verify_sample_ext": (_i, [_p, _i64, _i64, _i, _p, _p, _i64, _i64, _i, _p, _p, _p, _f,
                                    _i, _i, _p, _p, _p, _i64, _p, _p, _p, _sz, _p]),
+    "psd_verify_greedy_forced": (_i, [_p, _i64, _i64, _i, _p, _p, _i, _i, _p, _p, _p, _p, _sz,
+                                      _p]),
+    "psd_verify_sample_forced": (_i, [_p, _i64, _i64, _i, _p, _p, _i64, _i64, _i, _p, _p, _p,
+                                      _f, _i, _i, _p, _p, _p, _p, _i64, _p, _p, _p, _sz, _p]),
     "psd_commit": (_i, [_p, _p, _i, _p, _i, _p, _p, _i, _p, _i, _p]),
     "psd_index_copy_i32": (_i, [_p, _p, _p, _p, _i, _p]),
     "psd_fill_uniform_bf16": (_i, [_p, _sz, _c.c_uint64, _f, _p]),

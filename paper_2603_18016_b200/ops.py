@@ -53,11 +53,13 @@ def _rows_view(x: torch.Tensor, name: str):
 
 def verify_greedy(target_logits: torch.Tensor, draft_ids: torch.Tensor,
                   draft_len: torch.Tensor, accepted_len: torch.Tensor | None = None,
-                  out_tokens: torch.Tensor | None = None):
+                  out_tokens: torch.Tensor | None = None,
+                  forced_len: torch.Tensor | None = None):
     """Greedy speculative verification (K1).
 
     target_logits [B, K+1, V] fp32; draft_ids [B, K] int32; draft_len [B]
     int32.  Returns (accepted_len [B] int32, out_tokens [B, K+1] int32).
+    forced_len [B] int32: replay mode (psd_verify_greedy_forced).
     """
     _check(target_logits, "target_logits", torch.float32, 3)
     B, K1, V = target_logits.shape
@@ -74,6 +76,14 @@ def verify_greedy(target_logits: torch.Tensor, draft_ids: torch.Tensor,
     ws = _verify_workspace(dev, B, K, V, 0, False)
     sb, si = _rows_view(target_logits, "target_logits")
     lib = native.load()
+    if forced_len is not None:
+        _check(forced_len, "forced_len", torch.int32, 1)
+        native.check(lib.psd_verify_greedy_forced(
+            target_logits.data_ptr(), sb, si, V, draft_ids.contiguous().data_ptr(),
+            draft_len.contiguous().data_ptr(), B, K, forced_len.contiguous().data_ptr(),
+            accepted_len.data_ptr(), out_tokens.data_ptr(), ws.data_ptr(), ws.numel(),
+            _stream_ptr(dev)), "psd_verify_greedy_forced")
+        return accepted_len, out_tokens
     native.check(lib.psd_verify_greedy(
         target_logits.data_ptr(), sb, si, V, draft_ids.contiguous().data_ptr(),
         draft_len.contiguous().data_ptr(), B, K, accepted_len.data_ptr(),
@@ -87,14 +97,16 @@ def verify_sample(target_logits: torch.Tensor, draft_logits: torch.Tensor,
                   temperature: float = 1.0, accepted_len: torch.Tensor | None = None,
                   out_tokens: torch.Tensor | None = None, d_stats: torch.Tensor | None = None,
                   t_stats_out: torch.Tensor | None = None,
-                  t_stats_rows: torch.Tensor | None = None):
+                  t_stats_rows: torch.Tensor | None = None,
+                  forced_len: torch.Tensor | None = None):
     """Speculative rejection sampling (K1).
 
     target_logits [B, K+1, V], draft_logits [B, K, Vd] fp32 (Vd <= V);
     uniforms [B, K+1] fp32 in [0, 1).  Returns (accepted_len, out_tokens).
     d_stats [B, K, 2] fp32: cached (max, sum) of the draft rows (not re-read);
     t_stats_out [*, 2] + t_stats_rows [B] int32: receive the (max, sum) of
-    target row 0 (psd_verify_sample_ext).
+    target row 0 (psd_verify_sample_ext).  forced_len [B] int32: replay mode
+    (psd_verify_sample_forced).
     """
     _check(target_logits, "target_logits", torch.float32, 3)
     _check(draft_logits, "draft_logits", torch.float32, 3)
@@ -119,18 +131,22 @@ def verify_sample(target_logits: torch.Tensor, draft_logits: torch.Tensor,
         draft_logits, Vd = target_logits, V
     db, di = _rows_view(draft_logits, "draft_logits")
     lib = native.load()
-    if d_stats is not None or t_stats_out is not None:
+    if d_stats is not None or t_stats_out is not None or forced_len is not None:
         if d_stats is not None:
             _check(d_stats, "d_stats", torch.float32, 3)
-        native.check(lib.psd_verify_sample_ext(
+        if forced_len is not None:
+            _check(forced_len, "forced_len", torch.int32, 1)
+        native.check(lib.psd_verify_sample_forced(
             target_logits.data_ptr(), sb, si, V, draft_logits.data_ptr(), None, db, di, Vd,
             draft_ids.contiguous().data_ptr(), draft_len.contiguous().data_ptr(),
-            uniforms.contiguous().data_ptr(), float(temperature), B, K, accepted_len.data_ptr(),
+            uniforms.contiguous().data_ptr(), float(temperature), B, K,
+            forced_len.contiguous().data_ptr() if forced_len is not None else None,
+            accepted_len.data_ptr(),
             out_tokens.data_ptr(), d_stats.data_ptr() if d_stats is not None else None,
             d_stats.stride(0) // 2 if d_stats is not None else 0,
             t_stats_out.data_ptr() if t_stats_out is not None else None,
             t_stats_rows.data_ptr() if t_stats_rows is not None else None,
-            ws.data_ptr(), ws.numel(), _stream_ptr(dev)), "psd_verify_sample_ext")
+            ws.data_ptr(), ws.numel(), _stream_ptr(dev)), "psd_verify_sample_forced")
         return accepted_len, out_tokens
     native.check(lib.psd_verify_sample(
         target_logits.data_ptr(), sb, si, V, draft_logits.data_ptr(), db, di, Vd,

@@ -163,6 +163,8 @@ class PairTarget:
                       "wait_ms": 0.0}
 
     def bind(self, state: EngineState) -> None:
+        # commits of a previous run target slots / request ids of that run
+        self.pending_commits = []
         self.engine.bind(state)
 
     def estimate(self, state, plan):
@@ -237,6 +239,7 @@ class PairTarget:
                                  self.link.recv_rows(n, vq + 4, self.engine.device))
 
     def stop(self) -> None:
+        self.pending_commits = []
         self.link.send(np.asarray([MAGIC, K_STOP], np.int32))
 
 

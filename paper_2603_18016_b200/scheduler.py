@@ -178,6 +178,10 @@ class EngineState:
     sd_members: dict[int, None] = field(default_factory=dict)
     backend: Backend | None = None
     k_tuner: object | None = None  # ktune.KTuner: online draft depth (None = config.k)
+    # the last step's verified rows as (k_i, accepted) and its sequential draft
+    # steps (sum over its draft loops of max k_i): what the tuner observes
+    last_verified: list[tuple[int, int]] = field(default_factory=list)
+    last_draft_steps: int = 0
 
     def request_list(self) -> list[Request]:
         return [self.requests[rid] for rid in sorted(self.requests)]
@@ -300,9 +304,11 @@ def _commit_rows(state: EngineState, rows: list[VerifyRow],
     """Commit accepted + bonus per row; returns (accepted, bonus, finished)."""
     acc_total = bonus_total = 0
     finished: list[int] = []
+    state.last_verified = []
     for row in rows:
         req = state.requests[row.request_id]
         a = accepted.get(row.request_id, 0) if row.k > 0 else 0
+        state.last_verified.append((row.k, a))
         commit = min(a + 1, req.remaining)
         req.generated += commit
         state.kv.commit_write(row.request_id, commit)
@@ -398,6 +404,8 @@ def _psd_step(state: EngineState) -> StepRecord:
     record_target = target if (branch != "fallback" or target_ids) else skip
 
     quotas = {rid: _quota(state, rid) for rid in serial + overlap}
+    state.last_draft_steps = (max((quotas[r] for r in serial), default=0)
+                              + max((quotas[r] for r in overlap), default=0))
     plan = StepPlan(step_index, branch, prefill_ids, serial, overlap,
                     tuple(verify_ids), quotas, cfg.comm_overhead)
     prefill_est, serial_est, overlap_est = backend.estimate(state, plan)
@@ -465,6 +473,7 @@ def _sd_step(state: EngineState) -> StepRecord:
     state.newly_admitted = []
     ids = list(state.sd_members)
     quotas = {rid: _quota(state, rid) for rid in ids}
+    state.last_draft_steps = max(quotas.values(), default=0)
     plan = StepPlan(step_index, "sd", prefill_ids, tuple(ids), (), tuple(ids), quotas)
     _, serial_est, _ = backend.estimate(state, plan)
 
@@ -512,7 +521,8 @@ def step_once(state: EngineState, config: SimConfig | None = None) -> StepRecord
     state.step_log.append(rec)
     state.step_index = rec.step_index
     if state.k_tuner is not None:
-        state.k_tuner.observe(rec)
+        state.k_tuner.observe(rec, verified=state.last_verified,
+                              draft_steps=state.last_draft_steps)
     return rec
 
 

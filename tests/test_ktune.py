@@ -59,3 +59,29 @@ def test_without_tuner_the_run_is_unchanged():
     b, _ = run(cfg, make_requests([40] * 8, prompt_len=8), k_tuner=None)
     assert [(s.drafted_tokens, s.accepted_tokens) for s in a.step_log] == \
         [(s.drafted_tokens, s.accepted_tokens) for s in b.step_log]
+
+
+def test_rows_inversion_with_mixed_depths():
+    from paper_2603_18016_b200.ktune import invert_chain_accepts_rows
+    p = 0.7
+    pairs = [(1, 0), (3, 0), (5, 0), (8, 0)]
+    total = sum(expected_chain_accepts(p, k) for k, _ in pairs)
+    # spread the expected total over the rows (only the sum matters)
+    pairs = [(k, total / len(pairs)) for k, _ in pairs]
+    assert abs(invert_chain_accepts_rows(pairs) - p) < 1e-6
+
+
+def test_tuner_estimates_p_from_verified_rows_with_unequal_batches():
+    """Batches of different sizes (odd request count, arrivals ramping up and
+    draining): the skip batch's drafted count and the verified batch's
+    accepted count come from different rows, so p must come from the
+    verified rows alone."""
+    p = 0.8
+    tuner = KTuner(k_max=5, mode="psd", warmup=10_000, ema=0.05, k0=5)
+    cfg = _cfg("psd", 5, p, 0.5, 10.0)
+    lens = [60, 300, 45, 200, 90, 150, 30]  # 7 requests: batches of 4 and 3, uneven drain
+    st, rep = run(cfg, make_requests(lens, prompt_len=8), k_tuner=tuner)
+    assert rep.finished == 7
+    tail = tuner.history[len(tuner.history) // 3:]
+    est = sum(h[2] for h in tail) / len(tail)
+    assert abs(est - p) < 0.06, est

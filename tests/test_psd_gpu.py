@@ -105,12 +105,22 @@ def test_greedy_psd_identical_to_cpu_oracle(cuda_device, beta):
             [(s.drafted_tokens, s.accepted_tokens, s.bonus_tokens) for s in cs.step_log]
     else:
         # weak synthetic-language bias: logits of random-init models have
-        # near-ties; identity must hold except at documented near-ties
-        same = sum(a == b for a, b in zip(g, c))
+        # near-ties.  Every token of every GPU sequence (not just the first
+        # divergence) must be the oracle target's greedy choice given the GPU's
+        # own prefix, or a documented near-tie (tests/_parity.py)
+        from tests._parity import oracle_rows, teacher_forced
+        exact, ties = 0, []
+        for req, a in zip(gs.request_list(), g):
+            lg = oracle_rows(cb.t, cb.succ, cb.beta_t, req.prompt_ids, a)
+            e, t = teacher_forced(lg, a)
+            exact += e
+            ties += t
+        assert exact >= 0.97 * sum(len(a) for a in g), ties
+        # sequences that agree with the oracle PSD up to a divergence diverge
+        # only at one of those near-ties
         for req, a, b in zip(gs.request_list(), g, c):
             if a != b:
                 _near_tie_ok(cb, req, a, b)
-        assert same >= len(g) // 2
 
 
 def test_greedy_psd_equals_sd_on_gpu(cuda_device):
