@@ -348,7 +348,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 struct Seg {
-  int t, kb0, kb1, first;  // tile, k-block range, is the CTA's first segment
+  int t, kb0, kb1, first;  // tile, k-block range, is the (virtual) CTA's first segment
+  int v;                   // virtual CTA the segment belongs to
 };
 
 __device__ __forceinline__ long long sk_bound(long long c, const SKArgs& g) {
@@ -390,8 +391,13 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   int* s_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // Virtual CTAs: the work split (G shares, their k-block boundaries, the
+  // fix-up order) depends only on the GEMM shape and the SM count, never on how
+  // many CTAs actually run (psd_gemm_set_max_ctas): a capped launch's CTA c
+  // processes virtual CTAs c, c + gridDim.x, ...  So every output element is
+  // summed in the same order whatever the cap or the batch -- batch-invariant
+  // numerics (greedy PSD == SD token for token).
   const int c = blockIdx.x;
-  const long long u0 = sk_bound(c, g), u1 = sk_bound(c + 1, g);
 
   if (warp == 0 && lane == 0) {
     if (g.trace) g.trace[c * 16 + 0] = gtimer();
@@ -417,25 +423,33 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   // first this CTA's stream-K units over tiles D.., then its whole tiles
   // c, c+G, .. < D: a CTA ends on a whole tile, whose epilogue reads no partials
   struct SegIt {
-    long long u;
+    int v;
+    long long u, u0, u1;
     int dp;
   };
+  auto seg_begin = [&](int v) -> SegIt {
+    return SegIt{v, sk_bound(v, g), sk_bound(v, g), sk_bound(v + 1, g), v};
+  };
   auto next_seg = [&](SegIt& it, Seg& sg) -> bool {
-    if (it.u < u1) {
-      sg.t = g.D + (int)(it.u / g.KB);
-      sg.kb0 = (int)(it.u % g.KB);
-      sg.kb1 = (int)min((long long)g.KB, sg.kb0 + (u1 - it.u));
-      sg.first = it.u == u0;
-      it.u += sg.kb1 - sg.kb0;
-      return true;
-    }
-    if (it.dp < g.D) {
-      sg.t = it.dp;
-      sg.kb0 = 0;
-      sg.kb1 = g.KB;
-      sg.first = 0;
-      it.dp += g.G;
-      return true;
+    while (it.v < g.G) {
+      sg.v = it.v;
+      if (it.u < it.u1) {
+        sg.t = g.D + (int)(it.u / g.KB);
+        sg.kb0 = (int)(it.u % g.KB);
+        sg.kb1 = (int)min((long long)g.KB, sg.kb0 + (it.u1 - it.u));
+        sg.first = it.u == it.u0;
+        it.u += sg.kb1 - sg.kb0;
+        return true;
+      }
+      if (it.dp < g.D) {
+        sg.t = it.dp;
+        sg.kb0 = 0;
+        sg.kb1 = g.KB;
+        sg.first = 0;
+        it.dp += g.G;
+        return true;
+      }
+      it = seg_begin(it.v + (int)gridDim.x);
     }
     return false;
   };
@@ -444,13 +458,13 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     if (lane == 0) {
       const uint64_t pol_w = policy_evict_first();
       const uint64_t pol_x = policy_evict_last();
-      SegIt it{u0, c};
+      SegIt it = seg_begin(c);
       Seg sg;
       int i = 0;
       // PDL: the first stages' weight tiles stream before pdl_wait()
       int npre = 0;
       {
-        SegIt i0{u0, c};
+        SegIt i0 = seg_begin(c);
         Seg s0;
         if (next_seg(i0, s0)) {
           const int n0 = (s0.t / g.MT) * BM;
@@ -501,7 +515,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
-      SegIt it{u0, c};
+      SegIt it = seg_begin(c);
       Seg sg;
       int i = 0, j = 0;
       while (next_seg(it, sg)) {
@@ -537,7 +551,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     const int q = warp & 3;
     const int row = 32 * q + lane;  // tile row (weight row) of this thread
     pdl_wait();  // residual / partial workspace belong to the predecessor's epoch
-    SegIt it{u0, c};
+    SegIt it = seg_begin(c);
     Seg sg;
     int j = 0, eq = 0;
     while (next_seg(it, sg)) {
@@ -545,7 +559,8 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       const uint32_t aph = (j / NACC) & 1;
       const int n0 = (sg.t / g.MT) * BM, m0 = (sg.t % g.MT) * ACC_COLS;
       const bool split = sg.kb0 != 0 || sg.kb1 != g.KB;
-      int owner = c, last = c;
+      const int me = sg.v;  // virtual CTA of this segment
+      int owner = me, last = me;
       bool finisher = true;
       int* flag = s_flag + (j & 1);
       if (split) {
@@ -567,7 +582,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         if (g.trace && finisher && threadIdx.x == 64) g.trace[c * 16 + 6] += 1;
         if (!finisher) {
           // publish this segment's partial, take a ticket
-          float* mine = g.part + ((size_t)c * 2 + (sg.first ? 0 : 1)) * (ACC_COLS * BM);
+          float* mine = g.part + ((size_t)me * 2 + (sg.first ? 0 : 1)) * (ACC_COLS * BM);
 #pragma unroll 1
           for (int col0 = 0; col0 < ACC_COLS; col0 += 16 * EG) {
             uint32_t r[EG][16];
@@ -616,7 +631,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 #pragma unroll
               for (int k = 0; k < 16; ++k) v[e][k] = 0.f;
             for (int cc = owner; cc <= last; ++cc) {
-              if (cc == c) {
+              if (cc == me) {
 #pragma unroll
                 for (int e = 0; e < EG; ++e)
 #pragma unroll
@@ -891,6 +906,8 @@ int launch_bn(const CUtensorMap& mw, const CUtensorMap& mx, const GemmArgs& g, d
 }
 
 
+int sk_physical(int G);
+
 template <int BN, int EPI, bool TILED, int NT = 1, int SMEM_KB = 200>
 int launch_sk_bn_s(const CUtensorMap& mw, const CUtensorMap& mx, const SKArgs& g,
                    cudaStream_t st) {
@@ -904,8 +921,8 @@ int launch_sk_bn_s(const CUtensorMap& mw, const CUtensorMap& mx, const SKArgs& g
     if (e != cudaSuccess) return (int)e;
     attr_done = true;
   }
-  return (int)psd::launch(gemm_sk_kernel<BN, EPI, TILED, NT, SMEM_KB>, dim3(g.G), dim3(kThreads),
-                          SMEM, st, mw, mx, g);
+  return (int)psd::launch(gemm_sk_kernel<BN, EPI, TILED, NT, SMEM_KB>, dim3(sk_physical(g.G)),
+                          dim3(kThreads), SMEM, st, mw, mx, g);
 }
 
 template <int BN, int EPI, bool TILED, int NT = 1>
@@ -1053,10 +1070,14 @@ std::atomic<unsigned long long*>& sk_trace() {
 }
 
 int num_sms_raw();
-int num_sms() {
+
+// CTAs a stream-K launch of G virtual CTAs runs on: the cap, rounded so that
+// every physical CTA gets the same number of virtual ones when possible
+int sk_physical(int G) {
   const int cap = max_ctas_cap().load(std::memory_order_relaxed);
-  const int n = num_sms_raw();
-  return cap > 0 && cap < n ? cap : n;
+  if (cap <= 0 || cap >= G) return G;
+  const int per = (G + cap - 1) / cap;  // virtual CTAs per physical CTA
+  return (G + per - 1) / per;
 }
 
 int num_sms_raw() {
@@ -1089,13 +1110,17 @@ struct SKPlan {
 // (70B gate/up at M = 320: 426 -> 294 us; 8B gate/up at M = 384: 110 -> 117 us)
 SKPlan sk_plan(int M, int N, int K, bool allow_nt2 = true) {
   SKPlan p;
-  const TokGeo tg = tok_geo(M, allow_nt2 && (N / BM) >= 2 * num_sms());
+  // batch-invariant geometry: the k-block split of every tile depends only on
+  // (N, K) and the SM count -- not on the CTA cap, and not on M for M <= 512
+  // (two token tiles share a weight tile above 256 tokens, so the tile set is
+  // the same as at M <= 256)
+  const TokGeo tg = tok_geo(M, allow_nt2);
   p.bn = tg.bn;
   p.nt = tg.nt;
   p.KB = (K + BK - 1) / BK;
   p.MT = tg.mt;
   p.tiles = (N / BM) * p.MT;
-  p.G = (int)std::min<long long>(num_sms(), (long long)p.tiles * p.KB);
+  p.G = (int)std::min<long long>(num_sms_raw(), (long long)p.tiles * p.KB);
   // data-parallel + stream-K: each CTA takes tiles / G whole tiles and an
   // equal share of the remaining tiles' k-blocks; a remainder that would cut
   // every tile into more than ~2 pieces gets one more stream-K wave instead
@@ -1146,7 +1171,9 @@ int psd_gemm_plan(int M, int N, int K, int epi, int splits_hint, int* splits_out
   int splits = splits_hint;
   if (splits <= 0) {
     splits = 1;
-    if (tiles < 120) splits = std::max(1, std::min(num_sms() / tiles, kb_total / 4));
+    // from the SM count, not the CTA cap: the split (and so the summation order
+    // of every output element) must not depend on what runs beside the GEMM
+    if (tiles < 120) splits = std::max(1, std::min(num_sms_raw() / tiles, kb_total / 4));
   }
   splits = std::max(1, std::min(splits, kb_total));
   const int per = (kb_total + splits - 1) / splits;
@@ -1255,7 +1282,7 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
     // gate/up at M = 32: 14.3 vs 19.8 us, profiles/r01b_kbench_gemm_splits.txt)
     const TokGeo tg = tok_geo(M);
     const int tiles = (N / BM) * tg.mt;
-    if (tg.nt == 1 && tiles <= num_sms() && 4 * tiles >= 3 * num_sms()) splits_hint = 1;
+    if (tg.nt == 1 && tiles <= num_sms_raw() && 4 * tiles >= 3 * num_sms_raw()) splits_hint = 1;
   }
   if (splits_hint == 0) {
     // stream-K persistent path (default)

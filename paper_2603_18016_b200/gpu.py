@@ -648,7 +648,12 @@ class GpuBackend:
         whose accepted lengths land in ``acc_host``."""
         n = len(rows)
         nb = self._bucket(n)
-        kmax = max((r.k for r in rows), default=0)
+        # every verify pass has k_max + 1 query tokens per row, whatever this
+        # batch's deepest draft: a token's attention then runs with the same
+        # warp / key-group split in every pass (batch-invariant numerics, so
+        # greedy PSD, SD(m) and SD(2m) emit identical tokens); rows with k_i <
+        # k_max neither write KV past their drafts nor accept beyond k_i
+        kmax = self.k_max
         K1 = kmax + 1
         ldt = self.ldt
         sl = np.full(nb, self.scratch_slot, np.int64)

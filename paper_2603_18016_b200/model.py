@@ -387,6 +387,9 @@ class Forward:
         self.sets = sets
         import os
         self.fuse_rope = os.environ.get("PSD_FUSED_ROPE", "1") == "1"
+        # split count of the QKV / O / down split-K GEMMs (0 = the shape's
+        # default); tests use it to measure the forward's reordering noise floor
+        self.splits_hint = int(os.environ.get("PSD_SPLITS_HINT", "0"))
         # widest per-sequence query count that takes the fused path
         self.fuse_rope_max_q = int(os.environ.get("PSD_FUSED_ROPE_MAXQ", "2"))
         self.meta = torch.zeros(sets, o, dtype=torch.int32, device=dev)
@@ -481,7 +484,8 @@ class Forward:
                                      L["attn_norm"].data_ptr(), self.xn.data_ptr(), H, M, H,
                                      s.rms_eps, 1, st), "add+attn norm")
             _chk(lib.psd_gemm_partials(self.xn.data_ptr(), H, M, H, L["wqkv"].data_ptr(), H,
-                                       s.qkv_out, part, partn, 0, nsp, st), "gemm qkv")
+                                       s.qkv_out, part, partn, self.splits_hint, nsp, st),
+                 "gemm qkv")
             if fuse_rope:
                 # decode / verify: RoPE + KV write inside the attention kernel
                 _chk(lib.psd_attention_rope(
@@ -510,7 +514,7 @@ class Forward:
                                        else 0, self.att_ws.data_ptr(), self.att_ws.numel(), st),
                      "attention")
             _chk(lib.psd_gemm_partials(self.attn.data_ptr(), Dq, M, Dq, L["wo"].data_ptr(), Dq, H,
-                                       part, partn, 0, nsp, st), "gemm o")
+                                       part, partn, self.splits_hint, nsp, st), "gemm o")
             if tp:  # row-parallel O: sum the ranks' partial outputs
                 self._allreduce(nsp._obj.value * M * H)
             _chk(lib.psd_add_rmsnorm(X, H, part, nsp._obj.value, M * H, H, None,
@@ -520,7 +524,7 @@ class Forward:
                                    self.act.data_ptr(), Fp, native.EPI_SILU, None, 0, 0, ws, wsn,
                                    st), "gemm gate/up")
             _chk(lib.psd_gemm_partials(self.act.data_ptr(), Fp, M, Fp, L["wdown"].data_ptr(), Fp,
-                                       H, part, partn, 0, nsp, st), "gemm down")
+                                       H, part, partn, self.splits_hint, nsp, st), "gemm down")
             if tp:  # row-parallel down
                 self._allreduce(nsp._obj.value * M * H)
             prev_S = nsp._obj.value

@@ -39,11 +39,13 @@ def teacher_forced(lg: np.ndarray, out, tie_tol: float = 0.05):
     return exact, ties
 
 
-def gpu_logits(backend, prompt, out):
+def gpu_logits(backend, prompt, out, splits_hint: int = 0):
     """The device target forward's fp32 logits (bigram bias included) of the
     rows that emitted ``out``: one prefill pass over prompt + out[:-1] with
     its own block-table row (uses blocks 1.. of the backend's KV cache, which
-    are free once a run has finished)."""
+    are free once a run has finished).  ``splits_hint`` > 0 forces that
+    split-K count on the QKV / O / down GEMMs: an equally valid summation order,
+    whose distance to the default is the forward's own noise floor."""
     import torch
 
     from paper_2603_18016_b200.model import Forward
@@ -58,6 +60,7 @@ def gpu_logits(backend, prompt, out):
     p = len(prompt)
     rows = np.arange(p - 1, n, dtype=np.int32)
     fwd = Forward(m, n, 4, len(rows), bt)
+    fwd.splits_hint = splits_hint
     fwd.begin()
     fwd.stage(0, {"tokens": np.asarray(seq[:n], np.int32),
                   "positions": np.arange(n, dtype=np.int32),
@@ -71,6 +74,24 @@ def gpu_logits(backend, prompt, out):
     fwd.run(n, 1, n, len(rows), logits, V, bigram=(backend.succ_t, backend.beta_target))
     torch.cuda.synchronize()
     return logits.cpu().numpy()
+
+
+def noise_floor_ok(got: np.ndarray, ref: np.ndarray, alt: np.ndarray, factor: float = 1.5,
+                   atol_frac: float = 1e-2):
+    """The device logits are as close to the oracle's as two valid device
+    summation orders are to each other: max |got - ref| <= factor x max |got -
+    alt| + atol_frac x rms(ref), and the same for the RMS error.  bf16 storage
+    of every activation turns any reordering into a half-ulp noise on most
+    elements, which the 32-layer random-init stack accumulates (~sqrt(depth):
+    profiles/r02_forward_noise_floor.txt), so a fixed rtol cannot hold at depth
+    while this bound does."""
+    rms = float(np.sqrt((ref.astype(np.float64) ** 2).mean()))
+    e_max, f_max = float(np.abs(got - ref).max()), float(np.abs(got - alt).max())
+    e_rms = float(np.sqrt(((got.astype(np.float64) - ref) ** 2).mean()))
+    f_rms = float(np.sqrt(((got.astype(np.float64) - alt) ** 2).mean()))
+    ok = e_max <= factor * f_max + atol_frac * rms and e_rms <= factor * f_rms + atol_frac * rms
+    return ok, {"err_max": e_max, "floor_max": f_max, "err_rms": e_rms, "floor_rms": f_rms,
+                "rms": rms}
 
 
 def elementwise_ok(got: np.ndarray, ref: np.ndarray, rtol: float = 1e-2,
