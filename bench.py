@@ -144,18 +144,22 @@ def _time_kernel(fn, iters: int = 20) -> float:
     return e0.elapsed_time(e1) / iters
 
 
-def _ncu_traffic():
+TRAFFIC_FILE = os.path.join("profiles", "r02_ncu_traffic.json")
+
+
+def _ncu_traffic(key: str):
     """dram__bytes_read.sum + dram__bytes_write.sum of one launch of the
-    roofline kernel from the committed ncu --set full capture (profiles/)."""
+    roofline kernel, from this round's ncu --set full capture of the same
+    kernel at the same shape (TRAFFIC_FILE, written by tools/ncu_traffic.py)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01b_ncu_traffic.json")) as fh:
-            t = json.load(fh)["gate_up_M192_N28672_K4096"]
+        with open(os.path.join(ROOT, TRAFFIC_FILE)) as fh:
+            t = json.load(fh)[key]
         return t["dram_read"] + t["dram_write"]
     except (OSError, KeyError, ValueError):
         return None
 
 
-def kernel_rooflines(backend, hbm_peak: float) -> tuple[dict, dict]:
+def kernel_rooflines(backend, hbm_peak: float, bf16_peak: float) -> tuple[dict, dict]:
     """Dominant kernel (verify-forward gate/up GEMM) and K1 at the workload shapes."""
     import torch
     from paper_2603_18016_b200 import native, ops
@@ -167,7 +171,7 @@ def kernel_rooflines(backend, hbm_peak: float) -> tuple[dict, dict]:
     x = torch.randn(M, s.hidden, device=dev).to(torch.bfloat16)
     out = torch.empty(M, s.ffn_padded, dtype=torch.bfloat16, device=dev)
     ws = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
-    # rotate over all 32 layers' weights so every launch streams from HBM
+    # rotate over all layers' weights so every launch streams from HBM
     ws_list = [L["wgu"] for L in backend.target.layers]
     it = [0]
 
@@ -175,16 +179,45 @@ def kernel_rooflines(backend, hbm_peak: float) -> tuple[dict, dict]:
         ops.gemm(x, ws_list[it[0] % len(ws_list)], out=out, epi=native.EPI_SILU, workspace=ws)
         it[0] += 1
 
+    lib = native.load()
     ms = _time_kernel(gemm, 64)
+    # the same GEMM under the CTA cap it runs with inside an overlapped PSD step
+    # (the draft's kernels take the other SMs there); timed alone here
+    cap = backend.verify_ctas
+    ms_cap = None
+    if cap:
+        lib.psd_gemm_set_max_ctas(cap)
+        try:
+            ms_cap = _time_kernel(gemm, 64)
+        finally:
+            lib.psd_gemm_set_max_ctas(0)
+    N, Kd = w.shape[0], s.hidden
     nbytes = w.numel() * 2 + x.numel() * 2 + out.numel() * 2
-    roof = {"kernel": f"gemm_sk_kernel<SILU> (verify gate/up, M={M} N={w.shape[0]} "
-                      f"K={s.hidden})",
-            "bound": "hbm", "achieved": round(nbytes / (ms * 1e-3) / 1e9, 1),
-            "peak": hbm_peak, "unit": "GB/s",
-            "frac": round(nbytes / (ms * 1e-3) / 1e9 / hbm_peak, 4), "traffic": (_ncu_traffic() if (M, w.shape[0], s.hidden) == (192, 28672, 4096)
-                                   else None),
+    flops = 2 * M * N * Kd
+    # roofline class from arithmetic intensity vs the ridge point of the
+    # measured peaks (M = 192 is below the ridge, M = 320 above)
+    intensity = flops / nbytes
+    ridge = bf16_peak * 1e12 / (hbm_peak * 1e9)
+    bound = "tensor" if intensity >= ridge else "hbm"
+    if bound == "hbm":
+        achieved, peak, unit = nbytes / (ms * 1e-3) / 1e9, hbm_peak, "GB/s"
+    else:
+        achieved, peak, unit = flops / (ms * 1e-3) / 1e12, bf16_peak, "TFLOP/s"
+    roof = {"kernel": f"gemm_sk_kernel<SILU> (verify gate/up, M={M} N={N} K={Kd})",
+            "bound": bound, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
+            "frac": round(achieved / peak, 4),
+            "traffic": _ncu_traffic(f"gate_up_M{M}_N{N}_K{Kd}"),
+            "traffic_source": TRAFFIC_FILE,
+            "intensity_flop_per_byte": round(intensity, 1), "ridge_flop_per_byte": round(ridge, 1),
             "bytes_per_launch": nbytes, "us_per_launch": round(ms * 1e3, 2),
-            "tflops": round(2 * M * w.shape[0] * s.hidden / (ms * 1e-3) / 1e12, 1)}
+            "tflops": round(flops / (ms * 1e-3) / 1e12, 1),
+            "timing": "alone, all SMs, back-to-back launches rotating over every layer's weights",
+            "psd_step_config": ({"ctas": cap, "us_per_launch": round(ms_cap * 1e3, 2),
+                                 "GBps": round(nbytes / (ms_cap * 1e-3) / 1e9, 1),
+                                 "frac": round(nbytes / (ms_cap * 1e-3) / 1e9 / hbm_peak, 4),
+                                 "note": "CTA cap of the verify GEMMs in overlapped PSD steps, "
+                                         "timed alone (beside the draft the SMs are shared)"}
+                                if ms_cap else None)}
     B, K, V = CFG["m"], CFG["k"], s.vocab
     sets = [make_inputs(B, K, V, False, dev, seed=i) for i in range(3)]
     j = [0]
@@ -282,6 +315,68 @@ def cpu_sample(steps: int = 1, n_req: int = 2, out_len: int = 6):
         total_s += time.perf_counter() - t0
         total_tok += rep.total_generated
     return total_tok / total_s, total_s, total_tok, os.cpu_count()
+
+
+def cpu_plan_baselines(vocab: int) -> dict:
+    """BASELINE.md §2, timed on this host: (1) the reference's scheduler
+    algorithm (the byte-identical port with the reference's latency / coin-flip
+    models, SimBackend; one Python thread) on the workload's PSD and SD
+    configs, p = 0.8; (2) the CPU verification oracle (oracle/verify_oracle.c,
+    one thread) at the workload's verify shape, GB/s over the same algorithmic
+    bytes as K1; (3) the CPU oracle end to end on config 1 (tiny pair, 2 x 8
+    requests, k = 4, greedy): PSD and sequential SD tok/s, mean accepted length."""
+    import numpy as np
+    from oracle import verify as ov
+    from oracle.psd_cpu import CpuBackend
+    from paper_2603_18016_b200 import SimConfig, make_requests, mean_accepted_length, run
+    from paper_2603_18016_b200.sim import SimBackend
+    from paper_2603_18016_b200.verify_bench import algorithmic_bytes
+    out = {"cores_host": os.cpu_count()}
+    # (1) scheduler wall clock (virtual-time backend)
+    sched = {}
+    for mode, fac in (("psd", 1), ("standard-sd", 2)):
+        reqs = make_requests([CFG["output"]] * CFG["n_requests"], prompt_len=CFG["prompt"])
+        t0 = time.perf_counter()
+        run(SimConfig(mode=mode, m=CFG["m"], k=CFG["k"], sd_batch_factor=fac), reqs,
+            backend=SimBackend())
+        sched[mode] = round((time.perf_counter() - t0) * 1e3, 1)
+    out["scheduler_wall_ms"] = dict(sched, threads=1,
+                                    note="reference scheduler semantics (port, byte-identical "
+                                         "step logs) with its latency and coin-flip acceptance "
+                                         "models, p = 0.8")
+    # (2) CPU verification oracle at the verify shape
+    B, K = CFG["m"], CFG["k"]
+    rng = np.random.default_rng(0)
+    t = (rng.standard_normal((B, K + 1, vocab), dtype=np.float32) * 2.0)
+    ids = t[:, :K].argmax(axis=2).astype(np.int32)
+    ln = np.full(B, K, np.int32)
+    t0 = time.perf_counter()
+    ov.verify_greedy(t, ids, ln)
+    dt = time.perf_counter() - t0
+    d = (t[:, :K] + rng.standard_normal((B, K, vocab), dtype=np.float32) * 0.5)
+    u = rng.random((B, K + 1), dtype=np.float32)
+    t0 = time.perf_counter()
+    ov.verify_sample(t, d, ids, ln, u)
+    dts = time.perf_counter() - t0
+    gb, gbs = algorithmic_bytes(B, K, vocab, False), algorithmic_bytes(B, K, vocab, True)
+    out["verify_oracle"] = {"shape": f"B={B} k={K} V={vocab}", "threads": 1,
+                            "greedy_GBps": round(gb / dt / 1e9, 3),
+                            "sampling_GBps": round(gbs / dts / 1e9, 3)}
+    del t, d
+    # (3) config 1 on the CPU oracle: PSD vs sequential SD
+    c1 = {}
+    be = CpuBackend("tiny-target", "tiny-draft", seed=0, beta_target=3.0, beta_draft=12.0,
+                    max_seq_len=64)
+    for mode, fac in (("psd", 1), ("standard-sd", 2)):
+        reqs = make_requests([32] * 16, prompt_len=16)
+        t0 = time.perf_counter()
+        _, rep = run(SimConfig(mode=mode, m=8, k=4, sd_batch_factor=fac), reqs, backend=be)
+        dt = time.perf_counter() - t0
+        c1[mode] = {"tok_s": round(rep.total_generated / dt, 1),
+                    "mean_accepted_len": round(mean_accepted_length(rep), 4)}
+    out["cfg1_cpu_oracle"] = dict(c1, workload="tiny pair, 2 x 8 requests, prompt 16, "
+                                               "output 32, k = 4, greedy", threads=1)
+    return out
 
 
 def run_reference(args) -> None:
@@ -439,20 +534,25 @@ def run_ours(args) -> None:
         DraftServer(GpuDraftEngine(be), link).serve()
         pd.finalize()
         return
+    x0 = be.transfer_bytes()
     t0 = time.perf_counter()
     st, rep_e2e = one("psd")
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
+    x1 = be.transfer_bytes()
     if pairs:
         backend.stop()
-    roof, vk = kernel_rooflines(be, hbm_peak)
+    roof, vk = kernel_rooflines(be, hbm_peak, bf16_peak)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             v, secs, toks, cores = cpu_sample()
             cpu = {"value": round(v, 4), "unit": "tok/s", "cores": cores, "kind": "port",
-                   "sample": f"2 requests x 6 tokens, prompt 128, k=5, 8B/1B shapes "
-                             f"({toks} tokens in {secs:.1f} s)"}
+                   "sample": f"CPU oracle PSD (numpy / BLAS forward on the host cores, C "
+                             f"verify), 2 "
+                             f"requests x 6 tokens, prompt 128, k=5, 8B/1B shapes "
+                             f"({toks} tokens in {secs:.1f} s)",
+                   "plan": cpu_plan_baselines(be.tshape.vocab)}
         except MemoryError as exc:  # pragma: no cover
             cpu = {"value": None, "unit": "tok/s", "cores": os.cpu_count(), "kind": "port",
                    "sample": f"skipped: {exc}"}
@@ -476,8 +576,8 @@ def run_ours(args) -> None:
     r0 = psd["reps"][0]
     steps_sd = sd["steps"] / max(1, args.steps)
     steps_psd = psd["steps"] / max(1, args.steps)
-    h2d = CFG["n_requests"] * CFG["prompt"] * 4 + int(steps_psd) * 4 * 2 * CFG["m"]
-    d2h = CFG["n_requests"] * CFG["output"] * 4 + int(steps_psd) * 4 * CFG["m"]
+    # counted at every host <-> device copy the backend issued during the e2e pass
+    h2d, d2h = x1[0] - x0[0], x1[1] - x0[1]
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "tok/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,

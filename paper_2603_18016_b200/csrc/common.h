@@ -65,17 +65,26 @@ inline cudaError_t set_smem_limit(const void* k, int bytes, cudaStream_t st = nu
   return e;
 }
 
-// set_smem_limit once per kernel (kernels sharing a signature share a
-// function-pointer type, so a per-type static flag would not do)
+// set_smem_limit once per (device, kernel): function attributes belong to the
+// kernel's instance on the current device, so a process driving several GPUs
+// sets them on each (kernels sharing a signature share a function-pointer
+// type, so a per-type static flag would not do either)
 inline cudaError_t ensure_smem_limit(const void* k, int bytes, cudaStream_t st = nullptr) {
   static std::mutex mu;
-  static const void* done[64];
+  static const void* done_k[256];
+  static int done_dev[256];
   static int n = 0;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
   std::lock_guard<std::mutex> lock(mu);
   for (int i = 0; i < n; ++i)
-    if (done[i] == k) return cudaSuccess;
-  const cudaError_t e = set_smem_limit(k, bytes, st);
-  if (e == cudaSuccess && n < 64) done[n++] = k;
+    if (done_k[i] == k && done_dev[i] == dev) return cudaSuccess;
+  e = set_smem_limit(k, bytes, st);
+  if (e == cudaSuccess && n < 256) {
+    done_k[n] = k;
+    done_dev[n++] = dev;
+  }
   return e;
 }
 

@@ -894,12 +894,10 @@ template <int BN, int EPI>
 int launch_bn(const CUtensorMap& mw, const CUtensorMap& mx, const GemmArgs& g, dim3 grid,
               cudaStream_t st) {
   using C = Cfg<BN>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = psd::set_smem_limit((const void*)gemm_kernel<BN, EPI>,
-                                        C::SMEM + ep_stage_bytes<EPI>(), st);
+  {
+    const cudaError_t e = psd::ensure_smem_limit((const void*)gemm_kernel<BN, EPI>,
+                                                 C::SMEM + ep_stage_bytes<EPI>(), st);
     if (e != cudaSuccess) return (int)e;
-    attr_done = true;
   }
   return (int)psd::launch(gemm_kernel<BN, EPI>, grid, dim3(kThreads),
                           C::SMEM + ep_stage_bytes<EPI>(), st, mw, mx, g);
@@ -914,12 +912,10 @@ int launch_sk_bn_s(const CUtensorMap& mw, const CUtensorMap& mx, const SKArgs& g
   using C = Cfg<BN, NT, SMEM_KB>;
   constexpr int SMEM = C::SMEM + ep_stage_bytes<EPI>();
   static_assert(SMEM <= 227 * 1024, "stream-K GEMM shared memory");
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e =
-        psd::set_smem_limit((const void*)gemm_sk_kernel<BN, EPI, TILED, NT, SMEM_KB>, SMEM, st);
+  {
+    const cudaError_t e = psd::ensure_smem_limit(
+        (const void*)gemm_sk_kernel<BN, EPI, TILED, NT, SMEM_KB>, SMEM, st);
     if (e != cudaSuccess) return (int)e;
-    attr_done = true;
   }
   return (int)psd::launch(gemm_sk_kernel<BN, EPI, TILED, NT, SMEM_KB>, dim3(sk_physical(g.G)),
                           dim3(kThreads), SMEM, st, mw, mx, g);
@@ -948,12 +944,10 @@ template <int BN, int EPI, int NT>
 int launch_bn_nt(const CUtensorMap& mw, const CUtensorMap& mx, const GemmArgs& g, dim3 grid,
                  cudaStream_t st) {
   using C = Cfg<BN, NT>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = psd::set_smem_limit((const void*)gemm_kernel<BN, EPI, NT>,
-                                        C::SMEM + ep_stage_bytes<EPI>(), st);
+  {
+    const cudaError_t e = psd::ensure_smem_limit((const void*)gemm_kernel<BN, EPI, NT>,
+                                                 C::SMEM + ep_stage_bytes<EPI>(), st);
     if (e != cudaSuccess) return (int)e;
-    attr_done = true;
   }
   return (int)psd::launch(gemm_kernel<BN, EPI, NT>, grid, dim3(kThreads),
                           C::SMEM + ep_stage_bytes<EPI>(), st, mw, mx, g);

@@ -6,17 +6,19 @@
 // (oracle/verify_oracle.c) because both evaluate include/psd_canon.h in the
 // canonical order documented there.
 //
-// Two kernels, HBM-bound by design:
+// Two kernels per launch, HBM-bound by design:
 //   verify_stats<SAMPLE>  grid (slice, request*row): every active (row, slice)
 //       streams 8192 fp32 logits once with 128-bit L1-bypassing loads and
-//       produces (max, sum-exp) [sampling] or (max, argmax) [greedy] partials;
-//       the last CTA of each request (atomic ticket) folds the slices, runs the
-//       accept test of all k drafts at once (one lane per draft, __ballot_sync
-//       finds the first rejection) and writes the accepted prefix.  Greedy is
-//       done after this kernel.
-//   verify_sample         grid (1024-block, request): block sums of the
-//       residual max(0, p - q) (or p for the bonus), the last CTA per request
-//       does the normalised prefix search and writes the final token.
+//       produces the canonical (max, sum-exp) [sampling] or (max, argmax)
+//       [greedy] partial.
+//   greedy:   verify_fold, one CTA per request: folds the slices, tests all k
+//       drafts at once (one lane per draft, __ballot_sync finds the first
+//       rejection), writes the accepted prefix and the bonus token.
+//   sampling: verify_sample, grid (8-block chunk, request): each CTA folds and
+//       decides for its request, then sums its chunk's 1024-element blocks of
+//       the residual max(0, p - q) (or p for the bonus); the last chunk of a
+//       request (atomic ticket) does the normalised prefix search and writes
+//       the sampled token.
 // Algorithmic bytes: greedy 4V*sum(k_b+1); sampling
 // 4V*sum(2k_b+1) (+ small terms).  The sampling pass re-reads one (t, d) row
 // pair per request (mostly from L2).
@@ -48,8 +50,8 @@ struct Params {
   const int32_t* ids; const int32_t* len; const float* u;
   float c; int B, K;  // c = psd_scale(1/T)
   int32_t* acc; int32_t* out;
-  int* cnt_a; int* cnt_b;
-  float2* part; Plan* plan; float* wblk;
+  int* cnt_b;
+  float2* part; float* wblk;
   int NS, NB, R;
   // cached softmax statistics (M, S) of the draft rows: row (b, i) at
   // d_stats[d_rows[b] * d_stats_ld + i].  The draft sampler computed them with
@@ -152,42 +154,17 @@ __device__ __forceinline__ float shfl_add_tree(float v) {
   return v;
 }
 
-// number of stats CTAs request b launches work in
-__device__ __forceinline__ int expected_stats(const Params& p, int kb, bool sample) {
-  const int nst = (p.V + PSD_SLICE - 1) / PSD_SLICE;
-  const int nsd = (p.Vd + PSD_SLICE - 1) / PSD_SLICE;
-  return nst * (kb + 1) + (sample && !p.d_stats ? nsd * kb : 0);
-}
 
-// one (request b, row r, slice) statistics item; the last item of request b
-// folds and decides (and, sampling, publishes the plan of the sampling pass)
+// ---- statistics of one 8192-logit slice held in registers ------------------
+// Thread `tid` holds the canonical float4 vectors tid + 256 j (j = 0..7) of
+// the slice starting at element `base` of a row of n logits.  Returns, valid on
+// thread 0 only, the slice partial: (max, canonical exp2 sum) when SAMPLE, else
+// (max, first index attaining it as int bits).  Two __syncthreads; the shared
+// scratch may be reused by the next call right after it returns.
 template <bool SAMPLE>
-__device__ __forceinline__ void stats_item(const Params& p, int slice, int b, int r) {
-  const int kb = p.len[b];
-  const bool is_draft = r > p.K;
-  const int i = is_draft ? r - (p.K + 1) : r;
-  const int n = is_draft ? p.Vd : p.V;
-  const bool active = (is_draft ? i < kb && !p.d_stats : i <= kb) && slice * PSD_SLICE < n;
-  if (!active) return;
-  const int db = p.d_rows ? p.d_rows[b] : b;
-  const float* row = is_draft ? p.d + db * p.dsb + i * p.dsi : p.t + b * p.tsb + i * p.tsi;
+__device__ __forceinline__ float2 slice_partial(const float4 (&v)[8], int base, int n, float c) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int base = slice * PSD_SLICE;
-
-  // every slice but a row's last is full: no per-element bounds checks there
   const bool full = base + PSD_SLICE <= n;
-  float4 v[8];
-  if (full) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = ld_stream(row + base + 4 * (tid + kThreads * j));
-  } else {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int e = base + 4 * (tid + kThreads * j);
-      v[j] = e < n ? ld_stream(row + e)
-                   : make_float4(PSD_NEG_INF, PSD_NEG_INF, PSD_NEG_INF, PSD_NEG_INF);
-    }
-  }
   // exact slice max: lane -> warp (xor tree) -> block
   float lm = PSD_NEG_INF;
 #pragma unroll
@@ -199,21 +176,20 @@ __device__ __forceinline__ void stats_item(const Params& p, int slice, int b, in
   __shared__ float s_max[kThreads / 32];
   __shared__ float s_sum[kThreads / 32];
   __shared__ int s_idx[kThreads / 32];
-  __shared__ int s_last;
   if (lane == 0) s_max[warp] = wm;
   __syncthreads();
   float M = s_max[0];
 #pragma unroll
   for (int q = 1; q < kThreads / 32; ++q) M = psd_max(M, s_max[q]);
-
+  float2 res = make_float2(M, 0.0f);
   if constexpr (SAMPLE) {
-    const float bias = psd_bias(M, p.c);
-    const unsigned long long c2 = f2_pack(p.c, p.c), b2 = f2_pack(bias, bias);
+    const float bias = psd_bias(M, c);
+    const unsigned long long c2 = f2_pack(c, c), b2 = f2_pack(bias, bias);
     float s = 0.0f;
     auto lane_sum = [&](bool check) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        // invalid elements (-inf) are not part of the row: skip them
+        // elements past the row end (-inf or stale) are not part of it: skip
         const int e = base + 4 * (tid + kThreads * j);
         if (!check || e < n) {
           float wx, wy, wz, ww;
@@ -239,7 +215,7 @@ __device__ __forceinline__ void stats_item(const Params& p, int slice, int b, in
       for (int off = 4; off >= 1; off >>= 1)
 #pragma unroll
         for (int q = 0; q < off; ++q) w[q] = psd_add(w[q], w[q + off]);
-      p.part[(b * p.R + r) * p.NS + slice] = make_float2(M, w[0]);
+      res.y = w[0];
     }
   } else {
     // first (lowest) index attaining M
@@ -248,10 +224,12 @@ __device__ __forceinline__ void stats_item(const Params& p, int slice, int b, in
 #pragma unroll
       for (int j = 7; j >= 0; --j) {
         const int e = base + 4 * (tid + kThreads * j);
-        if (v[j].w == M) idx = e + 3;
-        if (v[j].z == M) idx = e + 2;
-        if (v[j].y == M) idx = e + 1;
-        if (v[j].x == M) idx = e;
+        if (e < n) {
+          if (v[j].w == M) idx = e + 3;
+          if (v[j].z == M) idx = e + 2;
+          if (v[j].y == M) idx = e + 1;
+          if (v[j].x == M) idx = e;
+        }
       }
     }
 #pragma unroll
@@ -262,20 +240,23 @@ __device__ __forceinline__ void stats_item(const Params& p, int slice, int b, in
       int w = s_idx[0];
 #pragma unroll
       for (int q = 1; q < 8; ++q) w = min(w, s_idx[q]);
-      p.part[(b * p.R + r) * p.NS + slice] = make_float2(M, __int_as_float(w));
+      res.y = __int_as_float(w);
     }
   }
+  return res;
+}
 
-  // ---- last CTA of request b: fold slices, decide --------------------------
-  if (tid == 0) {
-    __threadfence();
-    const int ticket = atomicAdd(p.cnt_a + b, 1);
-    s_last = ticket == expected_stats(p, kb, SAMPLE) - 1;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-
+// ---- fold + decision of request b -------------------------------------------
+// Run by every thread of one CTA once all of b's slice partials are published
+// (the statistics kernel completed).  Folds each row's slices left to right,
+// tests all k_b drafts at once (lane i tests draft i; the first zero bit of the
+// ballot is the first rejection) and returns, in shared memory, the plan of
+// the sampling pass.  `publish`: this CTA writes accepted_len, the accepted
+// tokens (and the greedy bonus token) and the target-row statistics.
+template <bool SAMPLE>
+__device__ void fold_decide(const Params& p, int b, bool publish, Plan* s_plan) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kb = p.len[b];
   __shared__ float2 s_part[(2 * PSD_MAX_K + 1) * PSD_MAX_SLICES];
   __shared__ float sMt[PSD_MAX_K + 1], sSt[PSD_MAX_K + 1], sMd[PSD_MAX_K], sSd[PSD_MAX_K];
   __shared__ int sG[PSD_MAX_K + 1];
@@ -314,7 +295,6 @@ __device__ __forceinline__ void stats_item(const Params& p, int slice, int b, in
   }
   __syncthreads();
   if (warp == 0) {
-    // lane i tests draft i; first rejection = first zero bit of the ballot
     bool ok = false;
     const int x = lane < kb ? p.ids[b * p.K + lane] : -1;
     if (lane < kb) {
@@ -334,17 +314,21 @@ __device__ __forceinline__ void stats_item(const Params& p, int slice, int b, in
     const unsigned rej = __ballot_sync(0xffffffffu, !ok) & ((1u << kb) - 1u);
     int a = rej ? __ffs(rej) - 1 : kb;
     if (p.forced) a = min(max(__ldg(p.forced + b), 0), kb);
-    int32_t* o = p.out + b * (p.K + 1);
-    if (lane <= p.K) o[lane] = lane < a ? x : (!SAMPLE && lane == a ? sG[a] : -1);
-    if (lane == 0) {
-      p.acc[b] = a;
-      if (p.t_stats_out) {
-        const int dst = p.t_stats_rows[b];
+    if (publish) {
+      int32_t* o = p.out + b * (p.K + 1);
+      if (lane <= p.K) o[lane] = lane < a ? x : (!SAMPLE && lane == a ? sG[a] : -1);
+      if (lane == 0) {
+        p.acc[b] = a;
         if constexpr (SAMPLE) {
-          if (dst >= 0) p.t_stats_out[dst] = make_float2(sMt[0], sSt[0]);
+          if (p.t_stats_out) {
+            const int dst = p.t_stats_rows[b];
+            if (dst >= 0) p.t_stats_out[dst] = make_float2(sMt[0], sSt[0]);
+          }
         }
       }
-      if constexpr (SAMPLE) {
+    }
+    if constexpr (SAMPLE) {
+      if (lane == 0) {
         Plan pl;
         pl.row = a;
         pl.Mt = sMt[a]; pl.St = sSt[a];
@@ -352,19 +336,59 @@ __device__ __forceinline__ void stats_item(const Params& p, int slice, int b, in
         pl.Md = a < kb ? sMd[a] : 0.0f;
         pl.Sd = a < kb ? sSd[a] : 0.0f;
         pl.pad[0] = pl.pad[1] = 0;
-        p.plan[b] = pl;
+        *s_plan = pl;
       }
-      p.cnt_a[b] = 0;  // self-cleaning ticket for the next launch
     }
   }
+  __syncthreads();
 }
 
+// ---- statistics pass ----------------------------------------------------------
+// One (request b, row r, slice) item per CTA: 8192 logits streamed once with
+// 128-bit L1-bypassing loads (all eight vectors of a thread in flight at once),
+// the canonical slice partial written to the workspace.  No completion
+// tracking: the fold / decision runs in the next kernel (verify_fold, or
+// inside verify_sample), which a stream (PDL) dependency orders after this
+// one.  Measured against the ticketed variant (the last CTA of a request folds
+// and decides) and a persistent TMA-bulk-copy variant: profiles/r02_k1_variants.txt.
 template <bool SAMPLE>
 __global__ void __launch_bounds__(kThreads)
 verify_stats(const Params p) {
   pdl_wait();
   pdl_trigger();
-  stats_item<SAMPLE>(p, blockIdx.x, blockIdx.y / p.R, blockIdx.y % p.R);
+  const int slice = blockIdx.x, b = blockIdx.y / p.R, r = blockIdx.y % p.R;
+  const int kb = p.len[b];
+  const bool is_draft = r > p.K;
+  const int i = is_draft ? r - (p.K + 1) : r;
+  const int n = is_draft ? p.Vd : p.V;
+  const bool active = (is_draft ? i < kb && !p.d_stats : i <= kb) && slice * PSD_SLICE < n;
+  if (!active) return;
+  const int db = p.d_rows ? p.d_rows[b] : b;
+  const float* row = is_draft ? p.d + db * p.dsb + i * p.dsi : p.t + b * p.tsb + i * p.tsi;
+  const int tid = threadIdx.x;
+  const int base = slice * PSD_SLICE;
+  float4 v[8];
+  if (base + PSD_SLICE <= n) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = ld_stream(row + base + 4 * (tid + kThreads * j));
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int e = base + 4 * (tid + kThreads * j);
+      v[j] = e < n ? ld_stream(row + e)
+                   : make_float4(PSD_NEG_INF, PSD_NEG_INF, PSD_NEG_INF, PSD_NEG_INF);
+    }
+  }
+  const float2 part = slice_partial<SAMPLE>(v, base, n, p.c);
+  if (tid == 0) p.part[(b * p.R + r) * p.NS + slice] = part;
+}
+
+// greedy: fold + decide, one CTA per request
+__global__ void __launch_bounds__(kThreads)
+verify_fold(const Params p) {
+  pdl_wait();
+  pdl_trigger();
+  fold_decide<false>(p, blockIdx.x, true, nullptr);
 }
 
 // ---- sampling pass ---------------------------------------------------------
@@ -511,13 +535,11 @@ __device__ float seq_fold(const float* v, int n, float* prefix) {
 // one chunk of request b's sampling pass; the last chunk runs the prefix search
 __device__ __forceinline__ void sample_item(const Params& p, int chunk, int b, int nchunks) {
   const int tid = threadIdx.x;
-  Plan pl;
-  {
-    const float4* pp = reinterpret_cast<const float4*>(p.plan + b);
-    const float4 q0 = __ldcg(pp), q1 = __ldcg(pp + 1);
-    pl.mode = __float_as_int(q0.x); pl.row = __float_as_int(q0.y);
-    pl.Mt = q0.z; pl.St = q0.w; pl.Md = q1.x; pl.Sd = q1.y;
-  }
+  // every chunk CTA folds request b's statistics and decides (cheap, and no
+  // completion tracking in the statistics pass); chunk 0 publishes the result
+  __shared__ Plan s_plan;
+  fold_decide<true>(p, b, chunk == 0, &s_plan);
+  const Plan pl = s_plan;
   WeightCtx w;
   w.V = p.V; w.Vd = p.Vd; w.c = p.c;
   w.t = p.t + b * p.tsb + pl.row * p.tsi;
@@ -632,22 +654,27 @@ verify_sample(const Params p) {
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 
-cudaError_t launch_sampling(Params p, cudaStream_t st) {
-  dim3 grid(p.NS, p.B * p.R);
-  cudaError_t e = psd::launch(verify_stats<true>, grid, dim3(kThreads), 0, st, p);
-  if (e != cudaSuccess) return e;
-  const int nc = (p.NB + kChunkBlks - 1) / kChunkBlks;
-  return psd::launch(verify_sample, dim3(nc, p.B), dim3(kThreads), 0, st, p);
-}
-
 template <bool SAMPLE>
 cudaError_t launch_stats(const Params& p, cudaStream_t st) {
   dim3 grid(p.NS, p.B * p.R);
   return psd::launch(verify_stats<SAMPLE>, grid, dim3(kThreads), 0, st, p);
 }
 
+cudaError_t launch_greedy(const Params& p, cudaStream_t st) {
+  cudaError_t e = launch_stats<false>(p, st);
+  if (e != cudaSuccess) return e;
+  return psd::launch(verify_fold, dim3(p.B), dim3(kThreads), 0, st, p);
+}
+
+cudaError_t launch_sampling(const Params& p, cudaStream_t st) {
+  cudaError_t e = launch_stats<true>(p, st);
+  if (e != cudaSuccess) return e;
+  const int nc = (p.NB + kChunkBlks - 1) / kChunkBlks;
+  return psd::launch(verify_sample, dim3(nc, p.B), dim3(kThreads), 0, st, p);
+}
+
 struct WsLayout {
-  size_t cnt_a, cnt_b, part, plan, wblk, total;
+  size_t cnt_b, part, wblk, total;
 };
 
 WsLayout layout(int B, int K, int V, int Vd, int sampling) {
@@ -657,10 +684,8 @@ WsLayout layout(int B, int K, int V, int Vd, int sampling) {
   const int R = (K + 1) + (sampling ? K : 0);
   WsLayout L;
   size_t off = 0;
-  L.cnt_a = off; off = align_up(off + sizeof(int) * B);
   L.cnt_b = off; off = align_up(off + sizeof(int) * B);
   L.part = off; off = align_up(off + sizeof(float2) * (size_t)B * R * NS);
-  L.plan = off; off = align_up(off + sizeof(Plan) * (size_t)B);
   L.wblk = off; off = align_up(off + sizeof(float) * (size_t)B * NB);
   L.total = off;
   return L;
@@ -709,11 +734,11 @@ int psd_verify_greedy_forced(const float* target_logits, int64_t t_stride_b, int
   p.d = nullptr; p.Vd = 0; p.ids = draft_ids; p.len = draft_len; p.u = nullptr;
   p.c = psd_scale(1.0f); p.B = B; p.K = K; p.acc = accepted_len; p.out = out_tokens;
   p.forced = forced_len;
-  p.cnt_a = reinterpret_cast<int*>(w + L.cnt_a); p.cnt_b = reinterpret_cast<int*>(w + L.cnt_b);
-  p.part = reinterpret_cast<float2*>(w + L.part); p.plan = reinterpret_cast<Plan*>(w + L.plan);
+  p.cnt_b = reinterpret_cast<int*>(w + L.cnt_b);
+  p.part = reinterpret_cast<float2*>(w + L.part);
   p.wblk = reinterpret_cast<float*>(w + L.wblk);
   p.NS = (V + PSD_SLICE - 1) / PSD_SLICE; p.NB = (V + PSD_SBLK - 1) / PSD_SBLK; p.R = K + 1;
-  return (int)launch_stats<false>(p, (cudaStream_t)stream);
+  return (int)launch_greedy(p, (cudaStream_t)stream);
 }
 
 int psd_verify_sample(const float* target_logits, int64_t t_stride_b, int64_t t_stride_i, int V,
@@ -735,8 +760,8 @@ int psd_verify_sample(const float* target_logits, int64_t t_stride_b, int64_t t_
   p.d = draft_logits; p.dsb = d_stride_b; p.dsi = d_stride_i; p.Vd = Vd;
   p.ids = draft_ids; p.len = draft_len; p.u = uniforms;
   p.c = psd_scale(1.0f / temperature); p.B = B; p.K = K; p.acc = accepted_len; p.out = out_tokens;
-  p.cnt_a = reinterpret_cast<int*>(w + L.cnt_a); p.cnt_b = reinterpret_cast<int*>(w + L.cnt_b);
-  p.part = reinterpret_cast<float2*>(w + L.part); p.plan = reinterpret_cast<Plan*>(w + L.plan);
+  p.cnt_b = reinterpret_cast<int*>(w + L.cnt_b);
+  p.part = reinterpret_cast<float2*>(w + L.part);
   p.wblk = reinterpret_cast<float*>(w + L.wblk);
   p.NS = (V + PSD_SLICE - 1) / PSD_SLICE; p.NB = (V + PSD_SBLK - 1) / PSD_SBLK;
   p.R = 2 * K + 1;
@@ -800,8 +825,8 @@ int psd_verify_sample_forced(const float* target_logits, int64_t t_stride_b, int
   p.forced = forced_len;
   p.ids = draft_ids; p.len = draft_len; p.u = uniforms;
   p.c = psd_scale(1.0f / temperature); p.B = B; p.K = K; p.acc = accepted_len; p.out = out_tokens;
-  p.cnt_a = reinterpret_cast<int*>(w + L.cnt_a); p.cnt_b = reinterpret_cast<int*>(w + L.cnt_b);
-  p.part = reinterpret_cast<float2*>(w + L.part); p.plan = reinterpret_cast<Plan*>(w + L.plan);
+  p.cnt_b = reinterpret_cast<int*>(w + L.cnt_b);
+  p.part = reinterpret_cast<float2*>(w + L.part);
   p.wblk = reinterpret_cast<float*>(w + L.wblk);
   p.NS = (V + PSD_SLICE - 1) / PSD_SLICE; p.NB = (V + PSD_SBLK - 1) / PSD_SBLK;
   p.R = 2 * K + 1;

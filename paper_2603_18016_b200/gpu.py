@@ -237,6 +237,9 @@ class GpuBackend:
         self.graph_streams: list = []
         self.graph_launches: dict[tuple, int] = {}
         self.launches = 0  # kernels of libpsd.so executed (graph replays included)
+        # bytes this backend copied host -> device / device -> host (e2e accounting)
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
         self.slots: dict[int, int] = {}
         self.free_slots = list(range(max_requests - 1, -1, -1))
         self.pending_k: dict[int, int] = {}
@@ -340,6 +343,7 @@ class GpuBackend:
         req = state.requests[rid]
         n = req.generated
         req.output_ids = self.outputs[s, :n].cpu().tolist()
+        self.d2h_bytes += 4 * n
         self.free_slots.append(s)
         self.pending_k.pop(rid, None)
 
@@ -364,6 +368,7 @@ class GpuBackend:
             bt[s, :len(blocks)] = blocks
             self.nblk[s] = len(blocks)
         self.block_table.copy_(self.block_table_host, non_blocking=True)
+        self.h2d_bytes += self.block_table_host.numel() * 4
 
     def _admit(self, state, ids) -> None:
         """Assign slots and initialise slot tokens for new requests."""
@@ -390,6 +395,7 @@ class GpuBackend:
         dev = self.device
         stage = torch.from_numpy(np.concatenate([idx, val])).pin_memory().to(dev,
                                                                             non_blocking=True)
+        self.h2d_bytes += stage.numel() * 4
         st = torch.cuda.current_stream(dev).cuda_stream
         lib = native.load()
         native.check(lib.psd_index_copy_i32(self.slot_tok.data_ptr(), stage.data_ptr(),
@@ -399,6 +405,7 @@ class GpuBackend:
         if reset_generated:
             sl = torch.tensor([t[0] for t in triples], dtype=torch.int64)
             self.generated[sl.to(dev)] = 0
+            self.h2d_bytes += 8 * len(triples)
 
     def _set_slot_values(self, pairs) -> None:
         """slot_tok.view(-1)[flat] = value for (flat, value) pairs (draft ids
@@ -408,6 +415,7 @@ class GpuBackend:
             return
         arr = np.asarray(pairs, dtype=np.int32).T.reshape(-1)
         stage = torch.from_numpy(arr).pin_memory().to(self.device, non_blocking=True)
+        self.h2d_bytes += stage.numel() * 4
         st = torch.cuda.current_stream(self.device).cuda_stream
         native.check(native.load().psd_index_copy_i32(
             self.slot_tok.data_ptr(), stage.data_ptr(), stage[n:].data_ptr(), None, n, st),
@@ -591,6 +599,7 @@ class GpuBackend:
             for i in range(kmax):
                 kh[2 * B + i * B:2 * B + i * B + nb] = np.where(real & (i < k), sl * K + i, -1)
             self.d_key.copy_(self.d_key_host[self.d_key_cur], non_blocking=True)
+            self.h2d_bytes += self.d_key.numel() * 4
             ev = torch.cuda.Event()
             ev.record()
             self.d_key_events[self.d_key_cur] = ev
@@ -702,11 +711,13 @@ class GpuBackend:
             vm[3 * B:3 * B + nb * kmax] = (sl[:, None] * ldt + 2 + np.arange(kmax)[None, :]
                                            ).reshape(-1)
         self.v_meta.copy_(self.v_meta_host, non_blocking=True)
+        self.h2d_bytes += self.v_meta_host.numel() * 4
         if self.mode == "sample":
             kh = self.v_key_host.numpy()
             kh[:nb] = [r.request_id for r in rows] + [0] * (nb - n)
             kh[B:B + nb] = L
             self.v_key.copy_(self.v_key_host, non_blocking=True)
+            self.h2d_bytes += self.v_key_host.numel() * 4
         capped = beside_draft and self.verify_ctas > 0
         self._run_graph(("verify", nb, kmax, capped, self.replay),
                         lambda: self._verify_launch(nb, kmax, capped))
@@ -784,6 +795,16 @@ class GpuBackend:
                                     self.max_out, st), "commit")
         self.acc_host[:nb].copy_(self.v_acc[:nb], non_blocking=True)
         self.out_host[:nb * K1].copy_(self.v_out[:nb * K1], non_blocking=True)
+        self.d2h_bytes += 4 * nb * (K1 + 1)
+
+    def transfer_bytes(self) -> tuple[int, int]:
+        """(host -> device, device -> host) bytes copied so far, the forwards'
+        metadata uploads included."""
+        h2d = self.h2d_bytes
+        for f in (getattr(self, "tfwd", None), getattr(self, "dfwd", None)):
+            if f is not None:
+                h2d += f.h2d_bytes
+        return h2d, self.d2h_bytes
 
     # ------------------------------------------------------------------
     def execute(self, state: EngineState, plan: StepPlan, rows: list[VerifyRow]) -> StepResult:

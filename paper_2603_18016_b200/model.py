@@ -393,6 +393,7 @@ class Forward:
         # widest per-sequence query count that takes the fused path
         self.fuse_rope_max_q = int(os.environ.get("PSD_FUSED_ROPE_MAXQ", "2"))
         self.meta = torch.zeros(sets, o, dtype=torch.int32, device=dev)
+        self.h2d_bytes = 0  # metadata bytes uploaded (GpuBackend.transfer_bytes)
         # ring of pinned staging buffers: an async H2D copy reads its buffer
         # when it executes, so a buffer is rewritten only after its copy ran
         self.ring = 4
@@ -441,6 +442,7 @@ class Forward:
     def upload(self, n_sets: int = 1) -> None:
         """Copy staged sets 0..n_sets-1 to the device on the current stream."""
         self.meta[:n_sets].copy_(self.meta_host[self._cur, :n_sets], non_blocking=True)
+        self.h2d_bytes += n_sets * self.meta_host.shape[2] * 4
         ev = torch.cuda.Event()
         ev.record()
         self._events[self._cur] = ev

@@ -5,8 +5,9 @@
 Algorithmic bytes per launch:
   greedy   4 V sum_b(k_b+1) + 4 B k + 4 B (k+2)
   sampling 4 V sum_b(2 k_b+1) + 4 B (k+1) + 4 B k + 4 B (k+2)
-Timing: CUDA events on the launching stream, median of N launches, L2 flushed
-(a 256 MiB write) before every timed launch.
+Timing: K1 behind an L2 flush (a 256 MiB write), ten of each captured in a
+CUDA graph; K1 time = (graph time - flush-only graph time) / 10, CUDA events,
+median of several replays.
 """
 
 from __future__ import annotations
@@ -43,35 +44,81 @@ def make_inputs(B, K, V, sampling, device, seed=0):
     return t, d, ids, ln, u
 
 
-def time_verify(B, K, V, sampling, iters=30, device="cuda", flush=True):
+def time_verify(B, K, V, sampling, iters=30, device="cuda", flush=True, cached=False):
+    """Median device time of one K1 launch (both kernels when sampling).
+
+    Ten (L2 flush, K1) pairs are captured in one CUDA graph and ten flushes
+    in another; K1's time is the difference of the two replays / 10 (median
+    of several), so it excludes host launch latency and includes the
+    in-graph launch gap, as in the PSD loop.  cached: the draft rows'
+    (max, sum) come from the draft sampler (psd_verify_sample_ext), so K1
+    streams the target rows only."""
     dev = torch.device(device)
     t, d, ids, ln, u = make_inputs(B, K, V, sampling, dev)
     scratch = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush else None
+    stats = None
+    if cached and sampling and K:
+        stats = torch.empty(B, K, 2, device=dev)
+        rows = d.reshape(B * K, 1, V)
+        ops.verify_sample(rows, rows[:, :0], torch.zeros(B * K, 0, dtype=torch.int32,
+                                                         device=dev),
+                          torch.zeros(B * K, dtype=torch.int32, device=dev),
+                          torch.rand(B * K, 1, device=dev), t_stats_out=stats.view(B * K, 2),
+                          t_stats_rows=torch.arange(B * K, dtype=torch.int32, device=dev))
 
     def launch():
         if sampling:
-            ops.verify_sample(t, d, ids, ln, u)
+            ops.verify_sample(t, d, ids, ln, u, d_stats=stats)
         else:
             ops.verify_greedy(t, ids, ln)
 
-    for _ in range(3):
-        launch()
+    # warm up on the capture stream: the workspace (keyed by stream) exists
+    # before capture, so the graphs hold the kernels only
+    s = torch.cuda.Stream(device=dev)
+    s.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            launch()
     torch.cuda.synchronize()
-    times = []
-    for _ in range(iters):
-        if flush:
-            scratch.fill_(1)
+    reps = 10
+
+    def capture(with_k1):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
+            for _ in range(reps):
+                if flush:
+                    scratch.fill_(1)
+                if with_k1:
+                    launch()
+        return g
+
+    g_k1, g_flush = capture(True), capture(False)
+
+    def timed(g):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        launch()
+        g.replay()
         e1.record()
         torch.cuda.synchronize()
-        times.append(e0.elapsed_time(e1))
+        return e0.elapsed_time(e1)
+    times = []
+    for _ in range(max(3, iters // reps)):
+        times.append((timed(g_k1) - timed(g_flush)) / reps)
     ms = statistics.median(times)
     nbytes = algorithmic_bytes(B, K, V, sampling)
-    return {"B": B, "k": K, "V": V, "mode": "sampling" if sampling else "greedy",
-            "us": ms * 1e3, "bytes": nbytes, "GBps": nbytes / (ms * 1e-3) / 1e9}
+    r = {"B": B, "k": K, "V": V, "mode": "sampling" if sampling else "greedy",
+         "us": ms * 1e3, "bytes": nbytes, "GBps": nbytes / (ms * 1e-3) / 1e9}
+    if stats is not None:
+        r["mode"] = "sampling_cached_q"
+        r["bytes_streamed"] = algorithmic_bytes(B, K, V, False)
+        r["GBps_streamed"] = r["bytes_streamed"] / (ms * 1e-3) / 1e9
+    return r
+
+
+# where the PSD loop runs K1 with the draft sampler's cached q statistics (cfg2,
+# cfg3 shapes)
+CACHED_POINTS = {(32, 5, 128256), (32, 4, 152064)}
 
 
 def sweep(quick: bool):
@@ -86,6 +133,8 @@ def sweep(quick: bool):
     for B, K, V in pts:
         for sampling in (False, True):
             out.append(time_verify(B, K, V, sampling))
+        if K and (B, K, V) in CACHED_POINTS:
+            out.append(time_verify(B, K, V, True, cached=True))
     return out
 
 
