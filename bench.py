@@ -159,6 +159,18 @@ def _ncu_traffic(key: str):
         return None
 
 
+def _sk_physical(dev, cap: int) -> int:
+    """CTAs a stream-K GEMM runs on under a CTA cap (gemm.cu sk_physical): the
+    work is split over one virtual CTA per SM whatever the cap, and each
+    physical CTA takes the same number of virtual ones."""
+    import torch
+    G = torch.cuda.get_device_properties(dev).multi_processor_count
+    if cap <= 0 or cap >= G:
+        return G
+    per = -(-G // cap)
+    return -(-G // per)
+
+
 def kernel_rooflines(backend, hbm_peak: float, bf16_peak: float) -> tuple[dict, dict]:
     """Dominant kernel (verify-forward gate/up GEMM) and K1 at the workload shapes."""
     import torch
@@ -212,7 +224,8 @@ def kernel_rooflines(backend, hbm_peak: float, bf16_peak: float) -> tuple[dict, 
             "bytes_per_launch": nbytes, "us_per_launch": round(ms * 1e3, 2),
             "tflops": round(flops / (ms * 1e-3) / 1e12, 1),
             "timing": "alone, all SMs, back-to-back launches rotating over every layer's weights",
-            "psd_step_config": ({"ctas": cap, "us_per_launch": round(ms_cap * 1e3, 2),
+            "psd_step_config": ({"cta_cap": cap, "ctas": _sk_physical(dev, cap),
+                                 "us_per_launch": round(ms_cap * 1e3, 2),
                                  "GBps": round(nbytes / (ms_cap * 1e-3) / 1e9, 1),
                                  "frac": round(nbytes / (ms_cap * 1e-3) / 1e9 / hbm_peak, 4),
                                  "note": "CTA cap of the verify GEMMs in overlapped PSD steps, "
@@ -274,6 +287,27 @@ def kernel_rooflines(backend, hbm_peak: float, bf16_peak: float) -> tuple[dict, 
               "GBps_streamed": round(read_c / (ms3 * 1e-3) / 1e9, 1),
               "frac_streamed": round(read_c / (ms3 * 1e-3) / 1e9 / hbm_peak, 4)}}
     return roof, vk
+
+
+def verify_sweep_summary(hbm_peak: float) -> dict:
+    """K1 over a grid of BASELINE config 5 (batch x k x vocab, greedy and
+    sampling; verify_bench.time_verify: L2 flushed, inside CUDA graphs):
+    min / median fraction of the HBM peak.  The full 500-point sweep is
+    profiles/r02_verify_sweep.txt."""
+    import statistics as stt
+    from paper_2603_18016_b200.verify_bench import time_verify
+    pts = [(B, K, V) for B in (8, 64, 512) for K in (1, 4, 8) for V in (32000, 262144)]
+    rows = {"greedy": [], "sampling": []}
+    for B, K, V in pts:
+        for sampling in (False, True):
+            r = time_verify(B, K, V, sampling, iters=20)
+            rows[r["mode"]].append((B, K, V, round(r["GBps"] / hbm_peak, 4)))
+    out = {"grid": "B {8, 64, 512} x k {1, 4, 8} x V {32000, 262144}", "peak_GBps": hbm_peak}
+    for mode, rs in rows.items():
+        fr = [x[3] for x in rs]
+        out[mode] = {"min_frac": min(fr), "median_frac": round(stt.median(fr), 4),
+                     "max_frac": max(fr), "points": rs}
+    return out
 
 
 def draft_hiding(states) -> dict:
@@ -424,17 +458,85 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+def replica_sd(args, rank, world, dev, barrier) -> dict:
+    """SD(2m) with every rank an independent target + draft replica, timed
+    like the main modes (warm-up, barrier, CUDA events, max over ranks)."""
+    import torch
+
+    from paper_2603_18016_b200 import dist as pd
+    from paper_2603_18016_b200 import run
+    from paper_2603_18016_b200.gpu import GpuBackend
+    be = GpuBackend(CFG["target"], CFG["draft"], max_requests=CFG["n_requests"],
+                    max_batch=CFG["n_requests"], k_max=CFG["k"],
+                    max_seq_len=CFG["prompt"] + CFG["output"] + 16, seed=rank // 2,
+                    beta_target=BETA_TARGET, beta_draft=BETA_DRAFT, device=dev,
+                    mode="sample" if args.workload == "cfg3" else "greedy", temperature=1.0)
+    for _ in range(args.warmup):
+        run(_config("standard-sd"), _workload(rank), backend=be)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    tok = 0
+    for _ in range(args.steps):
+        _, rep = run(_config("standard-sd"), _workload(rank), backend=be)
+        tok += rep.total_generated
+    e1.record()
+    barrier()
+    tokens, ms = pd.aggregate(tok, e0.elapsed_time(e1), dev)
+    del be
+    torch.cuda.empty_cache()
+    return {"value": round(tokens / (ms * 1e-3), 1), "unit": "tok/s",
+            "mode": f"standard-sd (sd_batch_factor 2), {world} independent replicas, target "
+                    "+ draft on every GPU"}
+
+
+def pair_model(psd: dict, sdm: dict, sd: dict, steps: int) -> dict:
+    """One-GPU model of the dedicated-draft-GPU pair (SURVEY §7 hard part 1),
+    from this run's isolated phase timings: SD(m) steps draft then verify one
+    batch of m alone on the GPU, so its per-step draft and verify times are
+    what each GPU of a pair would spend.  A pair's PSD step = max(draft,
+    verify) (+ the id hand-off, ~0.1 ms over NVLink, neglected); the baselines
+    on the same two GPUs are SD with the draft on its own GPU (draft + verify
+    per step) and two SD(2m) replicas."""
+    if not sdm["steps"]:
+        return {}
+    d = sdm["draft_ms"] / sdm["steps"]
+    v = sdm["verify_ms"] / sdm["steps"]
+    tok_pass = psd["tokens"] / steps
+    psd_steps = psd["steps"] / steps
+    sdm_steps = sdm["steps"] / steps
+    t_psd = psd_steps * max(d, v) * 1e-3
+    t_sdd = sdm_steps * (d + v) * 1e-3
+    rep2 = 2 * sd["tokens"] / (sd["ms"] * 1e-3)
+    return {"draft_ms_per_step": round(d, 3), "verify_ms_per_step": round(v, 3),
+            "psd_pair_tok_s": round(tok_pass / t_psd, 1),
+            "sd_dedicated_draft_tok_s": round(tok_pass / t_sdd, 1),
+            "sd2m_two_replicas_tok_s": round(rep2, 1),
+            "psd_pair_vs_sd_dedicated_draft": round(t_sdd / t_psd, 4),
+            "psd_pair_vs_sd2m_two_replicas": round(tok_pass / t_psd / rep2, 4),
+            "note": "model from isolated one-GPU phase times (SD(m) steps), not a 2-GPU "
+                    "measurement"}
+
+
 def run_ours(args) -> None:
     import torch
 
     from paper_2603_18016_b200 import dist as pd
-    world, rank, local = pd.init("nccl")
+    world, rank, local = pd.init(args.dist_backend)
+    # --dist-backend gloo with more ranks than GPUs (a smoke run of the pair
+    # protocol on one GPU) shares the devices round-robin
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     from paper_2603_18016_b200 import mean_accepted_length, run
     from paper_2603_18016_b200.gpu import GpuBackend
 
     hbm_peak, bf16_peak, peak_kind = _peaks()
+    if args.layout == "auto":
+        # PSD's structural gain needs the draft on its own GPU (PAPER.md:407):
+        # even N runs N/2 (target GPU, draft GPU) pairs; N = 1 (or odd) runs
+        # target + draft on each GPU, two streams
+        args.layout = "pairs" if world >= 2 and world % 2 == 0 else "replicas"
     pairs = args.layout == "pairs"
     tp_layout = args.layout == "tp"
     global BETA_TARGET, BETA_DRAFT
@@ -465,7 +567,7 @@ def run_ours(args) -> None:
         from paper_2603_18016_b200.pair import (DraftServer, GpuDraftEngine, GpuTargetEngine,
                                                 PairLink, PairTarget)
         peer = rank + 1 if rank % 2 == 0 else rank - 1
-        link = PairLink(peer, dev)
+        link = PairLink(peer, dev if args.dist_backend == "nccl" else None)
         if not is_draft_rank:
             backend = PairTarget(GpuTargetEngine(be), link)
 
@@ -532,17 +634,23 @@ def run_ours(args) -> None:
     barrier()
     if is_draft_rank:
         DraftServer(GpuDraftEngine(be), link).serve()
+    else:
+        x0 = be.transfer_bytes()
+        t0 = time.perf_counter()
+        st, rep_e2e = one("psd")
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        x1 = be.transfer_bytes()
+        if pairs:
+            backend.stop()
+    # the other baseline on the same GPUs: every GPU an independent SD(2m)
+    # replica (target + draft on one GPU, its own 64 requests)
+    sd_rep = replica_sd(args, rank, world, dev, barrier) if pairs else None
+    if is_draft_rank:
         pd.finalize()
         return
-    x0 = be.transfer_bytes()
-    t0 = time.perf_counter()
-    st, rep_e2e = one("psd")
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
-    x1 = be.transfer_bytes()
-    if pairs:
-        backend.stop()
     roof, vk = kernel_rooflines(be, hbm_peak, bf16_peak)
+    vsweep = verify_sweep_summary(hbm_peak) if rank == 0 and not args.no_sweep else None
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -602,19 +710,25 @@ def run_ours(args) -> None:
                    "l2": "inputs > L2 (weights 18.5 GB streamed per step)",
                    "synthetic_language_beta": [BETA_TARGET, BETA_DRAFT]},
         "sd": {"value": round(sd_value, 1), "unit": "tok/s",
-               "mode": "standard-sd, one batch of 64 (sd_batch_factor 2)",
+               "mode": ("standard-sd with the draft on its own GPU (the paper's baseline), "
+                        if pairs else "standard-sd, ") + "one batch of 64 (sd_batch_factor 2)",
                "steps_per_pass": steps_sd,
                "draft_ms_per_pass": round(sd["draft_ms"] / args.steps, 2),
                "verify_ms_per_pass": round(sd["verify_ms"] / args.steps, 2),
                "gpu_launches": launches.get("standard-sd")},
         "sd_m": {"value": round(sdm["tokens"] / (sdm["ms"] * 1e-3), 1), "unit": "tok/s",
-                 "mode": "standard-sd, batches of m=32 (sd_batch_factor 1), the PSD batch size"},
+                 "mode": ("standard-sd with the draft on its own GPU, " if pairs else
+                          "standard-sd, ") + "batches of m (sd_batch_factor 1), the PSD batch "
+                                             "size"},
         "psd_ktune": ({"value": round(results["psd-ktune"]["tokens"]
                                       / (results["psd-ktune"]["ms"] * 1e-3), 1),
                        "unit": "tok/s", "final_k": tuners[-1].k if tuners else None,
                        "p_est": round(tuners[-1].p, 4) if tuners and tuners[-1].p else None}
                       if "psd-ktune" in results and results["psd-ktune"] else None),
         "psd_vs_sd": round(value / sd_value, 4),
+        "sd_replicas": sd_rep,
+        "psd_vs_sd_replicas": (round(value / sd_rep["value"], 4) if sd_rep else None),
+        "pair_model": (pair_model(psd, sdm, sd, args.steps) if world == 1 else None),
         "psd_vs_sd_m": round(value / (sdm["tokens"] / (sdm["ms"] * 1e-3)), 4),
         "greedy_identical": ident,
         "mean_accepted_len": round(mean_accepted_length(r0), 4),
@@ -634,6 +748,7 @@ def run_ours(args) -> None:
         "clocks": psd["clocks"],
         "roofline": dict(roof, peak_kind=peak_kind),
         "verify_kernel": vk,
+        "verify_sweep": vsweep,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
@@ -647,13 +762,19 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="torch.distributed backend (gloo: host transport, for a smoke run "
+                         "of the multi-rank layouts on one GPU)")
+    ap.add_argument("--no-sweep", action="store_true",
+                    help="skip the config-5 verify-kernel grid (verify_sweep)")
     ap.add_argument("--ktune", action="store_true",
                     help="also run PSD with the online draft-depth tuner (ktune.KTuner)")
     ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3"],
                     help="cfg2: 8B / 1B greedy (the headline); cfg3: Qwen2.5-7B / 0.5B, "
                          "T = 1.0 rejection sampling over the 152k vocabulary")
-    ap.add_argument("--layout", default="replicas", choices=["replicas", "pairs", "tp"],
-                    help="replicas: each GPU runs target+draft (two streams); pairs: "
+    ap.add_argument("--layout", default="auto", choices=["auto", "replicas", "pairs", "tp"],
+                    help="auto: pairs for an even number of GPUs, else replicas; "
+                         "replicas: each GPU runs target+draft (two streams); pairs: "
                          "dedicated draft GPU per target GPU (NCCL hand-off, pair.py); tp: "
                          "BASELINE config 4, 70B target tensor-parallel over all GPUs")
     args = ap.parse_args()

@@ -220,6 +220,37 @@ int psd_copy_rows_f32(float* dst, const int32_t* dst_rows, int64_t dst_ld, const
 int psd_gather_rows_f32(float* dst, int64_t dst_ld, const float* src, const int32_t* src_rows,
                         int64_t src_ld, int nrows, int ncols, void* stream);
 
+/* ---- C1 / C2: peer-memory communicator (NVLink / NVSwitch load-stores) ---
+ * Replaces the scalar `comm_overhead` the reference adds to a PSD step
+ * (pkg/src/specsim/request_model.py:128; engine.py:435-442) with the real
+ * exchanges: the row-parallel all-reduce of a tensor-parallel target (C2) and
+ * the draft-id hand-off between a draft GPU and its target GPU (C1).
+ * One process per GPU.  psd_comm_create allocates this rank's region and
+ * writes its IPC handle (psd_comm_handle_bytes bytes) to handle_out; the
+ * caller exchanges the handles (any host transport) and passes all `world`
+ * of them, in rank order, to psd_comm_open.  Every rank must issue the same
+ * sequence of all-reduce calls; kernels wait on peers with a 10 s watchdog
+ * (trap) instead of hanging.  Kernels may be captured in CUDA graphs. */
+#define PSD_COMM_MAX_WORLD 16
+size_t psd_comm_handle_bytes(void);
+int psd_comm_create(int rank, int world, size_t buf_bytes, size_t mbox_bytes, void** comm,
+                    void* handle_out);
+int psd_comm_open(void* comm, const void* handles);
+int psd_comm_destroy(void* comm);
+/* out[i] = sum over ranks r = 0..world-1 (in that order) of
+ * sum over s = 0..S-1 (in that order) of partials_r[s * stride + i]:
+ * the split-K reduction of a row-parallel GEMM fused with the cross-rank sum;
+ * bit-identical on every rank.  n, stride multiples of 4, 16-byte aligned,
+ * 4 n <= buf_bytes. */
+int psd_tp_allreduce_partials(void* comm, const float* partials, int S, size_t stride, size_t n,
+                              float* out, void* stream);
+int psd_tp_allreduce_f32(void* comm, float* data, size_t n, void* stream);
+/* mailbox (depth 1 per peer pair): put copies n int32 into this rank's slot
+ * of `peer`'s mailbox once the peer consumed the previous message; get waits
+ * for the next message from `peer` and copies it to dst.  4 n <= mbox_bytes. */
+int psd_p2p_put_i32(void* comm, int peer, const int32_t* src, int n, void* stream);
+int psd_p2p_get_i32(void* comm, int peer, int32_t* dst, int n, void* stream);
+
 /* ---- K5 / glue: KV commit of accepted tokens, token routing ---------------
  * psd_commit replaces the commit rule + KV write accounting of a verified row
  * (pkg/src/specsim/engine.py:257-262; kv_manager.py:130-144): per row b

@@ -51,9 +51,13 @@ class CpuTargetEngine:
             cb.t.forward([(state.requests[rid].prompt_ids[:-1], 0) for rid in ids],
                          [cb.tc[r] for r in ids])
 
-    def inject(self, drafts: dict):
-        for rid, ids in drafts.items():
-            self.cb.pending[rid] = list(ids)
+    def inject_ids(self, rows, ids):
+        """Flat drafted ids in row order (rows: (rid, slot, L, k))."""
+        ids = [int(x) for x in ids]
+        i = 0
+        for rid, _, _, k in rows:
+            self.cb.pending[rid] = ids[i:i + k]
+            i += k
 
     def verify(self, state, rows: list[VerifyRow]):
         t0 = time.perf_counter()
@@ -87,8 +91,11 @@ class CpuDraftEngine:
         if rows:
             self.cb.d.forward([(p[:-1], 0) for _, _, p in rows], [self.cb.dc[r] for r, _, _ in rows])
 
-    def draft(self, rows):
+    def draft(self, rows, prev_us: int):
+        """(flat ids in row order + prev_us, (start, end) host times)."""
         for rid, _, L, _ in rows:
             assert len(self.cb.seq[rid]) == L, (rid, len(self.cb.seq[rid]), L)
+        t0 = time.perf_counter()
         self.cb._draft(None, [r[0] for r in rows], {r[0]: r[3] for r in rows})
-        return {r[0]: list(self.cb.pending[r[0]]) for r in rows}
+        flat = [t for r in rows for t in self.cb.pending[r[0]]]
+        return np.asarray(flat + [prev_us], np.int32), (t0, time.perf_counter())

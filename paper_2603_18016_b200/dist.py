@@ -41,6 +41,8 @@ def aggregate(tokens: int, ms: float, device=None) -> tuple[int, float]:
     """(sum of tokens, max of device ms) over ranks; identity when world == 1."""
     if not dist.is_initialized() or dist.get_world_size() == 1:
         return tokens, ms
+    if dist.get_backend() == "gloo":
+        device = None  # gloo reduces host tensors
     t = torch.tensor([float(tokens), ms], dtype=torch.float64,
                      device=device if device is not None else "cpu")
     tok = t[:1].clone()

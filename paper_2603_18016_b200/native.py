@@ -67,6 +67,14 @@ SIGNATURES: dict[str, tuple] = {
     "psd_launch_count": (_c.c_longlong, []),
     "psd_gemm_set_max_ctas": (None, [_i]),
     "psd_gemm_set_trace": (None, [_p]),
+    "psd_comm_handle_bytes": (_sz, []),
+    "psd_comm_create": (_i, [_i, _i, _sz, _sz, _c.POINTER(_p), _p]),
+    "psd_comm_open": (_i, [_p, _p]),
+    "psd_comm_destroy": (_i, [_p]),
+    "psd_tp_allreduce_partials": (_i, [_p, _p, _i, _sz, _sz, _p, _p]),
+    "psd_tp_allreduce_f32": (_i, [_p, _p, _sz, _p]),
+    "psd_p2p_put_i32": (_i, [_p, _i, _p, _i, _p]),
+    "psd_p2p_get_i32": (_i, [_p, _i, _p, _i, _p]),
     "psd_mk_smem_bytes": (_sz, []),
     "psd_mk_create": (_p, [_p]),
     "psd_mk_destroy": (None, [_p]),

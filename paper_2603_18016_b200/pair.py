@@ -16,8 +16,16 @@ the overlap the reference only models as max(verify, draft).
 The protocol is engine-agnostic: ``GpuTargetEngine`` / ``GpuDraftEngine``
 wrap :class:`~.gpu.GpuBackend` (roles "target" / "draft"); the CPU tests
 (tests/test_pair_gloo.py) plug the numpy oracle engines into the same classes
-over gloo.  Transport = ``dist.send``/``recv`` of small int32 tensors (NCCL:
-on-device; gloo: host).
+over gloo.  Transport = ``dist.send``/``recv``.  The command message is a
+small int32 array the draft rank's host decodes; the drafted ids (and, when
+sampling, the q rows) stay on the devices under NCCL: the draft rank gathers
+them into one int32 buffer on its GPU and sends it without a host sync; the
+target rank receives into a device buffer and scatters it into its slot
+table with a kernel (``psd_index_copy_i32``), stream-ordered before the
+verification that reads them.  Each id message carries, in its last element,
+the draft rank's CUDA-event time of its previous draft phase (µs), so no host
+ever waits for a draft to finish just to time it.  Under gloo the same
+buffers travel through host memory.
 """
 
 from __future__ import annotations
@@ -70,6 +78,25 @@ class PairLink:
         dist.recv(buf, self.peer)
         self.bytes_recv += buf.numel() * 4
         return buf if device is None else buf.to(device, non_blocking=True)
+
+    def send_ids(self, ids) -> None:
+        """Flat int32 ids (device tensor under NCCL, else host) as one message."""
+        t = ids if isinstance(ids, torch.Tensor) else torch.from_numpy(
+            np.ascontiguousarray(ids, dtype=np.int32))
+        if self.device is None:
+            t = t.cpu()
+        elif not t.is_cuda:
+            t = t.to(self.device)
+        dist.send(t.contiguous(), self.peer)
+        self.bytes_sent += 4 * t.numel()
+
+    def recv_ids(self, n: int) -> torch.Tensor:
+        """n int32 (device tensor under NCCL, host under gloo); no host sync."""
+        buf = torch.empty(n, dtype=torch.int32,
+                          device=self.device if self.device is not None else "cpu")
+        dist.recv(buf, self.peer)
+        self.bytes_recv += 4 * n
+        return buf
 
     def recv(self) -> np.ndarray:
         hdr = self._t(np.zeros(1, np.int32))
@@ -127,25 +154,13 @@ def decode_step(msg: np.ndarray) -> dict:
             "overlap": overlap, "table": table}
 
 
-def encode_drafts(rows, drafts: dict, ms: float) -> np.ndarray:
-    out = [MAGIC, len(rows), int(ms * 1000)]
-    for r in rows:
-        d = drafts[r[0]]
-        out += [r[0], len(d)] + list(d)
-    return np.asarray(out, np.int32)
-
-
-def decode_drafts(msg: np.ndarray) -> tuple[dict, float]:
-    if msg[0] != MAGIC:
-        raise RuntimeError("PSD pair protocol: bad draft reply")
-    n, ms = int(msg[1]), msg[2] / 1000.0
-    i = 3
-    out = {}
-    for _ in range(n):
-        rid, k = int(msg[i]), int(msg[i + 1])
-        out[rid] = msg[i + 2:i + 2 + k].tolist()
-        i += 2 + k
-    return out, ms
+def split_ids(rows, flat) -> dict:
+    """{rid: [ids]} from a flat id array in row order (rows: (rid, slot, L, k))."""
+    out, i = {}, 0
+    for rid, _, _, k in rows:
+        out[rid] = [int(x) for x in flat[i:i + k]]
+        i += k
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -201,19 +216,11 @@ class PairTarget:
         self.pending_commits = []
         eng.prefill(state, plan.prefill_ids)
         t1 = time.perf_counter()
-        serial_ms = 0.0
-        if serial:
-            drafts, serial_ms = decode_drafts(self.link.recv())
-            eng.inject(drafts)
-            self._recv_q(serial, drafts)
+        serial_ms = self._take_drafts(serial)
         t2 = time.perf_counter()
         accepted, committed, verify_ms = eng.verify(state, rows) if rows else ({}, {}, 0.0)
         t3 = time.perf_counter()
-        overlap_ms = 0.0
-        if overlap:
-            drafts, overlap_ms = decode_drafts(self.link.recv())
-            eng.inject(drafts)
-            self._recv_q(overlap, drafts)
+        overlap_ms = self._take_drafts(overlap)
         t4 = time.perf_counter()
         for rid, toks in committed.items():
             self.pending_commits.append((rid, eng.slot_of(rid), toks))
@@ -225,22 +232,44 @@ class PairTarget:
         self.stats["wait_ms"] += ms(t1, t2) + ms(t3, t4)
         return StepResult(ms(t0, t1), serial_ms, overlap_ms, verify_ms, ms(t0, t4), accepted)
 
-    def _recv_q(self, rows, drafts) -> None:
+    def _take_drafts(self, rows) -> float:
+        """Receive one phase's drafted ids (+ q rows when sampling) and hand
+        them to the engine; returns the draft time that message reports (the
+        draft rank's previous phase, CUDA events, ms).  Nothing here waits on
+        the host: the ids land in a device buffer the engine scatters from."""
+        if not rows:
+            return 0.0
+        n = sum(r[3] for r in rows)
+        msg = self.link.recv_ids(n + 1)
+        self.engine.inject_ids(rows, msg[:n])
+        self._recv_q(rows)
+        ms = 0.0
+        prev = getattr(self, "_prev_msg", None)
+        if prev is not None:  # long complete: read without stalling
+            ms = int(prev[-1]) / 1000.0
+        self._prev_msg = msg
+        return ms
+
+    def _recv_q(self, rows) -> None:
         """Sampling mode: the draft distributions of the drafted tokens follow
         the draft ids (one [sum k, V_draft + 4] fp32 message, rows in draft
         order, each row's canonical (max, sum) in columns V, V + 1)."""
         vq = getattr(self.engine, "q_vocab", 0)
         if not vq:
             return
-        n = sum(len(drafts[r[0]]) for r in rows)
+        n = sum(r[3] for r in rows)
         if n:
             # each row carries its canonical (max, sum) in two extra columns
-            self.engine.inject_q(rows, drafts,
-                                 self.link.recv_rows(n, vq + 4, self.engine.device))
+            self.engine.inject_q(rows, self.link.recv_rows(n, vq + 4, self.engine.device))
 
     def stop(self) -> None:
+        """End of a run: the draft rank answers with the time of its last
+        draft phase (the one no id message reported)."""
         self.pending_commits = []
         self.link.send(np.asarray([MAGIC, K_STOP], np.int32))
+        last = self.link.recv()
+        self.stats["draft_ms"] += int(last[0]) / 1000.0 if last.size else 0.0
+        self._prev_msg = None
 
 
 class DraftServer:
@@ -253,9 +282,15 @@ class DraftServer:
 
     def serve(self) -> int:
         eng = self.engine
+        prev_us = 0  # CUDA-event time of the previous draft phase
+        pending = None  # (start, end) events of the phase in flight
         while True:
             cmd = decode_step(self.link.recv())
+            if pending is not None:
+                prev_us = _elapsed_us(*pending)
+                pending = None
             if cmd["stop"]:
+                self.link.send(np.asarray([prev_us], np.int32))
                 return self.steps
             eng.set_tables(cmd["table"])
             eng.commit(cmd["commits"])  # before admissions: a freed slot may be reused
@@ -263,13 +298,23 @@ class DraftServer:
             eng.prefill(cmd["admit"])
             for rows in (cmd["serial"], cmd["overlap"]):
                 if rows:
-                    t0 = time.perf_counter()
-                    drafts = eng.draft(rows)
-                    self.link.send(encode_drafts(rows, drafts, (time.perf_counter() - t0) * 1e3))
+                    if pending is not None:
+                        prev_us = _elapsed_us(*pending)
+                    ids, pending = eng.draft(rows, prev_us)
+                    self.link.send_ids(ids)
                     q = eng.q_rows(rows) if getattr(eng, "q_vocab", 0) else None
                     if q is not None and q.shape[0]:
                         self.link.send_rows(q)
             self.steps += 1
+
+
+def _elapsed_us(e0, e1) -> int:
+    """Microseconds between two recorded events (CUDA events, or host
+    perf_counter floats for the CPU engines)."""
+    if isinstance(e0, float):
+        return int((e1 - e0) * 1e6)
+    e1.synchronize()
+    return int(e0.elapsed_time(e1) * 1000)
 
 
 # ---------------------------------------------------------------------------
@@ -315,14 +360,29 @@ class GpuTargetEngine:
             with torch.cuda.stream(be.s_target):
                 be._prefill(state, ids, be.tfwd, "target")
 
-    def inject(self, drafts: dict):
+    def inject_ids(self, rows, ids: torch.Tensor) -> None:
+        """Drafted ids (flat, row order; device buffer under NCCL) ->
+        slot_tok[slot, 2 + i] by one scatter kernel on the target stream."""
         be = self.be
-        pairs = []
-        for rid, ids in drafts.items():
-            s = be.slots[rid]
-            pairs += [(s * be.ldt + 2 + i, t) for i, t in enumerate(ids)]
+        dst = []
+        for rid, slot, _, k in rows:
+            dst += [slot * be.ldt + 2 + i for i in range(k)]
+        if not dst:
+            return
+        idx = torch.from_numpy(np.asarray(dst, np.int32)).pin_memory()
+        # the ids arrived in the current stream's order (NCCL recv / host)
+        be.s_target.wait_stream(torch.cuda.current_stream(be.device))
         with torch.cuda.stream(be.s_target):
-            be._set_slot_values(pairs)
+            idx_d = idx.to(be.device, non_blocking=True)
+            src = ids.to(be.device, non_blocking=True) if not ids.is_cuda else ids
+            from . import native
+            native.check(native.load().psd_index_copy_i32(
+                be.slot_tok.data_ptr(), idx_d.data_ptr(), src.data_ptr(), None, len(dst),
+                torch.cuda.current_stream(be.device).cuda_stream), "draft ids in")
+            be.launches += 1
+            be.h2d_bytes += 4 * len(dst) * (1 if ids.is_cuda else 2)
+            src.record_stream(be.s_target)
+            idx_d.record_stream(be.s_target)
 
     @property
     def q_vocab(self) -> int:
@@ -332,14 +392,14 @@ class GpuTargetEngine:
     def device(self):
         return self.be.device
 
-    def inject_q(self, rows, drafts, q: torch.Tensor) -> None:
+    def inject_q(self, rows, q: torch.Tensor) -> None:
         """q rows in draft order -> qbuf[slot * k_max + i] (what K1 reads);
         their canonical (max, sum), the last two columns -> qstats, so K1
         takes the cached-statistics path as in a single process."""
         be = self.be
         dst = []
-        for rid, slot, _, _ in rows:
-            dst += [slot * be.k_max + i for i in range(len(drafts[rid]))]
+        for rid, slot, _, k in rows:
+            dst += [slot * be.k_max + i for i in range(k)]
         idx = torch.from_numpy(np.asarray(dst, np.int32)).pin_memory()
         # q arrived in the current stream's order (NCCL recv / host copy)
         be.s_target.wait_stream(torch.cuda.current_stream(be.device))
@@ -364,7 +424,7 @@ class GpuTargetEngine:
         ev1.synchronize()
         acc = be.acc_host.numpy()[:n]
         out = be.out_host.numpy()
-        K1 = max((r.k for r in rows), default=0) + 1
+        K1 = be.k_max + 1  # every verify pass is k_max + 1 tokens wide (GpuBackend._verify)
         accepted, committed = {}, {}
         for r, row in enumerate(rows):
             a = int(acc[r])
@@ -412,11 +472,32 @@ class GpuDraftEngine:
         if rows:
             self.be._prefill_rows([(slot, p) for _, slot, p in rows], self.be.dfwd)
 
-    def draft(self, rows):
+    def draft(self, rows, prev_us: int):
+        """Draft `rows` on this GPU; returns (message, events): the drafted
+        ids gathered from slot_tok in row order plus `prev_us` as the last
+        element, one device int32 buffer ready to send, and the CUDA events
+        bracketing this phase.  No host synchronisation."""
         be = self.be
+        dev = be.device
+        src = []
+        for rid, slot, _, k in rows:
+            src += [slot * be.ldt + 2 + i for i in range(k)]
+        n = len(src)
+        host = torch.from_numpy(np.asarray(src + [prev_us], np.int32)).pin_memory()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
         be._draft_rows(rows)
-        st = be.slot_tok.cpu().numpy()  # synchronises the draft stream
-        return {rid: st[slot, 2:2 + k].tolist() for rid, slot, _, k in rows}
+        e1.record()
+        hd = host.to(dev, non_blocking=True)
+        be.h2d_bytes += 4 * (n + 1)
+        msg = torch.empty(n + 1, dtype=torch.int32, device=dev)
+        from . import native
+        st = torch.cuda.current_stream(dev).cuda_stream
+        native.check(native.load().psd_index_copy_i32(msg.data_ptr(), None, be.slot_tok.data_ptr(),
+                                                      hd.data_ptr(), n, st), "draft ids out")
+        be.launches += 1
+        msg[n:].copy_(hd[n:])
+        return msg, (e0, e1)
 
     @property
     def q_vocab(self) -> int:
