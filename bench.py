@@ -553,9 +553,20 @@ def run_ours(args) -> None:
     # pairs: even rank = target GPU (scheduler), odd rank = dedicated draft GPU
     roles = ("target", "draft") if not pairs else (("target",) if rank % 2 == 0 else ("draft",))
     replica = rank // 2 if pairs else rank
-    tp = (rank, world, torch.distributed.group.WORLD) if tp_layout and world > 1 else None
+    tp = None
+    tp_size = 1
     if tp_layout:
-        replica = 0  # one replica spread over all ranks (SPMD scheduler)
+        # world // tp_size replicas, each a tensor-parallel target over tp_size
+        # ranks (SPMD scheduler) with the draft on a second stream of every TP
+        # rank: the 8-GPU cfg4 layout "two TP4 replicas" (SURVEY §7 hard part 8)
+        tp_size = args.tp or world
+        if world % tp_size:
+            raise SystemExit("--tp must divide the number of GPUs")
+        replica = rank // tp_size
+        groups = [torch.distributed.new_group(list(range(r * tp_size, (r + 1) * tp_size)))
+                  for r in range(world // tp_size)] if world > 1 else []
+        if tp_size > 1:
+            tp = (rank % tp_size, tp_size, groups[replica])
     be = GpuBackend(CFG["target"], CFG["draft"], max_requests=CFG["n_requests"],
                     max_batch=CFG["n_requests"], k_max=CFG["k"], tp=tp,
                     max_seq_len=CFG["prompt"] + CFG["output"] + 16, seed=replica,
@@ -624,7 +635,7 @@ def run_ours(args) -> None:
         ms_local = e0.elapsed_time(e1)
         tokens, ms = pd.aggregate(sum(r.total_generated for r in reps), ms_local, dev)
         if tp_layout:
-            tokens //= world  # every TP rank emits the same tokens
+            tokens //= tp_size  # every TP rank of a replica emits the same tokens
         results[mode] = {"ms": ms, "tokens": tokens, "reps": reps, "states": states,
                          "clocks": clocks.stop() if clocks else None,
                          "draft_ms": backend.stats["draft_ms"] - stats0["draft_ms"],
@@ -690,22 +701,25 @@ def run_ours(args) -> None:
         "metric": METRIC, "value": round(value, 1), "unit": "tok/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(psd["ms"] / args.steps, 2), "higher_is_better": True,
-        "scaling": "strong" if tp_layout else "weak", "vs_baseline": None, "dtype": "bf16",
+        "scaling": ("strong" if tp_layout and tp_size == world else "weak"), "vs_baseline": None,
+        "dtype": "bf16",
         "data": "synthetic",
         "config": {"workload": ("cfg3: Qwen2.5-7B target / Qwen2.5-0.5B draft shapes, "
                                 "random-init bf16, 2x32 requests, k=4, prompt 128, output 256, "
                                 "T=1.0 rejection sampling, both models on one GPU"
                                 if sampling else
-                                "cfg4: Llama-3.1-70B target (tensor-parallel over all GPUs) / "
+                                "cfg4: Llama-3.1-70B target (tensor-parallel replicas, --tp "
+                                "ranks each, draft on a second stream of every TP rank) / "
                                 "Llama-3.2-1B draft shapes, random-init bf16, 2x64 requests, "
                                 "k=4, prompt 128, output 256, greedy" if tp_layout else
                                 "cfg2: Llama-3.1-8B target / Llama-3.2-1B draft shapes, "
                                 "random-init bf16, 2x32 requests, k=5, prompt 128, output 256, "
                                 "greedy, 1 GPU per replica (draft / verify on separate streams)"),
-                   "global_batch": (1 if tp_layout else world // 2 if pairs else world)
+                   "global_batch": (world // tp_size if tp_layout else
+                                    world // 2 if pairs else world)
                    * CFG["n_requests"],
                    "seq_len": CFG["prompt"] + CFG["output"],
-                   "parallelism": (f"tp{world}" if tp_layout else
+                   "parallelism": (f"tp{tp_size}x{world // tp_size}" if tp_layout else
                                    f"pairs{world // 2}" if pairs else f"replicas{world}"),
                    "l2": "inputs > L2 (weights 18.5 GB streamed per step)",
                    "synthetic_language_beta": [BETA_TARGET, BETA_DRAFT]},
@@ -765,6 +779,8 @@ def main() -> None:
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="torch.distributed backend (gloo: host transport, for a smoke run "
                          "of the multi-rank layouts on one GPU)")
+    ap.add_argument("--tp", type=int, default=0,
+                    help="--layout tp: ranks per tensor-parallel replica (default: all)")
     ap.add_argument("--no-sweep", action="store_true",
                     help="skip the config-5 verify-kernel grid (verify_sweep)")
     ap.add_argument("--ktune", action="store_true",

@@ -106,6 +106,22 @@ int psd_verify_sample_forced(const float* target_logits, int64_t t_stride_b, int
                              void* t_stats_out, const int32_t* t_stats_rows, void* ws,
                              size_t ws_bytes, void* stream);
 
+/* Vocabulary-parallel greedy K1 (tensor-parallel LM head):
+ * each rank reduces its logits shard (columns vocab_offset .. + V of the full
+ * row) to canonical slice partials (max, global argmax index) -- floats
+ * (psd_verify_partials_count) -- the ranks exchange them (e.g.
+ * psd_tp_allgather_f32: W x count floats, rank order) and every rank folds
+ * all W shards and decides (same accepted_len / out_tokens as psd_verify_greedy
+ * on the gathered rows, without gathering M x V logits). */
+size_t psd_verify_partials_count(int B, int K, int V);
+int psd_verify_greedy_partials(const float* target_logits, int64_t t_stride_b,
+                               int64_t t_stride_i, int V, int vocab_offset,
+                               const int32_t* draft_len, int B, int K, float* partials,
+                               void* stream);
+int psd_verify_greedy_fold(const float* partials, int W, int V_shard, const int32_t* draft_ids,
+                           const int32_t* draft_len, int B, int K, const int32_t* forced_len,
+                           int32_t* accepted_len, int32_t* out_tokens, void* stream);
+
 /* ---- K2: bf16 GEMM on tcgen05 (TMEM accumulators, TMA, mbarrier ring) -----
  *   Y[m, n] = epi( sum_k X[m*ldx + k] * W[n*ldw + k] )   X [M,K], W [N,K] bf16
  * Replaces the virtual pass durations verify_latency / draft_latency
@@ -139,15 +155,6 @@ int psd_gemm_plan(int M, int N, int K, int epi, int splits_hint, int* splits_out
 int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, int N, void* Y,
                   int ldy, int epi, const void* R, int ldr, int splits_hint, void* workspace,
                   size_t workspace_bytes, void* stream);
-/* Pre-tiled weights: [N/128][ceil(K/64)][128][64] bf16 with the 128-byte
- * swizzle applied, so every (128-row, 64-col) weight tile is one contiguous,
- * already-swizzled 16 KB block loaded with a single 1-D bulk copy (sequential
- * HBM bursts, no tensor-map walk).  psd_gemm_tiled = stream-K GEMM on them. */
-size_t psd_tiled_weight_bytes(int N, int K);
-int psd_tile_weights(const void* W, int N, int K, int ldw, void* tiled, void* stream);
-int psd_gemm_tiled(const void* X, int ldx, int M, int K, const void* W_tiled, int N, void* Y,
-                   int ldy, int epi, const void* R, int ldr, void* workspace,
-                   size_t workspace_bytes, void* stream);
 /* fp32 split-K partials P[z][m][n] (z < *splits_used, row pitch N); the
  * consumer kernel (psd_add_rmsnorm, psd_rope_kv) reduces them in z order, so
  * no separate reduction launch is needed.  Fewer splits are used when
@@ -208,6 +215,10 @@ int psd_attention_rope(const float* qkv_partials, int S, size_t slice, const int
 /* synthetic-language logit bias: logits[m, successor[prev_tokens[m]]] += beta */
 int psd_bigram_bias(float* logits, int64_t ld, const int32_t* prev_tokens, int M,
                     const int32_t* successor, int V, float beta, void* stream);
+/* the same on a vocabulary shard: logits hold columns [v0, v1) */
+int psd_bigram_bias_range(float* logits, int64_t ld, const int32_t* prev_tokens, int M,
+                          const int32_t* successor, int V, float beta, int v0, int v1,
+                          void* stream);
 /* out[b*n + i] = Philox4x32-10(key seed, counter (request_ids[b], verify_index[b],
  * base + i, 0)), top 24 bits / 2^24, in [0, 1) */
 int psd_philox_uniforms(uint64_t seed, const int32_t* request_ids, const int32_t* verify_index,
@@ -236,6 +247,12 @@ size_t psd_comm_handle_bytes(void);
 int psd_comm_create(int rank, int world, size_t buf_bytes, size_t mbox_bytes, void** comm,
                     void* handle_out);
 int psd_comm_open(void* comm, const void* handles);
+/* One process driving `world` ranks (devices[r], ranks may share a device):
+ * comms[r] ready to use, no IPC (peer access enabled between distinct
+ * devices).  Rank r's calls must run on devices[r], concurrently with the
+ * other ranks' (separate streams). */
+int psd_comm_create_local(int world, const int* devices, size_t buf_bytes, size_t mbox_bytes,
+                          void** comms);
 int psd_comm_destroy(void* comm);
 /* out[i] = sum over ranks r = 0..world-1 (in that order) of
  * sum over s = 0..S-1 (in that order) of partials_r[s * stride + i]:
@@ -245,6 +262,8 @@ int psd_comm_destroy(void* comm);
 int psd_tp_allreduce_partials(void* comm, const float* partials, int S, size_t stride, size_t n,
                               float* out, void* stream);
 int psd_tp_allreduce_f32(void* comm, float* data, size_t n, void* stream);
+/* out[r * n + i] = src_r[i] for every rank r (out must not alias src) */
+int psd_tp_allgather_f32(void* comm, const float* src, size_t n, float* out, void* stream);
 /* mailbox (depth 1 per peer pair): put copies n int32 into this rank's slot
  * of `peer`'s mailbox once the peer consumed the previous message; get waits
  * for the next message from `peer` and copies it to dst.  4 n <= mbox_bytes. */
@@ -275,41 +294,6 @@ int psd_fill_uniform_bf16(void* out, size_t n, uint64_t seed, float span, void* 
 int psd_fill_uniform_bf16_block(void* out, int64_t ld, int rows, int cols, int64_t full_cols,
                                 int64_t row0, int64_t col0, uint64_t seed, float span,
                                 void* stream);
-
-/* ---- fused k-step greedy draft decode (csrc/decode_mk.cu) -------------------
- * One persistent kernel runs all k draft steps of a batch (embedding, every
- * layer, LM head, argmax, scatter of the draft token into slot_tok).  The
- * model and the forward buffers are bound once; psd_mk_launch enqueues one
- * launch (graph-capturable once a (nb, steps) program was built eagerly).
- * Replaces the per-kernel draft forward of model.py for head_dim 32/64, greedy. */
-typedef struct {
-  int layers, hidden, heads, kv_heads, head_dim, ffn /* padded to 64 */, vocab;
-  float eps, attn_scale, beta;
-  int block_size, max_blocks, grid /* 0 = all SMs */, max_tokens;
-  /* 9 per layer: wqkv, wo, wgu (packed), wdown, attn_norm, mlp_norm, bqkv|NULL, k cache, v cache */
-  const void* const* layer_ptrs;
-  const void* embed;
-  const void* lm_head;
-  const void* final_norm;
-  const float* inv_freq;
-  const int32_t* successor; /* synthetic-language successor table (beta = 0: unused) */
-  const int32_t* block_table;
-  void* x; void* xn; void* attn; void* act; void* xf; /* forward buffers, >= 64 rows */
-  float* part;   /* split-K partials */
-  void* argpart; /* (vocab / 128) * 64 float2 */
-  int32_t* slot_tok;
-  int32_t* meta; int set_stride; int field_offsets[11];
-} psd_mk_model;
-size_t psd_mk_smem_bytes(void);
-void* psd_mk_create(const psd_mk_model* model);
-void psd_mk_destroy(void* handle);
-int psd_mk_grid(void* handle);
-int psd_mk_launch(void* handle, int nb, int steps, void* stream);
-/* Diagnostics: ops of a built (nb, steps) program (-1: not built), and a launch
- * that records per-CTA per-op %globaltimer stamps (entry, inputs ready, done)
- * into trace[grid][n_ops][3] (u64). */
-int psd_mk_n_ops(void* handle, int nb, int steps);
-int psd_mk_launch_traced(void* handle, int nb, int steps, void* trace, void* stream);
 
 #ifdef __cplusplus
 }

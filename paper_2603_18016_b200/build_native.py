@@ -16,7 +16,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libpsd.so")
-BUILD = os.path.join(HERE, "csrc", "_build")
+BUILD = os.path.join(HERE, "csrc", "_build" + ("_exp" if os.environ.get("PSD_EXPERIMENTAL",
+                                                                        "0") == "1" else ""))
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -24,8 +25,17 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxe
          "-Xptxas", "-v", "-I", os.path.join(HERE, "..", "include")]
 
 
+# PSD_EXPERIMENTAL=1 also builds the parked variants declared in
+# include/psd_experimental.h (fused k-step draft decode, pre-tiled weight GEMM)
+EXPERIMENTAL = os.environ.get("PSD_EXPERIMENTAL", "0") == "1"
+EXPERIMENTAL_ONLY = {"decode_mk.cu"}
+if EXPERIMENTAL:
+    FLAGS = FLAGS + ["-DPSD_EXPERIMENTAL=1"]
+
+
 def _sources():
-    return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
+    srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
+    return [s for s in srcs if EXPERIMENTAL or os.path.basename(s) not in EXPERIMENTAL_ONLY]
 
 
 def _needs(obj: str, src: str, headers: list[str]) -> bool:
@@ -57,9 +67,16 @@ def build(verbose: bool = False, jobs: int = 8) -> str:
             raise RuntimeError(f"nvcc failed on {src}")
         if verbose:
             sys.stdout.write(out)
-    if not os.path.exists(OUT) or any(os.path.getmtime(o) > os.path.getmtime(OUT) for o in objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", OUT] + objs + ["-lcuda"] * 0
+    # relink when an object changed or the object set did (experimental switch)
+    stamp = os.path.join(BUILD, "..", "_link_objs.txt")
+    want = "\n".join(objs)
+    have = open(stamp).read() if os.path.exists(stamp) else ""
+    if (have != want or not os.path.exists(OUT)
+            or any(os.path.getmtime(o) > os.path.getmtime(OUT) for o in objs)):
+        cmd = [NVCC] + ARCH + ["-shared", "-o", OUT] + objs
         subprocess.run(cmd, check=True)
+        with open(stamp, "w") as fh:
+            fh.write(want)
     return OUT
 
 

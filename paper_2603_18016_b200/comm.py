@@ -53,6 +53,28 @@ class PeerComm:
         with torch.cuda.device(self.device):
             native.check(lib.psd_comm_open(self._c, allh), "psd_comm_open")
 
+    @classmethod
+    def local_group(cls, devices, buf_bytes: int = 64 << 20,
+                    mbox_bytes: int = 1 << 20) -> list["PeerComm"]:
+        """One process driving len(devices) ranks (psd_comm_create_local): no
+        IPC, no process group.  Rank r's calls must be issued on devices[r],
+        on a stream that runs concurrently with the other ranks' streams."""
+        world = len(devices)
+        lib = native.load()
+        devs = (ctypes.c_int * world)(*[torch.device(d).index or 0 for d in devices])
+        hs = (ctypes.c_void_p * world)()
+        native.check(lib.psd_comm_create_local(world, devs, buf_bytes, mbox_bytes, hs),
+                     "psd_comm_create_local")
+        out = []
+        for r in range(world):
+            c = cls.__new__(cls)
+            c.group, c.rank, c.world = None, r, world
+            c.device = torch.device("cuda", devs[r])
+            c._c = ctypes.c_void_p(hs[r])
+            c.buf_bytes, c.mbox_bytes = buf_bytes, mbox_bytes
+            out.append(c)
+        return out
+
     def _stream(self) -> int:
         return torch.cuda.current_stream(self.device).cuda_stream
 
@@ -73,6 +95,15 @@ class PeerComm:
     def allreduce_(self, data: torch.Tensor) -> torch.Tensor:
         return self.allreduce_partials(data.view(-1), 1, data.numel(), data.numel(),
                                        data.view(-1)).view(data.shape)
+
+    def allgather(self, src: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+        """out.view(world, -1)[r] = rank r's src (fp32, n % 4 == 0)."""
+        n = src.numel()
+        if out.numel() < self.world * n or src.dtype != torch.float32:
+            raise ConfigError("allgather: fp32, out holds world * n")
+        native.check(native.load().psd_tp_allgather_f32(
+            self._c, src.data_ptr(), n, out.data_ptr(), self._stream()), "psd_tp_allgather_f32")
+        return out
 
     def put(self, peer: int, src: torch.Tensor) -> None:
         if src.dtype != torch.int32 or not src.is_cuda:

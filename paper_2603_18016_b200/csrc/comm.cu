@@ -49,8 +49,8 @@ constexpr int kReady = 0;          // [kMaxWorld] written by peers
 constexpr int kSeq = 64;           // [kMaxWorld] mailbox: messages src has put here
 constexpr int kAck = 128;          // [kMaxWorld] mailbox: messages dst consumed from me
 constexpr int kEpoch = 192;        // local: all-reduce calls completed
-constexpr int kArrive = 193;       // local: CTA tickets of phase 1 (monotonic)
-constexpr int kDone = 194;         // local: CTA tickets of phase 3 (monotonic)
+constexpr int kArrive = 193;       // local: CTA tickets of phase 1 (reset per call)
+constexpr int kDone = 194;         // local: CTA tickets of phase 3 (reset per call)
 constexpr int kSent = 256;         // local [kMaxWorld]: messages I put to dst
 constexpr int kConsumed = 320;     // local [kMaxWorld]: messages I consumed from src
 constexpr int kThreads = 256;
@@ -62,6 +62,7 @@ struct Comm {
   char* peer[kMaxWorld];
   bool opened;
   int device;
+  bool local_group;  // psd_comm_create_local: peers are this process's own regions
 };
 
 struct Handle {
@@ -99,6 +100,7 @@ struct ARArgs {
   int S;
   size_t stride, n, buf_bytes;
   float* out;
+  int gather;  // 0: out = sum over ranks; 1: out[r * n + i] = rank r's data
 };
 
 __global__ void __launch_bounds__(kThreads) allreduce_kernel(const ARArgs a) {
@@ -131,9 +133,13 @@ __global__ void __launch_bounds__(kThreads) allreduce_kernel(const ARArgs a) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();
+    // per-call ticket (grids differ between calls): the last CTA resets it;
+    // no other CTA of this call touches it again, and the next call starts
+    // after this one completed (stream order)
     const unsigned long long t =
         atomicAdd(reinterpret_cast<unsigned long long*>(ctrl + kArrive), 1ull);
-    s_last = t == E * gridDim.x - 1;
+    s_last = t == gridDim.x - 1;
+    if (s_last) *reinterpret_cast<volatile uint64_t*>(ctrl + kArrive) = 0;
   }
   __syncthreads();
   if (s_last && threadIdx.x < a.world) {
@@ -142,8 +148,17 @@ __global__ void __launch_bounds__(kThreads) allreduce_kernel(const ARArgs a) {
   }
   if (threadIdx.x < a.world) wait_geq(ctrl + kReady + threadIdx.x, E);
   __syncthreads();
-  // 3. sum the ranks' buffers in rank order (identical on every rank)
-  for (size_t i = tid0; i < nv; i += step) {
+  // 3. sum the ranks' buffers in rank order (identical on every rank), or
+  //    gather them rank after rank
+  if (a.gather) {
+    for (int r = 0; r < a.world; ++r) {
+      const float4* src =
+          reinterpret_cast<const float4*>(a.region[r] + kCtrl + par * a.buf_bytes);
+      float4* dst = reinterpret_cast<float4*>(a.out) + r * nv;
+      for (size_t i = tid0; i < nv; i += step) dst[i] = __ldcv(src + i);
+    }
+  }
+  for (size_t i = tid0; i < nv && !a.gather; i += step) {
     float4 v = __ldcv(reinterpret_cast<const float4*>(a.region[0] + kCtrl + par * a.buf_bytes) +
                       i);
     for (int r = 1; r < a.world; ++r) {
@@ -159,7 +174,10 @@ __global__ void __launch_bounds__(kThreads) allreduce_kernel(const ARArgs a) {
     __threadfence();
     const unsigned long long t =
         atomicAdd(reinterpret_cast<unsigned long long*>(ctrl + kDone), 1ull);
-    if (t == E * gridDim.x - 1) *reinterpret_cast<volatile uint64_t*>(ctrl + kEpoch) = E;
+    if (t == gridDim.x - 1) {
+      *reinterpret_cast<volatile uint64_t*>(ctrl + kDone) = 0;
+      *reinterpret_cast<volatile uint64_t*>(ctrl + kEpoch) = E;
+    }
   }
   pdl_trigger();
 }
@@ -270,6 +288,61 @@ int psd_comm_create(int rank, int world, size_t buf_bytes, size_t mbox_bytes, vo
   return (int)cudaDeviceSynchronize();
 }
 
+int psd_comm_create_local(int world, const int* devices, size_t buf_bytes, size_t mbox_bytes,
+                          void** comms) {
+  if (!comms || !devices || world < 1 || world > kMaxWorld) return (int)cudaErrorInvalidValue;
+  buf_bytes = (buf_bytes + 255) & ~size_t(255);
+  mbox_bytes = (mbox_bytes + 255) & ~size_t(255);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  Comm* cs[kMaxWorld] = {};
+  cudaError_t e = cudaSuccess;
+  for (int r = 0; r < world && e == cudaSuccess; ++r) {
+    cs[r] = new (std::nothrow) Comm();
+    if (!cs[r]) { e = cudaErrorMemoryAllocation; break; }
+    cs[r]->rank = r;
+    cs[r]->world = world;
+    cs[r]->buf_bytes = buf_bytes;
+    cs[r]->mbox_bytes = mbox_bytes;
+    cs[r]->region_bytes = kCtrl + 2 * buf_bytes + (size_t)world * mbox_bytes;
+    cs[r]->device = devices[r];
+    cs[r]->local_group = true;
+    e = cudaSetDevice(devices[r]);
+    if (e == cudaSuccess) e = cudaMalloc(&cs[r]->local, cs[r]->region_bytes);
+    if (e == cudaSuccess) e = cudaMemset(cs[r]->local, 0, kCtrl);
+    // direct peer access between distinct devices (same-device ranks need none)
+    for (int q = 0; q < r && e == cudaSuccess; ++q) {
+      if (devices[q] == devices[r]) continue;
+      int ok = 0;
+      cudaDeviceCanAccessPeer(&ok, devices[r], devices[q]);
+      if (!ok) { e = cudaErrorPeerAccessUnsupported; break; }
+      cudaSetDevice(devices[r]);
+      cudaError_t pe = cudaDeviceEnablePeerAccess(devices[q], 0);
+      if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) e = pe;
+      cudaSetDevice(devices[q]);
+      pe = cudaDeviceEnablePeerAccess(devices[r], 0);
+      if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) e = pe;
+      cudaGetLastError();  // clear a sticky "already enabled"
+    }
+  }
+  if (e == cudaSuccess) {
+    for (int r = 0; r < world; ++r) {
+      for (int q = 0; q < kMaxWorld; ++q) cs[r]->peer[q] = q < world ? cs[q]->local : nullptr;
+      cs[r]->opened = true;
+      comms[r] = cs[r];
+    }
+    e = cudaDeviceSynchronize();
+  } else {
+    for (int r = 0; r < world; ++r)
+      if (cs[r]) {
+        if (cs[r]->local) cudaFree(cs[r]->local);
+        delete cs[r];
+      }
+  }
+  cudaSetDevice(prev);
+  return (int)e;
+}
+
 int psd_comm_open(void* comm, const void* handles) {
   Comm* c = static_cast<Comm*>(comm);
   if (!c || !handles) return (int)cudaErrorInvalidValue;
@@ -292,15 +365,16 @@ int psd_comm_destroy(void* comm) {
   Comm* c = static_cast<Comm*>(comm);
   if (!c) return 0;
   cudaDeviceSynchronize();
-  for (int r = 0; r < c->world; ++r)
-    if (r != c->rank && c->peer[r]) cudaIpcCloseMemHandle(c->peer[r]);
+  if (!c->local_group)
+    for (int r = 0; r < c->world; ++r)
+      if (r != c->rank && c->peer[r]) cudaIpcCloseMemHandle(c->peer[r]);
   cudaFree(c->local);
   delete c;
   return 0;
 }
 
-int psd_tp_allreduce_partials(void* comm, const float* partials, int S, size_t stride, size_t n,
-                              float* out, void* stream) {
+static int launch_ar(void* comm, const float* partials, int S, size_t stride, size_t n,
+                     float* out, int gather, void* stream) {
   Comm* c = static_cast<Comm*>(comm);
   if (!c || !c->opened || !partials || !out || S < 1) return (int)cudaErrorInvalidValue;
   if ((n & 3) || (stride & 3) || n * sizeof(float) > c->buf_bytes ||
@@ -316,6 +390,7 @@ int psd_tp_allreduce_partials(void* comm, const float* partials, int S, size_t s
   a.n = n;
   a.buf_bytes = c->buf_bytes;
   a.out = out;
+  a.gather = gather;
   // resident grid (the CTAs wait on each other's tickets): half the SMs
   const size_t want = (n / 4 + kThreads - 1) / kThreads;
   int grid = sm_count_dev() / 2;
@@ -324,8 +399,18 @@ int psd_tp_allreduce_partials(void* comm, const float* partials, int S, size_t s
                           (cudaStream_t)stream, a);
 }
 
+int psd_tp_allreduce_partials(void* comm, const float* partials, int S, size_t stride, size_t n,
+                              float* out, void* stream) {
+  return launch_ar(comm, partials, S, stride, n, out, 0, stream);
+}
+
 int psd_tp_allreduce_f32(void* comm, float* data, size_t n, void* stream) {
   return psd_tp_allreduce_partials(comm, data, 1, n, n, data, stream);
+}
+
+int psd_tp_allgather_f32(void* comm, const float* src, size_t n, float* out, void* stream) {
+  if (out == src) return (int)cudaErrorInvalidValue;
+  return launch_ar(comm, src, 1, n, n, out, 1, stream);
 }
 
 int psd_p2p_put_i32(void* comm, int peer, const int32_t* src, int n, void* stream) {

@@ -38,6 +38,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/psd.h"
+#include "../../include/psd_experimental.h"
 #include "common.h"
 #include "sm100.cuh"
 

@@ -30,6 +30,7 @@
 #include <mutex>
 
 #include "../../include/psd.h"
+#include "../../include/psd_experimental.h"
 #include "common.h"
 #include "sm100.cuh"
 
@@ -982,6 +983,7 @@ int launch_sk(int bn, const CUtensorMap& mw, const CUtensorMap& mx, const SKArgs
   return (int)cudaErrorInvalidValue;
 }
 
+#if PSD_EXPERIMENTAL
 // [N, K] row-major -> [N/128][KB][128][64] with the 128-byte swizzle applied
 // (16-byte chunk j of row r stored at chunk j ^ (r & 7)), K zero-padded
 __global__ void tile_weights_kernel(const __nv_bfloat16* __restrict__ W, int N, int K, int ldw,
@@ -1009,6 +1011,7 @@ __global__ void tile_weights_kernel(const __nv_bfloat16* __restrict__ W, int N, 
     reinterpret_cast<uint4*>(T)[q] = v;
   }
 }
+#endif  // PSD_EXPERIMENTAL
 
 int token_tile(int M) {
   if (M > 256) {
@@ -1184,6 +1187,7 @@ int psd_gemm_plan(int M, int N, int K, int epi, int splits_hint, int* splits_out
   return 0;
 }
 
+#if PSD_EXPERIMENTAL
 size_t psd_tiled_weight_bytes(int N, int K) {
   return (size_t)N * ((K + BK - 1) / BK) * BK * sizeof(__nv_bfloat16);
 }
@@ -1229,6 +1233,7 @@ int psd_gemm_tiled(const void* X, int ldx, int M, int K, const void* W_tiled, in
   }
   return (int)cudaErrorInvalidValue;
 }
+#endif  // PSD_EXPERIMENTAL
 
 int psd_gemm_partials(const void* X, int ldx, int M, int K, const void* W, int ldw, int N,
                       float* P, size_t p_bytes, int splits_hint, int* splits_used, void* stream) {

@@ -754,16 +754,20 @@ int att_splits(int ctas, int max_kv_len) {
 }
 
 // ---- synthetic-language bias (shared by draft and target) -----------------------
+// logits hold vocabulary columns [v0, v1) (a tensor-parallel shard, or the
+// whole row with v0 = 0, v1 = V)
 __global__ void bigram_bias_kernel(float* __restrict__ logits, int64_t ld,
                                    const int32_t* __restrict__ prev, int M,
-                                   const int32_t* __restrict__ succ, int V, float beta) {
+                                   const int32_t* __restrict__ succ, int V, float beta, int v0,
+                                   int v1) {
   pdl_wait();
   pdl_trigger();
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= M) return;
   const int t = prev[m];
   if (t < 0 || t >= V) return;
-  logits[m * ld + succ[t]] += beta;
+  const int col = succ[t];
+  if (col >= v0 && col < v1) logits[m * ld + col - v0] += beta;
 }
 
 // ---- Philox4x32-10 uniforms keyed (seed, request, verify index, position) ------
@@ -1108,9 +1112,17 @@ int psd_attention_rope(const float* qkv_partials, int S, size_t slice, const int
 
 int psd_bigram_bias(float* logits, int64_t ld, const int32_t* prev_tokens, int M,
                     const int32_t* successor, int V, float beta, void* stream) {
+  return psd_bigram_bias_range(logits, ld, prev_tokens, M, successor, V, beta, 0, 1 << 30,
+                               stream);
+}
+
+int psd_bigram_bias_range(float* logits, int64_t ld, const int32_t* prev_tokens, int M,
+                          const int32_t* successor, int V, float beta, int v0, int v1,
+                          void* stream) {
   if (M <= 0) return 0;
   return (int)psd::launch(bigram_bias_kernel, dim3((M + 127) / 128), dim3(128), 0,
-                          (cudaStream_t)stream, logits, ld, prev_tokens, M, successor, V, beta);
+                          (cudaStream_t)stream, logits, ld, prev_tokens, M, successor, V, beta,
+                          v0, v1);
 }
 
 int psd_philox_uniforms(uint64_t seed, const int32_t* request_ids, const int32_t* verify_index,

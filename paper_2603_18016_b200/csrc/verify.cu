@@ -61,6 +61,7 @@ struct Params {
   // output: (M, S) of target row 0 of request b to t_stats_out[t_stats_rows[b]]
   // (skipped for a negative row) -- how the draft sampler publishes them
   float2* t_stats_out; const int32_t* t_stats_rows;
+  int voff;  // vocabulary offset of this logits shard (greedy partials of a TP rank)
   // replay mode (null: the real test): accept exactly min(forced[b], k_b)
   // drafts, then emit the target's token at that row -- GpuBackend's
   // acceptance="replay" commits the reference's coin-flip counts
@@ -379,8 +380,45 @@ verify_stats(const Params p) {
                    : make_float4(PSD_NEG_INF, PSD_NEG_INF, PSD_NEG_INF, PSD_NEG_INF);
     }
   }
-  const float2 part = slice_partial<SAMPLE>(v, base, n, p.c);
+  float2 part = slice_partial<SAMPLE>(v, base, n, p.c);
+  if (!SAMPLE && p.voff && __float_as_int(part.y) != 0x7fffffff)
+    part.y = __int_as_float(__float_as_int(part.y) + p.voff);
   if (tid == 0) p.part[(b * p.R + r) * p.NS + slice] = part;
+}
+
+// greedy over W vocabulary shards (tensor-parallel LM head):
+// partials [W][B][K+1][NS] (max, global argmax index); one CTA per request,
+// row r folded by thread r (argmax: any order, ties -> lowest index), then
+// the same ballot test as verify_fold.  Every rank runs it on the gathered
+// partials and reaches the same decision.
+__global__ void __launch_bounds__(kThreads)
+verify_fold_sharded(const Params p, int W) {
+  pdl_wait();
+  pdl_trigger();
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kb = p.len[b];
+  __shared__ int sG[PSD_MAX_K + 1];
+  if (tid <= kb) {
+    psd_vi a = {PSD_NEG_INF, 0x7fffffff};
+    const size_t per_w = (size_t)p.B * p.R * p.NS;
+    for (int w = 0; w < W; ++w)
+      for (int q = 0; q < p.NS; ++q) {
+        const float2 v = __ldcg(p.part + w * per_w + ((size_t)b * p.R + tid) * p.NS + q);
+        if (__float_as_int(v.y) != 0x7fffffff) a = psd_argmax2(a, psd_vi{v.x, __float_as_int(v.y)});
+      }
+    sG[tid] = a.i;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int x = lane < kb ? p.ids[b * p.K + lane] : -1;
+    const bool ok = lane < kb && x == sG[lane];
+    const unsigned rej = __ballot_sync(0xffffffffu, !ok) & ((1u << kb) - 1u);
+    int a = rej ? __ffs(rej) - 1 : kb;
+    if (p.forced) a = min(max(__ldg(p.forced + b), 0), kb);
+    int32_t* o = p.out + b * (p.K + 1);
+    if (lane <= p.K) o[lane] = lane < a ? x : (lane == a ? sG[a] : -1);
+    if (lane == 0) p.acc[b] = a;
+  }
 }
 
 // greedy: fold + decide, one CTA per request
@@ -719,6 +757,39 @@ int psd_verify_greedy(const float* target_logits, int64_t t_stride_b, int64_t t_
                       void* stream) {
   return psd_verify_greedy_forced(target_logits, t_stride_b, t_stride_i, V, draft_ids, draft_len,
                                   B, K, nullptr, accepted_len, out_tokens, ws, ws_bytes, stream);
+}
+
+size_t psd_verify_partials_count(int B, int K, int V) {
+  return (size_t)B * (K + 1) * ((V + PSD_SLICE - 1) / PSD_SLICE) * 2;
+}
+
+int psd_verify_greedy_partials(const float* target_logits, int64_t t_stride_b,
+                               int64_t t_stride_i, int V, int vocab_offset,
+                               const int32_t* draft_len, int B, int K, float* partials,
+                               void* stream) {
+  if (!partials) return (int)cudaErrorInvalidValue;
+  int rc = check_common(target_logits, t_stride_b, t_stride_i, V, B, K, partials, 1, 0);
+  if (rc) return rc;
+  Params p{};
+  p.t = target_logits; p.tsb = t_stride_b; p.tsi = t_stride_i; p.V = V; p.len = draft_len;
+  p.c = psd_scale(1.0f); p.B = B; p.K = K; p.voff = vocab_offset;
+  p.part = reinterpret_cast<float2*>(partials);
+  p.NS = (V + PSD_SLICE - 1) / PSD_SLICE; p.NB = (V + PSD_SBLK - 1) / PSD_SBLK; p.R = K + 1;
+  return (int)launch_stats<false>(p, (cudaStream_t)stream);
+}
+
+int psd_verify_greedy_fold(const float* partials, int W, int V_shard, const int32_t* draft_ids,
+                           const int32_t* draft_len, int B, int K, const int32_t* forced_len,
+                           int32_t* accepted_len, int32_t* out_tokens, void* stream) {
+  if (!partials || W < 1 || V_shard <= 0 || B <= 0 || K < 0 || K > PSD_MAX_K)
+    return (int)cudaErrorInvalidValue;
+  Params p{};
+  p.ids = draft_ids; p.len = draft_len; p.B = B; p.K = K; p.forced = forced_len;
+  p.acc = accepted_len; p.out = out_tokens;
+  p.part = reinterpret_cast<float2*>(const_cast<float*>(partials));
+  p.NS = (V_shard + PSD_SLICE - 1) / PSD_SLICE; p.R = K + 1;
+  return (int)psd::launch(verify_fold_sharded, dim3(B), dim3(kThreads), 0, (cudaStream_t)stream,
+                          p, W);
 }
 
 int psd_verify_greedy_forced(const float* target_logits, int64_t t_stride_b, int64_t t_stride_i,

@@ -195,13 +195,16 @@ class GpuBackend:
             self.s_draft = (torch.cuda.Stream(dev, priority=hi if prio == "draft" else lo)
                             if dual_stream else self.s_target)
             torch.cuda.synchronize(dev)
-        # fused k-step greedy draft decode (csrc/decode_mk.cu): one persistent
-        # kernel per draft loop instead of ~130 launches per step.
-        # PSD_FUSED_DRAFT=0 keeps the per-kernel forward (A/B runs).
+        # fused k-step greedy draft decode (csrc/decode_mk.cu, experimental
+        # build only): one persistent kernel per draft loop instead of ~130
+        # launches per step; measured 35 % slower, off by default
         import os
         self.mk = None
         want_mk = fused_draft if fused_draft is not None else \
             os.environ.get("PSD_FUSED_DRAFT", "0") == "1"
+        if want_mk and not native.has("psd_mk_create"):
+            raise ConfigError("fused_draft needs the experimental build (PSD_EXPERIMENTAL=1 "
+                              "python -m paper_2603_18016_b200.build_native)")
         if want_mk and has_d and mode == "greedy":
             grid = mk_grid or int(os.environ.get("PSD_MK_GRID", "0"))
             with torch.cuda.device(dev):
@@ -229,6 +232,7 @@ class GpuBackend:
         self.qstats_cache = os.environ.get("PSD_QSTATS_CACHE", "1") == "1"
         # set when a dedicated draft GPU ships the q statistics with the q rows
         self.qstats_remote = False
+        self.c3_part = self.c3_all = None  # TP greedy: K1 partials of this shard / all
         self.seed_draft = (seed * 0x9E3779B1 + 0xD7A7) & 0xFFFFFFFFFFFF
         self.seed_verify = (seed * 0x85EBCA77 + 0x7E51) & 0xFFFFFFFFFFFF
         self.capture_verify = None  # set to a list to record K1 inputs (tests)
@@ -756,8 +760,12 @@ class GpuBackend:
                                             self.slot_tok.data_ptr(),
                                             fwd.view("gather_src").data_ptr(), M, st),
                      "verify gather")
+        # tensor-parallel greedy target over peer memory: each rank reduces its
+        # LM-head vocabulary shard to K1 partials, the ranks all-gather the
+        # partials (KBs instead of M x V logits) and fold them identically
+        c3 = (self.mode == "greedy" and fwd.comm is not None and self.capture_verify is None)
         fwd.run(M, nb, K1, M, self.tlogits, self.tshape.vocab,
-                bigram=(self.succ_t, self.beta_target))
+                bigram=(self.succ_t, self.beta_target), shard_out=c3)
         v_len = self.v_meta[:nb]
         v_slot = self.v_meta[B:B + nb]
         forced = self.v_meta[2 * B:2 * B + nb] if self.replay else None
@@ -771,7 +779,24 @@ class GpuBackend:
             v_ids = self.v_ids[:nb, :0]
         logits = self.tlogits[:M].view(nb, K1, -1)
         out = self.v_out[:nb * K1].view(nb, K1)
-        if self.mode == "greedy":
+        if c3:
+            tm = self.target
+            vs, vp = tm.vocab_shard, tm.shape.vocab
+            cnt = lib.psd_verify_partials_count(nb, kmax, vs)
+            if self.c3_part is None:
+                full = lib.psd_verify_partials_count(B, self.k_max, vs)
+                self.c3_part = torch.empty(full, dtype=torch.float32, device=self.device)
+                self.c3_all = torch.empty(tm.tp[1] * full, dtype=torch.float32,
+                                          device=self.device)
+            native.check(lib.psd_verify_greedy_partials(
+                fwd.lshard.data_ptr(), K1 * vp, vp, vs, tm.tp[0] * vs, v_len.data_ptr(), nb,
+                kmax, self.c3_part.data_ptr(), st), "verify partials (shard)")
+            fwd.comm.allgather(self.c3_part[:cnt], self.c3_all)
+            native.check(lib.psd_verify_greedy_fold(
+                self.c3_all.data_ptr(), tm.tp[1], vs, v_ids.data_ptr(), v_len.data_ptr(), nb,
+                kmax, forced.data_ptr() if forced is not None else None, self.v_acc.data_ptr(),
+                out.data_ptr(), st), "verify fold (shards)")
+        elif self.mode == "greedy":
             ops.verify_greedy(logits, v_ids, v_len, self.v_acc[:nb], out, forced_len=forced)
         else:
             native.check(lib.psd_philox_uniforms(

@@ -343,7 +343,15 @@ class Forward:
         self.act = torch.empty(T, s.ffn_padded, dtype=bf, device=dev)
         self.xf = torch.empty(max_logit_rows, s.hidden, dtype=bf, device=dev)
         self.prev = torch.empty(max_logit_rows, dtype=torch.int32, device=dev)
+        self.comm = None
         if model.tp is not None and model.tp[1] > 1:
+            import os
+            if os.environ.get("PSD_TP_COMM", "peer") == "peer":
+                # C2 over NVLink peer memory: the split-K reduction of the
+                # row-parallel O / down GEMMs fused with the cross-rank sum
+                # (csrc/comm.cu); PSD_TP_COMM=dist keeps torch.distributed
+                from .comm import PeerComm
+                self.comm = PeerComm(model.tp[2], buf_bytes=T * s.hidden * 4, device=dev)
             self.lshard = torch.empty(max_logit_rows * s.vocab, dtype=torch.float32, device=dev)
             self.lgather = torch.empty(model.tp[1] * max_logit_rows * s.vocab,
                                        dtype=torch.float32, device=dev)
@@ -403,11 +411,21 @@ class Forward:
         self._cur = 0
 
     # ---- tensor parallelism (target TP) ---------------------
-    def _allreduce(self, n: int) -> None:
-        """Sum the ranks' row-parallel partial outputs (fp32 split-K partials:
-        the sum is linear, so the consumer's split reduction stays unchanged)."""
+    def _tp_reduce(self, S: int, n: int) -> int:
+        """Sum the ranks' row-parallel partial outputs (S fp32 split-K slices of
+        n = M * H floats); returns the slice count the consumer reduces.
+
+        Peer memory (default): one kernel sums the local splits and the ranks'
+        sums in fixed (rank, split) order into slice 0 -- n floats cross
+        NVLink per rank instead of S * n, and every rank holds identical bits
+        (consumer: 1 slice).  torch.distributed fallback: all-reduce of all S
+        slices (linear, so the consumer's split reduction is unchanged)."""
+        if self.comm is not None:
+            self.comm.allreduce_partials(self.part, S, n, n, self.part)
+            return 1
         import torch.distributed as dist
-        dist.all_reduce(self.part[:n], group=self.model.tp[2])
+        dist.all_reduce(self.part[:S * n], group=self.model.tp[2])
+        return S
 
     def _gather_logits(self, logits: torch.Tensor, ld: int, R: int) -> None:
         import torch.distributed as dist
@@ -449,10 +467,14 @@ class Forward:
 
     def run(self, n_tokens: int, n_seqs: int, max_q_len: int, n_logit_rows: int,
             logits: torch.Tensor | None, logits_ld: int = 0, bigram=None,
-            set_index: int = 0) -> None:
+            set_index: int = 0, shard_out: bool = False) -> None:
         """Enqueue the forward on the current stream.  ``tokens`` may be
         filled on device beforehand (draft loop); ``logits`` (fp32, row pitch
-        ``logits_ld``) receives the LM-head output of ``logit_rows``."""
+        ``logits_ld``) receives the LM-head output of ``logit_rows``.
+        shard_out (tensor-parallel target): keep this rank's vocabulary shard
+        in ``lshard`` ([rows, vocab shard padded], bigram bias applied to the
+        shard's columns) instead of all-gathering full rows -- the greedy
+        verifier reduces shards to partials."""
         m = self.model
         s = m.shape
         lib = m._lib
@@ -517,9 +539,10 @@ class Forward:
                      "attention")
             _chk(lib.psd_gemm_partials(self.attn.data_ptr(), Dq, M, Dq, L["wo"].data_ptr(), Dq, H,
                                        part, partn, self.splits_hint, nsp, st), "gemm o")
+            S_o = nsp._obj.value
             if tp:  # row-parallel O: sum the ranks' partial outputs
-                self._allreduce(nsp._obj.value * M * H)
-            _chk(lib.psd_add_rmsnorm(X, H, part, nsp._obj.value, M * H, H, None,
+                S_o = self._tp_reduce(S_o, M * H)
+            _chk(lib.psd_add_rmsnorm(X, H, part, S_o, M * H, H, None,
                                      L["mlp_norm"].data_ptr(), self.xn.data_ptr(), H, M, H,
                                      s.rms_eps, 1, st), "add+mlp norm")
             _chk(lib.psd_gemm_bf16(self.xn.data_ptr(), H, M, H, L["wgu"].data_ptr(), H, 2 * Fp,
@@ -527,9 +550,9 @@ class Forward:
                                    st), "gemm gate/up")
             _chk(lib.psd_gemm_partials(self.act.data_ptr(), Fp, M, Fp, L["wdown"].data_ptr(), Fp,
                                        H, part, partn, self.splits_hint, nsp, st), "gemm down")
-            if tp:  # row-parallel down
-                self._allreduce(nsp._obj.value * M * H)
             prev_S = nsp._obj.value
+            if tp:  # row-parallel down
+                prev_S = self._tp_reduce(prev_S, M * H)
         if n_logit_rows == 0 or logits is None:
             return  # prefill: only the KV cache is needed
         R = n_logit_rows
@@ -539,10 +562,22 @@ class Forward:
         V = m.full_vocab
         ld = logits_ld or V
         if tp:
-            # vocab-parallel LM head: this rank's slice, all-gathered into full rows
+            # vocab-parallel LM head: this rank's slice (all-gathered into full
+            # rows unless the caller consumes the shard)
             _chk(lib.psd_gemm_bf16(self.xf.data_ptr(), H, R, H, m.lm_head.data_ptr(), H, s.vocab,
                                    self.lshard.data_ptr(), s.vocab, native.EPI_F32, None, 0, 0,
                                    ws, wsn, st), "gemm lm_head shard")
+            if shard_out:
+                if bigram is not None and bigram[1] != 0.0:
+                    v0 = tp[0] * m.vocab_shard
+                    _chk(lib.psd_index_copy_i32(self.prev.data_ptr(), None,
+                                                v["tokens"].data_ptr(),
+                                                v["logit_rows"].data_ptr(), R, st), "prev tokens")
+                    _chk(lib.psd_bigram_bias_range(self.lshard.data_ptr(), s.vocab,
+                                                   self.prev.data_ptr(), R, bigram[0].data_ptr(),
+                                                   V, float(bigram[1]), v0, v0 + m.vocab_shard,
+                                                   st), "bigram shard")
+                return
             self._gather_logits(logits, ld, R)
         else:
             _chk(lib.psd_gemm_bf16(self.xf.data_ptr(), H, R, H, m.lm_head.data_ptr(), H, s.vocab,

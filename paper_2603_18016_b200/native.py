@@ -47,6 +47,7 @@ SIGNATURES: dict[str, tuple] = {
     "psd_attention_rope": (_i, [_p, _i, _sz, _p, _p, _p, _p, _p, _p, _p, _i, _p, _p, _p, _p, _p,
                                 _i, _i, _i, _i, _i, _i, _f, _p, _p]),
     "psd_bigram_bias": (_i, [_p, _i64, _p, _i, _p, _i, _f, _p]),
+    "psd_bigram_bias_range": (_i, [_p, _i64, _p, _i, _p, _i, _f, _i, _i, _p]),
     "psd_philox_uniforms": (_i, [_c.c_uint64, _p, _p, _i, _i, _i, _p, _p]),
     "psd_rope_kv_partials": (_i, [_p, _i, _sz, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _p, _p]),
     "psd_copy_rows_f32": (_i, [_p, _p, _i64, _p, _i64, _i, _i, _p]),
@@ -59,6 +60,9 @@ SIGNATURES: dict[str, tuple] = {
                                       _p]),
     "psd_verify_sample_forced": (_i, [_p, _i64, _i64, _i, _p, _p, _i64, _i64, _i, _p, _p, _p,
                                       _f, _i, _i, _p, _p, _p, _p, _i64, _p, _p, _p, _sz, _p]),
+    "psd_verify_partials_count": (_sz, [_i, _i, _i]),
+    "psd_verify_greedy_partials": (_i, [_p, _i64, _i64, _i, _i, _p, _i, _i, _p, _p]),
+    "psd_verify_greedy_fold": (_i, [_p, _i, _i, _p, _p, _i, _i, _p, _p, _p, _p]),
     "psd_commit": (_i, [_p, _p, _i, _p, _i, _p, _p, _i, _p, _i, _p]),
     "psd_index_copy_i32": (_i, [_p, _p, _p, _p, _i, _p]),
     "psd_fill_uniform_bf16": (_i, [_p, _sz, _c.c_uint64, _f, _p]),
@@ -70,9 +74,11 @@ SIGNATURES: dict[str, tuple] = {
     "psd_comm_handle_bytes": (_sz, []),
     "psd_comm_create": (_i, [_i, _i, _sz, _sz, _c.POINTER(_p), _p]),
     "psd_comm_open": (_i, [_p, _p]),
+    "psd_comm_create_local": (_i, [_i, _p, _sz, _sz, _p]),
     "psd_comm_destroy": (_i, [_p]),
     "psd_tp_allreduce_partials": (_i, [_p, _p, _i, _sz, _sz, _p, _p]),
     "psd_tp_allreduce_f32": (_i, [_p, _p, _sz, _p]),
+    "psd_tp_allgather_f32": (_i, [_p, _p, _sz, _p, _p]),
     "psd_p2p_put_i32": (_i, [_p, _i, _p, _i, _p]),
     "psd_p2p_get_i32": (_i, [_p, _i, _p, _i, _p]),
     "psd_mk_smem_bytes": (_sz, []),
@@ -103,9 +109,20 @@ EPI_BF16, EPI_F32, EPI_RESID, EPI_SILU, EPI_PARTIAL = 0, 1, 2, 3, 4
 _lib = None
 
 
-def header_symbols() -> list[str]:
-    """Every function declared in include/psd.h."""
-    with open(HEADER) as fh:
+# include/psd_experimental.h (PSD_EXPERIMENTAL=1 builds only)
+EXPERIMENTAL = ("psd_tiled_weight_bytes", "psd_tile_weights", "psd_gemm_tiled",
+                "psd_mk_smem_bytes", "psd_mk_create", "psd_mk_destroy", "psd_mk_grid",
+                "psd_mk_launch", "psd_mk_n_ops", "psd_mk_launch_traced")
+
+
+def has(name: str) -> bool:
+    """Whether the loaded library exports `name` (experimental symbols)."""
+    return getattr(load(), name, None) is not None
+
+
+def header_symbols(path: str = HEADER) -> list[str]:
+    """Every function declared in include/psd.h (or `path`)."""
+    with open(path) as fh:
         text = fh.read()
     return sorted(set(re.findall(r"^\s*(?:int|size_t|void|float|long long)\s*\**\s*(psd_\w+)\s*\(",
                                  text, re.M)))
@@ -124,7 +141,11 @@ def load():
     except OSError as exc:
         raise NativeError(f"cannot load {LIB_PATH}: {exc}") from exc
     for name, (res, args) in SIGNATURES.items():
-        fn = getattr(lib, name)
+        fn = getattr(lib, name, None)
+        if fn is None:
+            if name in EXPERIMENTAL:
+                continue  # built only with PSD_EXPERIMENTAL=1
+            raise NativeError(f"{LIB_PATH} does not export {name}")
         fn.restype = res
         fn.argtypes = args
     _lib = lib

@@ -41,15 +41,16 @@ def _worker(rank, port, q):
     comm = PeerComm(buf_bytes=8 << 20, mbox_bytes=1 << 16, device=dev)
     errs = []
     S, n = 3, 4096 * 12
-    for call in range(5):  # both staging parities, several epochs
-        mine = _data(rank, call, S, n)
+    for call in range(6):  # both staging parities, several epochs, varying grids
+        nc = n if call % 2 == 0 else 1024 + 4 * call
+        mine = _data(rank, call, S, nc)
         part = mine.to(dev).contiguous()
-        out = torch.empty(n, device=dev)
-        comm.allreduce_partials(part.view(-1), S, n, n, out)
+        out = torch.empty(nc, device=dev)
+        comm.allreduce_partials(part.view(-1), S, nc, nc, out)
         torch.cuda.synchronize()
         ref = None
         for r in range(2):  # ranks in order, each its splits in order
-            d = _data(r, call, S, n)
+            d = _data(r, call, S, nc)
             acc = d[0].clone()
             for s in range(1, S):
                 acc = acc + d[s]
@@ -61,7 +62,7 @@ def _worker(rank, port, q):
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=st):
         comm.allreduce_partials(buf, S, n, n, buf)
-    for call in range(5, 8):
+    for call in range(6, 9):
         buf.copy_(_data(rank, call, S, n).view(-1).to(dev))
         g.replay()
         torch.cuda.synchronize()
@@ -106,3 +107,57 @@ def test_peer_allreduce_and_mailbox(cuda_device):
     for rank, errs, got in res:
         assert all(errs), (rank, errs)
         assert all(got), (rank, got)
+
+
+def test_local_group_allreduce_gather_mailbox(cuda_device):
+    """Two ranks driven by one process on one GPU (psd_comm_create_local), each
+    on its own stream so their kernels run concurrently: the same protocol as
+    across GPUs, without relying on time slicing between processes."""
+    import torch
+
+    from paper_2603_18016_b200.comm import PeerComm
+    dev = cuda_device
+    comms = PeerComm.local_group([dev, dev], buf_bytes=4 << 20, mbox_bytes=1 << 16)
+    streams = [torch.cuda.Stream(dev) for _ in comms]
+    S, n = 3, 4096 * 10
+
+    def both(fn):
+        torch.cuda.synchronize()
+        for r, (c, st) in enumerate(zip(comms, streams)):
+            with torch.cuda.stream(st):
+                fn(r, c)
+        torch.cuda.synchronize()
+
+    for call in range(6):  # varying sizes: the per-call grid changes
+        nc = n if call % 2 == 0 else 1024 + 4 * call
+        parts = [_data(r, call, S, nc).to(dev) for r in range(2)]
+        outs = [torch.empty(nc, device=dev) for _ in range(2)]
+        both(lambda r, c: c.allreduce_partials(parts[r].view(-1), S, nc, nc, outs[r]))
+        ref = None
+        for r in range(2):
+            d = _data(r, call, S, nc)
+            acc = d[0] + d[1] + d[2]
+            ref = acc if ref is None else ref + acc
+        for r in range(2):
+            assert torch.equal(outs[r].cpu(), ref), (call, r)
+    # all-gather
+    src = [torch.randn(n, device=dev) for _ in range(2)]
+    gat = [torch.empty(2 * n, device=dev) for _ in range(2)]
+    both(lambda r, c: c.allgather(src[r], gat[r]))
+    for r in range(2):
+        assert torch.equal(gat[r].view(2, n)[0], src[0]) and torch.equal(gat[r].view(2, n)[1],
+                                                                         src[1])
+    # mailbox, both directions, several rounds
+    for i in range(3):
+        msg = [torch.arange(64, dtype=torch.int32, device=dev) + 1000 * i + 7 * r
+               for r in range(2)]
+        dst = [torch.empty(64, dtype=torch.int32, device=dev) for _ in range(2)]
+
+        def xchg(r, c):
+            c.put(1 - r, msg[r])
+            c.get(1 - r, dst[r])
+        both(xchg)
+        for r in range(2):
+            assert torch.equal(dst[r], msg[1 - r])
+    for c in comms:
+        c.close()

@@ -110,6 +110,8 @@ def test_tiny_model_gemm_shapes(cuda_device, M, N, K, epi):
 @pytest.mark.parametrize("M,N,K,epi", [(192, 1024, 4096, "bf16"), (32, 2048, 1000, "silu"),
                                        (63, 1024, 256, "f32"), (300, 512, 704, "bf16")])
 def test_gemm_pretiled_weights(cuda_device, M, N, K, epi):
+    if not native.has("psd_gemm_tiled"):
+        pytest.skip("experimental build only (PSD_EXPERIMENTAL=1)")
     dev = cuda_device
     g = torch.Generator(device=dev).manual_seed(M * 3 + N + K)
     x = torch.randn(M, K, device=dev, generator=g).to(bf)

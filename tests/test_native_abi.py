@@ -11,7 +11,10 @@ from paper_2603_18016_b200 import native
 def test_header_declares_signatures():
     declared = native.header_symbols()
     assert declared, "no psd_* declarations found in include/psd.h"
-    assert sorted(native.SIGNATURES) == declared
+    exp = native.header_symbols(os.path.join(os.path.dirname(native.HEADER),
+                                             "psd_experimental.h"))
+    assert sorted(exp) == sorted(native.EXPERIMENTAL)
+    assert sorted(native.SIGNATURES) == sorted(declared + exp)
 
 
 def test_library_exports_every_header_symbol():

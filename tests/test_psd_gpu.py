@@ -188,6 +188,9 @@ def test_continuous_batching_preemption_and_k_overrides_on_gpu(cuda_device):
 
 @pytest.mark.parametrize("draft", ["llama-3.2-1b", "tiny-draft"])
 def test_fused_draft_decode_matches_per_kernel_forward(cuda_device, draft):
+    from paper_2603_18016_b200 import native
+    if not native.has("psd_mk_create"):
+        pytest.skip("experimental build only (PSD_EXPERIMENTAL=1)")
     """The fused k-step draft decode (csrc/decode_mk.cu, one persistent kernel)
     proposes the same draft tokens as the per-kernel forward: identical
     drafted / accepted counts in every step and identical outputs."""

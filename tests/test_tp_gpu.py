@@ -30,7 +30,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _logits(model_tp, seed=3):
+def _logits(model_tp, seed=3, splits_hint=0):
     """One prefill + logits of every prompt token through Forward."""
     from paper_2603_18016_b200.model import PRESETS, Forward, Transformer
     dev = torch.device("cuda:0")
@@ -41,6 +41,7 @@ def _logits(model_tp, seed=3):
     bt[0, :4] = torch.tensor([1, 2, 3, 4])
     bt[1, :4] = torch.tensor([5, 6, 7, 8])
     fwd = Forward(m, 128, 8, 64, bt)
+    fwd.splits_hint = splits_hint
     rng = np.random.default_rng(0)
     lens = [23, 40]
     toks = [rng.integers(0, shape.vocab, n).tolist() for n in lens]
@@ -63,9 +64,9 @@ def _logits(model_tp, seed=3):
     return logits.cpu().numpy()
 
 
-def _worker(rank, port, q):
+def _worker(rank, port, q, transport="peer", graphs=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE="2",
-                      RANK=str(rank), LOCAL_RANK=str(rank))
+                      RANK=str(rank), LOCAL_RANK=str(rank), PSD_TP_COMM=transport)
     import torch.distributed as dist
 
     from paper_2603_18016_b200 import SimConfig, make_requests, run
@@ -73,24 +74,34 @@ def _worker(rank, port, q):
     dist.init_process_group("gloo", init_method="env://")
     group = dist.group.WORLD
     lg = _logits((rank, 2, group))
-    gb = GpuBackend("tiny-target-tp", "tiny-draft", tp=(rank, 2, group), **KW)
+    gb = GpuBackend("tiny-target-tp", "tiny-draft", tp=(rank, 2, group),
+                    **dict(KW, use_graphs=graphs))
     cfg = SimConfig(mode="psd", m=8, k=4)
     st, rep = run(cfg, make_requests([24] * 16, prompt_len=16), backend=gb)
     q.put((rank, lg, [r.output_ids for r in st.request_list()], rep.finished))
     dist.destroy_process_group()
 
 
-def test_tp2_target_matches_unsharded(cuda_device):
+@pytest.mark.parametrize("transport,graphs", [("peer", False), ("peer", True), ("dist", False)],
+                         ids=["peer", "peer-graphs", "torch-dist"])
+def test_tp2_target_matches_unsharded(cuda_device, transport, graphs):
+    """peer: C2 all-reduce and the C3 greedy shard partials over CUDA-IPC peer
+    memory (csrc/comm.cu), also inside CUDA graphs; torch-dist: all-reduce /
+    all-gather through torch.distributed."""
+    from tests._parity import noise_floor_ok
     from paper_2603_18016_b200 import SimConfig, make_requests, run
     from paper_2603_18016_b200.gpu import GpuBackend
     ref_logits = _logits(None)
+    # the unsharded model's own reordering noise: another valid split-K count
+    alt_logits = _logits(None, splits_hint=1)
     st, rep = run(SimConfig(mode="psd", m=8, k=4), make_requests([24] * 16, prompt_len=16),
                   backend=GpuBackend("tiny-target-tp", "tiny-draft", **KW))
     ref = [r.output_ids for r in st.request_list()]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, port, q, transport, graphs))
+             for r in range(2)]
     for p in procs:
         p.start()
     got = dict((m[0], m[1:]) for m in (q.get(timeout=600) for _ in procs))
@@ -99,7 +110,9 @@ def test_tp2_target_matches_unsharded(cuda_device):
         assert p.exitcode == 0
     for r in (0, 1):
         lg, outs, finished = got[r]
-        err = np.abs(lg - ref_logits).max()
-        assert err <= 1e-2 * np.abs(ref_logits).max(), err
+        # the sharded forward sums in another order (rank slices, then ranks);
+        # it must sit within the unsharded model's own reordering noise floor
+        ok, info = noise_floor_ok(lg, ref_logits, alt_logits)
+        assert ok, info
         assert finished == 16
         assert outs == ref
