@@ -578,7 +578,16 @@ def run_ours(args) -> None:
         from paper_2603_18016_b200.pair import (DraftServer, GpuDraftEngine, GpuTargetEngine,
                                                 PairLink, PairTarget)
         peer = rank + 1 if rank % 2 == 0 else rank - 1
-        link = PairLink(peer, dev if args.dist_backend == "nccl" else None)
+        # drafted ids through a 2-rank peer-memory mailbox (csrc/comm.cu) by
+        # default; PSD_PAIR_LINK=dist keeps them on dist.send / recv
+        pair_groups = [torch.distributed.new_group([2 * t, 2 * t + 1])
+                       for t in range(world // 2)]
+        comm = None
+        if os.environ.get("PSD_PAIR_LINK", "peer") == "peer":
+            from paper_2603_18016_b200.comm import PeerComm
+            comm = PeerComm(pair_groups[rank // 2], buf_bytes=1 << 12, mbox_bytes=1 << 20,
+                            device=dev)
+        link = PairLink(peer, dev if args.dist_backend == "nccl" else None, comm=comm)
         if not is_draft_rank:
             backend = PairTarget(GpuTargetEngine(be), link)
 

@@ -48,9 +48,13 @@ K_STEP, K_STOP = 0, 1
 class PairLink:
     """Length-prefixed int32 messages to / from one peer rank."""
 
-    def __init__(self, peer: int, device=None) -> None:
+    def __init__(self, peer: int, device=None, comm=None) -> None:
         self.peer = peer
         self.device = device  # CUDA device for NCCL, None for gloo
+        # comm (a 2-rank comm.PeerComm): drafted ids go through its device
+        # mailbox over NVLink peer memory (psd_p2p_put/get_i32) instead of
+        # dist.send / recv; commands and q rows still use dist
+        self.comm = comm
         self.bytes_sent = 0
         self.bytes_recv = 0
 
@@ -83,6 +87,10 @@ class PairLink:
         """Flat int32 ids (device tensor under NCCL, else host) as one message."""
         t = ids if isinstance(ids, torch.Tensor) else torch.from_numpy(
             np.ascontiguousarray(ids, dtype=np.int32))
+        if self.comm is not None:
+            self.comm.put(1 - self.comm.rank, t.to(self.comm.device).contiguous())
+            self.bytes_sent += 4 * t.numel()
+            return
         if self.device is None:
             t = t.cpu()
         elif not t.is_cuda:
@@ -91,7 +99,13 @@ class PairLink:
         self.bytes_sent += 4 * t.numel()
 
     def recv_ids(self, n: int) -> torch.Tensor:
-        """n int32 (device tensor under NCCL, host under gloo); no host sync."""
+        """n int32 (device tensor under NCCL / the peer mailbox, host under
+        gloo); no host sync."""
+        if self.comm is not None:
+            buf = torch.empty(n, dtype=torch.int32, device=self.comm.device)
+            self.comm.get(1 - self.comm.rank, buf)
+            self.bytes_recv += 4 * n
+            return buf
         buf = torch.empty(n, dtype=torch.int32,
                           device=self.device if self.device is not None else "cpu")
         dist.recv(buf, self.peer)

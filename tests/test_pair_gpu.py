@@ -30,7 +30,7 @@ def _cfg_reqs():
                                                          prompt_len=10)
 
 
-def _worker(rank, port, q, extra=None):
+def _worker(rank, port, q, extra=None, mailbox=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE="2",
                       RANK=str(rank), LOCAL_RANK=str(rank))
     import torch.distributed as dist
@@ -40,20 +40,27 @@ def _worker(rank, port, q, extra=None):
     from paper_2603_18016_b200.pair import (DraftServer, GpuDraftEngine, GpuTargetEngine,
                                             PairLink, PairTarget)
     dist.init_process_group("gloo", init_method="env://")
+    comm = None
+    if mailbox:  # drafted ids through the peer-memory mailbox (csrc/comm.cu)
+        import torch
+
+        from paper_2603_18016_b200.comm import PeerComm
+        comm = PeerComm(mbox_bytes=1 << 16, buf_bytes=1 << 12, device=torch.device("cuda:0"))
     if rank == 0:
         gb = GpuBackend("tiny-target", "tiny-draft", roles=("target",), **KW, **(extra or {}))
-        be = PairTarget(GpuTargetEngine(gb), PairLink(1))
+        be = PairTarget(GpuTargetEngine(gb), PairLink(1, comm=comm))
         cfg, reqs = _cfg_reqs()
         st, rep = run(cfg, reqs, backend=be)
         be.stop()
         q.put(("out", [r.output_ids for r in st.request_list()], rep.finished))
     else:
         gb = GpuBackend("tiny-target", "tiny-draft", roles=("draft",), **KW, **(extra or {}))
-        q.put(("steps", DraftServer(GpuDraftEngine(gb), PairLink(0)).serve()))
+        q.put(("steps", DraftServer(GpuDraftEngine(gb), PairLink(0, comm=comm)).serve()))
     dist.destroy_process_group()
 
 
-def test_pair_gpu_engines_match_single_process(cuda_device):
+@pytest.mark.parametrize("mailbox", [False, True], ids=["dist", "peer-mailbox"])
+def test_pair_gpu_engines_match_single_process(cuda_device, mailbox):
     from paper_2603_18016_b200 import run
     from paper_2603_18016_b200.gpu import GpuBackend
     cfg, reqs = _cfg_reqs()
@@ -62,7 +69,7 @@ def test_pair_gpu_engines_match_single_process(cuda_device):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, port, q, None, mailbox)) for r in range(2)]
     for p in procs:
         p.start()
     got = dict((m[0], m[1:]) for m in (q.get(timeout=600) for _ in procs))
