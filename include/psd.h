@@ -145,6 +145,12 @@ int psd_verify_greedy_fold(const float* partials, int W, int V_shard, const int3
 /* Cap the CTAs of subsequently enqueued (or captured) GEMM grids (0 = all SMs):
  * the verify forward runs beside the draft loop on one GPU. */
 void psd_gemm_set_max_ctas(int n);
+/* Whole-K geometry for subsequently enqueued GEMMs (1 = on): no k-splitting
+ * (one split for the grid split-K GEMMs, whole tiles only for stream-K), so
+ * every output element is summed over K in the same order for any M -- the
+ * prefill passes use it, making a prompt's KV cache independent of which
+ * prompts share its prefill chunk. */
+void psd_gemm_set_whole_k(int on);
 /* Diagnostics: a device buffer of [CTAs][16] u64 that subsequent stream-K GEMMs
  * fill with %globaltimer stamps per CTA (entry, first operands, last MMA
  * issued, last accumulator ready, epilogue done, segments, fast finishes, rounds);

@@ -1060,6 +1060,15 @@ std::atomic<int>& max_ctas_cap() {
   return v;
 }
 
+// whole-K geometry (psd_gemm_set_whole_k): no k-splitting at all -- grid
+// split-K runs one split, stream-K GEMMs run whole tiles only -- so every
+// output element is one CTA's sequential accumulation over K whatever M is
+// (prefill chunks of any composition give a prompt the same KV cache)
+std::atomic<int>& whole_k() {
+  static std::atomic<int> v{0};
+  return v;
+}
+
 // stream-K timeline buffer (psd_gemm_set_trace; null = off)
 std::atomic<unsigned long long*>& sk_trace() {
   static std::atomic<unsigned long long*> v{nullptr};
@@ -1124,6 +1133,7 @@ SKPlan sk_plan(int M, int N, int K, bool allow_nt2 = true) {
   p.D = sk_dp_enabled() ? p.G * (p.tiles / p.G) : 0;
   if (p.D > 0 && p.D < p.tiles && (long long)(p.tiles - p.D) * p.KB < (long long)p.G * (p.KB / 2))
     p.D -= p.G;
+  if (whole_k().load(std::memory_order_relaxed)) p.D = p.tiles;
   p.U = (long long)(p.tiles - p.D) * p.KB;
   p.part_bytes = (size_t)p.G * 2 * p.nt * p.bn * BM * sizeof(float);
   // tickets live at a FIXED offset (start of the workspace) so GEMMs of any
@@ -1155,6 +1165,8 @@ extern "C" {
 
 void psd_gemm_set_max_ctas(int n) { max_ctas_cap().store(n > 0 ? n : 0); }
 
+void psd_gemm_set_whole_k(int on) { whole_k().store(on ? 1 : 0); }
+
 void psd_gemm_set_trace(void* trace) {
   sk_trace().store(static_cast<unsigned long long*>(trace));
 }
@@ -1171,6 +1183,7 @@ int psd_gemm_plan(int M, int N, int K, int epi, int splits_hint, int* splits_out
     // from the SM count, not the CTA cap: the split (and so the summation order
     // of every output element) must not depend on what runs beside the GEMM
     if (tiles < 120) splits = std::max(1, std::min(num_sms_raw() / tiles, kb_total / 4));
+    if (whole_k().load(std::memory_order_relaxed)) splits = 1;
   }
   splits = std::max(1, std::min(splits, kb_total));
   const int per = (kb_total + splits - 1) / splits;

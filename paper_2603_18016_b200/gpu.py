@@ -135,8 +135,9 @@ class GpuBackend:
             self.succ_t = torch.from_numpy(succ).to(dev)
             self.succ_d = torch.from_numpy(succ[:self.dshape.vocab].copy()).to(dev)
             B, K = max_batch, k_max
-            vt_tokens = max(B * (K + 1), prefill_chunk_tokens)
-            vd_tokens = max(2 * B, prefill_chunk_tokens)
+            # a prompt longer than a chunk is prefilled alone
+            vt_tokens = max(B * (K + 1), prefill_chunk_tokens, max_seq_len)
+            vd_tokens = max(2 * B, prefill_chunk_tokens, max_seq_len)
             self.tfwd = Forward(self.target, vt_tokens, max(B, 256), B * (K + 1),
                                 self.block_table, sets=1, max_kv_len=0) if has_t else None
             self.dfwd = Forward(self.draft, vd_tokens, max(B, 256), B, self.block_table,
@@ -467,9 +468,17 @@ class GpuBackend:
                           "q_pos0": np.asarray(q_pos0, np.int32),
                           "kv_len": np.asarray(kv_len, np.int32)})
             fwd.upload(1)
-            c0 = native.load().psd_launch_count()
-            fwd.run(len(toks), len(chunk), max(q_len), 0, None)
-            self.launches += native.load().psd_launch_count() - c0
+            lib = native.load()
+            c0 = lib.psd_launch_count()
+            # whole-K GEMM geometry: a prompt's KV cache is the same whatever
+            # else shares its chunk (requests are admitted in different groups
+            # by PSD, SD(m) and SD(2m) -- continuous batching)
+            lib.psd_gemm_set_whole_k(1)
+            try:
+                fwd.run(len(toks), len(chunk), max(q_len), 0, None)
+            finally:
+                lib.psd_gemm_set_whole_k(0)
+            self.launches += lib.psd_launch_count() - c0
 
     # ---- bucketed, graph-captured device passes ------------------------
     def _bucket(self, n: int) -> int:

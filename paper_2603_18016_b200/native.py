@@ -70,6 +70,7 @@ SIGNATURES: dict[str, tuple] = {
                                          _p]),
     "psd_launch_count": (_c.c_longlong, []),
     "psd_gemm_set_max_ctas": (None, [_i]),
+    "psd_gemm_set_whole_k": (None, [_i]),
     "psd_gemm_set_trace": (None, [_p]),
     "psd_comm_handle_bytes": (_sz, []),
     "psd_comm_create": (_i, [_i, _i, _sz, _sz, _c.POINTER(_p), _p]),

@@ -45,7 +45,13 @@ def runs(cuda_device):
                     make_requests([OUT_GPU] * N_REQ, prompt_len=PROMPT), backend=gb)
     sd, _ = run(SimConfig(mode="standard-sd", m=N_REQ // 2, k=K, sd_batch_factor=2),
                 make_requests([OUT_GPU] * N_REQ, prompt_len=PROMPT), backend=gb)
-    return gb, psd, prep, sd
+    # SD(m): batches of m, later requests admitted one by one as earlier ones
+    # finish (continuous batching), so prompts are prefilled in other groups
+    # than in PSD
+    sdm, _ = run(SimConfig(mode="standard-sd", m=N_REQ // 2, k=K, sd_batch_factor=1),
+                 make_requests([OUT_GPU - 3 * (i % 2) for i in range(N_REQ)], prompt_len=PROMPT),
+                 backend=gb)
+    return gb, psd, prep, sd, sdm
 
 
 @pytest.fixture(scope="module")
@@ -60,18 +66,22 @@ def cpu(runs):
 
 
 def test_psd_equals_sd_at_cfg2_shapes(runs):
-    gb, psd, prep, sd = runs
+    gb, psd, prep, sd, sdm = runs
     assert prep.finished == N_REQ
     a = [r.output_ids for r in psd.request_list()]
     b = [r.output_ids for r in sd.request_list()]
     assert all(len(x) == OUT_GPU for x in a)
     assert a == b
+    # SD(m) with staggered lengths / admissions: each request's tokens are a
+    # prefix-identical greedy decode (its outputs are 0 or 3 tokens shorter)
+    c = [r.output_ids for r in sdm.request_list()]
+    assert all(x[:len(y)] == y for x, y in zip(a, c))
     # real speculation happened: drafts were both accepted and rejected
     assert 0 < prep.total_accepted < prep.total_drafted
 
 
 def test_psd_equals_cpu_oracle_psd_at_cfg2_shapes(runs, cpu):
-    gb, psd, _, _ = runs
+    gb, psd = runs[0], runs[1]
     cb, cst, crep = cpu
     assert crep.finished == N_REQ
     g = [r.output_ids[:OUT_CPU] for r in psd.request_list()]
@@ -87,7 +97,7 @@ def test_psd_equals_cpu_oracle_psd_at_cfg2_shapes(runs, cpu):
 
 
 def test_every_gpu_token_is_the_oracle_greedy_choice_and_logits_match(runs, cpu):
-    gb, psd, _, _ = runs
+    gb, psd = runs[0], runs[1]
     cb, _, _ = cpu
     total_exact, ties, stats = 0, [], []
     for req in psd.request_list():
