@@ -129,19 +129,32 @@ def _config(mode: str):
                      sd_batch_factor=2 if mode == "standard-sd" else 1)
 
 
-def _time_kernel(fn, iters: int = 20) -> float:
-    """Average device time (ms) of fn() on the current stream, CUDA events."""
+def _time_graph(fn, n: int = 32, replays: int = 5) -> float:
+    """Average device time (ms) of fn() captured n times back to back in one
+    CUDA graph (as the PSD loop launches its kernels), median over replays."""
+    import statistics as stt
     import torch
-    for _ in range(3):
-        fn()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            fn()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(iters):
-        fn()
-    e1.record()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
+        for _ in range(n):
+            fn()
+    g.replay()
     torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / iters
+    times = []
+    for _ in range(replays):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) / n)
+    return stt.median(times)
 
 
 TRAFFIC_FILE = os.path.join("profiles", "r02_ncu_traffic.json")
@@ -175,7 +188,7 @@ def kernel_rooflines(backend, hbm_peak: float, bf16_peak: float) -> tuple[dict, 
     """Dominant kernel (verify-forward gate/up GEMM) and K1 at the workload shapes."""
     import torch
     from paper_2603_18016_b200 import native, ops
-    from paper_2603_18016_b200.verify_bench import algorithmic_bytes, make_inputs
+    from paper_2603_18016_b200.verify_bench import time_verify
     dev = backend.device
     s = backend.tshape
     M = CFG["m"] * (CFG["k"] + 1)
@@ -192,7 +205,7 @@ def kernel_rooflines(backend, hbm_peak: float, bf16_peak: float) -> tuple[dict, 
         it[0] += 1
 
     lib = native.load()
-    ms = _time_kernel(gemm, 64)
+    ms = _time_graph(gemm, 64)
     # the same GEMM under the CTA cap it runs with inside an overlapped PSD step
     # (the draft's kernels take the other SMs there); timed alone here
     cap = backend.verify_ctas
@@ -200,7 +213,7 @@ def kernel_rooflines(backend, hbm_peak: float, bf16_peak: float) -> tuple[dict, 
     if cap:
         lib.psd_gemm_set_max_ctas(cap)
         try:
-            ms_cap = _time_kernel(gemm, 64)
+            ms_cap = _time_graph(gemm, 64)
         finally:
             lib.psd_gemm_set_max_ctas(0)
     N, Kd = w.shape[0], s.hidden
@@ -223,7 +236,8 @@ def kernel_rooflines(backend, hbm_peak: float, bf16_peak: float) -> tuple[dict, 
             "intensity_flop_per_byte": round(intensity, 1), "ridge_flop_per_byte": round(ridge, 1),
             "bytes_per_launch": nbytes, "us_per_launch": round(ms * 1e3, 2),
             "tflops": round(flops / (ms * 1e-3) / 1e12, 1),
-            "timing": "alone, all SMs, back-to-back launches rotating over every layer's weights",
+            "timing": "alone, all SMs, 64 launches back to back in a CUDA graph rotating over "
+                      "every layer's weights (inputs > L2)",
             "psd_step_config": ({"cta_cap": cap, "ctas": _sk_physical(dev, cap),
                                  "us_per_launch": round(ms_cap * 1e3, 2),
                                  "GBps": round(nbytes / (ms_cap * 1e-3) / 1e9, 1),
@@ -231,52 +245,25 @@ def kernel_rooflines(backend, hbm_peak: float, bf16_peak: float) -> tuple[dict, 
                                  "note": "CTA cap of the verify GEMMs in overlapped PSD steps, "
                                          "timed alone (beside the draft the SMs are shared)"}
                                 if ms_cap else None)}
+    # K1 as the PSD loop runs it: inside CUDA graphs, behind an L2 flush
+    # (verify_bench.time_verify: graph of (flush, K1) pairs minus a graph of
+    # flushes), so the number is the kernels' device time, not host launch rate
     B, K, V = CFG["m"], CFG["k"], s.vocab
-    sets = [make_inputs(B, K, V, False, dev, seed=i) for i in range(3)]
-    j = [0]
-
-    def k1():
-        t, d, ids, ln, u = sets[j[0] % 3]
-        ops.verify_greedy(t, ids, ln)
-        j[0] += 1
-
-    ms1 = _time_kernel(k1, 60)
-    vb = algorithmic_bytes(B, K, V, False)
-    sets_s = [make_inputs(B, K, V, True, dev, seed=10 + i) for i in range(3)]
-
-    def k1s():
-        t, d, ids, ln, u = sets_s[j[0] % 3]
-        ops.verify_sample(t, d, ids, ln, u)
-        j[0] += 1
-
-    ms2 = _time_kernel(k1s, 30)
-    vbs = algorithmic_bytes(B, K, V, True)
+    rg = time_verify(B, K, V, False, iters=60, device=dev)
+    rs = time_verify(B, K, V, True, iters=30, device=dev)
     # the PSD loop's sampling K1: q-row statistics cached by the draft sampler
     # (psd_verify_sample_ext), so the draft rows are not streamed again
-    qstats = []
-    for t, d, ids, ln, u in sets_s:
-        st = torch.empty(B, K, 2, device=dev)
-        rows = d.reshape(B * K, 1, -1)
-        ops.verify_sample(rows, rows[:, :0],
-                          torch.zeros(B * K, 0, dtype=torch.int32, device=dev),
-                          torch.zeros(B * K, dtype=torch.int32, device=dev),
-                          torch.rand(B * K, 1, device=dev), t_stats_out=st.view(B * K, 2),
-                          t_stats_rows=torch.arange(B * K, dtype=torch.int32, device=dev))
-        qstats.append(st)
-
-    def k1c():
-        t, d, ids, ln, u = sets_s[j[0] % 3]
-        ops.verify_sample(t, d, ids, ln, u, d_stats=qstats[j[0] % 3])
-        j[0] += 1
-
-    ms3 = _time_kernel(k1c, 30)
-    read_c = algorithmic_bytes(B, K, V, False)  # target rows + ids (+ one q element per draft)
+    rc = time_verify(B, K, V, True, iters=30, device=dev, cached=True)
+    vb, vbs = rg["bytes"], rs["bytes"]
+    read_c = rc["bytes_streamed"]
+    ms1, ms2, ms3 = rg["us"] * 1e-3, rs["us"] * 1e-3, rc["us"] * 1e-3
+    timing = "CUDA graph, L2 flushed before every launch (verify_bench.time_verify)"
     vk = {"greedy": {"B": B, "k": K, "V": V, "us": round(ms1 * 1e3, 2), "bytes": vb,
                      "GBps": round(vb / (ms1 * 1e-3) / 1e9, 1),
-                     "frac": round(vb / (ms1 * 1e-3) / 1e9 / hbm_peak, 4)},
+                     "frac": round(vb / (ms1 * 1e-3) / 1e9 / hbm_peak, 4), "timing": timing},
           "sampling": {"B": B, "k": K, "V": V, "us": round(ms2 * 1e3, 2), "bytes": vbs,
                        "GBps": round(vbs / (ms2 * 1e-3) / 1e9, 1),
-                       "frac": round(vbs / (ms2 * 1e-3) / 1e9 / hbm_peak, 4)},
+                       "frac": round(vbs / (ms2 * 1e-3) / 1e9 / hbm_peak, 4), "timing": timing},
           "sampling_cached_q": {
               "B": B, "k": K, "V": V, "us": round(ms3 * 1e3, 2),
               "note": "q-row (max, sum) cached by the draft sampler; streams the k+1 target "
@@ -285,7 +272,8 @@ def kernel_rooflines(backend, hbm_peak: float, bf16_peak: float) -> tuple[dict, 
               "GBps_algorithmic": round(vbs / (ms3 * 1e-3) / 1e9, 1),
               "bytes_streamed": read_c,
               "GBps_streamed": round(read_c / (ms3 * 1e-3) / 1e9, 1),
-              "frac_streamed": round(read_c / (ms3 * 1e-3) / 1e9 / hbm_peak, 4)}}
+              "frac_streamed": round(read_c / (ms3 * 1e-3) / 1e9 / hbm_peak, 4),
+              "timing": timing}}
     return roof, vk
 
 

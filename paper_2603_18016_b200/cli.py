@@ -41,6 +41,7 @@ DEFAULTS: dict[str, str] = {
     "engine.mode": "psd", "engine.m": "4", "engine.k": "3", "engine.capacity": "",
     "engine.comm_overhead": "0.0", "engine.seed": "1234", "engine.assign_policy": "skip-batch",
     "engine.sd_batch_factor": "1", "engine.k_per_request": "",
+    "engine.draft_selection": "all",
     "draft.kind": "constant", "draft.base": "1.0", "draft.per_token": "0.0",
     "draft.per_request": "0.0",
     "verify.kind": "constant", "verify.base": "1.0", "verify.per_token": "0.0",
@@ -122,7 +123,8 @@ def build(cfg: dict) -> tuple[SimConfig, WorkloadSpec]:
         comm_overhead=_num(cfg, "engine.comm_overhead", float), acceptance=acc,
         block_size=_num(cfg, "kv.block_size", int), seed=_num(cfg, "engine.seed", int),
         assign_policy=cfg["engine.assign_policy"], kv_policy=cfg["kv.policy"],
-        sd_batch_factor=_num(cfg, "engine.sd_batch_factor", int), k_overrides=k_over))
+        sd_batch_factor=_num(cfg, "engine.sd_batch_factor", int), k_overrides=k_over,
+        draft_selection=cfg["engine.draft_selection"].strip()))
     count = cfg["workload.count"].strip()
     spec = WorkloadSpec(
         arrival=cfg["workload.arrival"], rate=_num(cfg, "workload.rate", float),

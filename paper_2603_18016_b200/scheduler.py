@@ -32,6 +32,7 @@ from .batches import BatchManager
 from .errors import CapacityError, ProtocolError
 from .kvtable import ALLOCATE, AllocationContext, KVBlockTable
 from .metrics import MetricsReport, compute_metrics
+from .selection import AcceptanceTracker, select_depths
 from .records import (TERMINAL_STATES, Request, RequestState, SimConfig, StepRecord,
                       validate_config)
 
@@ -182,6 +183,8 @@ class EngineState:
     # steps (sum over its draft loops of max k_i): what the tuner observes
     last_verified: list[tuple[int, int]] = field(default_factory=list)
     last_draft_steps: int = 0
+    # selection.AcceptanceTracker when config.draft_selection == "tetris"
+    acceptance_tracker: object | None = None
 
     def request_list(self) -> list[Request]:
         return [self.requests[rid] for rid in sorted(self.requests)]
@@ -249,6 +252,24 @@ def _quota(state: EngineState, rid: int) -> int:
     return min(depth, left if left > 0 else 0)
 
 
+def _select(state: EngineState, quotas: dict[int, int], groups, capacity: int) -> dict[int, int]:
+    """draft_selection "tetris": trim each group's depths to ``capacity``
+    (selection.select_depths); "all" keeps them (over-capacity then fails in
+    _check_capacity as in the reference)."""
+    if state.config.draft_selection != "tetris":
+        return quotas
+    tr = state.acceptance_tracker
+    if tr is None:
+        tr = state.acceptance_tracker = AcceptanceTracker(
+            state.config.acceptance.token_probability(0.0))
+    out = dict(quotas)
+    for g in groups:
+        if g:
+            sub = {rid: quotas[rid] for rid in g}
+            out.update(select_depths(sub, capacity, {rid: tr.p(rid) for rid in g}))
+    return out
+
+
 def _grow(state: EngineState, ctx: AllocationContext,
           sizing: dict[int, tuple[int, float]],
           decisions: dict[int, str] | None = None) -> tuple[tuple[int, ...], tuple[int, ...]]:
@@ -309,6 +330,8 @@ def _commit_rows(state: EngineState, rows: list[VerifyRow],
         req = state.requests[row.request_id]
         a = accepted.get(row.request_id, 0) if row.k > 0 else 0
         state.last_verified.append((row.k, a))
+        if state.acceptance_tracker is not None:
+            state.acceptance_tracker.observe(row.request_id, row.k, a)
         commit = min(a + 1, req.remaining)
         req.generated += commit
         state.kv.commit_write(row.request_id, commit)
@@ -404,6 +427,8 @@ def _psd_step(state: EngineState) -> StepRecord:
     record_target = target if (branch != "fallback" or target_ids) else skip
 
     quotas = {rid: _quota(state, rid) for rid in serial + overlap}
+    # each drafted group is verified as one pass: fit it to the capacity
+    quotas = _select(state, quotas, (serial, overlap), cfg.effective_capacity)
     state.last_draft_steps = (max((quotas[r] for r in serial), default=0)
                               + max((quotas[r] for r in overlap), default=0))
     plan = StepPlan(step_index, branch, prefill_ids, serial, overlap,
@@ -473,6 +498,8 @@ def _sd_step(state: EngineState) -> StepRecord:
     state.newly_admitted = []
     ids = list(state.sd_members)
     quotas = {rid: _quota(state, rid) for rid in ids}
+    quotas = _select(state, quotas, (tuple(ids),),
+                     cfg.effective_capacity * cfg.sd_batch_factor)
     state.last_draft_steps = max(quotas.values(), default=0)
     plan = StepPlan(step_index, "sd", prefill_ids, tuple(ids), (), tuple(ids), quotas)
     _, serial_est, _ = backend.estimate(state, plan)
