@@ -732,6 +732,360 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
   }
 }
 
+// ---- decode attention: every key of a sequence in flight at once -------------
+// For draft decode passes (<= 16 query rows per kv head: 1-2 tokens x G heads).
+// One CTA per (sequence, kv head) issues the cp.async copies of ALL its key
+// tiles at once (up to `cap` tiles per round -- the whole context at the
+// BASELINE shapes: one HBM round trip instead of a ring of them); the keys of
+// earlier steps are requested before griddepcontrol.wait.  With ROPE the CTA
+// rotates its queries from the QKV split-K partials and writes this step's
+// K / V rows both to the paged cache (for later steps) and straight into its
+// shared-memory tiles, so they are not read back through L2.  Tiles are stored
+// unpadded with the 16-byte chunks XOR-swizzled per row (ldmatrix of 8
+// consecutive keys hits 8 bank groups).  Math as in attention_kernel (key
+// groups of warps, mma.sync m16n8k16, online exp2 softmax, shared-memory merge
+// of the key groups).  Measured variants (profiles/r02_attn_dec.txt): a
+// cluster split of the keys with a DSMEM merge was 2-5x slower at these
+// shapes, 8 warps instead of 4 no faster.
+template <int D>
+__device__ __forceinline__ uint32_t swz(int r, int c) {
+  constexpr int CPR = D / 8;  // 16-byte chunks per key row
+  if constexpr (CPR >= 8)
+    return (uint32_t)(r * CPR + ((c & ~7) | ((c & 7) ^ (r & 7)))) * 16u;
+  else
+    return (uint32_t)(r * CPR + (c ^ ((r >> 1) & 3))) * 16u;
+}
+
+constexpr int ADEC_KT = 32;  // keys per tile
+
+template <int D, bool ROPE>
+__global__ void __launch_bounds__(ATT_THREADS)
+attn_dec_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ kc,
+                const __nv_bfloat16* __restrict__ vc, const int32_t* __restrict__ block_table,
+                int max_blocks, const int32_t* __restrict__ seq_slot,
+                const int32_t* __restrict__ q_start, const int32_t* __restrict__ q_len,
+                const int32_t* __restrict__ q_pos0, const int32_t* __restrict__ kv_len, int Hq,
+                int Hkv, int bs, float scale_log2, int cap, __nv_bfloat16* __restrict__ out,
+                const RopeSrc rs) {
+  constexpr int KT = ADEC_KT;
+  constexpr int P = D + 8;                 // sQ row pitch
+  constexpr int TB = KT * D * 2;           // bytes of one K (or V) tile
+  constexpr int CPR = D / 8;
+  constexpr int PER_T = KT * CPR / ATT_THREADS;
+  static_assert(KT * CPR % ATT_THREADS == 0, "tile chunks must tile the CTA");
+  constexpr int KG = 4;                    // one row group (<= 16 rows), 4 key groups
+  const int seq = blockIdx.x, hk = blockIdx.y;
+  const int G = Hq / Hkv;
+  const int tid = threadIdx.x, lane = tid & 31, kg = tid >> 5;
+  const int g = lane >> 2, c = lane & 3;
+
+  const int nt = q_len[seq];
+  const int R = nt * G;
+  const int kvl = kv_len[seq];
+  const int qs = q_start[seq];
+  const int first_pos = q_pos0[seq];
+  const int last_key = nt > 0 ? min(first_pos + nt - 1, kvl - 1) : -1;
+  const int ntl = last_key >= 0 ? last_key / KT + 1 : 0;
+
+  extern __shared__ __align__(128) uint8_t ad_smem[];
+  typedef __nv_bfloat16 Row[P];
+  Row* sQ = reinterpret_cast<Row*>(ad_smem);
+  uint8_t* sKV = ad_smem + ((16 * P * 2 + 127) & ~127);  // cap x (K tile, V tile)
+  int* bt = reinterpret_cast<int*>(sKV + (size_t)cap * 2 * TB);
+  const int bs_shift = __ffs(bs) - 1;
+  const int nblk_used = last_key >= 0 ? min((last_key >> bs_shift) + 1, max_blocks) : 0;
+  if (nt > 0) {
+    const int* btg = block_table + (size_t)seq_slot[seq] * max_blocks;
+    for (int i = tid; i < nblk_used; i += ATT_THREADS) bt[i] = btg[i];
+  }
+  __syncthreads();
+  const size_t head_off = (size_t)hk * D;
+  // tiles [t0, t0 + n) into slots 0..n-1.  direct: rows of this step's keys
+  // are not copied (RoPE stores them into the slots); rows past the last key
+  // are zero-filled
+  auto load_tiles = [&](int t0, int n, bool direct) {
+    for (int j = 0; j < n; ++j) {
+      const int tile = t0 + j;
+      const uint32_t sk = static_cast<uint32_t>(__cvta_generic_to_shared(sKV + (size_t)j * 2 * TB));
+      const uint32_t sv = sk + TB;
+#pragma unroll
+      for (int i = 0; i < PER_T; ++i) {
+        const int idx = tid + ATT_THREADS * i;
+        const int r = idx / CPR, cc = idx % CPR;
+        const int key = tile * KT + r;
+        const bool ok = key <= last_key;
+        if (direct && ok && key >= first_pos) continue;
+        size_t o = 0;
+        if (ok)
+          o = ((((size_t)bt[key >> bs_shift] << bs_shift) + (key & (bs - 1))) * Hkv) * D +
+              head_off + cc * 8;
+        const uint32_t off = swz<D>(r, cc);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sk + off),
+                     "l"(kc + o), "r"(ok ? 16 : 0));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sv + off),
+                     "l"(vc + o), "r"(ok ? 16 : 0));
+      }
+    }
+    cp_async_commit();
+  };
+  const int n0 = min(ntl, cap);
+  // this step's keys go straight into the slots when they lie in round 0
+  const bool direct = ROPE && (first_pos / KT) < n0;
+  load_tiles(0, n0, direct);
+  pdl_wait();
+  pdl_trigger();
+  if constexpr (ROPE) {
+    constexpr int half = D / 2;
+    const int NQKV = (Hq + 2 * Hkv) * D;
+    const int nrot = nt * (G + 1) * half;
+    // slot address of element i of new key row t (round 0 only)
+    auto kv_slot = [&](int t, int i, bool v) -> __nv_bfloat16* {
+      const int key = first_pos + t;
+      const int j = key / KT, r = key % KT;
+      return reinterpret_cast<__nv_bfloat16*>(sKV + (size_t)j * 2 * TB + (v ? TB : 0) +
+                                              swz<D>(r, i / 8) + (i % 8) * 2);
+    };
+    for (int idx = tid; idx < nrot + nt * D; idx += ATT_THREADS) {
+      if (idx >= nrot) {
+        const int t = (idx - nrot) / D, i = (idx - nrot) % D;
+        const int m = qs + t;
+        const int sl = rs.slots[m];
+        if (sl < 0) continue;
+        const int col = (Hq + Hkv + hk) * D + i;
+        float a = sum_parts(rs, (size_t)m * NQKV + col);
+        if (rs.bias) a = a + __bfloat162float(rs.bias[col]);
+        vc_w(vc, ((size_t)sl * Hkv + hk) * D + i, a);
+        if (direct && first_pos + t <= last_key) *kv_slot(t, i, true) = __float2bfloat16(a);
+        continue;
+      }
+      const int t = idx / ((G + 1) * half), rem = idx % ((G + 1) * half);
+      const int hh = rem / half, i = rem % half;
+      const int m = qs + t;
+      if (hh == G && rs.slots[m] < 0) continue;
+      const int head = hh < G ? hk * G + hh : Hq + hk;
+      const int col = head * D + i;
+      float a = sum_parts(rs, (size_t)m * NQKV + col);
+      float b = sum_parts(rs, (size_t)m * NQKV + col + half);
+      if (rs.bias) {
+        a = __bfloat162float(__float2bfloat16(a + __bfloat162float(rs.bias[col])));
+        b = __bfloat162float(__float2bfloat16(b + __bfloat162float(rs.bias[col + half])));
+      }
+      float sn, cs;
+      sincosf((float)rs.positions[m] * rs.inv_freq[i], &sn, &cs);
+      const __nv_bfloat16 ra = __float2bfloat16(a * cs - b * sn);
+      const __nv_bfloat16 rb = __float2bfloat16(b * cs + a * sn);
+      if (hh < G) {
+        sQ[t * G + hh][i] = ra;
+        sQ[t * G + hh][i + half] = rb;
+      } else {
+        __nv_bfloat16* dst = const_cast<__nv_bfloat16*>(kc) + ((size_t)rs.slots[m] * Hkv + hk) * D;
+        dst[i] = ra;
+        dst[i + half] = rb;
+        if (direct && first_pos + t <= last_key) {
+          *kv_slot(t, i, false) = ra;
+          *kv_slot(t, i + half, false) = rb;
+        }
+      }
+    }
+    for (int idx = tid; idx < (16 - R) * D; idx += ATT_THREADS)
+      sQ[R + idx / D][idx % D] = __float2bfloat16(0.f);
+    // rows read back through L2 in a later round need the global writes first
+    if (!direct) __threadfence();
+  } else {
+    for (int idx = tid; idx < 16 * (D / 8); idx += ATT_THREADS) {
+      const int r = idx / (D / 8), cc = idx % (D / 8);
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (r < R) {
+        const int t = r / G, gg = r % G;
+        v = *reinterpret_cast<const uint4*>(q + ((size_t)(qs + t) * Hq + hk * G + gg) * D + cc * 8);
+      }
+      *reinterpret_cast<uint4*>(&sQ[r][cc * 8]) = v;
+    }
+  }
+  __syncthreads();
+
+  const bool active = R > 0;
+  const int r0 = g, r1 = g + 8;
+  const int lim0 = r0 < R ? min(first_pos + r0 / G, kvl - 1) : -1;
+  const int lim1 = r1 < R ? min(first_pos + r1 / G, kvl - 1) : -1;
+  uint32_t qf[D / 16][4];
+#pragma unroll
+  for (int kk = 0; kk < D / 16; ++kk) {
+    qf[kk][0] = *reinterpret_cast<const uint32_t*>(&sQ[r0][kk * 16 + 2 * c]);
+    qf[kk][1] = *reinterpret_cast<const uint32_t*>(&sQ[r1][kk * 16 + 2 * c]);
+    qf[kk][2] = *reinterpret_cast<const uint32_t*>(&sQ[r0][kk * 16 + 8 + 2 * c]);
+    qf[kk][3] = *reinterpret_cast<const uint32_t*>(&sQ[r1][kk * 16 + 8 + 2 * c]);
+  }
+  float o[D / 8][4];
+#pragma unroll
+  for (int n = 0; n < D / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  const int lrow = lane & 7, lmat = lane >> 3;
+
+  for (int rb = 0; rb < ntl; rb += cap) {
+    const int nr = min(cap, ntl - rb);
+    if (rb > 0) {
+      __syncthreads();  // the previous round's tiles are consumed
+      load_tiles(rb, nr, false);
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    if (!active) continue;
+    for (int j = kg; j < nr; j += KG) {
+      const int kt = rb + j;
+      const uint32_t sk = static_cast<uint32_t>(__cvta_generic_to_shared(sKV + (size_t)j * 2 * TB));
+      const uint32_t sv = sk + TB;
+      float sacc[KT / 8][4];
+#pragma unroll
+      for (int n = 0; n < KT / 8; ++n) sacc[n][0] = sacc[n][1] = sacc[n][2] = sacc[n][3] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+#pragma unroll
+        for (int n = 0; n < KT / 8; n += 2) {
+          uint32_t kb[4];
+          const int krow = (n + (lmat >> 1)) * 8 + lrow;
+          const uint32_t a = sk + swz<D>(krow, 2 * kk + (lmat & 1));
+          asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(kb[0]), "=r"(kb[1]), "=r"(kb[2]), "=r"(kb[3]) : "r"(a));
+          mma_bf16_16816(sacc[n], qf[kk], kb[0], kb[1]);
+          mma_bf16_16816(sacc[n + 1], qf[kk], kb[2], kb[3]);
+        }
+      }
+      float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+      for (int n = 0; n < KT / 8; ++n) {
+        const int key = kt * KT + n * 8 + 2 * c;
+        sacc[n][0] = key <= lim0 ? sacc[n][0] * scale_log2 : -INFINITY;
+        sacc[n][1] = key + 1 <= lim0 ? sacc[n][1] * scale_log2 : -INFINITY;
+        sacc[n][2] = key <= lim1 ? sacc[n][2] * scale_log2 : -INFINITY;
+        sacc[n][3] = key + 1 <= lim1 ? sacc[n][3] * scale_log2 : -INFINITY;
+        mx0 = fmaxf(mx0, fmaxf(sacc[n][0], sacc[n][1]));
+        mx1 = fmaxf(mx1, fmaxf(sacc[n][2], sacc[n][3]));
+      }
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+      const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+      const float base0 = mn0 == -INFINITY ? 0.f : mn0;
+      const float base1 = mn1 == -INFINITY ? 0.f : mn1;
+      const float al0 = exp2f(m0 - base0), al1 = exp2f(m1 - base1);
+      m0 = mn0;
+      m1 = mn1;
+      float ps0 = 0.f, ps1 = 0.f;
+      uint32_t pf[KT / 16][4];
+#pragma unroll
+      for (int n = 0; n < KT / 8; ++n) {
+        const float p0 = exp2f(sacc[n][0] - base0), p1 = exp2f(sacc[n][1] - base0);
+        const float p2 = exp2f(sacc[n][2] - base1), p3 = exp2f(sacc[n][3] - base1);
+        ps0 += p0 + p1;
+        ps1 += p2 + p3;
+        const int kk = n >> 1;
+        if ((n & 1) == 0) {
+          pf[kk][0] = pack_bf16(p0, p1);
+          pf[kk][1] = pack_bf16(p2, p3);
+        } else {
+          pf[kk][2] = pack_bf16(p0, p1);
+          pf[kk][3] = pack_bf16(p2, p3);
+        }
+      }
+      l0 = l0 * al0 + ps0;
+      l1 = l1 * al1 + ps1;
+#pragma unroll
+      for (int n = 0; n < D / 8; ++n) {
+        o[n][0] *= al0; o[n][1] *= al0; o[n][2] *= al1; o[n][3] *= al1;
+      }
+#pragma unroll
+      for (int kk = 0; kk < KT / 16; ++kk) {
+#pragma unroll
+        for (int n = 0; n < D / 8; n += 2) {
+          uint32_t vb[4];
+          const int krow = kk * 16 + (lmat & 1) * 8 + lrow;
+          const uint32_t a = sv + swz<D>(krow, n + (lmat >> 1));
+          asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(vb[0]), "=r"(vb[1]), "=r"(vb[2]), "=r"(vb[3]) : "r"(a));
+          mma_bf16_16816(o[n], pf[kk], vb[0], vb[1]);
+          mma_bf16_16816(o[n + 1], pf[kk], vb[2], vb[3]);
+        }
+      }
+    }
+  }
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  // merge the key groups: warps 1..3 publish in the (now idle) tile region,
+  // warp 0 merges in key-group order
+  cp_async_wait<0>();
+  __syncthreads();
+  float* scr = reinterpret_cast<float*>(sKV);
+  const int slot_floats = 16 * D + 32;
+  if (active && kg > 0) {
+    float* sp = scr + kg * slot_floats;
+#pragma unroll
+    for (int n = 0; n < D / 8; ++n) {
+      const int d = n * 8 + 2 * c;
+      sp[g * D + d] = o[n][0];
+      sp[g * D + d + 1] = o[n][1];
+      sp[(g + 8) * D + d] = o[n][2];
+      sp[(g + 8) * D + d + 1] = o[n][3];
+    }
+    if (c == 0) {
+      sp[16 * D + g] = m0;
+      sp[16 * D + g + 8] = m1;
+      sp[16 * D + 16 + g] = l0;
+      sp[16 * D + 16 + g + 8] = l1;
+    }
+  }
+  __syncthreads();
+  if (!active || kg != 0) return;
+  float M0 = m0, M1 = m1;
+  for (int j = 1; j < KG; ++j) {
+    const float* sp = scr + j * slot_floats;
+    M0 = fmaxf(M0, sp[16 * D + g]);
+    M1 = fmaxf(M1, sp[16 * D + g + 8]);
+  }
+  const float w00 = M0 == -INFINITY ? 0.f : exp2f(m0 - M0);
+  const float w10 = M1 == -INFINITY ? 0.f : exp2f(m1 - M1);
+  l0 *= w00;
+  l1 *= w10;
+#pragma unroll
+  for (int n = 0; n < D / 8; ++n) {
+    o[n][0] *= w00; o[n][1] *= w00; o[n][2] *= w10; o[n][3] *= w10;
+  }
+  for (int j = 1; j < KG; ++j) {
+    const float* sp = scr + j * slot_floats;
+    const float mj0 = sp[16 * D + g], mj1 = sp[16 * D + g + 8];
+    const float wj0 = mj0 == -INFINITY ? 0.f : exp2f(mj0 - M0);
+    const float wj1 = mj1 == -INFINITY ? 0.f : exp2f(mj1 - M1);
+    l0 += sp[16 * D + 16 + g] * wj0;
+    l1 += sp[16 * D + 16 + g + 8] * wj1;
+#pragma unroll
+    for (int n = 0; n < D / 8; ++n) {
+      const int d = n * 8 + 2 * c;
+      o[n][0] += sp[g * D + d] * wj0;
+      o[n][1] += sp[g * D + d + 1] * wj0;
+      o[n][2] += sp[(g + 8) * D + d] * wj1;
+      o[n][3] += sp[(g + 8) * D + d + 1] * wj1;
+    }
+  }
+  const float inv0 = l0 > 0.f ? 1.f / l0 : 0.f, inv1 = l1 > 0.f ? 1.f / l1 : 0.f;
+#pragma unroll
+  for (int n = 0; n < D / 8; ++n) {
+    const int d = n * 8 + 2 * c;
+    if (r0 < R) {
+      const int t = r0 / G, gg = r0 % G;
+      *reinterpret_cast<__nv_bfloat162*>(out + ((size_t)(qs + t) * Hq + hk * G + gg) * D + d) =
+          __floats2bfloat162_rn(o[n][0] * inv0, o[n][1] * inv0);
+    }
+    if (r1 < R) {
+      const int t = r1 / G, gg = r1 % G;
+      *reinterpret_cast<__nv_bfloat162*>(out + ((size_t)(qs + t) * Hq + hk * G + gg) * D + d) =
+          __floats2bfloat162_rn(o[n][2] * inv1, o[n][3] * inv1);
+    }
+  }
+}
+
 // key splits for split-KV: a decode/verify CTA's latency is its serial chain
 // of key tiles, so split until every CTA has <= ~128 keys or the grid holds
 // ~4 waves of 148 SMs (>= 32 keys per split)
@@ -1077,12 +1431,67 @@ static int attention_launch(const void* q, const void* k_cache, const void* v_ca
   return (int)err;
 }
 
+// decode attention (attn_dec_kernel): one CTA per (sequence, kv head), every
+// key tile in flight (cap = the block table's tiles, fewer if shared memory
+// runs out: several rounds).  PSD_ATT_DEC=0 routes these passes to
+// attention_kernel (A/B runs).
+static bool attn_dec_eligible(int max_q_len, int G, int D) {
+  static const int on = [] {
+    const char* e = getenv("PSD_ATT_DEC");
+    return e ? atoi(e) : 1;
+  }();
+  return on && max_q_len * G <= 16 && (D == 32 || D == 64 || D == 128);
+}
+
+static int attn_dec_launch(const void* q, const void* k_cache, const void* v_cache,
+                           const int32_t* block_table, int max_blocks, const int32_t* seq_slot,
+                           const int32_t* q_start, const int32_t* q_len, const int32_t* q_pos0,
+                           const int32_t* kv_len, int num_seqs, int Hq, int Hkv, int D,
+                           int block_size, float scale, void* out, const RopeSrc* rope,
+                           void* stream) {
+  int cap = (max_blocks * block_size + ADEC_KT - 1) / ADEC_KT;
+  const int TB = ADEC_KT * D * 2;
+  const int sq = (16 * (D + 8) * 2 + 127) & ~127;
+  const int scratch = 4 * (16 * D + 32) * 4;  // key-group merge slots
+  auto bytes = [&](int cp) { return sq + std::max(cp * 2 * TB + max_blocks * 4, scratch); };
+  while (cap > 1 && bytes(cap) > 200 * 1024) --cap;
+  cap = std::max(cap, 1);
+  const int smem = bytes(cap);
+  const RopeSrc rs = rope ? *rope : RopeSrc{};
+  const float sl2 = scale * 1.44269504088896341f;
+  cudaError_t err = cudaSuccess;
+  auto go = [&](auto kern) {
+    if ((err = psd::ensure_smem_limit((const void*)kern, 200 * 1024 + 1024, (cudaStream_t)stream)))
+      return;
+    err = psd::launch(kern, dim3(num_seqs, Hkv), dim3(ATT_THREADS), smem, (cudaStream_t)stream,
+                      static_cast<const __nv_bfloat16*>(q),
+                      static_cast<const __nv_bfloat16*>(k_cache),
+                      static_cast<const __nv_bfloat16*>(v_cache), block_table, max_blocks,
+                      seq_slot, q_start, q_len, q_pos0, kv_len, Hq, Hkv, block_size, sl2, cap,
+                      static_cast<__nv_bfloat16*>(out), rs);
+  };
+  const bool r = rope != nullptr;
+  switch (D) {
+    case 32: r ? go(attn_dec_kernel<32, true>) : go(attn_dec_kernel<32, false>); break;
+    case 64: r ? go(attn_dec_kernel<64, true>) : go(attn_dec_kernel<64, false>); break;
+    case 128: r ? go(attn_dec_kernel<128, true>) : go(attn_dec_kernel<128, false>); break;
+    default: return (int)cudaErrorInvalidValue;
+  }
+  return (int)err;
+}
+
 int psd_attention(const void* q, const void* k_cache, const void* v_cache,
                   const int32_t* block_table, int max_blocks, const int32_t* seq_slot,
                   const int32_t* q_start, const int32_t* q_len, const int32_t* q_pos0,
                   const int32_t* kv_len, int num_seqs, int max_q_len, int Hq, int Hkv, int D,
                   int block_size, float scale, void* out, int max_kv_len, void* workspace,
                   size_t workspace_bytes, void* stream) {
+  if (num_seqs > 0 && Hkv > 0 && Hq % Hkv == 0 && max_blocks <= ATT_MAX_BLOCKS &&
+      block_size > 0 && !(block_size & (block_size - 1)) &&
+      attn_dec_eligible(max_q_len, Hq / Hkv, D))
+    return attn_dec_launch(q, k_cache, v_cache, block_table, max_blocks, seq_slot, q_start, q_len,
+                           q_pos0, kv_len, num_seqs, Hq, Hkv, D, block_size, scale, out, nullptr,
+                           stream);
   return attention_launch(q, k_cache, v_cache, block_table, max_blocks, seq_slot, q_start, q_len,
                           q_pos0, kv_len, num_seqs, max_q_len, Hq, Hkv, D, block_size, scale, out,
                           max_kv_len, workspace, workspace_bytes, nullptr, stream);
@@ -1105,6 +1514,12 @@ int psd_attention_rope(const float* qkv_partials, int S, size_t slice, const int
   rs.slots = slots;
   rs.inv_freq = inv_freq;
   rs.bias = static_cast<const __nv_bfloat16*>(qkv_bias);
+  if (num_seqs > 0 && Hkv > 0 && Hq % Hkv == 0 && S <= 16 && max_blocks <= ATT_MAX_BLOCKS &&
+      block_size > 0 && !(block_size & (block_size - 1)) &&
+      attn_dec_eligible(max_q_len, Hq / Hkv, D))
+    return attn_dec_launch(nullptr, k_cache, v_cache, block_table, max_blocks, seq_slot, q_start,
+                           q_len, q_pos0, kv_len, num_seqs, Hq, Hkv, D, block_size, scale, out, &rs,
+                           stream);
   return attention_launch(nullptr, k_cache, v_cache, block_table, max_blocks, seq_slot, q_start,
                           q_len, q_pos0, kv_len, num_seqs, max_q_len, Hq, Hkv, D, block_size,
                           scale, out, 0, nullptr, 0, &rs, stream);

@@ -15,13 +15,12 @@ from paper_2603_18016_b200 import native
 pytestmark = pytest.mark.gpu
 
 
-def _case(dev, D, Hq, Hkv, seqs, bs=16, nblocks=200, seed=0):
+def _case(dev, D, Hq, Hkv, seqs, bs=16, nblocks=200, seed=0, maxb=40):
     g = torch.Generator(device=dev).manual_seed(seed)
     M = sum(ql for ql, _, _ in seqs)
     q = torch.randn(M, Hq, D, device=dev, generator=g).to(torch.bfloat16)
     kc = torch.randn(nblocks * bs, Hkv, D, device=dev, generator=g).to(torch.bfloat16)
     vc = torch.randn(nblocks * bs, Hkv, D, device=dev, generator=g).to(torch.bfloat16)
-    maxb = 40
     bt = torch.zeros(len(seqs), maxb, dtype=torch.int32, device=dev)
     perm = torch.randperm(nblocks - 1, generator=torch.Generator().manual_seed(seed)) + 1
     used = 0
@@ -90,3 +89,37 @@ def test_attention_matches_torch(cuda_device, D, Hq, Hkv):
         torch.cuda.synchronize()
         err = (out.float() - ref).abs().max().item()
         assert err < 2e-2, (kvhint, err)
+
+
+@pytest.mark.parametrize("D,Hq,Hkv", [(128, 32, 8), (64, 32, 8), (32, 8, 2), (128, 28, 4),
+                                      (128, 64, 8), (64, 14, 2)])
+@pytest.mark.parametrize("maxb", [2, 8, 40, 200])
+def test_decode_attention_matches_torch(cuda_device, D, Hq, Hkv, maxb):
+    """Decode widths (q_len * G <= 16) take attn_dec_kernel: one CTA per
+    (sequence, kv head) with every key tile in flight; the tiles per round come
+    from the block-table width (maxb 2 / 8 / 40: one round; 200: 3200 keys,
+    several rounds at D = 128)."""
+    kmax = maxb * 16
+    seqs = [(6, 140, 146), (6, 7, 10), (2, 30, 32), (1, 63, 64), (6, 0, 1), (5, 300, 305),
+            (1, 600, 601), (6, 3000, 3006), (2, 1, 3)]
+    seqs = [s for s in seqs if max(s[2], s[1] + s[0]) <= kmax]
+    G = Hq // Hkv
+    seqs = [(min(ql, 16 // G), p0, kv) for ql, p0, kv in seqs]
+    need = sum((max(kv, p0 + ql) + 15) // 16 for ql, p0, kv in seqs)
+    q, kc, vc, bt, meta = _case(cuda_device, D, Hq, Hkv, seqs, nblocks=need + 8, maxb=maxb)
+    lib = native.load()
+    st = torch.cuda.current_stream().cuda_stream
+    ref = _ref(q, kc, vc, bt, meta, seqs, Hq, Hkv, D)
+    maxq = max(s[0] for s in seqs)
+    out = torch.full_like(q, float("nan"))
+    for _ in range(2):
+        rc = lib.psd_attention(q.data_ptr(), kc.data_ptr(), vc.data_ptr(), bt.data_ptr(),
+                               bt.shape[1], meta["seq_slot"].data_ptr(),
+                               meta["q_start"].data_ptr(), meta["q_len"].data_ptr(),
+                               meta["q_pos0"].data_ptr(), meta["kv_len"].data_ptr(),
+                               len(seqs), maxq, Hq, Hkv, D, 16, 1.0 / math.sqrt(D),
+                               out.data_ptr(), 0, None, 0, st)
+        assert rc == 0
+    torch.cuda.synchronize()
+    err = (out.float() - ref).abs().max().item()
+    assert err < 2e-2, err
