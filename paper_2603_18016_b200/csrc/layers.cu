@@ -355,7 +355,7 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
   extern __shared__ __align__(16) uint8_t att_smem[];
   typedef __nv_bfloat16 Row[P];
   Row* sQ = reinterpret_cast<Row*>(att_smem);
-  Row* ring = reinterpret_cast<Row*>(att_smem + sizeof(Row) * ATT_MAXR);
+  Row* ring = reinterpret_cast<Row*>(att_smem + sizeof(Row) * RG * 16);  // sQ: RG x 16 rows
   // stage s, key group j: K rows at ring[((s*KG + j)*2) * KT], V rows right after
   auto sK = [&](int st, int j) { return ring + ((st * KG + j) * 2) * KT; };
   auto sV = [&](int st, int j) { return ring + ((st * KG + j) * 2 + 1) * KT; };
@@ -376,28 +376,41 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
   constexpr int PER_T = KT * CPR / ATT_THREADS;    // chunks per thread per tile
   static_assert(KT * CPR % ATT_THREADS == 0, "tile chunks must tile the CTA");
   const int bs_shift = __ffs(bs) - 1;
-  const size_t head_off = (size_t)hk * D;
+  // per-thread constants of its PER_T chunk positions (row r, chunk cc):
+  // element offset inside a cache block, block step, shared-memory offset --
+  // per tile only the block-table entry and one wide multiply-add remain
+  uint32_t c_off[PER_T], c_soff[PER_T];
+  int c_row[PER_T], c_blk[PER_T];
+#pragma unroll
+  for (int i = 0; i < PER_T; ++i) {
+    const int idx = tid + ATT_THREADS * i;
+    const int r = idx / CPR, cc = idx % CPR;  // compile-time divisors
+    c_row[i] = r;
+    c_blk[i] = r >> bs_shift;
+    c_off[i] = (uint32_t)(((r & (bs - 1)) * Hkv + hk) * D + cc * 8);
+    c_soff[i] = (uint32_t)(r * P + cc * 8) * 2u;
+  }
+  const uint32_t blk_elems = (uint32_t)(bs * Hkv * D);
+  const uint32_t ring_s = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
   auto load_group = [&](int gi, int st, int part) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       if (j >= KG) break;
       const int tile = ta + gi * KG + j;
-      Row* K = sK(st, j);
-      Row* V = sV(st, j);
+      const uint32_t sk = ring_s + (uint32_t)(((st * KG + j) * 2) * KT * P * 2);
+      const uint32_t sv = sk + (uint32_t)(KT * P * 2);
+      const int blk0 = (tile * KT) >> bs_shift;
 #pragma unroll
       for (int i = 0; i < PER_T; ++i) {
-        const int idx = tid + ATT_THREADS * i;
-        const int r = idx / CPR, cc = idx % CPR;  // compile-time divisors
-        const int key = tile * KT + r;
+        const int key = tile * KT + c_row[i];
         const bool ok = key <= last_key && tile < tb;
         const bool old = ok && key < first_pos;
         if ((part == 1 && !old) || (part == 2 && old)) continue;
-        size_t o = 0;
-        if (ok)
-          o = ((((size_t)bt[key >> bs_shift] << bs_shift) + (key & (bs - 1))) * Hkv) * D +
-              head_off + cc * 8;
-        cp_async16(&K[r][cc * 8], kc + o, ok);
-        cp_async16(&V[r][cc * 8], vc + o, ok);
+        const uint64_t o = ok ? (uint64_t)(uint32_t)bt[blk0 + c_blk[i]] * blk_elems + c_off[i] : 0ull;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sk + c_soff[i]),
+                     "l"(kc + o), "r"(ok ? 16 : 0));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sv + c_soff[i]),
+                     "l"(vc + o), "r"(ok ? 16 : 0));
       }
     }
     cp_async_commit();
@@ -454,12 +467,12 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
         }
       }
     }
-    for (int idx = tid; idx < (ATT_MAXR - R) * D; idx += ATT_THREADS)
+    for (int idx = tid; idx < (RG * 16 - R) * D; idx += ATT_THREADS)
       sQ[R + idx / D][idx % D] = __float2bfloat16(0.f);
     __threadfence();  // this step's K / V rows are read back below through L2
     __syncthreads();
   } else {
-    for (int idx = tid; idx < ATT_MAXR * (D / 8); idx += ATT_THREADS) {
+    for (int idx = tid; idx < RG * 16 * (D / 8); idx += ATT_THREADS) {
       const int r = idx / (D / 8), cc = idx % (D / 8);
       uint4 v = make_uint4(0, 0, 0, 0);
       if (r < R) {
@@ -799,30 +812,38 @@ attn_dec_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __rest
     for (int i = tid; i < nblk_used; i += ATT_THREADS) bt[i] = btg[i];
   }
   __syncthreads();
-  const size_t head_off = (size_t)hk * D;
+  // per-thread constants of its chunk positions (see attention_kernel)
+  uint32_t c_off[PER_T], c_soff[PER_T];
+  int c_row[PER_T], c_blk[PER_T];
+#pragma unroll
+  for (int i = 0; i < PER_T; ++i) {
+    const int idx = tid + ATT_THREADS * i;
+    const int r = idx / CPR, cc = idx % CPR;
+    c_row[i] = r;
+    c_blk[i] = r >> bs_shift;
+    c_off[i] = (uint32_t)(((r & (bs - 1)) * Hkv + hk) * D + cc * 8);
+    c_soff[i] = swz<D>(r, cc);
+  }
+  const uint32_t blk_elems = (uint32_t)(bs * Hkv * D);
+  const uint32_t skv_s = static_cast<uint32_t>(__cvta_generic_to_shared(sKV));
   // tiles [t0, t0 + n) into slots 0..n-1.  direct: rows of this step's keys
   // are not copied (RoPE stores them into the slots); rows past the last key
   // are zero-filled
   auto load_tiles = [&](int t0, int n, bool direct) {
     for (int j = 0; j < n; ++j) {
       const int tile = t0 + j;
-      const uint32_t sk = static_cast<uint32_t>(__cvta_generic_to_shared(sKV + (size_t)j * 2 * TB));
+      const uint32_t sk = skv_s + (uint32_t)(j * 2 * TB);
       const uint32_t sv = sk + TB;
+      const int blk0 = (tile * KT) >> bs_shift;
 #pragma unroll
       for (int i = 0; i < PER_T; ++i) {
-        const int idx = tid + ATT_THREADS * i;
-        const int r = idx / CPR, cc = idx % CPR;
-        const int key = tile * KT + r;
+        const int key = tile * KT + c_row[i];
         const bool ok = key <= last_key;
         if (direct && ok && key >= first_pos) continue;
-        size_t o = 0;
-        if (ok)
-          o = ((((size_t)bt[key >> bs_shift] << bs_shift) + (key & (bs - 1))) * Hkv) * D +
-              head_off + cc * 8;
-        const uint32_t off = swz<D>(r, cc);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sk + off),
+        const uint64_t o = ok ? (uint64_t)(uint32_t)bt[blk0 + c_blk[i]] * blk_elems + c_off[i] : 0ull;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sk + c_soff[i]),
                      "l"(kc + o), "r"(ok ? 16 : 0));
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sv + off),
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sv + c_soff[i]),
                      "l"(vc + o), "r"(ok ? 16 : 0));
       }
     }
@@ -1370,6 +1391,14 @@ size_t psd_attention_workspace_bytes(int num_seqs, int Hkv, int max_q_len, int H
   return 4096 * sizeof(int) + units * S * ATT_MAXR * (D + 2) * sizeof(float);
 }
 
+static int att_ns() {
+  static const int v = [] {
+    const char* e = getenv("PSD_ATT_NS");
+    return e ? atoi(e) : 3;
+  }();
+  return v;
+}
+
 static int attention_launch(const void* q, const void* k_cache, const void* v_cache,
                             const int32_t* block_table, int max_blocks, const int32_t* seq_slot,
                             const int32_t* q_start, const int32_t* q_len, const int32_t* q_pos0,
@@ -1403,8 +1432,8 @@ static int attention_launch(const void* q, const void* k_cache, const void* v_ca
   const float sl2 = scale * 1.44269504088896341f;
   const RopeSrc rs = rope ? *rope : RopeSrc{};
   cudaError_t err = cudaSuccess;
-  auto go = [&](auto kern, int kt, int d) {
-    const int smem = (ATT_MAXR + 2 * ATT_STAGES * KG * kt) * (d + 8) * 2;
+  auto go = [&](auto kern, int kt, int d, int ns = ATT_STAGES) {
+    const int smem = (RG * 16 + 2 * ns * KG * kt) * (d + 8) * 2;
     if ((err = psd::ensure_smem_limit((const void*)kern, 200 * 1024, (cudaStream_t)stream)))
       return;
     err = psd::launch(kern, grid, dim3(ATT_THREADS), smem, (cudaStream_t)stream,
@@ -1423,7 +1452,10 @@ static int attention_launch(const void* q, const void* k_cache, const void* v_ca
       else go(attention_kernel<64, 32, ATT_STAGES, false>, 32, 64);
       break;
     case 128:
+      // verify passes (k + 1 tokens x G heads): one more ring stage keeps two
+      // tile groups in flight per CTA (PSD_ATT_NS=2: the 2-stage ring)
       if (rope) go(attention_kernel<128, 32, ATT_STAGES, true>, 32, 128);
+      else if (att_ns() >= 3) go(attention_kernel<128, 32, 3, false>, 32, 128, 3);
       else go(attention_kernel<128, 32, ATT_STAGES, false>, 32, 128);
       break;
     default: return (int)cudaErrorInvalidValue;
