@@ -15,6 +15,7 @@
 
 #include "../../include/psd.h"
 #include "common.h"
+#include "sm100.cuh"
 
 namespace {
 
@@ -745,6 +746,285 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
   }
 }
 
+// ---- paged attention with TMA key / value tiles ------------------------------
+// Verify and prefill passes (no fused RoPE), D in {64, 128}, 16-token blocks.
+// The cp.async form issues one 16-byte copy per thread per key-row chunk:
+// ncu showed the verify kernel issue-bound on that copy + address stream
+// (profiles/r02_attn_tma.txt).  Here one elected thread moves each
+// (16-token block, kv head, 64-dim half) box with a 3-D TMA copy over the
+// cache viewed as [slots][Hkv][D]: the box lands 128-byte swizzled (SW128),
+// which is exactly the XOR pattern the ldmatrix addressing below undoes, and
+// blocks past the sequence load with a negative slot coordinate (zero fill).
+// Ring stages complete on mbarriers (expect_tx).  Math, warp roles and the
+// key-group merge as in attention_kernel.
+template <int D, int NS>
+__global__ void __launch_bounds__(ATT_THREADS)
+attention_tma_kernel(const __grid_constant__ CUtensorMap tmK,
+                     const __grid_constant__ CUtensorMap tmV, const __nv_bfloat16* __restrict__ q,
+                     const int32_t* __restrict__ block_table, int max_blocks,
+                     const int32_t* __restrict__ seq_slot, const int32_t* __restrict__ q_start,
+                     const int32_t* __restrict__ q_len, const int32_t* __restrict__ q_pos0,
+                     const int32_t* __restrict__ kv_len, int Hq, int Hkv, float scale_log2,
+                     int tok_per_chunk, int RG, __nv_bfloat16* __restrict__ out) {
+  constexpr int KT = 32;                 // keys per tile = two 16-token blocks
+  constexpr int NB64 = D / 64;           // 64-dim boxes per key row
+  constexpr int BOXB = 16 * 128;         // one box: 16 keys x 64 dims bf16
+  constexpr int TILEB = 2 * NB64 * BOXB; // one K (or V) tile
+  constexpr int P = D + 8;
+  const int KG = 4 / RG;
+  const int seq = blockIdx.x, hk = blockIdx.y, chunk = blockIdx.z;
+  const int G = Hq / Hkv;
+  const int ql = q_len[seq];
+  const int t0 = chunk * tok_per_chunk;
+  if (t0 >= ql) return;
+  const int nt = min(tok_per_chunk, ql - t0);
+  const int R = nt * G;
+  const int kvl = kv_len[seq];
+  const int qs = q_start[seq];
+  const int first_pos = q_pos0[seq];
+  const int last_key = min(first_pos + t0 + nt - 1, kvl - 1);
+  const int* btg = block_table + (size_t)seq_slot[seq] * max_blocks;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, c = lane & 3;
+  const int rg = warp % RG, kg = warp / RG;
+  __shared__ int bt[ATT_MAX_BLOCKS];
+  __shared__ __align__(8) uint64_t full[NS];
+  const int nblk_used = min((last_key >> 4) + 1, max_blocks);
+  for (int i = tid; i < nblk_used; i += ATT_THREADS) bt[i] = btg[i];
+  extern __shared__ __align__(1024) uint8_t at_smem[];
+  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(at_smem) + 1023) &
+                                             ~uintptr_t(1023));
+  typedef __nv_bfloat16 Row[P];
+  Row* sQ = reinterpret_cast<Row*>(ring + (size_t)NS * KG * 2 * TILEB);
+  if (tid == 0) {
+    psd::tma_prefetch(&tmK);
+    psd::tma_prefetch(&tmV);
+    for (int s = 0; s < NS; ++s) psd::mbar_init(full + s, 1);
+    psd::fence_barrier_init();
+  }
+  const int ntiles = last_key / KT + 1;
+  const int ngroups = (ntiles + KG - 1) / KG;
+  __syncthreads();  // bt staged, barriers initialised
+  const uint32_t ring_s = psd::smem_u32(ring);
+  auto kbase = [&](int st, int j) { return ring + (size_t)((st * KG + j) * 2) * TILEB; };
+  // group gi -> stage st (thread 0): KG tiles x 2 blocks x NB64 boxes, K and V
+  auto issue = [&](int gi, int st) {
+    psd::mbar_arrive_expect_tx(full + st, (uint32_t)(KG * 2 * TILEB));
+    for (int j = 0; j < KG; ++j) {
+      const int tile = gi * KG + j;
+      uint8_t* kd = kbase(st, j);
+      uint8_t* vd = kd + TILEB;
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int blk = tile * 2 + b;
+        const int slot = (tile < ntiles && blk < nblk_used) ? bt[blk] * 16 : -16;
+#pragma unroll
+        for (int x = 0; x < NB64; ++x) {
+          psd::tma_load_3d(kd + (b * NB64 + x) * BOXB, &tmK, full + st, x * 64, hk, slot);
+          psd::tma_load_3d(vd + (b * NB64 + x) * BOXB, &tmV, full + st, x * 64, hk, slot);
+        }
+      }
+    }
+  };
+  pdl_wait();
+  pdl_trigger();
+  if (tid == 0) {
+    for (int t = 0; t < NS - 1 && t < ngroups; ++t) issue(t, t);
+  }
+  for (int idx = tid; idx < RG * 16 * (D / 8); idx += ATT_THREADS) {
+    const int r = idx / (D / 8), cc = idx % (D / 8);
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r < R) {
+      const int t = r / G, gg = r % G;
+      v = *reinterpret_cast<const uint4*>(q + ((size_t)(qs + t0 + t) * Hq + hk * G + gg) * D +
+                                          cc * 8);
+    }
+    *reinterpret_cast<uint4*>(&sQ[r][cc * 8]) = v;
+  }
+  __syncthreads();
+
+  const bool active = kg < KG && rg * 16 < R;
+  const int r0 = rg * 16 + g, r1 = r0 + 8;
+  const int lim0 = r0 < R ? min(first_pos + t0 + r0 / G, kvl - 1) : -1;
+  const int lim1 = r1 < R ? min(first_pos + t0 + r1 / G, kvl - 1) : -1;
+  uint32_t qf[D / 16][4];
+  if (active) {
+#pragma unroll
+    for (int kk = 0; kk < D / 16; ++kk) {
+      qf[kk][0] = *reinterpret_cast<const uint32_t*>(&sQ[r0][kk * 16 + 2 * c]);
+      qf[kk][1] = *reinterpret_cast<const uint32_t*>(&sQ[r1][kk * 16 + 2 * c]);
+      qf[kk][2] = *reinterpret_cast<const uint32_t*>(&sQ[r0][kk * 16 + 8 + 2 * c]);
+      qf[kk][3] = *reinterpret_cast<const uint32_t*>(&sQ[r1][kk * 16 + 8 + 2 * c]);
+    }
+  }
+  float o[D / 8][4];
+#pragma unroll
+  for (int n = 0; n < D / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  const int lrow = lane & 7, lmat = lane >> 3;
+  // byte offset of (key row, 16-byte dim chunk) inside a SW128 tile
+  auto toff = [](int row, int ch) -> uint32_t {
+    return (uint32_t)(((((row >> 4) * NB64 + (ch >> 3)) * 16 + (row & 15)) << 7) +
+                      (((ch & 7) ^ (row & 7)) << 4));
+  };
+
+  for (int gi = 0; gi < ngroups; ++gi) {
+    const int st = gi % NS;
+    if (tid == 0 && gi + NS - 1 < ngroups) issue(gi + NS - 1, (gi + NS - 1) % NS);
+    psd::mbar_wait(full + st, (uint32_t)((gi / NS) & 1));
+    const int kt = gi * KG + kg;
+    if (active && kt < ntiles) {
+      const uint32_t sk = ring_s + (uint32_t)((st * KG + kg) * 2) * TILEB;
+      const uint32_t sv = sk + TILEB;
+      float sacc[KT / 8][4];
+#pragma unroll
+      for (int n = 0; n < KT / 8; ++n) sacc[n][0] = sacc[n][1] = sacc[n][2] = sacc[n][3] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+#pragma unroll
+        for (int n = 0; n < KT / 8; n += 2) {
+          uint32_t kb[4];
+          const uint32_t a = sk + toff((n + (lmat >> 1)) * 8 + lrow, 2 * kk + (lmat & 1));
+          asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(kb[0]), "=r"(kb[1]), "=r"(kb[2]), "=r"(kb[3]) : "r"(a));
+          mma_bf16_16816(sacc[n], qf[kk], kb[0], kb[1]);
+          mma_bf16_16816(sacc[n + 1], qf[kk], kb[2], kb[3]);
+        }
+      }
+      float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+      for (int n = 0; n < KT / 8; ++n) {
+        const int key = kt * KT + n * 8 + 2 * c;
+        sacc[n][0] = key <= lim0 ? sacc[n][0] * scale_log2 : -INFINITY;
+        sacc[n][1] = key + 1 <= lim0 ? sacc[n][1] * scale_log2 : -INFINITY;
+        sacc[n][2] = key <= lim1 ? sacc[n][2] * scale_log2 : -INFINITY;
+        sacc[n][3] = key + 1 <= lim1 ? sacc[n][3] * scale_log2 : -INFINITY;
+        mx0 = fmaxf(mx0, fmaxf(sacc[n][0], sacc[n][1]));
+        mx1 = fmaxf(mx1, fmaxf(sacc[n][2], sacc[n][3]));
+      }
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+      const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+      const float base0 = mn0 == -INFINITY ? 0.f : mn0;
+      const float base1 = mn1 == -INFINITY ? 0.f : mn1;
+      const float al0 = exp2f(m0 - base0), al1 = exp2f(m1 - base1);
+      m0 = mn0;
+      m1 = mn1;
+      float ps0 = 0.f, ps1 = 0.f;
+      uint32_t pf[KT / 16][4];
+#pragma unroll
+      for (int n = 0; n < KT / 8; ++n) {
+        const float p0 = exp2f(sacc[n][0] - base0), p1 = exp2f(sacc[n][1] - base0);
+        const float p2 = exp2f(sacc[n][2] - base1), p3 = exp2f(sacc[n][3] - base1);
+        ps0 += p0 + p1;
+        ps1 += p2 + p3;
+        const int kk = n >> 1;
+        if ((n & 1) == 0) {
+          pf[kk][0] = pack_bf16(p0, p1);
+          pf[kk][1] = pack_bf16(p2, p3);
+        } else {
+          pf[kk][2] = pack_bf16(p0, p1);
+          pf[kk][3] = pack_bf16(p2, p3);
+        }
+      }
+      l0 = l0 * al0 + ps0;
+      l1 = l1 * al1 + ps1;
+#pragma unroll
+      for (int n = 0; n < D / 8; ++n) {
+        o[n][0] *= al0; o[n][1] *= al0; o[n][2] *= al1; o[n][3] *= al1;
+      }
+#pragma unroll
+      for (int kk = 0; kk < KT / 16; ++kk) {
+#pragma unroll
+        for (int n = 0; n < D / 8; n += 2) {
+          uint32_t vb[4];
+          const uint32_t a = sv + toff(kk * 16 + (lmat & 1) * 8 + lrow, n + (lmat >> 1));
+          asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(vb[0]), "=r"(vb[1]), "=r"(vb[2]), "=r"(vb[3]) : "r"(a));
+          mma_bf16_16816(o[n], pf[kk], vb[0], vb[1]);
+          mma_bf16_16816(o[n + 1], pf[kk], vb[2], vb[3]);
+        }
+      }
+    }
+    __syncthreads();  // stage st is free for the group NS - 1 ahead
+  }
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  if (KG > 1) {
+    // merge key-group states through the (idle) ring: warp (rg, kg > 0)
+    // publishes, warp (rg, 0) merges in key-group order
+    float* scr = reinterpret_cast<float*>(ring);
+    const int slot_floats = 16 * D + 32;
+    if (active && kg > 0) {
+      float* sp = scr + (rg * KG + kg) * slot_floats;
+#pragma unroll
+      for (int n = 0; n < D / 8; ++n) {
+        const int d = n * 8 + 2 * c;
+        sp[g * D + d] = o[n][0];
+        sp[g * D + d + 1] = o[n][1];
+        sp[(g + 8) * D + d] = o[n][2];
+        sp[(g + 8) * D + d + 1] = o[n][3];
+      }
+      if (c == 0) {
+        sp[16 * D + g] = m0;
+        sp[16 * D + g + 8] = m1;
+        sp[16 * D + 16 + g] = l0;
+        sp[16 * D + 16 + g + 8] = l1;
+      }
+    }
+    __syncthreads();
+    if (active && kg == 0) {
+      float M0 = m0, M1 = m1;
+      for (int j = 1; j < KG; ++j) {
+        const float* sp = scr + (rg * KG + j) * slot_floats;
+        M0 = fmaxf(M0, sp[16 * D + g]);
+        M1 = fmaxf(M1, sp[16 * D + g + 8]);
+      }
+      const float w00 = M0 == -INFINITY ? 0.f : exp2f(m0 - M0);
+      const float w10 = M1 == -INFINITY ? 0.f : exp2f(m1 - M1);
+      l0 *= w00;
+      l1 *= w10;
+#pragma unroll
+      for (int n = 0; n < D / 8; ++n) {
+        o[n][0] *= w00; o[n][1] *= w00; o[n][2] *= w10; o[n][3] *= w10;
+      }
+      for (int j = 1; j < KG; ++j) {
+        const float* sp = scr + (rg * KG + j) * slot_floats;
+        const float mj0 = sp[16 * D + g], mj1 = sp[16 * D + g + 8];
+        const float wj0 = mj0 == -INFINITY ? 0.f : exp2f(mj0 - M0);
+        const float wj1 = mj1 == -INFINITY ? 0.f : exp2f(mj1 - M1);
+        l0 += sp[16 * D + 16 + g] * wj0;
+        l1 += sp[16 * D + 16 + g + 8] * wj1;
+#pragma unroll
+        for (int n = 0; n < D / 8; ++n) {
+          const int d = n * 8 + 2 * c;
+          o[n][0] += sp[g * D + d] * wj0;
+          o[n][1] += sp[g * D + d + 1] * wj0;
+          o[n][2] += sp[(g + 8) * D + d] * wj1;
+          o[n][3] += sp[(g + 8) * D + d + 1] * wj1;
+        }
+      }
+    }
+  }
+  if (!active || kg != 0) return;
+  const float inv0 = l0 > 0.f ? 1.f / l0 : 0.f, inv1 = l1 > 0.f ? 1.f / l1 : 0.f;
+  const int ta0 = r0 / G, ga0 = r0 % G, ta1 = r1 / G, ga1 = r1 % G;
+#pragma unroll
+  for (int n = 0; n < D / 8; ++n) {
+    const int d = n * 8 + 2 * c;
+    if (r0 < R)
+      *reinterpret_cast<__nv_bfloat162*>(out + ((size_t)(qs + t0 + ta0) * Hq + hk * G + ga0) * D +
+                                         d) = __floats2bfloat162_rn(o[n][0] * inv0, o[n][1] * inv0);
+    if (r1 < R)
+      *reinterpret_cast<__nv_bfloat162*>(out + ((size_t)(qs + t0 + ta1) * Hq + hk * G + ga1) * D +
+                                         d) = __floats2bfloat162_rn(o[n][2] * inv1, o[n][3] * inv1);
+  }
+}
+
 // ---- decode attention: every key of a sequence in flight at once -------------
 // For draft decode passes (<= 16 query rows per kv head: 1-2 tokens x G heads).
 // One CTA per (sequence, kv head) issues the cp.async copies of ALL its key
@@ -1391,10 +1671,51 @@ size_t psd_attention_workspace_bytes(int num_seqs, int Hkv, int max_q_len, int H
   return 4096 * sizeof(int) + units * S * ATT_MAXR * (D + 2) * sizeof(float);
 }
 
+// TMA view of one paged cache tensor [slots][Hkv][D] bf16: box = 64 dims x 1
+// head x 16 slots, 128-byte swizzle.  The slot extent is left open (2^24):
+// coordinates come from the block table, negative ones zero-fill.
+typedef CUresult (*KvEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                               const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                               CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static KvEncodeFn kv_encode_fn() {
+  static KvEncodeFn fn = [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      return reinterpret_cast<KvEncodeFn>(p);
+    return (KvEncodeFn) nullptr;
+  }();
+  return fn;
+}
+
+static int make_kv_map(CUtensorMap* map, const void* base, int Hkv, int D) {
+  KvEncodeFn fn = kv_encode_fn();
+  if (!fn || (reinterpret_cast<uintptr_t>(base) & 15)) return 1;
+  cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)Hkv, (cuuint64_t)1 << 24};
+  cuuint64_t strides[2] = {(cuuint64_t)D * 2, (cuuint64_t)Hkv * D * 2};
+  cuuint32_t box[3] = {64, 1, 16};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : 1;
+}
+
+// PSD_ATT_TMA=0 keeps the cp.async kernel for verify / prefill (A/B runs)
+static int att_tma() {
+  static const int v = [] {
+    const char* e = getenv("PSD_ATT_TMA");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 static int att_ns() {
   static const int v = [] {
     const char* e = getenv("PSD_ATT_NS");
-    return e ? atoi(e) : 3;
+    return e ? atoi(e) : 2;
   }();
   return v;
 }
@@ -1432,6 +1753,25 @@ static int attention_launch(const void* q, const void* k_cache, const void* v_ca
   const float sl2 = scale * 1.44269504088896341f;
   const RopeSrc rs = rope ? *rope : RopeSrc{};
   cudaError_t err = cudaSuccess;
+  if (!rope && S == 1 && block_size == 16 && (D == 64 || D == 128) && att_tma()) {
+    CUtensorMap mk, mv;
+    if (make_kv_map(&mk, k_cache, Hkv, D) == 0 && make_kv_map(&mv, v_cache, Hkv, D) == 0) {
+      const int ns = att_ns() >= 3 ? 3 : 2;
+      const int tileb = 32 * D * 2;
+      const int smem = 1024 + ns * KG * 2 * tileb + RG * 16 * (D + 8) * 2;
+      auto go_tma = [&](auto kern) {
+        if ((err = psd::ensure_smem_limit((const void*)kern, 200 * 1024, (cudaStream_t)stream)))
+          return;
+        err = psd::launch(kern, dim3(num_seqs, Hkv, chunks), dim3(ATT_THREADS), smem,
+                          (cudaStream_t)stream, mk, mv, static_cast<const __nv_bfloat16*>(q),
+                          block_table, max_blocks, seq_slot, q_start, q_len, q_pos0, kv_len, Hq,
+                          Hkv, sl2, tpc, RG, static_cast<__nv_bfloat16*>(out));
+      };
+      if (D == 64) ns == 3 ? go_tma(attention_tma_kernel<64, 3>) : go_tma(attention_tma_kernel<64, 2>);
+      else ns == 3 ? go_tma(attention_tma_kernel<128, 3>) : go_tma(attention_tma_kernel<128, 2>);
+      return (int)err;
+    }
+  }
   auto go = [&](auto kern, int kt, int d, int ns = ATT_STAGES) {
     const int smem = (RG * 16 + 2 * ns * KG * kt) * (d + 8) * 2;
     if ((err = psd::ensure_smem_limit((const void*)kern, 200 * 1024, (cudaStream_t)stream)))
