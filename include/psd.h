@@ -142,6 +142,7 @@ int psd_verify_greedy_fold(const float* partials, int W, int V_shard, const int3
 #define PSD_EPI_RESID 2
 #define PSD_EPI_SILU 3
 #define PSD_EPI_PARTIAL 4 /* internal: split-K partials */
+#define PSD_EPI_ARGMAX 5 /* internal: per-(128-row tile, token) (max, first argmax) partials (K6) */
 /* Cap the CTAs of subsequently enqueued (or captured) GEMM grids (0 = all SMs):
  * the verify forward runs beside the draft loop on one GPU. */
 void psd_gemm_set_max_ctas(int n);
@@ -167,6 +168,24 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
  * p_bytes cannot hold splits*M*N floats. */
 int psd_gemm_partials(const void* X, int ldx, int M, int K, const void* W, int ldw, int N,
                       float* P, size_t p_bytes, int splits_hint, int* splits_used, void* stream);
+
+/* K6, the draft's greedy sampler fused into its LM head (replaces the logits
+ * store + psd_bigram_bias + psd_verify_greedy(k = 0) of a draft step; seam
+ * engine.py:355-364, 376-380): the stream-K LM-head GEMM's epilogue reduces
+ * every finished (128-row vocabulary tile, token) to (max, lowest argmax
+ * index) -- after adding `beta` to token m's logit at column
+ * successor[tokens[rows ? rows[m] : m]] when successor and beta != 0 -- into
+ * `partials` (psd_argmax_partials_bytes); psd_argmax_fold reduces the tiles
+ * (ties -> lowest index, K1's canonical argmax) into out_tokens[m] and/or
+ * dst[dst_idx[m]] (skipped when negative).  M <= 128, N % 128 == 0; the
+ * workspace is psd_gemm_bf16's stream-K workspace. */
+size_t psd_argmax_partials_bytes(int M, int N);
+int psd_gemm_argmax(const void* X, int ldx, int M, int K, const void* W, int ldw, int N,
+                    const int32_t* tokens, const int32_t* rows, const int32_t* successor,
+                    float beta, void* partials, void* workspace, size_t workspace_bytes,
+                    void* stream);
+int psd_argmax_fold(const void* partials, int M, int N, int32_t* out_tokens, int32_t* dst,
+                    const int32_t* dst_idx, void* stream);
 
 /* ---- K3/K3'/K4: forward-pass building blocks (bf16 storage, fp32 math) ----
  * Same seam as K2 (the virtual pass durations).  Row-major activations. */

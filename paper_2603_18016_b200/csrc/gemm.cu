@@ -26,6 +26,7 @@
 // fused SiLU(gate) * up (weights packed gate/up per 64-row half tile).
 #include <algorithm>
 #include <atomic>
+#include <cstring>
 #include <cstdlib>
 #include <mutex>
 
@@ -63,7 +64,7 @@ constexpr int ep_buf_bytes() {
 // staging bytes of an epilogue kind (0: per-thread global stores)
 template <int EPI>
 constexpr int ep_stage_bytes() {
-  return EPI == PSD_EPI_RESID ? 0 : kEpBytes;
+  return (EPI == PSD_EPI_RESID || EPI == PSD_EPI_ARGMAX) ? 0 : kEpBytes;
 }
 
 // NT token tiles of BN rows per weight tile (NT = 2 for 256 < M <= 512: every
@@ -340,6 +341,14 @@ struct SKArgs {
   int D;                      // tiles 0..D-1 whole per CTA (c, c+G, ..), after its stream-K units
   int tma_y;                  // finished tiles leave through TMA stores of tmY
   CUtensorMap tmY;            // Y [M][N_out] (bf16 / f32), box 16 tokens x 128 (64 SiLU) rows
+  // PSD_EPI_ARGMAX (K6, the draft's greedy LM head): Y = float2 [M][N / 128]
+  // (max, first argmax index) per (vocabulary tile, token); token m's logit at
+  // column succ[tok[rows[m]]] gets + beta first (the synthetic-language bias,
+  // as psd_bigram_bias adds it to stored logits)
+  const int32_t* am_tok;
+  const int32_t* am_rows;
+  const int32_t* am_succ;
+  float am_beta;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -552,6 +561,20 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     const int q = warp & 3;
     const int row = 32 * q + lane;  // tile row (weight row) of this thread
     pdl_wait();  // residual / partial workspace belong to the predecessor's epoch
+    __shared__ int s_bcol[EPI == PSD_EPI_ARGMAX ? 256 : 1];
+    __shared__ float s_amv[EPI == PSD_EPI_ARGMAX ? 16 * 136 : 1];
+    if constexpr (EPI == PSD_EPI_ARGMAX) {
+      // biased column of every token (three dependent loads, off the MMAs' path)
+      for (int m = threadIdx.x - 64; m < 256; m += 128) {
+        int col = -1;
+        if (m < g.M && g.am_succ && g.am_beta != 0.f) {
+          const int t = g.am_tok[g.am_rows ? g.am_rows[m] : m];
+          if (t >= 0 && t < g.N) col = g.am_succ[t];
+        }
+        s_bcol[m] = col;
+      }
+      named_bar_sync(1, 128);
+    }
     SegIt it = seg_begin(c);
     Seg sg;
     int j = 0, eq = 0;
@@ -663,6 +686,43 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           for (int e = 0; e < EG; ++e) {
             const int col = col0 + 16 * e;
             if (col >= ACC_COLS) break;
+            if constexpr (EPI == PSD_EPI_ARGMAX) {
+              // per token column: max over the tile's 128 rows and the lowest
+              // row attaining it.  Rows go through shared memory transposed
+              // ([16 columns][136]: conflict-free both ways); 8 threads per
+              // column scan rows p, p + 8, ... and merge by shuffles
+              const int n = n0 + row;
+#pragma unroll
+              for (int k = 0; k < 16; ++k)
+                s_amv[k * 136 + row] = n < g.N ? v[e][k] : -INFINITY;
+              named_bar_sync(1, 128);
+              {
+                const int t = threadIdx.x - 64;
+                const int k = t >> 3, p = t & 7;
+                const int m = m0 + col + k;
+                const int brow = m < g.M ? s_bcol[m] - n0 : -1;
+                float bv = -INFINITY;
+                int bi = 0;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                  const int r = i * 8 + p;
+                  float x = s_amv[k * 136 + r];
+                  if (r == brow) x += g.am_beta;
+                  if (x > bv) { bv = x; bi = r; }
+                }
+#pragma unroll
+                for (int off = 4; off >= 1; off >>= 1) {
+                  const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+                  const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+                  if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+                }
+                if (p == 0 && m < g.M)
+                  static_cast<float2*>(g.Y)[(size_t)m * (g.N / BM) + n0 / BM] =
+                      make_float2(bv, __int_as_float(n0 + bi));
+              }
+              named_bar_sync(1, 128);
+              continue;
+            }
             if constexpr (EPS > 0) {
               if (g.tma_y) {
                 // stage 16 tokens x the tile's output rows in smem, one TMA
@@ -1159,6 +1219,43 @@ int launch_epi(int bn, const CUtensorMap& mw, const CUtensorMap& mx, const GemmA
 }
 
 
+// K6 fold: token m's argmax over the vocabulary tiles' (max, index) partials
+// (ties -> lowest index, as K1's canonical argmax); optionally scattered into
+// dst[dst_idx[m]] (the draft token into its slot; a negative index skips)
+__global__ void __launch_bounds__(256)
+argmax_fold_kernel(const float2* __restrict__ part, int ntiles, int M, int32_t* __restrict__ out,
+                   int32_t* __restrict__ dst, const int32_t* __restrict__ dst_idx) {
+  pdl_wait();
+  pdl_trigger();
+  const int m = blockIdx.x, tid = threadIdx.x;
+  float bv = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int t = tid; t < ntiles; t += 256) {
+    const float2 p = __ldcg(part + (size_t)m * ntiles + t);
+    const int i = __float_as_int(p.y);
+    if (p.x > bv || (p.x == bv && i < bi)) { bv = p.x; bi = i; }
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+    if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+  }
+  __shared__ float sv[8];
+  __shared__ int si[8];
+  if ((tid & 31) == 0) { sv[tid >> 5] = bv; si[tid >> 5] = bi; }
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < 8; ++w)
+      if (sv[w] > bv || (sv[w] == bv && si[w] < bi)) { bv = sv[w]; bi = si[w]; }
+    if (out) out[m] = bi;
+    if (dst && dst_idx) {
+      const int d = dst_idx[m];
+      if (d >= 0) dst[d] = bi;
+    }
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -1247,6 +1344,58 @@ int psd_gemm_tiled(const void* X, int ldx, int M, int K, const void* W_tiled, in
   return (int)cudaErrorInvalidValue;
 }
 #endif  // PSD_EXPERIMENTAL
+
+size_t psd_argmax_partials_bytes(int M, int N) {
+  return (size_t)(N / BM) * M * sizeof(float2);
+}
+
+int psd_gemm_argmax(const void* X, int ldx, int M, int K, const void* W, int ldw, int N,
+                    const int32_t* tokens, const int32_t* rows, const int32_t* successor,
+                    float beta, void* partials, void* workspace, size_t workspace_bytes,
+                    void* stream) {
+  if (!X || !W || !partials || M <= 0 || M > 128 || N <= 0 || K <= 0 || (K % 8) || (N % BM))
+    return (int)cudaErrorInvalidValue;
+  if (successor && beta != 0.f && !tokens) return (int)cudaErrorInvalidValue;
+  if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(W)) & 15)
+    return (int)cudaErrorMisalignedAddress;
+  if ((ldx % 8) || (ldw % 8)) return (int)cudaErrorMisalignedAddress;
+  const SKPlan p = sk_plan(M, N, K);
+  if (p.nt != 1 || p.MT != 1) return (int)cudaErrorInvalidValue;
+  if (!workspace || workspace_bytes < p.part_bytes + p.ticket_bytes || p.tiles > kMaxTiles)
+    return (int)cudaErrorInvalidValue;
+  CUtensorMap mw, mx;
+  int rc;
+  if ((rc = make_map(&mw, W, N, K, ldw, BM))) return rc;
+  if ((rc = make_map(&mx, X, M, K, ldx, p.bn))) return rc;
+  SKArgs g;
+  memset(&g, 0, sizeof(g));
+  g.M = M; g.N = N; g.K = K;
+  g.KB = p.KB; g.MT = p.MT; g.tiles = p.tiles; g.G = p.G; g.U = p.U; g.D = p.D;
+  g.Y = partials; g.ldy = M;
+  g.tickets = static_cast<int*>(workspace);
+  g.part = reinterpret_cast<float*>(static_cast<char*>(workspace) + p.ticket_bytes);
+  g.trace = nullptr;
+  g.Wt = nullptr;
+  g.tma_y = 0;
+  g.am_tok = tokens; g.am_rows = rows; g.am_succ = successor; g.am_beta = beta;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (p.bn) {
+    case 32: return launch_sk_bn<32, PSD_EPI_ARGMAX, false>(mw, mx, g, st);
+    case 64: return launch_sk_bn<64, PSD_EPI_ARGMAX, false>(mw, mx, g, st);
+    case 96: return launch_sk_bn<96, PSD_EPI_ARGMAX, false>(mw, mx, g, st);
+    case 128: return launch_sk_bn<128, PSD_EPI_ARGMAX, false>(mw, mx, g, st);
+  }
+  return (int)cudaErrorInvalidValue;
+}
+
+int psd_argmax_fold(const void* partials, int M, int N, int32_t* out_tokens, int32_t* dst,
+                    const int32_t* dst_idx, void* stream) {
+  if (!partials || M <= 0 || N <= 0 || (N % BM) || (!out_tokens && !(dst && dst_idx)))
+    return (int)cudaErrorInvalidValue;
+  return (int)psd::launch(argmax_fold_kernel, dim3(M), dim3(256), 0, (cudaStream_t)stream,
+                          static_cast<const float2*>(partials), N / BM, M, out_tokens, dst,
+                          dst_idx);
+}
 
 int psd_gemm_partials(const void* X, int ldx, int M, int K, const void* W, int ldw, int N,
                       float* P, size_t p_bytes, int splits_hint, int* splits_used, void* stream) {

@@ -210,6 +210,10 @@ class GpuBackend:
             grid = mk_grid or int(os.environ.get("PSD_MK_GRID", "0"))
             with torch.cuda.device(dev):
                 self.mk = self._make_mk(grid)
+        # K6: the greedy draft's argmax (+ bias) in its LM-head epilogue
+        # (PSD_K6=0: logits + bigram + K1(k = 0) + scatter, for A/B runs)
+        self.k6 = (os.environ.get("PSD_K6", "1") == "1" and has_d
+                   and self.dshape.vocab % 128 == 0 and max_batch <= 128)
         # verify GEMM grids capped below the SM count when the draft loop runs
         # beside them (dual stream): PSD_VERIFY_CTAS (0 = all SMs)
         # Default from the drafting / verify weight-volume ratio r = k x draft
@@ -639,6 +643,14 @@ class GpuBackend:
                                                 self.slot_tok.data_ptr(),
                                                 fwd.view("gather_src", i).data_ptr(), M, st),
                          "draft gather")
+            if self.mode == "greedy" and self.k6:
+                # K6: argmax (+ bias) in the LM head's epilogue, the fold
+                # scatters the token into its slot -- no logits, no K1 launch
+                fwd.run(M, nb, 2 if i == 0 else 1, nb, None, self.dshape.vocab,
+                        bigram=(self.succ_d, self.beta_draft), set_index=i,
+                        argmax_into=(self.d_out[:nb], self.slot_tok,
+                                     fwd.view("scatter_dst", i)))
+                continue
             fwd.run(M, nb, 2 if i == 0 else 1, nb, self.dlogits, self.dshape.vocab,
                     bigram=(self.succ_d, self.beta_draft), set_index=i)
             if self.mode == "greedy":

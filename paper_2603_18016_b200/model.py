@@ -343,6 +343,10 @@ class Forward:
         self.act = torch.empty(T, s.ffn_padded, dtype=bf, device=dev)
         self.xf = torch.empty(max_logit_rows, s.hidden, dtype=bf, device=dev)
         self.prev = torch.empty(max_logit_rows, dtype=torch.int32, device=dev)
+        # K6 argmax partials (allocated here: never inside a graph capture)
+        self.amax = (torch.empty(native.load().psd_argmax_partials_bytes(max_logit_rows, s.vocab),
+                                 dtype=torch.uint8, device=dev)
+                     if s.vocab % 128 == 0 and max_logit_rows <= 128 else None)
         self.comm = None
         if model.tp is not None and model.tp[1] > 1:
             import os
@@ -467,14 +471,18 @@ class Forward:
 
     def run(self, n_tokens: int, n_seqs: int, max_q_len: int, n_logit_rows: int,
             logits: torch.Tensor | None, logits_ld: int = 0, bigram=None,
-            set_index: int = 0, shard_out: bool = False) -> None:
+            set_index: int = 0, shard_out: bool = False, argmax_into=None) -> None:
         """Enqueue the forward on the current stream.  ``tokens`` may be
         filled on device beforehand (draft loop); ``logits`` (fp32, row pitch
         ``logits_ld``) receives the LM-head output of ``logit_rows``.
         shard_out (tensor-parallel target): keep this rank's vocabulary shard
         in ``lshard`` ([rows, vocab shard padded], bigram bias applied to the
         shard's columns) instead of all-gathering full rows -- the greedy
-        verifier reduces shards to partials."""
+        verifier reduces shards to partials.
+        argmax_into (greedy draft step, K6): (out_tokens, dst, dst_idx) -- the
+        LM head's epilogue reduces the (biased) logits to per-tile argmax
+        partials and one fold writes each row's token to out_tokens[m] and
+        dst[dst_idx[m]]; no logits are stored."""
         m = self.model
         s = m.shape
         lib = m._lib
@@ -553,7 +561,7 @@ class Forward:
             prev_S = nsp._obj.value
             if tp:  # row-parallel down
                 prev_S = self._tp_reduce(prev_S, M * H)
-        if n_logit_rows == 0 or logits is None:
+        if n_logit_rows == 0 or (logits is None and argmax_into is None):
             return  # prefill: only the KV cache is needed
         R = n_logit_rows
         _chk(lib.psd_add_rmsnorm(X, H, part, prev_S, M * H, H, v["logit_rows"].data_ptr(),
@@ -561,6 +569,21 @@ class Forward:
                                  0, st), "final norm")
         V = m.full_vocab
         ld = logits_ld or V
+        if argmax_into is not None and not tp:
+            out_tok, dst, dst_idx = argmax_into
+            if self.amax is None:
+                raise ValueError("argmax LM head needs vocab % 128 == 0 and <= 128 logit rows")
+            succ, beta = bigram if bigram is not None else (None, 0.0)
+            _chk(lib.psd_gemm_argmax(self.xf.data_ptr(), H, R, H, m.lm_head.data_ptr(), H, s.vocab,
+                                     v["tokens"].data_ptr(), v["logit_rows"].data_ptr(),
+                                     succ.data_ptr() if succ is not None else None, float(beta),
+                                     self.amax.data_ptr(), ws, wsn, st), "gemm lm_head argmax")
+            _chk(lib.psd_argmax_fold(self.amax.data_ptr(), R, s.vocab,
+                                     out_tok.data_ptr() if out_tok is not None else None,
+                                     dst.data_ptr() if dst is not None else None,
+                                     dst_idx.data_ptr() if dst_idx is not None else None, st),
+                 "argmax fold")
+            return
         if tp:
             # vocab-parallel LM head: this rank's slice (all-gathered into full
             # rows unless the caller consumes the shard)

@@ -34,6 +34,9 @@ SIGNATURES: dict[str, tuple] = {
                                _p, _p, _p, _sz, _p]),
     "psd_gemm_plan": (_i, [_i, _i, _i, _i, _i, _c.POINTER(_i), _c.POINTER(_sz)]),
     "psd_gemm_bf16": (_i, [_p, _i, _i, _i, _p, _i, _i, _p, _i, _i, _p, _i, _i, _p, _sz, _p]),
+    "psd_argmax_partials_bytes": (_sz, [_i, _i]),
+    "psd_gemm_argmax": (_i, [_p, _i, _i, _i, _p, _i, _i, _p, _p, _p, _f, _p, _p, _sz, _p]),
+    "psd_argmax_fold": (_i, [_p, _i, _i, _p, _p, _p, _p]),
     "psd_embed": (_i, [_p, _i, _p, _i, _p, _p]),
     "psd_add_rmsnorm": (_i, [_p, _i, _p, _i, _sz, _i, _p, _p, _p, _i, _i, _i, _f, _i, _p]),
     "psd_rope_kv": (_i, [_p, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _p, _p]),

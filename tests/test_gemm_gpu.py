@@ -162,3 +162,47 @@ def test_gemm_trace_timeline(cuda_device):
     ops.gemm(x, w, epi=native.EPI_SILU, splits=0)
     torch.cuda.synchronize()
     assert int(tr.abs().sum()) == 0
+
+
+@pytest.mark.parametrize("M,N,K", [(32, 128256, 2048), (1, 1024, 256), (8, 151936, 896),
+                                   (64, 128256, 2048), (100, 2048, 512)])
+@pytest.mark.parametrize("bias", [False, True])
+def test_lm_head_argmax_epilogue(cuda_device, M, N, K, bias):
+    """K6: argmax (+ the synthetic-language bias) in the stream-K LM head's
+    epilogue + the tile fold == argmax of the same GEMM's stored fp32 logits
+    after psd_bigram_bias (bit-identical values, lowest index on ties), and
+    the fold's scatter into dst."""
+    dev = cuda_device
+    g = torch.Generator(device=dev).manual_seed(M + N + K)
+    x = torch.randn(M, K, device=dev, generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device=dev, generator=g) * 0.05).to(torch.bfloat16)
+    w[N // 2] = w[N // 3]       # exact ties: the lower index must win
+    w[N - 1] = w[5]
+    lib = native.load()
+    st = torch.cuda.current_stream().cuda_stream
+    ws = torch.zeros(256 << 20, dtype=torch.uint8, device=dev)
+    tokens = torch.randint(0, N, (M + 3,), device=dev, dtype=torch.int32, generator=g)
+    rows = torch.arange(M, device=dev, dtype=torch.int32) + 3
+    succ = torch.randint(0, N, (N,), device=dev, dtype=torch.int32, generator=g)
+    beta = 7.0 if bias else 0.0
+    logits = torch.empty(M, N, device=dev)
+    assert lib.psd_gemm_bf16(x.data_ptr(), K, M, K, w.data_ptr(), K, N, logits.data_ptr(), N,
+                             native.EPI_F32, None, 0, 0, ws.data_ptr(), ws.numel(), st) == 0
+    if bias:
+        prev = tokens[rows.long()].contiguous()
+        assert lib.psd_bigram_bias(logits.data_ptr(), N, prev.data_ptr(), M, succ.data_ptr(), N,
+                                   beta, st) == 0
+    part = torch.empty(lib.psd_argmax_partials_bytes(M, N), dtype=torch.uint8, device=dev)
+    out = torch.full((M,), -1, dtype=torch.int32, device=dev)
+    dst = torch.full((2 * M,), -7, dtype=torch.int32, device=dev)
+    dst_idx = (torch.arange(M, device=dev, dtype=torch.int32) * 2)
+    dst_idx[0] = -1  # skipped
+    assert lib.psd_gemm_argmax(x.data_ptr(), K, M, K, w.data_ptr(), K, N, tokens.data_ptr(),
+                               rows.data_ptr(), succ.data_ptr() if bias else None, beta,
+                               part.data_ptr(), ws.data_ptr(), ws.numel(), st) == 0
+    assert lib.psd_argmax_fold(part.data_ptr(), M, N, out.data_ptr(), dst.data_ptr(),
+                               dst_idx.data_ptr(), st) == 0
+    torch.cuda.synchronize()
+    ref = logits.argmax(dim=1).to(torch.int32)
+    assert torch.equal(out, ref)
+    assert dst[0].item() == -7 and torch.equal(dst[2::2], ref[1:])

@@ -257,6 +257,46 @@ def verify_case(tag, B, K, V, sampling, cached=False):
     report(f"K1 {tag}", f"B={B} k={K} V={V}", us, algorithmic_bytes(B, K, V, sampling))
 
 
+def lm_argmax_case(tag, M, N, K, copies=2):
+    """K6: the draft's greedy LM head + sampler, fused (argmax epilogue + fold)
+    vs stored logits + bigram bias + K1 (k = 0)"""
+    x = torch.randn(M, K, device=dev).to(bf)
+    ws = [(torch.randn(N, K, device=dev) * 0.02).to(bf) for _ in range(copies)]
+    wsp = torch.zeros(64 << 20, dtype=torch.uint8, device=dev)
+    logits = torch.empty(M, N, device=dev)
+    tok = torch.randint(0, N, (M,), dtype=torch.int32, device=dev)
+    succ = torch.randint(0, N, (N,), dtype=torch.int32, device=dev)
+    part = torch.empty(lib.psd_argmax_partials_bytes(M, N), dtype=torch.uint8, device=dev)
+    out = torch.empty(M, dtype=torch.int32, device=dev)
+    ids0 = torch.zeros(M, 0, dtype=torch.int32, device=dev)
+    len0 = torch.zeros(M, dtype=torch.int32, device=dev)
+    acc = torch.empty(M, dtype=torch.int32, device=dev)
+    o1 = torch.empty(M, 1, dtype=torch.int32, device=dev)
+    it = [0]
+
+    def fused():
+        st = torch.cuda.current_stream().cuda_stream
+        w = ws[it[0] % copies]
+        it[0] += 1
+        assert lib.psd_gemm_argmax(x.data_ptr(), K, M, K, w.data_ptr(), K, N, tok.data_ptr(), None,
+                                   succ.data_ptr(), 16.0, part.data_ptr(), wsp.data_ptr(),
+                                   wsp.numel(), st) == 0
+        assert lib.psd_argmax_fold(part.data_ptr(), M, N, out.data_ptr(), None, None, st) == 0
+
+    def unfused():
+        st = torch.cuda.current_stream().cuda_stream
+        w = ws[it[0] % copies]
+        it[0] += 1
+        assert lib.psd_gemm_bf16(x.data_ptr(), K, M, K, w.data_ptr(), K, N, logits.data_ptr(), N,
+                                 native.EPI_F32, None, 0, 0, wsp.data_ptr(), wsp.numel(), st) == 0
+        assert lib.psd_bigram_bias(logits.data_ptr(), N, tok.data_ptr(), M, succ.data_ptr(), N,
+                                   16.0, st) == 0
+        ops.verify_greedy(logits.view(M, 1, N), ids0, len0, acc, o1)
+    nbytes = N * K * 2 + M * K * 2
+    report(f"lm head+argmax {tag} fused", f"M={M} N={N} K={K}", timeit(fused), nbytes)
+    report(f"lm head+argmax {tag} unfused", f"M={M} N={N} K={K}", timeit(unfused), nbytes)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--json", default=None)
@@ -373,6 +413,9 @@ def main():
         norm_case("1B", 32, 2048, 6)
         rope_case("8B", 192, 32, 8, 128, 3)
         rope_case("1B", 32, 32, 8, 64, 6)
+    if want("lmargmax"):
+        lm_argmax_case("1B", 32, 128256, 2048)
+        lm_argmax_case("1B M64", 64, 128256, 2048)
     if want("k1"):
         verify_case("greedy cfg2", 32, 5, 128256, False)
         verify_case("sample cfg2", 32, 5, 128256, True)
