@@ -526,7 +526,10 @@ def run_ours(args) -> None:
         # target + draft on each GPU, two streams
         args.layout = "pairs" if world >= 2 and world % 2 == 0 else "replicas"
     pairs = args.layout == "pairs"
-    tp_layout = args.layout == "tp"
+    # tp-draft: the paper's cfg4 deployment -- a tensor-parallel target over
+    # --tp ranks plus one dedicated draft rank per replica (world % (tp + 1) == 0)
+    tp_draft = args.layout == "tp-draft"
+    tp_layout = args.layout == "tp" or tp_draft
     global BETA_TARGET, BETA_DRAFT
     if tp_layout:
         CFG.update(CFG4)
@@ -535,6 +538,8 @@ def run_ours(args) -> None:
     if sampling:
         CFG.update(CFG3)
         BETA_TARGET, BETA_DRAFT = BETAS_CFG3
+    if args.models:  # smoke runs of a layout at smaller shapes (not a bench number)
+        CFG["target"], CFG["draft"] = args.models.split(",")
     if pairs and world % 2:
         raise SystemExit("--layout pairs needs an even number of GPUs")
     # replicas: every rank = target + draft on one GPU (two streams)
@@ -543,7 +548,20 @@ def run_ours(args) -> None:
     replica = rank // 2 if pairs else rank
     tp = None
     tp_size = 1
-    if tp_layout:
+    group_size = 1  # ranks per replica
+    if tp_draft:
+        tp_size = args.tp or max(1, world - 1)
+        group_size = tp_size + 1
+        if world % group_size:
+            raise SystemExit("--layout tp-draft needs a multiple of (--tp + 1) GPUs")
+        replica, li = rank // group_size, rank % group_size
+        roles = ("draft",) if li == tp_size else ("target",)
+        groups = [torch.distributed.new_group(list(range(r * group_size,
+                                                         r * group_size + tp_size)))
+                  for r in range(world // group_size)]
+        if tp_size > 1 and li < tp_size:
+            tp = (li, tp_size, groups[replica])
+    elif tp_layout:
         # world // tp_size replicas, each a tensor-parallel target over tp_size
         # ranks (SPMD scheduler) with the draft on a second stream of every TP
         # rank: the 8-GPU cfg4 layout "two TP4 replicas" (SURVEY §7 hard part 8)
@@ -560,8 +578,29 @@ def run_ours(args) -> None:
                     max_seq_len=CFG["prompt"] + CFG["output"] + 16, seed=replica,
                     beta_target=BETA_TARGET, beta_draft=BETA_DRAFT, device=dev, roles=roles,
                     mode="sample" if sampling else "greedy", temperature=1.0)
-    is_draft_rank = pairs and rank % 2 == 1
+    is_draft_rank = (pairs and rank % 2 == 1) or (tp_draft and "target" not in roles)
     backend = be
+    if tp_draft:
+        from paper_2603_18016_b200.pair import (DraftServer, GpuDraftEngine, GpuTargetEngine,
+                                                PairLink, PairTarget)
+        base = replica * group_size
+        draft_rank = base + tp_size
+        rep_groups = [torch.distributed.new_group(list(range(r * group_size,
+                                                             (r + 1) * group_size)))
+                      for r in range(world // group_size)]
+        comm = None
+        if os.environ.get("PSD_PAIR_LINK", "peer") == "peer":
+            from paper_2603_18016_b200.comm import PeerComm
+            comm = PeerComm(rep_groups[replica], buf_bytes=1 << 12, mbox_bytes=1 << 20,
+                            device=dev)
+        nccl = dev if args.dist_backend == "nccl" else None
+        if is_draft_rank:
+            link = PairLink(base, nccl, comm=comm, comm_peer=0)
+            followers = tuple(PairLink(base + j, nccl, comm=comm, comm_peer=j)
+                              for j in range(1, tp_size))
+        else:
+            link = PairLink(draft_rank, nccl, comm=comm, comm_peer=tp_size)
+            backend = PairTarget(GpuTargetEngine(be), link, leader=rank == base)
     if pairs:
         from paper_2603_18016_b200.pair import (DraftServer, GpuDraftEngine, GpuTargetEngine,
                                                 PairLink, PairTarget)
@@ -601,16 +640,17 @@ def run_ours(args) -> None:
     for mode in modes:
         if is_draft_rank:
             # serve warm-up + timed passes of this mode, then join the timing reduction
-            DraftServer(GpuDraftEngine(be), link).serve()
+            fol = followers if tp_draft else ()
+            DraftServer(GpuDraftEngine(be), link, fol).serve()
             barrier()
-            DraftServer(GpuDraftEngine(be), link).serve()
+            DraftServer(GpuDraftEngine(be), link, fol).serve()
             barrier()
             pd.aggregate(0, 0.0, dev)
             results[mode] = None
             continue
         for _ in range(args.warmup):
             one(mode)
-        if pairs:
+        if pairs or tp_draft:
             backend.stop()
         barrier()
         clocks = Clocks(local) if mode == "psd" else None
@@ -625,7 +665,7 @@ def run_ours(args) -> None:
             reps.append(rep_)
             states.append(st_)
         e1.record()
-        if pairs:
+        if pairs or tp_draft:
             backend.stop()
         barrier()
         launches[mode] = be.launches - l0
@@ -641,7 +681,7 @@ def run_ours(args) -> None:
     # end to end through the public API with host prompts / host outputs
     barrier()
     if is_draft_rank:
-        DraftServer(GpuDraftEngine(be), link).serve()
+        DraftServer(GpuDraftEngine(be), link, followers if tp_draft else ()).serve()
     else:
         x0 = be.transfer_bytes()
         t0 = time.perf_counter()
@@ -649,7 +689,7 @@ def run_ours(args) -> None:
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
         x1 = be.transfer_bytes()
-        if pairs:
+        if pairs or tp_draft:
             backend.stop()
     # the other baseline on the same GPUs: every GPU an independent SD(2m)
     # replica (target + draft on one GPU, its own 64 requests)
@@ -705,18 +745,22 @@ def run_ours(args) -> None:
                                 "random-init bf16, 2x32 requests, k=4, prompt 128, output 256, "
                                 "T=1.0 rejection sampling, both models on one GPU"
                                 if sampling else
-                                "cfg4: Llama-3.1-70B target (tensor-parallel replicas, --tp "
-                                "ranks each, draft on a second stream of every TP rank) / "
+                                ("cfg4: Llama-3.1-70B target (tensor-parallel over --tp ranks "
+                                 "+ a dedicated draft rank per replica) / " if tp_draft else
+                                 "cfg4: Llama-3.1-70B target (tensor-parallel replicas, --tp "
+                                 "ranks each, draft on a second stream of every TP rank) / ") +
                                 "Llama-3.2-1B draft shapes, random-init bf16, 2x64 requests, "
                                 "k=4, prompt 128, output 256, greedy" if tp_layout else
                                 "cfg2: Llama-3.1-8B target / Llama-3.2-1B draft shapes, "
                                 "random-init bf16, 2x32 requests, k=5, prompt 128, output 256, "
                                 "greedy, 1 GPU per replica (draft / verify on separate streams)"),
-                   "global_batch": (world // tp_size if tp_layout else
+                   "global_batch": (world // group_size if tp_draft else
+                                    world // tp_size if tp_layout else
                                     world // 2 if pairs else world)
                    * CFG["n_requests"],
                    "seq_len": CFG["prompt"] + CFG["output"],
-                   "parallelism": (f"tp{tp_size}x{world // tp_size}" if tp_layout else
+                   "parallelism": (f"tp{tp_size}+draft x{world // group_size}" if tp_draft else
+                                   f"tp{tp_size}x{world // tp_size}" if tp_layout else
                                    f"pairs{world // 2}" if pairs else f"replicas{world}"),
                    "l2": "inputs > L2 (weights 18.5 GB streamed per step)",
                    "synthetic_language_beta": [BETA_TARGET, BETA_DRAFT]},
@@ -778,6 +822,9 @@ def main() -> None:
                          "of the multi-rank layouts on one GPU)")
     ap.add_argument("--tp", type=int, default=0,
                     help="--layout tp: ranks per tensor-parallel replica (default: all)")
+    ap.add_argument("--models", default="",
+                    help="TARGET,DRAFT preset override for smoke runs of a layout (e.g. "
+                         "tp-draft with 8B / 1B shapes on one GPU); not a bench number")
     ap.add_argument("--no-sweep", action="store_true",
                     help="skip the config-5 verify-kernel grid (verify_sweep)")
     ap.add_argument("--ktune", action="store_true",
@@ -785,11 +832,14 @@ def main() -> None:
     ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3"],
                     help="cfg2: 8B / 1B greedy (the headline); cfg3: Qwen2.5-7B / 0.5B, "
                          "T = 1.0 rejection sampling over the 152k vocabulary")
-    ap.add_argument("--layout", default="auto", choices=["auto", "replicas", "pairs", "tp"],
+    ap.add_argument("--layout", default="auto",
+                    choices=["auto", "replicas", "pairs", "tp", "tp-draft"],
                     help="auto: pairs for an even number of GPUs, else replicas; "
                          "replicas: each GPU runs target+draft (two streams); pairs: "
                          "dedicated draft GPU per target GPU (NCCL hand-off, pair.py); tp: "
-                         "BASELINE config 4, 70B target tensor-parallel over all GPUs")
+                         "BASELINE config 4, 70B target tensor-parallel over all GPUs; "
+                         "tp-draft: config 4 as deployed in the paper, a --tp-way "
+                         "tensor-parallel target + a dedicated draft GPU per replica")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

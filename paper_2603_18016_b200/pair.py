@@ -48,13 +48,16 @@ K_STEP, K_STOP = 0, 1
 class PairLink:
     """Length-prefixed int32 messages to / from one peer rank."""
 
-    def __init__(self, peer: int, device=None, comm=None) -> None:
+    def __init__(self, peer: int, device=None, comm=None, comm_peer: int | None = None) -> None:
         self.peer = peer
         self.device = device  # CUDA device for NCCL, None for gloo
-        # comm (a 2-rank comm.PeerComm): drafted ids go through its device
-        # mailbox over NVLink peer memory (psd_p2p_put/get_i32) instead of
-        # dist.send / recv; commands and q rows still use dist
+        # comm (a comm.PeerComm over the pair, or over a target group + its
+        # draft rank): drafted ids go through its device mailbox over NVLink
+        # peer memory (psd_p2p_put/get_i32) instead of dist.send / recv;
+        # commands and q rows still use dist.  comm_peer: the peer's rank in
+        # the comm (default: the other rank of a 2-rank comm)
         self.comm = comm
+        self.comm_peer = (1 - comm.rank if comm is not None and comm_peer is None else comm_peer)
         self.bytes_sent = 0
         self.bytes_recv = 0
 
@@ -88,7 +91,7 @@ class PairLink:
         t = ids if isinstance(ids, torch.Tensor) else torch.from_numpy(
             np.ascontiguousarray(ids, dtype=np.int32))
         if self.comm is not None:
-            self.comm.put(1 - self.comm.rank, t.to(self.comm.device).contiguous())
+            self.comm.put(self.comm_peer, t.to(self.comm.device).contiguous())
             self.bytes_sent += 4 * t.numel()
             return
         if self.device is None:
@@ -103,7 +106,7 @@ class PairLink:
         gloo); no host sync."""
         if self.comm is not None:
             buf = torch.empty(n, dtype=torch.int32, device=self.comm.device)
-            self.comm.get(1 - self.comm.rank, buf)
+            self.comm.get(self.comm_peer, buf)
             self.bytes_recv += 4 * n
             return buf
         buf = torch.empty(n, dtype=torch.int32,
@@ -181,11 +184,17 @@ def split_ids(rows, flat) -> dict:
 # protocol roles
 # ---------------------------------------------------------------------------
 class PairTarget:
-    """Scheduler backend on the target rank (Backend protocol)."""
+    """Scheduler backend on the target rank (Backend protocol).
 
-    def __init__(self, engine, link: PairLink) -> None:
+    A tensor-parallel target (the paper's TP target + a dedicated
+    draft GPU) runs one PairTarget per TP rank, all driving the same SPMD
+    scheduler: the leader (TP rank 0) sends the commands, every rank receives
+    the drafted ids (and q rows) -- each verifies with them."""
+
+    def __init__(self, engine, link: PairLink, leader: bool = True) -> None:
         self.engine = engine
         self.link = link
+        self.leader = leader
         self.block_pool = getattr(engine, "block_pool", None)
         self.pending_commits: list = []
         self.stats = {"draft_ms": 0.0, "verify_ms": 0.0, "prefill_ms": 0.0, "steps": 0,
@@ -226,7 +235,8 @@ class PairTarget:
 
         serial = draft_rows(plan.serial_draft_ids)
         overlap = draft_rows(plan.overlap_draft_ids)
-        self.link.send(encode_step(admit, self.pending_commits, serial, overlap, table))
+        if self.leader:
+            self.link.send(encode_step(admit, self.pending_commits, serial, overlap, table))
         self.pending_commits = []
         eng.prefill(state, plan.prefill_ids)
         t1 = time.perf_counter()
@@ -280,18 +290,22 @@ class PairTarget:
         """End of a run: the draft rank answers with the time of its last
         draft phase (the one no id message reported)."""
         self.pending_commits = []
-        self.link.send(np.asarray([MAGIC, K_STOP], np.int32))
+        if self.leader:
+            self.link.send(np.asarray([MAGIC, K_STOP], np.int32))
         last = self.link.recv()
         self.stats["draft_ms"] += int(last[0]) / 1000.0 if last.size else 0.0
         self._prev_msg = None
 
 
 class DraftServer:
-    """Command loop on the draft rank."""
+    """Command loop on the draft rank.  ``link`` reaches the target rank that
+    sends the commands; ``followers`` (the other ranks of a tensor-parallel
+    target) receive the same drafted ids / q rows and the stop reply."""
 
-    def __init__(self, engine, link: PairLink) -> None:
+    def __init__(self, engine, link: PairLink, followers: tuple = ()) -> None:
         self.engine = engine
         self.link = link
+        self.followers = tuple(followers)
         self.steps = 0
 
     def serve(self) -> int:
@@ -304,7 +318,8 @@ class DraftServer:
                 prev_us = _elapsed_us(*pending)
                 pending = None
             if cmd["stop"]:
-                self.link.send(np.asarray([prev_us], np.int32))
+                for lk in (self.link,) + self.followers:
+                    lk.send(np.asarray([prev_us], np.int32))
                 return self.steps
             eng.set_tables(cmd["table"])
             eng.commit(cmd["commits"])  # before admissions: a freed slot may be reused
@@ -315,10 +330,11 @@ class DraftServer:
                     if pending is not None:
                         prev_us = _elapsed_us(*pending)
                     ids, pending = eng.draft(rows, prev_us)
-                    self.link.send_ids(ids)
                     q = eng.q_rows(rows) if getattr(eng, "q_vocab", 0) else None
-                    if q is not None and q.shape[0]:
-                        self.link.send_rows(q)
+                    for lk in (self.link,) + self.followers:
+                        lk.send_ids(ids)
+                        if q is not None and q.shape[0]:
+                            lk.send_rows(q)
             self.steps += 1
 
 

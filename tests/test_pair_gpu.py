@@ -114,3 +114,58 @@ def _worker_kw(rank, port, q, extra):
     global KW
     KW = {k: v for k, v in KW.items() if k not in extra}
     _worker(rank, port, q, extra)
+
+
+def _worker_tp(rank, port, q):
+    """ranks 0, 1: a tensor-parallel (TP = 2) target; rank 2: its dedicated
+    draft rank -- three processes sharing cuda:0 over gloo"""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE="3",
+                      RANK=str(rank), LOCAL_RANK=str(rank))
+    import torch.distributed as dist
+
+    from paper_2603_18016_b200 import SimConfig, make_requests, run
+    from paper_2603_18016_b200.gpu import GpuBackend
+    from paper_2603_18016_b200.pair import (DraftServer, GpuDraftEngine, GpuTargetEngine,
+                                            PairLink, PairTarget)
+    dist.init_process_group("gloo", init_method="env://")
+    tpg = dist.new_group([0, 1])
+    kw = dict(KW, beta_target=6.0)
+    cfg = SimConfig(mode="psd", m=8, k=4)
+    reqs = make_requests([24] * 16, prompt_len=16)
+    if rank < 2:
+        gb = GpuBackend("tiny-target-tp", "tiny-draft", roles=("target",), tp=(rank, 2, tpg), **kw)
+        be = PairTarget(GpuTargetEngine(gb), PairLink(2), leader=rank == 0)
+        st, rep = run(cfg, reqs, backend=be)
+        be.stop()
+        q.put((f"out{rank}", [r.output_ids for r in st.request_list()], rep.finished,
+               rep.total_accepted))
+    else:
+        gb = GpuBackend("tiny-target-tp", "tiny-draft", roles=("draft",), **kw)
+        q.put(("steps", DraftServer(GpuDraftEngine(gb), PairLink(0),
+                                    followers=(PairLink(1),)).serve()))
+    dist.destroy_process_group()
+
+
+def test_tp_target_with_dedicated_draft_rank(cuda_device):
+    """The paper's cfg4 deployment shape: a tensor-parallel target with the
+    draft on its own rank (here TP = 2 + 1 on one GPU).  Both TP ranks emit
+    the tokens of the single-process unsharded run (greedy, clear margins)."""
+    from paper_2603_18016_b200 import SimConfig, make_requests, run
+    from paper_2603_18016_b200.gpu import GpuBackend
+    st, rep = run(SimConfig(mode="psd", m=8, k=4), make_requests([24] * 16, prompt_len=16),
+                  backend=GpuBackend("tiny-target-tp", "tiny-draft", **dict(KW, beta_target=6.0)))
+    ref = [r.output_ids for r in st.request_list()]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_tp, args=(r, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    got = dict((m[0], m[1:]) for m in (q.get(timeout=600) for _ in procs))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for r in (0, 1):
+        outs, finished, accepted = got[f"out{r}"]
+        assert finished == 16 and outs == ref and accepted > 0
+    assert got["steps"][0] > 0
