@@ -194,7 +194,7 @@ def kernel_rooflines(backend, hbm_peak: float, bf16_peak: float) -> tuple[dict, 
     M = CFG["m"] * (CFG["k"] + 1)
     w = backend.target.layers[0]["wgu"]
     x = torch.randn(M, s.hidden, device=dev).to(torch.bfloat16)
-    out = torch.empty(M, s.ffn_padded, dtype=torch.bfloat16, device=dev)
+    out = torch.empty(M, w.shape[0] // 2, dtype=torch.bfloat16, device=dev)  # SiLU: N / 2 (a TP shard under --tp)
     ws = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
     # rotate over all layers' weights so every launch streams from HBM
     ws_list = [L["wgu"] for L in backend.target.layers]
@@ -759,6 +759,8 @@ def run_ours(args) -> None:
                                     world // 2 if pairs else world)
                    * CFG["n_requests"],
                    "seq_len": CFG["prompt"] + CFG["output"],
+                   "models": f"{CFG['target']} / {CFG['draft']}" + (" (--models smoke override)"
+                                                                    if args.models else ""),
                    "parallelism": (f"tp{tp_size}+draft x{world // group_size}" if tp_draft else
                                    f"tp{tp_size}x{world // tp_size}" if tp_layout else
                                    f"pairs{world // 2}" if pairs else f"replicas{world}"),
