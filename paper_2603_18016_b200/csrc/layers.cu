@@ -85,16 +85,46 @@ __device__ __forceinline__ void sum_partials8(const float* __restrict__ P, size_
   }
 }
 
+// all S <= 16 partials of one 8-wide chunk requested at once (one L2 round
+// trip), then summed in z order -- same arithmetic as sum_partials8
+__device__ __forceinline__ void sum_partials8_all(const float* __restrict__ P, size_t slice, int S,
+                                                  size_t off, float (&v)[8]) {
+  float4 c[16][2];
+#pragma unroll
+  for (int z = 0; z < 16; ++z)
+    if (z < S) {
+      const float4* q4 = reinterpret_cast<const float4*>(P + (size_t)z * slice + off);
+      c[z][0] = q4[0];
+      c[z][1] = q4[1];
+    }
+  v[0] = c[0][0].x; v[1] = c[0][0].y; v[2] = c[0][0].z; v[3] = c[0][0].w;
+  v[4] = c[0][1].x; v[5] = c[0][1].y; v[6] = c[0][1].z; v[7] = c[0][1].w;
+#pragma unroll
+  for (int z = 1; z < 16; ++z)
+    if (z < S) {
+      v[0] += c[z][0].x; v[1] += c[z][0].y; v[2] += c[z][0].z; v[3] += c[z][0].w;
+      v[4] += c[z][1].x; v[5] += c[z][1].y; v[6] += c[z][1].z; v[7] += c[z][1].w;
+    }
+}
+
 template <int NV>  // NV = 8-wide chunks per thread (H / 8 / NORM_THREADS rounded up)
 __global__ void __launch_bounds__(NORM_THREADS)
 add_rmsnorm_kernel(__nv_bfloat16* __restrict__ x, int ldx, const float* __restrict__ P, int S,
                    size_t slice, int ldp, const int32_t* __restrict__ rows,
                    const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ y, int ldy,
                    int H, float eps, int write_back) {
-  pdl_wait();
-  pdl_trigger();
+  // the norm weights and the row map do not depend on the predecessor:
+  // fetched before griddepcontrol.wait
   const int m = blockIdx.x;
   const int src = rows ? rows[m] : m;
+  uint4 wv[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int e = (threadIdx.x + k * NORM_THREADS) * 8;
+    if (e < H) wv[k] = *reinterpret_cast<const uint4*>(w + e);
+  }
+  pdl_wait();
+  pdl_trigger();
   __nv_bfloat16* xr = x + (size_t)src * ldx;
   const float* pr = P ? P + (size_t)src * ldp : nullptr;
   float v[NV][8];
@@ -109,7 +139,8 @@ add_rmsnorm_kernel(__nv_bfloat16* __restrict__ x, int ldx, const float* __restri
       for (int t = 0; t < 8; ++t) v[k][t] = __bfloat162float(b8[t]);
       if (pr) {
         float acc[8];
-        sum_partials8(pr, slice, S, e, acc);
+        if (NV == 1 && S <= 16) sum_partials8_all(pr, slice, S, e, acc);
+        else sum_partials8(pr, slice, S, e, acc);
         uint4 o;
         __nv_bfloat16* o8 = reinterpret_cast<__nv_bfloat16*>(&o);
 #pragma unroll
@@ -139,8 +170,7 @@ add_rmsnorm_kernel(__nv_bfloat16* __restrict__ x, int ldx, const float* __restri
   for (int k = 0; k < NV; ++k) {
     const int e = (threadIdx.x + k * NORM_THREADS) * 8;
     if (e < H) {
-      uint4 wu = *reinterpret_cast<const uint4*>(w + e);
-      const __nv_bfloat16* w8 = reinterpret_cast<const __nv_bfloat16*>(&wu);
+      const __nv_bfloat16* w8 = reinterpret_cast<const __nv_bfloat16*>(&wv[k]);
       uint4 o;
       __nv_bfloat16* o8 = reinterpret_cast<__nv_bfloat16*>(&o);
 #pragma unroll
