@@ -1168,7 +1168,6 @@ attn_dec_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __rest
   if constexpr (ROPE) {
     constexpr int half = D / 2;
     const int NQKV = (Hq + 2 * Hkv) * D;
-    const int nrot = nt * (G + 1) * half;
     // slot address of element i of new key row t (round 0 only)
     auto kv_slot = [&](int t, int i, bool v) -> __nv_bfloat16* {
       const int key = first_pos + t;
@@ -1176,45 +1175,50 @@ attn_dec_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __rest
       return reinterpret_cast<__nv_bfloat16*>(sKV + (size_t)j * 2 * TB + (v ? TB : 0) +
                                               swz<D>(r, i / 8) + (i % 8) * 2);
     };
-    for (int idx = tid; idx < nrot + nt * D; idx += ATT_THREADS) {
-      if (idx >= nrot) {
-        const int t = (idx - nrot) / D, i = (idx - nrot) % D;
-        const int m = qs + t;
-        const int sl = rs.slots[m];
-        if (sl < 0) continue;
-        const int col = (Hq + Hkv + hk) * D + i;
-        float a = sum_parts(rs, (size_t)m * NQKV + col);
-        if (rs.bias) a = a + __bfloat162float(rs.bias[col]);
-        vc_w(vc, ((size_t)sl * Hkv + hk) * D + i, a);
-        if (direct && first_pos + t <= last_key) *kv_slot(t, i, true) = __float2bfloat16(a);
-        continue;
-      }
-      const int t = idx / ((G + 1) * half), rem = idx % ((G + 1) * half);
-      const int hh = rem / half, i = rem % half;
+    // per token: (G + 1) rotation heads x half pairs, then the D values of
+    // the V row -- every index split is by a power of two (no runtime division)
+    const int nrot1 = (G + 1) * half;
+    for (int t = 0; t < nt; ++t) {
       const int m = qs + t;
-      if (hh == G && rs.slots[m] < 0) continue;
-      const int head = hh < G ? hk * G + hh : Hq + hk;
-      const int col = head * D + i;
-      float a = sum_parts(rs, (size_t)m * NQKV + col);
-      float b = sum_parts(rs, (size_t)m * NQKV + col + half);
-      if (rs.bias) {
-        a = __bfloat162float(__float2bfloat16(a + __bfloat162float(rs.bias[col])));
-        b = __bfloat162float(__float2bfloat16(b + __bfloat162float(rs.bias[col + half])));
-      }
-      float sn, cs;
-      sincosf((float)rs.positions[m] * rs.inv_freq[i], &sn, &cs);
-      const __nv_bfloat16 ra = __float2bfloat16(a * cs - b * sn);
-      const __nv_bfloat16 rb = __float2bfloat16(b * cs + a * sn);
-      if (hh < G) {
-        sQ[t * G + hh][i] = ra;
-        sQ[t * G + hh][i + half] = rb;
-      } else {
-        __nv_bfloat16* dst = const_cast<__nv_bfloat16*>(kc) + ((size_t)rs.slots[m] * Hkv + hk) * D;
-        dst[i] = ra;
-        dst[i + half] = rb;
-        if (direct && first_pos + t <= last_key) {
-          *kv_slot(t, i, false) = ra;
-          *kv_slot(t, i + half, false) = rb;
+      const int sl = rs.slots[m];
+      const float pos = (float)rs.positions[m];
+      const bool to_smem = direct && first_pos + t <= last_key;
+      for (int j = tid; j < nrot1 + D; j += ATT_THREADS) {
+        if (j >= nrot1) {
+          const int i = j - nrot1;
+          if (sl < 0) continue;
+          const int col = (Hq + Hkv + hk) * D + i;
+          float a = sum_parts(rs, (size_t)m * NQKV + col);
+          if (rs.bias) a = a + __bfloat162float(rs.bias[col]);
+          vc_w(vc, ((size_t)sl * Hkv + hk) * D + i, a);
+          if (to_smem) *kv_slot(t, i, true) = __float2bfloat16(a);
+          continue;
+        }
+        const int hh = j / half, i = j % half;
+        if (hh == G && sl < 0) continue;
+        const int head = hh < G ? hk * G + hh : Hq + hk;
+        const int col = head * D + i;
+        float a = sum_parts(rs, (size_t)m * NQKV + col);
+        float b = sum_parts(rs, (size_t)m * NQKV + col + half);
+        if (rs.bias) {
+          a = __bfloat162float(__float2bfloat16(a + __bfloat162float(rs.bias[col])));
+          b = __bfloat162float(__float2bfloat16(b + __bfloat162float(rs.bias[col + half])));
+        }
+        float sn, cs;
+        sincosf(pos * rs.inv_freq[i], &sn, &cs);
+        const __nv_bfloat16 ra = __float2bfloat16(a * cs - b * sn);
+        const __nv_bfloat16 rb = __float2bfloat16(b * cs + a * sn);
+        if (hh < G) {
+          sQ[t * G + hh][i] = ra;
+          sQ[t * G + hh][i + half] = rb;
+        } else {
+          __nv_bfloat16* dst = const_cast<__nv_bfloat16*>(kc) + ((size_t)sl * Hkv + hk) * D;
+          dst[i] = ra;
+          dst[i + half] = rb;
+          if (to_smem) {
+            *kv_slot(t, i, false) = ra;
+            *kv_slot(t, i + half, false) = rb;
+          }
         }
       }
     }
@@ -1401,19 +1405,15 @@ attn_dec_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __rest
     }
   }
   const float inv0 = l0 > 0.f ? 1.f / l0 : 0.f, inv1 = l1 > 0.f ? 1.f / l1 : 0.f;
+  __nv_bfloat16* o0 = out + ((size_t)(qs + r0 / G) * Hq + hk * G + r0 % G) * D;
+  __nv_bfloat16* o1 = out + ((size_t)(qs + r1 / G) * Hq + hk * G + r1 % G) * D;
 #pragma unroll
   for (int n = 0; n < D / 8; ++n) {
     const int d = n * 8 + 2 * c;
-    if (r0 < R) {
-      const int t = r0 / G, gg = r0 % G;
-      *reinterpret_cast<__nv_bfloat162*>(out + ((size_t)(qs + t) * Hq + hk * G + gg) * D + d) =
-          __floats2bfloat162_rn(o[n][0] * inv0, o[n][1] * inv0);
-    }
-    if (r1 < R) {
-      const int t = r1 / G, gg = r1 % G;
-      *reinterpret_cast<__nv_bfloat162*>(out + ((size_t)(qs + t) * Hq + hk * G + gg) * D + d) =
-          __floats2bfloat162_rn(o[n][2] * inv1, o[n][3] * inv1);
-    }
+    if (r0 < R)
+      *reinterpret_cast<__nv_bfloat162*>(o0 + d) = __floats2bfloat162_rn(o[n][0] * inv0, o[n][1] * inv0);
+    if (r1 < R)
+      *reinterpret_cast<__nv_bfloat162*>(o1 + d) = __floats2bfloat162_rn(o[n][2] * inv1, o[n][3] * inv1);
   }
 }
 
