@@ -397,6 +397,10 @@ def main():
             gemm_case(f"{tag} sk f32", M, N, K, "f32", splits=0)
     if want("gemmgu"):
         gemm_case("8B gate/up", 192, 28672, 4096, "silu")
+    if want("gemmguM"):
+        # gate/up vs M: B (token) traffic through L2 grows with M, weights do not
+        for mm in (32, 64, 96, 128, 160, 192, 256):
+            gemm_case(f"8B gate/up M{mm}", mm, 28672, 4096, "silu")
     if want("attnrope"):
         attn_rope_case("1B draft", 32, 1, 300, 32, 8, 64, 6)
         attn_rope_case("1B draft step0", 32, 2, 300, 32, 8, 64, 6)
