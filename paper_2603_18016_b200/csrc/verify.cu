@@ -264,6 +264,20 @@ __device__ void fold_decide(const Params& p, int b, bool publish, Plan* s_plan) 
   const int nst = (p.V + PSD_SLICE - 1) / PSD_SLICE;
   const int nsd = (p.Vd + PSD_SLICE - 1) / PSD_SLICE;
   const int nrows = SAMPLE && !p.d_stats ? 2 * kb + 1 : kb + 1;
+  // the drafted tokens' raw logits: requested now so their (random, HBM)
+  // loads overlap the partial staging and the fold below
+  int x_tok = -1;
+  float x_t = 0.0f, x_d = 0.0f;
+  if (warp == 0 && lane < kb) {
+    x_tok = p.ids[b * p.K + lane];
+    if constexpr (SAMPLE) {
+      if (x_tok >= 0 && x_tok < p.V) {
+        x_t = __ldg(p.t + b * p.tsb + lane * p.tsi + x_tok);
+        if (x_tok < p.Vd)
+          x_d = __ldg(p.d + (int64_t)(p.d_rows ? p.d_rows[b] : b) * p.dsb + lane * p.dsi + x_tok);
+      }
+    }
+  }
   // stage every partial of request b in shared memory (parallel loads)
   for (int q = tid; q < nrows * p.NS; q += kThreads) {
     const int rowi = q / p.NS, sl = q % p.NS;
@@ -297,15 +311,12 @@ __device__ void fold_decide(const Params& p, int b, bool publish, Plan* s_plan) 
   __syncthreads();
   if (warp == 0) {
     bool ok = false;
-    const int x = lane < kb ? p.ids[b * p.K + lane] : -1;
+    const int x = x_tok;
     if (lane < kb) {
       if constexpr (SAMPLE) {
         if (x >= 0 && x < p.V) {
-          const float* tr = p.t + b * p.tsb + lane * p.tsi;
-          const float* drw = p.d + (int64_t)(p.d_rows ? p.d_rows[b] : b) * p.dsb + lane * p.dsi;
-          const float et = psd_weight(__ldg(tr + x), p.c, psd_bias(sMt[lane], p.c));
-          const float ed =
-              x < p.Vd ? psd_weight(__ldg(drw + x), p.c, psd_bias(sMd[lane], p.c)) : 0.0f;
+          const float et = psd_weight(x_t, p.c, psd_bias(sMt[lane], p.c));
+          const float ed = x < p.Vd ? psd_weight(x_d, p.c, psd_bias(sMd[lane], p.c)) : 0.0f;
           ok = psd_accept(p.u[b * (p.K + 1) + lane], et, ed, sSt[lane], sSd[lane]);
         }
       } else {
@@ -613,8 +624,16 @@ __device__ __forceinline__ void sample_item(const Params& p, int chunk, int b, i
   for (int k = tid; k < p.NB; k += kThreads) wb[k] = __ldcg(p.wblk + b * p.NB + k);
   __syncthreads();
 
-  // degenerate residual (sums to 0 in fp32): fall back to sampling from p
-  if (tid == 0) s_int = (w.residual && !(seq_fold(wb, p.NB, nullptr) > 0.0f)) ? 1 : 0;
+  // canonical block prefix P_b (sequential fold, kept in smem), T = u * R;
+  // chosen block = first with P_b > T (found in parallel).  A degenerate
+  // residual (sums to 0 in fp32) falls back to sampling from p: the block sums
+  // of p, then the same fold
+  if (tid == 0) {
+    const float R = seq_fold(wb, p.NB, s_pref);
+    s_int = (w.residual && !(R > 0.0f)) ? 1 : 0;
+    s_T = psd_mul(p.u[b * (p.K + 1) + p.K], R);
+    s_chosen = 0x7fffffff;
+  }
   __syncthreads();
   if (s_int) {
     w.residual = 0;
@@ -624,15 +643,12 @@ __device__ __forceinline__ void sample_item(const Params& p, int chunk, int b, i
       if (tid < n) wb[k0 + tid] = s_blk[tid];
     }
     __syncthreads();
+    if (tid == 0) {
+      const float R = seq_fold(wb, p.NB, s_pref);
+      s_T = psd_mul(p.u[b * (p.K + 1) + p.K], R);
+    }
+    __syncthreads();
   }
-  // canonical block prefix P_b (sequential fold, kept in smem), T = u * R;
-  // chosen block = first with P_b > T (found in parallel)
-  if (tid == 0) {
-    const float R = seq_fold(wb, p.NB, s_pref);
-    s_T = psd_mul(p.u[b * (p.K + 1) + p.K], R);
-    s_chosen = 0x7fffffff;
-  }
-  __syncthreads();
   for (int k = tid; k < p.NB; k += kThreads)
     if (s_pref[k + 1] > s_T) atomicMin(&s_chosen, k);
   __syncthreads();
