@@ -856,10 +856,20 @@ attention_tma_kernel(const __grid_constant__ CUtensorMap tmK,
       }
     }
   };
+  // prefetch groups whose blocks hold only keys of earlier steps before
+  // griddepcontrol.wait: the predecessor (the RoPE / KV-write kernel) writes
+  // only this step's keys, so these loads overlap its tail
+  int npre = 0;
+  if (tid == 0) {
+    while (npre < NS - 1 && npre < ngroups && (npre + 1) * KG * KT <= first_pos) {
+      issue(npre, npre);
+      ++npre;
+    }
+  }
   pdl_wait();
   pdl_trigger();
   if (tid == 0) {
-    for (int t = 0; t < NS - 1 && t < ngroups; ++t) issue(t, t);
+    for (int t = npre; t < NS - 1 && t < ngroups; ++t) issue(t, t);
   }
   for (int idx = tid; idx < RG * 16 * (D / 8); idx += ATT_THREADS) {
     const int r = idx / (D / 8), cc = idx % (D / 8);

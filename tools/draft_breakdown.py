@@ -1,6 +1,8 @@
-"""Marginal in-graph cost of each kernel family in one draft decode step.
+"""Marginal in-graph cost of each kernel family in one draft decode step
+(or, with qlen > 2, one verify pass: qlen query tokens per sequence, fp32
+logits for every row as the target's verification needs them).
 
-    python tools/draft_breakdown.py [preset] [nseq] [ctx]
+    python tools/draft_breakdown.py [preset] [nseq] [ctx] [qlen]
 
 Builds the 1B draft (random init), prefills nseq sequences of ctx tokens,
 captures one decode step (1 token per sequence, K6 greedy LM head) in a CUDA
@@ -22,6 +24,7 @@ from paper_2603_18016_b200.model import PRESETS, Forward, Transformer  # noqa: E
 preset = sys.argv[1] if len(sys.argv) > 1 else "llama-3.2-1b"
 nseq = int(sys.argv[2]) if len(sys.argv) > 2 else 32
 ctx = int(sys.argv[3]) if len(sys.argv) > 3 else 300
+qlen = int(sys.argv[4]) if len(sys.argv) > 4 else 1
 shape = PRESETS[preset]
 dev = torch.device("cuda:0")
 bs = 16
@@ -29,7 +32,8 @@ mb = (ctx + 16) // bs + 2
 m = Transformer(shape, dev, seed=1, num_blocks=nseq * mb + 1, block_size=bs,
                 max_blocks_per_seq=mb)
 bt = torch.arange(1, 1 + nseq * mb, dtype=torch.int32, device=dev).view(nseq, mb)
-fwd = Forward(m, max(nseq * 64, 256), nseq, nseq, bt, sets=1)
+fwd = Forward(m, max(nseq * 64, 256), nseq, nseq * max(1, int(sys.argv[4]) if len(sys.argv) > 4
+                                                         else 1), bt, sets=1)
 rng = np.random.default_rng(0)
 lib = native.load()
 
@@ -54,14 +58,18 @@ for c0 in range(0, nseq, 4):
     fwd.run(len(seqs) * ctx, len(seqs), ctx, 0, None, shape.vocab)
 torch.cuda.synchronize()
 # the decode step's metadata
+M = nseq * qlen
 fwd.begin()
-fwd.stage(0, {"tokens": rng.integers(0, shape.vocab, nseq).astype(np.int32),
-              "positions": np.full(nseq, ctx, np.int32),
-              "slots": np.asarray([slot(s_, ctx) for s_ in range(nseq)], np.int32),
+fwd.stage(0, {"tokens": rng.integers(0, shape.vocab, M).astype(np.int32),
+              "positions": np.tile(ctx + np.arange(qlen), nseq).astype(np.int32),
+              "slots": np.asarray([slot(s_, ctx + t) for s_ in range(nseq) for t in range(qlen)],
+                                  np.int32),
               "seq_slot": np.arange(nseq, dtype=np.int32),
-              "q_start": np.arange(nseq, dtype=np.int32), "q_len": np.ones(nseq, np.int32),
-              "q_pos0": np.full(nseq, ctx, np.int32), "kv_len": np.full(nseq, ctx + 1, np.int32),
-              "logit_rows": np.arange(nseq, dtype=np.int32),
+              "q_start": (np.arange(nseq) * qlen).astype(np.int32),
+              "q_len": np.full(nseq, qlen, np.int32),
+              "q_pos0": np.full(nseq, ctx, np.int32),
+              "kv_len": np.full(nseq, ctx + qlen, np.int32),
+              "logit_rows": np.arange(min(M, nseq * qlen), dtype=np.int32),
               "scatter_dst": np.arange(nseq, dtype=np.int32)})
 fwd.upload(1)
 succ = torch.as_tensor(rng.integers(0, shape.vocab, shape.vocab), dtype=torch.int32, device=dev)
@@ -69,9 +77,15 @@ out = torch.empty(nseq, dtype=torch.int32, device=dev)
 dst = torch.empty(nseq, dtype=torch.int32, device=dev)
 
 
+logits = torch.empty(M, shape.vocab, device=dev) if qlen > 2 else None
+
+
 def step():
-    fwd.run(nseq, nseq, 1, nseq, None, shape.vocab, bigram=(succ, 16.0),
-            argmax_into=(out, dst, fwd.view("scatter_dst", 0)))
+    if qlen > 2:  # verify pass: fp32 logits of every row
+        fwd.run(M, nseq, qlen, M, logits, shape.vocab)
+    else:
+        fwd.run(M, nseq, qlen, nseq, None, shape.vocab, bigram=(succ, 16.0),
+                argmax_into=(out, dst, fwd.view("scatter_dst", 0)))
 
 
 def timed(reps=20):
@@ -98,12 +112,14 @@ def timed(reps=20):
 
 
 base = timed()
-print(f"{preset} nseq={nseq} ctx={ctx}: decode step {base:8.1f} us")
+print(f"{preset} nseq={nseq} ctx={ctx} qlen={qlen}: step {base:8.1f} us")
 families = {
     "attention+rope": ["psd_attention_rope"],
+    "rope_kv": ["psd_rope_kv_partials"],
+    "attention": ["psd_attention"],
     "add_rmsnorm": ["psd_add_rmsnorm"],
     "split-K GEMMs (qkv, o, down)": ["psd_gemm_partials"],
-    "stream-K GEMM (gate/up)": ["psd_gemm_bf16"],
+    "stream-K GEMMs (gate/up; LM head when qlen > 2)": ["psd_gemm_bf16"],
     "LM head + argmax (K6)": ["psd_gemm_argmax", "psd_argmax_fold"],
     "embed": ["psd_embed"],
 }
