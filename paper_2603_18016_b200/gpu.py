@@ -210,6 +210,7 @@ class GpuBackend:
             grid = mk_grid or int(os.environ.get("PSD_MK_GRID", "0"))
             with torch.cuda.device(dev):
                 self.mk = self._make_mk(grid)
+        self._step_events = None
         # K6: the greedy draft's argmax (+ bias) in its LM-head epilogue
         # (PSD_K6=0: logits + bigram + K1(k = 0) + scatter, for A/B runs)
         self.k6 = (os.environ.get("PSD_K6", "1") == "1" and has_d
@@ -567,40 +568,45 @@ class GpuBackend:
         real = np.arange(nb) < n
         fwd = self.dfwd
         fwd.begin()
-        for i in range(kmax):
-            if i == 0:
-                pos = np.stack([L - 2, L - 1], axis=1).reshape(-1)
-                srow = np.repeat(sl, 2)
-                kvs = np.where(np.repeat(real, 2), self._slots_at(srow, np.maximum(pos, 0)), -1)
-                arrays = {
-                    "gather_src": (srow * ldt + np.tile([0, 1], nb)).astype(np.int32),
-                    "positions": np.where(np.repeat(real, 2), pos, 0).astype(np.int32),
-                    "slots": kvs.astype(np.int32),
-                    "seq_slot": sl,
-                    "q_start": np.arange(0, 2 * nb, 2, dtype=np.int32),
-                    "q_len": np.full(nb, 2, np.int32),
-                    "q_pos0": np.where(real, L - 2, 0).astype(np.int32),
-                    "kv_len": np.where(real, L, 1).astype(np.int32),
-                    "logit_rows": np.arange(1, 2 * nb, 2, dtype=np.int32),
-                    "scatter_dst": np.where(real, sl * ldt + 2, -1).astype(np.int32),
-                }
-            else:
-                act = real & (i < k)
-                pos = L - 1 + i
-                arrays = {
-                    "gather_src": (sl * ldt + 2 + i - 1).astype(np.int32),
-                    "positions": np.where(act, pos, 0).astype(np.int32),
-                    "slots": np.where(act, self._slots_at(sl, np.where(act, pos, 0)),
-                                      -1).astype(np.int32),
-                    "seq_slot": sl,
-                    "q_start": np.arange(nb, dtype=np.int32),
-                    "q_len": np.ones(nb, np.int32),
-                    "q_pos0": np.where(act, pos, 0).astype(np.int32),
-                    "kv_len": np.where(act, L + i, 1).astype(np.int32),
-                    "logit_rows": np.arange(nb, dtype=np.int32),
-                    "scatter_dst": np.where(act, sl * ldt + 2 + i, -1).astype(np.int32),
-                }
-            fwd.stage(i, arrays)
+        # step 0: the last two committed tokens of every row (the one before
+        # the bonus token may lack draft KV)
+        pos = np.stack([L - 2, L - 1], axis=1).reshape(-1)
+        srow = np.repeat(sl, 2)
+        real2 = np.repeat(real, 2)
+        kvs = np.where(real2, self._slots_at(srow, np.maximum(pos, 0)), -1)
+        fwd.stage(0, {
+            "gather_src": (srow * ldt + np.tile([0, 1], nb)).astype(np.int32),
+            "positions": np.where(real2, pos, 0).astype(np.int32),
+            "slots": kvs.astype(np.int32),
+            "seq_slot": sl,
+            "q_start": np.arange(0, 2 * nb, 2, dtype=np.int32),
+            "q_len": np.full(nb, 2, np.int32),
+            "q_pos0": np.where(real, L - 2, 0).astype(np.int32),
+            "kv_len": np.where(real, L, 1).astype(np.int32),
+            "logit_rows": np.arange(1, 2 * nb, 2, dtype=np.int32),
+            "scatter_dst": np.where(real, sl * ldt + 2, -1).astype(np.int32),
+        })
+        if kmax > 1:
+            # steps 1 .. kmax-1 at once ([kmax - 1, nb]): step i feeds the
+            # previous draft at position L - 1 + i
+            i = np.arange(1, kmax)[:, None]
+            act = real[None, :] & (i < k[None, :])
+            pos = (L - 1)[None, :] + i
+            sl2 = np.broadcast_to(sl, act.shape)
+            ar = np.broadcast_to(np.arange(nb, dtype=np.int32), act.shape)
+            fwd.stage_many(1, {
+                "gather_src": (sl[None, :] * ldt + 1 + i).astype(np.int32),
+                "positions": np.where(act, pos, 0).astype(np.int32),
+                "slots": np.where(act, self._slots_at(sl2, np.where(act, pos, 0)),
+                                  -1).astype(np.int32),
+                "seq_slot": sl2,
+                "q_start": ar,
+                "q_len": np.ones(act.shape, np.int32),
+                "q_pos0": np.where(act, pos, 0).astype(np.int32),
+                "kv_len": np.where(act, L[None, :] + i, 1).astype(np.int32),
+                "logit_rows": ar,
+                "scatter_dst": np.where(act, sl[None, :] * ldt + 2 + i, -1).astype(np.int32),
+            })
         fwd.upload(kmax)
         if self.mode == "sample":
             self.d_key_cur = (self.d_key_cur + 1) % self.d_key_ring
@@ -856,8 +862,10 @@ class GpuBackend:
     def execute(self, state: EngineState, plan: StepPlan, rows: list[VerifyRow]) -> StepResult:
         dev = self.device
         ts, ds = self.s_target, self.s_draft
-        ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-        e_start, e_pf_t, e_pf_d, e_sd, e_ov, e_v0, e_v1 = (ev() for _ in range(7))
+        # the step's timing events, created once (every step ends synchronised)
+        if self._step_events is None:
+            self._step_events = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+        e_start, e_pf_t, e_pf_d, e_sd, e_ov, e_v0, e_v1 = self._step_events
         t_host = time.perf_counter()
         cur = torch.cuda.current_stream(dev)
         cur.synchronize()

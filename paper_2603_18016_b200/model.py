@@ -461,6 +461,16 @@ class Forward:
                 raise ConfigError(f"forward metadata {name}: {len(arr)} > capacity {n}")
             host[o:o + len(arr)] = arr
 
+    def stage_many(self, first_set: int, arrays: dict[str, np.ndarray]) -> None:
+        """Write metadata of sets first_set .. first_set + n - 1 at once:
+        each array is [n, len] (one row per set)."""
+        host = self._host_np[self._cur]
+        for name, arr in arrays.items():
+            o, n = self._offsets[name]
+            if arr.shape[1] > n:
+                raise ConfigError(f"forward metadata {name}: {arr.shape[1]} > capacity {n}")
+            host[first_set:first_set + arr.shape[0], o:o + arr.shape[1]] = arr
+
     def upload(self, n_sets: int = 1) -> None:
         """Copy staged sets 0..n_sets-1 to the device on the current stream."""
         self.meta[:n_sets].copy_(self.meta_host[self._cur, :n_sets], non_blocking=True)
