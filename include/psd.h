@@ -308,6 +308,33 @@ int psd_commit(const int32_t* accepted_len, const int32_t* out_tokens, int K,
 /* dst[dst_idx ? dst_idx[i] : i] = src[src_idx ? src_idx[i] : i], negative dst skipped */
 int psd_index_copy_i32(int32_t* dst, const int32_t* dst_idx, const int32_t* src,
                        const int32_t* src_idx, int n, void* stream);
+/* ---- host-side staging of the draft / verify pass metadata ---------------
+ * (no reference counterpart: the reference's passes are virtual durations,
+ * SURVEY §8a a16, request_model.py:92-117 called at engine.py:338, 359-360,
+ * 378, 402, 429).  Pure host code: fills the pinned metadata set(s) of a
+ * forward (field order tokens, positions, slots, seq_slot, q_start, q_len,
+ * q_pos0, kv_len, logit_rows, gather_src, scatter_dst; `fields` = 11
+ * offset / capacity pairs in int32 units) for n real rows padded to nb with
+ * the scratch slot.  KV write slots come from the block table
+ * (block_table[slot * bt_ld + pos / block_size] * block_size + pos % block_size);
+ * a position past nblk[slot] blocks is PSD_STAGE_KV_OVERRUN unless `replay`
+ * (then that row writes nowhere, -1).
+ * psd_stage_draft: kmax decode sets (set_stride int32 apart); set 0 feeds the
+ *   last two committed tokens (positions L-2, L-1), set i >= 1 the draft at
+ *   L-1+i for rows with i < k[r]; scatter targets slot * ldt + 2 + i.
+ * psd_stage_verify: one set of nb * (kmax + 1) query tokens (row r token j
+ *   at position L-1+j; KV written for j <= k[r]). */
+#define PSD_STAGE_BAD_ARGS 1001
+#define PSD_STAGE_CAPACITY 1002
+#define PSD_STAGE_KV_OVERRUN 1003
+int psd_stage_draft(int32_t* sets, int64_t set_stride, const int32_t* fields,
+                    const int32_t* block_table, int bt_ld, const int32_t* nblk, int block_size,
+                    int replay, int ldt, int scratch_slot, const int32_t* slot, const int32_t* L,
+                    const int32_t* k, int n, int nb, int kmax);
+int psd_stage_verify(int32_t* set, const int32_t* fields, const int32_t* block_table, int bt_ld,
+                     const int32_t* nblk, int block_size, int replay, int ldt, int scratch_slot,
+                     const int32_t* slot, const int32_t* L, const int32_t* k, int n, int nb,
+                     int kmax);
 /* kernels enqueued by this library so far (host-side counter; a captured
  * CUDA graph's launches are counted once, at capture) */
 long long psd_launch_count(void);

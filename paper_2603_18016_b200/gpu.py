@@ -124,8 +124,11 @@ class GpuBackend:
             self.block_table = torch.zeros(nslot, self.max_blocks, dtype=i32, device=dev)
             self.block_table_host = torch.zeros(nslot, self.max_blocks, dtype=i32).pin_memory()
             self.bt_np = self.block_table_host.numpy()
-            self.nblk = np.zeros(nslot, np.int64)
+            self.bt_ptr = self.block_table_host.data_ptr()
+            self.nblk = np.zeros(nslot, np.int32)
             self.nblk[self.scratch_slot] = 1
+            # per-pass row arrays (slot, committed length, k) for the stagers
+            self._rows_np = np.zeros((3, max_batch), np.int32)
             self.ldt = k_max + 2
             self.slot_tok = torch.zeros(nslot, self.ldt, dtype=i32, device=dev)
             self.generated = torch.zeros(max_requests, dtype=i32, device=dev)
@@ -211,6 +214,7 @@ class GpuBackend:
             with torch.cuda.device(dev):
                 self.mk = self._make_mk(grid)
         self._step_events = None
+        self._bt_sig = {}  # slot -> (request, block-list version) on the host table
         # K6: the greedy draft's argmax (+ bias) in its LM-head epilogue
         # (PSD_K6=0: logits + bigram + K1(k = 0) + scatter, for A/B runs)
         self.k6 = (os.environ.get("PSD_K6", "1") == "1" and has_d
@@ -354,6 +358,7 @@ class GpuBackend:
         n = req.generated
         req.output_ids = self.outputs[s, :n].cpu().tolist()
         self.d2h_bytes += 4 * n
+        self._bt_sig.pop(s, None)
         self.free_slots.append(s)
         self.pending_k.pop(rid, None)
 
@@ -368,15 +373,24 @@ class GpuBackend:
         return blocks[bi] * self.block_size + pos % self.block_size
 
     def _upload_block_table(self, state) -> None:
+        """Host block table -> device.  Rows are rewritten only for slots whose
+        (request, block-list version) changed; rows of free slots are never
+        read (no batch references them)."""
         bt = self.bt_np
-        bt[:] = 0
-        self.nblk[:self.max_requests] = 0
+        sig = self._bt_sig
+        kv = state.kv
         for rid, s in self.slots.items():
-            blocks = state.kv.blocks_of(rid)
-            if len(blocks) > self.max_blocks:
-                raise KVError(f"request {rid}: {len(blocks)} blocks > max {self.max_blocks}")
-            bt[s, :len(blocks)] = blocks
-            self.nblk[s] = len(blocks)
+            key = (rid, kv.list_version(rid))
+            if sig.get(s) == key:
+                continue
+            blocks = kv.blocks_of(rid)
+            n = len(blocks)
+            if n > self.max_blocks:
+                raise KVError(f"request {rid}: {n} blocks > max {self.max_blocks}")
+            bt[s, :n] = blocks
+            bt[s, n:] = 0
+            self.nblk[s] = n
+            sig[s] = key
         self.block_table.copy_(self.block_table_host, non_blocking=True)
         self.h2d_bytes += self.block_table_host.numel() * 4
 
@@ -549,64 +563,41 @@ class GpuBackend:
                            state.requests[rid].prompt_len + state.requests[rid].generated,
                            quotas[rid]) for rid in ids if quotas[rid] > 0])
 
+    def _stage_rows(self, n: int, nb: int, L_pad: int):
+        """(slot, L, k) row arrays padded to nb (scratch slot, L_pad, 0)."""
+        a = self._rows_np
+        sl, L, k = a[0, :nb], a[1, :nb], a[2, :nb]
+        sl[n:] = self.scratch_slot
+        L[n:] = L_pad
+        k[n:] = 0
+        return sl, L, k
+
+    def _stage_check(self, rc: int, what: str) -> None:
+        if rc == 0:
+            return
+        if rc == native.STAGE_KV_OVERRUN:
+            raise KVError(f"{what}: KV position beyond the request's allocated blocks")
+        raise ConfigError(f"{what}: metadata staging failed ({rc})")
+
     def _draft_rows(self, draft_rows) -> None:
         """k-step draft decode of (rid, slot, committed length L, k) rows; the
-        drafts land in slot_tok[slot, 2..2+k)."""
+        drafts land in slot_tok[slot, 2..2+k).  The forward metadata of all
+        k steps is staged natively (psd_stage_draft)."""
         if not draft_rows:
             return
-        rows = [r[0] for r in draft_rows]
-        n = len(rows)
+        n = len(draft_rows)
         nb = self._bucket(n)
-        sl = np.full(nb, self.scratch_slot, np.int32)
-        L = np.full(nb, 2, np.int64)
-        k = np.zeros(nb, np.int64)
+        sl, L, k = self._stage_rows(n, nb, 2)
         sl[:n] = [r[1] for r in draft_rows]
         L[:n] = [r[2] for r in draft_rows]
         k[:n] = [r[3] for r in draft_rows]
-        kmax = int(k.max())
-        ldt = self.ldt
-        real = np.arange(nb) < n
+        kmax = int(k[:n].max())
         fwd = self.dfwd
         fwd.begin()
-        # step 0: the last two committed tokens of every row (the one before
-        # the bonus token may lack draft KV)
-        pos = np.stack([L - 2, L - 1], axis=1).reshape(-1)
-        srow = np.repeat(sl, 2)
-        real2 = np.repeat(real, 2)
-        kvs = np.where(real2, self._slots_at(srow, np.maximum(pos, 0)), -1)
-        fwd.stage(0, {
-            "gather_src": (srow * ldt + np.tile([0, 1], nb)).astype(np.int32),
-            "positions": np.where(real2, pos, 0).astype(np.int32),
-            "slots": kvs.astype(np.int32),
-            "seq_slot": sl,
-            "q_start": np.arange(0, 2 * nb, 2, dtype=np.int32),
-            "q_len": np.full(nb, 2, np.int32),
-            "q_pos0": np.where(real, L - 2, 0).astype(np.int32),
-            "kv_len": np.where(real, L, 1).astype(np.int32),
-            "logit_rows": np.arange(1, 2 * nb, 2, dtype=np.int32),
-            "scatter_dst": np.where(real, sl * ldt + 2, -1).astype(np.int32),
-        })
-        if kmax > 1:
-            # steps 1 .. kmax-1 at once ([kmax - 1, nb]): step i feeds the
-            # previous draft at position L - 1 + i
-            i = np.arange(1, kmax)[:, None]
-            act = real[None, :] & (i < k[None, :])
-            pos = (L - 1)[None, :] + i
-            sl2 = np.broadcast_to(sl, act.shape)
-            ar = np.broadcast_to(np.arange(nb, dtype=np.int32), act.shape)
-            fwd.stage_many(1, {
-                "gather_src": (sl[None, :] * ldt + 1 + i).astype(np.int32),
-                "positions": np.where(act, pos, 0).astype(np.int32),
-                "slots": np.where(act, self._slots_at(sl2, np.where(act, pos, 0)),
-                                  -1).astype(np.int32),
-                "seq_slot": sl2,
-                "q_start": ar,
-                "q_len": np.ones(act.shape, np.int32),
-                "q_pos0": np.where(act, pos, 0).astype(np.int32),
-                "kv_len": np.where(act, L[None, :] + i, 1).astype(np.int32),
-                "logit_rows": ar,
-                "scatter_dst": np.where(act, sl[None, :] * ldt + 2 + i, -1).astype(np.int32),
-            })
+        self._stage_check(native.load().psd_stage_draft(
+            fwd.host_set_ptr(0), fwd.set_size, fwd.fields_ptr, self.bt_ptr, self.max_blocks,
+            self.nblk.ctypes.data, self.block_size, int(self.replay), self.ldt, self.scratch_slot,
+            sl.ctypes.data, L.ctypes.data, k.ctypes.data, n, nb, kmax), "draft staging")
         fwd.upload(kmax)
         if self.mode == "sample":
             self.d_key_cur = (self.d_key_cur + 1) % self.d_key_ring
@@ -615,7 +606,8 @@ class GpuBackend:
                 ev.synchronize()
             kh = self.d_key_host[self.d_key_cur].numpy()
             B = self.max_batch
-            kh[:nb] = [r for r in rows] + [0] * (nb - n)
+            real = np.arange(nb) < n
+            kh[:nb] = [r[0] for r in draft_rows] + [0] * (nb - n)
             kh[B:B + nb] = L
             # q storage row of (row r, step i): slot * k_max + i (scratch slot for padding)
             K = self.k_max
@@ -696,9 +688,7 @@ class GpuBackend:
         kmax = self.k_max
         K1 = kmax + 1
         ldt = self.ldt
-        sl = np.full(nb, self.scratch_slot, np.int64)
-        L = np.full(nb, 1, np.int64)
-        k = np.zeros(nb, np.int64)
+        sl, L, k = self._stage_rows(n, nb, 1)
         for r, row in enumerate(rows):
             rid = row.request_id
             if row.k != self.pending_k.get(rid, 0):
@@ -709,23 +699,12 @@ class GpuBackend:
             L[r] = req.prompt_len + req.generated
             k[r] = row.k
         real = np.arange(nb) < n
-        j = np.arange(K1)[None, :]
-        src = np.where((j == 0) | (j > k[:, None]), 1, 1 + j)
-        pos = (L - 1)[:, None] + j
-        wr = real[:, None] & (j <= k[:, None])
-        slots = np.where(wr, self._slots_at(np.repeat(sl, K1).reshape(nb, K1),
-                                            np.where(wr, pos, 0)), -1)
         fwd = self.tfwd
         fwd.begin()
-        fwd.stage(0, {"gather_src": (sl[:, None] * ldt + src).reshape(-1).astype(np.int32),
-                      "positions": np.where(real[:, None], pos, 0).reshape(-1).astype(np.int32),
-                      "slots": slots.reshape(-1).astype(np.int32),
-                      "seq_slot": sl.astype(np.int32),
-                      "q_start": np.arange(0, nb * K1, K1, dtype=np.int32),
-                      "q_len": np.full(nb, K1, np.int32),
-                      "q_pos0": np.where(real, L - 1, 0).astype(np.int32),
-                      "kv_len": np.where(real, L + k, 1).astype(np.int32),
-                      "logit_rows": np.arange(nb * K1, dtype=np.int32)})
+        self._stage_check(native.load().psd_stage_verify(
+            fwd.host_set_ptr(0), fwd.fields_ptr, self.bt_ptr, self.max_blocks,
+            self.nblk.ctypes.data, self.block_size, int(self.replay), ldt, self.scratch_slot,
+            sl.ctypes.data, L.ctypes.data, k.ctypes.data, n, nb, kmax), "verify staging")
         fwd.upload(1)
         vm = self.v_meta_host.numpy()
         B = self.max_batch

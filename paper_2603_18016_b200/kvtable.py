@@ -99,6 +99,7 @@ class KVBlockTable:
         self._allocated: dict[int, int] = {}
         self._blocks: dict[int, list[int]] = {}
         self.version = 0  # bumped whenever a physical block list changes
+        self._list_version: dict[int, int] = {}  # per request, same rule
 
     # -- queries --------------------------------------------------------
     def written_of(self, request_id: int) -> int:
@@ -109,6 +110,10 @@ class KVBlockTable:
 
     def blocks_of(self, request_id: int) -> list[int]:
         return self._blocks.get(request_id, [])
+
+    def list_version(self, request_id: int) -> int:
+        """Changes whenever ``blocks_of(request_id)`` does (device-table caching)."""
+        return self._list_version.get(request_id, 0)
 
     @property
     def total_blocks_in_use(self) -> int:
@@ -154,6 +159,7 @@ class KVBlockTable:
             self.pool.give(blocks[target:])
             del blocks[target:]
         self.version += 1
+        self._list_version[request_id] = self.version
 
     def ensure_capacity(self, request_id: int, total_tokens: int) -> int:
         """Grow the allocation to cover ``total_tokens``; returns blocks added."""
@@ -208,6 +214,7 @@ class KVBlockTable:
         del self._written[request_id]
         self.has_deferred.discard(request_id)
         blocks = self._blocks.pop(request_id, None)
+        self._list_version.pop(request_id, None)
         if blocks:
             self.pool.give(blocks)
             self.version += 1

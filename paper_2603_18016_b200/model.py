@@ -413,6 +413,10 @@ class Forward:
         self._host_np = self.meta_host.numpy()
         self._events = [None] * self.ring
         self._cur = 0
+        # (offset, capacity) per META_FIELDS entry, for the native stagers
+        self.fields_np = np.array([v for name in META_FIELDS for v in self._offsets[name]],
+                                  np.int32)
+        self.fields_ptr = self.fields_np.ctypes.data
 
     # ---- tensor parallelism (target TP) ---------------------
     def _tp_reduce(self, S: int, n: int) -> int:
@@ -451,6 +455,10 @@ class Forward:
         ev = self._events[self._cur]
         if ev is not None:
             ev.synchronize()
+
+    def host_set_ptr(self, set_index: int = 0) -> int:
+        """Address of a metadata set in the current pinned staging buffer."""
+        return self.meta_host.data_ptr() + 4 * (self._cur * self.sets + set_index) * self.set_size
 
     def stage(self, set_index: int, arrays: dict[str, np.ndarray]) -> None:
         """Write host metadata (int32) for one set into pinned staging."""

@@ -68,6 +68,8 @@ SIGNATURES: dict[str, tuple] = {
     "psd_verify_greedy_fold": (_i, [_p, _i, _i, _p, _p, _i, _i, _p, _p, _p, _p]),
     "psd_commit": (_i, [_p, _p, _i, _p, _i, _p, _p, _i, _p, _i, _p]),
     "psd_index_copy_i32": (_i, [_p, _p, _p, _p, _i, _p]),
+    "psd_stage_draft": (_i, [_p, _i64, _p, _p, _i, _p, _i, _i, _i, _i, _p, _p, _p, _i, _i, _i]),
+    "psd_stage_verify": (_i, [_p, _p, _p, _i, _p, _i, _i, _i, _i, _p, _p, _p, _i, _i, _i]),
     "psd_fill_uniform_bf16": (_i, [_p, _sz, _c.c_uint64, _f, _p]),
     "psd_fill_uniform_bf16_block": (_i, [_p, _i64, _i, _i, _i64, _i64, _i64, _c.c_uint64, _f,
                                          _p]),
@@ -154,6 +156,12 @@ def load():
         fn.argtypes = args
     _lib = lib
     return lib
+
+
+# psd_stage_* return codes (include/psd.h)
+STAGE_BAD_ARGS = 1001
+STAGE_CAPACITY = 1002
+STAGE_KV_OVERRUN = 1003
 
 
 def check(rc: int, what: str) -> None:

@@ -57,7 +57,7 @@ def rg(key, launch):
 
 be.execute, be._run_graph = ex, rg
 fwd = be.dfwd
-for n in ("stage", "upload", "begin"):
+for n in ("stage", "stage_many", "upload", "begin"):
     f = getattr(fwd, n)
 
     def g(*a, _f=f, _n=n, **k):
