@@ -329,6 +329,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUt
 struct SKArgs {
   int M, N, K;
   int KB, MT, tiles, G;
+  // token-tile groups: every group of ACC_COLS tokens runs the same schedule
+  // of G1 virtual CTAs over its T1 = N / 128 weight tiles (G = G1 * MT), so a
+  // tile's k-split -- and every output element's summation order -- depends
+  // on (N, K) and the SM count only, never on M (batch-invariant at any M)
+  int G1, T1;
   long long U;
   void* Y;
   int ldy;
@@ -360,15 +365,17 @@ __device__ __forceinline__ unsigned long long gtimer() {
 struct Seg {
   int t, kb0, kb1, first;  // tile, k-block range, is the (virtual) CTA's first segment
   int v;                   // virtual CTA the segment belongs to
+  int tl, vb;              // group-local tile, first virtual CTA of the group
 };
 
+// first stream-K unit of a group's virtual CTA c (0 <= c <= G1)
 __device__ __forceinline__ long long sk_bound(long long c, const SKArgs& g) {
-  return c * g.U / g.G;
+  return c * g.U / g.G1;
 }
-// CTA holding unit u
+// group-local virtual CTA holding unit u
 __device__ __forceinline__ int sk_owner(long long u, const SKArgs& g) {
-  long long c = u * g.G / g.U;
-  while (c + 1 < g.G && sk_bound(c + 1, g) <= u) ++c;
+  long long c = u * g.G1 / g.U;
+  while (c + 1 < g.G1 && sk_bound(c + 1, g) <= u) ++c;
   while (c > 0 && sk_bound(c, g) > u) --c;
   return (int)c;
 }
@@ -432,36 +439,66 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   // segment iterator (identical sequence in every role)
   // first this CTA's stream-K units over tiles D.., then its whole tiles
   // c, c+G, .. < D: a CTA ends on a whole tile, whose epilogue reads no partials
+  // virtual CTA v = group * G1 + v1 works on group `group`'s tiles (tile
+  // index group * T1 + local tile; token tile group = tile / T1).  A physical
+  // CTA walks its group-local virtual CTAs v1 = c, c + grid, ...; each local
+  // segment (weight tile, k-range) is run for every token group back to back,
+  // so the groups re-read a weight k-block from L2 right after its first
+  // fetch (the weights stream from HBM once at any M)
   struct SegIt {
-    int v;
+    int v1;
     long long u, u0, u1;
     int dp;
+    int gi, have;  // next token group of the current local segment
+    int tl, kb0, kb1, first;
   };
-  auto seg_begin = [&](int v) -> SegIt {
-    return SegIt{v, sk_bound(v, g), sk_bound(v, g), sk_bound(v + 1, g), v};
+  auto seg_begin = [&](int v1) -> SegIt {
+    SegIt it;
+    it.v1 = v1;
+    it.u = it.u0 = sk_bound(v1, g);
+    it.u1 = sk_bound(v1 + 1, g);
+    it.dp = v1;
+    it.gi = 0;
+    it.have = 0;
+    it.tl = it.kb0 = it.kb1 = it.first = 0;
+    return it;
   };
   auto next_seg = [&](SegIt& it, Seg& sg) -> bool {
-    while (it.v < g.G) {
-      sg.v = it.v;
-      if (it.u < it.u1) {
-        sg.t = g.D + (int)(it.u / g.KB);
-        sg.kb0 = (int)(it.u % g.KB);
-        sg.kb1 = (int)min((long long)g.KB, sg.kb0 + (it.u1 - it.u));
-        sg.first = it.u == it.u0;
-        it.u += sg.kb1 - sg.kb0;
+    while (true) {
+      if (it.have && it.gi < g.MT) {
+        sg.tl = it.tl;
+        sg.kb0 = it.kb0;
+        sg.kb1 = it.kb1;
+        sg.first = it.first;
+        sg.vb = it.gi * g.G1;
+        sg.v = sg.vb + it.v1;
+        sg.t = it.gi * g.T1 + it.tl;
+        ++it.gi;
         return true;
+      }
+      it.have = 0;
+      it.gi = 0;
+      if (it.v1 >= g.G1) return false;
+      if (it.u < it.u1) {
+        it.tl = g.D + (int)(it.u / g.KB);
+        it.kb0 = (int)(it.u % g.KB);
+        it.kb1 = (int)min((long long)g.KB, it.kb0 + (it.u1 - it.u));
+        it.first = it.u == it.u0;
+        it.u += it.kb1 - it.kb0;
+        it.have = 1;
+        continue;
       }
       if (it.dp < g.D) {
-        sg.t = it.dp;
-        sg.kb0 = 0;
-        sg.kb1 = g.KB;
-        sg.first = 0;
-        it.dp += g.G;
-        return true;
+        it.tl = it.dp;
+        it.kb0 = 0;
+        it.kb1 = g.KB;
+        it.first = 0;
+        it.dp += g.G1;
+        it.have = 1;
+        continue;
       }
-      it = seg_begin(it.v + (int)gridDim.x);
+      it = seg_begin(it.v1 + (int)gridDim.x);
     }
-    return false;
   };
 
   if (warp == 0) {
@@ -477,7 +514,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         SegIt i0 = seg_begin(c);
         Seg s0;
         if (next_seg(i0, s0)) {
-          const int n0 = (s0.t / g.MT) * BM;
+          const int n0 = (s0.t % g.T1) * BM;
           npre = min(s0.kb1 - s0.kb0, C::STAGES);
           for (int j = 0; j < npre; ++j) {
             mbar_arrive_expect_tx(full + j, C::STAGE);
@@ -493,7 +530,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       }
       pdl_wait();
       while (next_seg(it, sg)) {
-        const int n0 = (sg.t / g.MT) * BM, m0 = (sg.t % g.MT) * ACC_COLS;
+        const int n0 = (sg.t % g.T1) * BM, m0 = (sg.t / g.T1) * ACC_COLS;
         for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++i) {
           const int s = i % C::STAGES;
           const uint32_t ph = (i / C::STAGES) & 1;
@@ -581,15 +618,15 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     while (next_seg(it, sg)) {
       const int a = j % NACC;
       const uint32_t aph = (j / NACC) & 1;
-      const int n0 = (sg.t / g.MT) * BM, m0 = (sg.t % g.MT) * ACC_COLS;
+      const int n0 = (sg.t % g.T1) * BM, m0 = (sg.t / g.T1) * ACC_COLS;
       const bool split = sg.kb0 != 0 || sg.kb1 != g.KB;
       const int me = sg.v;  // virtual CTA of this segment
       int owner = me, last = me;
       bool finisher = true;
       int* flag = s_flag + (j & 1);
       if (split) {
-        owner = sk_owner((long long)(sg.t - g.D) * g.KB, g);
-        last = sk_owner((long long)(sg.t - g.D) * g.KB + g.KB - 1, g);
+        owner = sg.vb + sk_owner((long long)(sg.tl - g.D) * g.KB, g);
+        last = sg.vb + sk_owner((long long)(sg.tl - g.D) * g.KB + g.KB - 1, g);
         // every other contributor already published: finish without
         // publishing (the usual case for the tile a CTA ends on, i.e. the
         // tail).  Checked while this segment's MMAs are still running.
@@ -661,7 +698,8 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 #pragma unroll
                   for (int k = 0; k < 16; ++k) v[e][k] += __uint_as_float(r[e][k]);
               } else {
-                const bool first_of_cc = sk_bound(cc, g) >= (long long)(sg.t - g.D) * g.KB;
+                const bool first_of_cc =
+                    sk_bound(cc - sg.vb, g) >= (long long)(sg.tl - g.D) * g.KB;
                 const float* pp = g.part + ((size_t)cc * 2 + (first_of_cc ? 0 : 1)) * (ACC_COLS * BM);
                 float w[EG][16];
 #pragma unroll
@@ -978,7 +1016,7 @@ int launch_sk_bn_s(const CUtensorMap& mw, const CUtensorMap& mx, const SKArgs& g
         (const void*)gemm_sk_kernel<BN, EPI, TILED, NT, SMEM_KB>, SMEM, st);
     if (e != cudaSuccess) return (int)e;
   }
-  return (int)psd::launch(gemm_sk_kernel<BN, EPI, TILED, NT, SMEM_KB>, dim3(sk_physical(g.G)),
+  return (int)psd::launch(gemm_sk_kernel<BN, EPI, TILED, NT, SMEM_KB>, dim3(sk_physical(g.G1)),
                           dim3(kThreads), SMEM, st, mw, mx, g);
 }
 
@@ -1087,8 +1125,8 @@ int token_tile(int M) {
   return std::max(32, (M + 31) / 32 * 32);
 }
 
-// token geometry: bn rows per token tile, nt token tiles per weight tile (2 for
-// 256 < M <= 512, so weights stream once), mt token-tile groups.  PSD_GEMM_NT2=0
+// token geometry: bn rows per token tile, nt token tiles per weight tile (2
+// above 256 tokens), mt token-tile groups (1 up to 512 tokens).  PSD_GEMM_NT2=0
 // keeps one token tile per CTA (A/B runs)
 struct TokGeo {
   int bn, nt, mt;
@@ -1102,8 +1140,12 @@ int nt2_enabled() {
 }
 TokGeo tok_geo(int M, bool allow_nt2 = true) {
   TokGeo t;
-  if (allow_nt2 && M > 256 && M <= 512 && nt2_enabled()) {
-    t.bn = std::min(256, ((M + 1) / 2 + 31) / 32 * 32);
+  if (allow_nt2 && M > 256 && nt2_enabled()) {
+    // above 512 tokens: groups of <= 512 (two token tiles each), each group
+    // running the one-group schedule (sk_plan), so fewer groups re-read the
+    // weights and fix up split tiles than with single token tiles
+    const int groups = (M + 511) / 512;
+    t.bn = std::min(256, ((M + 2 * groups - 1) / (2 * groups) + 31) / 32 * 32);
     t.nt = 2;
   } else {
     t.bn = token_tile(M);
@@ -1167,7 +1209,7 @@ bool sk_dp_enabled() {
 }
 
 struct SKPlan {
-  int bn, nt, KB, MT, tiles, G, D;
+  int bn, nt, KB, MT, tiles, G, D, G1, T1;
   long long U;
   size_t part_bytes, ticket_bytes;
 };
@@ -1177,24 +1219,28 @@ struct SKPlan {
 SKPlan sk_plan(int M, int N, int K, bool allow_nt2 = true) {
   SKPlan p;
   // batch-invariant geometry: the k-block split of every tile depends only on
-  // (N, K) and the SM count -- not on the CTA cap, and not on M for M <= 512
-  // (two token tiles share a weight tile above 256 tokens, so the tile set is
-  // the same as at M <= 256)
+  // (N, K) and the SM count -- not on the CTA cap, and not on M.  One group's
+  // schedule (G1 virtual CTAs over the T1 = N / 128 weight tiles) is planned
+  // as for a single token tile; M > 512 runs MT groups of it (G = G1 * MT
+  // virtual CTAs, a physical CTA runs a segment for every group in turn),
+  // 256 < M <= 512 one group with two token tiles per weight tile
   const TokGeo tg = tok_geo(M, allow_nt2);
   p.bn = tg.bn;
   p.nt = tg.nt;
   p.KB = (K + BK - 1) / BK;
   p.MT = tg.mt;
-  p.tiles = (N / BM) * p.MT;
-  p.G = (int)std::min<long long>(num_sms_raw(), (long long)p.tiles * p.KB);
-  // data-parallel + stream-K: each CTA takes tiles / G whole tiles and an
+  p.T1 = N / BM;
+  p.tiles = p.T1 * p.MT;
+  p.G1 = (int)std::min<long long>(num_sms_raw(), (long long)p.T1 * p.KB);
+  p.G = p.G1 * p.MT;
+  // data-parallel + stream-K: each CTA takes T1 / G1 whole tiles and an
   // equal share of the remaining tiles' k-blocks; a remainder that would cut
   // every tile into more than ~2 pieces gets one more stream-K wave instead
-  p.D = sk_dp_enabled() ? p.G * (p.tiles / p.G) : 0;
-  if (p.D > 0 && p.D < p.tiles && (long long)(p.tiles - p.D) * p.KB < (long long)p.G * (p.KB / 2))
-    p.D -= p.G;
-  if (whole_k().load(std::memory_order_relaxed)) p.D = p.tiles;
-  p.U = (long long)(p.tiles - p.D) * p.KB;
+  p.D = sk_dp_enabled() ? p.G1 * (p.T1 / p.G1) : 0;
+  if (p.D > 0 && p.D < p.T1 && (long long)(p.T1 - p.D) * p.KB < (long long)p.G1 * (p.KB / 2))
+    p.D -= p.G1;
+  if (whole_k().load(std::memory_order_relaxed)) p.D = p.T1;
+  p.U = (long long)(p.T1 - p.D) * p.KB;
   p.part_bytes = (size_t)p.G * 2 * p.nt * p.bn * BM * sizeof(float);
   // tickets live at a FIXED offset (start of the workspace) so GEMMs of any
   // shape can share one workspace: each leaves its tickets zeroed
@@ -1271,14 +1317,14 @@ void psd_gemm_set_trace(void* trace) {
 int psd_gemm_plan(int M, int N, int K, int epi, int splits_hint, int* splits_out,
                   size_t* workspace_bytes) {
   if (M <= 0 || N <= 0 || K <= 0 || (K % 8) || (N % BM)) return (int)cudaErrorInvalidValue;
-  const TokGeo tg = tok_geo(M);
-  const int tiles = (N / BM) * tg.mt;
+  // weight tiles of ONE token tile: the split (and so the summation order of
+  // every output element) depends on (N, K) and the SM count -- not on M, and
+  // not on the CTA cap or what runs beside the GEMM
+  const int tiles = N / BM;
   const int kb_total = (K + BK - 1) / BK;
   int splits = splits_hint;
   if (splits <= 0) {
     splits = 1;
-    // from the SM count, not the CTA cap: the split (and so the summation order
-    // of every output element) must not depend on what runs beside the GEMM
     if (tiles < 120) splits = std::max(1, std::min(num_sms_raw() / tiles, kb_total / 4));
     if (whole_k().load(std::memory_order_relaxed)) splits = 1;
   }
@@ -1328,6 +1374,7 @@ int psd_gemm_tiled(const void* X, int ldx, int M, int K, const void* W_tiled, in
   SKArgs g;
   g.M = M; g.N = N; g.K = K;
   g.KB = p.KB; g.MT = p.MT; g.tiles = p.tiles; g.G = p.G; g.U = p.U; g.D = p.D;
+  g.G1 = p.G1; g.T1 = p.T1;
   g.Y = Y; g.ldy = ldy; g.R = static_cast<const __nv_bfloat16*>(R); g.ldr = ldr;
   g.tickets = static_cast<int*>(workspace);
   g.part = reinterpret_cast<float*>(static_cast<char*>(workspace) + p.ticket_bytes);
@@ -1371,6 +1418,7 @@ int psd_gemm_argmax(const void* X, int ldx, int M, int K, const void* W, int ldw
   memset(&g, 0, sizeof(g));
   g.M = M; g.N = N; g.K = K;
   g.KB = p.KB; g.MT = p.MT; g.tiles = p.tiles; g.G = p.G; g.U = p.U; g.D = p.D;
+  g.G1 = p.G1; g.T1 = p.T1;
   g.Y = partials; g.ldy = M;
   g.tickets = static_cast<int*>(workspace);
   g.part = reinterpret_cast<float*>(static_cast<char*>(workspace) + p.ticket_bytes);
@@ -1440,10 +1488,11 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
   if (splits_hint == 0 && M > 0 && N % BM == 0) {
     // one wave of whole-K tiles (>= 3/4 of the SMs busy, no tail): the plain
     // grid kernel beats stream-K, whose fix-ups buy nothing here (1B draft
-    // gate/up at M = 32: 14.3 vs 19.8 us, profiles/r01b_kbench_gemm_splits.txt)
-    const TokGeo tg = tok_geo(M);
-    const int tiles = (N / BM) * tg.mt;
-    if (tg.nt == 1 && tiles <= num_sms_raw() && 4 * tiles >= 3 * num_sms_raw()) splits_hint = 1;
+    // gate/up at M = 32: 14.3 vs 19.8 us, profiles/r01b_kbench_gemm_splits.txt).
+    // Decided on the weight tiles of one token tile so that every M takes the
+    // same path (batch-invariant summation order)
+    const int tiles = N / BM;
+    if (tiles <= num_sms_raw() && 4 * tiles >= 3 * num_sms_raw()) splits_hint = 1;
   }
   if (splits_hint == 0) {
     // stream-K persistent path (default)
@@ -1458,6 +1507,7 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
     SKArgs g;
     g.M = M; g.N = N; g.K = K;
     g.KB = p.KB; g.MT = p.MT; g.tiles = p.tiles; g.G = p.G; g.U = p.U; g.D = p.D;
+    g.G1 = p.G1; g.T1 = p.T1;
     g.Y = Y; g.ldy = ldy; g.R = static_cast<const __nv_bfloat16*>(R); g.ldr = ldr;
     g.tickets = static_cast<int*>(workspace);
     g.part = reinterpret_cast<float*>(static_cast<char*>(workspace) + p.ticket_bytes);

@@ -206,3 +206,56 @@ def test_lm_head_argmax_epilogue(cuda_device, M, N, K, bias):
     ref = logits.argmax(dim=1).to(torch.int32)
     assert torch.equal(out, ref)
     assert dst[0].item() == -7 and torch.equal(dst[2::2], ref[1:])
+
+
+@pytest.mark.parametrize("N,K,epi", [(4096, 4096, native.EPI_F32), (2048, 8192, native.EPI_F32),
+                                     (8192, 4096, native.EPI_SILU),
+                                     (128256, 4096, native.EPI_F32)])
+def test_stream_k_batch_invariant_any_m(cuda_device, N, K, epi):
+    """Stream-K: a token's output bits do not depend on how many tokens share
+    the launch -- M = 24 .. 1100 (one, two and up to five token tiles per
+    weight tile), with and without a CTA cap -- so greedy PSD and SD(2m)
+    agree at any verify width (cfg4's SD(2m) pass is 640 tokens)."""
+    g = torch.Generator(device=cuda_device).manual_seed(N + K)
+    Mmax = 1100
+    x = torch.randn(Mmax, K, device=cuda_device, generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device=cuda_device, generator=g) * 0.05).to(torch.bfloat16)
+    lib = native.load()
+    ref = ops.gemm(x[:24], w, epi=epi)
+    for M, cap in ((24, 74), (192, 0), (320, 0), (512, 0), (640, 0), (640, 74), (1100, 0)):
+        lib.psd_gemm_set_max_ctas(cap)
+        try:
+            y = ops.gemm(x[:M], w, epi=epi)
+        finally:
+            lib.psd_gemm_set_max_ctas(0)
+        torch.cuda.synchronize()
+        assert torch.equal(y[:24], ref), (M, cap)
+    _close(y, _ref(x, w) if epi != native.EPI_SILU else y.float(), K)
+
+
+@pytest.mark.parametrize("N,K", [(4096, 4096), (6144, 4096), (8192, 8192), (2048, 8192)])
+def test_split_k_partials_batch_invariant_any_m(cuda_device, N, K):
+    """Grid split-K: the split count and every slice's bits for a token are
+    the same at M = 32 and M = 640 / 1024 (the consumer then sums the same
+    slices in the same order)."""
+    import ctypes
+    g = torch.Generator(device=cuda_device).manual_seed(N * 3 + K)
+    Mmax = 1024
+    x = torch.randn(Mmax, K, device=cuda_device, generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device=cuda_device, generator=g) * 0.05).to(torch.bfloat16)
+    lib = native.load()
+    part = torch.empty(16 * Mmax * N, device=cuda_device)
+    out = {}
+    for M in (32, 320, 640, 1024):
+        sp = ctypes.c_int()
+        native.check(lib.psd_gemm_partials(x.data_ptr(), K, M, K, w.data_ptr(), K, N,
+                                           part.data_ptr(), part.numel() * 4, 0,
+                                           ctypes.byref(sp),
+                                           torch.cuda.current_stream().cuda_stream), "partials")
+        torch.cuda.synchronize()
+        out[M] = (sp.value, part[:sp.value * M * N].view(sp.value, M, N)[:, :32].clone())
+    s0, p0 = out[32]
+    for M, (s, p) in out.items():
+        assert s == s0, (M, s, s0)
+        assert torch.equal(p, p0), M
+    _close(p0.sum(0), _ref(x[:32], w), K)
