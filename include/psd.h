@@ -335,6 +335,9 @@ int psd_stage_verify(int32_t* set, const int32_t* fields, const int32_t* block_t
                      const int32_t* nblk, int block_size, int replay, int ldt, int scratch_slot,
                      const int32_t* slot, const int32_t* L, const int32_t* k, int n, int nb,
                      int kmax);
+/* stream-ordered copy (cudaMemcpyAsync, direction from the pointers): the
+ * per-step metadata uploads from pinned staging, without a kernel */
+int psd_copy_async(void* dst, const void* src, size_t bytes, void* stream);
 /* kernels enqueued by this library so far (host-side counter; a captured
  * CUDA graph's launches are counted once, at capture) */
 long long psd_launch_count(void);

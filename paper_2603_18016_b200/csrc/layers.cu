@@ -1612,6 +1612,11 @@ int psd_index_copy_i32(int32_t* dst, const int32_t* dst_idx, const int32_t* src,
                           (cudaStream_t)stream, dst, dst_idx, src, src_idx, n);
 }
 
+int psd_copy_async(void* dst, const void* src, size_t bytes, void* stream) {
+  if (bytes == 0) return 0;
+  return (int)cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)stream);
+}
+
 int psd_commit(const int32_t* accepted_len, const int32_t* out_tokens, int K,
                const int32_t* row_slot, int n, int32_t* generated, int32_t* slot_tokens,
                int slot_tokens_ld, int32_t* outputs, int outputs_ld, void* stream) {

@@ -372,6 +372,13 @@ class GpuBackend:
             raise KVError(f"request {rid}: KV position {pos} beyond its {len(blocks)} blocks")
         return blocks[bi] * self.block_size + pos % self.block_size
 
+    def _h2d(self, dst: torch.Tensor, src: torch.Tensor) -> None:
+        """Stream-ordered copy of pinned host staging into a same-sized device
+        buffer on the current stream (psd_copy_async: no torch dispatch)."""
+        native.check(native.load().psd_copy_async(
+            dst.data_ptr(), src.data_ptr(), src.numel() * src.element_size(),
+            torch.cuda.current_stream(self.device).cuda_stream), "h2d copy")
+
     def _upload_block_table(self, state) -> None:
         """Host block table -> device.  Rows are rewritten only for slots whose
         (request, block-list version) changed; rows of free slots are never
@@ -391,7 +398,7 @@ class GpuBackend:
             bt[s, n:] = 0
             self.nblk[s] = n
             sig[s] = key
-        self.block_table.copy_(self.block_table_host, non_blocking=True)
+        self._h2d(self.block_table, self.block_table_host)
         self.h2d_bytes += self.block_table_host.numel() * 4
 
     def _admit(self, state, ids) -> None:
@@ -613,7 +620,7 @@ class GpuBackend:
             K = self.k_max
             for i in range(kmax):
                 kh[2 * B + i * B:2 * B + i * B + nb] = np.where(real & (i < k), sl * K + i, -1)
-            self.d_key.copy_(self.d_key_host[self.d_key_cur], non_blocking=True)
+            self._h2d(self.d_key, self.d_key_host[self.d_key_cur])
             self.h2d_bytes += self.d_key.numel() * 4
             ev = torch.cuda.Event()
             ev.record()
@@ -720,13 +727,13 @@ class GpuBackend:
         if kmax:
             vm[3 * B:3 * B + nb * kmax] = (sl[:, None] * ldt + 2 + np.arange(kmax)[None, :]
                                            ).reshape(-1)
-        self.v_meta.copy_(self.v_meta_host, non_blocking=True)
+        self._h2d(self.v_meta, self.v_meta_host)
         self.h2d_bytes += self.v_meta_host.numel() * 4
         if self.mode == "sample":
             kh = self.v_key_host.numpy()
             kh[:nb] = [r.request_id for r in rows] + [0] * (nb - n)
             kh[B:B + nb] = L
-            self.v_key.copy_(self.v_key_host, non_blocking=True)
+            self._h2d(self.v_key, self.v_key_host)
             self.h2d_bytes += self.v_key_host.numel() * 4
         capped = beside_draft and self.verify_ctas > 0
         self._run_graph(("verify", nb, kmax, capped, self.replay),

@@ -412,6 +412,7 @@ class Forward:
         self.meta_host = torch.zeros(self.ring, sets, o, dtype=torch.int32).pin_memory()
         self._host_np = self.meta_host.numpy()
         self._events = [None] * self.ring
+        self._event_pool = [torch.cuda.Event() for _ in range(self.ring)]
         self._cur = 0
         # (offset, capacity) per META_FIELDS entry, for the native stagers
         self.fields_np = np.array([v for name in META_FIELDS for v in self._offsets[name]],
@@ -481,9 +482,11 @@ class Forward:
 
     def upload(self, n_sets: int = 1) -> None:
         """Copy staged sets 0..n_sets-1 to the device on the current stream."""
-        self.meta[:n_sets].copy_(self.meta_host[self._cur, :n_sets], non_blocking=True)
-        self.h2d_bytes += n_sets * self.meta_host.shape[2] * 4
-        ev = torch.cuda.Event()
+        nbytes = n_sets * self.set_size * 4
+        _chk(self.model._lib.psd_copy_async(self.meta.data_ptr(), self.host_set_ptr(0), nbytes,
+                                            _stream_ptr(self.model.device)), "metadata upload")
+        self.h2d_bytes += nbytes
+        ev = self._event_pool[self._cur]
         ev.record()
         self._events[self._cur] = ev
 
