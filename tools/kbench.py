@@ -66,11 +66,8 @@ def report(name, shape, us, nbytes, flops=0):
 def gemm_case(tag, M, N, K, epi, copies=6, legacy=False, tiled=False, splits=None):
     x = torch.randn(M, K, device=dev).to(bf)
     if tiled and not hasattr(lib, "psd_tile_weights"):
-        try:
-            lib.psd_tile_weights
-        except AttributeError:
-            print(f"{tag}: pre-tiled GEMM not built (PSD_EXPERIMENTAL=1)")
-            return
+        print(f"{tag}: pre-tiled GEMM not built (PSD_EXPERIMENTAL=1)")
+        return
     ws = [(torch.randn(N, K, device=dev) * 0.02).to(bf) for _ in range(copies)]
     if tiled:
         tws = []
