@@ -204,11 +204,11 @@ __device__ __forceinline__ void tile_epilogue_tma(const GemmArgs& g, uint32_t tm
   if (threadIdx.x == 64) bulk_wait<0>();
 }
 
-template <int BN, int EPI, int NT = 1>
+template <int BN, int EPI, int NT = 1, int SMEM_KB = 200>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
             const __grid_constant__ GemmArgs g) {
-  using C = Cfg<BN, NT>;
+  using C = Cfg<BN, NT, SMEM_KB>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -989,17 +989,46 @@ void set_out_map(SKArgs& g, int epi, void* Y, int M, int N, int ldy) {
     g.tma_y = 1;
 }
 
-template <int BN, int EPI>
-int launch_bn(const CUtensorMap& mw, const CUtensorMap& mx, const GemmArgs& g, dim3 grid,
-              cudaStream_t st) {
-  using C = Cfg<BN>;
+template <int BN, int EPI, int SMEM_KB>
+int launch_bn_s(const CUtensorMap& mw, const CUtensorMap& mx, const GemmArgs& g, dim3 grid,
+                cudaStream_t st) {
+  using C = Cfg<BN, 1, SMEM_KB>;
   {
-    const cudaError_t e = psd::ensure_smem_limit((const void*)gemm_kernel<BN, EPI>,
+    const cudaError_t e = psd::ensure_smem_limit((const void*)gemm_kernel<BN, EPI, 1, SMEM_KB>,
                                                  C::SMEM + ep_stage_bytes<EPI>(), st);
     if (e != cudaSuccess) return (int)e;
   }
-  return (int)psd::launch(gemm_kernel<BN, EPI>, grid, dim3(kThreads),
+  return (int)psd::launch(gemm_kernel<BN, EPI, 1, SMEM_KB>, grid, dim3(kThreads),
                           C::SMEM + ep_stage_bytes<EPI>(), st, mw, mx, g);
+}
+
+// Decode-width GEMMs of the draft (split-K QKV / O / down with <= 16
+// k-blocks per CTA at <= 64 tokens, the whole-K gate/up at <= 32 tokens) run
+// an 80 KB ring instead of 200 KB, so their CTAs fit on an SM beside the
+// neighbouring kernel's (the decode attention, the next small GEMM):
+// launched early by PDL they stream their weights while the predecessor
+// still runs.  cfg2 draft phase -2.5 %, PSD +3.2 %, SD(2m) unchanged
+// (profiles/r02_small_ring.txt).  PSD_GEMM_SMALL_RING: 0 = the full ring for
+// every shape, 1 = split-K with <= 8 k-blocks only, 2 = default
+int small_ring_enabled() {
+  static int v = [] {
+    const char* e = getenv("PSD_GEMM_SMALL_RING");
+    return e ? atoi(e) : 2;
+  }();
+  return v;
+}
+
+template <int BN, int EPI>
+int launch_bn(const CUtensorMap& mw, const CUtensorMap& mx, const GemmArgs& g, dim3 grid,
+              cudaStream_t st) {
+  if constexpr (EPI == PSD_EPI_PARTIAL && BN <= 64) {
+    if (small_ring_enabled() && g.kb_per_split <= (small_ring_enabled() >= 2 ? 16 : 8))
+      return launch_bn_s<BN, EPI, 80>(mw, mx, g, grid, st);
+  }
+  if constexpr (EPI == PSD_EPI_SILU && BN <= 32) {
+    if (small_ring_enabled() >= 2) return launch_bn_s<BN, EPI, 80>(mw, mx, g, grid, st);
+  }
+  return launch_bn_s<BN, EPI, 200>(mw, mx, g, grid, st);
 }
 
 
