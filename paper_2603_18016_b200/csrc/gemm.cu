@@ -1051,6 +1051,15 @@ int launch_sk_bn_s(const CUtensorMap& mw, const CUtensorMap& mx, const SKArgs& g
 
 template <int BN, int EPI, bool TILED, int NT = 1>
 int launch_sk_bn(const CUtensorMap& mw, const CUtensorMap& mx, const SKArgs& g, cudaStream_t st) {
+  // the draft's stream-K gate/up at <= 32 tokens (small models whose FFN
+  // tiles do not fill one wave): the same 80 KB ring as launch_bn's
+  if constexpr (EPI == PSD_EPI_SILU && BN <= 32 && NT == 1 && !TILED) {
+    static const int on = [] {
+      const char* e = getenv("PSD_GEMM_SK_SMALL");
+      return e ? atoi(e) : 1;
+    }();
+    if (on && small_ring_enabled() >= 2) return launch_sk_bn_s<BN, EPI, TILED, NT, 80>(mw, mx, g, st);
+  }
   return launch_sk_bn_s<BN, EPI, TILED, NT, 200>(mw, mx, g, st);
 }
 
