@@ -215,6 +215,7 @@ class GpuBackend:
                 self.mk = self._make_mk(grid)
         self._step_events = None
         self._bt_sig = {}  # slot -> (request, block-list version) on the host table
+        self.draft_first = os.environ.get("PSD_DRAFT_FIRST", "0") == "1"
         # K6: the greedy draft's argmax (+ bias) in its LM-head epilogue
         # (PSD_K6=0: logits + bigram + K1(k = 0) + scatter, for A/B runs)
         self.k6 = (os.environ.get("PSD_K6", "1") == "1" and has_d
@@ -874,17 +875,25 @@ class GpuBackend:
             self._draft_loop(state, plan.serial_draft_ids, plan.quotas)
             e_sd.record(ds)
         ts.wait_event(e_sd)
+        # the verify is enqueued first: with the draft loop shortened it is the
+        # longer of the two overlapped passes, so it gets the earlier start
+        # (PSD_DRAFT_FIRST=1: the previous order)
+        def verify():
+            with torch.cuda.stream(ts):
+                e_v0.record(ts)
+                if rows:
+                    # capped GEMM grids only while drafts run beside the verify
+                    self._verify(state, rows, beside_draft=any(
+                        plan.quotas.get(rid, 0) > 0 for rid in plan.overlap_draft_ids))
+                e_v1.record(ts)
+        if not self.draft_first:
+            verify()
         with torch.cuda.stream(ds):
             # overlapped drafts of the skip batch
             self._draft_loop(state, plan.overlap_draft_ids, plan.quotas)
             e_ov.record(ds)
-        with torch.cuda.stream(ts):
-            e_v0.record(ts)
-            if rows:
-                # capped GEMM grids only while drafts run beside the verify
-                self._verify(state, rows, beside_draft=any(
-                    plan.quotas.get(rid, 0) > 0 for rid in plan.overlap_draft_ids))
-            e_v1.record(ts)
+        if self.draft_first:
+            verify()
         e_v1.synchronize()
         e_ov.synchronize()
         accepted = {}
