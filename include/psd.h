@@ -122,6 +122,15 @@ int psd_verify_greedy_fold(const float* partials, int W, int V_shard, const int3
                            const int32_t* draft_len, int B, int K, const int32_t* forced_len,
                            int32_t* accepted_len, int32_t* out_tokens, void* stream);
 
+/* Greedy K1 fused into the target LM head: argmax_tokens[b * (K + 1) + j] is
+ * the argmax (ties -> lowest index) of row j of request b's target logits
+ * with the synthetic-language bias, produced by psd_gemm_argmax (K6 epilogue)
+ * + psd_argmax_fold without storing logits; accepted_len / out_tokens as
+ * psd_verify_greedy(_forced) on those logits. */
+int psd_verify_greedy_tokens(const int32_t* argmax_tokens, const int32_t* draft_ids,
+                             const int32_t* draft_len, int B, int K, const int32_t* forced_len,
+                             int32_t* accepted_len, int32_t* out_tokens, void* stream);
+
 /* ---- K2: bf16 GEMM on tcgen05 (TMEM accumulators, TMA, mbarrier ring) -----
  *   Y[m, n] = epi( sum_k X[m*ldx + k] * W[n*ldw + k] )   X [M,K], W [N,K] bf16
  * Replaces the virtual pass durations verify_latency / draft_latency
@@ -177,7 +186,7 @@ int psd_gemm_partials(const void* X, int ldx, int M, int K, const void* W, int l
  * successor[tokens[rows ? rows[m] : m]] when successor and beta != 0 -- into
  * `partials` (psd_argmax_partials_bytes); psd_argmax_fold reduces the tiles
  * (ties -> lowest index, K1's canonical argmax) into out_tokens[m] and/or
- * dst[dst_idx[m]] (skipped when negative).  M <= 128, N % 128 == 0; the
+ * dst[dst_idx[m]] (skipped when negative).  M <= 256, N % 128 == 0; the
  * workspace is psd_gemm_bf16's stream-K workspace. */
 size_t psd_argmax_partials_bytes(int M, int N);
 int psd_gemm_argmax(const void* X, int ldx, int M, int K, const void* W, int ldw, int N,

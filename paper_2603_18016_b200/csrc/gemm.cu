@@ -1438,7 +1438,7 @@ int psd_gemm_argmax(const void* X, int ldx, int M, int K, const void* W, int ldw
                     const int32_t* tokens, const int32_t* rows, const int32_t* successor,
                     float beta, void* partials, void* workspace, size_t workspace_bytes,
                     void* stream) {
-  if (!X || !W || !partials || M <= 0 || M > 128 || N <= 0 || K <= 0 || (K % 8) || (N % BM))
+  if (!X || !W || !partials || M <= 0 || M > 256 || N <= 0 || K <= 0 || (K % 8) || (N % BM))
     return (int)cudaErrorInvalidValue;
   if (successor && beta != 0.f && !tokens) return (int)cudaErrorInvalidValue;
   if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(W)) & 15)
@@ -1470,6 +1470,10 @@ int psd_gemm_argmax(const void* X, int ldx, int M, int K, const void* W, int ldw
     case 64: return launch_sk_bn<64, PSD_EPI_ARGMAX, false>(mw, mx, g, st);
     case 96: return launch_sk_bn<96, PSD_EPI_ARGMAX, false>(mw, mx, g, st);
     case 128: return launch_sk_bn<128, PSD_EPI_ARGMAX, false>(mw, mx, g, st);
+    case 160: return launch_sk_bn<160, PSD_EPI_ARGMAX, false>(mw, mx, g, st);
+    case 192: return launch_sk_bn<192, PSD_EPI_ARGMAX, false>(mw, mx, g, st);
+    case 224: return launch_sk_bn<224, PSD_EPI_ARGMAX, false>(mw, mx, g, st);
+    case 256: return launch_sk_bn<256, PSD_EPI_ARGMAX, false>(mw, mx, g, st);
   }
   return (int)cudaErrorInvalidValue;
 }

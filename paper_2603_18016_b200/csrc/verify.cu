@@ -432,6 +432,26 @@ verify_fold_sharded(const Params p, int W) {
   }
 }
 
+// greedy from per-row argmax tokens (the target LM head's K6 epilogue +
+// argmax fold): one warp per request, the same ballot test and outputs as
+// verify_fold / verify_fold_sharded
+__global__ void __launch_bounds__(32)
+verify_accept_tokens(const int32_t* __restrict__ tok, const Params p) {
+  pdl_wait();
+  pdl_trigger();
+  const int b = blockIdx.x, lane = threadIdx.x;
+  const int kb = p.len[b];
+  const int* g = tok + (size_t)b * (p.K + 1);
+  const int x = lane < kb ? p.ids[b * p.K + lane] : -1;
+  const bool ok = lane < kb && x == g[lane];
+  const unsigned rej = __ballot_sync(0xffffffffu, !ok) & ((1u << kb) - 1u);
+  int a = rej ? __ffs(rej) - 1 : kb;
+  if (p.forced) a = min(max(__ldg(p.forced + b), 0), kb);
+  int32_t* o = p.out + b * (p.K + 1);
+  if (lane <= p.K) o[lane] = lane < a ? x : (lane == a ? g[a] : -1);
+  if (lane == 0) p.acc[b] = a;
+}
+
 // greedy: fold + decide, one CTA per request
 __global__ void __launch_bounds__(kThreads)
 verify_fold(const Params p) {
@@ -806,6 +826,19 @@ int psd_verify_greedy_fold(const float* partials, int W, int V_shard, const int3
   p.NS = (V_shard + PSD_SLICE - 1) / PSD_SLICE; p.R = K + 1;
   return (int)psd::launch(verify_fold_sharded, dim3(B), dim3(kThreads), 0, (cudaStream_t)stream,
                           p, W);
+}
+
+int psd_verify_greedy_tokens(const int32_t* argmax_tokens, const int32_t* draft_ids,
+                             const int32_t* draft_len, int B, int K, const int32_t* forced_len,
+                             int32_t* accepted_len, int32_t* out_tokens, void* stream) {
+  if (!argmax_tokens || B <= 0 || K < 0 || K > PSD_MAX_K || (K > 0 && !draft_ids) ||
+      !draft_len || !accepted_len || !out_tokens)
+    return (int)cudaErrorInvalidValue;
+  Params p{};
+  p.ids = draft_ids; p.len = draft_len; p.B = B; p.K = K; p.forced = forced_len;
+  p.acc = accepted_len; p.out = out_tokens;
+  return (int)psd::launch(verify_accept_tokens, dim3(B), dim3(32), 0, (cudaStream_t)stream,
+                          argmax_tokens, p);
 }
 
 int psd_verify_greedy_forced(const float* target_logits, int64_t t_stride_b, int64_t t_stride_i,

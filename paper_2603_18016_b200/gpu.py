@@ -178,6 +178,7 @@ class GpuBackend:
             self.v_ids = torch.empty(B, K, dtype=i32, device=dev)
             self.v_acc = torch.empty(B, dtype=i32, device=dev)
             self.v_out = torch.empty(B * (K + 1), dtype=i32, device=dev)
+            self.v_tok = torch.empty(B * (K + 1), dtype=i32, device=dev)  # argmax per row
             self.v_len = torch.empty(B, dtype=i32, device=dev)
             self.v_slot = torch.empty(B, dtype=i32, device=dev)
             # v_meta: [0, B) draft depths, [B, 2B) slots, [2B, 3B) replay counts,
@@ -216,6 +217,9 @@ class GpuBackend:
         self._step_events = None
         self._bt_sig = {}  # slot -> (request, block-list version) on the host table
         self.draft_first = os.environ.get("PSD_DRAFT_FIRST", "0") == "1"
+        # greedy verification through the target LM head's argmax epilogue
+        # (PSD_K1_EPI=0: stored logits + K1, for A/B runs)
+        self.k1_epi = os.environ.get("PSD_K1_EPI", "1") == "1"
         # K6: the greedy draft's argmax (+ bias) in its LM-head epilogue
         # (PSD_K6=0: logits + bigram + K1(k = 0) + scatter, for A/B runs)
         self.k6 = (os.environ.get("PSD_K6", "1") == "1" and has_d
@@ -778,8 +782,19 @@ class GpuBackend:
         # LM-head vocabulary shard to K1 partials, the ranks all-gather the
         # partials (KBs instead of M x V logits) and fold them identically
         c3 = (self.mode == "greedy" and fwd.comm is not None and self.capture_verify is None)
-        fwd.run(M, nb, K1, M, self.tlogits, self.tshape.vocab,
-                bigram=(self.succ_t, self.beta_target), shard_out=c3)
+        # greedy K1 fused into the LM head: the K6 epilogue reduces each logit
+        # row to (max, argmax) per vocabulary tile, a fold gives the argmax
+        # token per row, one warp per request decides -- no M x V logits are
+        # stored or re-read (same decisions as K1 on the stored logits)
+        k1_epi = (self.mode == "greedy" and self.k1_epi and fwd.comm is None
+                  and self.capture_verify is None and M <= fwd.amax_rows)
+        if k1_epi:
+            fwd.run(M, nb, K1, M, None, self.tshape.vocab,
+                    bigram=(self.succ_t, self.beta_target),
+                    argmax_into=(self.v_tok[:M], None, None))
+        else:
+            fwd.run(M, nb, K1, M, self.tlogits, self.tshape.vocab,
+                    bigram=(self.succ_t, self.beta_target), shard_out=c3)
         v_len = self.v_meta[:nb]
         v_slot = self.v_meta[B:B + nb]
         forced = self.v_meta[2 * B:2 * B + nb] if self.replay else None
@@ -810,6 +825,11 @@ class GpuBackend:
                 self.c3_all.data_ptr(), tm.tp[1], vs, v_ids.data_ptr(), v_len.data_ptr(), nb,
                 kmax, forced.data_ptr() if forced is not None else None, self.v_acc.data_ptr(),
                 out.data_ptr(), st), "verify fold (shards)")
+        elif k1_epi:
+            native.check(lib.psd_verify_greedy_tokens(
+                self.v_tok.data_ptr(), v_ids.data_ptr(), v_len.data_ptr(), nb, kmax,
+                forced.data_ptr() if forced is not None else None, self.v_acc.data_ptr(),
+                out.data_ptr(), st), "verify (argmax tokens)")
         elif self.mode == "greedy":
             ops.verify_greedy(logits, v_ids, v_len, self.v_acc[:nb], out, forced_len=forced)
         else:

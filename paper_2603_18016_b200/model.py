@@ -343,10 +343,13 @@ class Forward:
         self.act = torch.empty(T, s.ffn_padded, dtype=bf, device=dev)
         self.xf = torch.empty(max_logit_rows, s.hidden, dtype=bf, device=dev)
         self.prev = torch.empty(max_logit_rows, dtype=torch.int32, device=dev)
-        # K6 argmax partials (allocated here: never inside a graph capture)
-        self.amax = (torch.empty(native.load().psd_argmax_partials_bytes(max_logit_rows, s.vocab),
-                                 dtype=torch.uint8, device=dev)
-                     if s.vocab % 128 == 0 and max_logit_rows <= 128 else None)
+        # K6 argmax partials for up to 256 logit rows (the draft's LM head, and
+        # the target's when its greedy verification folds argmax tokens);
+        # allocated here: never inside a graph capture
+        self.amax_rows = min(max_logit_rows, 256) if s.vocab % 128 == 0 else 0
+        self.amax = (torch.empty(native.load().psd_argmax_partials_bytes(self.amax_rows,
+                                                                         s.vocab),
+                                 dtype=torch.uint8, device=dev) if self.amax_rows else None)
         self.comm = None
         if model.tp is not None and model.tp[1] > 1:
             import os
@@ -592,8 +595,8 @@ class Forward:
         ld = logits_ld or V
         if argmax_into is not None and not tp:
             out_tok, dst, dst_idx = argmax_into
-            if self.amax is None:
-                raise ValueError("argmax LM head needs vocab % 128 == 0 and <= 128 logit rows")
+            if self.amax is None or R > self.amax_rows:
+                raise ValueError("argmax LM head needs vocab % 128 == 0 and <= 256 logit rows")
             succ, beta = bigram if bigram is not None else (None, 0.0)
             _chk(lib.psd_gemm_argmax(self.xf.data_ptr(), H, R, H, m.lm_head.data_ptr(), H, s.vocab,
                                      v["tokens"].data_ptr(), v["logit_rows"].data_ptr(),

@@ -68,6 +68,7 @@ SIGNATURES: dict[str, tuple] = {
     "psd_verify_greedy_fold": (_i, [_p, _i, _i, _p, _p, _i, _i, _p, _p, _p, _p]),
     "psd_commit": (_i, [_p, _p, _i, _p, _i, _p, _p, _i, _p, _i, _p]),
     "psd_index_copy_i32": (_i, [_p, _p, _p, _p, _i, _p]),
+    "psd_verify_greedy_tokens": (_i, [_p, _p, _p, _i, _i, _p, _p, _p, _p]),
     "psd_copy_async": (_i, [_p, _p, _sz, _p]),
     "psd_stage_draft": (_i, [_p, _i64, _p, _p, _i, _p, _i, _i, _i, _i, _p, _p, _p, _i, _i, _i]),
     "psd_stage_verify": (_i, [_p, _p, _p, _i, _p, _i, _i, _i, _i, _p, _p, _p, _i, _i, _i]),

@@ -165,7 +165,8 @@ def test_gemm_trace_timeline(cuda_device):
 
 
 @pytest.mark.parametrize("M,N,K", [(32, 128256, 2048), (1, 1024, 256), (8, 151936, 896),
-                                   (64, 128256, 2048), (100, 2048, 512)])
+                                   (64, 128256, 2048), (100, 2048, 512), (192, 128256, 4096),
+                                   (256, 4096, 1024)])
 @pytest.mark.parametrize("bias", [False, True])
 def test_lm_head_argmax_epilogue(cuda_device, M, N, K, bias):
     """K6: argmax (+ the synthetic-language bias) in the stream-K LM head's
@@ -259,3 +260,57 @@ def test_split_k_partials_batch_invariant_any_m(cuda_device, N, K):
         assert s == s0, (M, s, s0)
         assert torch.equal(p, p0), M
     _close(p0.sum(0), _ref(x[:32], w), K)
+
+
+@pytest.mark.parametrize("B,K", [(32, 5), (7, 8), (40, 1), (3, 0)])
+@pytest.mark.parametrize("forced", [False, True])
+def test_verify_greedy_from_argmax_epilogue(cuda_device, B, K, forced):
+    """Greedy K1 fused into the target LM head (the verify path at <= 256 rows):
+    psd_gemm_argmax + psd_argmax_fold + psd_verify_greedy_tokens give the same
+    accepted lengths and output tokens as K1 (psd_verify_greedy) on the stored,
+    biased fp32 logits -- drafts agreeing with the target for a random prefix."""
+    dev = cuda_device
+    N, H = 32000, 1024
+    R = B * (K + 1)
+    g = torch.Generator(device=dev).manual_seed(B * 31 + K + forced)
+    x = torch.randn(R, H, device=dev, generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, H, device=dev, generator=g) * 0.05).to(torch.bfloat16)
+    lib = native.load()
+    st = torch.cuda.current_stream().cuda_stream
+    ws = torch.zeros(128 << 20, dtype=torch.uint8, device=dev)
+    tokens = torch.randint(0, N, (R,), device=dev, dtype=torch.int32, generator=g)
+    succ = torch.randint(0, N, (N,), device=dev, dtype=torch.int32, generator=g)
+    beta = 7.0
+    logits = torch.empty(R, N, device=dev)
+    assert lib.psd_gemm_bf16(x.data_ptr(), H, R, H, w.data_ptr(), H, N, logits.data_ptr(), N,
+                             native.EPI_F32, None, 0, 0, ws.data_ptr(), ws.numel(), st) == 0
+    assert lib.psd_bigram_bias(logits.data_ptr(), N, tokens.data_ptr(), R, succ.data_ptr(), N,
+                               beta, st) == 0
+    torch.cuda.synchronize()
+    am = logits.argmax(dim=1).view(B, K + 1)
+    # drafts: the target's choice for a random prefix, then a miss
+    ids = torch.randint(0, N, (B, max(K, 1)), device=dev, dtype=torch.int32, generator=g)[:, :K]
+    for b in range(B):
+        keep = int(torch.randint(0, K + 1, (1,), generator=torch.Generator().manual_seed(b)))
+        ids[b, :keep] = am[b, :keep].to(torch.int32)
+    ids = ids.contiguous()
+    ln = torch.randint(0, K + 1, (B,), device=dev, dtype=torch.int32, generator=g)
+    fl = torch.randint(0, K + 1, (B,), device=dev, dtype=torch.int32, generator=g) if forced else None
+    acc_ref = torch.empty(B, dtype=torch.int32, device=dev)
+    out_ref = torch.empty(B, K + 1, dtype=torch.int32, device=dev)
+    ops.verify_greedy(logits.view(B, K + 1, N), ids, ln, acc_ref, out_ref, forced_len=fl)
+    part = torch.empty(lib.psd_argmax_partials_bytes(R, N), dtype=torch.uint8, device=dev)
+    tok = torch.empty(R, dtype=torch.int32, device=dev)
+    assert lib.psd_gemm_argmax(x.data_ptr(), H, R, H, w.data_ptr(), H, N, tokens.data_ptr(),
+                               None, succ.data_ptr(), beta, part.data_ptr(), ws.data_ptr(),
+                               ws.numel(), st) == 0
+    assert lib.psd_argmax_fold(part.data_ptr(), R, N, tok.data_ptr(), None, None, st) == 0
+    acc = torch.full((B,), -9, dtype=torch.int32, device=dev)
+    out = torch.full((B, K + 1), -9, dtype=torch.int32, device=dev)
+    assert lib.psd_verify_greedy_tokens(tok.data_ptr(), ids.data_ptr(), ln.data_ptr(), B, K,
+                                        fl.data_ptr() if fl is not None else None,
+                                        acc.data_ptr(), out.data_ptr(), st) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(tok.view(B, K + 1), am.to(torch.int32))
+    assert torch.equal(acc, acc_ref)
+    assert torch.equal(out, out_ref)
