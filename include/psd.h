@@ -186,7 +186,7 @@ int psd_gemm_partials(const void* X, int ldx, int M, int K, const void* W, int l
  * successor[tokens[rows ? rows[m] : m]] when successor and beta != 0 -- into
  * `partials` (psd_argmax_partials_bytes); psd_argmax_fold reduces the tiles
  * (ties -> lowest index, K1's canonical argmax) into out_tokens[m] and/or
- * dst[dst_idx[m]] (skipped when negative).  M <= 256, N % 128 == 0; the
+ * dst[dst_idx[m]] (skipped when negative).  M <= 512, N % 128 == 0; the
  * workspace is psd_gemm_bf16's stream-K workspace. */
 size_t psd_argmax_partials_bytes(int M, int N);
 int psd_gemm_argmax(const void* X, int ldx, int M, int K, const void* W, int ldw, int N,

@@ -598,11 +598,11 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     const int q = warp & 3;
     const int row = 32 * q + lane;  // tile row (weight row) of this thread
     pdl_wait();  // residual / partial workspace belong to the predecessor's epoch
-    __shared__ int s_bcol[EPI == PSD_EPI_ARGMAX ? 256 : 1];
+    __shared__ int s_bcol[EPI == PSD_EPI_ARGMAX ? 512 : 1];
     __shared__ float s_amv[EPI == PSD_EPI_ARGMAX ? 16 * 136 : 1];
     if constexpr (EPI == PSD_EPI_ARGMAX) {
       // biased column of every token (three dependent loads, off the MMAs' path)
-      for (int m = threadIdx.x - 64; m < 256; m += 128) {
+      for (int m = threadIdx.x - 64; m < 512; m += 128) {
         int col = -1;
         if (m < g.M && g.am_succ && g.am_beta != 0.f) {
           const int t = g.am_tok[g.am_rows ? g.am_rows[m] : m];
@@ -1438,14 +1438,14 @@ int psd_gemm_argmax(const void* X, int ldx, int M, int K, const void* W, int ldw
                     const int32_t* tokens, const int32_t* rows, const int32_t* successor,
                     float beta, void* partials, void* workspace, size_t workspace_bytes,
                     void* stream) {
-  if (!X || !W || !partials || M <= 0 || M > 256 || N <= 0 || K <= 0 || (K % 8) || (N % BM))
+  if (!X || !W || !partials || M <= 0 || M > 512 || N <= 0 || K <= 0 || (K % 8) || (N % BM))
     return (int)cudaErrorInvalidValue;
   if (successor && beta != 0.f && !tokens) return (int)cudaErrorInvalidValue;
   if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(W)) & 15)
     return (int)cudaErrorMisalignedAddress;
   if ((ldx % 8) || (ldw % 8)) return (int)cudaErrorMisalignedAddress;
   const SKPlan p = sk_plan(M, N, K);
-  if (p.nt != 1 || p.MT != 1) return (int)cudaErrorInvalidValue;
+  if (p.MT != 1) return (int)cudaErrorInvalidValue;
   if (!workspace || workspace_bytes < p.part_bytes + p.ticket_bytes || p.tiles > kMaxTiles)
     return (int)cudaErrorInvalidValue;
   CUtensorMap mw, mx;
@@ -1465,6 +1465,7 @@ int psd_gemm_argmax(const void* X, int ldx, int M, int K, const void* W, int ldw
   g.tma_y = 0;
   g.am_tok = tokens; g.am_rows = rows; g.am_succ = successor; g.am_beta = beta;
   cudaStream_t st = (cudaStream_t)stream;
+  if (p.nt == 2) return launch_sk_nt2<PSD_EPI_ARGMAX>(p.bn, mw, mx, g, st);
   switch (p.bn) {
     case 32: return launch_sk_bn<32, PSD_EPI_ARGMAX, false>(mw, mx, g, st);
     case 64: return launch_sk_bn<64, PSD_EPI_ARGMAX, false>(mw, mx, g, st);

@@ -343,10 +343,10 @@ class Forward:
         self.act = torch.empty(T, s.ffn_padded, dtype=bf, device=dev)
         self.xf = torch.empty(max_logit_rows, s.hidden, dtype=bf, device=dev)
         self.prev = torch.empty(max_logit_rows, dtype=torch.int32, device=dev)
-        # K6 argmax partials for up to 256 logit rows (the draft's LM head, and
+        # K6 argmax partials for up to 512 logit rows (the draft's LM head, and
         # the target's when its greedy verification folds argmax tokens);
         # allocated here: never inside a graph capture
-        self.amax_rows = min(max_logit_rows, 256) if s.vocab % 128 == 0 else 0
+        self.amax_rows = min(max_logit_rows, 512) if s.vocab % 128 == 0 else 0
         self.amax = (torch.empty(native.load().psd_argmax_partials_bytes(self.amax_rows,
                                                                          s.vocab),
                                  dtype=torch.uint8, device=dev) if self.amax_rows else None)
@@ -596,7 +596,7 @@ class Forward:
         if argmax_into is not None and not tp:
             out_tok, dst, dst_idx = argmax_into
             if self.amax is None or R > self.amax_rows:
-                raise ValueError("argmax LM head needs vocab % 128 == 0 and <= 256 logit rows")
+                raise ValueError("argmax LM head needs vocab % 128 == 0 and <= 512 logit rows")
             succ, beta = bigram if bigram is not None else (None, 0.0)
             _chk(lib.psd_gemm_argmax(self.xf.data_ptr(), H, R, H, m.lm_head.data_ptr(), H, s.vocab,
                                      v["tokens"].data_ptr(), v["logit_rows"].data_ptr(),

@@ -166,7 +166,7 @@ def test_gemm_trace_timeline(cuda_device):
 
 @pytest.mark.parametrize("M,N,K", [(32, 128256, 2048), (1, 1024, 256), (8, 151936, 896),
                                    (64, 128256, 2048), (100, 2048, 512), (192, 128256, 4096),
-                                   (256, 4096, 1024)])
+                                   (256, 4096, 1024), (384, 128256, 4096), (512, 4096, 1024)])
 @pytest.mark.parametrize("bias", [False, True])
 def test_lm_head_argmax_epilogue(cuda_device, M, N, K, bias):
     """K6: argmax (+ the synthetic-language bias) in the stream-K LM head's
@@ -262,7 +262,7 @@ def test_split_k_partials_batch_invariant_any_m(cuda_device, N, K):
     _close(p0.sum(0), _ref(x[:32], w), K)
 
 
-@pytest.mark.parametrize("B,K", [(32, 5), (7, 8), (40, 1), (3, 0)])
+@pytest.mark.parametrize("B,K", [(32, 5), (7, 8), (40, 1), (3, 0), (64, 5)])
 @pytest.mark.parametrize("forced", [False, True])
 def test_verify_greedy_from_argmax_epilogue(cuda_device, B, K, forced):
     """Greedy K1 fused into the target LM head (the verify path at <= 256 rows):
