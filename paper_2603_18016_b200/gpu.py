@@ -786,7 +786,8 @@ class GpuBackend:
         # row to (max, argmax) per vocabulary tile, a fold gives the argmax
         # token per row, one warp per request decides -- no M x V logits are
         # stored or re-read (same decisions as K1 on the stored logits)
-        k1_epi = (self.mode == "greedy" and self.k1_epi and fwd.comm is None
+        tp = self.target.tp
+        k1_epi = (self.mode == "greedy" and self.k1_epi and (tp is None or tp[1] <= 1)
                   and self.capture_verify is None and M <= fwd.amax_rows)
         if k1_epi:
             fwd.run(M, nb, K1, M, None, self.tshape.vocab,
