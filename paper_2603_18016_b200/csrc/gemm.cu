@@ -1534,8 +1534,17 @@ int psd_gemm_bf16(const void* X, int ldx, int M, int K, const void* W, int ldw, 
     // gate/up at M = 32: 14.3 vs 19.8 us, profiles/r01b_kbench_gemm_splits.txt).
     // Decided on the weight tiles of one token tile so that every M takes the
     // same path (batch-invariant summation order)
+    // Short-K GEMMs (K <= 1024: a few k-blocks per tile) take it from half a
+    // wave: their stream-K fix-ups would cost more than the idle SMs (Qwen2.5-
+    // 0.5B gate/up, 76 tiles x 14 k-blocks)
     const int tiles = N / BM;
-    if (tiles <= num_sms_raw() && 4 * tiles >= 3 * num_sms_raw()) splits_hint = 1;
+    static const int short_k = [] {
+      const char* e = getenv("PSD_GEMM_SHORTK_WAVE");
+      return e ? atoi(e) : 1;
+    }();
+    if (tiles <= num_sms_raw() &&
+        (4 * tiles >= 3 * num_sms_raw() || (short_k && K <= 1024 && 2 * tiles >= num_sms_raw())))
+      splits_hint = 1;
   }
   if (splits_hint == 0) {
     // stream-K persistent path (default)

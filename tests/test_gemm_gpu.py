@@ -211,7 +211,8 @@ def test_lm_head_argmax_epilogue(cuda_device, M, N, K, bias):
 
 @pytest.mark.parametrize("N,K,epi", [(4096, 4096, native.EPI_F32), (2048, 8192, native.EPI_F32),
                                      (8192, 4096, native.EPI_SILU),
-                                     (128256, 4096, native.EPI_F32)])
+                                     (128256, 4096, native.EPI_F32),
+                                     (9728, 896, native.EPI_SILU)])
 def test_stream_k_batch_invariant_any_m(cuda_device, N, K, epi):
     """Stream-K: a token's output bits do not depend on how many tokens share
     the launch -- M = 24 .. 1100 (one, two and up to five token tiles per
