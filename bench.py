@@ -700,7 +700,10 @@ def run_ours(args) -> None:
     roof, vk = kernel_rooflines(be, hbm_peak, bf16_peak)
     vsweep = verify_sweep_summary(hbm_peak) if rank == 0 and not args.no_sweep else None
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    # the CPU sample is quoted on the 8B / 1B shapes: cfg2 / cfg3 runs only
+    # (the 70B layouts skip it)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.layout not in ("tp",
+                                                                                   "tp-draft"):
         try:
             v, secs, toks, cores = cpu_sample()
             cpu = {"value": round(v, 4), "unit": "tok/s", "cores": cores, "kind": "port",
