@@ -1709,7 +1709,8 @@ static int rope_launch(const QkvSrc& src, int M, int Hq, int Hkv, int D,
 size_t psd_attention_workspace_bytes(int num_seqs, int Hkv, int max_q_len, int Hq, int D,
                                      int max_kv_len) {
   const int G = Hq / Hkv;
-  const int tpc = ATT_MAXR / std::max(1, G);
+  // the finer token chunking attention_launch may pick (two key groups per CTA)
+  const int tpc = std::max(1, std::min(ATT_MAXR / std::max(1, G), 32 / std::max(1, G)));
   const int chunks = (max_q_len + tpc - 1) / tpc;
   const int S = att_splits(num_seqs * Hkv * chunks, max_kv_len);
   const size_t units = (size_t)num_seqs * Hkv * chunks;
@@ -1777,7 +1778,15 @@ static int attention_launch(const void* q, const void* k_cache, const void* v_ca
   const int G = Hq / Hkv;
   if (G > ATT_MAXR || max_blocks > ATT_MAX_BLOCKS) return (int)cudaErrorInvalidValue;
   if (block_size <= 0 || (block_size & (block_size - 1))) return (int)cudaErrorInvalidValue;
-  const int tpc = ATT_MAXR / G;
+  int tpc = ATT_MAXR / G;
+  // keep two key groups per CTA: when a sequence's rows would fill all four
+  // warps as row groups (e.g. Qwen2.5-7B verify: 5 tokens x 7 heads), split
+  // its tokens over two CTAs instead (PSD_ATT_KG2=0: the single-chunk split)
+  static const int kg2 = [] {
+    const char* e = getenv("PSD_ATT_KG2");
+    return e ? atoi(e) : 1;
+  }();
+  if (kg2 && (std::min(max_q_len, tpc) * G + 15) / 16 > 2) tpc = std::max(1, 32 / G);
   const int chunks = (max_q_len + tpc - 1) / tpc;
   // rows per CTA -> row groups; the other warps become key groups
   const int rmax = std::min(ATT_MAXR, std::min(max_q_len, tpc) * G);
