@@ -1786,7 +1786,12 @@ static int attention_launch(const void* q, const void* k_cache, const void* v_ca
     const char* e = getenv("PSD_ATT_KG2");
     return e ? atoi(e) : 1;
   }();
-  if (kg2 && (std::min(max_q_len, tpc) * G + 15) / 16 > 2) tpc = std::max(1, 32 / G);
+  // (not with fused RoPE, which needs a sequence's tokens in one CTA, nor
+  // with split-KV, whose merge keeps the one-chunk geometry)
+  if (kg2 && !rope && att_splits(num_seqs * Hkv * ((max_q_len + tpc - 1) / tpc),
+                                 max_kv_len) == 1 &&
+      (std::min(max_q_len, tpc) * G + 15) / 16 > 2)
+    tpc = std::max(1, 32 / G);
   const int chunks = (max_q_len + tpc - 1) / tpc;
   // rows per CTA -> row groups; the other warps become key groups
   const int rmax = std::min(ATT_MAXR, std::min(max_q_len, tpc) * G);
