@@ -423,6 +423,8 @@ def main():
     if want("lmargmax"):
         lm_argmax_case("1B", 32, 128256, 2048)
         lm_argmax_case("1B M64", 64, 128256, 2048)
+        lm_argmax_case("8B verify M192", 192, 128256, 4096)
+        lm_argmax_case("8B SD(2m) M384", 384, 128256, 4096)
     if want("k1"):
         verify_case("greedy cfg2", 32, 5, 128256, False)
         verify_case("sample cfg2", 32, 5, 128256, True)
